@@ -1,0 +1,192 @@
+/*
+ * pmf.h -- C ABI of the B200-native spectral point-mass filter (PMF) hot path.
+ *
+ * Method: Matousek, Dunik, Brandner, "Efficient Spectral Differentiation in
+ * Grid-Based Continuous State Estimation" (FUSION 2024, arXiv 2412.07240).
+ * Citations "P:<n>" are lines of PAPER.md; readings "R<n>" are listed in
+ * DESIGN.md §3.
+ *
+ * Model (eq:dynam / eq:meas):  dx = A x dt + dw,  E[dw dw^T] = Q dt
+ * (Q is the FPE diffusion matrix of eq:fokker P:55, R1), z_k = h(x_k) + v_k.
+ *
+ * A filter's density is a point-mass density (PMD, eq:PDF_pm P:116) on an
+ * N_0 x ... x N_{nx-1} equidistant grid that moves with the drift (eq:gridMov
+ * P:142). Point j = (j_0..j_{nx-1}) sits at the physical location
+ *        xi_j = c + B u_j,   u_j[m] = j_m - (N_m - 1)/2          (R10)
+ * with c the grid centre and B the (possibly sheared) nx x nx placement matrix.
+ *
+ * MEMORY LAYOUT (R-layout, P:114/P:346 MATLAB reshape): weights of one filter
+ * are N_0*...*N_{nx-1} values with axis 0 FASTEST; filters are stacked
+ * batch-major (filter index slowest). Real type per pmf_config.dtype (double
+ * or float). Matrices are row-major, nx x nx, packed (stride nx).
+ *
+ * OWNERSHIP: the caller owns every host array and device buffer it passes; they
+ * are read (or written) during the call only. The context owns its device
+ * buffers (weights, spectrum, per-filter state) and its work is enqueued on
+ * pmf_config.stream. Host outputs (pmf_moments, pmf_get_weights to host,
+ * pmf_get_grid) synchronise that stream; nothing else does.
+ *
+ * LAZINESS: pmf_predict and pmf_regrid validate their arguments and RECORD the
+ * operation; it is executed (fused with what follows) by the next call that
+ * needs the density: pmf_update, pmf_get_weights, pmf_device_weights,
+ * pmf_sync. Results are identical to eager execution.
+ *
+ * ERRORS: every int-returning call returns PMF_OK (0) or a negative PMF_E_*
+ * code; pmf_last_error() gives a message. A failed call leaves the context
+ * unchanged unless the code is PMF_E_CUDA (the context is then unusable).
+ * There is no CPU fallback: the library requires a CUDA device (sm_100a).
+ */
+#ifndef PMF_H
+#define PMF_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PMF_MAX_NX 4
+#define PMF_MAX_NZ 4
+
+/* return codes */
+#define PMF_OK               0
+#define PMF_E_ARG           -1  /* bad argument (null pointer, bad enum, nx/nz range, non-diagonal Q in AXIS_LITERAL mode) */
+#define PMF_E_ODD_N         -2  /* points per axis odd (the spectral interpolant needs even N)             */
+#define PMF_E_RADIX         -3  /* N not of the form 2^a 3^b with 4 <= N <= PMF max (see pmf_create)             */
+#define PMF_E_Q_NOT_PSD     -4  /* Q not symmetric positive semi-definite                                         */
+#define PMF_E_SINGULAR_GRID -5  /* grid matrix B not invertible                                                    */
+#define PMF_E_NO_SUPPORT    -6  /* normaliser zero/non-finite: measurement incompatible with grid support,       */
+                                /* or degenerate posterior covariance at regrid (R12)                            */
+#define PMF_E_DT            -7  /* dt <= 0, steps < 1, or Euler trace factor base 1 -/+ dt tr(A) <= 0 (R5)       */
+#define PMF_E_STATE         -8  /* call out of order (e.g. predict before a density was set)                     */
+#define PMF_E_CUDA          -9  /* CUDA runtime failure or no usable device                                        */
+#define PMF_E_NOMEM        -10  /* device allocation failed                                                        */
+
+/* enums */
+#define PMF_F64 0
+#define PMF_F32 1
+
+#define PMF_DIFF_FULL          0  /* R3: index-space diffusion D_n = B_n^-1 Q B_n^-T, cross terms kept (default) */
+#define PMF_DIFF_AXIS_LITERAL  1  /* Alg. 2-3 literally: per-axis L^(m) = N ||B_n[:,m]||, no cross    */
+
+#define PMF_TRACE_PHYSICAL (-1)   /* R5: s = (1 - dt tr A)^l   (eq:easyFPE P:92)                                   */
+#define PMF_TRACE_PRINTED    1    /* Alg. 4 as printed: s = (1 + dt tr A)^l; normalised output identical   */
+
+#define PMF_PATH_AUTO     0  /* resident per-filter kernel when it fits, else the pencil path                    */
+#define PMF_PATH_PENCIL   1  /* multi-pass per-axis pencil kernels (any nx <= 4)                                */
+#define PMF_PATH_RESIDENT 2  /* one CTA per filter, whole half-spectrum in shared memory (nx=2: N0=N1=128; nx=1) */
+
+#define PMF_LIK_LINEAR_GAUSS 0   /* z = H x + v, v ~ N(0, R), nz <= 4 (eq:meas P:36)                               */
+#define PMF_LIK_RANGE_GAUSS  1   /* z = ||x|| + v, v ~ N(0, sigma^2), nz = 1 (C3)                                   */
+
+typedef struct pmf_ctx pmf_ctx;
+
+typedef struct {
+    int   nx;          /* state dimension, 1..4                                                    */
+    int   n[4];        /* points per axis N_m (even, 2^a 3^b, 4 <= N_m <= 1024; n[m] for m>=nx ignored) */
+    int   batch;       /* number of independent filters sharing A, Q and the likelihood kind       */
+    int   dtype;       /* PMF_F64 or PMF_F32 (storage + transform precision; reductions are fp64)   */
+    int   diff_mode;   /* PMF_DIFF_FULL (default 0) or PMF_DIFF_AXIS_LITERAL                       */
+    int   trace_sign;  /* PMF_TRACE_PHYSICAL (0 is read as PHYSICAL) or PMF_TRACE_PRINTED          */
+    int   path;        /* PMF_PATH_AUTO / PENCIL / RESIDENT                                         */
+    int   device;      /* CUDA device ordinal the context lives on                                 */
+    void* stream;      /* cudaStream_t to enqueue on; NULL = the legacy default stream             */
+} pmf_config;
+
+typedef struct {
+    int    kind;       /* PMF_LIK_*                                                                 */
+    int    nz;         /* measurement dimension (LINEAR_GAUSS: 1..4; RANGE_GAUSS: 1)                */
+    double H[16];      /* LINEAR_GAUSS: nz x nx row-major, packed                                  */
+    double R[16];      /* LINEAR_GAUSS: nz x nz noise covariance, symmetric positive definite       */
+    double sigma;      /* RANGE_GAUSS: noise standard deviation > 0                                 */
+} pmf_likelihood;
+
+/* Create a context: validates sizes (PMF_E_ODD_N, PMF_E_RADIX), A (nx x nx) and
+ * Q (nx x nx, symmetric PSD -> else PMF_E_Q_NOT_PSD), allocates the device
+ * buffers on cfg->device. No density is set yet (PMF_E_STATE until
+ * pmf_set_gaussian / pmf_set_state). *out receives the handle. */
+int pmf_create(const pmf_config* cfg, const double* A, const double* Q, pmf_ctx** out);
+
+/* Release every device buffer (synchronises the stream). NULL is a no-op. */
+void pmf_destroy(pmf_ctx* ctx);
+
+/* Message of the last error on this context (or of the last failed
+ * pmf_create in this thread when ctx is NULL). Never NULL. */
+const char* pmf_last_error(const pmf_ctx* ctx);
+
+/* Initial density p(x_0) (P:48 footnote): for each filter b, the grid
+ * c = mean_b, B = diag(2 k_sigma sqrt(cov_b[m][m]) / N_m) (R10), weights
+ * N(xi; mean_b, cov_b) normalised so vol * sum w = 1 (vol = |det B|, R9).
+ * mean: host batch x nx; cov: host batch x nx x nx (SPD). */
+int pmf_set_gaussian(pmf_ctx* ctx, const double* mean, const double* cov, double k_sigma);
+
+/* Set an arbitrary state: grid (center: host batch x nx, B: host batch x nx x nx)
+ * and weights (batch x N_total in dtype, host or device per weights_on_device;
+ * a device pointer must be on cfg->device). The weights are normalised on
+ * entry (vol * sum w = 1). PMF_E_SINGULAR_GRID if some B is singular. */
+int pmf_set_state(pmf_ctx* ctx, const double* center, const double* B,
+                  const void* weights, int weights_on_device);
+
+/* Time update over one prediction interval tau = dt * steps with `steps` Euler
+ * substeps of length dt: Alg. 1-6 of §V.B --
+ * forward DFT per axis (1/N each, eq:fourtrsf P:221), multiply by
+ * s * prod_{n<steps} psi_n with psi_n the semi-implicit Euler factor of Alg. 3
+ * (R2-R4, R7) on the grid at the start of substep n, inverse DFT,
+ * normalise (Alg. 6; closed form, R9). The grid moves: c <- e^{A tau} c,
+ * B <- e^{A tau} B (eq:gridMov P:142-148). Lazy (see LAZINESS).
+ * PMF_E_DT if dt <= 0, steps < 1 or 1 -/+ dt tr(A) <= 0. */
+int pmf_predict(pmf_ctx* ctx, double dt, int steps);
+
+/* Measurement update (Bayes, eq:filt P:46): w_i <- w_i p(z - h(xi_i)) at the
+ * (moved) grid points (R13), normaliser C = vol sum w_i p(z|xi_i),
+ * w <- w / C; the moments of the posterior (R14) are computed on
+ * the device in the same pass. z: batch x nz doubles, host or device.
+ * Per-filter failure (C == 0 or non-finite) is reported by pmf_moments
+ * (PMF_E_NO_SUPPORT). */
+int pmf_update(pmf_ctx* ctx, const double* z, int z_on_device, const pmf_likelihood* lik);
+
+/* Copy the posterior moments of the last update to host arrays (any may be
+ * NULL): mean batch x nx, cov batch x nx x nx, log_norm batch (log of the
+ * P:49 normaliser). Synchronises. PMF_E_STATE before the first update,
+ * PMF_E_NO_SUPPORT if any filter's last update failed. */
+int pmf_moments(pmf_ctx* ctx, double* mean, double* cov, double* log_norm);
+
+/* Re-centre every filter's grid on its last posterior (R12; the paper is silent,
+ * north_star "re-centre the grid"): c' = mean, B' = diag(2 k_sigma sqrt(cov_mm)/N_m),
+ * multilinear interpolation of the old weights at the new points with zero
+ * ghost nodes, renormalised. Lazy. PMF_E_STATE before the first update. */
+int pmf_regrid(pmf_ctx* ctx, double k_sigma);
+
+/* One filter epoch = pmf_predict(dt, steps); pmf_update(z, lik); pmf_regrid(k_sigma)
+ * (the regrid stays pending and is fused into the next epoch's load). */
+int pmf_step(pmf_ctx* ctx, double dt, int steps, const double* z, int z_on_device,
+             const pmf_likelihood* lik, double k_sigma);
+
+/* Normalised density values (vol * sum = 1) of all filters on their current
+ * grids, batch x N_total in dtype; dst on host or on cfg->device. Flushes
+ * pending work. */
+int pmf_get_weights(pmf_ctx* ctx, void* dst, int dst_on_device);
+
+/* Current grids: center batch x nx, B batch x nx x nx (host; either may be NULL).
+ * Flushes pending work and synchronises. */
+int pmf_get_grid(pmf_ctx* ctx, double* center, double* B);
+
+/* Flush pending work and wait for the stream. */
+int pmf_sync(pmf_ctx* ctx);
+
+/* Number of kernels this context has launched so far. */
+int64_t pmf_launch_count(const pmf_ctx* ctx);
+
+/* Bytes of device memory owned by the context. */
+int64_t pmf_device_bytes(const pmf_ctx* ctx);
+
+/* Kernel path the context uses (PMF_PATH_PENCIL or PMF_PATH_RESIDENT). */
+int pmf_path(const pmf_ctx* ctx);
+
+/* Library version string. */
+const char* pmf_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PMF_H */

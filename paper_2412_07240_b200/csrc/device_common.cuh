@@ -1,0 +1,251 @@
+// device_common.cuh -- small device helpers: complex arithmetic, nx<=4 linear
+// algebra, per-filter epoch constants, deterministic block reductions.
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+#include "pmf_internal.h"
+
+namespace pmf {
+
+#define PMF_PI 3.14159265358979323846
+
+template <typename T> struct C2;
+template <> struct C2<double> { using type = double2; };
+template <> struct C2<float> { using type = float2; };
+
+template <typename V> __device__ __forceinline__ V cadd(V a, V b) { return {a.x + b.x, a.y + b.y}; }
+template <typename V> __device__ __forceinline__ V csub(V a, V b) { return {a.x - b.x, a.y - b.y}; }
+template <typename V> __device__ __forceinline__ V cmul(V a, V b) {
+    return {fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x)};
+}
+// a * conj(b)
+template <typename V> __device__ __forceinline__ V cmulc(V a, V b) {
+    return {fma(a.x, b.x, a.y * b.y), fma(a.y, b.x, -a.x * b.y)};
+}
+// multiply by -i (fwd) / +i (inv)
+template <bool INV, typename V> __device__ __forceinline__ V mul_mi(V a) {
+    if (INV) return {-a.y, a.x};
+    return {a.y, -a.x};
+}
+
+// ---------------------------------------------------------------- small linear algebra (stride 4)
+__device__ __forceinline__ void mat_mul4(int nx, const double* A, const double* B, double* C) {
+    for (int i = 0; i < nx; ++i)
+        for (int j = 0; j < nx; ++j) {
+            double s = 0.0;
+            for (int k = 0; k < nx; ++k) s = fma(A[i * 4 + k], B[k * 4 + j], s);
+            C[i * 4 + j] = s;
+        }
+}
+
+// Gauss-Jordan inverse with partial pivoting; returns determinant (0 if singular).
+__device__ inline double mat_inv4(int nx, const double* A, double* Ai) {
+    double M[16], I[16];
+    for (int i = 0; i < 16; ++i) { M[i] = A[i]; I[i] = 0.0; }
+    for (int i = 0; i < nx; ++i) I[i * 4 + i] = 1.0;
+    double det = 1.0;
+    for (int col = 0; col < nx; ++col) {
+        int piv = col;
+        double best = fabs(M[col * 4 + col]);
+        for (int r = col + 1; r < nx; ++r)
+            if (fabs(M[r * 4 + col]) > best) { best = fabs(M[r * 4 + col]); piv = r; }
+        if (best == 0.0) return 0.0;
+        if (piv != col) {
+            for (int k = 0; k < 4; ++k) {
+                double t = M[col * 4 + k]; M[col * 4 + k] = M[piv * 4 + k]; M[piv * 4 + k] = t;
+                t = I[col * 4 + k]; I[col * 4 + k] = I[piv * 4 + k]; I[piv * 4 + k] = t;
+            }
+            det = -det;
+        }
+        double p = M[col * 4 + col];
+        det *= p;
+        double ip = 1.0 / p;
+        for (int k = 0; k < 4; ++k) { M[col * 4 + k] *= ip; I[col * 4 + k] *= ip; }
+        for (int r = 0; r < nx; ++r) {
+            if (r == col) continue;
+            double f = M[r * 4 + col];
+            if (f == 0.0) continue;
+            for (int k = 0; k < 4; ++k) {
+                M[r * 4 + k] = fma(-f, M[col * 4 + k], M[r * 4 + k]);
+                I[r * 4 + k] = fma(-f, I[col * 4 + k], I[r * 4 + k]);
+            }
+        }
+    }
+    for (int i = 0; i < 16; ++i) Ai[i] = I[i];
+    return det;
+}
+
+__device__ __forceinline__ int pair_index(int nx, int a, int b) {
+    // packed order: diagonal 0..nx-1, then (0,1),(0,2),(0,3),(1,2),(1,3),(2,3) restricted to nx
+    int idx = nx;
+    for (int i = 0; i < nx; ++i)
+        for (int j = i + 1; j < nx; ++j) {
+            if (i == a && j == b) return idx;
+            ++idx;
+        }
+    return -1;
+}
+
+// Per-filter Euler-factor coefficients for the l substeps of one prediction
+// interval (Alg. 3 P:333-336 with R3/R4): for substep n the factor is
+//   f_n(kappa) = 1 + sum_a cf[a] kappa_a^2 + sum_{a<b} cf[pair(a,b)] kx_a kx_b
+// with cf_diag = dt/2 D_n,aa and cf_pair = dt D_n,ab (the 2 of the symmetric
+// cross term folded in), D_n = B^-1 E_n B^-T (FULL) or diag(Q_mm/||B_n[:,m]||^2)
+// (AXIS_LITERAL). Writes 10 doubles per substep (packed as pair_index).
+__device__ inline void epoch_coefs(const double* B, const ModelParams& mp,
+                                   const SubstepEntry* sub, double* out) {
+    const int nx = mp.nx;
+    double Bi[16];
+    mat_inv4(nx, B, Bi);
+    for (int s = 0; s < mp.l; ++s) {
+        double D[16];
+        if (mp.diff_mode == 0) {
+            double T1[16], BiT[16];
+            for (int i = 0; i < 4; ++i)
+                for (int j = 0; j < 4; ++j) BiT[i * 4 + j] = Bi[j * 4 + i];
+            mat_mul4(nx, Bi, sub[s].E, T1);
+            mat_mul4(nx, T1, BiT, D);
+        } else {
+            double Bn[16];
+            mat_mul4(nx, sub[s].P, B, Bn);
+            for (int i = 0; i < 16; ++i) D[i] = 0.0;
+            for (int m = 0; m < nx; ++m) {
+                double len2 = 0.0;
+                for (int r = 0; r < nx; ++r) len2 = fma(Bn[r * 4 + m], Bn[r * 4 + m], len2);
+                D[m * 4 + m] = mp.Q[m * 4 + m] / len2;
+            }
+        }
+        double* o = out + 10 * s;
+        for (int k = 0; k < 10; ++k) o[k] = 0.0;
+        int idx = nx;
+        for (int a = 0; a < nx; ++a) {
+            o[a] = 0.5 * mp.dt * D[a * 4 + a];
+            for (int b = a + 1; b < nx; ++b) o[idx++] = mp.dt * 0.5 * (D[a * 4 + b] + D[b * 4 + a]);
+        }
+    }
+}
+
+__device__ __forceinline__ double det4(int nx, const double* B) {
+    double Bi[16];
+    return mat_inv4(nx, B, Bi);
+}
+
+// signed wavenumber of transform index k (N even): [0..N/2-1] -> k, [N/2..N-1] -> k - N
+__device__ __forceinline__ int signed_k(int k, int N) { return k < N / 2 ? k : k - N; }
+
+// ---------------------------------------------------------------- likelihood at a physical point
+__device__ __forceinline__ double log_lik(const LikParams& lp, const double* x, const double* z) {
+    if (lp.kind == 1) {
+        double r2 = 0.0;
+        for (int a = 0; a < lp.nx; ++a) r2 = fma(x[a], x[a], r2);
+        double d = (z[0] - sqrt(r2)) * lp.inv_sigma;
+        return fma(-0.5 * d, d, lp.lognorm);
+    }
+    double r[4];
+    for (int i = 0; i < lp.nz; ++i) {
+        double hx = 0.0;
+        for (int a = 0; a < lp.nx; ++a) hx = fma(lp.H[i * 4 + a], x[a], hx);
+        r[i] = z[i] - hx;
+    }
+    double e = 0.0;
+    for (int i = 0; i < lp.nz; ++i) {
+        double t = 0.0;
+        for (int j = 0; j < lp.nz; ++j) t = fma(lp.Rinv[i * 4 + j], r[j], t);
+        e = fma(r[i], t, e);
+    }
+    return fma(-0.5, e, lp.lognorm);
+}
+
+// ---------------------------------------------------------------- moment accumulators
+// acc[0] = sum w, acc[1..nx] = sum w u_a, then sum w u_a u_b (a<=b) packed row-wise.
+__device__ __forceinline__ void acc_moments(int nx, double w, const double* u, double* acc) {
+    acc[0] += w;
+    int k = 1 + nx;
+    for (int a = 0; a < nx; ++a) {
+        double wu = w * u[a];
+        acc[1 + a] += wu;
+        for (int b = a; b < nx; ++b) { acc[k] = fma(wu, u[b], acc[k]); ++k; }
+    }
+}
+
+// Deterministic block sum of NV doubles per thread; result valid in thread 0.
+// scratch: >= 32 * NV doubles of shared memory.
+template <int NV>
+__device__ inline void block_sum(double* v, double* scratch) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+        double x = v[i];
+        for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
+        v[i] = x;
+    }
+    __syncthreads();
+    if (lane == 0)
+        for (int i = 0; i < NV; ++i) scratch[wid * NV + i] = v[i];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < NV; ++i) {
+            double s = 0.0;
+            for (int w = 0; w < nw; ++w) s += scratch[w * NV + i];
+            v[i] = s;
+        }
+    }
+    __syncthreads();
+}
+
+// Finalise moments from accumulators (index coordinates u) into physical mean/cov:
+// ubar = S1/S0, S = S2/S0 - ubar ubar^T, mean = c + B ubar, cov = B S B^T (R14).
+__device__ inline void finish_moments(int nx, const double* acc, const double* c, const double* B,
+                                      double* mean, double* cov) {
+    double S0 = acc[0];
+    double ub[4] = {0, 0, 0, 0}, Su[16];
+    for (int a = 0; a < nx; ++a) ub[a] = acc[1 + a] / S0;
+    int k = 1 + nx;
+    for (int a = 0; a < nx; ++a)
+        for (int b = a; b < nx; ++b) {
+            double v = acc[k++] / S0 - ub[a] * ub[b];
+            Su[a * 4 + b] = v;
+            Su[b * 4 + a] = v;
+        }
+    for (int a = 0; a < nx; ++a) {
+        double m = c[a];
+        for (int b = 0; b < nx; ++b) m = fma(B[a * 4 + b], ub[b], m);
+        mean[a] = m;
+    }
+    double T[16];
+    for (int a = 0; a < nx; ++a)
+        for (int b = 0; b < nx; ++b) {
+            double s = 0.0;
+            for (int k2 = 0; k2 < nx; ++k2) s = fma(B[a * 4 + k2], Su[k2 * 4 + b], s);
+            T[a * 4 + b] = s;
+        }
+    for (int a = 0; a < nx; ++a)
+        for (int b = 0; b < nx; ++b) {
+            double s = 0.0;
+            for (int k2 = 0; k2 < nx; ++k2) s = fma(T[a * 4 + k2], B[b * 4 + k2], s);
+            cov[a * 4 + b] = s;
+        }
+    for (int a = 0; a < nx; ++a)
+        for (int b = a + 1; b < nx; ++b) {
+            double v = 0.5 * (cov[a * 4 + b] + cov[b * 4 + a]);
+            cov[a * 4 + b] = v;
+            cov[b * 4 + a] = v;
+        }
+}
+
+// New grid of the re-centring policy (R12): c' = mean, B' = diag(2 ks sqrt(cov_mm)/N_m).
+// Returns false when some variance is non-finite or <= 0.
+__device__ inline bool regrid_target(int nx, const int* n, const FilterState& st, double ks,
+                                     double* cn, double* Bn) {
+    for (int i = 0; i < 16; ++i) Bn[i] = 0.0;
+    bool ok = true;
+    for (int a = 0; a < nx; ++a) {
+        double v = st.cov[a * 4 + a];
+        if (!(v > 0.0) || !isfinite(v)) ok = false;
+        cn[a] = st.mean[a];
+        Bn[a * 4 + a] = 2.0 * ks * sqrt(v) / n[a];
+    }
+    return ok;
+}
+
+}  // namespace pmf

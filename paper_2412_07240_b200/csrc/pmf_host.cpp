@@ -1,0 +1,704 @@
+// pmf_host.cpp -- C ABI runtime of the spectral PMF (include/pmf.h).
+//
+// Owns the device buffers of a context, validates arguments, computes the
+// per-prediction model constants on the host in fp64 (matrix exponentials of
+// the drift, eq:gridMov P:142-148; trace factor, Alg. 4), and drives the
+// kernels. predict/regrid are recorded and executed lazily (fused with the
+// update that follows), see include/pmf.h "LAZINESS".
+#include "../../include/pmf.h"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "pmf_internal.h"
+
+using namespace pmf;
+
+namespace {
+
+thread_local std::string g_create_error = "";
+
+struct Pending {
+    bool predict = false;
+    double dt = 0.0;
+    int steps = 0;
+    bool regrid = false;
+    double k_sigma = 0.0;
+};
+
+}  // namespace
+
+struct pmf_ctx {
+    pmf_config cfg{};
+    Dims d{};
+    int dtype = 0;
+    int path = PMF_PATH_PENCIL;
+    size_t esize = 8;
+    double A[16]{}, Q[16]{};
+    cudaStream_t stream = nullptr;
+    // device buffers
+    void* W = nullptr;
+    void* W2 = nullptr;
+    void* S = nullptr;
+    FilterState* st = nullptr;
+    double* partials = nullptr;
+    size_t partials_bytes = 0;
+    double* coef = nullptr;
+    size_t coef_bytes = 0;
+    SubstepEntry* sub = nullptr;
+    size_t sub_bytes = 0;
+    double* z = nullptr;
+    double* gauss = nullptr;
+    void* tw[4] = {nullptr, nullptr, nullptr, nullptr};
+    int64_t bytes = 0;
+    // host-side model cache (per (dt, steps))
+    double cached_dt = -1.0;
+    int cached_steps = -1;
+    ModelParams mp{};
+    // state machine
+    bool have_density = false;
+    bool have_update = false;
+    Pending pend;
+    int64_t launches = 0;
+    std::string err;
+};
+
+// ============================================================================ helpers
+static int fail(pmf_ctx* c, int code, const std::string& msg) {
+    if (c) c->err = msg;
+    else g_create_error = msg;
+    return code;
+}
+
+static int cuda_fail(pmf_ctx* c, cudaError_t e, const char* where) {
+    return fail(c, PMF_E_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define CK(ctx, x, where)                                      \
+    do {                                                       \
+        cudaError_t e_ = (x);                                  \
+        if (e_ != cudaSuccess) return cuda_fail(ctx, e_, where); \
+    } while (0)
+
+static void mat_mul(int n, const double* A, const double* B, double* C) {  // stride 4
+    double T[16] = {0};
+    for (int i = 0; i < n; ++i)
+        for (int j = 0; j < n; ++j) {
+            double s = 0.0;
+            for (int k = 0; k < n; ++k) s += A[i * 4 + k] * B[k * 4 + j];
+            T[i * 4 + j] = s;
+        }
+    std::memcpy(C, T, sizeof(T));
+}
+
+// e^{M}: scaling and squaring with a degree-20 Taylor polynomial (||M/2^k|| <= 1/2
+// makes the truncation error < 1e-25 relative).
+static void expm4(int n, const double* M, double* out) {
+    double norm = 0.0;
+    for (int i = 0; i < n; ++i) {
+        double r = 0.0;
+        for (int j = 0; j < n; ++j) r += std::fabs(M[i * 4 + j]);
+        norm = std::max(norm, r);
+    }
+    int k = 0;
+    while (norm > 0.5) { norm *= 0.5; ++k; }
+    double X[16] = {0}, S[16] = {0}, T[16] = {0};
+    const double sc = std::ldexp(1.0, -k);
+    for (int i = 0; i < n; ++i)
+        for (int j = 0; j < n; ++j) X[i * 4 + j] = M[i * 4 + j] * sc;
+    for (int i = 0; i < n; ++i) { S[i * 4 + i] = 1.0; T[i * 4 + i] = 1.0; }
+    for (int t = 1; t <= 20; ++t) {
+        mat_mul(n, T, X, T);
+        for (int i = 0; i < 16; ++i) T[i] /= t;
+        for (int i = 0; i < 16; ++i) S[i] += T[i];
+    }
+    for (int s = 0; s < k; ++s) mat_mul(n, S, S, S);
+    std::memcpy(out, S, sizeof(S));
+}
+
+// eigenvalues of a symmetric n x n (stride 4) matrix by cyclic Jacobi
+static void sym_eig(int n, const double* Ain, double* ev) {
+    double A[16];
+    std::memcpy(A, Ain, sizeof(A));
+    for (int sweep = 0; sweep < 60; ++sweep) {
+        double off = 0.0;
+        for (int p = 0; p < n; ++p)
+            for (int q = p + 1; q < n; ++q) off += A[p * 4 + q] * A[p * 4 + q];
+        if (off < 1e-300) break;
+        for (int p = 0; p < n; ++p)
+            for (int q = p + 1; q < n; ++q) {
+                double apq = A[p * 4 + q];
+                if (std::fabs(apq) < 1e-300) continue;
+                double th = 0.5 * (A[q * 4 + q] - A[p * 4 + p]) / apq;
+                double t = (th >= 0 ? 1.0 : -1.0) / (std::fabs(th) + std::sqrt(th * th + 1.0));
+                double c = 1.0 / std::sqrt(t * t + 1.0), s = t * c;
+                for (int k = 0; k < n; ++k) {
+                    double akp = A[k * 4 + p], akq = A[k * 4 + q];
+                    A[k * 4 + p] = c * akp - s * akq;
+                    A[k * 4 + q] = s * akp + c * akq;
+                }
+                for (int k = 0; k < n; ++k) {
+                    double apk = A[p * 4 + k], aqk = A[q * 4 + k];
+                    A[p * 4 + k] = c * apk - s * aqk;
+                    A[q * 4 + k] = s * apk + c * aqk;
+                }
+            }
+    }
+    for (int i = 0; i < n; ++i) ev[i] = A[i * 4 + i];
+}
+
+static double det_inv(int n, const double* Ain, double* Ai) {  // host Gauss-Jordan, stride 4
+    double M[16], I[16] = {0};
+    std::memcpy(M, Ain, sizeof(M));
+    for (int i = 0; i < n; ++i) I[i * 4 + i] = 1.0;
+    double det = 1.0;
+    for (int col = 0; col < n; ++col) {
+        int piv = col;
+        for (int r = col + 1; r < n; ++r)
+            if (std::fabs(M[r * 4 + col]) > std::fabs(M[piv * 4 + col])) piv = r;
+        if (M[piv * 4 + col] == 0.0) return 0.0;
+        if (piv != col) {
+            for (int k = 0; k < 4; ++k) {
+                std::swap(M[col * 4 + k], M[piv * 4 + k]);
+                std::swap(I[col * 4 + k], I[piv * 4 + k]);
+            }
+            det = -det;
+        }
+        double p = M[col * 4 + col];
+        det *= p;
+        for (int k = 0; k < 4; ++k) { M[col * 4 + k] /= p; I[col * 4 + k] /= p; }
+        for (int r = 0; r < n; ++r) {
+            if (r == col) continue;
+            double f = M[r * 4 + col];
+            for (int k = 0; k < 4; ++k) { M[r * 4 + k] -= f * M[col * 4 + k]; I[r * 4 + k] -= f * I[col * 4 + k]; }
+        }
+    }
+    if (Ai) std::memcpy(Ai, I, sizeof(I));
+    return det;
+}
+
+static void unpack(int n, const double* src, double* dst) {  // packed n x n -> stride 4
+    for (int i = 0; i < 16; ++i) dst[i] = 0.0;
+    for (int i = 0; i < n; ++i)
+        for (int j = 0; j < n; ++j) dst[i * 4 + j] = src[i * n + j];
+}
+
+static bool radix_ok(int N) {
+    if (N < 4 || N > 1024) return false;
+    int m = N;
+    while (m % 2 == 0) m /= 2;
+    while (m % 3 == 0) m /= 3;
+    return m == 1;
+}
+
+static int dalloc(pmf_ctx* c, void** p, size_t bytes) {
+    if (bytes == 0) bytes = 16;
+    cudaError_t e = cudaMalloc(p, bytes);
+    if (e != cudaSuccess) { cudaGetLastError(); return fail(c, PMF_E_NOMEM, std::string("cudaMalloc: ") + cudaGetErrorString(e)); }
+    c->bytes += (int64_t)bytes;
+    return PMF_OK;
+}
+
+static PencilBufs bufs(pmf_ctx* c) {
+    PencilBufs b;
+    b.W = c->W; b.W2 = c->W2; b.S = c->S; b.st = c->st; b.partials = c->partials; b.coef = c->coef;
+    b.sub = c->sub; b.z = c->z; b.gauss = c->gauss;
+    return b;
+}
+
+static Twiddles twid(pmf_ctx* c) {
+    Twiddles t;
+    for (int i = 0; i < 4; ++i) t.tw[i] = c->tw[i];
+    return t;
+}
+
+// Model constants of a prediction interval tau = dt*steps: e^{A tau}, the trace
+// factor s (R5), and per-substep E_n = e^{-A n dt} Q e^{-A^T n dt}, P_n = e^{A n dt}.
+static int prepare_model(pmf_ctx* c, double dt, int steps) {
+    if (c->cached_dt == dt && c->cached_steps == steps) return PMF_OK;
+    const int nx = c->d.nx;
+    ModelParams mp{};
+    mp.nx = nx;
+    mp.l = steps;
+    mp.diff_mode = c->cfg.diff_mode;
+    mp.dt = dt;
+    double trA = 0.0;
+    for (int a = 0; a < nx; ++a) trA += c->A[a * 4 + a];
+    const int sgn = (c->cfg.trace_sign == PMF_TRACE_PRINTED) ? 1 : -1;
+    mp.s = std::pow(1.0 + sgn * dt * trA, steps);
+    double M[16];
+    for (int i = 0; i < 16; ++i) M[i] = c->A[i] * (dt * steps);
+    expm4(nx, M, mp.Mtau);
+    std::memcpy(mp.Q, c->Q, sizeof(mp.Q));
+    std::vector<SubstepEntry> tab(steps);
+    for (int s = 0; s < steps; ++s) {
+        double Mn[16], En[16], EnT[16], T1[16];
+        for (int i = 0; i < 16; ++i) Mn[i] = -c->A[i] * (dt * s);
+        expm4(nx, Mn, En);                            // e^{-A n dt}
+        for (int i = 0; i < 4; ++i)
+            for (int j = 0; j < 4; ++j) EnT[i * 4 + j] = En[j * 4 + i];
+        mat_mul(nx, En, c->Q, T1);
+        mat_mul(nx, T1, EnT, tab[s].E);
+        for (int i = 0; i < 16; ++i) Mn[i] = c->A[i] * (dt * s);
+        expm4(nx, Mn, tab[s].P);
+    }
+    size_t need = sizeof(SubstepEntry) * steps;
+    if (need > c->sub_bytes) {
+        if (c->sub) { cudaFree(c->sub); c->bytes -= (int64_t)c->sub_bytes; c->sub = nullptr; }
+        int r = dalloc(c, (void**)&c->sub, need);
+        if (r) return r;
+        c->sub_bytes = need;
+    }
+    size_t cneed = sizeof(double) * coef_stride(steps) * (size_t)c->d.batch;
+    if (cneed > c->coef_bytes) {
+        if (c->coef) { cudaFree(c->coef); c->bytes -= (int64_t)c->coef_bytes; c->coef = nullptr; }
+        int r = dalloc(c, (void**)&c->coef, cneed);
+        if (r) return r;
+        c->coef_bytes = cneed;
+    }
+    CK(c, cudaMemcpyAsync(c->sub, tab.data(), need, cudaMemcpyHostToDevice, c->stream), "upload substep table");
+    // the host vector dies at return: make the copy complete before that
+    CK(c, cudaStreamSynchronize(c->stream), "sync model upload");
+    c->mp = mp;
+    c->cached_dt = dt;
+    c->cached_steps = steps;
+    return PMF_OK;
+}
+
+static int make_lik(pmf_ctx* c, const pmf_likelihood* lik, LikParams& lp) {
+    if (!lik) return fail(c, PMF_E_ARG, "likelihood is NULL");
+    const int nx = c->d.nx;
+    lp = LikParams{};
+    lp.kind = lik->kind;
+    lp.nx = nx;
+    if (lik->kind == PMF_LIK_RANGE_GAUSS) {
+        if (!(lik->sigma > 0.0)) return fail(c, PMF_E_ARG, "range likelihood needs sigma > 0");
+        lp.nz = 1;
+        lp.inv_sigma = 1.0 / lik->sigma;
+        lp.lognorm = -std::log(lik->sigma * std::sqrt(2.0 * M_PI));
+        return PMF_OK;
+    }
+    if (lik->kind != PMF_LIK_LINEAR_GAUSS) return fail(c, PMF_E_ARG, "unknown likelihood kind");
+    const int nz = lik->nz;
+    if (nz < 1 || nz > PMF_MAX_NZ) return fail(c, PMF_E_ARG, "nz must be 1..4");
+    lp.nz = nz;
+    for (int i = 0; i < nz; ++i)
+        for (int a = 0; a < nx; ++a) lp.H[i * 4 + a] = lik->H[i * nx + a];
+    double R[16], Ri[16];
+    unpack(nz, lik->R, R);
+    double det = det_inv(nz, R, Ri);
+    if (!(det > 0.0)) return fail(c, PMF_E_ARG, "R must be positive definite");
+    std::memcpy(lp.Rinv, Ri, sizeof(Ri));
+    lp.lognorm = -0.5 * (nz * std::log(2.0 * M_PI) + std::log(det));
+    return PMF_OK;
+}
+
+static int upload_z(pmf_ctx* c, const double* z, int on_device, int nz) {
+    if (!z) return fail(c, PMF_E_ARG, "z is NULL");
+    size_t bytes = sizeof(double) * nz * (size_t)c->d.batch;
+    CK(c, cudaMemcpyAsync(c->z, z, bytes, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                          c->stream), "upload z");
+    return PMF_OK;
+}
+
+// Execute pending regrid/predict, optionally fused with an update.
+static int flush(pmf_ctx* c, const LikParams* lp) {
+    PencilBufs b = bufs(c);
+    cudaError_t e = cudaSuccess;
+    if (c->path == PMF_PATH_RESIDENT) {
+        if (!c->pend.regrid && !c->pend.predict && !lp) return PMF_OK;
+        e = launch_resident(c->d, c->dtype, b, twid(c), c->pend.predict ? &c->mp : nullptr, lp,
+                            c->pend.regrid ? c->pend.k_sigma : -1.0, c->stream, &c->launches);
+        if (e != cudaSuccess) return cuda_fail(c, e, "resident epoch kernel");
+    } else {
+        if (c->pend.regrid) {
+            e = launch_regrid(c->d, c->dtype, b, c->pend.k_sigma, c->stream, &c->launches);
+            if (e != cudaSuccess) return cuda_fail(c, e, "regrid");
+            std::swap(c->W, c->W2);
+        }
+        b = bufs(c);
+        if (c->pend.predict) {
+            e = launch_predict_pencil(c->d, c->dtype, b, twid(c), c->mp, lp, c->stream, &c->launches);
+            if (e != cudaSuccess) return cuda_fail(c, e, "predict");
+        } else if (lp) {
+            e = launch_update(c->d, c->dtype, b, *lp, c->stream, &c->launches);
+            if (e != cudaSuccess) return cuda_fail(c, e, "update");
+        }
+    }
+    c->pend = Pending{};
+    return PMF_OK;
+}
+
+template <typename T>
+static void make_twiddles(int N, std::vector<T>& out) {
+    out.resize(2 * N);
+    const long double pi = 3.141592653589793238462643383279502884L;
+    for (int m = 0; m < N; ++m) {
+        long double ang = 2.0L * pi * (long double)m / (long double)N;
+        out[2 * m] = (T)cosl(ang);
+        out[2 * m + 1] = (T)(-sinl(ang));
+    }
+}
+
+// ============================================================================ ABI
+extern "C" {
+
+const char* pmf_version(void) { return "pmf-b200 0.1 (sm_100a)"; }
+
+const char* pmf_last_error(const pmf_ctx* ctx) {
+    if (!ctx) return g_create_error.c_str();
+    return ctx->err.c_str();
+}
+
+int pmf_create(const pmf_config* cfg, const double* A, const double* Q, pmf_ctx** out) {
+    if (!cfg || !A || !Q || !out) return fail(nullptr, PMF_E_ARG, "null argument");
+    *out = nullptr;
+    const int nx = cfg->nx;
+    if (nx < 1 || nx > PMF_MAX_NX) return fail(nullptr, PMF_E_ARG, "nx must be 1..4");
+    if (cfg->batch < 1) return fail(nullptr, PMF_E_ARG, "batch must be >= 1");
+    if (cfg->dtype != PMF_F64 && cfg->dtype != PMF_F32) return fail(nullptr, PMF_E_ARG, "bad dtype");
+    if (cfg->diff_mode != PMF_DIFF_FULL && cfg->diff_mode != PMF_DIFF_AXIS_LITERAL)
+        return fail(nullptr, PMF_E_ARG, "bad diff_mode");
+    for (int m = 0; m < nx; ++m) {
+        if (cfg->n[m] % 2) return fail(nullptr, PMF_E_ODD_N, "points per axis must be even (P:219)");
+        if (!radix_ok(cfg->n[m])) return fail(nullptr, PMF_E_RADIX, "N must be 2^a 3^b in [4, 1024]");
+    }
+    double Qs[16];
+    unpack(nx, Q, Qs);
+    for (int i = 0; i < nx; ++i) {
+        for (int j = 0; j < nx; ++j) {
+            if (!std::isfinite(Qs[i * 4 + j]) || !std::isfinite(A[i * nx + j]))
+                return fail(nullptr, PMF_E_ARG, "A and Q must be finite");
+            double scale = std::max(std::fabs(Qs[i * 4 + j]), std::fabs(Qs[j * 4 + i]));
+            if (std::fabs(Qs[i * 4 + j] - Qs[j * 4 + i]) > 1e-12 * std::max(scale, 1e-300) &&
+                std::fabs(Qs[i * 4 + j] - Qs[j * 4 + i]) > 0)
+                return fail(nullptr, PMF_E_Q_NOT_PSD, "Q must be symmetric");
+        }
+    }
+    double ev[4];
+    sym_eig(nx, Qs, ev);
+    double qmax = 0.0;
+    for (int i = 0; i < nx; ++i) qmax = std::max(qmax, std::fabs(ev[i]));
+    for (int i = 0; i < nx; ++i)
+        if (ev[i] < -1e-12 * std::max(qmax, 1e-300)) return fail(nullptr, PMF_E_Q_NOT_PSD, "Q must be PSD");
+    if (cfg->diff_mode == PMF_DIFF_AXIS_LITERAL)
+        for (int i = 0; i < nx; ++i)
+            for (int j = 0; j < nx; ++j)
+                if (i != j && Qs[i * 4 + j] != 0.0)
+                    return fail(nullptr, PMF_E_ARG, "AXIS_LITERAL needs a diagonal Q (Alg. 3 uses Q^(m,m))");
+
+    int ndev = 0;
+    cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        return fail(nullptr, PMF_E_CUDA, "no CUDA device available (the library has no CPU fallback)");
+    }
+    if (cfg->device < 0 || cfg->device >= ndev) return fail(nullptr, PMF_E_ARG, "bad device ordinal");
+    e = cudaSetDevice(cfg->device);
+    if (e != cudaSuccess) return fail(nullptr, PMF_E_CUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(e));
+    cudaDeviceProp prop;
+    cudaGetDeviceProperties(&prop, cfg->device);
+    if (prop.major != 10) return fail(nullptr, PMF_E_CUDA, "device is not sm_100 (Blackwell B200)");
+
+    pmf_ctx* c = new pmf_ctx();
+    c->cfg = *cfg;
+    c->dtype = cfg->dtype;
+    c->esize = cfg->dtype == PMF_F64 ? 8 : 4;
+    c->stream = (cudaStream_t)cfg->stream;
+    unpack(nx, A, c->A);
+    std::memcpy(c->Q, Qs, sizeof(Qs));
+    Dims& d = c->d;
+    d.nx = nx;
+    d.ntot = 1;
+    for (int m = 0; m < 4; ++m) d.n[m] = m < nx ? cfg->n[m] : 1;
+    for (int m = 0; m < nx; ++m) d.ntot *= d.n[m];
+    d.H0 = d.n[0] / 2 + 1;
+    d.nspec = d.ntot / d.n[0] * d.H0;
+    d.batch = cfg->batch;
+
+    bool res_ok = resident_supported(d, c->dtype);
+    if (cfg->path == PMF_PATH_RESIDENT && !res_ok) {
+        delete c;
+        return fail(nullptr, PMF_E_ARG, "resident path not supported for this grid/dtype");
+    }
+    c->path = (cfg->path == PMF_PATH_PENCIL || !res_ok) ? PMF_PATH_PENCIL : PMF_PATH_RESIDENT;
+
+    const size_t wbytes = c->esize * (size_t)d.ntot * d.batch;
+    int r = PMF_OK;
+    if (!r) r = dalloc(c, &c->W, wbytes);
+    if (!r && c->path == PMF_PATH_PENCIL) r = dalloc(c, &c->W2, wbytes);
+    if (!r && c->path == PMF_PATH_PENCIL && nx > 1) r = dalloc(c, &c->S, 2 * c->esize * (size_t)d.nspec * d.batch);
+    if (!r) r = dalloc(c, (void**)&c->st, sizeof(FilterState) * d.batch);
+    // reduction scratch: the largest per-pass block count (pencil C2R rows / points kernels)
+    size_t nblk = (size_t)d.batch * 512;
+    nblk = std::max(nblk, (size_t)(d.ntot / d.n[0]) * d.batch);
+    c->partials_bytes = nblk * NMOM * sizeof(double);
+    if (!r) r = dalloc(c, (void**)&c->partials, c->partials_bytes);
+    if (!r) r = dalloc(c, (void**)&c->z, sizeof(double) * PMF_MAX_NZ * d.batch);
+    if (!r) r = dalloc(c, (void**)&c->gauss, sizeof(double) * 21 * d.batch);
+    for (int m = 0; m < nx && !r; ++m) {
+        const int N = d.n[m];
+        if (c->dtype == PMF_F64) {
+            std::vector<double> t;
+            make_twiddles(N, t);
+            r = dalloc(c, &c->tw[m], t.size() * sizeof(double));
+            if (!r && cudaMemcpy(c->tw[m], t.data(), t.size() * sizeof(double), cudaMemcpyHostToDevice) != cudaSuccess)
+                r = fail(c, PMF_E_CUDA, "twiddle upload");
+        } else {
+            std::vector<float> t;
+            make_twiddles(N, t);
+            r = dalloc(c, &c->tw[m], t.size() * sizeof(float));
+            if (!r && cudaMemcpy(c->tw[m], t.data(), t.size() * sizeof(float), cudaMemcpyHostToDevice) != cudaSuccess)
+                r = fail(c, PMF_E_CUDA, "twiddle upload");
+        }
+    }
+    if (!r) {
+        std::vector<FilterState> z(d.batch);
+        std::memset(z.data(), 0, sizeof(FilterState) * d.batch);
+        if (cudaMemcpy(c->st, z.data(), sizeof(FilterState) * d.batch, cudaMemcpyHostToDevice) != cudaSuccess)
+            r = fail(c, PMF_E_CUDA, "state init");
+    }
+    if (r) {
+        std::string m = c->err;
+        pmf_destroy(c);
+        if (!m.empty()) g_create_error = m;
+        return r;
+    }
+    *out = c;
+    return PMF_OK;
+}
+
+void pmf_destroy(pmf_ctx* c) {
+    if (!c) return;
+    cudaSetDevice(c->cfg.device);
+    cudaStreamSynchronize(c->stream);
+    void* ptrs[] = {c->W, c->W2, c->S, c->st, c->partials, c->coef, c->sub, c->z, c->gauss,
+                    c->tw[0], c->tw[1], c->tw[2], c->tw[3]};
+    for (void* p : ptrs)
+        if (p) cudaFree(p);
+    delete c;
+}
+
+int pmf_set_gaussian(pmf_ctx* c, const double* mean, const double* cov, double k_sigma) {
+    if (!c || !mean || !cov) return fail(c, PMF_E_ARG, "null argument");
+    if (!(k_sigma > 0.0)) return fail(c, PMF_E_ARG, "k_sigma must be > 0");
+    CK(c, cudaSetDevice(c->cfg.device), "cudaSetDevice");
+    const Dims& d = c->d;
+    const int nx = d.nx;
+    std::vector<FilterState> st(d.batch);
+    std::vector<double> g(21 * (size_t)d.batch, 0.0);
+    for (int b = 0; b < d.batch; ++b) {
+        FilterState& f = st[b];
+        std::memset(&f, 0, sizeof(f));
+        double P[16], Pi[16];
+        unpack(nx, cov + (size_t)b * nx * nx, P);
+        double det = det_inv(nx, P, Pi);
+        if (!(det > 0.0)) return fail(c, PMF_E_ARG, "cov must be positive definite");
+        for (int a = 0; a < nx; ++a) {
+            f.c[a] = mean[(size_t)b * nx + a];
+            f.B[a * 4 + a] = 2.0 * k_sigma * std::sqrt(P[a * 4 + a]) / d.n[a];   // R10
+            g[21 * (size_t)b + a] = mean[(size_t)b * nx + a];
+        }
+        for (int i = 0; i < 16; ++i) g[21 * (size_t)b + 4 + i] = Pi[i];
+        g[21 * (size_t)b + 20] = -0.5 * (nx * std::log(2.0 * M_PI) + std::log(det));
+        f.scale = 1.0;
+    }
+    c->pend = Pending{};
+    CK(c, cudaMemcpyAsync(c->st, st.data(), sizeof(FilterState) * d.batch, cudaMemcpyHostToDevice, c->stream),
+       "state upload");
+    CK(c, cudaMemcpyAsync(c->gauss, g.data(), sizeof(double) * g.size(), cudaMemcpyHostToDevice, c->stream),
+       "gauss upload");
+    PencilBufs b = bufs(c);
+    cudaError_t e = launch_init_gaussian(d, c->dtype, b, c->stream, &c->launches);
+    if (e != cudaSuccess) return cuda_fail(c, e, "init_gaussian");
+    CK(c, cudaStreamSynchronize(c->stream), "set_gaussian sync");
+    c->have_density = true;
+    c->have_update = false;
+    return PMF_OK;
+}
+
+int pmf_set_state(pmf_ctx* c, const double* center, const double* B, const void* weights, int on_device) {
+    if (!c || !center || !B || !weights) return fail(c, PMF_E_ARG, "null argument");
+    CK(c, cudaSetDevice(c->cfg.device), "cudaSetDevice");
+    const Dims& d = c->d;
+    const int nx = d.nx;
+    std::vector<FilterState> st(d.batch);
+    for (int b = 0; b < d.batch; ++b) {
+        FilterState& f = st[b];
+        std::memset(&f, 0, sizeof(f));
+        unpack(nx, B + (size_t)b * nx * nx, f.B);
+        if (det_inv(nx, f.B, nullptr) == 0.0) return fail(c, PMF_E_SINGULAR_GRID, "grid matrix B is singular");
+        for (int a = 0; a < nx; ++a) f.c[a] = center[(size_t)b * nx + a];
+        f.scale = 1.0;
+    }
+    c->pend = Pending{};
+    CK(c, cudaMemcpyAsync(c->st, st.data(), sizeof(FilterState) * d.batch, cudaMemcpyHostToDevice, c->stream),
+       "state upload");
+    CK(c, cudaMemcpyAsync(c->W, weights, c->esize * (size_t)d.ntot * d.batch,
+                          on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c->stream),
+       "weights upload");
+    PencilBufs b = bufs(c);
+    cudaError_t e = launch_normalise_state(d, c->dtype, b, c->stream, &c->launches);
+    if (e != cudaSuccess) return cuda_fail(c, e, "normalise");
+    CK(c, cudaStreamSynchronize(c->stream), "set_state sync");
+    c->have_density = true;
+    c->have_update = false;
+    return PMF_OK;
+}
+
+int pmf_predict(pmf_ctx* c, double dt, int steps) {
+    if (!c) return fail(c, PMF_E_ARG, "null context");
+    if (!c->have_density) return fail(c, PMF_E_STATE, "no density set");
+    if (!(dt > 0.0) || steps < 1 || !std::isfinite(dt)) return fail(c, PMF_E_DT, "dt must be > 0 and steps >= 1");
+    double trA = 0.0;
+    for (int a = 0; a < c->d.nx; ++a) trA += c->A[a * 4 + a];
+    const int sgn = (c->cfg.trace_sign == PMF_TRACE_PRINTED) ? 1 : -1;
+    if (!(1.0 + sgn * dt * trA > 0.0)) return fail(c, PMF_E_DT, "Euler trace factor base 1 -/+ dt tr(A) <= 0 (R5)");
+    CK(c, cudaSetDevice(c->cfg.device), "cudaSetDevice");
+    if (c->pend.predict) {   // two predicts in a row: run the first one now
+        int r = flush(c, nullptr);
+        if (r) return r;
+    }
+    int r = prepare_model(c, dt, steps);
+    if (r) return r;
+    c->pend.predict = true;
+    c->pend.dt = dt;
+    c->pend.steps = steps;
+    return PMF_OK;
+}
+
+int pmf_update(pmf_ctx* c, const double* z, int z_on_device, const pmf_likelihood* lik) {
+    if (!c) return fail(c, PMF_E_ARG, "null context");
+    if (!c->have_density) return fail(c, PMF_E_STATE, "no density set");
+    LikParams lp;
+    int r = make_lik(c, lik, lp);
+    if (r) return r;
+    CK(c, cudaSetDevice(c->cfg.device), "cudaSetDevice");
+    r = upload_z(c, z, z_on_device, lp.nz);
+    if (r) return r;
+    r = flush(c, &lp);
+    if (r) return r;
+    c->have_update = true;
+    return PMF_OK;
+}
+
+int pmf_regrid(pmf_ctx* c, double k_sigma) {
+    if (!c) return fail(c, PMF_E_ARG, "null context");
+    if (!c->have_update) return fail(c, PMF_E_STATE, "regrid needs the moments of an update");
+    if (!(k_sigma > 0.0)) return fail(c, PMF_E_ARG, "k_sigma must be > 0");
+    CK(c, cudaSetDevice(c->cfg.device), "cudaSetDevice");
+    if (c->pend.regrid || c->pend.predict) {
+        int r = flush(c, nullptr);
+        if (r) return r;
+    }
+    c->pend.regrid = true;
+    c->pend.k_sigma = k_sigma;
+    return PMF_OK;
+}
+
+int pmf_step(pmf_ctx* c, double dt, int steps, const double* z, int z_on_device, const pmf_likelihood* lik,
+             double k_sigma) {
+    int r = pmf_predict(c, dt, steps);
+    if (r) return r;
+    r = pmf_update(c, z, z_on_device, lik);
+    if (r) return r;
+    return pmf_regrid(c, k_sigma);
+}
+
+int pmf_moments(pmf_ctx* c, double* mean, double* cov, double* log_norm) {
+    if (!c) return fail(c, PMF_E_ARG, "null context");
+    if (!c->have_update) return fail(c, PMF_E_STATE, "no update has run");
+    CK(c, cudaSetDevice(c->cfg.device), "cudaSetDevice");
+    const Dims& d = c->d;
+    std::vector<FilterState> st(d.batch);
+    CK(c, cudaMemcpyAsync(st.data(), c->st, sizeof(FilterState) * d.batch, cudaMemcpyDeviceToHost, c->stream),
+       "state download");
+    CK(c, cudaStreamSynchronize(c->stream), "moments sync");
+    const int nx = d.nx;
+    int bad = 0;
+    for (int b = 0; b < d.batch; ++b) {
+        const FilterState& f = st[b];
+        if (f.status) bad = 1;
+        for (int a = 0; a < nx; ++a) {
+            if (mean) mean[(size_t)b * nx + a] = f.mean[a];
+            if (cov)
+                for (int q = 0; q < nx; ++q) cov[(size_t)b * nx * nx + a * nx + q] = f.cov[a * 4 + q];
+        }
+        if (log_norm) log_norm[b] = f.logC;
+    }
+    if (bad) return fail(c, PMF_E_NO_SUPPORT, "measurement incompatible with grid support (some filter)");
+    return PMF_OK;
+}
+
+int pmf_get_weights(pmf_ctx* c, void* dst, int dst_on_device) {
+    if (!c || !dst) return fail(c, PMF_E_ARG, "null argument");
+    if (!c->have_density) return fail(c, PMF_E_STATE, "no density set");
+    CK(c, cudaSetDevice(c->cfg.device), "cudaSetDevice");
+    int r = flush(c, nullptr);
+    if (r) return r;
+    const Dims& d = c->d;
+    size_t bytes = c->esize * (size_t)d.ntot * d.batch;
+    PencilBufs b = bufs(c);
+    if (dst_on_device) {
+        cudaError_t e = launch_scale_out(d, c->dtype, b, dst, c->stream, &c->launches);
+        if (e != cudaSuccess) return cuda_fail(c, e, "scale_out");
+        return PMF_OK;
+    }
+    void* tmp = c->path == PMF_PATH_PENCIL ? c->W2 : nullptr;
+    bool own = false;
+    if (!tmp) {
+        int rr = dalloc(c, &tmp, bytes);
+        if (rr) return rr;
+        own = true;
+    }
+    cudaError_t e = launch_scale_out(d, c->dtype, b, tmp, c->stream, &c->launches);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(dst, tmp, bytes, cudaMemcpyDeviceToHost, c->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+    if (own) { cudaFree(tmp); c->bytes -= (int64_t)bytes; }
+    if (e != cudaSuccess) return cuda_fail(c, e, "get_weights");
+    return PMF_OK;
+}
+
+int pmf_get_grid(pmf_ctx* c, double* center, double* B) {
+    if (!c) return fail(c, PMF_E_ARG, "null context");
+    if (!c->have_density) return fail(c, PMF_E_STATE, "no density set");
+    CK(c, cudaSetDevice(c->cfg.device), "cudaSetDevice");
+    int r = flush(c, nullptr);
+    if (r) return r;
+    const Dims& d = c->d;
+    std::vector<FilterState> st(d.batch);
+    CK(c, cudaMemcpyAsync(st.data(), c->st, sizeof(FilterState) * d.batch, cudaMemcpyDeviceToHost, c->stream),
+       "state download");
+    CK(c, cudaStreamSynchronize(c->stream), "grid sync");
+    const int nx = d.nx;
+    for (int b = 0; b < d.batch; ++b)
+        for (int a = 0; a < nx; ++a) {
+            if (center) center[(size_t)b * nx + a] = st[b].c[a];
+            if (B)
+                for (int q = 0; q < nx; ++q) B[(size_t)b * nx * nx + a * nx + q] = st[b].B[a * 4 + q];
+        }
+    return PMF_OK;
+}
+
+int pmf_sync(pmf_ctx* c) {
+    if (!c) return fail(c, PMF_E_ARG, "null context");
+    CK(c, cudaSetDevice(c->cfg.device), "cudaSetDevice");
+    if (c->have_density) {
+        int r = flush(c, nullptr);
+        if (r) return r;
+    }
+    CK(c, cudaStreamSynchronize(c->stream), "sync");
+    return PMF_OK;
+}
+
+int64_t pmf_launch_count(const pmf_ctx* c) { return c ? c->launches : 0; }
+int64_t pmf_device_bytes(const pmf_ctx* c) { return c ? c->bytes : 0; }
+int pmf_path(const pmf_ctx* c) { return c ? c->path : -1; }
+
+}  // extern "C"

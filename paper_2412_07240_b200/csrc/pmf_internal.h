@@ -1,0 +1,105 @@
+// pmf_internal.h -- structures shared by the host runtime (pmf_host.cpp) and the
+// CUDA kernels. Not part of the ABI (include/pmf.h is).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace pmf {
+
+constexpr int MAXNX = 4;
+constexpr int NMOM = 15;           // 1 + nx + nx(nx+1)/2 accumulators for nx = 4
+
+// Per-filter state, device resident, fp64. The stored weights W (dtype) and
+// `scale` represent the normalised density scale * W on the grid (c, B):
+// physical point xi_j = c + B u_j, u_j[m] = j_m - (N_m - 1)/2 (R10).
+struct FilterState {
+    double c[4];
+    double B[16];       // row-major, row stride 4
+    double scale;       // density = scale * W; invariant: vol * sum(scale W) = 1
+    double logC;        // log of the last update's normaliser
+    double mean[4];     // posterior moments of the last update (physical)
+    double cov[16];     // row stride 4
+    double mass;        // sum of the stored weights after the last update
+    int status;         // 0, or PMF_E_NO_SUPPORT when the last update/regrid failed
+    int has_moments;
+};
+
+// Model constants of one prediction interval (host computed, kernel param).
+struct ModelParams {
+    int nx, l, diff_mode, pad;
+    double dt;          // Euler substep
+    double s;           // trace factor (1 -/+ dt tr A)^l (R5)
+    double Mtau[16];    // e^{A tau}, row stride 4
+    double Q[16];
+};
+
+// Device table, one entry per substep n < l (host computed, uploaded per predict):
+//   E_n = e^{-A n dt} Q e^{-A^T n dt}   (so D_n = B^-1 E_n B^-T, R3)
+//   P_n = e^{A n dt}                    (B_n = P_n B, for AXIS_LITERAL)
+struct SubstepEntry {
+    double E[16];
+    double P[16];
+};
+
+// Likelihood parameters (kernel param).
+struct LikParams {
+    int kind, nz, nx, pad;
+    double H[16];       // nz x nx, row stride 4
+    double Rinv[16];    // nz x nz, row stride 4
+    double lognorm;     // -0.5 log((2 pi)^nz det R)  or  -log(sigma sqrt(2 pi))
+    double inv_sigma;
+};
+
+struct Dims {
+    int nx;
+    int n[4];
+    int H0;                 // N_0/2 + 1 (half spectrum along axis 0)
+    long long ntot;         // real points per filter
+    long long nspec;        // complex half-spectrum points per filter
+    int batch;
+};
+
+// Number of doubles per filter in the pencil path's epoch-coefficient buffer.
+inline int coef_stride(int l) { return 4 + 10 * l; }
+
+// ---------------------------------------------------------------------------
+// launchers (implemented in the .cu files); all return a cudaError_t and
+// increment *launches by the number of kernels launched.
+// ---------------------------------------------------------------------------
+struct Twiddles {        // per distinct axis length: forward table e^{-2 pi i m / N}
+    const void* tw[4];   // device pointers per axis (complex of dtype)
+};
+
+struct PencilBufs {
+    void* W;             // real weights [batch][ntot]
+    void* W2;            // second real buffer (regrid target)
+    void* S;             // complex half spectrum [batch][nspec]
+    FilterState* st;
+    double* partials;    // reduction scratch
+    double* coef;        // [batch][coef_stride(l)]
+    const SubstepEntry* sub;
+    const double* z;     // [batch][nz]
+    const double* gauss; // [batch][nx + 16 + 1] mean, inverse cov, log norm (set_gaussian)
+};
+
+cudaError_t launch_init_gaussian(const Dims& d, int dtype, PencilBufs& b, cudaStream_t s, int64_t* launches);
+cudaError_t launch_normalise_state(const Dims& d, int dtype, PencilBufs& b, cudaStream_t s, int64_t* launches);
+cudaError_t launch_update(const Dims& d, int dtype, PencilBufs& b, const LikParams& lp,
+                          cudaStream_t s, int64_t* launches);
+cudaError_t launch_regrid(const Dims& d, int dtype, PencilBufs& b, double k_sigma,
+                          cudaStream_t s, int64_t* launches);   // swaps b.W / b.W2
+cudaError_t launch_predict_pencil(const Dims& d, int dtype, PencilBufs& b, const Twiddles& tw,
+                                  const ModelParams& mp, const LikParams* lp /* null = no update */,
+                                  cudaStream_t s, int64_t* launches);
+cudaError_t launch_scale_out(const Dims& d, int dtype, const PencilBufs& b, void* dst,
+                             cudaStream_t s, int64_t* launches);
+
+// resident (one CTA per filter) fused epoch kernel
+bool resident_supported(const Dims& d, int dtype);
+cudaError_t launch_resident(const Dims& d, int dtype, PencilBufs& b, const Twiddles& tw,
+                            const ModelParams* mp /* null = no predict */,
+                            const LikParams* lp /* null = no update */,
+                            double regrid_k_sigma /* < 0 = no regrid */,
+                            cudaStream_t s, int64_t* launches);
+
+}  // namespace pmf

@@ -1,0 +1,244 @@
+"""Thin ctypes binding of libpmf.so (include/pmf.h): argument marshalling only.
+
+Every step of the filter runs in the library's CUDA kernels; this module only
+packs arrays, passes torch's CUDA stream and device pointers, and raises
+``PMFError`` on non-zero return codes. There is no CPU fallback: importing
+works anywhere, but creating a ``Filter`` needs libpmf.so and a CUDA device.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import Optional
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libpmf.so")
+
+PMF_OK = 0
+ERRORS = {-1: "PMF_E_ARG", -2: "PMF_E_ODD_N", -3: "PMF_E_RADIX", -4: "PMF_E_Q_NOT_PSD",
+          -5: "PMF_E_SINGULAR_GRID", -6: "PMF_E_NO_SUPPORT", -7: "PMF_E_DT", -8: "PMF_E_STATE",
+          -9: "PMF_E_CUDA", -10: "PMF_E_NOMEM"}
+F64, F32 = 0, 1
+DIFF_FULL, DIFF_AXIS_LITERAL = 0, 1
+TRACE_PHYSICAL, TRACE_PRINTED = -1, 1
+PATH_AUTO, PATH_PENCIL, PATH_RESIDENT = 0, 1, 2
+LIK_LINEAR_GAUSS, LIK_RANGE_GAUSS = 0, 1
+
+# every symbol include/pmf.h declares (checked by tests/test_abi.py)
+SYMBOLS = ["pmf_create", "pmf_destroy", "pmf_last_error", "pmf_set_gaussian", "pmf_set_state",
+           "pmf_predict", "pmf_update", "pmf_moments", "pmf_regrid", "pmf_step", "pmf_get_weights",
+           "pmf_get_grid", "pmf_sync", "pmf_launch_count", "pmf_device_bytes", "pmf_path", "pmf_version"]
+
+
+class PMFError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"{ERRORS.get(code, code)}: {msg}")
+        self.code = code
+
+
+class pmf_config(C.Structure):
+    _fields_ = [("nx", C.c_int), ("n", C.c_int * 4), ("batch", C.c_int), ("dtype", C.c_int),
+                ("diff_mode", C.c_int), ("trace_sign", C.c_int), ("path", C.c_int), ("device", C.c_int),
+                ("stream", C.c_void_p)]
+
+
+class pmf_likelihood(C.Structure):
+    _fields_ = [("kind", C.c_int), ("nz", C.c_int), ("H", C.c_double * 16), ("R", C.c_double * 16),
+                ("sigma", C.c_double)]
+
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH) -> C.CDLL:
+    """Load libpmf.so; raises (loudly) if it has not been built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(f"libpmf.so not built at {path}: run `python -m paper_2412_07240_b200.build` "
+                          "(there is no CPU fallback)")
+    lib = C.CDLL(path)
+    P, D, I, V = C.c_void_p, C.POINTER(C.c_double), C.c_int, C.c_void_p
+    sig = {
+        "pmf_create": (I, [C.POINTER(pmf_config), D, D, C.POINTER(P)]),
+        "pmf_destroy": (None, [P]),
+        "pmf_last_error": (C.c_char_p, [P]),
+        "pmf_set_gaussian": (I, [P, D, D, C.c_double]),
+        "pmf_set_state": (I, [P, D, D, V, I]),
+        "pmf_predict": (I, [P, C.c_double, I]),
+        "pmf_update": (I, [P, V, I, C.POINTER(pmf_likelihood)]),
+        "pmf_moments": (I, [P, D, D, D]),
+        "pmf_regrid": (I, [P, C.c_double]),
+        "pmf_step": (I, [P, C.c_double, I, V, I, C.POINTER(pmf_likelihood), C.c_double]),
+        "pmf_get_weights": (I, [P, V, I]),
+        "pmf_get_grid": (I, [P, D, D]),
+        "pmf_sync": (I, [P]),
+        "pmf_launch_count": (C.c_int64, [P]),
+        "pmf_device_bytes": (C.c_int64, [P]),
+        "pmf_path": (I, [P]),
+        "pmf_version": (C.c_char_p, []),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def _dptr(a: np.ndarray):
+    return a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+def make_likelihood(kind: int, nx: int, H=None, R=None, sigma: float = 0.0) -> pmf_likelihood:
+    lk = pmf_likelihood()
+    lk.kind = kind
+    if kind == LIK_RANGE_GAUSS:
+        lk.nz = 1
+        lk.sigma = float(sigma)
+    else:
+        H = np.atleast_2d(np.asarray(H, dtype=np.float64))
+        R = np.atleast_2d(np.asarray(R, dtype=np.float64))
+        lk.nz = H.shape[0]
+        for i, v in enumerate(H.reshape(-1)):
+            lk.H[i] = v
+        for i, v in enumerate(R.reshape(-1)):
+            lk.R[i] = v
+    return lk
+
+
+class Filter:
+    """A batch of spectral point-mass filters on the GPU (one pmf_ctx)."""
+
+    def __init__(self, nx: int, n, A, Q, batch: int = 1, dtype: str = "f64", diff_mode: int = DIFF_FULL,
+                 trace_sign: int = TRACE_PHYSICAL, path: int = PATH_AUTO, device: int = 0,
+                 stream: Optional[int] = None):
+        self.lib = load_library()
+        self.nx, self.n, self.batch = nx, tuple(int(v) for v in n), batch
+        self.dtype = dtype
+        self.np_dtype = np.float64 if dtype == "f64" else np.float32
+        cfg = pmf_config()
+        cfg.nx = nx
+        for i in range(4):
+            cfg.n[i] = self.n[i] if i < nx else 1
+        cfg.batch = batch
+        cfg.dtype = F64 if dtype == "f64" else F32
+        cfg.diff_mode = diff_mode
+        cfg.trace_sign = trace_sign
+        cfg.path = path
+        cfg.device = device
+        if stream is None:
+            try:
+                import torch
+                if torch.cuda.is_available():
+                    stream = torch.cuda.current_stream(device).cuda_stream
+            except Exception:
+                stream = None
+        cfg.stream = C.c_void_p(stream) if stream else None
+        A = np.ascontiguousarray(np.asarray(A, dtype=np.float64).reshape(nx, nx))
+        Q = np.ascontiguousarray(np.asarray(Q, dtype=np.float64).reshape(nx, nx))
+        h = C.c_void_p()
+        rc = self.lib.pmf_create(C.byref(cfg), _dptr(A), _dptr(Q), C.byref(h))
+        if rc != PMF_OK:
+            raise PMFError(rc, self.lib.pmf_last_error(None).decode())
+        self.h = h
+        self.ntot = int(np.prod(self.n))
+
+    # --------------------------------------------------------------- helpers
+    def _check(self, rc: int):
+        if rc != PMF_OK:
+            raise PMFError(rc, self.lib.pmf_last_error(self.h).decode())
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.pmf_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # --------------------------------------------------------------- ABI
+    def set_gaussian(self, mean, cov, k_sigma: float):
+        mean = np.ascontiguousarray(np.broadcast_to(np.asarray(mean, dtype=np.float64),
+                                                    (self.batch, self.nx)))
+        cov = np.ascontiguousarray(np.broadcast_to(np.asarray(cov, dtype=np.float64),
+                                                   (self.batch, self.nx, self.nx)))
+        self._check(self.lib.pmf_set_gaussian(self.h, _dptr(mean), _dptr(cov), float(k_sigma)))
+
+    def set_state(self, center, B, weights):
+        center = np.ascontiguousarray(np.asarray(center, dtype=np.float64).reshape(self.batch, self.nx))
+        B = np.ascontiguousarray(np.asarray(B, dtype=np.float64).reshape(self.batch, self.nx, self.nx))
+        if hasattr(weights, "data_ptr"):      # torch tensor on the device
+            self._check(self.lib.pmf_set_state(self.h, _dptr(center), _dptr(B), C.c_void_p(weights.data_ptr()), 1))
+        else:
+            w = np.ascontiguousarray(np.asarray(weights, dtype=self.np_dtype).reshape(-1))
+            self._check(self.lib.pmf_set_state(self.h, _dptr(center), _dptr(B), w.ctypes.data_as(C.c_void_p), 0))
+
+    def predict(self, dt: float, steps: int):
+        self._check(self.lib.pmf_predict(self.h, float(dt), int(steps)))
+
+    def _z(self, z):
+        if hasattr(z, "data_ptr"):
+            return C.c_void_p(z.data_ptr()), 1, z
+        zz = np.ascontiguousarray(np.asarray(z, dtype=np.float64).reshape(-1))
+        return zz.ctypes.data_as(C.c_void_p), 0, zz
+
+    def update(self, z, lik: pmf_likelihood):
+        p, dev, keep = self._z(z)
+        self._check(self.lib.pmf_update(self.h, p, dev, C.byref(lik)))
+        del keep
+
+    def regrid(self, k_sigma: float):
+        self._check(self.lib.pmf_regrid(self.h, float(k_sigma)))
+
+    def step(self, dt: float, steps: int, z, lik: pmf_likelihood, k_sigma: float):
+        p, dev, keep = self._z(z)
+        self._check(self.lib.pmf_step(self.h, float(dt), int(steps), p, dev, C.byref(lik), float(k_sigma)))
+        del keep
+
+    def moments(self):
+        mean = np.empty((self.batch, self.nx))
+        cov = np.empty((self.batch, self.nx, self.nx))
+        logc = np.empty(self.batch)
+        self._check(self.lib.pmf_moments(self.h, _dptr(mean), _dptr(cov), _dptr(logc)))
+        return mean, cov, logc
+
+    def moments_into(self, mean: np.ndarray, cov: np.ndarray, logc: np.ndarray):
+        self._check(self.lib.pmf_moments(self.h, _dptr(mean), _dptr(cov), _dptr(logc)))
+
+    def weights(self) -> np.ndarray:
+        """Normalised densities, shape (batch, N_{nx-1}, ..., N_0) (axis 0 fastest)."""
+        out = np.empty((self.batch,) + tuple(reversed(self.n)), dtype=self.np_dtype)
+        self._check(self.lib.pmf_get_weights(self.h, out.ctypes.data_as(C.c_void_p), 0))
+        return out
+
+    def weights_to(self, tensor):
+        """Write the normalised densities into a device tensor (torch)."""
+        self._check(self.lib.pmf_get_weights(self.h, C.c_void_p(tensor.data_ptr()), 1))
+
+    def grid(self):
+        c = np.empty((self.batch, self.nx))
+        B = np.empty((self.batch, self.nx, self.nx))
+        self._check(self.lib.pmf_get_grid(self.h, _dptr(c), _dptr(B)))
+        return c, B
+
+    def sync(self):
+        self._check(self.lib.pmf_sync(self.h))
+
+    @property
+    def launches(self) -> int:
+        return int(self.lib.pmf_launch_count(self.h))
+
+    @property
+    def device_bytes(self) -> int:
+        return int(self.lib.pmf_device_bytes(self.h))
+
+    @property
+    def path(self) -> int:
+        return int(self.lib.pmf_path(self.h))

@@ -1,0 +1,145 @@
+"""GPU parity: the CUDA path through the C ABI vs the CPU oracle on the same
+seeded inputs (element-wise weights, moments, normaliser, grid) -- bar: relative
+L-inf normalised by the peak density <= 1e-10 (fp64), <= 1e-4 (fp32)."""
+import numpy as np
+import pytest
+
+from oracle import pmf_oracle as O
+from paper_2412_07240_b200 import pmf
+from workloads import make_config, random_density, simulate
+
+from parity_util import TOL, compare_runs, lik_of, rel_linf, run_gpu, run_oracle
+
+pytestmark = pytest.mark.gpu
+
+CASES = {
+    # name: (config id, overrides, T)   sizes span several tiles + ragged tails, radix 2 and 3
+    "C1": ("C1", {}, 20),
+    "C1b3": ("C1", {"batch": 3, "n": (96,)}, 5),
+    "C2s": ("C2", {"n": (48, 32)}, 6),
+    "C3s": ("C3", {"n": (16, 12, 24)}, 4),
+    "C4s": ("C4", {"n": (8, 6, 12, 8)}, 3),
+    "C5s": ("C5", {"batch": 5, "n": (24, 32)}, 4),
+}
+
+
+@pytest.mark.parametrize("name", list(CASES))
+@pytest.mark.parametrize("path", [pmf.PATH_PENCIL, pmf.PATH_AUTO])
+def test_filter_run_parity_f64(name, path):
+    cid, over, T = CASES[name]
+    cfg = make_config(cid, **over)
+    zs = simulate(cfg, T=T)["z"]
+    g = run_gpu(cfg, zs, T, path=path)
+    orc = run_oracle(cfg, zs, T)
+    e = compare_runs(cfg, g, orc, T, TOL["f64"])
+    assert e["w"] <= 1e-10, e
+    assert e["mean"] <= 1e-10 and e["cov"] <= 1e-10 and e["logC"] <= 1e-10 and e["grid"] <= 1e-10, e
+
+
+@pytest.mark.parametrize("name", ["C2s", "C5s"])
+def test_filter_run_parity_f32(name):
+    cid, over, T = CASES[name]
+    cfg = make_config(cid, **over)
+    zs = simulate(cfg, T=T)["z"]
+    g = run_gpu(cfg, zs, T, dtype="f32")
+    orc = run_oracle(cfg, zs, T)
+    e = compare_runs(cfg, g, orc, T, TOL["f32"])
+    assert e["w"] <= 1e-4 and e["mean"] <= 1e-4 and e["cov"] <= 1e-4, e
+
+
+def test_step_api_equals_unfused_sequence():
+    cfg = make_config("C5", batch=3, n=(24, 32))
+    T = 3
+    zs = simulate(cfg, T=T)["z"]
+    a = run_gpu(cfg, zs, T)
+    b = run_gpu(cfg, zs, T, use_step=True)
+    for k in range(T + 1):
+        assert np.max(np.abs(a["mean"][k] - b["mean"][k])) < 1e-12
+        assert np.max(np.abs(a["logC"][k] - b["logC"][k])) < 1e-12
+
+
+@pytest.mark.parametrize("nx,n", [(2, (32, 24)), (3, (12, 16, 8))])
+@pytest.mark.parametrize("mode", ["full", "axis_literal", "printed_trace"])
+def test_predict_operator_parity_sheared(nx, n, mode):
+    """One predict from a non-Gaussian density on a sheared grid with
+    non-diagonal A (and Q for the full mode)."""
+    rng = np.random.default_rng(11 + nx)
+    A = 0.5 * rng.standard_normal((nx, nx))
+    if mode == "axis_literal":
+        Q = np.diag(rng.uniform(0.05, 0.3, nx))
+    else:
+        M = rng.standard_normal((nx, nx))
+        Q = 0.05 * (M @ M.T) + 0.02 * np.eye(nx)
+    B = np.diag(rng.uniform(0.05, 0.1, nx)) + 0.01 * rng.standard_normal((nx, nx))
+    c = rng.standard_normal(nx)
+    wlib = random_density(n, 1, seed=3)[0]
+    diff = O.DIFF_AXIS_LITERAL if mode == "axis_literal" else O.DIFF_FULL
+    ts = O.TRACE_SIGN_PRINTED if mode == "printed_trace" else O.TRACE_SIGN_PHYSICAL
+    f = pmf.Filter(nx, n, A, Q, diff_mode=diff, trace_sign=ts)
+    f.set_state(c[None], B[None], wlib)
+    tau, l = 0.3, 7
+    f.predict(tau / l, l)
+    wg = f.weights()[0]
+    cg, Bg = f.grid()
+    w0 = O.normalise(O.from_lib(wlib, n), B)
+    wo, co, Bo = O.predict(w0, c, B, A, Q, tau, l, diff_mode=diff, trace_sign=ts)
+    assert rel_linf(wg, O.to_lib(wo)) <= 1e-10
+    assert rel_linf(Bg[0], Bo) <= 1e-13 and rel_linf(cg[0], co) <= 1e-13
+
+
+def test_update_and_regrid_operator_parity():
+    """Standalone update (range likelihood) and regrid on a sheared grid."""
+    n = (20, 16, 12)
+    cfg = make_config("C3", n=n)
+    rng = np.random.default_rng(5)
+    B = np.diag([0.12, 0.1, 0.11]) + 0.02 * rng.standard_normal((3, 3))
+    c = np.array([1.5, 0.2, -0.1])
+    wlib = random_density(n, 1, seed=9)[0]
+    f = pmf.Filter(3, n, cfg.A, cfg.Q)
+    f.set_state(c[None], B[None], wlib)
+    z = np.array([[1.6]])
+    f.update(z, lik_of(cfg))
+    mean, cov, logc = f.moments()
+    w0 = O.normalise(O.from_lib(wlib, n), B)
+    X = O.grid_points(c, B, n)
+    wo, lo = O.update(w0, c, B, O.lik_range_gauss(X, z[0], cfg.sigma))
+    mo, co = O.moments(wo, c, B)
+    assert rel_linf(f.weights()[0], O.to_lib(wo)) <= 1e-10
+    assert abs(logc[0] - lo) <= 1e-10 and rel_linf(mean[0], mo) <= 1e-10 and rel_linf(cov[0], co) <= 1e-10
+    f.regrid(4.0)
+    wg = f.weights()[0]
+    cg, Bg = f.grid()
+    c2, B2 = O.regrid_target(mo, co, n, 4.0)
+    wr = O.regrid(wo, c, B, c2, B2)
+    assert rel_linf(wg, O.to_lib(wr)) <= 1e-10
+    assert rel_linf(Bg[0], B2) <= 1e-12
+
+
+def test_error_codes():
+    cfg = make_config("C1")
+    f = pmf.Filter(1, cfg.n, cfg.A, cfg.Q)
+    with pytest.raises(pmf.PMFError) as e:
+        f.predict(0.01, 10)
+    assert e.value.code == -8                        # PMF_E_STATE
+    f.set_gaussian(cfg.prior_mean, cfg.prior_cov[None], cfg.k_sigma)
+    with pytest.raises(pmf.PMFError) as e:
+        f.predict(-1.0, 10)
+    assert e.value.code == -7                        # PMF_E_DT
+    with pytest.raises(pmf.PMFError) as e:
+        f.regrid(6.0)
+    assert e.value.code == -8
+    f.update(np.array([[1e6]]), lik_of(cfg))          # far outside the support: normaliser underflows to 0
+    with pytest.raises(pmf.PMFError) as e:
+        f.moments()
+    assert e.value.code == -6                        # PMF_E_NO_SUPPORT
+
+
+def test_launch_count_and_determinism():
+    cfg = make_config("C5", batch=4, n=(32, 32))
+    zs = simulate(cfg, T=2)["z"]
+    a = run_gpu(cfg, zs, 2)
+    b = run_gpu(cfg, zs, 2)
+    assert a["filter"].launches > 0
+    for k in range(3):
+        assert np.array_equal(a["w"][k], b["w"][k])          # fixed-order reductions: bitwise
+        assert np.array_equal(a["mean"][k], b["mean"][k])
