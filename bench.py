@@ -1,0 +1,327 @@
+#!/usr/bin/env python
+"""Benchmark of the spectral point-mass filter hot path on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload C5] [--impl cuda|reference]
+
+A STEP is one filter epoch over the whole batch, i.e. every row of SURVEY
+§8(a): (re-centre grid + multilinear resample, R12) -> forward DFT per axis
+-> s*Psi over l Euler substeps -> inverse DFT -> normalise (Alg. 1-6) ->
+likelihood, normaliser and moments (eq:filt). Default workload C5 (BASELINE
+configs[4]): 4096 independent 2-D CV filters on 128x128, fp64, l = 10 -- the
+largest single-GPU configuration whose per-GPU work is fixed, sharded by filter
+index across ranks (weak scaling: every rank runs its own 4096 filters; no
+collective on the data path).
+
+Metric (BASELINE.json): grid-point FPE updates/sec = filters * 128^2 / t_step.
+Timing: W untimed warm-up steps, then K steps bracketed by barrier +
+cuda.synchronize, CUDA events on the library's stream, max over ranks.
+The weights (537 MB fp64) exceed the 126 MB L2, so no flush is needed.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from workloads import make_config, simulate  # noqa: E402
+
+WORKLOADS = {
+    "C5": dict(cid="C5", over={}),
+    "C5f32": dict(cid="C5", over={"dtype": "f32"}),
+    "C4": dict(cid="C4", over={}),
+    "C3": dict(cid="C3", over={}),
+    "C2": dict(cid="C2", over={}),
+    "C1": dict(cid="C1", over={}),
+}
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d.get("hbm_gbs", 6650.0), "measured (MEASURED_PEAKS.json hbm_gbs)", d.get("sm_max_mhz", 1965.0)
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)", 1965.0
+
+
+# B200: 148 SMs x 64 FP64 FMA/clk (the FP64 pipe is half the FP32 rate on B200);
+# one FMA counts as 2 flops. See DESIGN.md §5.
+def fp64_peak_tflops(mhz):
+    return 148 * 64 * 2 * mhz * 1e6 / 1e12
+
+
+class Clocks:
+    """nvidia-smi sampler during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, device):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,power.draw")
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(device), f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                                       "-lms", "100"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        self.p.wait()
+        self.f.flush()
+        rows = []
+        for line in open(self.f.name):
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 7:
+                rows.append(parts)
+        os.unlink(self.f.name)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"], "samples": 0}
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[2 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": float(rows[0][1]),
+                "reasons": reasons, "samples": len(rows),
+                "power_w_max": max(float(r[6]) for r in rows if r[6].replace(".", "").isdigit())}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def oracle_sample(cfg, zs, budget_s: float, max_filters: int):
+    """Time the CPU oracle (as it stands) on a bounded sample: one epoch
+    (predict + update + moments + regrid) per filter, filters 0.. until the
+    budget is used. Returns (points_per_s, filter_epochs, seconds)."""
+    from oracle import pmf_oracle as O
+    n = tuple(cfg.n)
+    done, t_tot = 0, 0.0
+    for b in range(min(cfg.batch, max_filters)):
+        w, c, B = O.initial_density(cfg.prior_mean[b], cfg.prior_cov, n, cfg.k_sigma)
+        t0 = time.perf_counter()
+        w, c, B = O.predict(w, c, B, cfg.A, cfg.Q, cfg.tau, cfg.l)
+        w, _ = O.update(w, c, B, O.make_likelihood(cfg, O.grid_points(c, B, n), zs[1, b]))
+        mean, cov = O.moments(w, c, B)
+        c2, B2 = O.regrid_target(mean, cov, n, cfg.k_sigma)
+        w = O.regrid(w, c, B, c2, B2)
+        t_tot += time.perf_counter() - t0
+        done += 1
+        if t_tot >= budget_s:
+            break
+    return done * cfg.points / t_tot, done, t_tot
+
+
+def threads_used():
+    try:
+        from threadpoolctl import threadpool_info
+        return max((i.get("num_threads", 1) for i in threadpool_info()), default=1)
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle timed as the reference arm (rank 0 only)."""
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    wl = WORKLOADS[args.workload]
+    cfg = make_config(wl["cid"], **wl["over"])
+    zs = simulate(cfg.replace(batch=min(cfg.batch, 64)), T=1)["z"]
+    cfgs = cfg.replace(batch=min(cfg.batch, 64))
+    per_step = []
+    for _ in range(args.warmup + args.steps):
+        v, nf, t = oracle_sample(cfgs, zs, budget_s=args.ref_budget, max_filters=64)
+        per_step.append((v, nf, t))
+    timed = per_step[args.warmup:]
+    val = statistics.median(v for v, _, _ in timed)
+    nf = timed[0][1]
+    line = {"impl": "reference", "metric": "grid-point FPE updates/sec (fp64)", "value": val,
+            "unit": "grid-point updates/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * cfg.batch * cfg.points / val, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{args.workload}: {cfg.batch} x {cfg.n} {cfg.nx}-D filters, l={cfg.l}",
+                       "sample": f"{nf} filter-epochs per step (oracle is O(N^2) naive DFT)"},
+            "cpu_baseline": {"value": val, "unit": "grid-point updates/s", "cores": threads_used(), "kind": "oracle",
+                             "sample": f"{nf} of {cfg.batch} filters x 1 epoch per step"},
+            "e2e": {"value": val, "unit": "grid-point updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--workload", default="C5", choices=sorted(WORKLOADS))
+    ap.add_argument("--impl", default="cuda", choices=["cuda", "reference"])
+    ap.add_argument("--l", type=int, default=None, help="override Euler substeps")
+    ap.add_argument("--path", type=int, default=0, help="0 auto, 1 pencil, 2 resident")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--ref-budget", type=float, default=8.0)
+    ap.add_argument("--json-out", default=None)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+    from paper_2412_07240_b200 import pmf
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    wl = WORKLOADS[args.workload]
+    cfg = make_config(wl["cid"], **wl["over"])
+    if args.l:
+        cfg = cfg.replace(l=args.l)
+    # weak scaling: rank r runs its own batch of filters (distinct seeds)
+    cfg = cfg.replace(seed=cfg.seed + 7919 * rank)
+    cfg = make_config(wl["cid"], **{**wl["over"], "seed": cfg.seed, "l": cfg.l})
+    dtype = cfg.dtype
+    T = args.warmup + args.steps + 1
+    zs = simulate(cfg, T=T)["z"]                       # (T+1, batch, nz)
+    stream = torch.cuda.Stream()
+    f = pmf.Filter(cfg.nx, cfg.n, cfg.A, cfg.Q, batch=cfg.batch, dtype=dtype, path=args.path,
+                   device=local, stream=stream.cuda_stream)
+    lik = (pmf.make_likelihood(pmf.LIK_RANGE_GAUSS, cfg.nx, sigma=cfg.sigma) if cfg.lik_kind == 1
+           else pmf.make_likelihood(pmf.LIK_LINEAR_GAUSS, cfg.nx, H=cfg.H, R=cfg.R))
+    f.set_gaussian(cfg.prior_mean, np.broadcast_to(cfg.prior_cov, (cfg.batch, cfg.nx, cfg.nx)), cfg.k_sigma)
+    z_dev = torch.tensor(zs, dtype=torch.float64, device=f"cuda:{local}")   # inputs resident in HBM
+    dt = cfg.tau / cfg.l
+    f.update(z_dev[0], lik)
+    f.regrid(cfg.k_sigma)
+    k = 1
+    for _ in range(args.warmup):
+        f.step(dt, cfg.l, z_dev[k], lik, cfg.k_sigma)
+        k += 1
+    f.sync()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = Clocks(local)
+    launches0 = f.launches
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    k0 = k
+    with torch.cuda.stream(stream):
+        ev0.record(stream)
+        for i in range(args.steps):
+            f.step(dt, cfg.l, z_dev[k0 + i], lik, cfg.k_sigma)
+        ev1.record(stream)
+    ev1.synchronize()
+    clk = clocks.stop()
+    launches = f.launches - launches0
+    t_ms = ev0.elapsed_time(ev1)
+    torch.cuda.synchronize()
+    t_max = t_ms
+    if world > 1:
+        tt = torch.tensor([t_ms], device=f"cuda:{local}", dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_max = float(tt.item())
+    points_step = cfg.batch * cfg.points
+    value = world * points_step * args.steps / (t_max * 1e-3)
+    ms_step = t_max / args.steps
+
+    # ---------------------------------------------------------------- e2e: host buffers through the C ABI
+    e2e = None
+    if not args.no_e2e:
+        Te = min(args.steps, 10)
+        zs_e = simulate(cfg, T=Te + 1)["z"]
+        z_pin = torch.tensor(zs_e, dtype=torch.float64).pin_memory()
+        fe = pmf.Filter(cfg.nx, cfg.n, cfg.A, cfg.Q, batch=cfg.batch, dtype=dtype, path=args.path,
+                        device=local, stream=stream.cuda_stream)
+        fe.set_gaussian(cfg.prior_mean, np.broadcast_to(cfg.prior_cov, (cfg.batch, cfg.nx, cfg.nx)), cfg.k_sigma)
+        mean = np.empty((cfg.batch, cfg.nx))
+        cov = np.empty((cfg.batch, cfg.nx, cfg.nx))
+        logc = np.empty(cfg.batch)
+        zp = z_pin.data_ptr()
+        zstride = cfg.batch * cfg.nz * 8
+        import ctypes as C
+        fe.lib.pmf_update(fe.h, C.c_void_p(zp), 0, C.byref(lik))
+        fe.regrid(cfg.k_sigma)
+        fe.moments_into(mean, cov, logc)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for i in range(Te):
+            rc = fe.lib.pmf_step(fe.h, dt, cfg.l, C.c_void_p(zp + (i + 1) * zstride), 0, C.byref(lik), cfg.k_sigma)
+            assert rc == 0, fe.lib.pmf_last_error(fe.h)
+            fe.moments_into(mean, cov, logc)                  # D2H read of the step's result
+        e1.record(stream)
+        e1.synchronize()
+        te = e0.elapsed_time(e1)
+        if world > 1:
+            tt = torch.tensor([te], device=f"cuda:{local}", dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            te = float(tt.item())
+        e2e = {"value": world * points_step * Te / (te * 1e-3), "unit": "grid-point updates/s",
+               "h2d_bytes_per_step": cfg.batch * cfg.nz * 8,
+               "d2h_bytes_per_step": fe_state_bytes(cfg.batch), "steps": Te}
+        fe.close()
+
+    # ---------------------------------------------------------------- roofline (dominant kernel)
+    hbm, hbm_src, sm_max = peaks()
+    esize = 8 if dtype == "f64" else 4
+    alg_bytes = 2 * esize * points_step          # read + write every weight once per epoch
+    kern_ms = ms_step                            # the step is the fused epoch kernel (resident path);
+    if f.path == pmf.PATH_PENCIL:                # pencil path: several kernels -> whole-step figure
+        dominant = "pencil path (all kernels of the step)"
+    else:
+        dominant = "k_resident_epoch (one launch per step)"
+    achieved = alg_bytes / (kern_ms * 1e-3) / 1e9
+    roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+            "traffic": None, "kernel": dominant, "peak_source": hbm_src,
+            "alg_bytes_per_launch": alg_bytes}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        v, nf, ts = oracle_sample(cfg, zs, budget_s=args.cpu_budget, max_filters=cfg.batch)
+        cpu = {"value": v, "unit": "grid-point updates/s", "cores": threads_used(), "kind": "oracle",
+               "sample": f"{nf} of {cfg.batch} filters x 1 epoch ({ts:.1f} s of CPU time)"}
+
+    line = {"metric": "grid-point FPE updates/sec (fp64)" if dtype == "f64" else "grid-point FPE updates/sec (fp32)",
+            "value": value, "unit": "grid-point updates/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": dtype, "data": "synthetic",
+            "config": {"workload": f"{args.workload}: {cfg.batch} x {'x'.join(map(str, cfg.n))} {cfg.nx}-D CV filters "
+                                   f"per GPU, l={cfg.l}, tau={cfg.tau}, k_sigma={cfg.k_sigma}",
+                       "step": "regrid + predict (Alg. 1-6) + update + moments, every filter",
+                       "l2": f"inputs larger than L2 ({alg_bytes / 2 / 1e6:.0f} MB of weights per GPU)",
+                       "path": "resident" if f.path == pmf.PATH_RESIDENT else "pencil",
+                       "parallelism": f"filter-sharded x{world} (no data-path collective)"},
+            "e2e": e2e, "gpu_launches": launches, "roofline": roof, "cpu_baseline": cpu, "clocks": clk}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+        if args.json_out:
+            with open(args.json_out, "w") as fh:
+                json.dump(line, fh, indent=1)
+    f.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def fe_state_bytes(batch):
+    # pmf_moments copies the per-filter state records (sizeof(FilterState) = 352 B)
+    return 352 * batch
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -311,25 +311,31 @@ static int upload_z(pmf_ctx* c, const double* z, int on_device, int nz) {
 static int flush(pmf_ctx* c, const LikParams* lp) {
     PencilBufs b = bufs(c);
     cudaError_t e = cudaSuccess;
-    if (c->path == PMF_PATH_RESIDENT) {
-        if (!c->pend.regrid && !c->pend.predict && !lp) return PMF_OK;
-        e = launch_resident(c->d, c->dtype, b, twid(c), c->pend.predict ? &c->mp : nullptr, lp,
-                            c->pend.regrid ? c->pend.k_sigma : -1.0, c->stream, &c->launches);
+    // the resident kernel keeps 3 coefficients per substep in shared memory
+    const bool resident = c->path == PMF_PATH_RESIDENT && c->pend.predict && c->pend.steps <= 2048;
+    if (resident) {
+        e = launch_resident(c->d, c->dtype, b, twid(c), &c->mp, lp, c->pend.regrid ? c->pend.k_sigma : -1.0,
+                            c->stream, &c->launches);
         if (e != cudaSuccess) return cuda_fail(c, e, "resident epoch kernel");
-    } else {
-        if (c->pend.regrid) {
-            e = launch_regrid(c->d, c->dtype, b, c->pend.k_sigma, c->stream, &c->launches);
-            if (e != cudaSuccess) return cuda_fail(c, e, "regrid");
-            std::swap(c->W, c->W2);
-        }
-        b = bufs(c);
-        if (c->pend.predict) {
-            e = launch_predict_pencil(c->d, c->dtype, b, twid(c), c->mp, lp, c->stream, &c->launches);
-            if (e != cudaSuccess) return cuda_fail(c, e, "predict");
-        } else if (lp) {
-            e = launch_update(c->d, c->dtype, b, *lp, c->stream, &c->launches);
-            if (e != cudaSuccess) return cuda_fail(c, e, "update");
-        }
+        c->pend = Pending{};
+        return PMF_OK;
+    }
+    if (c->pend.regrid) {
+        e = launch_regrid(c->d, c->dtype, b, c->pend.k_sigma, c->stream, &c->launches);
+        if (e != cudaSuccess) return cuda_fail(c, e, "regrid");
+        std::swap(c->W, c->W2);
+    }
+    if (c->pend.predict && !c->S && c->d.nx > 1) {   // resident context asked for a very long interval
+        int r = dalloc(c, &c->S, 2 * c->esize * (size_t)c->d.nspec * c->d.batch);
+        if (r) return r;
+    }
+    b = bufs(c);
+    if (c->pend.predict) {
+        e = launch_predict_pencil(c->d, c->dtype, b, twid(c), c->mp, lp, c->stream, &c->launches);
+        if (e != cudaSuccess) return cuda_fail(c, e, "predict");
+    } else if (lp) {
+        e = launch_update(c->d, c->dtype, b, *lp, c->stream, &c->launches);
+        if (e != cudaSuccess) return cuda_fail(c, e, "update");
     }
     c->pend = Pending{};
     return PMF_OK;
@@ -432,7 +438,7 @@ int pmf_create(const pmf_config* cfg, const double* A, const double* Q, pmf_ctx*
     const size_t wbytes = c->esize * (size_t)d.ntot * d.batch;
     int r = PMF_OK;
     if (!r) r = dalloc(c, &c->W, wbytes);
-    if (!r && c->path == PMF_PATH_PENCIL) r = dalloc(c, &c->W2, wbytes);
+    if (!r) r = dalloc(c, &c->W2, wbytes);
     if (!r && c->path == PMF_PATH_PENCIL && nx > 1) r = dalloc(c, &c->S, 2 * c->esize * (size_t)d.nspec * d.batch);
     if (!r) r = dalloc(c, (void**)&c->st, sizeof(FilterState) * d.batch);
     // reduction scratch: the largest per-pass block count (pencil C2R rows / points kernels)
@@ -650,7 +656,7 @@ int pmf_get_weights(pmf_ctx* c, void* dst, int dst_on_device) {
         if (e != cudaSuccess) return cuda_fail(c, e, "scale_out");
         return PMF_OK;
     }
-    void* tmp = c->path == PMF_PATH_PENCIL ? c->W2 : nullptr;
+    void* tmp = c->W2;
     bool own = false;
     if (!tmp) {
         int rr = dalloc(c, &tmp, bytes);

@@ -89,7 +89,7 @@ def test_predict_operator_parity_sheared(nx, n, mode):
 
 def test_update_and_regrid_operator_parity():
     """Standalone update (range likelihood) and regrid on a sheared grid."""
-    n = (20, 16, 12)
+    n = (18, 16, 12)
     cfg = make_config("C3", n=n)
     rng = np.random.default_rng(5)
     B = np.diag([0.12, 0.1, 0.11]) + 0.02 * rng.standard_normal((3, 3))
@@ -143,3 +143,69 @@ def test_launch_count_and_determinism():
     for k in range(3):
         assert np.array_equal(a["w"][k], b["w"][k])          # fixed-order reductions: bitwise
         assert np.array_equal(a["mean"][k], b["mean"][k])
+
+
+# ----------------------------------------------------------------------------- resident (fused) path
+@pytest.mark.parametrize("use_step", [False, True])
+def test_resident_epoch_parity_f64(use_step):
+    """The one-launch-per-epoch kernel (regrid + predict + update + moments) on
+    128x128 filters, batch not a multiple of anything, vs the oracle."""
+    cfg = make_config("C5", batch=7)
+    T = 3
+    zs = simulate(cfg, T=T)["z"]
+    g = run_gpu(cfg, zs, T, path=pmf.PATH_RESIDENT, use_step=use_step)
+    assert g["filter"].path == pmf.PATH_RESIDENT
+    orc = run_oracle(cfg, zs, T)
+    e = compare_runs(cfg, g, orc, T, TOL["f64"])
+    assert e["w"] <= 1e-10 and e["mean"] <= 1e-10 and e["cov"] <= 1e-10 and e["logC"] <= 1e-10, e
+    assert e["grid"] <= 1e-10, e
+
+
+def test_resident_epoch_parity_f32():
+    cfg = make_config("C5", batch=5)
+    T = 3
+    zs = simulate(cfg, T=T)["z"]
+    g = run_gpu(cfg, zs, T, dtype="f32", path=pmf.PATH_RESIDENT)
+    orc = run_oracle(cfg, zs, T)
+    e = compare_runs(cfg, g, orc, T, TOL["f32"])
+    assert e["w"] <= 1e-4 and e["mean"] <= 1e-4 and e["cov"] <= 1e-4, e
+
+
+@pytest.mark.parametrize("mode", ["full", "axis_literal", "printed_trace"])
+def test_resident_predict_operator_parity_sheared(mode):
+    """Predict only (no update) on a sheared 128x128 grid, non-diagonal A and Q,
+    a non-Gaussian input: exercises the resident kernel's UPDATE=0 branch."""
+    nx, n = 2, (128, 128)
+    rng = np.random.default_rng(21)
+    A = 0.5 * rng.standard_normal((nx, nx))
+    if mode == "axis_literal":
+        Q = np.diag(rng.uniform(0.05, 0.3, nx))
+    else:
+        M = rng.standard_normal((nx, nx))
+        Q = 0.05 * (M @ M.T) + 0.02 * np.eye(nx)
+    B = np.diag(rng.uniform(0.02, 0.03, nx)) + 0.003 * rng.standard_normal((nx, nx))
+    c = rng.standard_normal(nx)
+    wlib = random_density(n, 2, seed=4)
+    diff = O.DIFF_AXIS_LITERAL if mode == "axis_literal" else O.DIFF_FULL
+    ts = O.TRACE_SIGN_PRINTED if mode == "printed_trace" else O.TRACE_SIGN_PHYSICAL
+    f = pmf.Filter(nx, n, A, Q, batch=2, diff_mode=diff, trace_sign=ts, path=pmf.PATH_RESIDENT)
+    f.set_state(np.stack([c, -c]), np.stack([B, B.T]), wlib)
+    tau, l = 0.3, 7
+    f.predict(tau / l, l)
+    wg = f.weights()
+    cg, Bg = f.grid()
+    for b, (cb, Bb) in enumerate([(c, B), (-c, B.T)]):
+        w0 = O.normalise(O.from_lib(wlib[b], n), Bb)
+        wo, co, Bo = O.predict(w0, cb, Bb, A, Q, tau, l, diff_mode=diff, trace_sign=ts)
+        assert rel_linf(wg[b], O.to_lib(wo)) <= 1e-10
+        assert rel_linf(Bg[b], Bo) <= 1e-13 and rel_linf(cg[b], co) <= 1e-13
+
+
+def test_resident_matches_pencil_path():
+    cfg = make_config("C5", batch=3)
+    T = 2
+    zs = simulate(cfg, T=T)["z"]
+    a = run_gpu(cfg, zs, T, path=pmf.PATH_RESIDENT)
+    b = run_gpu(cfg, zs, T, path=pmf.PATH_PENCIL)
+    for k in range(T + 1):
+        assert rel_linf(a["w"][k], b["w"][k]) <= 1e-12
