@@ -133,6 +133,36 @@ __device__ __forceinline__ double det4(int nx, const double* B) {
 // signed wavenumber of transform index k (N even): [0..N/2-1] -> k, [N/2..N-1] -> k - N
 __device__ __forceinline__ int signed_k(int k, int N) { return k < N / 2 ? k : k - N; }
 
+// ---------------------------------------------------------------- exp
+// exp(x) in fp64 for the likelihood: Cody-Waite reduction x = k ln2 + r, |r| <= ln2/2,
+// degree-13 Taylor polynomial (truncation < 1e-17 relative), scale by 2^k through the
+// exponent field. Arguments below -708 return 0 (true value < 3e-308, far below the
+// 1e-10 peak-relative parity bar); the likelihood exponent never exceeds +709.
+__device__ __forceinline__ double exp_fast(double x) {
+    const double C = 6755399441055744.0;                    // 1.5 * 2^52: round-to-nearest trick
+    const double kd0 = fma(x, 1.4426950408889634074, C);
+    const int k = __double2loint(kd0);
+    const double kd = kd0 - C;
+    double r = fma(kd, -6.93147180559945286227e-01, x);
+    r = fma(kd, -2.31904681384629955842e-17, r);
+    double p = 1.6059043836821614599e-10;                   // 1/13!
+    p = fma(p, r, 2.0876756987868098979e-09);               // 1/12!
+    p = fma(p, r, 2.5052108385441718775e-08);
+    p = fma(p, r, 2.7557319223985890653e-07);
+    p = fma(p, r, 2.7557319223985890653e-06);
+    p = fma(p, r, 2.4801587301587301587e-05);
+    p = fma(p, r, 1.9841269841269841270e-04);
+    p = fma(p, r, 1.3888888888888888889e-03);
+    p = fma(p, r, 8.3333333333333333333e-03);
+    p = fma(p, r, 4.1666666666666666667e-02);
+    p = fma(p, r, 1.6666666666666666667e-01);
+    p = fma(p, r, 0.5);
+    p = fma(p, r, 1.0);
+    p = fma(p, r, 1.0);
+    const double y = __hiloint2double(__double2hiint(p) + (int)((unsigned)k << 20), __double2loint(p));
+    return x < -708.0 ? 0.0 : y;
+}
+
 // ---------------------------------------------------------------- likelihood at a physical point
 __device__ __forceinline__ double log_lik(const LikParams& lp, const double* x, const double* z) {
     if (lp.kind == 1) {

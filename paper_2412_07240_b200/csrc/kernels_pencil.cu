@@ -257,7 +257,7 @@ __global__ void __launch_bounds__(kThreads) k_axis0_c2r(const typename C2<T>::ty
             double u[4], x[4];
             point_u(d, pt_base + i, u);
             phys(d.nx, f, u, x);
-            w = w * scale * exp(log_lik(lp, x, zf));
+            w = w * scale * exp_fast(log_lik(lp, x, zf));
             T wt = (T)w;
             dst[i] = wt;
             acc_moments(d.nx, (double)wt, u, acc);
@@ -312,7 +312,7 @@ __global__ void __launch_bounds__(kThreads) k_line_psi(T* __restrict__ W, Filter
         if (UPDATE) {
             double u = j - 0.5 * (N - 1), x;
             phys(1, f, &u, &x);
-            w = w * scale * exp(log_lik(lp, &x, zf));
+            w = w * scale * exp_fast(log_lik(lp, &x, zf));
             T wt = (T)w;
             row[j] = wt;
             acc_moments(1, (double)wt, &u, acc);
@@ -352,7 +352,7 @@ __global__ void __launch_bounds__(kThreads) k_points(T* __restrict__ W, const Fi
         point_u(d, pt, u);
         if (MODE == 0) {
             phys(d.nx, f, u, x);
-            double w = (double)Wf[pt] * f.scale * exp(log_lik(lp, x, zf));
+            double w = (double)Wf[pt] * f.scale * exp_fast(log_lik(lp, x, zf));
             T wt = (T)w;
             Wf[pt] = wt;
             acc_moments(d.nx, (double)wt, u, acc);

@@ -152,50 +152,269 @@ __device__ __forceinline__ int cslot(int s, int t, int m) {
     return row * PITCH + 2 * m + col;
 }
 
-struct Shared {              // per-filter constants (shared memory)
-    double cl[2], Bl[4];     // moved grid
-    double M[4], o[2];       // regrid map v = o + M u'
-    double qa, qb[2], qG[3]; // linear-Gauss: e(u) = qa + qb.u + u^T [qG0 qG1; qG1 qG2] u
-    double zr;               // range likelihood: z
-    double lognorm, inv_sigma;
-    double vol_l, s_over_n2;
-    double dc;
-    int skip;
+// ---------------------------------------------------------------------------
+// Per-filter constants of one epoch, written by k_res_prep (one thread per
+// filter) into a global table and staged into shared memory by TMA together
+// with the filter's weights. Layout (doubles), stride PRM_FIXED + 3 l (even):
+enum {
+    P_M = 0,        // 4: regrid map v = o + M u' (old index coordinates of new point u')
+    P_O = 4,        // 2
+    P_CL = 6,       // 2: moved grid centre c_l = e^{A tau} c0
+    P_BL = 8,       // 4: moved grid matrix B_l = e^{A tau} B0 (row-major 2x2)
+    P_VOL = 12,     // |det B_l|
+    P_QA = 13,      // linear-Gauss exponent e(u) = qa + qb.u + u^T G u (G = [g0 g1; g1 g2])
+    P_QB = 14,      // 2
+    P_QG = 16,      // 3
+    P_ZR = 19,      // range measurement z
+    P_SKIP = 20,    // 1.0: skip this filter (failed earlier / degenerate regrid)
+    P_S = 21,       // s / N^2 (trace factor and the transform scales)
+    P_LGN = 22,     // log normalising constant of the likelihood
+    P_ISG = 23,     // 1 / sigma (range likelihood)
+    PRM_FIXED = 24  // then 3 doubles per Euler substep: dt/2 D00, dt/2 D11, dt D01
 };
+inline int prm_stride(int l) { return (PRM_FIXED + 3 * l + 1) & ~1; }
 
 }  // namespace res
 
 using namespace res;
 
+// ============================================================================ prep (1 thread per filter)
+// Grid constants of the epoch: regrid target (R12), start-of-interval grid
+// (c0, B0), moved grid B_l = e^{A tau} B0 (eq:gridMov P:142-148), Euler-factor
+// coefficients on B0 for the l substeps (Alg. 3, R3/R4), and the
+// likelihood exponent as a quadratic form in the moved grid's index
+// coordinates (eq:meas P:36, R13). The state's grid becomes (c_l, B_l).
+__global__ void k_res_prep(FilterState* st, double* prm, int pstride, ModelParams mp,
+                           const SubstepEntry* __restrict__ sub, LikParams lp, const double* __restrict__ z,
+                           double ks, int update, int batch) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= batch) return;
+    FilterState& f = st[b];
+    double* P = prm + (long long)b * pstride;
+    const double B[4] = {f.B[0], f.B[1], f.B[4], f.B[5]};
+    const double c[2] = {f.c[0], f.c[1]};
+    double B0[4] = {B[0], B[1], B[2], B[3]}, c0[2] = {c[0], c[1]};
+    bool skip = f.status != 0;
+    if (ks > 0.0) {
+        const double v0 = f.cov[0], v1 = f.cov[5];
+        if (!(v0 > 0.0) || !(v1 > 0.0) || !isfinite(v0) || !isfinite(v1)) skip = true;
+        c0[0] = f.mean[0];
+        c0[1] = f.mean[1];
+        B0[0] = 2.0 * ks * sqrt(v0) / N;
+        B0[1] = 0.0;
+        B0[2] = 0.0;
+        B0[3] = 2.0 * ks * sqrt(v1) / N;
+        const double det = B[0] * B[3] - B[1] * B[2];
+        const double Bi[4] = {B[3] / det, -B[1] / det, -B[2] / det, B[0] / det};
+        P[P_M + 0] = Bi[0] * B0[0] + Bi[1] * B0[2];
+        P[P_M + 1] = Bi[0] * B0[1] + Bi[1] * B0[3];
+        P[P_M + 2] = Bi[2] * B0[0] + Bi[3] * B0[2];
+        P[P_M + 3] = Bi[2] * B0[1] + Bi[3] * B0[3];
+        const double d0 = c0[0] - c[0], d1 = c0[1] - c[1];
+        P[P_O + 0] = fma(Bi[0], d0, fma(Bi[1], d1, 0.5 * (N - 1)));
+        P[P_O + 1] = fma(Bi[2], d0, fma(Bi[3], d1, 0.5 * (N - 1)));
+    }
+    P[P_SKIP] = skip ? 1.0 : 0.0;
+    if (skip) {
+        f.status = -6;
+        return;
+    }
+    const double* Mt = mp.Mtau;      // stride 4
+    double Bl[4], cl[2];
+    Bl[0] = fma(Mt[0], B0[0], Mt[1] * B0[2]);
+    Bl[1] = fma(Mt[0], B0[1], Mt[1] * B0[3]);
+    Bl[2] = fma(Mt[4], B0[0], Mt[5] * B0[2]);
+    Bl[3] = fma(Mt[4], B0[1], Mt[5] * B0[3]);
+    cl[0] = fma(Mt[0], c0[0], Mt[1] * c0[1]);
+    cl[1] = fma(Mt[4], c0[0], Mt[5] * c0[1]);
+    for (int q = 0; q < 4; ++q) P[P_BL + q] = Bl[q];
+    P[P_CL] = cl[0];
+    P[P_CL + 1] = cl[1];
+    P[P_VOL] = fabs(Bl[0] * Bl[3] - Bl[1] * Bl[2]);
+    P[P_S] = mp.s / (double)(N * N);
+    P[P_LGN] = lp.lognorm;
+    P[P_ISG] = lp.inv_sigma;
+    if (update && lp.kind == 0) {
+        const double* zf = z + (long long)b * lp.nz;
+        double r0[4], G0[4], G1[4];
+        for (int i = 0; i < lp.nz; ++i) {
+            const double h0 = lp.H[i * 4], h1 = lp.H[i * 4 + 1];
+            r0[i] = zf[i] - fma(h0, cl[0], h1 * cl[1]);
+            G0[i] = fma(h0, Bl[0], h1 * Bl[2]);
+            G1[i] = fma(h0, Bl[1], h1 * Bl[3]);
+        }
+        double qa = 0, qb0 = 0, qb1 = 0, g00 = 0, g01 = 0, g11 = 0;
+        for (int i = 0; i < lp.nz; ++i)
+            for (int j = 0; j < lp.nz; ++j) {
+                const double R = lp.Rinv[i * 4 + j];
+                qa = fma(r0[i] * R, r0[j], qa);
+                qb0 = fma(-2.0 * G0[i] * R, r0[j], qb0);
+                qb1 = fma(-2.0 * G1[i] * R, r0[j], qb1);
+                g00 = fma(G0[i] * R, G0[j], g00);
+                g01 = fma(G0[i] * R, G1[j], g01);
+                g11 = fma(G1[i] * R, G1[j], g11);
+            }
+        P[P_QA] = qa;
+        P[P_QB] = qb0;
+        P[P_QB + 1] = qb1;
+        P[P_QG] = g00;
+        P[P_QG + 1] = g01;
+        P[P_QG + 2] = g11;
+    } else if (update) {
+        P[P_ZR] = z[b];
+    }
+    const double det0 = B0[0] * B0[3] - B0[1] * B0[2];
+    const double Bi0[4] = {B0[3] / det0, -B0[1] / det0, -B0[2] / det0, B0[0] / det0};
+    for (int n = 0; n < mp.l; ++n) {
+        double D00, D01, D11;
+        if (mp.diff_mode == 0) {           // R3: D_n = B0^-1 E_n B0^-T
+            const double* E = sub[n].E;
+            const double t00 = fma(Bi0[0], E[0], Bi0[1] * E[4]);
+            const double t01 = fma(Bi0[0], E[1], Bi0[1] * E[5]);
+            const double t10 = fma(Bi0[2], E[0], Bi0[3] * E[4]);
+            const double t11 = fma(Bi0[2], E[1], Bi0[3] * E[5]);
+            D00 = fma(t00, Bi0[0], t01 * Bi0[1]);
+            D01 = 0.5 * (fma(t00, Bi0[2], t01 * Bi0[3]) + fma(t10, Bi0[0], t11 * Bi0[1]));
+            D11 = fma(t10, Bi0[2], t11 * Bi0[3]);
+        } else {                           // Alg. 3 literally: per-axis L^(m) = N ||B_n[:,m]||
+            const double* Pn = sub[n].P;
+            const double b00 = fma(Pn[0], B0[0], Pn[1] * B0[2]);
+            const double b01 = fma(Pn[0], B0[1], Pn[1] * B0[3]);
+            const double b10 = fma(Pn[4], B0[0], Pn[5] * B0[2]);
+            const double b11 = fma(Pn[4], B0[1], Pn[5] * B0[3]);
+            D00 = mp.Q[0] / fma(b00, b00, b10 * b10);
+            D11 = mp.Q[5] / fma(b01, b01, b11 * b11);
+            D01 = 0.0;
+        }
+        P[PRM_FIXED + 3 * n] = 0.5 * mp.dt * D00;
+        P[PRM_FIXED + 3 * n + 1] = 0.5 * mp.dt * D11;
+        P[PRM_FIXED + 3 * n + 2] = mp.dt * D01;
+    }
+    f.c[0] = cl[0];
+    f.c[1] = cl[1];
+    f.B[0] = Bl[0];
+    f.B[1] = Bl[1];
+    f.B[4] = Bl[2];
+    f.B[5] = Bl[3];
+}
+
+// ============================================================================ finalize (1 thread per filter)
+// out[b] = {sum w, sum w u0, sum w u1, sum w u0^2, sum w u0 u1, sum w u1^2, DC}.
+// Update: C = sum w / (s DC), log C, scale = 1/(vol_l sum w), moments (R14).
+// Predict only: closed-form normalisation scale = 1 / (vol_l s DC) (Alg. 6).
+__global__ void k_res_finalize(FilterState* st, const double* __restrict__ out, const double* __restrict__ prm,
+                               int pstride, double s, int update, int batch) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= batch) return;
+    const double* P = prm + (long long)b * pstride;
+    if (P[P_SKIP] != 0.0) return;
+    FilterState& f = st[b];
+    const double* o = out + (long long)b * 8;
+    const double vol = P[P_VOL];
+    if (!update) {
+        f.scale = 1.0 / (vol * s * o[6]);
+        return;
+    }
+    // stored weights are the unnormalised prior (sum = s DC) times the likelihood:
+    // normaliser C = vol sum(prior_normalised lik) = o[0] / (s DC)
+    const double C = o[0] / (s * o[6]);
+    f.mass = o[0];
+    f.has_moments = 1;
+    if (!(C > 0.0) || !isfinite(C) || !(o[0] > 0.0)) {
+        f.status = -6;
+        f.logC = -INFINITY;
+        return;
+    }
+    f.status = 0;
+    f.logC = log(C);
+    f.scale = 1.0 / (vol * o[0]);
+    double acc[NMOM];
+    for (int i = 0; i < NMOM; ++i) acc[i] = 0.0;
+    for (int i = 0; i < 6; ++i) acc[i] = o[i];
+    finish_moments(2, acc, f.c, f.B, f.mean, f.cov);
+}
+
+// ============================================================================ TMA helpers
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        "WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
 template <typename T>
 struct ResArgs {
     T* W;
-    FilterState* st;
-    const double* z;
-    const SubstepEntry* sub;
-    ModelParams mp;
-    LikParams lp;
-    double ks;
+    const double* prm;
+    double* out;
+    int pstride;
+    int l;
     int batch;
+    int range;        // likelihood kind 1
 };
 
+// Staging row pitch in bytes for the weights (padded so the regrid gather's 8
+// rows per team hit distinct banks; 16-byte aligned for the bulk copies).
+template <typename T> struct StagePitch;
+template <> struct StagePitch<double> { static constexpr unsigned B = 130 * 8; };
+template <> struct StagePitch<float> { static constexpr unsigned B = 132 * 4; };
+
+// Stage filter `filt` (called by all of warp 0): its 128 weight rows into the X
+// region at pitch StagePitch, and its constants into pbuf, completing on `bar`.
+template <typename T>
+__device__ __forceinline__ void stage(const ResArgs<T>& a, int filt, void* Xr, double* pbuf,
+                                      unsigned long long* bar, int lane) {
+    constexpr unsigned RB = N * sizeof(T);
+    const unsigned pbytes = a.pstride * sizeof(double);
+    if (lane == 0) {
+        fence_proxy_async();
+        mbar_expect_tx(bar, N * RB + pbytes);
+    }
+    __syncwarp();
+    const char* src = reinterpret_cast<const char*>(a.W + (long long)filt * (N * N));
+    for (int r = lane; r < N; r += 32)
+        bulk_g2s(reinterpret_cast<char*>(Xr) + r * StagePitch<T>::B, src + r * RB, RB, bar);
+    if (lane == 0) bulk_g2s(pbuf, a.prm + (long long)filt * a.pstride, pbytes, bar);
+}
+
+// ============================================================================ the fused epoch kernel
 template <typename T, bool REGRID, bool UPDATE>
 __global__ void __launch_bounds__(NT, 1) k_resident_epoch(ResArgs<T> a) {
     using V = typename C2<T>::type;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    V* X = reinterpret_cast<V*>(smem_raw);                          // [H][PITCH]
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    V* X = reinterpret_cast<V*>(smem_raw);                          // [H][PITCH]; also the dense staging area
+    const char* Xs = reinterpret_cast<const char*>(smem_raw);       // staged weights, row j1 at j1 * StagePitch
     V* tw = X + H * PITCH;                                          // [16][8]  W128^{ts}
-    Shared* sh = reinterpret_cast<Shared*>(tw + 128);
-    double* red = reinterpret_cast<double*>(sh + 1);                // [16 warps][6]
-    T* cf = reinterpret_cast<T*>(red + 16 * 6);                      // [l][3]
+    double* red = reinterpret_cast<double*>(tw + 128);              // [16 warps][6]
+    double* dcs = red + 16 * 6;                                     // DC of the current filter
+    unsigned long long* bar = reinterpret_cast<unsigned long long*>(dcs + 2);
+    double* pb0 = reinterpret_cast<double*>(bar + 2);               // 2 x pstride parameter buffers
 
     const int tid = threadIdx.x;
     const int m = tid >> 3, t = tid & 7;
     const int lane = tid & 31, warp = tid >> 5;
-    // own s pair for the 8-point stages: {t, 16 - t}, thread 0 takes {0, 8}
-    const int sa = t, sb = (t == 0) ? 8 : 16 - t;
-    const int l = a.mp.l;
-    const int nx = 2;
+    const int sa = t, sb = (t == 0) ? 8 : 16 - t;   // own s pair of the 8-point stages
+    const int l = a.l;
 
     for (int i = tid; i < 128; i += NT) {
         const int s = i >> 3, tt = i & 7;
@@ -204,149 +423,36 @@ __global__ void __launch_bounds__(NT, 1) k_resident_epoch(ResArgs<T> a) {
         sincos(ang, &sn, &cs);
         tw[i] = V{(T)cs, (T)(-sn)};
     }
+    if (tid == 0) mbar_init(bar, 1);
+    __syncthreads();
+    if (warp == 0 && (int)blockIdx.x < a.batch) stage(a, blockIdx.x, smem_raw, pb0, bar, lane);
 
-    for (int filt = blockIdx.x; filt < a.batch; filt += gridDim.x) {
-        const long long off = (long long)filt * (N * N);
-        T* Wf = a.W + off;
-        // ---------------------------------------------------------------- P0
-        if (warp == 0) {
-            const FilterState& f = a.st[filt];
-            double B[4] = {f.B[0], f.B[1], f.B[4], f.B[5]};
-            double c[2] = {f.c[0], f.c[1]};
-            double B0[4] = {B[0], B[1], B[2], B[3]}, c0[2] = {c[0], c[1]};
-            int skip = f.status != 0;
-            double detB = B[0] * B[3] - B[1] * B[2];
-            double Bi[4] = {B[3] / detB, -B[1] / detB, -B[2] / detB, B[0] / detB};
-            if (REGRID) {
-                const double v0 = f.cov[0], v1 = f.cov[5];
-                if (!(v0 > 0.0) || !(v1 > 0.0) || !isfinite(v0) || !isfinite(v1)) skip = 1;
-                c0[0] = f.mean[0];
-                c0[1] = f.mean[1];
-                B0[0] = 2.0 * a.ks * sqrt(v0) / N;
-                B0[1] = 0.0;
-                B0[2] = 0.0;
-                B0[3] = 2.0 * a.ks * sqrt(v1) / N;
-            }
-            if (lane == 0) {
-                sh->skip = skip;
-                if (REGRID) {
-                    // v = B^-1 (c0 + B0 u' - c) + (N-1)/2
-                    sh->M[0] = Bi[0] * B0[0] + Bi[1] * B0[2];
-                    sh->M[1] = Bi[0] * B0[1] + Bi[1] * B0[3];
-                    sh->M[2] = Bi[2] * B0[0] + Bi[3] * B0[2];
-                    sh->M[3] = Bi[2] * B0[1] + Bi[3] * B0[3];
-                    const double d0 = c0[0] - c[0], d1 = c0[1] - c[1];
-                    sh->o[0] = fma(Bi[0], d0, fma(Bi[1], d1, 0.5 * (N - 1)));
-                    sh->o[1] = fma(Bi[2], d0, fma(Bi[3], d1, 0.5 * (N - 1)));
-                }
-                const double* Mt = a.mp.Mtau;      // stride 4
-                double Bl[4], cl[2];
-                Bl[0] = fma(Mt[0], B0[0], Mt[1] * B0[2]);
-                Bl[1] = fma(Mt[0], B0[1], Mt[1] * B0[3]);
-                Bl[2] = fma(Mt[4], B0[0], Mt[5] * B0[2]);
-                Bl[3] = fma(Mt[4], B0[1], Mt[5] * B0[3]);
-                cl[0] = fma(Mt[0], c0[0], Mt[1] * c0[1]);
-                cl[1] = fma(Mt[4], c0[0], Mt[5] * c0[1]);
-                for (int q = 0; q < 4; ++q) sh->Bl[q] = Bl[q];
-                sh->cl[0] = cl[0];
-                sh->cl[1] = cl[1];
-                sh->vol_l = fabs(Bl[0] * Bl[3] - Bl[1] * Bl[2]);
-                sh->s_over_n2 = a.mp.s / (double)(N * N);
-                // likelihood: residual r(u) = (z - H c_l) - (H B_l) u relative to the moved grid
-                // centre; e(u) = r^T R^-1 r expanded as a quadratic form in u (eq:meas P:36, R13)
-                const LikParams& lp = a.lp;
-                sh->lognorm = lp.lognorm;
-                sh->inv_sigma = lp.inv_sigma;
-                if (UPDATE && lp.kind == 0) {
-                    const double* zf = a.z + (long long)filt * lp.nz;
-                    double r0[4], G0[4], G1[4];
-                    for (int i = 0; i < lp.nz; ++i) {
-                        const double h0 = lp.H[i * 4], h1 = lp.H[i * 4 + 1];
-                        r0[i] = zf[i] - fma(h0, cl[0], h1 * cl[1]);
-                        G0[i] = fma(h0, Bl[0], h1 * Bl[2]);
-                        G1[i] = fma(h0, Bl[1], h1 * Bl[3]);
-                    }
-                    double qa = 0, qb0 = 0, qb1 = 0, g00 = 0, g01 = 0, g11 = 0;
-                    for (int i = 0; i < lp.nz; ++i)
-                        for (int j = 0; j < lp.nz; ++j) {
-                            const double R = lp.Rinv[i * 4 + j];
-                            qa = fma(r0[i] * R, r0[j], qa);
-                            qb0 = fma(-2.0 * G0[i] * R, r0[j], qb0);
-                            qb1 = fma(-2.0 * G1[i] * R, r0[j], qb1);
-                            g00 = fma(G0[i] * R, G0[j], g00);
-                            g01 = fma(G0[i] * R, G1[j], g01);
-                            g11 = fma(G1[i] * R, G1[j], g11);
-                        }
-                    sh->qa = qa;
-                    sh->qb[0] = qb0;
-                    sh->qb[1] = qb1;
-                    sh->qG[0] = g00;
-                    sh->qG[1] = g01;
-                    sh->qG[2] = g11;
-                } else if (UPDATE) {
-                    sh->zr = a.z[filt];
-                }
-            }
-            // Euler-factor coefficients on the start-of-interval grid B0 (R3/R4)
-            const double det0 = B0[0] * B0[3] - B0[1] * B0[2];
-            const double Bi0[4] = {B0[3] / det0, -B0[1] / det0, -B0[2] / det0, B0[0] / det0};
-            for (int n = lane; n < l; n += 32) {
-                double D00, D01, D11;
-                if (a.mp.diff_mode == 0) {
-                    const double* E = a.sub[n].E;
-                    // T1 = Bi0 E, D = T1 Bi0^T
-                    const double t00 = fma(Bi0[0], E[0], Bi0[1] * E[4]);
-                    const double t01 = fma(Bi0[0], E[1], Bi0[1] * E[5]);
-                    const double t10 = fma(Bi0[2], E[0], Bi0[3] * E[4]);
-                    const double t11 = fma(Bi0[2], E[1], Bi0[3] * E[5]);
-                    D00 = fma(t00, Bi0[0], t01 * Bi0[1]);
-                    const double D01a = fma(t00, Bi0[2], t01 * Bi0[3]);
-                    const double D10a = fma(t10, Bi0[0], t11 * Bi0[1]);
-                    D01 = 0.5 * (D01a + D10a);
-                    D11 = fma(t10, Bi0[2], t11 * Bi0[3]);
-                } else {
-                    const double* P = a.sub[n].P;
-                    const double b00 = fma(P[0], B0[0], P[1] * B0[2]);
-                    const double b01 = fma(P[0], B0[1], P[1] * B0[3]);
-                    const double b10 = fma(P[4], B0[0], P[5] * B0[2]);
-                    const double b11 = fma(P[4], B0[1], P[5] * B0[3]);
-                    D00 = a.mp.Q[0] / fma(b00, b00, b10 * b10);
-                    D11 = a.mp.Q[5] / fma(b01, b01, b11 * b11);
-                    D01 = 0.0;
-                }
-                cf[3 * n] = (T)(0.5 * a.mp.dt * D00);
-                cf[3 * n + 1] = (T)(0.5 * a.mp.dt * D11);
-                cf[3 * n + 2] = (T)(a.mp.dt * D01);
-            }
-        }
-        __syncthreads();
-        if (sh->skip) {
-            if (tid == 0) a.st[filt].status = -6;
+    int it = 0;
+    for (int filt = blockIdx.x; filt < a.batch; filt += gridDim.x, ++it) {
+        T* Wf = a.W + (long long)filt * (N * N);
+        const double* P = pb0 + (it & 1) * a.pstride;
+        double* Pn = pb0 + ((it + 1) & 1) * a.pstride;
+        const int nxt = filt + gridDim.x;
+        mbar_wait(bar, it & 1);                 // weights + constants of this filter are in shared memory
+
+        if (P[P_SKIP] != 0.0) {                 // failed filter: leave it untouched
             __syncthreads();
+            if (warp == 0 && nxt < a.batch) stage(a, nxt, smem_raw, Pn, bar, lane);
             continue;
         }
-        // prefetch the next filter into L2 while this one computes
-        if (tid < 8) {
-            const int nf = filt + gridDim.x;
-            if (nf < a.batch) {
-                const char* p = reinterpret_cast<const char*>(a.W + (long long)nf * (N * N)) + tid * (N * N * sizeof(T) / 8);
-                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"((unsigned)(N * N * sizeof(T) / 8))
-                             : "memory");
-            }
-        }
-
-        // ---------------------------------------------------------------- P1: load / regrid, FFT along axis 1
+        // ---------------------------------------------------------------- P1: (regrid-)load, FFT along axis 1
         {
             V z[16];
             if (!REGRID) {
 #pragma unroll
                 for (int r = 0; r < 16; ++r) {
                     const int j1 = t + 8 * r;
-                    z[r] = *reinterpret_cast<const V*>(Wf + j1 * N + 2 * m);
+                    z[r] = *reinterpret_cast<const V*>(Xs + j1 * StagePitch<T>::B + 2 * m * sizeof(T));
                 }
             } else {
-                const double M0 = sh->M[0], M1 = sh->M[1], M2 = sh->M[2], M3 = sh->M[3];
-                const double o0 = sh->o[0], o1 = sh->o[1];
+                // multilinear interpolation of the old weights at the new points (R12), zero ghosts
+                const double M0 = P[P_M], M1 = P[P_M + 1], M2 = P[P_M + 2], M3 = P[P_M + 3];
+                const double o0 = P[P_O], o1 = P[P_O + 1];
 #pragma unroll
                 for (int r = 0; r < 16; ++r) {
                     const double u1 = (t + 8 * r) - 0.5 * (N - 1);
@@ -358,26 +464,24 @@ __global__ void __launch_bounds__(NT, 1) k_resident_epoch(ResArgs<T> a) {
                         const double v1 = fma(M2, u0, fma(M3, u1, o1));
                         const double f0 = floor(v0), f1 = floor(v1);
                         const double a0 = v0 - f0, a1 = v1 - f1;
-                        const int i0 = (int)fmax(fmin(f0, 4096.0), -4096.0);
-                        const int i1 = (int)fmax(fmin(f1, 4096.0), -4096.0);
-                        double acc = 0.0;
-                        const bool x0 = (unsigned)i0 < (unsigned)N, x1 = (unsigned)(i0 + 1) < (unsigned)N;
-                        const bool y0 = (unsigned)i1 < (unsigned)N, y1 = (unsigned)(i1 + 1) < (unsigned)N;
-                        const T* row0 = Wf + i1 * N;
-                        if (y0) {
-                            if (x0) acc = fma((1.0 - a0) * (1.0 - a1), (double)row0[i0], acc);
-                            if (x1) acc = fma(a0 * (1.0 - a1), (double)row0[i0 + 1], acc);
-                        }
-                        if (y1) {
-                            if (x0) acc = fma((1.0 - a0) * a1, (double)row0[N + i0], acc);
-                            if (x1) acc = fma(a0 * a1, (double)row0[N + i0 + 1], acc);
-                        }
-                        val[e] = (T)acc;
+                        const int i0 = __double2int_rz(f0), i1 = __double2int_rz(f1);   // saturating
+                        const bool x0 = (unsigned)i0 < (unsigned)N, x1 = (unsigned)i0 + 1u < (unsigned)N;
+                        const bool y0 = (unsigned)i1 < (unsigned)N, y1 = (unsigned)i1 + 1u < (unsigned)N;
+                        const T* row0 = reinterpret_cast<const T*>(Xs + i1 * (int)StagePitch<T>::B) + i0;
+                        const T* row1 = reinterpret_cast<const T*>(Xs + (i1 + 1) * (int)StagePitch<T>::B) + i0;
+                        const double w00 = (y0 && x0) ? (double)row0[0] : 0.0;
+                        const double w01 = (y0 && x1) ? (double)row0[1] : 0.0;
+                        const double w10 = (y1 && x0) ? (double)row1[0] : 0.0;
+                        const double w11 = (y1 && x1) ? (double)row1[1] : 0.0;
+                        const double lo = fma(a0, w01 - w00, w00);
+                        const double hi = fma(a0, w11 - w10, w10);
+                        val[e] = (T)fma(a1, hi - lo, lo);
                     }
                     z[r] = V{val[0], val[1]};
                 }
             }
-            dft16<false>(z);                       // over r: Y_t(s)
+            __syncthreads();                      // the staged weights are consumed: X is free
+            dft16<false>(z);                      // over r: Y_t(s)
 #pragma unroll
             for (int s = 1; s < 16; ++s) z[s] = cmul(z[s], tw[s * 8 + t]);
 #pragma unroll
@@ -389,18 +493,15 @@ __global__ void __launch_bounds__(NT, 1) k_resident_epoch(ResArgs<T> a) {
                 pa[tt] = X[cslot(sa, tt, m)];
                 pb[tt] = X[cslot(sb, tt, m)];
             }
-            dft8<false>(pa);                       // Z(sa + 16 q)
-            dft8<false>(pb);                       // Z(sb + 16 q)
+            dft8<false>(pa);                      // Z(sa + 16 q)
+            dft8<false>(pb);                      // Z(sb + 16 q)
             __syncwarp();
             // unpack the two real columns: Wa = (Z(k) + conj Z(-k))/2, Wb = (Z(k) - conj Z(-k))/(2i)
             auto store_pair = [&](int k1, V zk, V zp) {
-                const V wa = V{T(0.5) * (zk.x + zp.x), T(0.5) * (zk.y - zp.y)};
-                const V wb = V{T(0.5) * (zk.y + zp.y), T(0.5) * (zp.x - zk.x)};
-                X[k1 * PITCH + 2 * m] = wa;
-                X[k1 * PITCH + 2 * m + 1] = wb;
+                X[k1 * PITCH + 2 * m] = V{T(0.5) * (zk.x + zp.x), T(0.5) * (zk.y - zp.y)};
+                X[k1 * PITCH + 2 * m + 1] = V{T(0.5) * (zk.y + zp.y), T(0.5) * (zp.x - zk.x)};
             };
             if (t == 0) {
-                // s = 0: k = 16 q, partner 16 (8 - q) mod 128;  s = 8: k = 8 + 16 q, partner 8 + 16 (7 - q)
 #pragma unroll
                 for (int q = 0; q <= 4; ++q) store_pair(16 * q, pa[q], pa[(8 - q) & 7]);
 #pragma unroll
@@ -415,7 +516,7 @@ __global__ void __launch_bounds__(NT, 1) k_resident_epoch(ResArgs<T> a) {
         }
         __syncthreads();
 
-        // ---------------------------------------------------------------- P2: rows, FFT axis 0, Psi, inverse
+        // ---------------------------------------------------------------- P2: rows, FFT axis 0, s Psi / N^2, inverse
         {
             V x[16];
             V* row = X + m * PITCH;
@@ -442,14 +543,14 @@ __global__ void __launch_bounds__(NT, 1) k_resident_epoch(ResArgs<T> a) {
                 pa[tt] = row[rslot(sa, tt)];
                 pb[tt] = row[rslot(sb, tt)];
             }
-            dft8<false>(pa);                       // F(sa + 16 q)
+            dft8<false>(pa);                      // F(sa + 16 q)
             dft8<false>(pb);
-            // ---- spectral multiplier s Psi(k0, k1) / N^2  (Alg. 3-4)
-            const T sn2 = (T)sh->s_over_n2;
+            const T sn2 = (T)P[P_S];
             const T kscale = (T)(2.0 * 3.14159265358979323846 / N);
-            // ps[q] = s Psi(k0 = sv + 16 q, k1) / N^2; kappa = 2 pi k / N (signed k), the
-            // cross term uses kx = kappa with the Nyquist wavenumber zeroed (R7)
-            auto psi8 = [&](int k1, int sv, T* ps) {
+            const double* cfp = P + PRM_FIXED;
+            // ps[q] = s Psi(k0[q], k1) / N^2 with kappa = 2 pi k / N (signed k) and the
+            // cross term's kx = kappa with the Nyquist wavenumber zeroed (R7)
+            auto psi8 = [&](int k1, const int* k0, T* ps) {
                 const int k1s = k1 < N / 2 ? k1 : k1 - N;
                 const T kap1 = kscale * (T)k1s;
                 const T kx1 = (k1 == N / 2) ? T(0) : kap1;
@@ -457,62 +558,91 @@ __global__ void __launch_bounds__(NT, 1) k_resident_epoch(ResArgs<T> a) {
                 T kk[8], kx[8], den[8];
 #pragma unroll
                 for (int q = 0; q < 8; ++q) {
-                    const int k0 = sv + 16 * q;
-                    const int k0s = k0 < N / 2 ? k0 : k0 - N;
+                    const int k0s = k0[q] < N / 2 ? k0[q] : k0[q] - N;
                     const T kap0 = kscale * (T)k0s;
                     kk[q] = kap0 * kap0;
-                    kx[q] = (k0 == N / 2) ? T(0) : kap0;
+                    kx[q] = (k0[q] == N / 2) ? T(0) : kap0;
                     den[q] = T(1);
                 }
                 for (int n = 0; n < l; ++n) {
-                    const T ca = cf[3 * n], cb = cf[3 * n + 1], cc = cf[3 * n + 2];
+                    const T ca = (T)cfp[3 * n], cb = (T)cfp[3 * n + 1], cc = (T)cfp[3 * n + 2];
                     const T gam = fma(cb, k1sq, T(1));
                     const T bet = cc * kx1;
 #pragma unroll
                     for (int q = 0; q < 8; ++q) den[q] *= fma(ca, kk[q], fma(bet, kx[q], gam));
                 }
+                if constexpr (sizeof(T) == 8) {
+                    // one division for the 8 values (prefix products), unless the product leaves range
+                    T pre[8];
+                    pre[0] = den[0];
+#pragma unroll
+                    for (int q = 1; q < 8; ++q) pre[q] = pre[q - 1] * den[q];
+                    if (pre[7] < T(1e300)) {
+                        T inv = sn2 / pre[7];
+#pragma unroll
+                        for (int q = 7; q > 0; --q) {
+                            ps[q] = inv * pre[q - 1];
+                            inv *= den[q];
+                        }
+                        ps[0] = inv;
+                        return;
+                    }
+                }
 #pragma unroll
                 for (int q = 0; q < 8; ++q) ps[q] = sn2 / den[q];
             };
-            // packed rows k1 = 0 (A) and 64 (B): R(k) = A(k) + i B(k) with A, B Hermitian;
-            // A(k) = (R(k) + conj R(-k))/2, B(k) = (R(k) - conj R(-k))/(2i). After the
-            // multiply R'(k) = A'(k) + i B'(k), R'(-k) = conj A'(k) + i conj B'(k).
+            // packed rows k1 = 0 (A) and 64 (B): R = A + i B with A, B Hermitian in k0.
+            // A(k) = (R(k) + conj R(-k))/2, B(k) = (R(k) - conj R(-k))/(2i); after the multiply
+            // R'(k) = A'(k) + i B'(k), R'(-k) = conj A'(k) + i conj B'(k).
             auto packed = [&](V& rk, V& rm, bool self, T pA, T pB, bool is_dc) {
                 const V R = rk, Rm = rm;
                 V A = V{T(0.5) * (R.x + Rm.x), T(0.5) * (R.y - Rm.y)};
                 V Bv = V{T(0.5) * (R.y + Rm.y), T(0.5) * (Rm.x - R.x)};
-                if (is_dc) sh->dc = (double)A.x;           // sum of the input weights (k = 0)
+                if (is_dc) *dcs = (double)A.x;    // sum of the input weights (k = 0)
                 A = V{A.x * pA, A.y * pA};
                 Bv = V{Bv.x * pB, Bv.y * pB};
                 rk = V{A.x - Bv.y, A.y + Bv.x};
                 if (!self) rm = V{A.x + Bv.y, Bv.x - A.y};
             };
-            if (m != 0) {
-                T ps[8];
-                psi8(m, sa, ps);
+            // every thread evaluates the multiplier on two lists of 8 wavenumbers:
+            //   rows m > 0: (k1 = m, k0 = sa + 16 q) and (k1 = m, k0 = sb + 16 q);
+            //   team 0 (rows 0 and 64 packed): one k0 per Hermitian pair -- thread t > 0 owns
+            //   k0 = t + 16 q, thread 0 owns 16 q and 8 + 16 q (q < 4) + the Nyquist k0 = 64 below.
+            int kx_[8], ky_[8];
 #pragma unroll
-                for (int q = 0; q < 8; ++q) pa[q] = V{pa[q].x * ps[q], pa[q].y * ps[q]};
-                psi8(m, sb, ps);
-#pragma unroll
-                for (int q = 0; q < 8; ++q) pb[q] = V{pb[q].x * ps[q], pb[q].y * ps[q]};
-            } else if (t != 0) {
-                T pA[8], pB[8];
-                psi8(0, sa, pA);
-                psi8(N / 2, sa, pB);
-#pragma unroll
-                for (int q = 0; q < 8; ++q) packed(pa[q], pb[7 - q], false, pA[q], pB[q], false);
-            } else {
-                T pA[8], pB[8];
-                psi8(0, 0, pA);                    // s = 0: k0 = 16 q, partner 16 (8 - q) mod 128
-                psi8(N / 2, 0, pB);
-#pragma unroll
-                for (int q = 0; q <= 4; ++q) packed(pa[q], pa[(8 - q) & 7], q == 0 || q == 4, pA[q], pB[q], q == 0);
-                psi8(0, 8, pA);                    // s = 8: k0 = 8 + 16 q, partner 8 + 16 (7 - q)
-                psi8(N / 2, 8, pB);
-#pragma unroll
-                for (int q = 0; q < 4; ++q) packed(pb[q], pb[7 - q], false, pA[q], pB[q], false);
+            for (int q = 0; q < 8; ++q) {
+                const int kl = (t == 0) ? ((q < 4) ? 16 * q : 8 + 16 * (q - 4)) : sa + 16 * q;
+                kx_[q] = (m != 0) ? sa + 16 * q : kl;
+                ky_[q] = (m != 0) ? sb + 16 * q : kl;
             }
-            dft8<true>(pa);                        // G_s(t'')
+            T px[8], py[8];
+            psi8(m, kx_, px);                        // team 0: row k1 = 0
+            psi8(m != 0 ? m : N / 2, ky_, py);       // team 0: row k1 = 64
+            if (m != 0) {
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    pa[q] = V{pa[q].x * px[q], pa[q].y * px[q]};
+                    pb[q] = V{pb[q].x * py[q], pb[q].y * py[q]};
+                }
+            } else if (t != 0) {
+#pragma unroll
+                for (int q = 0; q < 8; ++q) packed(pa[q], pb[7 - q], false, px[q], py[q], false);
+            } else {
+                // k0 = 64 (self-paired, both rows): scalar Euler product
+                T dA = T(1), dB = T(1);
+                const T kN = kscale * (T)(-N / 2);
+                for (int n = 0; n < l; ++n) {
+                    const T ca = (T)cfp[3 * n], cb = (T)cfp[3 * n + 1];
+                    dA *= fma(ca, kN * kN, T(1));
+                    dB *= fma(ca, kN * kN, fma(cb, kN * kN, T(1)));
+                }
+#pragma unroll
+                for (int q = 0; q < 4; ++q) packed(pa[q], pa[(8 - q) & 7], q == 0, px[q], py[q], q == 0);
+                packed(pa[4], pa[4], true, sn2 / dA, sn2 / dB, false);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) packed(pb[q], pb[7 - q], false, px[4 + q], py[4 + q], false);
+            }
+            dft8<true>(pa);                       // G_s(t'')
             dft8<true>(pb);
             __syncwarp();
 #pragma unroll
@@ -549,12 +679,12 @@ __global__ void __launch_bounds__(NT, 1) k_resident_epoch(ResArgs<T> a) {
         {
             V pa[8], pb[8];
             auto ld = [&](int k1, int col) -> V { return X[k1 * PITCH + 2 * m + col]; };
-            // Z(k) = Wa(k) + i Wb(k); for k > 64: Wa(k) = conj Wa(128 - k)
+            // Z(k) = Wa(k) + i Wb(k); for k > 64, Wa(k) = conj Wa(128 - k)
             auto zdir = [&](int k1) -> V {
                 const V wa = ld(k1, 0), wb = ld(k1, 1);
                 return V{wa.x - wb.y, wa.y + wb.x};
             };
-            auto zmir = [&](int kp) -> V {     // Z(128 - kp) from the stored kp <= 64
+            auto zmir = [&](int kp) -> V {
                 const V wa = ld(kp, 0), wb = ld(kp, 1);
                 return V{wa.x + wb.y, wb.x - wa.y};
             };
@@ -582,29 +712,25 @@ __global__ void __launch_bounds__(NT, 1) k_resident_epoch(ResArgs<T> a) {
             V x[16];
 #pragma unroll
             for (int s = 0; s < 16; ++s) x[s] = X[cslot(s, t, m)];
+            const double lgn = P[P_LGN];
+            double pe[2], qe[2];
+            const double g11 = P[P_QG + 2];
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const double u0 = (2 * m + e) - 0.5 * (N - 1);
+                pe[e] = fma(u0, fma(P[P_QG], u0, P[P_QB]), P[P_QA]);
+                qe[e] = fma(2.0 * P[P_QG + 1], u0, P[P_QB + 1]);
+            }
+            __syncthreads();                      // X is consumed
+            if (warp == 0 && nxt < a.batch) stage(a, nxt, smem_raw, Pn, bar, lane);   // overlaps the rest of P3
 #pragma unroll
             for (int s = 1; s < 16; ++s) {
                 V w = tw[s * 8 + t];
                 w.y = -w.y;
                 x[s] = cmul(x[s], w);
             }
-            dft16<true>(x);                        // x[r] = w(2m, t+8r) + i w(2m+1, t+8r)
-            // Alg. 6: sum of the predicted weights = s * DC  ->  normalised = w / (vol_l s DC)
-            const double scale_pred = 1.0 / (sh->vol_l * a.mp.s * sh->dc);
+            dft16<true>(x);                       // x[r] = w(2m, t+8r) + i w(2m+1, t+8r) (unnormalised)
             double acc[6] = {0, 0, 0, 0, 0, 0};
-            const double Bl0 = sh->Bl[0], Bl1 = sh->Bl[1], Bl2 = sh->Bl[2], Bl3 = sh->Bl[3];
-            const double cl0 = sh->cl[0], cl1 = sh->cl[1];
-            const bool range = a.lp.kind == 1;
-            const double lgn = sh->lognorm;
-            // linear-Gauss exponent along this thread's two columns: e = p_e + u1 (q_e + G11 u1)
-            double pe[2], qe[2];
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-                const double u0 = (2 * m + e) - 0.5 * (N - 1);
-                pe[e] = fma(u0, fma(sh->qG[0], u0, sh->qb[0]), sh->qa);
-                qe[e] = fma(2.0 * sh->qG[1], u0, sh->qb[1]);
-            }
-            const double g11 = sh->qG[2];
 #pragma unroll
             for (int r = 0; r < 16; ++r) {
                 const int j1 = t + 8 * r;
@@ -613,19 +739,21 @@ __global__ void __launch_bounds__(NT, 1) k_resident_epoch(ResArgs<T> a) {
 #pragma unroll
                 for (int e = 0; e < 2; ++e) {
                     const double u0 = (2 * m + e) - 0.5 * (N - 1);
-                    double w = (double)(e == 0 ? x[r].x : x[r].y);
+                    const double w = (double)(e == 0 ? x[r].x : x[r].y);
                     if (UPDATE) {
                         double ee;
-                        if (!range) {
+                        if (!a.range) {
                             ee = fma(u1, fma(g11, u1, qe[e]), pe[e]);
                         } else {
-                            const double x0 = fma(Bl0, u0, fma(Bl1, u1, cl0));
-                            const double x1 = fma(Bl2, u0, fma(Bl3, u1, cl1));
-                            const double d = (sh->zr - sqrt(fma(x0, x0, x1 * x1))) * sh->inv_sigma;
+                            // range likelihood: constants re-read from shared memory (P stays valid:
+                            // the next filter is staged into the other parameter buffer)
+                            const double y0 = fma(P[P_BL], u0, fma(P[P_BL + 1], u1, P[P_CL]));
+                            const double y1 = fma(P[P_BL + 2], u0, fma(P[P_BL + 3], u1, P[P_CL + 1]));
+                            const double d = (P[P_ZR] - sqrt(fma(y0, y0, y1 * y1))) * P[P_ISG];
                             ee = d * d;
                         }
-                        w = w * scale_pred * exp(fma(-0.5, ee, lgn));
-                        const T wt = (T)w;
+                        // unnormalised prior x likelihood; the normalisation is one scalar per filter
+                        const T wt = (T)(w * exp_fast(fma(-0.5, ee, lgn)));
                         outv[e] = wt;
                         const double wd = (double)wt;
                         acc[0] += wd;
@@ -652,41 +780,14 @@ __global__ void __launch_bounds__(NT, 1) k_resident_epoch(ResArgs<T> a) {
                     for (int i = 0; i < 6; ++i) red[warp * 6 + i] = acc[i];
             }
             __syncthreads();
-            if (tid == 0) {
-                FilterState& f = a.st[filt];
-                f.c[0] = sh->cl[0];
-                f.c[1] = sh->cl[1];
-                f.B[0] = sh->Bl[0];
-                f.B[1] = sh->Bl[1];
-                f.B[4] = sh->Bl[2];
-                f.B[5] = sh->Bl[3];
-                if (UPDATE) {
-                    double s6[6];
-                    for (int i = 0; i < 6; ++i) {
-                        double s = 0.0;
-                        for (int w = 0; w < NT / 32; ++w) s += red[w * 6 + i];
-                        s6[i] = s;
-                    }
-                    const double C = sh->vol_l * s6[0];
-                    f.mass = s6[0];
-                    f.has_moments = 1;
-                    if (!(C > 0.0) || !isfinite(C)) {
-                        f.status = -6;
-                        f.logC = -INFINITY;
-                    } else {
-                        f.status = 0;
-                        f.logC = log(C);
-                        f.scale = 1.0 / C;
-                        double acc15[NMOM];
-                        for (int i = 0; i < NMOM; ++i) acc15[i] = 0.0;
-                        for (int i = 0; i < 6; ++i) acc15[i] = s6[i];
-                        finish_moments(nx, acc15, f.c, f.B, f.mean, f.cov);
-                    }
-                } else {
-                    f.scale = scale_pred;
-                }
+            if (warp == 0) {
+                // per-filter sums in a fixed order (deterministic); the scalar work is in k_res_finalize
+                double v = 0.0;
+                if (UPDATE && lane < 6)
+                    for (int w = 0; w < NT / 32; ++w) v += red[w * 6 + lane];
+                if (lane == 6) v = *dcs;
+                if (lane < 7) a.out[(long long)filt * 8 + lane] = v;
             }
-            __syncthreads();
         }
     }
 }
@@ -696,58 +797,62 @@ bool resident_supported(const Dims& d, int dtype) {
     return d.nx == 2 && d.n[0] == N && d.n[1] == N;
 }
 
+size_t resident_param_bytes(int l, int batch) { return sizeof(double) * (size_t)prm_stride(l) * batch; }
+
 template <typename T, bool RG, bool UP>
 static cudaError_t launch_t(ResArgs<T> a, cudaStream_t s, int64_t* launches) {
     using V = typename C2<T>::type;
-    const size_t smem = sizeof(V) * (H * PITCH + 128) + sizeof(Shared) + 16 * 6 * sizeof(double) +
-                        3 * sizeof(T) * (size_t)a.mp.l + 64;
+    const size_t smem = sizeof(V) * (H * PITCH + 128) + 16 * 6 * sizeof(double) + 2 * sizeof(double) +
+                        2 * sizeof(unsigned long long) + 2 * sizeof(double) * (size_t)a.pstride;
     auto kern = k_resident_epoch<T, RG, UP>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) { fprintf(stderr, "[pmf] resident setattr smem=%zu: %s\n", smem, cudaGetErrorString(e)); return e; }
+    if (e != cudaSuccess) return e;
     int dev = 0, nsm = 148, occ = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, smem);
-    if (e != cudaSuccess) { fprintf(stderr, "[pmf] resident occupancy: %s\n", cudaGetErrorString(e)); return e; }
+    if (e != cudaSuccess) return e;
     if (occ < 1) return cudaErrorInvalidConfiguration;
     const int grid = std::min(a.batch, nsm * occ);
     kern<<<grid, NT, smem, s>>>(a);
     ++*launches;
-    e = cudaGetLastError();
-    if (e != cudaSuccess) {
-        cudaFuncAttributes fa;
-        cudaFuncGetAttributes(&fa, kern);
-        fprintf(stderr, "[pmf] resident launch grid=%d occ=%d smem=%zu regs=%d local=%zu maxthr=%d: %s\n", grid, occ, smem,
-                fa.numRegs, fa.localSizeBytes, fa.maxThreadsPerBlock, cudaGetErrorString(e));
-    }
-    return e;
+    return cudaGetLastError();
 }
 
 template <typename T>
-static cudaError_t launch_dt(const Dims& d, PencilBufs& b, const ModelParams* mp, const LikParams* lp, double ks,
+static cudaError_t launch_dt(const Dims& d, PencilBufs& b, const ModelParams& mp, const LikParams* lp, double ks,
                              cudaStream_t s, int64_t* launches) {
+    const int ps = prm_stride(mp.l);
+    LikParams lpv = lp ? *lp : LikParams{};
+    k_res_prep<<<(d.batch + 127) / 128, 128, 0, s>>>(b.st, b.coef, ps, mp, b.sub, lpv, b.z, ks, lp ? 1 : 0, d.batch);
+    ++*launches;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
     ResArgs<T> a;
     a.W = (T*)b.W;
-    a.st = b.st;
-    a.z = b.z;
-    a.sub = b.sub;
-    a.mp = *mp;
-    a.lp = lp ? *lp : LikParams{};
-    a.ks = ks;
+    a.prm = b.coef;
+    a.out = b.partials;
+    a.pstride = ps;
+    a.l = mp.l;
     a.batch = d.batch;
+    a.range = lpv.kind == 1;
     const bool rg = ks > 0.0;
-    if (rg && lp) return launch_t<T, true, true>(a, s, launches);
-    if (rg) return launch_t<T, true, false>(a, s, launches);
-    if (lp) return launch_t<T, false, true>(a, s, launches);
-    return launch_t<T, false, false>(a, s, launches);
+    if (rg && lp) e = launch_t<T, true, true>(a, s, launches);
+    else if (rg) e = launch_t<T, true, false>(a, s, launches);
+    else if (lp) e = launch_t<T, false, true>(a, s, launches);
+    else e = launch_t<T, false, false>(a, s, launches);
+    if (e != cudaSuccess) return e;
+    k_res_finalize<<<(d.batch + 127) / 128, 128, 0, s>>>(b.st, b.partials, b.coef, ps, mp.s, lp ? 1 : 0, d.batch);
+    ++*launches;
+    return cudaGetLastError();
 }
 
 cudaError_t launch_resident(const Dims& d, int dtype, PencilBufs& b, const Twiddles& tw, const ModelParams* mp,
                             const LikParams* lp, double ks, cudaStream_t s, int64_t* launches) {
     (void)tw;
     if (!mp) return cudaErrorInvalidValue;      // the host routes update-/regrid-only work to the point kernels
-    if (dtype == 0) return launch_dt<double>(d, b, mp, lp, ks, s, launches);
-    return launch_dt<float>(d, b, mp, lp, ks, s, launches);
+    if (dtype == 0) return launch_dt<double>(d, b, *mp, lp, ks, s, launches);
+    return launch_dt<float>(d, b, *mp, lp, ks, s, launches);
 }
 
 }  // namespace pmf

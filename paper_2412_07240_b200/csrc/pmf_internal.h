@@ -60,7 +60,8 @@ struct Dims {
 };
 
 // Number of doubles per filter in the pencil path's epoch-coefficient buffer.
-inline int coef_stride(int l) { return 4 + 10 * l; }
+// pencil path: 4 + 10 l; resident path: 24 + 3 l rounded up to even (kernels_resident.cu)
+inline int coef_stride(int l) { return (4 + 10 * l) > (26 + 3 * l) ? (4 + 10 * l) : (26 + 3 * l); }
 
 // ---------------------------------------------------------------------------
 // launchers (implemented in the .cu files); all return a cudaError_t and
