@@ -143,6 +143,10 @@ __device__ __forceinline__ void dft8(V* x) {
     x[7] = csub(a3, b3);
 }
 
+// Spectrum element (k1, j0) lives at X[k1 * PITCH + xcol(k1, j0)]: the two columns of a
+// pair swap places in rows with (k1 & 4), so the 8 threads of a team touching rows
+// t + 16 q of one column hit 8 distinct 16-byte bank groups (PITCH = 2 mod 8).
+__device__ __forceinline__ int xcol(int k1, int j0) { return j0 ^ ((k1 >> 2) & 1); }
 // exchange slot of element (s, t) inside a row (128 consecutive complex)
 __device__ __forceinline__ int rslot(int s, int t) { return s * 8 + (t ^ (s & 7)); }
 // exchange slot of element (s, t) inside the column pair of a team: (row, col)
@@ -375,9 +379,37 @@ struct ResArgs {
 
 // Staging row pitch in bytes for the weights (padded so the regrid gather's 8
 // rows per team hit distinct banks; 16-byte aligned for the bulk copies).
+// Staged weights: row j1 in [-1, 129] at byte (j1 + 1) * B, column j0 in [-1, 129] at
+// byte (j0 + OFF) * sizeof(T). The ring j = -1, 128, 129 is zero (the zero ghost nodes
+// of R12), the pitch B makes the 8 rows a team gathers from fall in distinct banks, and
+// (OFF * sizeof(T)) keeps every interior row 16-byte aligned for the bulk copies.
 template <typename T> struct StagePitch;
-template <> struct StagePitch<double> { static constexpr unsigned B = 130 * 8; };
-template <> struct StagePitch<float> { static constexpr unsigned B = 132 * 4; };
+template <> struct StagePitch<double> { static constexpr unsigned B = 134 * 8; static constexpr int OFF = 2; };
+template <> struct StagePitch<float> { static constexpr unsigned B = 140 * 4; static constexpr int OFF = 4; };
+constexpr int STAGE_ROWS = N + 3;
+template <typename T> __host__ __device__ constexpr unsigned stage_bytes() { return STAGE_ROWS * StagePitch<T>::B; }
+
+// zero the ghost ring of the staging area (called by all threads)
+template <typename T>
+__device__ __forceinline__ void zero_ring(void* Xr, int tid) {
+    char* base = reinterpret_cast<char*>(Xr);
+    constexpr int W = N + 3;                       // columns j0 = -1 .. 129 (+1 alignment slot)
+    // rows -1, 128, 129: all columns; rows 0..127: columns -1, 128, 129
+    for (int i = tid; i < 3 * W + 3 * N; i += NT) {
+        int row, col;
+        if (i < 3 * W) {
+            const int rr = i / W;
+            row = rr == 0 ? -1 : N - 1 + rr;
+            col = i - rr * W - 1;
+        } else {
+            const int k = i - 3 * W;
+            row = k / 3;
+            const int cc = k - 3 * row;
+            col = cc == 0 ? -1 : N - 1 + cc;
+        }
+        *reinterpret_cast<T*>(base + (row + 1) * StagePitch<T>::B + (col + StagePitch<T>::OFF) * sizeof(T)) = T(0);
+    }
+}
 
 // Stage filter `filt` (called by all of warp 0): its 128 weight rows into the X
 // region at pitch StagePitch, and its constants into pbuf, completing on `bar`.
@@ -393,7 +425,8 @@ __device__ __forceinline__ void stage(const ResArgs<T>& a, int filt, void* Xr, d
     __syncwarp();
     const char* src = reinterpret_cast<const char*>(a.W + (long long)filt * (N * N));
     for (int r = lane; r < N; r += 32)
-        bulk_g2s(reinterpret_cast<char*>(Xr) + r * StagePitch<T>::B, src + r * RB, RB, bar);
+        bulk_g2s(reinterpret_cast<char*>(Xr) + (r + 1) * StagePitch<T>::B + StagePitch<T>::OFF * sizeof(T), src + r * RB,
+                 RB, bar);
     if (lane == 0) bulk_g2s(pbuf, a.prm + (long long)filt * a.pstride, pbytes, bar);
 }
 
@@ -403,8 +436,10 @@ __global__ void __launch_bounds__(NT, 1) k_resident_epoch(ResArgs<T> a) {
     using V = typename C2<T>::type;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     V* X = reinterpret_cast<V*>(smem_raw);                          // [H][PITCH]; also the dense staging area
-    const char* Xs = reinterpret_cast<const char*>(smem_raw);       // staged weights, row j1 at j1 * StagePitch
-    V* tw = X + H * PITCH;                                          // [16][8]  W128^{ts}
+    // staged weights: element (j0, j1) at Xs + j1 * StagePitch + j0 * sizeof(T), j0, j1 in [-1, 129]
+    const char* Xs = reinterpret_cast<const char*>(smem_raw) + StagePitch<T>::B + StagePitch<T>::OFF * sizeof(T);
+    constexpr unsigned XBYTES = (sizeof(V) * H * PITCH > stage_bytes<T>()) ? sizeof(V) * H * PITCH : stage_bytes<T>();
+    V* tw = reinterpret_cast<V*>(smem_raw + XBYTES);                // [16][8]  W128^{ts}
     double* red = reinterpret_cast<double*>(tw + 128);              // [16 warps][6]
     double* dcs = red + 16 * 6;                                     // DC of the current filter
     unsigned long long* bar = reinterpret_cast<unsigned long long*>(dcs + 2);
@@ -424,6 +459,7 @@ __global__ void __launch_bounds__(NT, 1) k_resident_epoch(ResArgs<T> a) {
         tw[i] = V{(T)cs, (T)(-sn)};
     }
     if (tid == 0) mbar_init(bar, 1);
+    zero_ring<T>(smem_raw, tid);
     __syncthreads();
     if (warp == 0 && (int)blockIdx.x < a.batch) stage(a, blockIdx.x, smem_raw, pb0, bar, lane);
 
@@ -447,7 +483,7 @@ __global__ void __launch_bounds__(NT, 1) k_resident_epoch(ResArgs<T> a) {
 #pragma unroll
                 for (int r = 0; r < 16; ++r) {
                     const int j1 = t + 8 * r;
-                    z[r] = *reinterpret_cast<const V*>(Xs + j1 * StagePitch<T>::B + 2 * m * sizeof(T));
+                    z[r] = *reinterpret_cast<const V*>(Xs + j1 * (int)StagePitch<T>::B + 2 * m * (int)sizeof(T));
                 }
             } else {
                 // multilinear interpolation of the old weights at the new points (R12), zero ghosts
@@ -462,17 +498,15 @@ __global__ void __launch_bounds__(NT, 1) k_resident_epoch(ResArgs<T> a) {
                         const double u0 = (2 * m + e) - 0.5 * (N - 1);
                         const double v0 = fma(M0, u0, fma(M1, u1, o0));
                         const double v1 = fma(M2, u0, fma(M3, u1, o1));
-                        const double f0 = floor(v0), f1 = floor(v1);
-                        const double a0 = v0 - f0, a1 = v1 - f1;
-                        const int i0 = __double2int_rz(f0), i1 = __double2int_rz(f1);   // saturating
-                        const bool x0 = (unsigned)i0 < (unsigned)N, x1 = (unsigned)i0 + 1u < (unsigned)N;
-                        const bool y0 = (unsigned)i1 < (unsigned)N, y1 = (unsigned)i1 + 1u < (unsigned)N;
+                        // clamp to [-1, 128]: outside, every tap is a zero ghost or has weight 0
+                        const double c0 = fmin(fmax(v0, -1.0), (double)N), c1 = fmin(fmax(v1, -1.0), (double)N);
+                        const double f0 = floor(c0), f1 = floor(c1);
+                        const double a0 = c0 - f0, a1 = c1 - f1;
+                        const int i0 = (int)f0, i1 = (int)f1;
                         const T* row0 = reinterpret_cast<const T*>(Xs + i1 * (int)StagePitch<T>::B) + i0;
-                        const T* row1 = reinterpret_cast<const T*>(Xs + (i1 + 1) * (int)StagePitch<T>::B) + i0;
-                        const double w00 = (y0 && x0) ? (double)row0[0] : 0.0;
-                        const double w01 = (y0 && x1) ? (double)row0[1] : 0.0;
-                        const double w10 = (y1 && x0) ? (double)row1[0] : 0.0;
-                        const double w11 = (y1 && x1) ? (double)row1[1] : 0.0;
+                        const T* row1 = reinterpret_cast<const T*>(reinterpret_cast<const char*>(row0) + StagePitch<T>::B);
+                        const double w00 = (double)row0[0], w01 = (double)row0[1];
+                        const double w10 = (double)row1[0], w11 = (double)row1[1];
                         const double lo = fma(a0, w01 - w00, w00);
                         const double hi = fma(a0, w11 - w10, w10);
                         val[e] = (T)fma(a1, hi - lo, lo);
@@ -498,8 +532,8 @@ __global__ void __launch_bounds__(NT, 1) k_resident_epoch(ResArgs<T> a) {
             __syncwarp();
             // unpack the two real columns: Wa = (Z(k) + conj Z(-k))/2, Wb = (Z(k) - conj Z(-k))/(2i)
             auto store_pair = [&](int k1, V zk, V zp) {
-                X[k1 * PITCH + 2 * m] = V{T(0.5) * (zk.x + zp.x), T(0.5) * (zk.y - zp.y)};
-                X[k1 * PITCH + 2 * m + 1] = V{T(0.5) * (zk.y + zp.y), T(0.5) * (zp.x - zk.x)};
+                X[k1 * PITCH + xcol(k1, 2 * m)] = V{T(0.5) * (zk.x + zp.x), T(0.5) * (zk.y - zp.y)};
+                X[k1 * PITCH + xcol(k1, 2 * m + 1)] = V{T(0.5) * (zk.y + zp.y), T(0.5) * (zp.x - zk.x)};
             };
             if (t == 0) {
 #pragma unroll
@@ -528,7 +562,7 @@ __global__ void __launch_bounds__(NT, 1) k_resident_epoch(ResArgs<T> a) {
                 }
             } else {
 #pragma unroll
-                for (int r = 0; r < 16; ++r) x[r] = row[t + 8 * r];
+                for (int r = 0; r < 16; ++r) x[r] = row[xcol(m, t + 8 * r)];
             }
             dft16<false>(x);
 #pragma unroll
@@ -670,7 +704,7 @@ __global__ void __launch_bounds__(NT, 1) k_resident_epoch(ResArgs<T> a) {
                 }
             } else {
 #pragma unroll
-                for (int r = 0; r < 16; ++r) row[t + 8 * r] = x[r];
+                for (int r = 0; r < 16; ++r) row[xcol(m, t + 8 * r)] = x[r];
             }
         }
         __syncthreads();
@@ -678,7 +712,7 @@ __global__ void __launch_bounds__(NT, 1) k_resident_epoch(ResArgs<T> a) {
         // ---------------------------------------------------------------- P3: inverse axis 1, normalise, update
         {
             V pa[8], pb[8];
-            auto ld = [&](int k1, int col) -> V { return X[k1 * PITCH + 2 * m + col]; };
+            auto ld = [&](int k1, int col) -> V { return X[k1 * PITCH + xcol(k1, 2 * m + col)]; };
             // Z(k) = Wa(k) + i Wb(k); for k > 64, Wa(k) = conj Wa(128 - k)
             auto zdir = [&](int k1) -> V {
                 const V wa = ld(k1, 0), wb = ld(k1, 1);
@@ -722,6 +756,7 @@ __global__ void __launch_bounds__(NT, 1) k_resident_epoch(ResArgs<T> a) {
                 qe[e] = fma(2.0 * P[P_QG + 1], u0, P[P_QB + 1]);
             }
             __syncthreads();                      // X is consumed
+            zero_ring<T>(smem_raw, tid);          // visible to the gather after the end-of-filter barrier
             if (warp == 0 && nxt < a.batch) stage(a, nxt, smem_raw, Pn, bar, lane);   // overlaps the rest of P3
 #pragma unroll
             for (int s = 1; s < 16; ++s) {
@@ -730,44 +765,103 @@ __global__ void __launch_bounds__(NT, 1) k_resident_epoch(ResArgs<T> a) {
                 x[s] = cmul(x[s], w);
             }
             dft16<true>(x);                       // x[r] = w(2m, t+8r) + i w(2m+1, t+8r) (unnormalised)
-            double acc[6] = {0, 0, 0, 0, 0, 0};
-#pragma unroll
-            for (int r = 0; r < 16; ++r) {
-                const int j1 = t + 8 * r;
-                const double u1 = j1 - 0.5 * (N - 1);
-                T outv[2];
+            // Likelihood (linear Gauss): along this thread's column e the exponent is a quadratic
+            // in r (u1 = u1_0 + 8 r): E(r) = E0 + E1 r + E2 r^2, so L(r+1) = L(r) R(r) and
+            // R(r+1) = R(r) exp(2 E2) -- two multiplies per point. Used when every partial
+            // exponent stays inside the fp64 range (|E0| + 15|E1| + 225|E2| < 650; each step
+            // adds at most one rounding, < 16 ulp in total); otherwise exp per point.
+            double Lr[2], Rr[2], Gr[2];
+            bool rec = UPDATE && !a.range;
+            if (UPDATE && !a.range) {
+                const double u10 = t - 0.5 * (N - 1);
 #pragma unroll
                 for (int e = 0; e < 2; ++e) {
-                    const double u0 = (2 * m + e) - 0.5 * (N - 1);
-                    const double w = (double)(e == 0 ? x[r].x : x[r].y);
-                    if (UPDATE) {
-                        double ee;
-                        if (!a.range) {
-                            ee = fma(u1, fma(g11, u1, qe[e]), pe[e]);
-                        } else {
-                            // range likelihood: constants re-read from shared memory (P stays valid:
-                            // the next filter is staged into the other parameter buffer)
-                            const double y0 = fma(P[P_BL], u0, fma(P[P_BL + 1], u1, P[P_CL]));
-                            const double y1 = fma(P[P_BL + 2], u0, fma(P[P_BL + 3], u1, P[P_CL + 1]));
-                            const double d = (P[P_ZR] - sqrt(fma(y0, y0, y1 * y1))) * P[P_ISG];
-                            ee = d * d;
+                    const double base = fma(-0.5, pe[e], lgn);
+                    const double E0 = fma(-0.5, u10 * fma(g11, u10, qe[e]), base);
+                    const double E1 = -0.5 * (8.0 * qe[e] + 16.0 * g11 * u10);
+                    const double E2 = -32.0 * g11;
+                    rec = rec && (fabs(E0) + 15.0 * fabs(E1) + 225.0 * fabs(E2) < 650.0);
+                    Lr[e] = exp_fast(E0);
+                    Rr[e] = exp_fast(E1 + E2);
+                    Gr[e] = exp_fast(2.0 * E2);
+                }
+            }
+            // moments per column: S = sum w, Tm = sum w u1, U = sum w u1^2 (u0 is fixed per column)
+            double S[2] = {0, 0}, Tm[2] = {0, 0}, U[2] = {0, 0};
+            auto emit = [&](int r, int e, double w) -> T {
+                const T wt = (T)w;
+                if (UPDATE) {
+                    const double u1 = (t + 8 * r) - 0.5 * (N - 1);
+                    const double wd = (double)wt;
+                    const double wu = wd * u1;
+                    S[e] += wd;
+                    Tm[e] += wu;
+                    U[e] = fma(wu, u1, U[e]);
+                }
+                return wt;
+            };
+            if (!UPDATE) {
+#pragma unroll
+                for (int r = 0; r < 16; ++r)
+                    *reinterpret_cast<V*>(Wf + (t + 8 * r) * N + 2 * m) = V{(T)(double)x[r].x, (T)(double)x[r].y};
+            } else if (rec) {
+#pragma unroll
+                for (int r = 0; r < 16; ++r) {
+                    const T o0 = emit(r, 0, (double)x[r].x * Lr[0]);
+                    const T o1 = emit(r, 1, (double)x[r].y * Lr[1]);
+                    Lr[0] *= Rr[0];
+                    Rr[0] *= Gr[0];
+                    Lr[1] *= Rr[1];
+                    Rr[1] *= Gr[1];
+                    *reinterpret_cast<V*>(Wf + (t + 8 * r) * N + 2 * m) = V{o0, o1};
+                }
+            } else {
+#pragma unroll 1
+                for (int rr = 0; rr < 16; rr += 4) {
+                    // generic path (range likelihood or extreme exponents): exp per point; the
+                    // register array is indexed statically through the inner unrolled switch
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        V xv;
+                        switch (rr + q) {
+#define PMF_X(i) case i: xv = x[i]; break;
+                            PMF_X(0) PMF_X(1) PMF_X(2) PMF_X(3) PMF_X(4) PMF_X(5) PMF_X(6) PMF_X(7)
+                            PMF_X(8) PMF_X(9) PMF_X(10) PMF_X(11) PMF_X(12) PMF_X(13) PMF_X(14) PMF_X(15)
+#undef PMF_X
                         }
-                        // unnormalised prior x likelihood; the normalisation is one scalar per filter
-                        const T wt = (T)(w * exp_fast(fma(-0.5, ee, lgn)));
-                        outv[e] = wt;
-                        const double wd = (double)wt;
-                        acc[0] += wd;
-                        const double wu0 = wd * u0, wu1 = wd * u1;
-                        acc[1] += wu0;
-                        acc[2] += wu1;
-                        acc[3] = fma(wu0, u0, acc[3]);
-                        acc[4] = fma(wu0, u1, acc[4]);
-                        acc[5] = fma(wu1, u1, acc[5]);
-                    } else {
-                        outv[e] = (T)w;
+                        const int r = rr + q;
+                        const double u1 = (t + 8 * r) - 0.5 * (N - 1);
+                        T o[2];
+#pragma unroll
+                        for (int e = 0; e < 2; ++e) {
+                            double ee;
+                            if (!a.range) {
+                                ee = fma(u1, fma(g11, u1, qe[e]), pe[e]);
+                            } else {
+                                // range likelihood: constants re-read from shared memory (P stays
+                                // valid: the next filter is staged into the other parameter buffer)
+                                const double u0 = (2 * m + e) - 0.5 * (N - 1);
+                                const double y0 = fma(P[P_BL], u0, fma(P[P_BL + 1], u1, P[P_CL]));
+                                const double y1 = fma(P[P_BL + 2], u0, fma(P[P_BL + 3], u1, P[P_CL + 1]));
+                                const double d = (P[P_ZR] - sqrt(fma(y0, y0, y1 * y1))) * P[P_ISG];
+                                ee = d * d;
+                            }
+                            const double w = (double)(e == 0 ? xv.x : xv.y);
+                            o[e] = emit(r, e, w * exp_fast(fma(-0.5, ee, lgn)));
+                        }
+                        *reinterpret_cast<V*>(Wf + (t + 8 * r) * N + 2 * m) = V{o[0], o[1]};
                     }
                 }
-                *reinterpret_cast<V*>(Wf + j1 * N + 2 * m) = V{outv[0], outv[1]};
+            }
+            double acc[6];
+            {
+                const double ua = (2 * m) - 0.5 * (N - 1), ub = ua + 1.0;
+                acc[0] = S[0] + S[1];
+                acc[1] = fma(ua, S[0], ub * S[1]);
+                acc[2] = Tm[0] + Tm[1];
+                acc[3] = fma(ua * ua, S[0], ub * ub * S[1]);
+                acc[4] = fma(ua, Tm[0], ub * Tm[1]);
+                acc[5] = U[0] + U[1];
             }
             if (UPDATE) {
 #pragma unroll
@@ -802,7 +896,8 @@ size_t resident_param_bytes(int l, int batch) { return sizeof(double) * (size_t)
 template <typename T, bool RG, bool UP>
 static cudaError_t launch_t(ResArgs<T> a, cudaStream_t s, int64_t* launches) {
     using V = typename C2<T>::type;
-    const size_t smem = sizeof(V) * (H * PITCH + 128) + 16 * 6 * sizeof(double) + 2 * sizeof(double) +
+    const size_t xbytes = std::max<size_t>(sizeof(V) * H * PITCH, stage_bytes<T>());
+    const size_t smem = xbytes + sizeof(V) * 128 + 16 * 6 * sizeof(double) + 2 * sizeof(double) +
                         2 * sizeof(unsigned long long) + 2 * sizeof(double) * (size_t)a.pstride;
     auto kern = k_resident_epoch<T, RG, UP>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
