@@ -23,9 +23,7 @@ import argparse
 import json
 import os
 import statistics
-import subprocess
 import sys
-import tempfile
 import time
 
 import numpy as np
@@ -60,45 +58,64 @@ def fp64_peak_tflops(mhz):
 
 
 class Clocks:
-    """nvidia-smi sampler during the timed region (B200_PROFILING.md clocks line)."""
+    """SM clock and clock-event reasons sampled DURING the timed region (the
+    B200_PROFILING.md clocks line), via NVML from a background thread every 2 ms
+    (the timed region is only tens of ms, too short for `nvidia-smi -lms`)."""
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown"}
 
     def __init__(self, device):
-        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
-        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,power.draw")
+        import threading
+        self.samples, self.reasons, self.power = [], 0, []
+        self.stop_ev = threading.Event()
         try:
-            self.p = subprocess.Popen(["nvidia-smi", "-i", str(device), f"--query-gpu={q}", "--format=csv,noheader,nounits",
-                                       "-lms", "100"], stdout=self.f, stderr=subprocess.DEVNULL)
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
         except Exception:
-            self.p = None
+            self.nv = None
+            return
+        self.th = threading.Thread(target=self._run, daemon=True)
+        self.th.start()
+
+    def _run(self):
+        nv, h = self.nv, self.h
+        get_r = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+            nv.nvmlDeviceGetCurrentClocksThrottleReasons
+        while not self.stop_ev.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
+                self.reasons |= int(get_r(h))
+                self.power.append(nv.nvmlDeviceGetPowerUsage(h) / 1000.0)
+            except Exception:
+                pass
+            self.stop_ev.wait(0.002)
 
     def stop(self):
-        if self.p is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.p.terminate()
-        self.p.wait()
-        self.f.flush()
-        rows = []
-        for line in open(self.f.name):
-            parts = [x.strip() for x in line.split(",")]
-            if len(parts) >= 7:
-                rows.append(parts)
-        os.unlink(self.f.name)
-        if not rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"], "samples": 0}
-        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in rows for i in range(4) if r[2 + i].lower().startswith("active")})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": float(rows[0][1]),
-                "reasons": reasons, "samples": len(rows),
-                "power_w_max": max(float(r[6]) for r in rows if r[6].replace(".", "").isdigit())}
+        if self.nv is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"], "samples": 0}
+        self.stop_ev.set()
+        self.th.join()
+        rs = sorted(name for bit, name in self.REASONS.items() if self.reasons & bit)
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": float(self.max_mhz), "reasons": rs, "samples": len(self.samples),
+                "power_w_max": max(self.power) if self.power else None, "source": "nvml, 2 ms"}
 
 
 def dist_env():
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return rank, world, local
+    from paper_2412_07240_b200.dist import env
+    return env()
+
+
+def kernel_metrics(kernel: str):
+    """ncu numbers for `kernel` committed under profiles/ (dram traffic per launch,
+    FP64-pipe utilisation), written by tools/ncu_to_json.py from a --set full capture."""
+    p = os.path.join(ROOT, "profiles", "kernel_metrics.json")
+    if not os.path.exists(p):
+        return {}
+    return json.load(open(p)).get(kernel, {})
 
 
 def oracle_sample(cfg, zs, budget_s: float, max_filters: int):
@@ -163,7 +180,7 @@ def run_reference(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--workload", default="C5", choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="cuda", choices=["cuda", "reference"])
@@ -191,8 +208,8 @@ def main():
     if args.l:
         cfg = cfg.replace(l=args.l)
     # weak scaling: rank r runs its own batch of filters (distinct seeds)
-    cfg = cfg.replace(seed=cfg.seed + 7919 * rank)
-    cfg = make_config(wl["cid"], **{**wl["over"], "seed": cfg.seed, "l": cfg.l})
+    from paper_2412_07240_b200.dist import max_over_ranks, rank_seed
+    cfg = make_config(wl["cid"], **{**wl["over"], "seed": rank_seed(cfg.seed, rank), "l": cfg.l})
     dtype = cfg.dtype
     T = args.warmup + args.steps + 1
     zs = simulate(cfg, T=T)["z"]                       # (T+1, batch, nz)
@@ -215,6 +232,7 @@ def main():
         dist.barrier()
     clocks = Clocks(local)
     launches0 = f.launches
+    f.profile(True)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     k0 = k
     with torch.cuda.stream(stream):
@@ -225,13 +243,11 @@ def main():
     ev1.synchronize()
     clk = clocks.stop()
     launches = f.launches - launches0
+    kern_total_ms, kern_n = f.profile_read()
+    f.profile(False)
     t_ms = ev0.elapsed_time(ev1)
     torch.cuda.synchronize()
-    t_max = t_ms
-    if world > 1:
-        tt = torch.tensor([t_ms], device=f"cuda:{local}", dtype=torch.float64)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t_max = float(tt.item())
+    t_max = max_over_ranks(t_ms, device=f"cuda:{local}")
     points_step = cfg.batch * cfg.points
     value = world * points_step * args.steps / (t_max * 1e-3)
     ms_step = t_max / args.steps
@@ -265,30 +281,31 @@ def main():
             fe.moments_into(mean, cov, logc)                  # D2H read of the step's result
         e1.record(stream)
         e1.synchronize()
-        te = e0.elapsed_time(e1)
-        if world > 1:
-            tt = torch.tensor([te], device=f"cuda:{local}", dtype=torch.float64)
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            te = float(tt.item())
+        te = max_over_ranks(e0.elapsed_time(e1), device=f"cuda:{local}")
         e2e = {"value": world * points_step * Te / (te * 1e-3), "unit": "grid-point updates/s",
                "h2d_bytes_per_step": cfg.batch * cfg.nz * 8,
-               "d2h_bytes_per_step": fe_state_bytes(cfg.batch), "steps": Te}
+               "d2h_bytes_per_step": fe.moments_bytes, "steps": Te}
         fe.close()
 
     # ---------------------------------------------------------------- roofline (dominant kernel)
+    # algorithmic bytes: read + write every weight once per epoch; the kernel's
+    # average duration comes from CUDA events the library records around it on its stream.
     hbm, hbm_src, sm_max = peaks()
     esize = 8 if dtype == "f64" else 4
-    alg_bytes = 2 * esize * points_step          # read + write every weight once per epoch
-    kern_ms = ms_step                            # the step is the fused epoch kernel (resident path);
-    if f.path == pmf.PATH_PENCIL:                # pencil path: several kernels -> whole-step figure
-        dominant = "pencil path (all kernels of the step)"
+    alg_bytes = 2 * esize * points_step
+    kern_ms = kern_total_ms / max(kern_n, 1)
+    if f.path == pmf.PATH_RESIDENT:
+        kname = f"k_resident_epoch<{'double' if dtype == 'f64' else 'float'}, 1, 1>"
     else:
-        dominant = "k_resident_epoch (one launch per step)"
+        kname = "pencil predict (prep .. finalize)"
+    km = kernel_metrics(kname)
     achieved = alg_bytes / (kern_ms * 1e-3) / 1e9
     roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-            "traffic": None, "kernel": dominant, "peak_source": hbm_src,
-            "alg_bytes_per_launch": alg_bytes}
-
+            "traffic": km.get("dram_bytes"), "kernel": kname, "kernel_ms": kern_ms, "timed_launches": kern_n,
+            "share_of_step": kern_ms / ms_step, "peak_source": hbm_src, "alg_bytes_per_launch": alg_bytes,
+            "alg_bytes_per_point": 2 * esize,
+            "fp64_pipe_frac_ncu": (km["fp64_pipe_pct"] / 100.0) if "fp64_pipe_pct" in km else None,
+            "ncu_source": km.get("source")}
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         v, nf, ts = oracle_sample(cfg, zs, budget_s=args.cpu_budget, max_filters=cfg.batch)
@@ -315,11 +332,6 @@ def main():
     if world > 1:
         dist.destroy_process_group()
     return 0
-
-
-def fe_state_bytes(batch):
-    # pmf_moments copies the per-filter state records (sizeof(FilterState) = 352 B)
-    return 352 * batch
 
 
 if __name__ == "__main__":

@@ -28,8 +28,7 @@
  *
  * LAZINESS: pmf_predict and pmf_regrid validate their arguments and RECORD the
  * operation; it is executed (fused with what follows) by the next call that
- * needs the density: pmf_update, pmf_get_weights, pmf_device_weights,
- * pmf_sync. Results are identical to eager execution.
+ * needs the density: pmf_update, pmf_get_weights, pmf_get_grid, pmf_sync. Results are identical to eager execution.
  *
  * ERRORS: every int-returning call returns PMF_OK (0) or a negative PMF_E_*
  * code; pmf_last_error() gives a message. A failed call leaves the context
@@ -74,7 +73,7 @@ extern "C" {
 
 #define PMF_PATH_AUTO     0  /* resident per-filter kernel when it fits, else the pencil path                    */
 #define PMF_PATH_PENCIL   1  /* multi-pass per-axis pencil kernels (any nx <= 4)                                */
-#define PMF_PATH_RESIDENT 2  /* one CTA per filter, whole half-spectrum in shared memory (nx=2: N0=N1=128; nx=1) */
+#define PMF_PATH_RESIDENT 2  /* one CTA per filter, whole half-spectrum in shared memory (nx = 2, N0 = N1 = 128)   */
 
 #define PMF_LIK_LINEAR_GAUSS 0   /* z = H x + v, v ~ N(0, R), nz <= 4 (eq:meas P:36)                               */
 #define PMF_LIK_RANGE_GAUSS  1   /* z = ||x|| + v, v ~ N(0, sigma^2), nz = 1 (C3)                                   */
@@ -147,9 +146,13 @@ int pmf_update(pmf_ctx* ctx, const double* z, int z_on_device, const pmf_likelih
 
 /* Copy the posterior moments of the last update to host arrays (any may be
  * NULL): mean batch x nx, cov batch x nx x nx, log_norm batch (log of the
- * P:49 normaliser). Synchronises. PMF_E_STATE before the first update,
+ * P:49 normaliser). Packs (nx + nx^2 + 2) doubles per filter on the device and copies
+ * them to pinned memory; synchronises. PMF_E_STATE before the first update,
  * PMF_E_NO_SUPPORT if any filter's last update failed. */
 int pmf_moments(pmf_ctx* ctx, double* mean, double* cov, double* log_norm);
+
+/* Bytes pmf_moments copies device -> host per call ((nx + nx^2 + 2) doubles per filter). */
+int64_t pmf_moments_bytes(const pmf_ctx* ctx);
 
 /* Re-centre every filter's grid on its last posterior (R12; the paper is silent,
  * north_star "re-centre the grid"): c' = mean, B' = diag(2 k_sigma sqrt(cov_mm)/N_m),
@@ -176,6 +179,14 @@ int pmf_sync(pmf_ctx* ctx);
 
 /* Number of kernels this context has launched so far. */
 int64_t pmf_launch_count(const pmf_ctx* ctx);
+
+/* Kernel timing: while enabled, CUDA events are recorded on the context's stream
+ * around the dominant kernel of every executed prediction (the resident epoch
+ * kernel, or the whole pencil predict); pmf_profile_read waits for them and
+ * returns the summed milliseconds and the number of timed launches, then resets.
+ * pmf_profile(ctx, 1) also resets. */
+int pmf_profile(pmf_ctx* ctx, int enable);
+int pmf_profile_read(pmf_ctx* ctx, double* total_ms, int64_t* count);
 
 /* Bytes of device memory owned by the context. */
 int64_t pmf_device_bytes(const pmf_ctx* ctx);

@@ -514,6 +514,30 @@ __global__ void k_scale_out(const T* __restrict__ W, T* __restrict__ dst, const 
     }
 }
 
+// ============================================================================ compact moments for the host
+// out[b] = {mean (nx), cov (nx*nx, row-major), log C, status}
+__global__ void k_pack_moments(const FilterState* __restrict__ st, double* __restrict__ out, int nx, int batch) {
+    const int stride = nx + nx * nx + 2;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < batch * stride; i += gridDim.x * blockDim.x) {
+        const int b = i / stride, k = i - b * stride;
+        const FilterState& f = st[b];
+        double v;
+        if (k < nx) v = f.mean[k];
+        else if (k < nx + nx * nx) { const int q = k - nx; v = f.cov[(q / nx) * 4 + q % nx]; }
+        else if (k == nx + nx * nx) v = f.logC;
+        else v = (double)f.status;
+        out[i] = v;
+    }
+}
+
+cudaError_t launch_pack_moments(const Dims& d, const FilterState* st, double* out, cudaStream_t s,
+                                int64_t* launches) {
+    const int n = d.batch * (d.nx + d.nx * d.nx + 2);
+    k_pack_moments<<<std::min((n + 255) / 256, 1184), 256, 0, s>>>(st, out, d.nx, d.batch);
+    ++*launches;
+    return cudaGetLastError();
+}
+
 // ============================================================================ launchers
 #define PMF_TRY(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) return e_; } while (0)
 
@@ -528,6 +552,7 @@ static cudaError_t predict_pencil_t(const Dims& d, PencilBufs& b, const Twiddles
                                     const LikParams* lp, cudaStream_t s, int64_t* launches) {
     using V = typename C2<T>::type;
     const int cs = coef_stride(mp.l);
+    if (b.ev0) cudaEventRecord(b.ev0, s);
     k_predict_prep<<<(d.batch + 127) / 128, 128, 0, s>>>(b.st, b.coef, cs, mp, b.sub, d.batch);
     ++*launches;
     PMF_TRY(cudaGetLastError());
@@ -550,6 +575,7 @@ static cudaError_t predict_pencil_t(const Dims& d, PencilBufs& b, const Twiddles
             k_finalize<<<(d.batch + 3) / 4, 128, 0, s>>>(b.st, b.partials, 1, d.batch, d, 0);
             ++*launches;
         }
+        if (b.ev1) cudaEventRecord(b.ev1, s);
         return cudaGetLastError();
     }
     // axis 0 forward (R2C)
@@ -611,6 +637,7 @@ static cudaError_t predict_pencil_t(const Dims& d, PencilBufs& b, const Twiddles
         k_finalize<<<(d.batch + 3) / 4, 128, 0, s>>>(b.st, b.partials, (int)(rpf / P0), d.batch, d, 0);
         ++*launches;
     }
+    if (b.ev1) cudaEventRecord(b.ev1, s);
     return cudaGetLastError();
 }
 

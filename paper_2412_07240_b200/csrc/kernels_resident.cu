@@ -894,7 +894,7 @@ bool resident_supported(const Dims& d, int dtype) {
 size_t resident_param_bytes(int l, int batch) { return sizeof(double) * (size_t)prm_stride(l) * batch; }
 
 template <typename T, bool RG, bool UP>
-static cudaError_t launch_t(ResArgs<T> a, cudaStream_t s, int64_t* launches) {
+static cudaError_t launch_t(ResArgs<T> a, cudaStream_t s, int64_t* launches, cudaEvent_t ev0, cudaEvent_t ev1) {
     using V = typename C2<T>::type;
     const size_t xbytes = std::max<size_t>(sizeof(V) * H * PITCH, stage_bytes<T>());
     const size_t smem = xbytes + sizeof(V) * 128 + 16 * 6 * sizeof(double) + 2 * sizeof(double) +
@@ -909,7 +909,9 @@ static cudaError_t launch_t(ResArgs<T> a, cudaStream_t s, int64_t* launches) {
     if (e != cudaSuccess) return e;
     if (occ < 1) return cudaErrorInvalidConfiguration;
     const int grid = std::min(a.batch, nsm * occ);
+    if (ev0) cudaEventRecord(ev0, s);
     kern<<<grid, NT, smem, s>>>(a);
+    if (ev1) cudaEventRecord(ev1, s);
     ++*launches;
     return cudaGetLastError();
 }
@@ -932,10 +934,10 @@ static cudaError_t launch_dt(const Dims& d, PencilBufs& b, const ModelParams& mp
     a.batch = d.batch;
     a.range = lpv.kind == 1;
     const bool rg = ks > 0.0;
-    if (rg && lp) e = launch_t<T, true, true>(a, s, launches);
-    else if (rg) e = launch_t<T, true, false>(a, s, launches);
-    else if (lp) e = launch_t<T, false, true>(a, s, launches);
-    else e = launch_t<T, false, false>(a, s, launches);
+    if (rg && lp) e = launch_t<T, true, true>(a, s, launches, b.ev0, b.ev1);
+    else if (rg) e = launch_t<T, true, false>(a, s, launches, b.ev0, b.ev1);
+    else if (lp) e = launch_t<T, false, true>(a, s, launches, b.ev0, b.ev1);
+    else e = launch_t<T, false, false>(a, s, launches, b.ev0, b.ev1);
     if (e != cudaSuccess) return e;
     k_res_finalize<<<(d.batch + 127) / 128, 128, 0, s>>>(b.st, b.partials, b.coef, ps, mp.s, lp ? 1 : 0, d.batch);
     ++*launches;

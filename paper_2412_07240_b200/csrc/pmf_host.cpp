@@ -55,6 +55,8 @@ struct pmf_ctx {
     size_t sub_bytes = 0;
     double* z = nullptr;
     double* gauss = nullptr;
+    double* mom_dev = nullptr;       // compact moments [batch][nx + nx^2 + 2]
+    double* mom_host = nullptr;      // pinned host mirror
     void* tw[4] = {nullptr, nullptr, nullptr, nullptr};
     int64_t bytes = 0;
     // host-side model cache (per (dt, steps))
@@ -66,6 +68,10 @@ struct pmf_ctx {
     bool have_update = false;
     Pending pend;
     int64_t launches = 0;
+    // kernel timing (pmf_profile): event pairs around the dominant kernel of each flush
+    bool prof = false;
+    std::vector<cudaEvent_t> evs;
+    int nev = 0;
     std::string err;
 };
 
@@ -212,6 +218,22 @@ static PencilBufs bufs(pmf_ctx* c) {
     return b;
 }
 
+// events around the dominant kernel of this predict (pmf_profile)
+static void attach_events(pmf_ctx* c, PencilBufs& b) {
+    if (c->prof) {
+        if ((int)c->evs.size() < 2 * (c->nev + 1)) {
+            cudaEvent_t e0, e1;
+            cudaEventCreate(&e0);
+            cudaEventCreate(&e1);
+            c->evs.push_back(e0);
+            c->evs.push_back(e1);
+        }
+        b.ev0 = c->evs[2 * c->nev];
+        b.ev1 = c->evs[2 * c->nev + 1];
+        ++c->nev;
+    }
+}
+
 static Twiddles twid(pmf_ctx* c) {
     Twiddles t;
     for (int i = 0; i < 4; ++i) t.tw[i] = c->tw[i];
@@ -314,6 +336,7 @@ static int flush(pmf_ctx* c, const LikParams* lp) {
     // the resident kernel keeps 3 coefficients per substep in shared memory
     const bool resident = c->path == PMF_PATH_RESIDENT && c->pend.predict && c->pend.steps <= 2048;
     if (resident) {
+        attach_events(c, b);
         e = launch_resident(c->d, c->dtype, b, twid(c), &c->mp, lp, c->pend.regrid ? c->pend.k_sigma : -1.0,
                             c->stream, &c->launches);
         if (e != cudaSuccess) return cuda_fail(c, e, "resident epoch kernel");
@@ -331,6 +354,7 @@ static int flush(pmf_ctx* c, const LikParams* lp) {
     }
     b = bufs(c);
     if (c->pend.predict) {
+        attach_events(c, b);
         e = launch_predict_pencil(c->d, c->dtype, b, twid(c), c->mp, lp, c->stream, &c->launches);
         if (e != cudaSuccess) return cuda_fail(c, e, "predict");
     } else if (lp) {
@@ -448,6 +472,9 @@ int pmf_create(const pmf_config* cfg, const double* A, const double* Q, pmf_ctx*
     if (!r) r = dalloc(c, (void**)&c->partials, c->partials_bytes);
     if (!r) r = dalloc(c, (void**)&c->z, sizeof(double) * PMF_MAX_NZ * d.batch);
     if (!r) r = dalloc(c, (void**)&c->gauss, sizeof(double) * 21 * d.batch);
+    if (!r) r = dalloc(c, (void**)&c->mom_dev, sizeof(double) * (nx + nx * nx + 2) * d.batch);
+    if (!r && cudaMallocHost((void**)&c->mom_host, sizeof(double) * (nx + nx * nx + 2) * d.batch) != cudaSuccess)
+        r = fail(c, PMF_E_NOMEM, "cudaMallocHost (moments)");
     for (int m = 0; m < nx && !r; ++m) {
         const int N = d.n[m];
         if (c->dtype == PMF_F64) {
@@ -484,10 +511,12 @@ void pmf_destroy(pmf_ctx* c) {
     if (!c) return;
     cudaSetDevice(c->cfg.device);
     cudaStreamSynchronize(c->stream);
-    void* ptrs[] = {c->W, c->W2, c->S, c->st, c->partials, c->coef, c->sub, c->z, c->gauss,
+    void* ptrs[] = {c->W, c->W2, c->S, c->st, c->partials, c->coef, c->sub, c->z, c->gauss, c->mom_dev,
                     c->tw[0], c->tw[1], c->tw[2], c->tw[3]};
     for (void* p : ptrs)
         if (p) cudaFree(p);
+    if (c->mom_host) cudaFreeHost(c->mom_host);
+    for (cudaEvent_t e : c->evs) cudaEventDestroy(e);
     delete c;
 }
 
@@ -622,24 +651,28 @@ int pmf_moments(pmf_ctx* c, double* mean, double* cov, double* log_norm) {
     if (!c->have_update) return fail(c, PMF_E_STATE, "no update has run");
     CK(c, cudaSetDevice(c->cfg.device), "cudaSetDevice");
     const Dims& d = c->d;
-    std::vector<FilterState> st(d.batch);
-    CK(c, cudaMemcpyAsync(st.data(), c->st, sizeof(FilterState) * d.batch, cudaMemcpyDeviceToHost, c->stream),
-       "state download");
+    const int nx = d.nx, stride = nx + nx * nx + 2;
+    const size_t bytes = sizeof(double) * stride * (size_t)d.batch;
+    cudaError_t e = launch_pack_moments(d, c->st, c->mom_dev, c->stream, &c->launches);
+    if (e != cudaSuccess) return cuda_fail(c, e, "pack moments");
+    CK(c, cudaMemcpyAsync(c->mom_host, c->mom_dev, bytes, cudaMemcpyDeviceToHost, c->stream), "moments download");
     CK(c, cudaStreamSynchronize(c->stream), "moments sync");
-    const int nx = d.nx;
     int bad = 0;
     for (int b = 0; b < d.batch; ++b) {
-        const FilterState& f = st[b];
-        if (f.status) bad = 1;
-        for (int a = 0; a < nx; ++a) {
-            if (mean) mean[(size_t)b * nx + a] = f.mean[a];
-            if (cov)
-                for (int q = 0; q < nx; ++q) cov[(size_t)b * nx * nx + a * nx + q] = f.cov[a * 4 + q];
-        }
-        if (log_norm) log_norm[b] = f.logC;
+        const double* f = c->mom_host + (size_t)b * stride;
+        if (f[stride - 1] != 0.0) bad = 1;
+        if (mean)
+            for (int a = 0; a < nx; ++a) mean[(size_t)b * nx + a] = f[a];
+        if (cov)
+            for (int q = 0; q < nx * nx; ++q) cov[(size_t)b * nx * nx + q] = f[nx + q];
+        if (log_norm) log_norm[b] = f[nx + nx * nx];
     }
     if (bad) return fail(c, PMF_E_NO_SUPPORT, "measurement incompatible with grid support (some filter)");
     return PMF_OK;
+}
+
+int64_t pmf_moments_bytes(const pmf_ctx* c) {
+    return c ? (int64_t)sizeof(double) * (c->d.nx + c->d.nx * c->d.nx + 2) * c->d.batch : 0;
 }
 
 int pmf_get_weights(pmf_ctx* c, void* dst, int dst_on_device) {
@@ -704,6 +737,29 @@ int pmf_sync(pmf_ctx* c) {
 }
 
 int64_t pmf_launch_count(const pmf_ctx* c) { return c ? c->launches : 0; }
+
+int pmf_profile(pmf_ctx* c, int enable) {
+    if (!c) return fail(c, PMF_E_ARG, "null context");
+    c->prof = enable != 0;
+    c->nev = 0;
+    return PMF_OK;
+}
+
+int pmf_profile_read(pmf_ctx* c, double* total_ms, int64_t* count) {
+    if (!c || !total_ms || !count) return fail(c, PMF_E_ARG, "null argument");
+    CK(c, cudaSetDevice(c->cfg.device), "cudaSetDevice");
+    double tot = 0.0;
+    for (int i = 0; i < c->nev; ++i) {
+        CK(c, cudaEventSynchronize(c->evs[2 * i + 1]), "profile event");
+        float ms = 0.0f;
+        CK(c, cudaEventElapsedTime(&ms, c->evs[2 * i], c->evs[2 * i + 1]), "profile elapsed");
+        tot += ms;
+    }
+    *total_ms = tot;
+    *count = c->nev;
+    c->nev = 0;
+    return PMF_OK;
+}
 int64_t pmf_device_bytes(const pmf_ctx* c) { return c ? c->bytes : 0; }
 int pmf_path(const pmf_ctx* c) { return c ? c->path : -1; }
 

@@ -81,6 +81,7 @@ struct PencilBufs {
     const SubstepEntry* sub;
     const double* z;     // [batch][nz]
     const double* gauss; // [batch][nx + 16 + 1] mean, inverse cov, log norm (set_gaussian)
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;   // if set: recorded around the dominant kernel
 };
 
 cudaError_t launch_init_gaussian(const Dims& d, int dtype, PencilBufs& b, cudaStream_t s, int64_t* launches);
@@ -94,6 +95,9 @@ cudaError_t launch_predict_pencil(const Dims& d, int dtype, PencilBufs& b, const
                                   cudaStream_t s, int64_t* launches);
 cudaError_t launch_scale_out(const Dims& d, int dtype, const PencilBufs& b, void* dst,
                              cudaStream_t s, int64_t* launches);
+
+cudaError_t launch_pack_moments(const Dims& d, const FilterState* st, double* out, cudaStream_t s,
+                                int64_t* launches);
 
 // resident (one CTA per filter) fused epoch kernel
 bool resident_supported(const Dims& d, int dtype);

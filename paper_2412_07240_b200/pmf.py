@@ -29,7 +29,7 @@ LIK_LINEAR_GAUSS, LIK_RANGE_GAUSS = 0, 1
 # every symbol include/pmf.h declares (checked by tests/test_abi.py)
 SYMBOLS = ["pmf_create", "pmf_destroy", "pmf_last_error", "pmf_set_gaussian", "pmf_set_state",
            "pmf_predict", "pmf_update", "pmf_moments", "pmf_regrid", "pmf_step", "pmf_get_weights",
-           "pmf_get_grid", "pmf_sync", "pmf_launch_count", "pmf_device_bytes", "pmf_path", "pmf_version"]
+           "pmf_get_grid", "pmf_sync", "pmf_launch_count", "pmf_moments_bytes", "pmf_profile", "pmf_profile_read", "pmf_device_bytes", "pmf_path", "pmf_version"]
 
 
 class PMFError(RuntimeError):
@@ -77,6 +77,9 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         "pmf_get_grid": (I, [P, D, D]),
         "pmf_sync": (I, [P]),
         "pmf_launch_count": (C.c_int64, [P]),
+        "pmf_moments_bytes": (C.c_int64, [P]),
+        "pmf_profile": (I, [P, I]),
+        "pmf_profile_read": (I, [P, C.POINTER(C.c_double), C.POINTER(C.c_int64)]),
         "pmf_device_bytes": (C.c_int64, [P]),
         "pmf_path": (I, [P]),
         "pmf_version": (C.c_char_p, []),
@@ -234,6 +237,19 @@ class Filter:
     @property
     def launches(self) -> int:
         return int(self.lib.pmf_launch_count(self.h))
+
+    def profile(self, enable: bool = True):
+        self._check(self.lib.pmf_profile(self.h, 1 if enable else 0))
+
+    def profile_read(self):
+        """(total kernel milliseconds, number of timed launches) since profile(True); syncs."""
+        ms, n = C.c_double(), C.c_int64()
+        self._check(self.lib.pmf_profile_read(self.h, C.byref(ms), C.byref(n)))
+        return ms.value, n.value
+
+    @property
+    def moments_bytes(self) -> int:
+        return int(self.lib.pmf_moments_bytes(self.h))
 
     @property
     def device_bytes(self) -> int:
