@@ -471,6 +471,13 @@ __global__ void __launch_bounds__(NT, 1) k_resident_epoch(ResArgs<T> a) {
         const int nxt = filt + gridDim.x;
         mbar_wait(bar, it & 1);                 // weights + constants of this filter are in shared memory
 
+        if (warp == 0 && lane < 8 && nxt < a.batch) {
+            // pull the next filter's weights into L2 now; its TMA staging (issued late in P3,
+            // once X is free) then reads L2 instead of HBM
+            const char* p = reinterpret_cast<const char*>(a.W + (long long)nxt * (N * N)) + lane * (N * N * sizeof(T) / 8);
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"((unsigned)(N * N * sizeof(T) / 8))
+                         : "memory");
+        }
         if (P[P_SKIP] != 0.0) {                 // failed filter: leave it untouched
             __syncthreads();
             if (warp == 0 && nxt < a.batch) stage(a, nxt, smem_raw, Pn, bar, lane);
@@ -486,23 +493,35 @@ __global__ void __launch_bounds__(NT, 1) k_resident_epoch(ResArgs<T> a) {
                     z[r] = *reinterpret_cast<const V*>(Xs + j1 * (int)StagePitch<T>::B + 2 * m * (int)sizeof(T));
                 }
             } else {
-                // multilinear interpolation of the old weights at the new points (R12), zero ghosts
+                // multilinear interpolation of the old weights at the new points (R12), zero ghosts.
+                // v = o + M u' is affine in r: v(r) = v(0) + r * 8 M[:,1].
                 const double M0 = P[P_M], M1 = P[P_M + 1], M2 = P[P_M + 2], M3 = P[P_M + 3];
                 const double o0 = P[P_O], o1 = P[P_O + 1];
+                const double u10 = t - 0.5 * (N - 1);
+                const double s0 = 8.0 * M1, s1 = 8.0 * M3;
+                double b0[2], b1[2];
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const double u0 = (2 * m + e) - 0.5 * (N - 1);
+                    b0[e] = fma(M0, u0, fma(M1, u10, o0));
+                    b1[e] = fma(M2, u0, fma(M3, u10, o1));
+                }
+                // integer clamp to [-1, 128]: beyond it every tap is a zero ghost or has weight 0
+                auto split = [&](double v, int& i, double& a) {
+                    const double f = floor(v);
+                    const int fi = __double2int_rz(f);          // saturating
+                    i = min(max(fi, -1), N);
+                    a = (fi == i) ? v - f : 0.0;
+                };
 #pragma unroll
                 for (int r = 0; r < 16; ++r) {
-                    const double u1 = (t + 8 * r) - 0.5 * (N - 1);
                     T val[2];
 #pragma unroll
                     for (int e = 0; e < 2; ++e) {
-                        const double u0 = (2 * m + e) - 0.5 * (N - 1);
-                        const double v0 = fma(M0, u0, fma(M1, u1, o0));
-                        const double v1 = fma(M2, u0, fma(M3, u1, o1));
-                        // clamp to [-1, 128]: outside, every tap is a zero ghost or has weight 0
-                        const double c0 = fmin(fmax(v0, -1.0), (double)N), c1 = fmin(fmax(v1, -1.0), (double)N);
-                        const double f0 = floor(c0), f1 = floor(c1);
-                        const double a0 = c0 - f0, a1 = c1 - f1;
-                        const int i0 = (int)f0, i1 = (int)f1;
+                        int i0, i1;
+                        double a0, a1;
+                        split(fma((double)r, s0, b0[e]), i0, a0);
+                        split(fma((double)r, s1, b1[e]), i1, a1);
                         const T* row0 = reinterpret_cast<const T*>(Xs + i1 * (int)StagePitch<T>::B) + i0;
                         const T* row1 = reinterpret_cast<const T*>(reinterpret_cast<const char*>(row0) + StagePitch<T>::B);
                         const double w00 = (double)row0[0], w01 = (double)row0[1];
