@@ -56,10 +56,13 @@ __device__ __forceinline__ void stockham_stage(const V* __restrict__ src, V* __r
     const int NR = N / R;
     const int total = P * NR;
     const int twstep = N / (Ns * R);
+    // exact float-reciprocal division: the fractional part of (x + 0.5)/d is >= 0.5/d >> float error
+    const float invNR = 1.0f / (float)NR, invNs = 1.0f / (float)Ns;
     for (int t = threadIdx.x; t < total; t += blockDim.x) {
-        const int p = t / NR;
+        const int p = (int)(((float)t + 0.5f) * invNR);
         const int j = t - p * NR;
-        const int k = j % Ns;
+        const int jq = (int)(((float)j + 0.5f) * invNs);
+        const int k = j - jq * Ns;
         const V* s = src + p * PS;
         V v[R];
 #pragma unroll
@@ -73,7 +76,7 @@ __device__ __forceinline__ void stockham_stage(const V* __restrict__ src, V* __r
             }
         }
         SmallDFT<R, INV, V>::run(v);
-        const int idxD = (j / Ns) * Ns * R + k;
+        const int idxD = jq * Ns * R + k;
         V* d = dst + p * PS;
 #pragma unroll
         for (int r = 0; r < R; ++r) d[idxD + r * Ns] = v[r];

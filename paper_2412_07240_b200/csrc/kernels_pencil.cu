@@ -9,7 +9,8 @@
 //   axes nx-2..1 -> axis-0 C2R fused with the measurement update (eq:filt P:46)
 // and for nx = 1 as one fused line kernel. Each pass stages a tile of pencils in
 // shared memory (coalesced: contiguous inner index across threads) and runs the
-// Stockham FFT of fft_smem.cuh.
+// Stockham FFT of fft_smem.cuh. Kernels that touch points are templated on nx so
+// every per-point loop is static (no local-memory arrays).
 #include <algorithm>
 #include <cmath>
 #include <vector>
@@ -20,6 +21,7 @@
 namespace pmf {
 
 static constexpr int kThreads = 256;
+static constexpr int LCAP = 64;       // substeps kept per pencil in shared memory (Psi pass)
 
 static FFTPlan make_plan(int N) {
     FFTPlan p{};
@@ -48,13 +50,88 @@ static int pencils_per_cta(int N) {
     return std::min(p2, 32);
 }
 
+// unsigned division by a runtime constant d (1 <= d, x < 2^32): q = umulhi64(x, ceil(2^64/d))
+struct FastDiv {
+    unsigned long long m;
+    unsigned d;
+};
+static FastDiv make_div(unsigned d) {
+    FastDiv f;
+    f.d = d;
+    f.m = d == 1 ? 0ull : (~0ull / d) + 1ull;
+    return f;
+}
+__device__ __forceinline__ unsigned fdiv(unsigned x, const FastDiv& f) {
+    return f.d == 1 ? x : (unsigned)__umul64hi((unsigned long long)x, f.m);
+}
+
+struct DivSet {
+    FastDiv n[4];   // per axis
+};
+static DivSet make_divs(const Dims& d) {
+    DivSet s;
+    for (int a = 0; a < 4; ++a) s.n[a] = make_div((unsigned)d.n[a]);
+    return s;
+}
+
+// index offsets u of point pt (axis 0 fastest) of one filter
+template <int NX>
+__device__ __forceinline__ void point_u(const Dims& d, const DivSet& dv, unsigned pt, double* u) {
+#pragma unroll
+    for (int a = 0; a < NX; ++a) {
+        const unsigned q = (a < NX - 1) ? fdiv(pt, dv.n[a]) : 0u;
+        const unsigned j = (a < NX - 1) ? pt - q * (unsigned)d.n[a] : pt;
+        u[a] = (double)j - 0.5 * (d.n[a] - 1);
+        pt = q;
+    }
+}
+
+template <int NX>
+__device__ __forceinline__ void phys(const FilterState& f, const double* u, double* x) {
+#pragma unroll
+    for (int a = 0; a < NX; ++a) {
+        double s = f.c[a];
+#pragma unroll
+        for (int b = 0; b < NX; ++b) s = fma(f.B[a * 4 + b], u[b], s);
+        x[a] = s;
+    }
+}
+
+// moment accumulators: acc[0] = sum w, acc[1..NX] = sum w u_a, then sum w u_a u_b (a <= b)
+template <int NX>
+__device__ __forceinline__ void acc_mom(double w, const double* u, double* acc) {
+    acc[0] += w;
+    int k = 1 + NX;
+#pragma unroll
+    for (int a = 0; a < NX; ++a) {
+        const double wu = w * u[a];
+        acc[1 + a] += wu;
+#pragma unroll
+        for (int b = a; b < NX; ++b) {
+            acc[k] = fma(wu, u[b], acc[k]);
+            ++k;
+        }
+    }
+}
+
+// coefficient block per filter: [0] input scale, [4 .. 4+10l) Euler factors (epoch_coefs),
+// [lq(l) .. +16) likelihood exponent as a quadratic form in the moved grid's index
+// coordinates: e(u) = q[0] + sum_a q[1+a] u_a + sum_{a<=b} q[5+tri(a,b)] u_a u_b
+__host__ __device__ __forceinline__ int lq_off(int l) { return 4 + 10 * l; }
+
+// packed (a <= b) index 0..9 for nx <= 4
+__host__ __device__ __forceinline__ int tri(int a, int b) { return a * 4 - a * (a - 1) / 2 + (b - a); }
+
 // ============================================================================ prep
 // One thread per filter: Euler-factor coefficients (epoch_coefs), the input
 // scale, then move the grid (c <- M c, B <- M B, eq:gridMov) and set the
 // closed-form normalisation of Alg. 6: scale' = vol_0 / (vol_l s)  (R9; the DC
-// coefficient is multiplied by exactly s because psi(0) = 1).
+// coefficient is multiplied by exactly s because psi(0) = 1). With an update
+// pending, the linear-Gaussian exponent is expanded around the moved grid
+// (r(u) = (z - H c_l) - (H B_l) u; e = r^T R^-1 r, R13).
 __global__ void k_predict_prep(FilterState* st, double* coef, int cstride, ModelParams mp,
-                               const SubstepEntry* __restrict__ sub, int batch) {
+                               const SubstepEntry* __restrict__ sub, int batch, LikParams lp,
+                               const double* __restrict__ z, int update) {
     int b = blockIdx.x * blockDim.x + threadIdx.x;
     if (b >= batch) return;
     FilterState& f = st[b];
@@ -75,27 +152,46 @@ __global__ void k_predict_prep(FilterState* st, double* coef, int cstride, Model
     for (int i = 0; i < 16; ++i) f.B[i] = Bn[i];
     for (int a = 0; a < nx; ++a) f.c[a] = cn[a];
     f.scale = vol0 / (voll * mp.s);
-}
-
-// ============================================================================ spectral multiplier
-// s * Psi(k) / N_total for one spectral point (Alg. 3-4): kap[a] = 2 pi k_a / N_a
-// (signed k), kx = kap with the Nyquist wavenumber zeroed (R7).
-__device__ __forceinline__ double psi_point(int nx, int l, const double* __restrict__ cf,
-                                            const double* kap, const double* kx, double mult) {
-    double prod = 1.0;
-    for (int s = 0; s < l; ++s) {
-        const double* c = cf + 10 * s;
-        double f = 1.0;
-        int idx = nx;
-        for (int a = 0; a < nx; ++a) {
-            f = fma(c[a], kap[a] * kap[a], f);
-            for (int b = a + 1; b < nx; ++b) f = fma(c[idx++], kx[a] * kx[b], f);
+    double* q = cf + lq_off(mp.l);
+    for (int i = 0; i < 16; ++i) q[i] = 0.0;
+    if (update && lp.kind == 0) {
+        const double* zf = z + (long long)b * lp.nz;
+        double r0[4], G[16];
+        for (int i = 0; i < lp.nz; ++i) {
+            double hc = 0.0;
+            for (int a = 0; a < nx; ++a) hc = fma(lp.H[i * 4 + a], cn[a], hc);
+            r0[i] = zf[i] - hc;
+            for (int a = 0; a < nx; ++a) {
+                double g = 0.0;
+                for (int k = 0; k < nx; ++k) g = fma(lp.H[i * 4 + k], Bn[k * 4 + a], g);
+                G[i * 4 + a] = g;
+            }
         }
-        prod *= f;
+        double w[4];     // R^-1 r0
+        for (int i = 0; i < lp.nz; ++i) {
+            double s = 0.0;
+            for (int j = 0; j < lp.nz; ++j) s = fma(lp.Rinv[i * 4 + j], r0[j], s);
+            w[i] = s;
+        }
+        double qa = 0.0;
+        for (int i = 0; i < lp.nz; ++i) qa = fma(r0[i], w[i], qa);
+        q[0] = qa;
+        for (int a = 0; a < nx; ++a) {
+            double s = 0.0;
+            for (int i = 0; i < lp.nz; ++i) s = fma(G[i * 4 + a], w[i], s);
+            q[1 + a] = -2.0 * s;
+        }
+        for (int a = 0; a < nx; ++a)
+            for (int c = a; c < nx; ++c) {
+                double s = 0.0;
+                for (int i = 0; i < lp.nz; ++i)
+                    for (int j = 0; j < lp.nz; ++j) s = fma(G[i * 4 + a] * lp.Rinv[i * 4 + j], G[j * 4 + c], s);
+                q[5 + tri(a, c)] = (a == c) ? s : 2.0 * s;
+            }
     }
-    return mult / prod;
 }
 
+// ============================================================================ spectral multiplier helpers
 __device__ __forceinline__ void wavenum(int k, int N, double& kap, double& kx) {
     int ks = signed_k(k, N);
     kap = 2.0 * PMF_PI * ks / N;
@@ -118,15 +214,17 @@ __global__ void __launch_bounds__(kThreads) k_axis0_r2c(const T* __restrict__ W,
     const int filt = (int)(row0 / rpf);
     const T sc = (T)coef[(long long)filt * cstride];
     const T* src = W + row0 * N;
+    const float invN = 1.0f / N;
     for (int i = threadIdx.x; i < P * N; i += blockDim.x) {
-        int p = i / N, j = i - p * N;
+        const int p = (int)((i + 0.5f) * invN), j = i - p * N;
         a[p * PS + j] = V{src[i] * sc, T(0)};
     }
     __syncthreads();
     V* r = smem_fft<false>(a, b, P, PS, pl, tw);
     V* dst = S + row0 * d.H0;
+    const float invH = 1.0f / d.H0;
     for (int i = threadIdx.x; i < P * d.H0; i += blockDim.x) {
-        int p = i / d.H0, k = i - p * d.H0;
+        const int p = (int)((i + 0.5f) * invH), k = i - p * d.H0;
         dst[i] = r[p * PS + k];
     }
 }
@@ -135,7 +233,10 @@ __global__ void __launch_bounds__(kThreads) k_axis0_r2c(const T* __restrict__ W,
 // Pencils along axis m of the half-spectrum buffer: element (i, j, o) at
 // S[o*Nm*I + j*I + i], i < I = H0*N_1*..*N_{m-1}, o < O. A CTA takes P
 // consecutive i (coalesced rows of P complex) of one o.
-template <typename T, int MODE>   // MODE 0 fwd, 1 inv, 2 fwd*Psi*inv (last axis)
+// MODE 2 (last axis m = NX-1): forward, x s Psi(k) / N_total, inverse. Psi is
+// factored per pencil: for substep n, f_n = gam_n + bet_n kx_L + alp_n kap_L^2 with
+// (gam_n, bet_n) depending only on the pencil's other wavenumbers (Alg. 3, R3, R7).
+template <typename T, int MODE, int NX>
 __global__ void __launch_bounds__(kThreads) k_axis_c2c(typename C2<T>::type* __restrict__ S, Dims d, int m,
                                                         long long I, FFTPlan pl,
                                                         const typename C2<T>::type* __restrict__ tw, int P,
@@ -151,7 +252,7 @@ __global__ void __launch_bounds__(kThreads) k_axis_c2c(typename C2<T>::type* __r
     const long long i0 = (blockIdx.x - o * ntile) * P;
     V* base = S + o * (long long)N * I;
     for (int t = threadIdx.x; t < P * N; t += blockDim.x) {
-        int p = t % P, j = t / P;
+        const int j = t / P, p = t - j * P;     // P is a power of two
         long long i = i0 + p;
         a[p * PS + j] = (i < I) ? base[(long long)j * I + i] : V{T(0), T(0)};
     }
@@ -162,28 +263,75 @@ __global__ void __launch_bounds__(kThreads) k_axis_c2c(typename C2<T>::type* __r
     } else {
         r = smem_fft<false>(a, b, P, PS, pl, tw);
         if (MODE == 2) {
-            // last axis: o is the filter index
-            const double* cf = coef + o * cstride + 4;
-            const int nx = d.nx;
+            const double* cf = coef + o * cstride + 4;   // o is the filter index on the last axis
             double ntot = 1.0;
-            for (int q = 0; q < nx; ++q) ntot *= d.n[q];
+#pragma unroll
+            for (int q = 0; q < NX; ++q) ntot *= d.n[q];
             const double mult = mp.s / ntot;
-            for (int t = threadIdx.x; t < P * N; t += blockDim.x) {
-                int p = t / N, j = t - p * N;
-                long long i = i0 + p;
-                if (i >= I) continue;
-                double kap[4], kx[4];
+            const int l = mp.l;
+            const bool cached = l <= LCAP;
+            double* pg = reinterpret_cast<double*>(b + P * PS);    // [P][l][2]: gam, bet
+            constexpr int L = NX - 1;
+            auto pencil_k = [&](long long i, double* kap, double* kx) {
                 long long rem = i;
-                int k0 = (int)(rem % d.H0);
+                const int k0 = (int)(rem % d.H0);
                 rem /= d.H0;
                 wavenum(k0, d.n[0], kap[0], kx[0]);
-                for (int q = 1; q < m; ++q) {
-                    int kq = (int)(rem % d.n[q]);
+#pragma unroll
+                for (int q = 1; q < L; ++q) {
+                    const int kq = (int)(rem % d.n[q]);
                     rem /= d.n[q];
                     wavenum(kq, d.n[q], kap[q], kx[q]);
                 }
-                wavenum(j, N, kap[m], kx[m]);
-                T ps = (T)psi_point(nx, mp.l, cf, kap, kx, mult);
+            };
+            auto gam_bet = [&](const double* kap, const double* kx, int n, double& gam, double& bet) {
+                const double* c = cf + 10 * n;
+                double g = 1.0, bb = 0.0;
+#pragma unroll
+                for (int a2 = 0; a2 < L; ++a2) {
+                    g = fma(c[a2], kap[a2] * kap[a2], g);
+#pragma unroll
+                    for (int b2 = a2 + 1; b2 < L; ++b2) g = fma(c[pair_index(NX, a2, b2)], kx[a2] * kx[b2], g);
+                    bb = fma(c[pair_index(NX, a2, L)], kx[a2], bb);
+                }
+                gam = g;
+                bet = bb;
+            };
+            if (cached) {
+                for (int t = threadIdx.x; t < P * l; t += blockDim.x) {
+                    const int p = t / l, n = t - p * l;
+                    const long long i = i0 + p;
+                    double kap[4] = {0, 0, 0, 0}, kx[4] = {0, 0, 0, 0};
+                    if (i < I) pencil_k(i, kap, kx);
+                    double g, bb;
+                    gam_bet(kap, kx, n, g, bb);
+                    pg[2 * t] = g;
+                    pg[2 * t + 1] = bb;
+                }
+                __syncthreads();
+            }
+            for (int t = threadIdx.x; t < P * N; t += blockDim.x) {
+                const int p = t / N, j = t - p * N;
+                const long long i = i0 + p;
+                if (i >= I) continue;
+                double kapL, kxL;
+                wavenum(j, N, kapL, kxL);
+                const double kL2 = kapL * kapL;
+                double prod = 1.0;
+                if (cached) {
+                    const double* g = pg + 2 * p * l;
+                    for (int n = 0; n < l; ++n)
+                        prod *= fma(cf[10 * n + L], kL2, fma(g[2 * n + 1], kxL, g[2 * n]));
+                } else {
+                    double kap[4] = {0, 0, 0, 0}, kx[4] = {0, 0, 0, 0};
+                    pencil_k(i, kap, kx);
+                    for (int n = 0; n < l; ++n) {
+                        double g, bb;
+                        gam_bet(kap, kx, n, g, bb);
+                        prod *= fma(cf[10 * n + L], kL2, fma(bb, kxL, g));
+                    }
+                }
+                const T ps = (T)(mult / prod);
                 V v = r[p * PS + j];
                 r[p * PS + j] = V{v.x * ps, v.y * ps};
             }
@@ -193,74 +341,99 @@ __global__ void __launch_bounds__(kThreads) k_axis_c2c(typename C2<T>::type* __r
         }
     }
     for (int t = threadIdx.x; t < P * N; t += blockDim.x) {
-        int p = t % P, j = t / P;
+        const int j = t / P, p = t - j * P;
         long long i = i0 + p;
         if (i < I) base[(long long)j * I + i] = r[p * PS + j];
     }
 }
 
-// ============================================================================ point helpers
-__device__ __forceinline__ void point_u(const Dims& d, long long pt, double* u) {
-    long long rem = pt;
-    for (int q = 0; q < d.nx; ++q) {
-        int j = (int)(rem % d.n[q]);
-        rem /= d.n[q];
-        u[q] = j - 0.5 * (d.n[q] - 1);
-    }
-}
-
-__device__ __forceinline__ void phys(int nx, const FilterState& f, const double* u, double* x) {
-    for (int a = 0; a < nx; ++a) {
-        double s = f.c[a];
-        for (int b = 0; b < nx; ++b) s = fma(f.B[a * 4 + b], u[b], s);
-        x[a] = s;
-    }
-}
-
 // ============================================================================ axis-0 C2R (+ update)
-template <typename T, bool UPDATE>
+// Per row the likelihood exponent is a quadratic in u0: e = A_p + u0 (B_p + G00 u0).
+template <typename T, bool UPDATE, int NX>
 __global__ void __launch_bounds__(kThreads) k_axis0_c2r(const typename C2<T>::type* __restrict__ S, T* __restrict__ W,
-                                                         const FilterState* __restrict__ st, Dims d, FFTPlan pl,
-                                                         const typename C2<T>::type* __restrict__ tw, int P,
-                                                         LikParams lp, const double* __restrict__ z,
+                                                         const FilterState* __restrict__ st, Dims d, DivSet dv,
+                                                         FFTPlan pl, const typename C2<T>::type* __restrict__ tw,
+                                                         int P, LikParams lp, const double* __restrict__ z,
+                                                         const double* __restrict__ coef, int cstride, int lqo,
                                                          double* __restrict__ partials) {
     using V = typename C2<T>::type;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int N = d.n[0], PS = N + 1;
     V* a = reinterpret_cast<V*>(smem_raw);
     V* b = a + P * PS;
-    double* red = reinterpret_cast<double*>(b + P * PS);
+    double* red = reinterpret_cast<double*>(b + P * PS);            // 32 * NMOM
+    double* rowu = red + 32 * NMOM;                                  // [P][6]: u_1..u_3, A_p, B_p
     const long long rpf = d.ntot / N;
     const long long row0 = (long long)blockIdx.x * P;
     const int filt = (int)(row0 / rpf);
     const V* src = S + row0 * d.H0;
+    const float invN = 1.0f / N;
     for (int i = threadIdx.x; i < P * N; i += blockDim.x) {
-        int p = i / N, k = i - p * N;
+        const int p = (int)((i + 0.5f) * invN), k = i - p * N;
         V v;
         if (k < d.H0) v = src[p * d.H0 + k];
         else { v = src[p * d.H0 + (N - k)]; v.y = -v.y; }
         a[p * PS + k] = v;
     }
+    const FilterState& f = st[filt];
+    const double* q = coef + (long long)filt * cstride + lqo;
+    if (UPDATE) {
+        for (int p = threadIdx.x; p < P; p += blockDim.x) {
+            double u[4] = {0, 0, 0, 0};
+            unsigned rr = (unsigned)(row0 + p - (long long)filt * rpf);
+#pragma unroll
+            for (int a2 = 1; a2 < NX; ++a2) {
+                const unsigned qq = (a2 < NX - 1) ? fdiv(rr, dv.n[a2]) : 0u;
+                const unsigned j = (a2 < NX - 1) ? rr - qq * (unsigned)d.n[a2] : rr;
+                u[a2] = (double)j - 0.5 * (d.n[a2] - 1);
+                rr = qq;
+            }
+            double A = q[0], Bc = q[1];
+#pragma unroll
+            for (int a2 = 1; a2 < NX; ++a2) {
+                A = fma(q[1 + a2], u[a2], A);
+                Bc = fma(q[5 + tri(0, a2)], u[a2], Bc);
+#pragma unroll
+                for (int b2 = a2; b2 < NX; ++b2) A = fma(q[5 + tri(a2, b2)] * u[a2], u[b2], A);
+            }
+            double* ru = rowu + 6 * p;
+            ru[0] = u[1];
+            ru[1] = u[2];
+            ru[2] = u[3];
+            ru[3] = A;
+            ru[4] = Bc;
+        }
+    }
     __syncthreads();
     V* r = smem_fft<true>(a, b, P, PS, pl, tw);
-    const FilterState& f = st[filt];
     const double scale = f.scale;
-    const double* zf = z + (long long)filt * lp.nz;
     double acc[NMOM];
+#pragma unroll
     for (int i = 0; i < NMOM; ++i) acc[i] = 0.0;
     T* dst = W + row0 * N;
-    const long long pt_base = row0 * N - (long long)filt * d.ntot;
+    const double g00 = q[5];
+    const double* zf = z + (long long)filt * lp.nz;
     for (int i = threadIdx.x; i < P * N; i += blockDim.x) {
-        int p = i / N, j = i - p * N;
+        const int p = (int)((i + 0.5f) * invN), j = i - p * N;
         double w = (double)r[p * PS + j].x;
         if (UPDATE) {
-            double u[4], x[4];
-            point_u(d, pt_base + i, u);
-            phys(d.nx, f, u, x);
-            w = w * scale * exp_fast(log_lik(lp, x, zf));
-            T wt = (T)w;
+            const double* ru = rowu + 6 * p;
+            double u[4];
+            u[0] = j - 0.5 * (N - 1);
+#pragma unroll
+            for (int a2 = 1; a2 < NX; ++a2) u[a2] = ru[a2 - 1];
+            double ll;
+            if (lp.kind == 0) {
+                const double e = fma(u[0], fma(g00, u[0], ru[4]), ru[3]);
+                ll = fma(-0.5, e, lp.lognorm);
+            } else {
+                double x[4];
+                phys<NX>(f, u, x);
+                ll = log_lik(lp, x, zf);
+            }
+            const T wt = (T)(w * scale * exp_fast(ll));
             dst[i] = wt;
-            acc_moments(d.nx, (double)wt, u, acc);
+            acc_mom<NX>((double)wt, u, acc);
         } else {
             dst[i] = (T)w;
         }
@@ -268,7 +441,7 @@ __global__ void __launch_bounds__(kThreads) k_axis0_c2r(const typename C2<T>::ty
     if (UPDATE) {
         block_sum<NMOM>(acc, red);
         if (threadIdx.x == 0)
-            for (int q = 0; q < NMOM; ++q) partials[(long long)blockIdx.x * NMOM + q] = acc[q];
+            for (int q2 = 0; q2 < NMOM; ++q2) partials[(long long)blockIdx.x * NMOM + q2] = acc[q2];
     }
 }
 
@@ -296,7 +469,9 @@ __global__ void __launch_bounds__(kThreads) k_line_psi(T* __restrict__ W, Filter
     for (int k = threadIdx.x; k < N; k += blockDim.x) {
         double kap, kx;
         wavenum(k, N, kap, kx);
-        T ps = (T)psi_point(1, mp.l, cf + 4, &kap, &kx, mult);
+        double prod = 1.0;
+        for (int n = 0; n < mp.l; ++n) prod *= fma(cf[4 + 10 * n], kap * kap, 1.0);
+        const T ps = (T)(mult / prod);
         V v = r[k];
         r[k] = V{v.x * ps, v.y * ps};
     }
@@ -304,6 +479,7 @@ __global__ void __launch_bounds__(kThreads) k_line_psi(T* __restrict__ W, Filter
     r = smem_fft<true>(r, (r == a) ? b : a, 1, PS, pl, tw);
     const FilterState& f = st[filt];
     double acc[NMOM];
+#pragma unroll
     for (int i = 0; i < NMOM; ++i) acc[i] = 0.0;
     const double scale = f.scale;
     const double* zf = z + (long long)filt * lp.nz;
@@ -311,11 +487,11 @@ __global__ void __launch_bounds__(kThreads) k_line_psi(T* __restrict__ W, Filter
         double w = (double)r[j].x;
         if (UPDATE) {
             double u = j - 0.5 * (N - 1), x;
-            phys(1, f, &u, &x);
+            phys<1>(f, &u, &x);
             w = w * scale * exp_fast(log_lik(lp, &x, zf));
             T wt = (T)w;
             row[j] = wt;
-            acc_moments(1, (double)wt, &u, acc);
+            acc_mom<1>((double)wt, &u, acc);
         } else {
             row[j] = (T)w;
         }
@@ -328,44 +504,49 @@ __global__ void __launch_bounds__(kThreads) k_line_psi(T* __restrict__ W, Filter
 }
 
 // ============================================================================ per-filter point kernels
-// grid: batch * nbpf blocks; block (filt, q) covers points q, q+nbpf*blockDim, ...
+// grid: batch * nbpf blocks; block (filt, q) covers points q*blockDim + k*nbpf*blockDim
 static int blocks_per_filter(long long ntot) {
     long long nb = (ntot + kThreads * 8 - 1) / (kThreads * 8);
-    return (int)std::max(1LL, std::min(nb, 512LL));
+    return (int)std::max(1LL, std::min(nb, 1024LL));
 }
 
-template <typename T, int MODE>   // 0: standalone update, 1: init gaussian, 2: plain sum
+template <typename T, int MODE, int NX>   // 0: standalone update, 1: init gaussian, 2: plain sum
 __global__ void __launch_bounds__(kThreads) k_points(T* __restrict__ W, const FilterState* __restrict__ st, Dims d,
-                                                      int nbpf, LikParams lp, const double* __restrict__ z,
-                                                      const double* __restrict__ gauss,
+                                                      DivSet dv, int nbpf, LikParams lp,
+                                                      const double* __restrict__ z, const double* __restrict__ gauss,
                                                       double* __restrict__ partials) {
     __shared__ double red[32 * NMOM];
-    const int filt = blockIdx.x / nbpf, q = blockIdx.x - filt * nbpf;
+    const int filt = blockIdx.x / nbpf, qb = blockIdx.x - filt * nbpf;
     const FilterState& f = st[filt];
     T* Wf = W + (long long)filt * d.ntot;
     double acc[NMOM];
+#pragma unroll
     for (int i = 0; i < NMOM; ++i) acc[i] = 0.0;
     const double* zf = z ? z + (long long)filt * lp.nz : nullptr;
     const double* g = gauss ? gauss + (long long)filt * 21 : nullptr;
-    for (long long pt = (long long)q * blockDim.x + threadIdx.x; pt < d.ntot; pt += (long long)nbpf * blockDim.x) {
+    for (long long pt = (long long)qb * blockDim.x + threadIdx.x; pt < d.ntot; pt += (long long)nbpf * blockDim.x) {
         double u[4], x[4];
-        point_u(d, pt, u);
+        if (MODE != 2) {
+            point_u<NX>(d, dv, (unsigned)pt, u);
+            phys<NX>(f, u, x);
+        }
         if (MODE == 0) {
-            phys(d.nx, f, u, x);
-            double w = (double)Wf[pt] * f.scale * exp_fast(log_lik(lp, x, zf));
-            T wt = (T)w;
+            const double w = (double)Wf[pt] * f.scale * exp_fast(log_lik(lp, x, zf));
+            const T wt = (T)w;
             Wf[pt] = wt;
-            acc_moments(d.nx, (double)wt, u, acc);
+            acc_mom<NX>((double)wt, u, acc);
         } else if (MODE == 1) {
-            phys(d.nx, f, u, x);
-            double r[4], e = 0.0;
-            for (int a = 0; a < d.nx; ++a) r[a] = x[a] - g[a];
-            for (int a = 0; a < d.nx; ++a) {
+            double rr[4], e = 0.0;
+#pragma unroll
+            for (int a = 0; a < NX; ++a) rr[a] = x[a] - g[a];
+#pragma unroll
+            for (int a = 0; a < NX; ++a) {
                 double t = 0.0;
-                for (int b = 0; b < d.nx; ++b) t = fma(g[4 + a * 4 + b], r[b], t);
-                e = fma(r[a], t, e);
+#pragma unroll
+                for (int b = 0; b < NX; ++b) t = fma(g[4 + a * 4 + b], rr[b], t);
+                e = fma(rr[a], t, e);
             }
-            T wt = (T)exp(fma(-0.5, e, g[20]));
+            const T wt = (T)exp(fma(-0.5, e, g[20]));
             Wf[pt] = wt;
             acc[0] += (double)wt;
         } else {
@@ -377,28 +558,27 @@ __global__ void __launch_bounds__(kThreads) k_points(T* __restrict__ W, const Fi
         for (int i = 0; i < NMOM; ++i) partials[(long long)blockIdx.x * NMOM + i] = acc[i];
 }
 
-// ============================================================================ finalisers (1 warp per filter)
-__device__ inline void warp_sum_partials(const double* __restrict__ partials, long long first, int nb, double* acc) {
-    const int lane = threadIdx.x & 31;
+// ============================================================================ finalisers (1 block per filter)
+// Fixed-order sums of the per-CTA partials: thread k sums partials k, k+256, ...,
+// then a fixed tree (block_sum) -- deterministic for a given launch geometry.
+__device__ inline void block_sum_partials(const double* __restrict__ partials, long long first, int nb, double* acc,
+                                          double* red) {
+#pragma unroll
     for (int i = 0; i < NMOM; ++i) acc[i] = 0.0;
-    for (int k = lane; k < nb; k += 32)
+    for (int k = threadIdx.x; k < nb; k += blockDim.x)
+#pragma unroll
         for (int i = 0; i < NMOM; ++i) acc[i] += partials[(first + k) * NMOM + i];
-    for (int i = 0; i < NMOM; ++i) {
-        double x = acc[i];
-        for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
-        acc[i] = x;
-    }
+    block_sum<NMOM>(acc, red);
 }
 
 // MODE 0: update -> normaliser C = vol * sum, log C, scale = 1/C, moments.
 // MODE 1: renormalise (init/set_state): scale = 1/(vol * sum).
-__global__ void k_finalize(FilterState* st, const double* __restrict__ partials, int nbpf, int batch, Dims d,
-                           int mode) {
-    const int filt = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
-    if (filt >= batch) return;
+__global__ void k_finalize(FilterState* st, const double* __restrict__ partials, int nbpf, Dims d, int mode) {
+    __shared__ double red[32 * NMOM];
+    const int filt = blockIdx.x;
     double acc[NMOM];
-    warp_sum_partials(partials, (long long)filt * nbpf, nbpf, acc);
-    if ((threadIdx.x & 31) != 0) return;
+    block_sum_partials(partials, (long long)filt * nbpf, nbpf, acc, red);
+    if (threadIdx.x != 0) return;
     FilterState& f = st[filt];
     const int nx = d.nx;
     double vol = fabs(det4(nx, f.B));
@@ -424,62 +604,79 @@ __global__ void k_finalize(FilterState* st, const double* __restrict__ partials,
 // ============================================================================ regrid
 // Multilinear interpolation with zero ghost nodes at the points of the new grid
 // (R12). v = B^-1 (x' - c) + (N-1)/2 = o + M u' with M = B^-1 B', o = B^-1(c'-c)+(N-1)/2.
-template <typename T>
+template <typename T, int NX>
 __global__ void __launch_bounds__(kThreads) k_regrid_gather(const T* __restrict__ Wold, T* __restrict__ Wnew,
-                                                             const FilterState* __restrict__ st, Dims d, int nbpf,
-                                                             double ks, double* __restrict__ partials) {
+                                                             const FilterState* __restrict__ st, Dims d, DivSet dv,
+                                                             int nbpf, double ks, double* __restrict__ partials) {
     __shared__ double red[32 * NMOM];
     __shared__ double Msh[16], osh[4];
-    const int filt = blockIdx.x / nbpf, q = blockIdx.x - filt * nbpf;
+    const int filt = blockIdx.x / nbpf, qb = blockIdx.x - filt * nbpf;
     const FilterState& f = st[filt];
-    const int nx = d.nx;
     if (threadIdx.x == 0) {
         double cn[4], Bn[16], Bi[16];
-        regrid_target(nx, d.n, f, ks, cn, Bn);
-        mat_inv4(nx, f.B, Bi);
+        regrid_target(NX, d.n, f, ks, cn, Bn);
+        mat_inv4(NX, f.B, Bi);
         double M[16];
         for (int i = 0; i < 16; ++i) M[i] = 0.0;
-        mat_mul4(nx, Bi, Bn, M);
+        mat_mul4(NX, Bi, Bn, M);
         for (int i = 0; i < 16; ++i) Msh[i] = M[i];
-        for (int a = 0; a < nx; ++a) {
+        for (int a = 0; a < NX; ++a) {
             double s = 0.5 * (d.n[a] - 1);
-            for (int b = 0; b < nx; ++b) s = fma(Bi[a * 4 + b], cn[b] - f.c[b], s);
+            for (int b = 0; b < NX; ++b) s = fma(Bi[a * 4 + b], cn[b] - f.c[b], s);
             osh[a] = s;
         }
     }
     __syncthreads();
+    double M[16], o[4];
+#pragma unroll
+    for (int i = 0; i < NX; ++i) {
+        o[i] = osh[i];
+#pragma unroll
+        for (int j = 0; j < NX; ++j) M[i * 4 + j] = Msh[i * 4 + j];
+    }
+    long long stride[4];
+    stride[0] = 1;
+#pragma unroll
+    for (int a = 1; a < NX; ++a) stride[a] = stride[a - 1] * d.n[a - 1];
     const T* Wo = Wold + (long long)filt * d.ntot;
     T* Wn = Wnew + (long long)filt * d.ntot;
     double acc[NMOM];
+#pragma unroll
     for (int i = 0; i < NMOM; ++i) acc[i] = 0.0;
-    for (long long pt = (long long)q * blockDim.x + threadIdx.x; pt < d.ntot; pt += (long long)nbpf * blockDim.x) {
-        double u[4], v[4], fr[4];
-        int i0[4];
-        point_u(d, pt, u);
-        for (int a = 0; a < nx; ++a) {
-            double s = osh[a];
-            for (int b = 0; b < nx; ++b) s = fma(Msh[a * 4 + b], u[b], s);
-            v[a] = s;
-            double fl = floor(s);
-            i0[a] = (int)fmax(fmin(fl, 1e9), -1e9);
+    for (long long pt = (long long)qb * blockDim.x + threadIdx.x; pt < d.ntot; pt += (long long)nbpf * blockDim.x) {
+        double u[4];
+        point_u<NX>(d, dv, (unsigned)pt, u);
+        double fr[4];
+        long long base = 0;
+        bool lo_ok[4], hi_ok[4];
+#pragma unroll
+        for (int a = 0; a < NX; ++a) {
+            double s = o[a];
+#pragma unroll
+            for (int b = 0; b < NX; ++b) s = fma(M[a * 4 + b], u[b], s);
+            const double fl = floor(s);
+            const int i0 = __double2int_rz(fl);           // saturating
             fr[a] = s - fl;
+            lo_ok[a] = i0 >= 0 && i0 <= d.n[a] - 1;
+            hi_ok[a] = i0 >= -1 && i0 <= d.n[a] - 2;
+            base += (long long)i0 * stride[a];
         }
         double val = 0.0;
-        for (int corner = 0; corner < (1 << nx); ++corner) {
+#pragma unroll
+        for (int corner = 0; corner < (1 << NX); ++corner) {
             double wt = 1.0;
-            long long off = 0, stride = 1;
+            long long off = base;
             bool ok = true;
-            for (int a = 0; a < nx; ++a) {
-                int bit = (corner >> a) & 1;
-                int ia = i0[a] + bit;
+#pragma unroll
+            for (int a = 0; a < NX; ++a) {
+                const bool bit = (corner >> a) & 1;
                 wt *= bit ? fr[a] : (1.0 - fr[a]);
-                ok = ok && ia >= 0 && ia <= d.n[a] - 1;
-                off += (long long)ia * stride;
-                stride *= d.n[a];
+                ok = ok && (bit ? hi_ok[a] : lo_ok[a]);
+                if (bit) off += stride[a];
             }
             if (ok) val = fma(wt, (double)Wo[off], val);
         }
-        T vt = (T)val;
+        const T vt = (T)val;
         Wn[pt] = vt;
         acc[0] += (double)vt;
     }
@@ -488,13 +685,12 @@ __global__ void __launch_bounds__(kThreads) k_regrid_gather(const T* __restrict_
         for (int i = 0; i < NMOM; ++i) partials[(long long)blockIdx.x * NMOM + i] = acc[i];
 }
 
-__global__ void k_finalize_regrid(FilterState* st, const double* __restrict__ partials, int nbpf, int batch,
-                                  Dims d, double ks) {
-    const int filt = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
-    if (filt >= batch) return;
+__global__ void k_finalize_regrid(FilterState* st, const double* __restrict__ partials, int nbpf, Dims d, double ks) {
+    __shared__ double red[32 * NMOM];
+    const int filt = blockIdx.x;
     double acc[NMOM];
-    warp_sum_partials(partials, (long long)filt * nbpf, nbpf, acc);
-    if ((threadIdx.x & 31) != 0) return;
+    block_sum_partials(partials, (long long)filt * nbpf, nbpf, acc, red);
+    if (threadIdx.x != 0) return;
     FilterState& f = st[filt];
     double cn[4], Bn[16];
     bool ok = regrid_target(d.nx, d.n, f, ks, cn, Bn);
@@ -547,37 +743,11 @@ static cudaError_t smem_attr(K kernel, size_t bytes) {
     return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
 }
 
-template <typename T>
-static cudaError_t predict_pencil_t(const Dims& d, PencilBufs& b, const Twiddles& tw, const ModelParams& mp,
-                                    const LikParams* lp, cudaStream_t s, int64_t* launches) {
+template <typename T, int NX>
+static cudaError_t predict_nd(const Dims& d, PencilBufs& b, const Twiddles& tw, const ModelParams& mp,
+                              const LikParams* lp, const LikParams& lpv, int cs, cudaStream_t s, int64_t* launches) {
     using V = typename C2<T>::type;
-    const int cs = coef_stride(mp.l);
-    if (b.ev0) cudaEventRecord(b.ev0, s);
-    k_predict_prep<<<(d.batch + 127) / 128, 128, 0, s>>>(b.st, b.coef, cs, mp, b.sub, d.batch);
-    ++*launches;
-    PMF_TRY(cudaGetLastError());
-    LikParams lpv{};
-    if (lp) lpv = *lp;
-    if (d.nx == 1) {
-        FFTPlan pl = make_plan(d.n[0]);
-        size_t sm = 2 * (d.n[0] + 1) * sizeof(V) + 32 * NMOM * sizeof(double);
-        PMF_TRY(smem_attr(k_line_psi<T, true>, sm));
-        PMF_TRY(smem_attr(k_line_psi<T, false>, sm));
-        if (lp)
-            k_line_psi<T, true><<<d.batch, kThreads, sm, s>>>((T*)b.W, b.st, d, pl, (const V*)tw.tw[0], b.coef, cs,
-                                                              mp, lpv, b.z, b.partials);
-        else
-            k_line_psi<T, false><<<d.batch, kThreads, sm, s>>>((T*)b.W, b.st, d, pl, (const V*)tw.tw[0], b.coef, cs,
-                                                               mp, lpv, b.z, b.partials);
-        ++*launches;
-        PMF_TRY(cudaGetLastError());
-        if (lp) {
-            k_finalize<<<(d.batch + 3) / 4, 128, 0, s>>>(b.st, b.partials, 1, d.batch, d, 0);
-            ++*launches;
-        }
-        if (b.ev1) cudaEventRecord(b.ev1, s);
-        return cudaGetLastError();
-    }
+    const DivSet dv = make_divs(d);
     // axis 0 forward (R2C)
     const int N0 = d.n[0];
     const long long rpf = d.ntot / N0;
@@ -600,19 +770,21 @@ static cudaError_t predict_pencil_t(const Dims& d, PencilBufs& b, const Twiddles
         const int P = pencils_per_cta(N);
         FFTPlan pl = make_plan(N);
         size_t sm = 2 * (size_t)P * (N + 1) * sizeof(V);
+        if (mode == 2) sm += sizeof(double) * 2 * P * std::min(mp.l, LCAP);
         long long nblk = O * ((I + P - 1) / P);
-        PMF_TRY(smem_attr(k_axis_c2c<T, 0>, sm));
-        PMF_TRY(smem_attr(k_axis_c2c<T, 1>, sm));
-        PMF_TRY(smem_attr(k_axis_c2c<T, 2>, sm));
-        if (mode == 0)
-            k_axis_c2c<T, 0><<<(unsigned)nblk, kThreads, sm, s>>>((V*)b.S, d, m, I, pl, (const V*)tw.tw[m], P,
-                                                                   b.coef, cs, mp);
-        else if (mode == 1)
-            k_axis_c2c<T, 1><<<(unsigned)nblk, kThreads, sm, s>>>((V*)b.S, d, m, I, pl, (const V*)tw.tw[m], P,
-                                                                   b.coef, cs, mp);
-        else
-            k_axis_c2c<T, 2><<<(unsigned)nblk, kThreads, sm, s>>>((V*)b.S, d, m, I, pl, (const V*)tw.tw[m], P,
-                                                                   b.coef, cs, mp);
+        if (mode == 0) {
+            PMF_TRY(smem_attr(k_axis_c2c<T, 0, NX>, sm));
+            k_axis_c2c<T, 0, NX><<<(unsigned)nblk, kThreads, sm, s>>>((V*)b.S, d, m, I, pl, (const V*)tw.tw[m], P,
+                                                                       b.coef, cs, mp);
+        } else if (mode == 1) {
+            PMF_TRY(smem_attr(k_axis_c2c<T, 1, NX>, sm));
+            k_axis_c2c<T, 1, NX><<<(unsigned)nblk, kThreads, sm, s>>>((V*)b.S, d, m, I, pl, (const V*)tw.tw[m], P,
+                                                                       b.coef, cs, mp);
+        } else {
+            PMF_TRY(smem_attr(k_axis_c2c<T, 2, NX>, sm));
+            k_axis_c2c<T, 2, NX><<<(unsigned)nblk, kThreads, sm, s>>>((V*)b.S, d, m, I, pl, (const V*)tw.tw[m], P,
+                                                                       b.coef, cs, mp);
+        }
         ++*launches;
         return cudaGetLastError();
     };
@@ -620,25 +792,67 @@ static cudaError_t predict_pencil_t(const Dims& d, PencilBufs& b, const Twiddles
     PMF_TRY(strided(d.nx - 1, 2));
     for (int m = d.nx - 2; m >= 1; --m) PMF_TRY(strided(m, 1));
     // axis 0 inverse (C2R) + update
-    size_t smc = sm0 + 32 * NMOM * sizeof(double);
-    PMF_TRY(smem_attr(k_axis0_c2r<T, true>, smc));
-    PMF_TRY(smem_attr(k_axis0_c2r<T, false>, smc));
-    if (lp)
-        k_axis0_c2r<T, true><<<(unsigned)nrow_blocks, kThreads, smc, s>>>((const V*)b.S, (T*)b.W, b.st, d, pl0,
-                                                                          (const V*)tw.tw[0], P0, lpv, b.z,
-                                                                          b.partials);
-    else
-        k_axis0_c2r<T, false><<<(unsigned)nrow_blocks, kThreads, smc, s>>>((const V*)b.S, (T*)b.W, b.st, d, pl0,
-                                                                           (const V*)tw.tw[0], P0, lpv, b.z,
-                                                                           b.partials);
+    size_t smc = sm0 + 32 * NMOM * sizeof(double) + 6 * sizeof(double) * P0;
+    if (lp) {
+        PMF_TRY(smem_attr(k_axis0_c2r<T, true, NX>, smc));
+        k_axis0_c2r<T, true, NX><<<(unsigned)nrow_blocks, kThreads, smc, s>>>(
+            (const V*)b.S, (T*)b.W, b.st, d, dv, pl0, (const V*)tw.tw[0], P0, lpv, b.z, b.coef, cs, lq_off(mp.l),
+            b.partials);
+    } else {
+        PMF_TRY(smem_attr(k_axis0_c2r<T, false, NX>, smc));
+        k_axis0_c2r<T, false, NX><<<(unsigned)nrow_blocks, kThreads, smc, s>>>(
+            (const V*)b.S, (T*)b.W, b.st, d, dv, pl0, (const V*)tw.tw[0], P0, lpv, b.z, b.coef, cs, lq_off(mp.l),
+            b.partials);
+    }
     ++*launches;
     PMF_TRY(cudaGetLastError());
     if (lp) {
-        k_finalize<<<(d.batch + 3) / 4, 128, 0, s>>>(b.st, b.partials, (int)(rpf / P0), d.batch, d, 0);
+        k_finalize<<<d.batch, kThreads, 0, s>>>(b.st, b.partials, (int)(rpf / P0), d, 0);
         ++*launches;
     }
-    if (b.ev1) cudaEventRecord(b.ev1, s);
     return cudaGetLastError();
+}
+
+template <typename T>
+static cudaError_t predict_pencil_t(const Dims& d, PencilBufs& b, const Twiddles& tw, const ModelParams& mp,
+                                    const LikParams* lp, cudaStream_t s, int64_t* launches) {
+    using V = typename C2<T>::type;
+    const int cs = coef_stride(mp.l);
+    LikParams lpv{};
+    if (lp) lpv = *lp;
+    if (b.ev0) cudaEventRecord(b.ev0, s);
+    k_predict_prep<<<(d.batch + 127) / 128, 128, 0, s>>>(b.st, b.coef, cs, mp, b.sub, d.batch, lpv, b.z,
+                                                         lp ? 1 : 0);
+    ++*launches;
+    PMF_TRY(cudaGetLastError());
+    cudaError_t e = cudaSuccess;
+    if (d.nx == 1) {
+        FFTPlan pl = make_plan(d.n[0]);
+        size_t sm = 2 * (d.n[0] + 1) * sizeof(V) + 32 * NMOM * sizeof(double);
+        PMF_TRY(smem_attr(k_line_psi<T, true>, sm));
+        PMF_TRY(smem_attr(k_line_psi<T, false>, sm));
+        if (lp)
+            k_line_psi<T, true><<<d.batch, kThreads, sm, s>>>((T*)b.W, b.st, d, pl, (const V*)tw.tw[0], b.coef, cs,
+                                                              mp, lpv, b.z, b.partials);
+        else
+            k_line_psi<T, false><<<d.batch, kThreads, sm, s>>>((T*)b.W, b.st, d, pl, (const V*)tw.tw[0], b.coef, cs,
+                                                               mp, lpv, b.z, b.partials);
+        ++*launches;
+        PMF_TRY(cudaGetLastError());
+        if (lp) {
+            k_finalize<<<d.batch, kThreads, 0, s>>>(b.st, b.partials, 1, d, 0);
+            ++*launches;
+        }
+        e = cudaGetLastError();
+    } else if (d.nx == 2) {
+        e = predict_nd<T, 2>(d, b, tw, mp, lp, lpv, cs, s, launches);
+    } else if (d.nx == 3) {
+        e = predict_nd<T, 3>(d, b, tw, mp, lp, lpv, cs, s, launches);
+    } else {
+        e = predict_nd<T, 4>(d, b, tw, mp, lp, lpv, cs, s, launches);
+    }
+    if (b.ev1) cudaEventRecord(b.ev1, s);
+    return e;
 }
 
 cudaError_t launch_predict_pencil(const Dims& d, int dtype, PencilBufs& b, const Twiddles& tw,
@@ -647,17 +861,28 @@ cudaError_t launch_predict_pencil(const Dims& d, int dtype, PencilBufs& b, const
     return predict_pencil_t<float>(d, b, tw, mp, lp, s, launches);
 }
 
+template <typename T, int MODE, int NX>
+static cudaError_t points_nd(const Dims& d, PencilBufs& b, const LikParams& lp, cudaStream_t s, int64_t* launches,
+                             int fin_mode) {
+    int nbpf = blocks_per_filter(d.ntot);
+    k_points<T, MODE, NX><<<(unsigned)((long long)nbpf * d.batch), kThreads, 0, s>>>(
+        (T*)b.W, b.st, d, make_divs(d), nbpf, lp, b.z, b.gauss, b.partials);
+    ++*launches;
+    PMF_TRY(cudaGetLastError());
+    k_finalize<<<d.batch, kThreads, 0, s>>>(b.st, b.partials, nbpf, d, fin_mode);
+    ++*launches;
+    return cudaGetLastError();
+}
+
 template <typename T, int MODE>
 static cudaError_t points_t(const Dims& d, PencilBufs& b, const LikParams& lp, cudaStream_t s, int64_t* launches,
                             int fin_mode) {
-    int nbpf = blocks_per_filter(d.ntot);
-    k_points<T, MODE><<<(unsigned)((long long)nbpf * d.batch), kThreads, 0, s>>>((T*)b.W, b.st, d, nbpf, lp, b.z,
-                                                                                 b.gauss, b.partials);
-    ++*launches;
-    PMF_TRY(cudaGetLastError());
-    k_finalize<<<(d.batch + 3) / 4, 128, 0, s>>>(b.st, b.partials, nbpf, d.batch, d, fin_mode);
-    ++*launches;
-    return cudaGetLastError();
+    switch (d.nx) {
+        case 1: return points_nd<T, MODE, 1>(d, b, lp, s, launches, fin_mode);
+        case 2: return points_nd<T, MODE, 2>(d, b, lp, s, launches, fin_mode);
+        case 3: return points_nd<T, MODE, 3>(d, b, lp, s, launches, fin_mode);
+        default: return points_nd<T, MODE, 4>(d, b, lp, s, launches, fin_mode);
+    }
 }
 
 cudaError_t launch_update(const Dims& d, int dtype, PencilBufs& b, const LikParams& lp, cudaStream_t s,
@@ -678,17 +903,27 @@ cudaError_t launch_normalise_state(const Dims& d, int dtype, PencilBufs& b, cuda
     return points_t<float, 2>(d, b, lp, s, launches, 1);
 }
 
-template <typename T>
-static cudaError_t regrid_t(const Dims& d, PencilBufs& b, double ks, cudaStream_t s, int64_t* launches) {
+template <typename T, int NX>
+static cudaError_t regrid_nd(const Dims& d, PencilBufs& b, double ks, cudaStream_t s, int64_t* launches) {
     int nbpf = blocks_per_filter(d.ntot);
-    k_regrid_gather<T><<<(unsigned)((long long)nbpf * d.batch), kThreads, 0, s>>>((const T*)b.W, (T*)b.W2, b.st, d,
-                                                                                 nbpf, ks, b.partials);
+    k_regrid_gather<T, NX><<<(unsigned)((long long)nbpf * d.batch), kThreads, 0, s>>>(
+        (const T*)b.W, (T*)b.W2, b.st, d, make_divs(d), nbpf, ks, b.partials);
     ++*launches;
     PMF_TRY(cudaGetLastError());
-    k_finalize_regrid<<<(d.batch + 3) / 4, 128, 0, s>>>(b.st, b.partials, nbpf, d.batch, d, ks);
+    k_finalize_regrid<<<d.batch, kThreads, 0, s>>>(b.st, b.partials, nbpf, d, ks);
     ++*launches;
     std::swap(b.W, b.W2);
     return cudaGetLastError();
+}
+
+template <typename T>
+static cudaError_t regrid_t(const Dims& d, PencilBufs& b, double ks, cudaStream_t s, int64_t* launches) {
+    switch (d.nx) {
+        case 1: return regrid_nd<T, 1>(d, b, ks, s, launches);
+        case 2: return regrid_nd<T, 2>(d, b, ks, s, launches);
+        case 3: return regrid_nd<T, 3>(d, b, ks, s, launches);
+        default: return regrid_nd<T, 4>(d, b, ks, s, launches);
+    }
 }
 
 cudaError_t launch_regrid(const Dims& d, int dtype, PencilBufs& b, double ks, cudaStream_t s, int64_t* launches) {

@@ -466,7 +466,7 @@ int pmf_create(const pmf_config* cfg, const double* A, const double* Q, pmf_ctx*
     if (!r && c->path == PMF_PATH_PENCIL && nx > 1) r = dalloc(c, &c->S, 2 * c->esize * (size_t)d.nspec * d.batch);
     if (!r) r = dalloc(c, (void**)&c->st, sizeof(FilterState) * d.batch);
     // reduction scratch: the largest per-pass block count (pencil C2R rows / points kernels)
-    size_t nblk = (size_t)d.batch * 512;
+    size_t nblk = (size_t)d.batch * 1024;
     nblk = std::max(nblk, (size_t)(d.ntot / d.n[0]) * d.batch);
     c->partials_bytes = nblk * NMOM * sizeof(double);
     if (!r) r = dalloc(c, (void**)&c->partials, c->partials_bytes);

@@ -60,8 +60,9 @@ struct Dims {
 };
 
 // Number of doubles per filter in the pencil path's epoch-coefficient buffer.
-// pencil path: 4 + 10 l; resident path: 24 + 3 l rounded up to even (kernels_resident.cu)
-inline int coef_stride(int l) { return (4 + 10 * l) > (26 + 3 * l) ? (4 + 10 * l) : (26 + 3 * l); }
+// pencil path: 4 + 10 l + 16 (scale, Euler factors, likelihood quadratic form);
+// resident path: 24 + 3 l rounded up to even (kernels_resident.cu)
+inline int coef_stride(int l) { return (20 + 10 * l) > (26 + 3 * l) ? (20 + 10 * l) : (26 + 3 * l); }
 
 // ---------------------------------------------------------------------------
 // launchers (implemented in the .cu files); all return a cudaError_t and
