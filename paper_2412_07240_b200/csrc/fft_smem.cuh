@@ -6,6 +6,7 @@
 // computed once on the host in extended precision.
 #pragma once
 #include "device_common.cuh"
+#include "fft_reg.cuh"
 
 namespace pmf {
 
@@ -99,6 +100,92 @@ __device__ V* smem_fft(V* a, V* b, int P, int PS, const FFTPlan& pl, const V* __
         Ns *= R;
     }
     return a;
+}
+
+// ---------------------------------------------------------------------------
+// Compile-time Stockham FFT for the common pencil lengths: radix sequence,
+// strides and divisors are constants, radix-8 stages run reg::dft8.
+template <int N>
+__host__ __device__ constexpr int ct_nstages() {
+    return (N == 64 || N == 32 || N == 24 || N == 16 || N == 12) ? 2
+         : (N == 96 || N == 128 || N == 256 || N == 48 || N == 192 || N == 384 || N == 512) ? 3 : 0;
+}
+template <int N>
+__host__ __device__ constexpr int ct_radix(int st) {
+    // first stage (Ns = 1) takes the largest radix: no twiddles there
+    return N == 64 ? 8 : N == 32 ? (st == 0 ? 8 : 4) : N == 24 ? (st == 0 ? 8 : 3) : N == 16 ? 4 : N == 12 ? (st == 0 ? 4 : 3)
+         : N == 96 ? (st == 0 ? 8 : st == 1 ? 4 : 3) : N == 128 ? (st == 0 ? 8 : 4) : N == 256 ? (st < 2 ? 8 : 4)
+         : N == 48 ? (st < 2 ? 4 : 3) : N == 192 ? (st < 2 ? 8 : 3) : N == 384 ? (st < 2 ? 8 : 6) : N == 512 ? 8 : 0;
+}
+template <int N>
+inline constexpr bool ct_supported = ct_nstages<N>() > 0;
+
+template <int R, bool INV, typename V>
+__device__ __forceinline__ void reg_dft(V* v) {
+    if constexpr (R == 8) reg::dft8<INV>(v);
+    else if constexpr (R == 4) reg::r4<INV>(v[0], v[1], v[2], v[3]);
+    else if constexpr (R == 6) {
+        // 6 = 2 x 3: radix-3 over (0,2,4) and (1,3,5), twiddle W6, radix-2
+        V a[3] = {v[0], v[2], v[4]}, b[3] = {v[1], v[3], v[5]};
+        SmallDFT<3, INV, V>::run(a);
+        SmallDFT<3, INV, V>::run(b);
+        using T = decltype(v[0].x);
+        const T h = T(0.8660254037844386467637231707529361834714);
+        // W6^1 = (1/2, -h) forward, W6^2 = (-1/2, -h)
+        const T sg = INV ? h : -h;
+        b[1] = V{fma(b[1].x, T(0.5), -b[1].y * sg), fma(b[1].x, sg, b[1].y * T(0.5))};
+        b[2] = V{fma(b[2].x, T(-0.5), -b[2].y * sg), fma(b[2].x, sg, b[2].y * T(-0.5))};
+        for (int k = 0; k < 3; ++k) {
+            v[k] = cadd(a[k], b[k]);
+            v[k + 3] = csub(a[k], b[k]);
+        }
+    } else SmallDFT<R, INV, V>::run(v);
+}
+
+template <int N, int R, int NS, bool INV, typename V>
+__device__ __forceinline__ void ct_stage(const V* __restrict__ src, V* __restrict__ dst, int P,
+                                         const V* __restrict__ tw) {
+    constexpr int NR = N / R, PS = N + 1, TWS = N / (NS * R);
+    const int total = P * NR;
+    for (int t = threadIdx.x; t < total; t += blockDim.x) {
+        const int p = t / NR, j = t - p * NR;
+        const int jq = j / NS, k = j - jq * NS;
+        const V* s = src + p * PS;
+        V v[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) v[r] = s[j + r * NR];
+        if constexpr (NS > 1) {
+#pragma unroll
+            for (int r = 1; r < R; ++r) {
+                V w = tw[r * k * TWS];
+                if (INV) w.y = -w.y;
+                v[r] = cmul(v[r], w);
+            }
+        }
+        reg_dft<R, INV>(v);
+        V* d = dst + p * PS + jq * NS * R + k;
+#pragma unroll
+        for (int r = 0; r < R; ++r) d[r * NS] = v[r];
+    }
+}
+
+template <int N, int ST, int NS, bool INV, typename V>
+__device__ __forceinline__ V* ct_fft_rec(V* a, V* b, int P, const V* __restrict__ tw) {
+    if constexpr (ST >= ct_nstages<N>()) {
+        return a;
+    } else {
+        constexpr int R = ct_radix<N>(ST);
+        ct_stage<N, R, NS, INV>(a, b, P, tw);
+        __syncthreads();
+        return ct_fft_rec<N, ST + 1, NS * R, INV>(b, a, P, tw);
+    }
+}
+
+// NC > 0: compile-time transform of length NC; NC == 0: the runtime plan.
+template <int NC, bool INV, typename V>
+__device__ __forceinline__ V* fft_any(V* a, V* b, int P, int PS, const FFTPlan& pl, const V* __restrict__ tw) {
+    if constexpr (NC > 0) return ct_fft_rec<NC, 0, 1, INV>(a, b, P, tw);
+    else return smem_fft<INV>(a, b, P, PS, pl, tw);
 }
 
 }  // namespace pmf

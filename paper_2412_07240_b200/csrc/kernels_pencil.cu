@@ -12,6 +12,7 @@
 // Stockham FFT of fft_smem.cuh. Kernels that touch points are templated on nx so
 // every per-point loop is static (no local-memory arrays).
 #include <algorithm>
+#include <type_traits>
 #include <cmath>
 #include <vector>
 
@@ -199,14 +200,14 @@ __device__ __forceinline__ void wavenum(int k, int N, double& kap, double& kx) {
 }
 
 // ============================================================================ axis-0 R2C
-template <typename T>
+template <typename T, int NC>
 __global__ void __launch_bounds__(kThreads) k_axis0_r2c(const T* __restrict__ W, typename C2<T>::type* __restrict__ S,
                                                          const double* __restrict__ coef, int cstride, Dims d,
                                                          FFTPlan pl, const typename C2<T>::type* __restrict__ tw,
                                                          int P) {
     using V = typename C2<T>::type;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int N = d.n[0], PS = N + 1;
+    const int N = NC > 0 ? NC : d.n[0], PS = N + 1;
     V* a = reinterpret_cast<V*>(smem_raw);
     V* b = a + P * PS;
     const long long rpf = d.ntot / N;
@@ -220,7 +221,7 @@ __global__ void __launch_bounds__(kThreads) k_axis0_r2c(const T* __restrict__ W,
         a[p * PS + j] = V{src[i] * sc, T(0)};
     }
     __syncthreads();
-    V* r = smem_fft<false>(a, b, P, PS, pl, tw);
+    V* r = fft_any<NC, false>(a, b, P, PS, pl, tw);
     V* dst = S + row0 * d.H0;
     const float invH = 1.0f / d.H0;
     for (int i = threadIdx.x; i < P * d.H0; i += blockDim.x) {
@@ -236,7 +237,7 @@ __global__ void __launch_bounds__(kThreads) k_axis0_r2c(const T* __restrict__ W,
 // MODE 2 (last axis m = NX-1): forward, x s Psi(k) / N_total, inverse. Psi is
 // factored per pencil: for substep n, f_n = gam_n + bet_n kx_L + alp_n kap_L^2 with
 // (gam_n, bet_n) depending only on the pencil's other wavenumbers (Alg. 3, R3, R7).
-template <typename T, int MODE, int NX>
+template <typename T, int MODE, int NX, int NC>
 __global__ void __launch_bounds__(kThreads) k_axis_c2c(typename C2<T>::type* __restrict__ S, Dims d, int m,
                                                         long long I, FFTPlan pl,
                                                         const typename C2<T>::type* __restrict__ tw, int P,
@@ -244,7 +245,7 @@ __global__ void __launch_bounds__(kThreads) k_axis_c2c(typename C2<T>::type* __r
                                                         ModelParams mp) {
     using V = typename C2<T>::type;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int N = pl.N, PS = N + 1;
+    const int N = NC > 0 ? NC : pl.N, PS = N + 1;
     V* a = reinterpret_cast<V*>(smem_raw);
     V* b = a + P * PS;
     const long long ntile = (I + P - 1) / P;
@@ -259,9 +260,9 @@ __global__ void __launch_bounds__(kThreads) k_axis_c2c(typename C2<T>::type* __r
     __syncthreads();
     V* r;
     if (MODE == 1) {
-        r = smem_fft<true>(a, b, P, PS, pl, tw);
+        r = fft_any<NC, true>(a, b, P, PS, pl, tw);
     } else {
-        r = smem_fft<false>(a, b, P, PS, pl, tw);
+        r = fft_any<NC, false>(a, b, P, PS, pl, tw);
         if (MODE == 2) {
             const double* cf = coef + o * cstride + 4;   // o is the filter index on the last axis
             double ntot = 1.0;
@@ -337,7 +338,7 @@ __global__ void __launch_bounds__(kThreads) k_axis_c2c(typename C2<T>::type* __r
             }
             __syncthreads();
             V* other = (r == a) ? b : a;
-            r = smem_fft<true>(r, other, P, PS, pl, tw);
+            r = fft_any<NC, true>(r, other, P, PS, pl, tw);
         }
     }
     for (int t = threadIdx.x; t < P * N; t += blockDim.x) {
@@ -349,7 +350,7 @@ __global__ void __launch_bounds__(kThreads) k_axis_c2c(typename C2<T>::type* __r
 
 // ============================================================================ axis-0 C2R (+ update)
 // Per row the likelihood exponent is a quadratic in u0: e = A_p + u0 (B_p + G00 u0).
-template <typename T, bool UPDATE, int NX>
+template <typename T, bool UPDATE, int NX, int NC>
 __global__ void __launch_bounds__(kThreads) k_axis0_c2r(const typename C2<T>::type* __restrict__ S, T* __restrict__ W,
                                                          const FilterState* __restrict__ st, Dims d, DivSet dv,
                                                          FFTPlan pl, const typename C2<T>::type* __restrict__ tw,
@@ -358,7 +359,7 @@ __global__ void __launch_bounds__(kThreads) k_axis0_c2r(const typename C2<T>::ty
                                                          double* __restrict__ partials) {
     using V = typename C2<T>::type;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int N = d.n[0], PS = N + 1;
+    const int N = NC > 0 ? NC : d.n[0], PS = N + 1;
     V* a = reinterpret_cast<V*>(smem_raw);
     V* b = a + P * PS;
     double* red = reinterpret_cast<double*>(b + P * PS);            // 32 * NMOM
@@ -405,7 +406,7 @@ __global__ void __launch_bounds__(kThreads) k_axis0_c2r(const typename C2<T>::ty
         }
     }
     __syncthreads();
-    V* r = smem_fft<true>(a, b, P, PS, pl, tw);
+    V* r = fft_any<NC, true>(a, b, P, PS, pl, tw);
     const double scale = f.scale;
     double acc[NMOM];
 #pragma unroll
@@ -446,7 +447,7 @@ __global__ void __launch_bounds__(kThreads) k_axis0_c2r(const typename C2<T>::ty
 }
 
 // ============================================================================ nx = 1 fused line
-template <typename T, bool UPDATE>
+template <typename T, bool UPDATE, int NC>
 __global__ void __launch_bounds__(kThreads) k_line_psi(T* __restrict__ W, FilterState* __restrict__ st, Dims d,
                                                         FFTPlan pl, const typename C2<T>::type* __restrict__ tw,
                                                         const double* __restrict__ coef, int cstride,
@@ -454,7 +455,7 @@ __global__ void __launch_bounds__(kThreads) k_line_psi(T* __restrict__ W, Filter
                                                         double* __restrict__ partials) {
     using V = typename C2<T>::type;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int N = d.n[0], PS = N + 1;
+    const int N = NC > 0 ? NC : d.n[0], PS = N + 1;
     V* a = reinterpret_cast<V*>(smem_raw);
     V* b = a + PS;
     double* red = reinterpret_cast<double*>(b + PS);
@@ -464,7 +465,7 @@ __global__ void __launch_bounds__(kThreads) k_line_psi(T* __restrict__ W, Filter
     T* row = W + (long long)filt * N;
     for (int j = threadIdx.x; j < N; j += blockDim.x) a[j] = V{row[j] * sc, T(0)};
     __syncthreads();
-    V* r = smem_fft<false>(a, b, 1, PS, pl, tw);
+    V* r = fft_any<NC, false>(a, b, 1, PS, pl, tw);
     const double mult = mp.s / N;
     for (int k = threadIdx.x; k < N; k += blockDim.x) {
         double kap, kx;
@@ -476,7 +477,7 @@ __global__ void __launch_bounds__(kThreads) k_line_psi(T* __restrict__ W, Filter
         r[k] = V{v.x * ps, v.y * ps};
     }
     __syncthreads();
-    r = smem_fft<true>(r, (r == a) ? b : a, 1, PS, pl, tw);
+    r = fft_any<NC, true>(r, (r == a) ? b : a, 1, PS, pl, tw);
     const FilterState& f = st[filt];
     double acc[NMOM];
 #pragma unroll
@@ -743,6 +744,18 @@ static cudaError_t smem_attr(K kernel, size_t bytes) {
     return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
 }
 
+// dispatch a launch lambda on the compile-time FFT length (0 = runtime plan)
+template <typename F>
+static cudaError_t with_nc(int N, F&& f) {
+    switch (N) {
+        case 64: return f(std::integral_constant<int, 64>{});
+        case 96: return f(std::integral_constant<int, 96>{});
+        case 128: return f(std::integral_constant<int, 128>{});
+        case 256: return f(std::integral_constant<int, 256>{});
+        default: return f(std::integral_constant<int, 0>{});
+    }
+}
+
 template <typename T, int NX>
 static cudaError_t predict_nd(const Dims& d, PencilBufs& b, const Twiddles& tw, const ModelParams& mp,
                               const LikParams* lp, const LikParams& lpv, int cs, cudaStream_t s, int64_t* launches) {
@@ -755,11 +768,14 @@ static cudaError_t predict_nd(const Dims& d, PencilBufs& b, const Twiddles& tw, 
     FFTPlan pl0 = make_plan(N0);
     size_t sm0 = 2 * (size_t)P0 * (N0 + 1) * sizeof(V);
     long long nrow_blocks = (long long)d.batch * rpf / P0;
-    PMF_TRY(smem_attr(k_axis0_r2c<T>, sm0));
-    k_axis0_r2c<T><<<(unsigned)nrow_blocks, kThreads, sm0, s>>>((const T*)b.W, (V*)b.S, b.coef, cs, d, pl0,
-                                                                (const V*)tw.tw[0], P0);
+    PMF_TRY(with_nc(N0, [&](auto nc) -> cudaError_t {
+        constexpr int NC = decltype(nc)::value;
+        PMF_TRY(smem_attr(k_axis0_r2c<T, NC>, sm0));
+        k_axis0_r2c<T, NC><<<(unsigned)nrow_blocks, kThreads, sm0, s>>>((const T*)b.W, (V*)b.S, b.coef, cs, d, pl0,
+                                                                        (const V*)tw.tw[0], P0);
+        return cudaGetLastError();
+    }));
     ++*launches;
-    PMF_TRY(cudaGetLastError());
     // strided axes
     auto strided = [&](int m, int mode) -> cudaError_t {
         long long I = d.H0;
@@ -772,40 +788,47 @@ static cudaError_t predict_nd(const Dims& d, PencilBufs& b, const Twiddles& tw, 
         size_t sm = 2 * (size_t)P * (N + 1) * sizeof(V);
         if (mode == 2) sm += sizeof(double) * 2 * P * std::min(mp.l, LCAP);
         long long nblk = O * ((I + P - 1) / P);
-        if (mode == 0) {
-            PMF_TRY(smem_attr(k_axis_c2c<T, 0, NX>, sm));
-            k_axis_c2c<T, 0, NX><<<(unsigned)nblk, kThreads, sm, s>>>((V*)b.S, d, m, I, pl, (const V*)tw.tw[m], P,
-                                                                       b.coef, cs, mp);
-        } else if (mode == 1) {
-            PMF_TRY(smem_attr(k_axis_c2c<T, 1, NX>, sm));
-            k_axis_c2c<T, 1, NX><<<(unsigned)nblk, kThreads, sm, s>>>((V*)b.S, d, m, I, pl, (const V*)tw.tw[m], P,
-                                                                       b.coef, cs, mp);
-        } else {
-            PMF_TRY(smem_attr(k_axis_c2c<T, 2, NX>, sm));
-            k_axis_c2c<T, 2, NX><<<(unsigned)nblk, kThreads, sm, s>>>((V*)b.S, d, m, I, pl, (const V*)tw.tw[m], P,
-                                                                       b.coef, cs, mp);
-        }
+        cudaError_t e = with_nc(N, [&](auto nc) -> cudaError_t {
+            constexpr int NC = decltype(nc)::value;
+            if (mode == 0) {
+                PMF_TRY(smem_attr(k_axis_c2c<T, 0, 2, NC>, sm));
+                k_axis_c2c<T, 0, 2, NC><<<(unsigned)nblk, kThreads, sm, s>>>((V*)b.S, d, m, I, pl,
+                                                                              (const V*)tw.tw[m], P, b.coef, cs, mp);
+            } else if (mode == 1) {
+                PMF_TRY(smem_attr(k_axis_c2c<T, 1, 2, NC>, sm));
+                k_axis_c2c<T, 1, 2, NC><<<(unsigned)nblk, kThreads, sm, s>>>((V*)b.S, d, m, I, pl,
+                                                                              (const V*)tw.tw[m], P, b.coef, cs, mp);
+            } else {
+                PMF_TRY(smem_attr(k_axis_c2c<T, 2, NX, NC>, sm));
+                k_axis_c2c<T, 2, NX, NC><<<(unsigned)nblk, kThreads, sm, s>>>((V*)b.S, d, m, I, pl,
+                                                                               (const V*)tw.tw[m], P, b.coef, cs, mp);
+            }
+            return cudaGetLastError();
+        });
         ++*launches;
-        return cudaGetLastError();
+        return e;
     };
     for (int m = 1; m < d.nx - 1; ++m) PMF_TRY(strided(m, 0));
     PMF_TRY(strided(d.nx - 1, 2));
     for (int m = d.nx - 2; m >= 1; --m) PMF_TRY(strided(m, 1));
     // axis 0 inverse (C2R) + update
     size_t smc = sm0 + 32 * NMOM * sizeof(double) + 6 * sizeof(double) * P0;
-    if (lp) {
-        PMF_TRY(smem_attr(k_axis0_c2r<T, true, NX>, smc));
-        k_axis0_c2r<T, true, NX><<<(unsigned)nrow_blocks, kThreads, smc, s>>>(
-            (const V*)b.S, (T*)b.W, b.st, d, dv, pl0, (const V*)tw.tw[0], P0, lpv, b.z, b.coef, cs, lq_off(mp.l),
-            b.partials);
-    } else {
-        PMF_TRY(smem_attr(k_axis0_c2r<T, false, NX>, smc));
-        k_axis0_c2r<T, false, NX><<<(unsigned)nrow_blocks, kThreads, smc, s>>>(
-            (const V*)b.S, (T*)b.W, b.st, d, dv, pl0, (const V*)tw.tw[0], P0, lpv, b.z, b.coef, cs, lq_off(mp.l),
-            b.partials);
-    }
+    PMF_TRY(with_nc(N0, [&](auto nc) -> cudaError_t {
+        constexpr int NC = decltype(nc)::value;
+        if (lp) {
+            PMF_TRY(smem_attr(k_axis0_c2r<T, true, NX, NC>, smc));
+            k_axis0_c2r<T, true, NX, NC><<<(unsigned)nrow_blocks, kThreads, smc, s>>>(
+                (const V*)b.S, (T*)b.W, b.st, d, dv, pl0, (const V*)tw.tw[0], P0, lpv, b.z, b.coef, cs,
+                lq_off(mp.l), b.partials);
+        } else {
+            PMF_TRY(smem_attr(k_axis0_c2r<T, false, NX, NC>, smc));
+            k_axis0_c2r<T, false, NX, NC><<<(unsigned)nrow_blocks, kThreads, smc, s>>>(
+                (const V*)b.S, (T*)b.W, b.st, d, dv, pl0, (const V*)tw.tw[0], P0, lpv, b.z, b.coef, cs,
+                lq_off(mp.l), b.partials);
+        }
+        return cudaGetLastError();
+    }));
     ++*launches;
-    PMF_TRY(cudaGetLastError());
     if (lp) {
         k_finalize<<<d.batch, kThreads, 0, s>>>(b.st, b.partials, (int)(rpf / P0), d, 0);
         ++*launches;
@@ -829,16 +852,19 @@ static cudaError_t predict_pencil_t(const Dims& d, PencilBufs& b, const Twiddles
     if (d.nx == 1) {
         FFTPlan pl = make_plan(d.n[0]);
         size_t sm = 2 * (d.n[0] + 1) * sizeof(V) + 32 * NMOM * sizeof(double);
-        PMF_TRY(smem_attr(k_line_psi<T, true>, sm));
-        PMF_TRY(smem_attr(k_line_psi<T, false>, sm));
-        if (lp)
-            k_line_psi<T, true><<<d.batch, kThreads, sm, s>>>((T*)b.W, b.st, d, pl, (const V*)tw.tw[0], b.coef, cs,
-                                                              mp, lpv, b.z, b.partials);
-        else
-            k_line_psi<T, false><<<d.batch, kThreads, sm, s>>>((T*)b.W, b.st, d, pl, (const V*)tw.tw[0], b.coef, cs,
-                                                               mp, lpv, b.z, b.partials);
+        PMF_TRY(with_nc(d.n[0], [&](auto nc) -> cudaError_t {
+            constexpr int NC = decltype(nc)::value;
+            PMF_TRY(smem_attr(k_line_psi<T, true, NC>, sm));
+            PMF_TRY(smem_attr(k_line_psi<T, false, NC>, sm));
+            if (lp)
+                k_line_psi<T, true, NC><<<d.batch, kThreads, sm, s>>>((T*)b.W, b.st, d, pl, (const V*)tw.tw[0],
+                                                                      b.coef, cs, mp, lpv, b.z, b.partials);
+            else
+                k_line_psi<T, false, NC><<<d.batch, kThreads, sm, s>>>((T*)b.W, b.st, d, pl, (const V*)tw.tw[0],
+                                                                       b.coef, cs, mp, lpv, b.z, b.partials);
+            return cudaGetLastError();
+        }));
         ++*launches;
-        PMF_TRY(cudaGetLastError());
         if (lp) {
             k_finalize<<<d.batch, kThreads, 0, s>>>(b.st, b.partials, 1, d, 0);
             ++*launches;
