@@ -120,6 +120,13 @@ __host__ __device__ constexpr int ct_radix(int st) {
 template <int N>
 inline constexpr bool ct_supported = ct_nstages<N>() > 0;
 
+// Shared-memory layout of the compile-time path: one pad slot every 8 complex
+// (sx), so the stride-R writes of a Stockham stage hit distinct bank groups.
+template <int NC>
+__host__ __device__ __forceinline__ int sx(int j) { return NC > 0 ? j + (j >> 3) : j; }
+template <int NC>
+__host__ __device__ __forceinline__ int pencil_stride(int N) { return NC > 0 ? NC + NC / 8 + 1 : N + 1; }
+
 template <int R, bool INV, typename V>
 __device__ __forceinline__ void reg_dft(V* v) {
     if constexpr (R == 8) reg::dft8<INV>(v);
@@ -145,7 +152,7 @@ __device__ __forceinline__ void reg_dft(V* v) {
 template <int N, int R, int NS, bool INV, typename V>
 __device__ __forceinline__ void ct_stage(const V* __restrict__ src, V* __restrict__ dst, int P,
                                          const V* __restrict__ tw) {
-    constexpr int NR = N / R, PS = N + 1, TWS = N / (NS * R);
+    constexpr int NR = N / R, PS = N + N / 8 + 1, TWS = N / (NS * R);
     const int total = P * NR;
     for (int t = threadIdx.x; t < total; t += blockDim.x) {
         const int p = t / NR, j = t - p * NR;
@@ -153,7 +160,7 @@ __device__ __forceinline__ void ct_stage(const V* __restrict__ src, V* __restric
         const V* s = src + p * PS;
         V v[R];
 #pragma unroll
-        for (int r = 0; r < R; ++r) v[r] = s[j + r * NR];
+        for (int r = 0; r < R; ++r) v[r] = s[sx<N>(j + r * NR)];
         if constexpr (NS > 1) {
 #pragma unroll
             for (int r = 1; r < R; ++r) {
@@ -163,9 +170,10 @@ __device__ __forceinline__ void ct_stage(const V* __restrict__ src, V* __restric
             }
         }
         reg_dft<R, INV>(v);
-        V* d = dst + p * PS + jq * NS * R + k;
+        V* d = dst + p * PS;
+        const int o = jq * NS * R + k;
 #pragma unroll
-        for (int r = 0; r < R; ++r) d[r * NS] = v[r];
+        for (int r = 0; r < R; ++r) d[sx<N>(o + r * NS)] = v[r];
     }
 }
 

@@ -44,6 +44,11 @@ static int rows_per_cta(int N, long long rows_per_filter) {
     return p2;
 }
 
+static int pstride_host(int N) {
+    const bool ct = N == 64 || N == 96 || N == 128 || N == 256;   // with_nc's compile-time sizes
+    return ct ? N + N / 8 + 1 : N + 1;
+}
+
 static int pencils_per_cta(int N) {
     int P = std::max(1, 2048 / N);
     int p2 = 1;
@@ -207,7 +212,7 @@ __global__ void __launch_bounds__(kThreads) k_axis0_r2c(const T* __restrict__ W,
                                                          int P) {
     using V = typename C2<T>::type;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int N = NC > 0 ? NC : d.n[0], PS = N + 1;
+    const int N = NC > 0 ? NC : d.n[0], PS = pencil_stride<NC>(N);
     V* a = reinterpret_cast<V*>(smem_raw);
     V* b = a + P * PS;
     const long long rpf = d.ntot / N;
@@ -218,7 +223,7 @@ __global__ void __launch_bounds__(kThreads) k_axis0_r2c(const T* __restrict__ W,
     const float invN = 1.0f / N;
     for (int i = threadIdx.x; i < P * N; i += blockDim.x) {
         const int p = (int)((i + 0.5f) * invN), j = i - p * N;
-        a[p * PS + j] = V{src[i] * sc, T(0)};
+        a[p * PS + sx<NC>(j)] = V{src[i] * sc, T(0)};
     }
     __syncthreads();
     V* r = fft_any<NC, false>(a, b, P, PS, pl, tw);
@@ -226,7 +231,7 @@ __global__ void __launch_bounds__(kThreads) k_axis0_r2c(const T* __restrict__ W,
     const float invH = 1.0f / d.H0;
     for (int i = threadIdx.x; i < P * d.H0; i += blockDim.x) {
         const int p = (int)((i + 0.5f) * invH), k = i - p * d.H0;
-        dst[i] = r[p * PS + k];
+        dst[i] = r[p * PS + sx<NC>(k)];
     }
 }
 
@@ -245,7 +250,7 @@ __global__ void __launch_bounds__(kThreads) k_axis_c2c(typename C2<T>::type* __r
                                                         ModelParams mp) {
     using V = typename C2<T>::type;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int N = NC > 0 ? NC : pl.N, PS = N + 1;
+    const int N = NC > 0 ? NC : pl.N, PS = pencil_stride<NC>(N);
     V* a = reinterpret_cast<V*>(smem_raw);
     V* b = a + P * PS;
     const long long ntile = (I + P - 1) / P;
@@ -255,7 +260,7 @@ __global__ void __launch_bounds__(kThreads) k_axis_c2c(typename C2<T>::type* __r
     for (int t = threadIdx.x; t < P * N; t += blockDim.x) {
         const int j = t / P, p = t - j * P;     // P is a power of two
         long long i = i0 + p;
-        a[p * PS + j] = (i < I) ? base[(long long)j * I + i] : V{T(0), T(0)};
+        a[p * PS + sx<NC>(j)] = (i < I) ? base[(long long)j * I + i] : V{T(0), T(0)};
     }
     __syncthreads();
     V* r;
@@ -333,8 +338,8 @@ __global__ void __launch_bounds__(kThreads) k_axis_c2c(typename C2<T>::type* __r
                     }
                 }
                 const T ps = (T)(mult / prod);
-                V v = r[p * PS + j];
-                r[p * PS + j] = V{v.x * ps, v.y * ps};
+                V v = r[p * PS + sx<NC>(j)];
+                r[p * PS + sx<NC>(j)] = V{v.x * ps, v.y * ps};
             }
             __syncthreads();
             V* other = (r == a) ? b : a;
@@ -344,7 +349,7 @@ __global__ void __launch_bounds__(kThreads) k_axis_c2c(typename C2<T>::type* __r
     for (int t = threadIdx.x; t < P * N; t += blockDim.x) {
         const int j = t / P, p = t - j * P;
         long long i = i0 + p;
-        if (i < I) base[(long long)j * I + i] = r[p * PS + j];
+        if (i < I) base[(long long)j * I + i] = r[p * PS + sx<NC>(j)];
     }
 }
 
@@ -359,7 +364,7 @@ __global__ void __launch_bounds__(kThreads) k_axis0_c2r(const typename C2<T>::ty
                                                          double* __restrict__ partials) {
     using V = typename C2<T>::type;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int N = NC > 0 ? NC : d.n[0], PS = N + 1;
+    const int N = NC > 0 ? NC : d.n[0], PS = pencil_stride<NC>(N);
     V* a = reinterpret_cast<V*>(smem_raw);
     V* b = a + P * PS;
     double* red = reinterpret_cast<double*>(b + P * PS);            // 32 * NMOM
@@ -374,7 +379,7 @@ __global__ void __launch_bounds__(kThreads) k_axis0_c2r(const typename C2<T>::ty
         V v;
         if (k < d.H0) v = src[p * d.H0 + k];
         else { v = src[p * d.H0 + (N - k)]; v.y = -v.y; }
-        a[p * PS + k] = v;
+        a[p * PS + sx<NC>(k)] = v;
     }
     const FilterState& f = st[filt];
     const double* q = coef + (long long)filt * cstride + lqo;
@@ -416,7 +421,7 @@ __global__ void __launch_bounds__(kThreads) k_axis0_c2r(const typename C2<T>::ty
     const double* zf = z + (long long)filt * lp.nz;
     for (int i = threadIdx.x; i < P * N; i += blockDim.x) {
         const int p = (int)((i + 0.5f) * invN), j = i - p * N;
-        double w = (double)r[p * PS + j].x;
+        double w = (double)r[p * PS + sx<NC>(j)].x;
         if (UPDATE) {
             const double* ru = rowu + 6 * p;
             double u[4];
@@ -455,7 +460,7 @@ __global__ void __launch_bounds__(kThreads) k_line_psi(T* __restrict__ W, Filter
                                                         double* __restrict__ partials) {
     using V = typename C2<T>::type;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int N = NC > 0 ? NC : d.n[0], PS = N + 1;
+    const int N = NC > 0 ? NC : d.n[0], PS = pencil_stride<NC>(N);
     V* a = reinterpret_cast<V*>(smem_raw);
     V* b = a + PS;
     double* red = reinterpret_cast<double*>(b + PS);
@@ -463,7 +468,7 @@ __global__ void __launch_bounds__(kThreads) k_line_psi(T* __restrict__ W, Filter
     const double* cf = coef + (long long)filt * cstride;
     const T sc = (T)cf[0];
     T* row = W + (long long)filt * N;
-    for (int j = threadIdx.x; j < N; j += blockDim.x) a[j] = V{row[j] * sc, T(0)};
+    for (int j = threadIdx.x; j < N; j += blockDim.x) a[sx<NC>(j)] = V{row[j] * sc, T(0)};
     __syncthreads();
     V* r = fft_any<NC, false>(a, b, 1, PS, pl, tw);
     const double mult = mp.s / N;
@@ -473,8 +478,8 @@ __global__ void __launch_bounds__(kThreads) k_line_psi(T* __restrict__ W, Filter
         double prod = 1.0;
         for (int n = 0; n < mp.l; ++n) prod *= fma(cf[4 + 10 * n], kap * kap, 1.0);
         const T ps = (T)(mult / prod);
-        V v = r[k];
-        r[k] = V{v.x * ps, v.y * ps};
+        V v = r[sx<NC>(k)];
+        r[sx<NC>(k)] = V{v.x * ps, v.y * ps};
     }
     __syncthreads();
     r = fft_any<NC, true>(r, (r == a) ? b : a, 1, PS, pl, tw);
@@ -485,7 +490,7 @@ __global__ void __launch_bounds__(kThreads) k_line_psi(T* __restrict__ W, Filter
     const double scale = f.scale;
     const double* zf = z + (long long)filt * lp.nz;
     for (int j = threadIdx.x; j < N; j += blockDim.x) {
-        double w = (double)r[j].x;
+        double w = (double)r[sx<NC>(j)].x;
         if (UPDATE) {
             double u = j - 0.5 * (N - 1), x;
             phys<1>(f, &u, &x);
@@ -766,7 +771,7 @@ static cudaError_t predict_nd(const Dims& d, PencilBufs& b, const Twiddles& tw, 
     const long long rpf = d.ntot / N0;
     const int P0 = rows_per_cta(N0, rpf);
     FFTPlan pl0 = make_plan(N0);
-    size_t sm0 = 2 * (size_t)P0 * (N0 + 1) * sizeof(V);
+    size_t sm0 = 2 * (size_t)P0 * pstride_host(N0) * sizeof(V);
     long long nrow_blocks = (long long)d.batch * rpf / P0;
     PMF_TRY(with_nc(N0, [&](auto nc) -> cudaError_t {
         constexpr int NC = decltype(nc)::value;
@@ -785,7 +790,7 @@ static cudaError_t predict_nd(const Dims& d, PencilBufs& b, const Twiddles& tw, 
         const int N = d.n[m];
         const int P = pencils_per_cta(N);
         FFTPlan pl = make_plan(N);
-        size_t sm = 2 * (size_t)P * (N + 1) * sizeof(V);
+        size_t sm = 2 * (size_t)P * pstride_host(N) * sizeof(V);
         if (mode == 2) sm += sizeof(double) * 2 * P * std::min(mp.l, LCAP);
         long long nblk = O * ((I + P - 1) / P);
         cudaError_t e = with_nc(N, [&](auto nc) -> cudaError_t {
@@ -851,7 +856,7 @@ static cudaError_t predict_pencil_t(const Dims& d, PencilBufs& b, const Twiddles
     cudaError_t e = cudaSuccess;
     if (d.nx == 1) {
         FFTPlan pl = make_plan(d.n[0]);
-        size_t sm = 2 * (d.n[0] + 1) * sizeof(V) + 32 * NMOM * sizeof(double);
+        size_t sm = 2 * pstride_host(d.n[0]) * sizeof(V) + 32 * NMOM * sizeof(double);
         PMF_TRY(with_nc(d.n[0], [&](auto nc) -> cudaError_t {
             constexpr int NC = decltype(nc)::value;
             PMF_TRY(smem_attr(k_line_psi<T, true, NC>, sm));
