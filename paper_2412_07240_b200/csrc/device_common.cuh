@@ -201,7 +201,7 @@ __device__ __forceinline__ void acc_moments(int nx, double w, const double* u, d
 // Deterministic block sum of NV doubles per thread; result valid in thread 0.
 // scratch: >= 32 * NV doubles of shared memory.
 template <int NV>
-__device__ inline void block_sum(double* v, double* scratch) {
+__device__ __forceinline__ void block_sum(double* v, double* scratch) {
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
 #pragma unroll
     for (int i = 0; i < NV; ++i) {

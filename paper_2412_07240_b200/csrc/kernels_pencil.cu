@@ -206,7 +206,7 @@ __device__ __forceinline__ void wavenum(int k, int N, double& kap, double& kx) {
 
 // ============================================================================ axis-0 R2C
 template <typename T, int NC>
-__global__ void __launch_bounds__(kThreads) k_axis0_r2c(const T* __restrict__ W, typename C2<T>::type* __restrict__ S,
+__global__ void __launch_bounds__(kThreads, 2) k_axis0_r2c(const T* __restrict__ W, typename C2<T>::type* __restrict__ S,
                                                          const double* __restrict__ coef, int cstride, Dims d,
                                                          FFTPlan pl, const typename C2<T>::type* __restrict__ tw,
                                                          int P) {
@@ -243,7 +243,7 @@ __global__ void __launch_bounds__(kThreads) k_axis0_r2c(const T* __restrict__ W,
 // factored per pencil: for substep n, f_n = gam_n + bet_n kx_L + alp_n kap_L^2 with
 // (gam_n, bet_n) depending only on the pencil's other wavenumbers (Alg. 3, R3, R7).
 template <typename T, int MODE, int NX, int NC>
-__global__ void __launch_bounds__(kThreads) k_axis_c2c(typename C2<T>::type* __restrict__ S, Dims d, int m,
+__global__ void __launch_bounds__(kThreads, 2) k_axis_c2c(typename C2<T>::type* __restrict__ S, Dims d, int m,
                                                         long long I, FFTPlan pl,
                                                         const typename C2<T>::type* __restrict__ tw, int P,
                                                         const double* __restrict__ coef, int cstride,
@@ -356,12 +356,14 @@ __global__ void __launch_bounds__(kThreads) k_axis_c2c(typename C2<T>::type* __r
 // ============================================================================ axis-0 C2R (+ update)
 // Per row the likelihood exponent is a quadratic in u0: e = A_p + u0 (B_p + G00 u0).
 template <typename T, bool UPDATE, int NX, int NC>
-__global__ void __launch_bounds__(kThreads) k_axis0_c2r(const typename C2<T>::type* __restrict__ S, T* __restrict__ W,
+__global__ void __launch_bounds__(kThreads, 2) k_axis0_c2r(const typename C2<T>::type* __restrict__ S, T* __restrict__ W,
                                                          const FilterState* __restrict__ st, Dims d, DivSet dv,
                                                          FFTPlan pl, const typename C2<T>::type* __restrict__ tw,
                                                          int P, LikParams lp, const double* __restrict__ z,
                                                          const double* __restrict__ coef, int cstride, int lqo,
-                                                         double* __restrict__ partials) {
+                                                         double* __restrict__ partials, int cpf, int tpc) {
+    // CTA (filter, q) processes tiles [q tpc, (q+1) tpc) of P rows of its filter and
+    // writes ONE set of moment partials (cpf CTAs per filter).
     using V = typename C2<T>::type;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int N = NC > 0 ? NC : d.n[0], PS = pencil_stride<NC>(N);
@@ -370,79 +372,85 @@ __global__ void __launch_bounds__(kThreads) k_axis0_c2r(const typename C2<T>::ty
     double* red = reinterpret_cast<double*>(b + P * PS);            // 32 * NMOM
     double* rowu = red + 32 * NMOM;                                  // [P][6]: u_1..u_3, A_p, B_p
     const long long rpf = d.ntot / N;
-    const long long row0 = (long long)blockIdx.x * P;
-    const int filt = (int)(row0 / rpf);
-    const V* src = S + row0 * d.H0;
-    const float invN = 1.0f / N;
-    for (int i = threadIdx.x; i < P * N; i += blockDim.x) {
-        const int p = (int)((i + 0.5f) * invN), k = i - p * N;
-        V v;
-        if (k < d.H0) v = src[p * d.H0 + k];
-        else { v = src[p * d.H0 + (N - k)]; v.y = -v.y; }
-        a[p * PS + sx<NC>(k)] = v;
-    }
+    const int tiles = (int)(rpf / P);
+    const int filt = blockIdx.x / cpf, qc = blockIdx.x - filt * cpf;
+    const int t_end = min(tiles, (qc + 1) * tpc);
     const FilterState& f = st[filt];
     const double* q = coef + (long long)filt * cstride + lqo;
-    if (UPDATE) {
-        for (int p = threadIdx.x; p < P; p += blockDim.x) {
-            double u[4] = {0, 0, 0, 0};
-            unsigned rr = (unsigned)(row0 + p - (long long)filt * rpf);
-#pragma unroll
-            for (int a2 = 1; a2 < NX; ++a2) {
-                const unsigned qq = (a2 < NX - 1) ? fdiv(rr, dv.n[a2]) : 0u;
-                const unsigned j = (a2 < NX - 1) ? rr - qq * (unsigned)d.n[a2] : rr;
-                u[a2] = (double)j - 0.5 * (d.n[a2] - 1);
-                rr = qq;
-            }
-            double A = q[0], Bc = q[1];
-#pragma unroll
-            for (int a2 = 1; a2 < NX; ++a2) {
-                A = fma(q[1 + a2], u[a2], A);
-                Bc = fma(q[5 + tri(0, a2)], u[a2], Bc);
-#pragma unroll
-                for (int b2 = a2; b2 < NX; ++b2) A = fma(q[5 + tri(a2, b2)] * u[a2], u[b2], A);
-            }
-            double* ru = rowu + 6 * p;
-            ru[0] = u[1];
-            ru[1] = u[2];
-            ru[2] = u[3];
-            ru[3] = A;
-            ru[4] = Bc;
-        }
-    }
-    __syncthreads();
-    V* r = fft_any<NC, true>(a, b, P, PS, pl, tw);
     const double scale = f.scale;
+    const double g00 = q[5];
+    const double* zf = z + (long long)filt * lp.nz;
+    const float invN = 1.0f / N;
     double acc[NMOM];
 #pragma unroll
     for (int i = 0; i < NMOM; ++i) acc[i] = 0.0;
-    T* dst = W + row0 * N;
-    const double g00 = q[5];
-    const double* zf = z + (long long)filt * lp.nz;
-    for (int i = threadIdx.x; i < P * N; i += blockDim.x) {
-        const int p = (int)((i + 0.5f) * invN), j = i - p * N;
-        double w = (double)r[p * PS + sx<NC>(j)].x;
-        if (UPDATE) {
-            const double* ru = rowu + 6 * p;
-            double u[4];
-            u[0] = j - 0.5 * (N - 1);
-#pragma unroll
-            for (int a2 = 1; a2 < NX; ++a2) u[a2] = ru[a2 - 1];
-            double ll;
-            if (lp.kind == 0) {
-                const double e = fma(u[0], fma(g00, u[0], ru[4]), ru[3]);
-                ll = fma(-0.5, e, lp.lognorm);
-            } else {
-                double x[4];
-                phys<NX>(f, u, x);
-                ll = log_lik(lp, x, zf);
-            }
-            const T wt = (T)(w * scale * exp_fast(ll));
-            dst[i] = wt;
-            acc_mom<NX>((double)wt, u, acc);
-        } else {
-            dst[i] = (T)w;
+    for (int tile = qc * tpc; tile < t_end; ++tile) {
+        const long long rloc = (long long)tile * P;                  // first row of the tile in the filter
+        const long long row0 = (long long)filt * rpf + rloc;
+        const V* src = S + row0 * d.H0;
+        for (int i = threadIdx.x; i < P * N; i += blockDim.x) {
+            const int p = (int)((i + 0.5f) * invN), k = i - p * N;
+            V v;
+            if (k < d.H0) v = src[p * d.H0 + k];
+            else { v = src[p * d.H0 + (N - k)]; v.y = -v.y; }
+            a[p * PS + sx<NC>(k)] = v;
         }
+        if (UPDATE) {
+            for (int p = threadIdx.x; p < P; p += blockDim.x) {
+                double u[4] = {0, 0, 0, 0};
+                unsigned rr = (unsigned)(rloc + p);
+#pragma unroll
+                for (int a2 = 1; a2 < NX; ++a2) {
+                    const unsigned qq = (a2 < NX - 1) ? fdiv(rr, dv.n[a2]) : 0u;
+                    const unsigned j = (a2 < NX - 1) ? rr - qq * (unsigned)d.n[a2] : rr;
+                    u[a2] = (double)j - 0.5 * (d.n[a2] - 1);
+                    rr = qq;
+                }
+                double A = q[0], Bc = q[1];
+#pragma unroll
+                for (int a2 = 1; a2 < NX; ++a2) {
+                    A = fma(q[1 + a2], u[a2], A);
+                    Bc = fma(q[5 + tri(0, a2)], u[a2], Bc);
+#pragma unroll
+                    for (int b2 = a2; b2 < NX; ++b2) A = fma(q[5 + tri(a2, b2)] * u[a2], u[b2], A);
+                }
+                double* ru = rowu + 6 * p;
+                ru[0] = u[1];
+                ru[1] = u[2];
+                ru[2] = u[3];
+                ru[3] = A;
+                ru[4] = Bc;
+            }
+        }
+        __syncthreads();
+        V* r = fft_any<NC, true>(a, b, P, PS, pl, tw);
+        T* dst = W + row0 * N;
+        for (int i = threadIdx.x; i < P * N; i += blockDim.x) {
+            const int p = (int)((i + 0.5f) * invN), j = i - p * N;
+            double w = (double)r[p * PS + sx<NC>(j)].x;
+            if (UPDATE) {
+                const double* ru = rowu + 6 * p;
+                double u[4];
+                u[0] = j - 0.5 * (N - 1);
+#pragma unroll
+                for (int a2 = 1; a2 < NX; ++a2) u[a2] = ru[a2 - 1];
+                double ll;
+                if (lp.kind == 0) {
+                    const double e = fma(u[0], fma(g00, u[0], ru[4]), ru[3]);
+                    ll = fma(-0.5, e, lp.lognorm);
+                } else {
+                    double x[4];
+                    phys<NX>(f, u, x);
+                    ll = log_lik(lp, x, zf);
+                }
+                const T wt = (T)(w * scale * exp_fast(ll));
+                dst[i] = wt;
+                acc_mom<NX>((double)wt, u, acc);
+            } else {
+                dst[i] = (T)w;
+            }
+        }
+        __syncthreads();                     // the tile's shared memory is reused by the next tile
     }
     if (UPDATE) {
         block_sum<NMOM>(acc, red);
@@ -453,7 +461,7 @@ __global__ void __launch_bounds__(kThreads) k_axis0_c2r(const typename C2<T>::ty
 
 // ============================================================================ nx = 1 fused line
 template <typename T, bool UPDATE, int NC>
-__global__ void __launch_bounds__(kThreads) k_line_psi(T* __restrict__ W, FilterState* __restrict__ st, Dims d,
+__global__ void __launch_bounds__(kThreads, 2) k_line_psi(T* __restrict__ W, FilterState* __restrict__ st, Dims d,
                                                         FFTPlan pl, const typename C2<T>::type* __restrict__ tw,
                                                         const double* __restrict__ coef, int cstride,
                                                         ModelParams mp, LikParams lp, const double* __restrict__ z,
@@ -517,7 +525,7 @@ static int blocks_per_filter(long long ntot) {
 }
 
 template <typename T, int MODE, int NX>   // 0: standalone update, 1: init gaussian, 2: plain sum
-__global__ void __launch_bounds__(kThreads) k_points(T* __restrict__ W, const FilterState* __restrict__ st, Dims d,
+__global__ void __launch_bounds__(kThreads, 2) k_points(T* __restrict__ W, const FilterState* __restrict__ st, Dims d,
                                                       DivSet dv, int nbpf, LikParams lp,
                                                       const double* __restrict__ z, const double* __restrict__ gauss,
                                                       double* __restrict__ partials) {
@@ -611,7 +619,7 @@ __global__ void k_finalize(FilterState* st, const double* __restrict__ partials,
 // Multilinear interpolation with zero ghost nodes at the points of the new grid
 // (R12). v = B^-1 (x' - c) + (N-1)/2 = o + M u' with M = B^-1 B', o = B^-1(c'-c)+(N-1)/2.
 template <typename T, int NX>
-__global__ void __launch_bounds__(kThreads) k_regrid_gather(const T* __restrict__ Wold, T* __restrict__ Wnew,
+__global__ void __launch_bounds__(kThreads, 2) k_regrid_gather(const T* __restrict__ Wold, T* __restrict__ Wnew,
                                                              const FilterState* __restrict__ st, Dims d, DivSet dv,
                                                              int nbpf, double ks, double* __restrict__ partials) {
     __shared__ double red[32 * NMOM];
@@ -685,6 +693,185 @@ __global__ void __launch_bounds__(kThreads) k_regrid_gather(const T* __restrict_
         const T vt = (T)val;
         Wn[pt] = vt;
         acc[0] += (double)vt;
+    }
+    block_sum<NMOM>(acc, red);
+    if (threadIdx.x == 0)
+        for (int i = 0; i < NMOM; ++i) partials[(long long)blockIdx.x * NMOM + i] = acc[i];
+}
+
+// Row-separable regrid: when the old index coordinates v_a, a >= 1, do not depend on
+// the new u'_0 (M[a][0] == 0 for a >= 1 -- exactly the case after an axis-aligned
+// regrid followed by a CV-type drift, whose e^{A tau} is block upper triangular),
+// every point of a new axis-0 row interpolates between the SAME 2^(nx-1) old rows
+// with the SAME weights: blend those rows once (coalesced), then interpolate
+// linearly along axis 0 (zero ghosts at both ends). Identical to the 2^nx-tap
+// multilinear formula of R12 up to rounding order. Otherwise the kernel falls back
+// to the per-point gather (k_regrid_gather's arithmetic).
+template <typename T, int NX>
+__global__ void __launch_bounds__(128, 4) k_regrid_rows(const T* __restrict__ Wold, T* __restrict__ Wnew,
+                                                       const FilterState* __restrict__ st, Dims d, DivSet dv,
+                                                       int nbpf, double ks, double* __restrict__ partials) {
+    constexpr int NC = 1 << (NX - 1);                  // old rows blended per new row
+    constexpr int CH = 8;                              // new rows per chunk
+    __shared__ double red[32 * NMOM];
+    __shared__ double Msh[16], osh[4];
+    __shared__ int sep_sh;
+    __shared__ double rw[CH][NC];                      // corner weights (0 for invalid rows)
+    __shared__ long long roff[CH][NC];                 // old row offsets
+    __shared__ double rv0[CH];                         // v0 at u'_0 = 0 for the row
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    double* tmp = reinterpret_cast<double*>(smem_raw); // [CH][N0]
+    const int filt = blockIdx.x / nbpf, qb = blockIdx.x - filt * nbpf;
+    const FilterState& f = st[filt];
+    const int N0 = d.n[0];
+    if (threadIdx.x == 0) {
+        double cn[4], Bn[16], Bi[16];
+        regrid_target(NX, d.n, f, ks, cn, Bn);
+        mat_inv4(NX, f.B, Bi);
+        double M[16];
+        for (int i = 0; i < 16; ++i) M[i] = 0.0;
+        mat_mul4(NX, Bi, Bn, M);
+        int sep = 1;
+        for (int a2 = 1; a2 < NX; ++a2) sep &= (M[a2 * 4] == 0.0);
+        sep_sh = sep;
+        for (int i = 0; i < 16; ++i) Msh[i] = M[i];
+        for (int a2 = 0; a2 < NX; ++a2) {
+            double sacc = 0.5 * (d.n[a2] - 1);
+            for (int b2 = 0; b2 < NX; ++b2) sacc = fma(Bi[a2 * 4 + b2], cn[b2] - f.c[b2], sacc);
+            osh[a2] = sacc;
+        }
+    }
+    __syncthreads();
+    const T* Wo = Wold + (long long)filt * d.ntot;
+    T* Wn = Wnew + (long long)filt * d.ntot;
+    double acc[NMOM];
+#pragma unroll
+    for (int i = 0; i < NMOM; ++i) acc[i] = 0.0;
+    long long stride[4];
+    stride[0] = 1;
+#pragma unroll
+    for (int a2 = 1; a2 < NX; ++a2) stride[a2] = stride[a2 - 1] * d.n[a2 - 1];
+    if (sep_sh) {
+        const long long rpf = d.ntot / N0;
+        const long long per = (rpf + nbpf - 1) / nbpf;
+        const long long rb = (long long)qb * per, re = rb + per < rpf ? rb + per : rpf;
+        const float invN0 = 1.0f / N0;
+        for (long long c0 = rb; c0 < re; c0 += CH) {
+            const int nr = (int)((re - c0) < CH ? (re - c0) : CH);
+            // per-row constants: old-row corners and weights, v0 offset
+            if (threadIdx.x < nr) {
+                const int rl = threadIdx.x;
+                unsigned rr = (unsigned)(c0 + rl);
+                double u[4] = {0, 0, 0, 0};
+#pragma unroll
+                for (int a2 = 1; a2 < NX; ++a2) {
+                    const unsigned qq = (a2 < NX - 1) ? fdiv(rr, dv.n[a2]) : 0u;
+                    const unsigned j = (a2 < NX - 1) ? rr - qq * (unsigned)d.n[a2] : rr;
+                    u[a2] = (double)j - 0.5 * (d.n[a2] - 1);
+                    rr = qq;
+                }
+                double fr[4] = {0, 0, 0, 0};
+                int i0[4] = {0, 0, 0, 0};
+                double v0 = osh[0];
+#pragma unroll
+                for (int b2 = 1; b2 < NX; ++b2) v0 = fma(Msh[b2], u[b2], v0);
+                rv0[rl] = v0;
+#pragma unroll
+                for (int a2 = 1; a2 < NX; ++a2) {
+                    double v = osh[a2];
+#pragma unroll
+                    for (int b2 = 1; b2 < NX; ++b2) v = fma(Msh[a2 * 4 + b2], u[b2], v);
+                    const double fl = floor(v);
+                    i0[a2] = __double2int_rz(fl);
+                    fr[a2] = v - fl;
+                }
+#pragma unroll
+                for (int c = 0; c < NC; ++c) {
+                    double wt = 1.0;
+                    long long off = 0;
+                    bool ok = true;
+#pragma unroll
+                    for (int a2 = 1; a2 < NX; ++a2) {
+                        const int bit = (c >> (a2 - 1)) & 1;
+                        const int ia = i0[a2] + bit;
+                        wt *= bit ? fr[a2] : (1.0 - fr[a2]);
+                        ok = ok && ia >= 0 && ia <= d.n[a2] - 1;
+                        off += (long long)ia * stride[a2];
+                    }
+                    rw[rl][c] = ok ? wt : 0.0;
+                    roff[rl][c] = ok ? off : 0;
+                }
+            }
+            __syncthreads();
+            for (int e = threadIdx.x; e < nr * N0; e += blockDim.x) {
+                const int rl = (int)((e + 0.5f) * invN0), i = e - rl * N0;
+                double v = 0.0;
+#pragma unroll
+                for (int c = 0; c < NC; ++c) v = fma(rw[rl][c], (double)Wo[roff[rl][c] + i], v);
+                tmp[rl * N0 + i] = v;
+            }
+            __syncthreads();
+            const double M00 = Msh[0];
+            for (int e = threadIdx.x; e < nr * N0; e += blockDim.x) {
+                const int rl = (int)((e + 0.5f) * invN0), j = e - rl * N0;
+                const double v0 = fma(M00, (double)j - 0.5 * (N0 - 1), rv0[rl]);
+                const double fl = floor(v0);
+                const int ia = __double2int_rz(fl);
+                const double fa = v0 - fl;
+                const double lo = (ia >= 0 && ia <= N0 - 1) ? tmp[rl * N0 + ia] : 0.0;
+                const double hi = (ia >= -1 && ia <= N0 - 2) ? tmp[rl * N0 + ia + 1] : 0.0;
+                const T vt = (T)fma(fa, hi - lo, lo);
+                Wn[(c0 + rl) * N0 + j] = vt;
+                acc[0] += (double)vt;
+            }
+            __syncthreads();
+        }
+    } else {
+        double M[16], o[4];
+#pragma unroll
+        for (int i = 0; i < NX; ++i) {
+            o[i] = osh[i];
+#pragma unroll
+            for (int j = 0; j < NX; ++j) M[i * 4 + j] = Msh[i * 4 + j];
+        }
+        for (long long pt = (long long)qb * blockDim.x + threadIdx.x; pt < d.ntot;
+             pt += (long long)nbpf * blockDim.x) {
+            double u[4];
+            point_u<NX>(d, dv, (unsigned)pt, u);
+            double fr[4];
+            long long base = 0;
+            bool lo_ok[4], hi_ok[4];
+#pragma unroll
+            for (int a2 = 0; a2 < NX; ++a2) {
+                double sv = o[a2];
+#pragma unroll
+                for (int b2 = 0; b2 < NX; ++b2) sv = fma(M[a2 * 4 + b2], u[b2], sv);
+                const double fl = floor(sv);
+                const int ia = __double2int_rz(fl);
+                fr[a2] = sv - fl;
+                lo_ok[a2] = ia >= 0 && ia <= d.n[a2] - 1;
+                hi_ok[a2] = ia >= -1 && ia <= d.n[a2] - 2;
+                base += (long long)ia * stride[a2];
+            }
+            double val = 0.0;
+#pragma unroll
+            for (int corner = 0; corner < (1 << NX); ++corner) {
+                double wt = 1.0;
+                long long off = base;
+                bool ok = true;
+#pragma unroll
+                for (int a2 = 0; a2 < NX; ++a2) {
+                    const bool bit = (corner >> a2) & 1;
+                    wt *= bit ? fr[a2] : (1.0 - fr[a2]);
+                    ok = ok && (bit ? hi_ok[a2] : lo_ok[a2]);
+                    if (bit) off += stride[a2];
+                }
+                if (ok) val = fma(wt, (double)Wo[off], val);
+            }
+            const T vt = (T)val;
+            Wn[pt] = vt;
+            acc[0] += (double)vt;
+        }
     }
     block_sum<NMOM>(acc, red);
     if (threadIdx.x == 0)
@@ -816,26 +1003,30 @@ static cudaError_t predict_nd(const Dims& d, PencilBufs& b, const Twiddles& tw, 
     for (int m = 1; m < d.nx - 1; ++m) PMF_TRY(strided(m, 0));
     PMF_TRY(strided(d.nx - 1, 2));
     for (int m = d.nx - 2; m >= 1; --m) PMF_TRY(strided(m, 1));
-    // axis 0 inverse (C2R) + update
+    // axis 0 inverse (C2R) + update: cpf CTAs per filter, tpc tiles each
+    const int tiles_pf = (int)(rpf / P0);
+    const int cpf = std::max(1, std::min(tiles_pf, 2048 / std::max(1, d.batch)));
+    const int tpc = (tiles_pf + cpf - 1) / cpf;
+    const int cpf_used = (tiles_pf + tpc - 1) / tpc;
     size_t smc = sm0 + 32 * NMOM * sizeof(double) + 6 * sizeof(double) * P0;
     PMF_TRY(with_nc(N0, [&](auto nc) -> cudaError_t {
         constexpr int NC = decltype(nc)::value;
         if (lp) {
             PMF_TRY(smem_attr(k_axis0_c2r<T, true, NX, NC>, smc));
-            k_axis0_c2r<T, true, NX, NC><<<(unsigned)nrow_blocks, kThreads, smc, s>>>(
+            k_axis0_c2r<T, true, NX, NC><<<(unsigned)(cpf_used * d.batch), kThreads, smc, s>>>(
                 (const V*)b.S, (T*)b.W, b.st, d, dv, pl0, (const V*)tw.tw[0], P0, lpv, b.z, b.coef, cs,
-                lq_off(mp.l), b.partials);
+                lq_off(mp.l), b.partials, cpf_used, tpc);
         } else {
             PMF_TRY(smem_attr(k_axis0_c2r<T, false, NX, NC>, smc));
-            k_axis0_c2r<T, false, NX, NC><<<(unsigned)nrow_blocks, kThreads, smc, s>>>(
+            k_axis0_c2r<T, false, NX, NC><<<(unsigned)(cpf_used * d.batch), kThreads, smc, s>>>(
                 (const V*)b.S, (T*)b.W, b.st, d, dv, pl0, (const V*)tw.tw[0], P0, lpv, b.z, b.coef, cs,
-                lq_off(mp.l), b.partials);
+                lq_off(mp.l), b.partials, cpf_used, tpc);
         }
         return cudaGetLastError();
     }));
     ++*launches;
     if (lp) {
-        k_finalize<<<d.batch, kThreads, 0, s>>>(b.st, b.partials, (int)(rpf / P0), d, 0);
+        k_finalize<<<d.batch, kThreads, 0, s>>>(b.st, b.partials, cpf_used, d, 0);
         ++*launches;
     }
     return cudaGetLastError();
@@ -937,8 +1128,16 @@ cudaError_t launch_normalise_state(const Dims& d, int dtype, PencilBufs& b, cuda
 template <typename T, int NX>
 static cudaError_t regrid_nd(const Dims& d, PencilBufs& b, double ks, cudaStream_t s, int64_t* launches) {
     int nbpf = blocks_per_filter(d.ntot);
-    k_regrid_gather<T, NX><<<(unsigned)((long long)nbpf * d.batch), kThreads, 0, s>>>(
-        (const T*)b.W, (T*)b.W2, b.st, d, make_divs(d), nbpf, ks, b.partials);
+    if (NX >= 2) {
+        // row-separable path (falls back to the per-point gather inside when M is not)
+        const size_t sm = sizeof(double) * 8 * (size_t)d.n[0];
+        PMF_TRY(smem_attr(k_regrid_rows<T, NX>, sm));
+        k_regrid_rows<T, NX><<<(unsigned)((long long)nbpf * d.batch), 128, sm, s>>>(
+            (const T*)b.W, (T*)b.W2, b.st, d, make_divs(d), nbpf, ks, b.partials);
+    } else {
+        k_regrid_gather<T, NX><<<(unsigned)((long long)nbpf * d.batch), kThreads, 0, s>>>(
+            (const T*)b.W, (T*)b.W2, b.st, d, make_divs(d), nbpf, ks, b.partials);
+    }
     ++*launches;
     PMF_TRY(cudaGetLastError());
     k_finalize_regrid<<<d.batch, kThreads, 0, s>>>(b.st, b.partials, nbpf, d, ks);

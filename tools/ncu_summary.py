@@ -41,11 +41,12 @@ def main():
     ap.add_argument("rep")
     ap.add_argument("--top", type=int, default=12)
     ap.add_argument("--out", default=None)
+    ap.add_argument("--idx", type=int, default=0, help="which profiled launch in the report")
     a = ap.parse_args()
     lines = []
     p = lines.append
     raw = ncu_csv(a.rep, "--page", "raw")
-    h, units, vals = raw[0], raw[1], raw[2]
+    h, units, vals = raw[0], raw[1], raw[2 + a.idx]
     d = dict(zip(h, vals))
     u = dict(zip(h, units))
     p(f"report: {a.rep}")
@@ -65,7 +66,9 @@ def main():
     p("  stall reasons (warp-cycles per issued instruction):")
     for v, k in st[:10]:
         p(f"    {k:24s} {v:.3f}")
-    rows = ncu_csv(a.rep, "--page", "source", "--print-source", "sass")
+    allrows = ncu_csv(a.rep, "--page", "source", "--print-source", "sass")
+    starts = [i for i, r in enumerate(allrows) if r and r[0] == "Kernel Name"]
+    rows = allrows[starts[a.idx]:(starts[a.idx + 1] if a.idx + 1 < len(starts) else None)] if starts else []
     if len(rows) > 2:
         hh = rows[1]
         si, ni = hh.index("Source"), hh.index("Warp Stall Sampling (All Samples)")
