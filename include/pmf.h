@@ -165,6 +165,32 @@ int pmf_regrid(pmf_ctx* ctx, double k_sigma);
 int pmf_step(pmf_ctx* ctx, double dt, int steps, const double* z, int z_on_device,
              const pmf_likelihood* lik, double k_sigma);
 
+/* ---------------------------------------------------------------------------
+ * Sharded contexts: ONE filter (batch = 1, nx >= 2) whose grid
+ * is split into `world` slabs along its LAST axis (N_{nx-1} divisible by world).
+ * A predict does two all-to-all transposes (the last-axis transform needs whole
+ * pencils), an update one all-reduce of the moment sums, a regrid a grouped
+ * send/recv of the old planes each rank's new slab reads (R12). Everything else
+ * is local. The filter state (grid, moments) is replicated on every rank.
+ *
+ * pmf_nccl_unique_id: rank 0 creates the NCCL id (128 bytes) that every rank
+ * passes to pmf_create_sharded (broadcast it, e.g. with torch.distributed).
+ * libnccl.so.2 is loaded on first use (dlopen); PMF_E_CUDA if unavailable.
+ *
+ * pmf_create_sharded: cfg->n are the GLOBAL sizes. unique_id != NULL: this
+ * process is `rank` of `world` (one GPU each, NCCL over NVLink). unique_id ==
+ * NULL: "virtual ranks" -- all `world` slabs live in this one context on one
+ * device and the collectives become device copies; results equal the real
+ * sharded path up to the order of the all-reduce sum.
+ * Weights passed to pmf_set_state / returned by pmf_get_weights are the slabs
+ * the context holds, in slab order (virtual: the whole grid; real: the local
+ * slab, N_0 x ... x N_{nx-2} x (N_{nx-1}/world) values). */
+int pmf_nccl_unique_id(void* out128);
+int pmf_create_sharded(const pmf_config* cfg, const double* A, const double* Q, int rank, int world,
+                       const void* unique_id, pmf_ctx** out);
+/* Number of slabs the grid is split into (1 for an ordinary context). */
+int pmf_world(const pmf_ctx* ctx);
+
 /* Normalised density values (vol * sum = 1) of all filters on their current
  * grids, batch x N_total in dtype; dst on host or on cfg->device. Flushes
  * pending work. */

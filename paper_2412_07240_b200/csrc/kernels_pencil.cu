@@ -87,7 +87,7 @@ __device__ __forceinline__ void point_u(const Dims& d, const DivSet& dv, unsigne
     for (int a = 0; a < NX; ++a) {
         const unsigned q = (a < NX - 1) ? fdiv(pt, dv.n[a]) : 0u;
         const unsigned j = (a < NX - 1) ? pt - q * (unsigned)d.n[a] : pt;
-        u[a] = (double)j - 0.5 * (d.n[a] - 1);
+        u[a] = (double)(j + d.lo[a]) - 0.5 * (d.ng[a] - 1);
         pt = q;
     }
 }
@@ -247,7 +247,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_axis_c2c(typename C2<T>::type* 
                                                         long long I, FFTPlan pl,
                                                         const typename C2<T>::type* __restrict__ tw, int P,
                                                         const double* __restrict__ coef, int cstride,
-                                                        ModelParams mp) {
+                                                        ModelParams mp, long long inner_off) {
     using V = typename C2<T>::type;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int N = NC > 0 ? NC : pl.N, PS = pencil_stride<NC>(N);
@@ -272,14 +272,14 @@ __global__ void __launch_bounds__(kThreads, 2) k_axis_c2c(typename C2<T>::type* 
             const double* cf = coef + o * cstride + 4;   // o is the filter index on the last axis
             double ntot = 1.0;
 #pragma unroll
-            for (int q = 0; q < NX; ++q) ntot *= d.n[q];
+            for (int q = 0; q < NX; ++q) ntot *= d.ng[q];
             const double mult = mp.s / ntot;
             const int l = mp.l;
             const bool cached = l <= LCAP;
             double* pg = reinterpret_cast<double*>(b + P * PS);    // [P][l][2]: gam, bet
             constexpr int L = NX - 1;
             auto pencil_k = [&](long long i, double* kap, double* kx) {
-                long long rem = i;
+                long long rem = i + inner_off;          // global inner index (sharded: my range)
                 const int k0 = (int)(rem % d.H0);
                 rem /= d.H0;
                 wavenum(k0, d.n[0], kap[0], kx[0]);
@@ -403,7 +403,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_axis0_c2r(const typename C2<T>:
                 for (int a2 = 1; a2 < NX; ++a2) {
                     const unsigned qq = (a2 < NX - 1) ? fdiv(rr, dv.n[a2]) : 0u;
                     const unsigned j = (a2 < NX - 1) ? rr - qq * (unsigned)d.n[a2] : rr;
-                    u[a2] = (double)j - 0.5 * (d.n[a2] - 1);
+                    u[a2] = (double)(j + d.lo[a2]) - 0.5 * (d.ng[a2] - 1);
                     rr = qq;
                 }
                 double A = q[0], Bc = q[1];
@@ -585,16 +585,22 @@ __device__ inline void block_sum_partials(const double* __restrict__ partials, l
     block_sum<NMOM>(acc, red);
 }
 
+// Scalar tail of every reduction (sums acc[] over the whole filter):
 // MODE 0: update -> normaliser C = vol * sum, log C, scale = 1/C, moments.
 // MODE 1: renormalise (init/set_state): scale = 1/(vol * sum).
-__global__ void k_finalize(FilterState* st, const double* __restrict__ partials, int nbpf, Dims d, int mode) {
-    __shared__ double red[32 * NMOM];
-    const int filt = blockIdx.x;
-    double acc[NMOM];
-    block_sum_partials(partials, (long long)filt * nbpf, nbpf, acc, red);
-    if (threadIdx.x != 0) return;
-    FilterState& f = st[filt];
+// MODE 2: commit a regrid: new grid (R12), scale = 1/(vol' * sum).
+__device__ inline void finalize_from(FilterState& f, const double* acc, const Dims& d, int mode, double ks) {
     const int nx = d.nx;
+    if (mode == 2) {
+        double cn[4], Bn[16];
+        bool ok = regrid_target(nx, d.ng, f, ks, cn, Bn);
+        for (int a = 0; a < nx; ++a) f.c[a] = cn[a];
+        for (int i = 0; i < 16; ++i) f.B[i] = Bn[i];
+        double C = fabs(det4(nx, Bn)) * acc[0];
+        if (!ok || !(C > 0.0) || !isfinite(C)) { f.status = -6; return; }
+        f.scale = 1.0 / C;
+        return;
+    }
     double vol = fabs(det4(nx, f.B));
     double C = vol * acc[0];
     if (mode == 0) {
@@ -615,6 +621,51 @@ __global__ void k_finalize(FilterState* st, const double* __restrict__ partials,
     }
 }
 
+__global__ void k_finalize(FilterState* st, const double* __restrict__ partials, int nbpf, Dims d, int mode) {
+    __shared__ double red[32 * NMOM];
+    const int filt = blockIdx.x;
+    double acc[NMOM];
+    block_sum_partials(partials, (long long)filt * nbpf, nbpf, acc, red);
+    if (threadIdx.x != 0) return;
+    finalize_from(st[filt], acc, d, mode, 0.0);
+}
+
+// sharded path: per-rank totals (partials -> tot), then after the all-reduce the tail
+__global__ void k_reduce_partials(const double* __restrict__ partials, int nbpf, double* __restrict__ tot) {
+    __shared__ double red[32 * NMOM];
+    const int filt = blockIdx.x;
+    double acc[NMOM];
+    block_sum_partials(partials, (long long)filt * nbpf, nbpf, acc, red);
+    if (threadIdx.x == 0)
+        for (int i = 0; i < NMOM; ++i) tot[(long long)filt * NMOM + i] = acc[i];
+}
+
+__global__ void k_finalize_tot(FilterState* st, const double* __restrict__ tot, Dims d, int mode, double ks, int batch) {
+    const int filt = blockIdx.x * blockDim.x + threadIdx.x;
+    if (filt >= batch) return;
+    finalize_from(st[filt], tot + (long long)filt * NMOM, d, mode, ks);
+}
+
+// all-to-all packing of the half spectrum [planes][I] into per-destination blocks
+// [d][planes][I_d] (x in I_d starts at inner offset off_d), and the inverse.
+template <typename V>
+__global__ void k_pack_blocks(const V* __restrict__ S, V* __restrict__ send, long long I, int planes,
+                              const long long* __restrict__ off, int world, int unpack) {
+    // off[0..world]: inner-range boundaries; block d holds planes x (off[d+1]-off[d]) values
+    const long long total = (long long)planes * I;
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+         e += (long long)gridDim.x * blockDim.x) {
+        const long long pl = e / I, x = e - pl * I;
+        int dd = 0;
+        while (dd + 1 < world && x >= off[dd + 1]) ++dd;
+        const long long Id = off[dd + 1] - off[dd];
+        const long long boff = (long long)planes * off[dd];     // block start in the packed buffer
+        const long long pe = boff + pl * Id + (x - off[dd]);
+        if (unpack) const_cast<V*>(S)[e] = send[pe];
+        else send[pe] = S[e];
+    }
+}
+
 // ============================================================================ regrid
 // Multilinear interpolation with zero ghost nodes at the points of the new grid
 // (R12). v = B^-1 (x' - c) + (N-1)/2 = o + M u' with M = B^-1 B', o = B^-1(c'-c)+(N-1)/2.
@@ -628,14 +679,14 @@ __global__ void __launch_bounds__(kThreads, 2) k_regrid_gather(const T* __restri
     const FilterState& f = st[filt];
     if (threadIdx.x == 0) {
         double cn[4], Bn[16], Bi[16];
-        regrid_target(NX, d.n, f, ks, cn, Bn);
+        regrid_target(NX, d.ng, f, ks, cn, Bn);
         mat_inv4(NX, f.B, Bi);
         double M[16];
         for (int i = 0; i < 16; ++i) M[i] = 0.0;
         mat_mul4(NX, Bi, Bn, M);
         for (int i = 0; i < 16; ++i) Msh[i] = M[i];
         for (int a = 0; a < NX; ++a) {
-            double s = 0.5 * (d.n[a] - 1);
+            double s = 0.5 * (d.ng[a] - 1);
             for (int b = 0; b < NX; ++b) s = fma(Bi[a * 4 + b], cn[b] - f.c[b], s);
             osh[a] = s;
         }
@@ -652,7 +703,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_regrid_gather(const T* __restri
     stride[0] = 1;
 #pragma unroll
     for (int a = 1; a < NX; ++a) stride[a] = stride[a - 1] * d.n[a - 1];
-    const T* Wo = Wold + (long long)filt * d.ntot;
+    const T* Wo = Wold + (long long)filt * (d.ntot / d.n[NX - 1] * d.src_n);   // regrid source window
     T* Wn = Wnew + (long long)filt * d.ntot;
     double acc[NMOM];
 #pragma unroll
@@ -671,9 +722,12 @@ __global__ void __launch_bounds__(kThreads, 2) k_regrid_gather(const T* __restri
             const double fl = floor(s);
             const int i0 = __double2int_rz(fl);           // saturating
             fr[a] = s - fl;
-            lo_ok[a] = i0 >= 0 && i0 <= d.n[a] - 1;
-            hi_ok[a] = i0 >= -1 && i0 <= d.n[a] - 2;
-            base += (long long)i0 * stride[a];
+            // global bounds (zero ghosts); the last axis is addressed inside the source window
+            const int w0 = (a == NX - 1) ? i0 - d.src_lo : i0;
+            const int wn = (a == NX - 1) ? d.src_n : d.n[a];
+            lo_ok[a] = i0 >= 0 && i0 <= d.ng[a] - 1 && w0 >= 0 && w0 <= wn - 1;
+            hi_ok[a] = i0 >= -1 && i0 <= d.ng[a] - 2 && w0 >= -1 && w0 <= wn - 2;
+            base += (long long)w0 * stride[a];
         }
         double val = 0.0;
 #pragma unroll
@@ -726,7 +780,7 @@ __global__ void __launch_bounds__(128, 4) k_regrid_rows(const T* __restrict__ Wo
     const int N0 = d.n[0];
     if (threadIdx.x == 0) {
         double cn[4], Bn[16], Bi[16];
-        regrid_target(NX, d.n, f, ks, cn, Bn);
+        regrid_target(NX, d.ng, f, ks, cn, Bn);
         mat_inv4(NX, f.B, Bi);
         double M[16];
         for (int i = 0; i < 16; ++i) M[i] = 0.0;
@@ -736,13 +790,13 @@ __global__ void __launch_bounds__(128, 4) k_regrid_rows(const T* __restrict__ Wo
         sep_sh = sep;
         for (int i = 0; i < 16; ++i) Msh[i] = M[i];
         for (int a2 = 0; a2 < NX; ++a2) {
-            double sacc = 0.5 * (d.n[a2] - 1);
+            double sacc = 0.5 * (d.ng[a2] - 1);
             for (int b2 = 0; b2 < NX; ++b2) sacc = fma(Bi[a2 * 4 + b2], cn[b2] - f.c[b2], sacc);
             osh[a2] = sacc;
         }
     }
     __syncthreads();
-    const T* Wo = Wold + (long long)filt * d.ntot;
+    const T* Wo = Wold + (long long)filt * (d.ntot / d.n[NX - 1] * d.src_n);   // regrid source window
     T* Wn = Wnew + (long long)filt * d.ntot;
     double acc[NMOM];
 #pragma unroll
@@ -767,7 +821,7 @@ __global__ void __launch_bounds__(128, 4) k_regrid_rows(const T* __restrict__ Wo
                 for (int a2 = 1; a2 < NX; ++a2) {
                     const unsigned qq = (a2 < NX - 1) ? fdiv(rr, dv.n[a2]) : 0u;
                     const unsigned j = (a2 < NX - 1) ? rr - qq * (unsigned)d.n[a2] : rr;
-                    u[a2] = (double)j - 0.5 * (d.n[a2] - 1);
+                    u[a2] = (double)(j + d.lo[a2]) - 0.5 * (d.ng[a2] - 1);
                     rr = qq;
                 }
                 double fr[4] = {0, 0, 0, 0};
@@ -795,8 +849,10 @@ __global__ void __launch_bounds__(128, 4) k_regrid_rows(const T* __restrict__ Wo
                         const int bit = (c >> (a2 - 1)) & 1;
                         const int ia = i0[a2] + bit;
                         wt *= bit ? fr[a2] : (1.0 - fr[a2]);
-                        ok = ok && ia >= 0 && ia <= d.n[a2] - 1;
-                        off += (long long)ia * stride[a2];
+                        const int wa = (a2 == NX - 1) ? ia - d.src_lo : ia;
+                        const int wn = (a2 == NX - 1) ? d.src_n : d.n[a2];
+                        ok = ok && ia >= 0 && ia <= d.ng[a2] - 1 && wa >= 0 && wa <= wn - 1;
+                        off += (long long)wa * stride[a2];
                     }
                     rw[rl][c] = ok ? wt : 0.0;
                     roff[rl][c] = ok ? off : 0;
@@ -849,9 +905,11 @@ __global__ void __launch_bounds__(128, 4) k_regrid_rows(const T* __restrict__ Wo
                 const double fl = floor(sv);
                 const int ia = __double2int_rz(fl);
                 fr[a2] = sv - fl;
-                lo_ok[a2] = ia >= 0 && ia <= d.n[a2] - 1;
-                hi_ok[a2] = ia >= -1 && ia <= d.n[a2] - 2;
-                base += (long long)ia * stride[a2];
+                const int w0 = (a2 == NX - 1) ? ia - d.src_lo : ia;
+                const int wn = (a2 == NX - 1) ? d.src_n : d.n[a2];
+                lo_ok[a2] = ia >= 0 && ia <= d.ng[a2] - 1 && w0 >= 0 && w0 <= wn - 1;
+                hi_ok[a2] = ia >= -1 && ia <= d.ng[a2] - 2 && w0 >= -1 && w0 <= wn - 2;
+                base += (long long)w0 * stride[a2];
             }
             double val = 0.0;
 #pragma unroll
@@ -884,14 +942,7 @@ __global__ void k_finalize_regrid(FilterState* st, const double* __restrict__ pa
     double acc[NMOM];
     block_sum_partials(partials, (long long)filt * nbpf, nbpf, acc, red);
     if (threadIdx.x != 0) return;
-    FilterState& f = st[filt];
-    double cn[4], Bn[16];
-    bool ok = regrid_target(d.nx, d.n, f, ks, cn, Bn);
-    for (int a = 0; a < d.nx; ++a) f.c[a] = cn[a];
-    for (int i = 0; i < 16; ++i) f.B[i] = Bn[i];
-    double C = fabs(det4(d.nx, Bn)) * acc[0];
-    if (!ok || !(C > 0.0) || !isfinite(C)) { f.status = -6; return; }
-    f.scale = 1.0 / C;
+    finalize_from(st[filt], acc, d, 2, ks);
 }
 
 template <typename T>
@@ -948,86 +999,105 @@ static cudaError_t with_nc(int N, F&& f) {
     }
 }
 
+// Phases of the nx >= 2 predict (so the sharded path can insert its transposes):
+//   PH_FWD: axis-0 R2C + forward C2C along axes 1..L-1 (L = nx-1)
+//   PH_PSI: last axis forward * s Psi * inverse on `psibuf` (I x N_L pencils, inner offset)
+//   PH_INV: inverse C2C axes L-1..1 + axis-0 C2R (+ update); moment partials reduced to
+//           `tot` (sharded) or finalised into the state (tot == nullptr)
+enum { PH_FWD = 1, PH_PSI = 2, PH_INV = 4, PH_ALL = 7 };
+
 template <typename T, int NX>
 static cudaError_t predict_nd(const Dims& d, PencilBufs& b, const Twiddles& tw, const ModelParams& mp,
-                              const LikParams* lp, const LikParams& lpv, int cs, cudaStream_t s, int64_t* launches) {
+                              const LikParams* lp, const LikParams& lpv, int cs, cudaStream_t s, int64_t* launches,
+                              int phases = PH_ALL, void* psibuf = nullptr, long long psiI = -1,
+                              long long inner_off = 0, double* tot = nullptr) {
     using V = typename C2<T>::type;
     const DivSet dv = make_divs(d);
-    // axis 0 forward (R2C)
     const int N0 = d.n[0];
     const long long rpf = d.ntot / N0;
     const int P0 = rows_per_cta(N0, rpf);
     FFTPlan pl0 = make_plan(N0);
     size_t sm0 = 2 * (size_t)P0 * pstride_host(N0) * sizeof(V);
     long long nrow_blocks = (long long)d.batch * rpf / P0;
-    PMF_TRY(with_nc(N0, [&](auto nc) -> cudaError_t {
-        constexpr int NC = decltype(nc)::value;
-        PMF_TRY(smem_attr(k_axis0_r2c<T, NC>, sm0));
-        k_axis0_r2c<T, NC><<<(unsigned)nrow_blocks, kThreads, sm0, s>>>((const T*)b.W, (V*)b.S, b.coef, cs, d, pl0,
-                                                                        (const V*)tw.tw[0], P0);
-        return cudaGetLastError();
-    }));
-    ++*launches;
     // strided axes
-    auto strided = [&](int m, int mode) -> cudaError_t {
+    auto strided = [&](int m, int mode, V* buf, long long Iov, long long Oov, long long ioff) -> cudaError_t {
         long long I = d.H0;
         for (int q = 1; q < m; ++q) I *= d.n[q];
         long long O = d.batch;
         for (int q = m + 1; q < d.nx; ++q) O *= d.n[q];
-        const int N = d.n[m];
+        if (Iov >= 0) { I = Iov; O = Oov; }
+        const int N = (Iov >= 0) ? d.ng[m] : d.n[m];
         const int P = pencils_per_cta(N);
         FFTPlan pl = make_plan(N);
         size_t sm = 2 * (size_t)P * pstride_host(N) * sizeof(V);
         if (mode == 2) sm += sizeof(double) * 2 * P * std::min(mp.l, LCAP);
         long long nblk = O * ((I + P - 1) / P);
+        if (nblk == 0) return cudaSuccess;
         cudaError_t e = with_nc(N, [&](auto nc) -> cudaError_t {
             constexpr int NC = decltype(nc)::value;
             if (mode == 0) {
                 PMF_TRY(smem_attr(k_axis_c2c<T, 0, 2, NC>, sm));
-                k_axis_c2c<T, 0, 2, NC><<<(unsigned)nblk, kThreads, sm, s>>>((V*)b.S, d, m, I, pl,
-                                                                              (const V*)tw.tw[m], P, b.coef, cs, mp);
+                k_axis_c2c<T, 0, 2, NC><<<(unsigned)nblk, kThreads, sm, s>>>(buf, d, m, I, pl, (const V*)tw.tw[m], P,
+                                                                              b.coef, cs, mp, ioff);
             } else if (mode == 1) {
                 PMF_TRY(smem_attr(k_axis_c2c<T, 1, 2, NC>, sm));
-                k_axis_c2c<T, 1, 2, NC><<<(unsigned)nblk, kThreads, sm, s>>>((V*)b.S, d, m, I, pl,
-                                                                              (const V*)tw.tw[m], P, b.coef, cs, mp);
+                k_axis_c2c<T, 1, 2, NC><<<(unsigned)nblk, kThreads, sm, s>>>(buf, d, m, I, pl, (const V*)tw.tw[m], P,
+                                                                              b.coef, cs, mp, ioff);
             } else {
                 PMF_TRY(smem_attr(k_axis_c2c<T, 2, NX, NC>, sm));
-                k_axis_c2c<T, 2, NX, NC><<<(unsigned)nblk, kThreads, sm, s>>>((V*)b.S, d, m, I, pl,
-                                                                               (const V*)tw.tw[m], P, b.coef, cs, mp);
+                k_axis_c2c<T, 2, NX, NC><<<(unsigned)nblk, kThreads, sm, s>>>(buf, d, m, I, pl, (const V*)tw.tw[m],
+                                                                               P, b.coef, cs, mp, ioff);
             }
             return cudaGetLastError();
         });
         ++*launches;
         return e;
     };
-    for (int m = 1; m < d.nx - 1; ++m) PMF_TRY(strided(m, 0));
-    PMF_TRY(strided(d.nx - 1, 2));
-    for (int m = d.nx - 2; m >= 1; --m) PMF_TRY(strided(m, 1));
-    // axis 0 inverse (C2R) + update: cpf CTAs per filter, tpc tiles each
-    const int tiles_pf = (int)(rpf / P0);
-    const int cpf = std::max(1, std::min(tiles_pf, 2048 / std::max(1, d.batch)));
-    const int tpc = (tiles_pf + cpf - 1) / cpf;
-    const int cpf_used = (tiles_pf + tpc - 1) / tpc;
-    size_t smc = sm0 + 32 * NMOM * sizeof(double) + 6 * sizeof(double) * P0;
-    PMF_TRY(with_nc(N0, [&](auto nc) -> cudaError_t {
-        constexpr int NC = decltype(nc)::value;
-        if (lp) {
-            PMF_TRY(smem_attr(k_axis0_c2r<T, true, NX, NC>, smc));
-            k_axis0_c2r<T, true, NX, NC><<<(unsigned)(cpf_used * d.batch), kThreads, smc, s>>>(
-                (const V*)b.S, (T*)b.W, b.st, d, dv, pl0, (const V*)tw.tw[0], P0, lpv, b.z, b.coef, cs,
-                lq_off(mp.l), b.partials, cpf_used, tpc);
-        } else {
-            PMF_TRY(smem_attr(k_axis0_c2r<T, false, NX, NC>, smc));
-            k_axis0_c2r<T, false, NX, NC><<<(unsigned)(cpf_used * d.batch), kThreads, smc, s>>>(
-                (const V*)b.S, (T*)b.W, b.st, d, dv, pl0, (const V*)tw.tw[0], P0, lpv, b.z, b.coef, cs,
-                lq_off(mp.l), b.partials, cpf_used, tpc);
-        }
-        return cudaGetLastError();
-    }));
-    ++*launches;
-    if (lp) {
-        k_finalize<<<d.batch, kThreads, 0, s>>>(b.st, b.partials, cpf_used, d, 0);
+    if (phases & PH_FWD) {
+        // axis 0 forward (R2C)
+        PMF_TRY(with_nc(N0, [&](auto nc) -> cudaError_t {
+            constexpr int NC = decltype(nc)::value;
+            PMF_TRY(smem_attr(k_axis0_r2c<T, NC>, sm0));
+            k_axis0_r2c<T, NC><<<(unsigned)nrow_blocks, kThreads, sm0, s>>>((const T*)b.W, (V*)b.S, b.coef, cs, d,
+                                                                            pl0, (const V*)tw.tw[0], P0);
+            return cudaGetLastError();
+        }));
         ++*launches;
+        for (int m = 1; m < d.nx - 1; ++m) PMF_TRY(strided(m, 0, (V*)b.S, -1, -1, 0));
+    }
+    if (phases & PH_PSI) {
+        if (psibuf) PMF_TRY(strided(d.nx - 1, 2, (V*)psibuf, psiI, 1, inner_off));
+        else PMF_TRY(strided(d.nx - 1, 2, (V*)b.S, -1, -1, 0));
+    }
+    if (phases & PH_INV) {
+        for (int m = d.nx - 2; m >= 1; --m) PMF_TRY(strided(m, 1, (V*)b.S, -1, -1, 0));
+        // axis 0 inverse (C2R) + update: cpf CTAs per filter, tpc tiles each
+        const int tiles_pf = (int)(rpf / P0);
+        const int cpf = std::max(1, std::min(tiles_pf, 2048 / std::max(1, d.batch)));
+        const int tpc = (tiles_pf + cpf - 1) / cpf;
+        const int cpf_used = (tiles_pf + tpc - 1) / tpc;
+        size_t smc = sm0 + 32 * NMOM * sizeof(double) + 6 * sizeof(double) * P0;
+        PMF_TRY(with_nc(N0, [&](auto nc) -> cudaError_t {
+            constexpr int NC = decltype(nc)::value;
+            if (lp) {
+                PMF_TRY(smem_attr(k_axis0_c2r<T, true, NX, NC>, smc));
+                k_axis0_c2r<T, true, NX, NC><<<(unsigned)(cpf_used * d.batch), kThreads, smc, s>>>(
+                    (const V*)b.S, (T*)b.W, b.st, d, dv, pl0, (const V*)tw.tw[0], P0, lpv, b.z, b.coef, cs,
+                    lq_off(mp.l), b.partials, cpf_used, tpc);
+            } else {
+                PMF_TRY(smem_attr(k_axis0_c2r<T, false, NX, NC>, smc));
+                k_axis0_c2r<T, false, NX, NC><<<(unsigned)(cpf_used * d.batch), kThreads, smc, s>>>(
+                    (const V*)b.S, (T*)b.W, b.st, d, dv, pl0, (const V*)tw.tw[0], P0, lpv, b.z, b.coef, cs,
+                    lq_off(mp.l), b.partials, cpf_used, tpc);
+            }
+            return cudaGetLastError();
+        }));
+        ++*launches;
+        if (lp) {
+            if (tot) k_reduce_partials<<<d.batch, kThreads, 0, s>>>(b.partials, cpf_used, tot);
+            else k_finalize<<<d.batch, kThreads, 0, s>>>(b.st, b.partials, cpf_used, d, 0);
+            ++*launches;
+        }
     }
     return cudaGetLastError();
 }
@@ -1159,6 +1229,136 @@ static cudaError_t regrid_t(const Dims& d, PencilBufs& b, double ks, cudaStream_
 cudaError_t launch_regrid(const Dims& d, int dtype, PencilBufs& b, double ks, cudaStream_t s, int64_t* launches) {
     if (dtype == 0) return regrid_t<double>(d, b, ks, s, launches);
     return regrid_t<float>(d, b, ks, s, launches);
+}
+
+// ============================================================================ sharded building blocks
+template <typename T>
+static cudaError_t sh_phase_t(const Dims& d, PencilBufs& b, const Twiddles& tw, const ModelParams& mp,
+                              const LikParams* lp, int phase, void* psibuf, long long psiI, long long ioff,
+                              double* tot, cudaStream_t s, int64_t* launches) {
+    const int cs = coef_stride(mp.l);
+    LikParams lpv{};
+    if (lp) lpv = *lp;
+    if (d.nx == 2) return predict_nd<T, 2>(d, b, tw, mp, lp, lpv, cs, s, launches, phase, psibuf, psiI, ioff, tot);
+    if (d.nx == 3) return predict_nd<T, 3>(d, b, tw, mp, lp, lpv, cs, s, launches, phase, psibuf, psiI, ioff, tot);
+    return predict_nd<T, 4>(d, b, tw, mp, lp, lpv, cs, s, launches, phase, psibuf, psiI, ioff, tot);
+}
+
+cudaError_t sh_prep(const Dims& d, PencilBufs& b, const ModelParams& mp, const LikParams* lp, cudaStream_t s,
+                    int64_t* launches) {
+    LikParams lpv{};
+    if (lp) lpv = *lp;
+    k_predict_prep<<<(d.batch + 127) / 128, 128, 0, s>>>(b.st, b.coef, coef_stride(mp.l), mp, b.sub, d.batch, lpv,
+                                                         b.z, lp ? 1 : 0);
+    ++*launches;
+    return cudaGetLastError();
+}
+
+cudaError_t sh_phase(const Dims& d, int dtype, PencilBufs& b, const Twiddles& tw, const ModelParams& mp,
+                     const LikParams* lp, int phase, void* psibuf, long long psiI, long long ioff, double* tot,
+                     cudaStream_t s, int64_t* launches) {
+    if (dtype == 0) return sh_phase_t<double>(d, b, tw, mp, lp, phase, psibuf, psiI, ioff, tot, s, launches);
+    return sh_phase_t<float>(d, b, tw, mp, lp, phase, psibuf, psiI, ioff, tot, s, launches);
+}
+
+cudaError_t sh_pack(int dtype, void* S, void* send, long long I, int planes, const long long* d_off, int world,
+                    int unpack, cudaStream_t s, int64_t* launches) {
+    const long long total = (long long)planes * I;
+    const unsigned nb = (unsigned)std::max(1LL, std::min((total + 255) / 256, 148LL * 32));
+    if (dtype == 0)
+        k_pack_blocks<double2><<<nb, 256, 0, s>>>((const double2*)S, (double2*)send, I, planes, d_off, world, unpack);
+    else
+        k_pack_blocks<float2><<<nb, 256, 0, s>>>((const float2*)S, (float2*)send, I, planes, d_off, world, unpack);
+    ++*launches;
+    return cudaGetLastError();
+}
+
+template <typename T, int MODE>
+static cudaError_t sh_points_t(const Dims& d, PencilBufs& b, const LikParams& lp, double* tot, cudaStream_t s,
+                               int64_t* launches) {
+    int nbpf = blocks_per_filter(d.ntot);
+    const unsigned g = (unsigned)((long long)nbpf * d.batch);
+    switch (d.nx) {
+        case 2: k_points<T, MODE, 2><<<g, kThreads, 0, s>>>((T*)b.W, b.st, d, make_divs(d), nbpf, lp, b.z, b.gauss,
+                                                             b.partials); break;
+        case 3: k_points<T, MODE, 3><<<g, kThreads, 0, s>>>((T*)b.W, b.st, d, make_divs(d), nbpf, lp, b.z, b.gauss,
+                                                             b.partials); break;
+        default: k_points<T, MODE, 4><<<g, kThreads, 0, s>>>((T*)b.W, b.st, d, make_divs(d), nbpf, lp, b.z, b.gauss,
+                                                              b.partials); break;
+    }
+    ++*launches;
+    PMF_TRY(cudaGetLastError());
+    k_reduce_partials<<<d.batch, kThreads, 0, s>>>(b.partials, nbpf, tot);
+    ++*launches;
+    return cudaGetLastError();
+}
+
+// mode: 0 likelihood update, 1 init gaussian, 2 plain sum (set_state)
+cudaError_t sh_points(const Dims& d, int dtype, PencilBufs& b, int mode, const LikParams& lp, double* tot,
+                      cudaStream_t s, int64_t* launches) {
+    if (dtype == 0) {
+        if (mode == 0) return sh_points_t<double, 0>(d, b, lp, tot, s, launches);
+        if (mode == 1) return sh_points_t<double, 1>(d, b, lp, tot, s, launches);
+        return sh_points_t<double, 2>(d, b, lp, tot, s, launches);
+    }
+    if (mode == 0) return sh_points_t<float, 0>(d, b, lp, tot, s, launches);
+    if (mode == 1) return sh_points_t<float, 1>(d, b, lp, tot, s, launches);
+    return sh_points_t<float, 2>(d, b, lp, tot, s, launches);
+}
+
+template <typename T>
+static cudaError_t sh_regrid_t(const Dims& d, const void* src, void* dst, PencilBufs& b, double ks, double* tot,
+                               cudaStream_t s, int64_t* launches) {
+    int nbpf = blocks_per_filter(d.ntot);
+    const size_t sm = sizeof(double) * 8 * (size_t)d.n[0];
+    const unsigned g = (unsigned)((long long)nbpf * d.batch);
+    switch (d.nx) {
+        case 2:
+            PMF_TRY(smem_attr(k_regrid_rows<T, 2>, sm));
+            k_regrid_rows<T, 2><<<g, 128, sm, s>>>((const T*)src, (T*)dst, b.st, d, make_divs(d), nbpf, ks, b.partials);
+            break;
+        case 3:
+            PMF_TRY(smem_attr(k_regrid_rows<T, 3>, sm));
+            k_regrid_rows<T, 3><<<g, 128, sm, s>>>((const T*)src, (T*)dst, b.st, d, make_divs(d), nbpf, ks, b.partials);
+            break;
+        default:
+            PMF_TRY(smem_attr(k_regrid_rows<T, 4>, sm));
+            k_regrid_rows<T, 4><<<g, 128, sm, s>>>((const T*)src, (T*)dst, b.st, d, make_divs(d), nbpf, ks, b.partials);
+            break;
+    }
+    ++*launches;
+    PMF_TRY(cudaGetLastError());
+    k_reduce_partials<<<d.batch, kThreads, 0, s>>>(b.partials, nbpf, tot);
+    ++*launches;
+    return cudaGetLastError();
+}
+
+cudaError_t sh_regrid(const Dims& d, int dtype, const void* src, void* dst, PencilBufs& b, double ks, double* tot,
+                      cudaStream_t s, int64_t* launches) {
+    if (dtype == 0) return sh_regrid_t<double>(d, src, dst, b, ks, tot, s, launches);
+    return sh_regrid_t<float>(d, src, dst, b, ks, tot, s, launches);
+}
+
+// sum over ranks in rank order (virtual-rank all-reduce)
+__global__ void k_sum_ranks(const double* __restrict__ in, double* __restrict__ out, int world, int n) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double s = 0.0;
+    for (int r = 0; r < world; ++r) s += in[r * n + i];
+    out[i] = s;
+}
+
+cudaError_t launch_sum_ranks(const double* in, double* out, int world, int n, cudaStream_t s, int64_t* launches) {
+    k_sum_ranks<<<(n + 127) / 128, 128, 0, s>>>(in, out, world, n);
+    ++*launches;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_finalize_tot(const Dims& d, FilterState* st, const double* tot, int mode, double ks,
+                                cudaStream_t s, int64_t* launches) {
+    k_finalize_tot<<<(d.batch + 127) / 128, 128, 0, s>>>(st, tot, d, mode, ks, d.batch);
+    ++*launches;
+    return cudaGetLastError();
 }
 
 cudaError_t launch_scale_out(const Dims& d, int dtype, const PencilBufs& b, void* dst, cudaStream_t s,

@@ -1,0 +1,85 @@
+// pmf_ctx_impl.h -- the context object behind the C ABI and the host helpers
+// shared by pmf_host.cpp (single-device contexts) and pmf_sharded.cpp (contexts
+// whose grid is split into slabs along the last axis). Not part of the ABI.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/pmf.h"
+#include "pmf_internal.h"
+
+namespace pmf {
+struct ShardSet;   // pmf_sharded.cpp
+}
+
+struct Pending {
+    bool predict = false;
+    double dt = 0.0;
+    int steps = 0;
+    bool regrid = false;
+    double k_sigma = 0.0;
+};
+
+struct pmf_ctx {
+    pmf_config cfg{};
+    pmf::Dims d{};
+    int dtype = 0;
+    int path = PMF_PATH_PENCIL;
+    size_t esize = 8;
+    double A[16]{}, Q[16]{};
+    cudaStream_t stream = nullptr;
+    // device buffers
+    void* W = nullptr;
+    void* W2 = nullptr;
+    void* S = nullptr;
+    pmf::FilterState* st = nullptr;
+    double* partials = nullptr;
+    size_t partials_bytes = 0;
+    double* coef = nullptr;
+    size_t coef_bytes = 0;
+    pmf::SubstepEntry* sub = nullptr;
+    size_t sub_bytes = 0;
+    double* z = nullptr;
+    double* gauss = nullptr;
+    double* mom_dev = nullptr;       // compact moments [batch][nx + nx^2 + 2]
+    double* mom_host = nullptr;      // pinned host mirror
+    void* tw[4] = {nullptr, nullptr, nullptr, nullptr};
+    int64_t bytes = 0;
+    // host-side model cache (per (dt, steps))
+    double cached_dt = -1.0;
+    int cached_steps = -1;
+    pmf::ModelParams mp{};
+    // state machine
+    bool have_density = false;
+    bool have_update = false;
+    Pending pend;
+    int64_t launches = 0;
+    // kernel timing (pmf_profile): event pairs around the dominant kernel of each flush
+    bool prof = false;
+    std::vector<cudaEvent_t> evs;
+    int nev = 0;
+    std::string err;
+    // sharded context (slab decomposition along the last axis), else null
+    pmf::ShardSet* sh = nullptr;
+};
+
+// helpers implemented in pmf_host.cpp
+int pmf_fail(pmf_ctx* c, int code, const std::string& msg);
+int pmf_cuda_fail(pmf_ctx* c, cudaError_t e, const char* where);
+int pmf_dalloc(pmf_ctx* c, void** p, size_t bytes);
+int pmf_prepare_model(pmf_ctx* c, double dt, int steps);
+int pmf_make_lik(pmf_ctx* c, const pmf_likelihood* lik, pmf::LikParams& lp);
+double pmf_det_inv(int n, const double* A, double* Ai);
+void pmf_unpack(int n, const double* src, double* dst);
+int pmf_validate_model(const pmf_config* cfg, const double* A, const double* Q, double* Qs);
+template <typename T>
+void pmf_make_twiddles(int N, std::vector<T>& out);
+
+// sharded contexts (pmf_sharded.cpp)
+int sh_set_gaussian(pmf_ctx* c, const double* mean, const double* cov, double k_sigma);
+int sh_set_state(pmf_ctx* c, const double* center, const double* B, const void* weights, int on_device);
+int sh_flush(pmf_ctx* c, const pmf::LikParams* lp);
+int sh_get_weights(pmf_ctx* c, void* dst, int on_device);
+void sh_destroy(pmf_ctx* c);

@@ -17,63 +17,13 @@
 #include <vector>
 
 #include "pmf_internal.h"
+#include "pmf_ctx_impl.h"
 
 using namespace pmf;
 
 namespace {
-
 thread_local std::string g_create_error = "";
-
-struct Pending {
-    bool predict = false;
-    double dt = 0.0;
-    int steps = 0;
-    bool regrid = false;
-    double k_sigma = 0.0;
-};
-
 }  // namespace
-
-struct pmf_ctx {
-    pmf_config cfg{};
-    Dims d{};
-    int dtype = 0;
-    int path = PMF_PATH_PENCIL;
-    size_t esize = 8;
-    double A[16]{}, Q[16]{};
-    cudaStream_t stream = nullptr;
-    // device buffers
-    void* W = nullptr;
-    void* W2 = nullptr;
-    void* S = nullptr;
-    FilterState* st = nullptr;
-    double* partials = nullptr;
-    size_t partials_bytes = 0;
-    double* coef = nullptr;
-    size_t coef_bytes = 0;
-    SubstepEntry* sub = nullptr;
-    size_t sub_bytes = 0;
-    double* z = nullptr;
-    double* gauss = nullptr;
-    double* mom_dev = nullptr;       // compact moments [batch][nx + nx^2 + 2]
-    double* mom_host = nullptr;      // pinned host mirror
-    void* tw[4] = {nullptr, nullptr, nullptr, nullptr};
-    int64_t bytes = 0;
-    // host-side model cache (per (dt, steps))
-    double cached_dt = -1.0;
-    int cached_steps = -1;
-    ModelParams mp{};
-    // state machine
-    bool have_density = false;
-    bool have_update = false;
-    Pending pend;
-    int64_t launches = 0;
-    // kernel timing (pmf_profile): event pairs around the dominant kernel of each flush
-    bool prof = false;
-    std::vector<cudaEvent_t> evs;
-    int nev = 0;
-    std::string err;
-};
 
 // ============================================================================ helpers
 static int fail(pmf_ctx* c, int code, const std::string& msg) {
@@ -331,6 +281,7 @@ static int upload_z(pmf_ctx* c, const double* z, int on_device, int nz) {
 
 // Execute pending regrid/predict, optionally fused with an update.
 static int flush(pmf_ctx* c, const LikParams* lp) {
+    if (c->sh) return sh_flush(c, lp);
     PencilBufs b = bufs(c);
     cudaError_t e = cudaSuccess;
     // the resident kernel keeps 3 coefficients per substep in shared memory
@@ -376,19 +327,8 @@ static void make_twiddles(int N, std::vector<T>& out) {
     }
 }
 
-// ============================================================================ ABI
-extern "C" {
-
-const char* pmf_version(void) { return "pmf-b200 0.1 (sm_100a)"; }
-
-const char* pmf_last_error(const pmf_ctx* ctx) {
-    if (!ctx) return g_create_error.c_str();
-    return ctx->err.c_str();
-}
-
-int pmf_create(const pmf_config* cfg, const double* A, const double* Q, pmf_ctx** out) {
-    if (!cfg || !A || !Q || !out) return fail(nullptr, PMF_E_ARG, "null argument");
-    *out = nullptr;
+// argument validation shared by pmf_create and pmf_create_sharded (no device access)
+int pmf_validate_model(const pmf_config* cfg, const double* A, const double* Q, double* Qs) {
     const int nx = cfg->nx;
     if (nx < 1 || nx > PMF_MAX_NX) return fail(nullptr, PMF_E_ARG, "nx must be 1..4");
     if (cfg->batch < 1) return fail(nullptr, PMF_E_ARG, "batch must be >= 1");
@@ -399,7 +339,6 @@ int pmf_create(const pmf_config* cfg, const double* A, const double* Q, pmf_ctx*
         if (cfg->n[m] % 2) return fail(nullptr, PMF_E_ODD_N, "points per axis must be even (P:219)");
         if (!radix_ok(cfg->n[m])) return fail(nullptr, PMF_E_RADIX, "N must be 2^a 3^b in [4, 1024]");
     }
-    double Qs[16];
     unpack(nx, Q, Qs);
     for (int i = 0; i < nx; ++i) {
         for (int j = 0; j < nx; ++j) {
@@ -422,6 +361,42 @@ int pmf_create(const pmf_config* cfg, const double* A, const double* Q, pmf_ctx*
             for (int j = 0; j < nx; ++j)
                 if (i != j && Qs[i * 4 + j] != 0.0)
                     return fail(nullptr, PMF_E_ARG, "AXIS_LITERAL needs a diagonal Q (Alg. 3 uses Q^(m,m))");
+
+    return PMF_OK;
+}
+
+// ---------------------------------------------------------------- shared helpers (pmf_ctx_impl.h)
+int pmf_fail(pmf_ctx* c, int code, const std::string& msg) { return fail(c, code, msg); }
+int pmf_cuda_fail(pmf_ctx* c, cudaError_t e, const char* where) { return cuda_fail(c, e, where); }
+int pmf_dalloc(pmf_ctx* c, void** p, size_t bytes) { return dalloc(c, p, bytes); }
+int pmf_prepare_model(pmf_ctx* c, double dt, int steps) { return prepare_model(c, dt, steps); }
+int pmf_make_lik(pmf_ctx* c, const pmf_likelihood* lik, LikParams& lp) { return make_lik(c, lik, lp); }
+double pmf_det_inv(int n, const double* A, double* Ai) { return det_inv(n, A, Ai); }
+void pmf_unpack(int n, const double* src, double* dst) { unpack(n, src, dst); }
+template <typename T>
+void pmf_make_twiddles(int N, std::vector<T>& out) { make_twiddles<T>(N, out); }
+template void pmf_make_twiddles<double>(int, std::vector<double>&);
+template void pmf_make_twiddles<float>(int, std::vector<float>&);
+
+// ============================================================================ ABI
+extern "C" {
+
+const char* pmf_version(void) { return "pmf-b200 0.1 (sm_100a)"; }
+
+const char* pmf_last_error(const pmf_ctx* ctx) {
+    if (!ctx) return g_create_error.c_str();
+    return ctx->err.c_str();
+}
+
+int pmf_create(const pmf_config* cfg, const double* A, const double* Q, pmf_ctx** out) {
+    if (!cfg || !A || !Q || !out) return fail(nullptr, PMF_E_ARG, "null argument");
+    *out = nullptr;
+    const int nx = cfg->nx;
+    double Qs[16];
+    {
+        int rv = pmf_validate_model(cfg, A, Q, Qs);
+        if (rv) return rv;
+    }
 
     int ndev = 0;
     cudaError_t e = cudaGetDeviceCount(&ndev);
@@ -451,6 +426,12 @@ int pmf_create(const pmf_config* cfg, const double* A, const double* Q, pmf_ctx*
     d.H0 = d.n[0] / 2 + 1;
     d.nspec = d.ntot / d.n[0] * d.H0;
     d.batch = cfg->batch;
+    for (int m = 0; m < 4; ++m) {
+        d.ng[m] = d.n[m];
+        d.lo[m] = 0;
+    }
+    d.src_lo = 0;
+    d.src_n = d.n[nx - 1];
 
     bool res_ok = resident_supported(d, c->dtype);
     if (cfg->path == PMF_PATH_RESIDENT && !res_ok) {
@@ -509,6 +490,7 @@ int pmf_create(const pmf_config* cfg, const double* A, const double* Q, pmf_ctx*
 
 void pmf_destroy(pmf_ctx* c) {
     if (!c) return;
+    if (c->sh) sh_destroy(c);
     cudaSetDevice(c->cfg.device);
     cudaStreamSynchronize(c->stream);
     void* ptrs[] = {c->W, c->W2, c->S, c->st, c->partials, c->coef, c->sub, c->z, c->gauss, c->mom_dev,
@@ -523,6 +505,7 @@ void pmf_destroy(pmf_ctx* c) {
 int pmf_set_gaussian(pmf_ctx* c, const double* mean, const double* cov, double k_sigma) {
     if (!c || !mean || !cov) return fail(c, PMF_E_ARG, "null argument");
     if (!(k_sigma > 0.0)) return fail(c, PMF_E_ARG, "k_sigma must be > 0");
+    if (c->sh) return sh_set_gaussian(c, mean, cov, k_sigma);
     CK(c, cudaSetDevice(c->cfg.device), "cudaSetDevice");
     const Dims& d = c->d;
     const int nx = d.nx;
@@ -560,6 +543,7 @@ int pmf_set_gaussian(pmf_ctx* c, const double* mean, const double* cov, double k
 
 int pmf_set_state(pmf_ctx* c, const double* center, const double* B, const void* weights, int on_device) {
     if (!c || !center || !B || !weights) return fail(c, PMF_E_ARG, "null argument");
+    if (c->sh) return sh_set_state(c, center, B, weights, on_device);
     CK(c, cudaSetDevice(c->cfg.device), "cudaSetDevice");
     const Dims& d = c->d;
     const int nx = d.nx;
@@ -681,6 +665,7 @@ int pmf_get_weights(pmf_ctx* c, void* dst, int dst_on_device) {
     CK(c, cudaSetDevice(c->cfg.device), "cudaSetDevice");
     int r = flush(c, nullptr);
     if (r) return r;
+    if (c->sh) return sh_get_weights(c, dst, dst_on_device);
     const Dims& d = c->d;
     size_t bytes = c->esize * (size_t)d.ntot * d.batch;
     PencilBufs b = bufs(c);

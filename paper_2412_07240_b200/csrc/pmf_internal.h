@@ -52,11 +52,14 @@ struct LikParams {
 
 struct Dims {
     int nx;
-    int n[4];
+    int n[4];               // sizes of the block this context/shard holds (axis 0 first)
     int H0;                 // N_0/2 + 1 (half spectrum along axis 0)
-    long long ntot;         // real points per filter
-    long long nspec;        // complex half-spectrum points per filter
+    long long ntot;         // real points per filter in the block
+    long long nspec;        // complex half-spectrum points per filter in the block
     int batch;
+    int ng[4];              // global grid sizes (== n unless sharded along the last axis)
+    int lo[4];              // global index of the block's first point per axis
+    int src_lo, src_n;      // regrid source window along the last axis (global start, planes)
 };
 
 // Number of doubles per filter in the pencil path's epoch-coefficient buffer.
@@ -99,6 +102,23 @@ cudaError_t launch_scale_out(const Dims& d, int dtype, const PencilBufs& b, void
 
 cudaError_t launch_pack_moments(const Dims& d, const FilterState* st, double* out, cudaStream_t s,
                                 int64_t* launches);
+
+// sharded building blocks (slab decomposition along the last axis; pmf_sharded.cpp)
+enum { SH_PH_FWD = 1, SH_PH_PSI = 2, SH_PH_INV = 4 };
+cudaError_t sh_prep(const Dims& d, PencilBufs& b, const ModelParams& mp, const LikParams* lp, cudaStream_t s,
+                    int64_t* launches);
+cudaError_t sh_phase(const Dims& d, int dtype, PencilBufs& b, const Twiddles& tw, const ModelParams& mp,
+                     const LikParams* lp, int phase, void* psibuf, long long psiI, long long ioff, double* tot,
+                     cudaStream_t s, int64_t* launches);
+cudaError_t sh_pack(int dtype, void* S, void* send, long long I, int planes, const long long* d_off, int world,
+                    int unpack, cudaStream_t s, int64_t* launches);
+cudaError_t sh_points(const Dims& d, int dtype, PencilBufs& b, int mode, const LikParams& lp, double* tot,
+                      cudaStream_t s, int64_t* launches);
+cudaError_t sh_regrid(const Dims& d, int dtype, const void* src, void* dst, PencilBufs& b, double ks, double* tot,
+                      cudaStream_t s, int64_t* launches);
+cudaError_t launch_finalize_tot(const Dims& d, FilterState* st, const double* tot, int mode, double ks,
+                                cudaStream_t s, int64_t* launches);
+cudaError_t launch_sum_ranks(const double* in, double* out, int world, int n, cudaStream_t s, int64_t* launches);
 
 // resident (one CTA per filter) fused epoch kernel
 bool resident_supported(const Dims& d, int dtype);

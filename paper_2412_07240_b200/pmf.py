@@ -29,7 +29,8 @@ LIK_LINEAR_GAUSS, LIK_RANGE_GAUSS = 0, 1
 # every symbol include/pmf.h declares (checked by tests/test_abi.py)
 SYMBOLS = ["pmf_create", "pmf_destroy", "pmf_last_error", "pmf_set_gaussian", "pmf_set_state",
            "pmf_predict", "pmf_update", "pmf_moments", "pmf_regrid", "pmf_step", "pmf_get_weights",
-           "pmf_get_grid", "pmf_sync", "pmf_launch_count", "pmf_moments_bytes", "pmf_profile", "pmf_profile_read", "pmf_device_bytes", "pmf_path", "pmf_version"]
+           "pmf_get_grid", "pmf_sync", "pmf_launch_count", "pmf_moments_bytes", "pmf_nccl_unique_id",
+           "pmf_create_sharded", "pmf_world", "pmf_profile", "pmf_profile_read", "pmf_device_bytes", "pmf_path", "pmf_version"]
 
 
 class PMFError(RuntimeError):
@@ -78,6 +79,9 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         "pmf_sync": (I, [P]),
         "pmf_launch_count": (C.c_int64, [P]),
         "pmf_moments_bytes": (C.c_int64, [P]),
+        "pmf_nccl_unique_id": (I, [V]),
+        "pmf_create_sharded": (I, [C.POINTER(pmf_config), D, D, I, I, V, C.POINTER(P)]),
+        "pmf_world": (I, [P]),
         "pmf_profile": (I, [P, I]),
         "pmf_profile_read": (I, [P, C.POINTER(C.c_double), C.POINTER(C.c_int64)]),
         "pmf_device_bytes": (C.c_int64, [P]),
@@ -90,6 +94,16 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         fn.argtypes = args
     _lib = lib
     return lib
+
+
+def nccl_unique_id() -> bytes:
+    """128-byte NCCL id for pmf_create_sharded (create on rank 0, broadcast to the others)."""
+    lib = load_library()
+    buf = C.create_string_buffer(128)
+    rc = lib.pmf_nccl_unique_id(buf)
+    if rc != PMF_OK:
+        raise PMFError(rc, lib.pmf_last_error(None).decode())
+    return buf.raw
 
 
 def _dptr(a: np.ndarray):
@@ -118,7 +132,11 @@ class Filter:
 
     def __init__(self, nx: int, n, A, Q, batch: int = 1, dtype: str = "f64", diff_mode: int = DIFF_FULL,
                  trace_sign: int = TRACE_PHYSICAL, path: int = PATH_AUTO, device: int = 0,
-                 stream: Optional[int] = None):
+                 stream: Optional[int] = None, world: int = 1, rank: int = 0,
+                 unique_id: Optional[bytes] = None, sharded: bool = False):
+        """world > 1 (or sharded=True): one filter split into `world` slabs along the last
+        axis -- with `unique_id` (from nccl_unique_id(), broadcast to all ranks) this
+        process is `rank` over NCCL; without it all slabs are "virtual ranks" here."""
         self.lib = load_library()
         self.nx, self.n, self.batch = nx, tuple(int(v) for v in n), batch
         self.dtype = dtype
@@ -144,7 +162,12 @@ class Filter:
         A = np.ascontiguousarray(np.asarray(A, dtype=np.float64).reshape(nx, nx))
         Q = np.ascontiguousarray(np.asarray(Q, dtype=np.float64).reshape(nx, nx))
         h = C.c_void_p()
-        rc = self.lib.pmf_create(C.byref(cfg), _dptr(A), _dptr(Q), C.byref(h))
+        if world > 1 or sharded:
+            uid = C.create_string_buffer(bytes(unique_id), 128) if unique_id is not None else None
+            rc = self.lib.pmf_create_sharded(C.byref(cfg), _dptr(A), _dptr(Q), int(rank), int(world),
+                                             uid, C.byref(h))
+        else:
+            rc = self.lib.pmf_create(C.byref(cfg), _dptr(A), _dptr(Q), C.byref(h))
         if rc != PMF_OK:
             raise PMFError(rc, self.lib.pmf_last_error(None).decode())
         self.h = h
@@ -233,6 +256,10 @@ class Filter:
 
     def sync(self):
         self._check(self.lib.pmf_sync(self.h))
+
+    @property
+    def world(self) -> int:
+        return int(self.lib.pmf_world(self.h))
 
     @property
     def launches(self) -> int:

@@ -27,9 +27,9 @@ def make_filter(cfg, dtype="f64", path=pmf.PATH_AUTO, **kw):
     return f
 
 
-def run_gpu(cfg, zs, T, dtype="f64", path=pmf.PATH_AUTO, use_step=False, keep_weights=True):
+def run_gpu(cfg, zs, T, dtype="f64", path=pmf.PATH_AUTO, use_step=False, keep_weights=True, **kw):
     """Epoch loop of R15 through the C ABI; records what the oracle's run_filter records."""
-    f = make_filter(cfg, dtype, path)
+    f = make_filter(cfg, dtype, path, **kw)
     lik = lik_of(cfg)
     dt = cfg.tau / cfg.l
     rec = {"mean": [], "cov": [], "logC": [], "c": [], "B": [], "w": []}
