@@ -187,6 +187,8 @@ def main():
     ap.add_argument("--l", type=int, default=None, help="override Euler substeps")
     ap.add_argument("--path", type=int, default=0, help="0 auto, 1 pencil, 2 resident")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--virtual-ranks", type=int, default=1,
+                    help="split one filter into this many slabs on one GPU (exercises the sharded path)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--ref-budget", type=float, default=8.0)
@@ -207,15 +209,26 @@ def main():
     cfg = make_config(wl["cid"], **wl["over"])
     if args.l:
         cfg = cfg.replace(l=args.l)
-    # weak scaling: rank r runs its own batch of filters (distinct seeds)
     from paper_2412_07240_b200.dist import max_over_ranks, rank_seed
-    cfg = make_config(wl["cid"], **{**wl["over"], "seed": rank_seed(cfg.seed, rank), "l": cfg.l})
+    # One large filter (batch 1, C2-C4) with N > 1 GPUs (or --virtual-ranks): its grid is
+    # split into slabs along the last axis (strong scaling, all-to-all transposes).
+    # Batched filters (C5): every rank runs its own batch (weak scaling, no collective).
+    sharded = cfg.batch == 1 and cfg.nx >= 2 and (world > 1 or args.virtual_ranks > 1)
+    if not sharded:
+        cfg = make_config(wl["cid"], **{**wl["over"], "seed": rank_seed(cfg.seed, rank), "l": cfg.l})
     dtype = cfg.dtype
     T = args.warmup + args.steps + 1
     zs = simulate(cfg, T=T)["z"]                       # (T+1, batch, nz)
     stream = torch.cuda.Stream()
+    fkw = {}
+    if sharded and world > 1:
+        obj = [pmf.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        fkw = dict(world=world, rank=rank, unique_id=obj[0])
+    elif sharded:
+        fkw = dict(world=args.virtual_ranks, sharded=True)
     f = pmf.Filter(cfg.nx, cfg.n, cfg.A, cfg.Q, batch=cfg.batch, dtype=dtype, path=args.path,
-                   device=local, stream=stream.cuda_stream)
+                   device=local, stream=stream.cuda_stream, **fkw)
     lik = (pmf.make_likelihood(pmf.LIK_RANGE_GAUSS, cfg.nx, sigma=cfg.sigma) if cfg.lik_kind == 1
            else pmf.make_likelihood(pmf.LIK_LINEAR_GAUSS, cfg.nx, H=cfg.H, R=cfg.R))
     f.set_gaussian(cfg.prior_mean, np.broadcast_to(cfg.prior_cov, (cfg.batch, cfg.nx, cfg.nx)), cfg.k_sigma)
@@ -249,7 +262,8 @@ def main():
     torch.cuda.synchronize()
     t_max = max_over_ranks(t_ms, device=f"cuda:{local}")
     points_step = cfg.batch * cfg.points
-    value = world * points_step * args.steps / (t_max * 1e-3)
+    ranks_work = 1 if sharded else world             # strong (sharded) vs weak scaling
+    value = ranks_work * points_step * args.steps / (t_max * 1e-3)
     ms_step = t_max / args.steps
 
     # ---------------------------------------------------------------- e2e: host buffers through the C ABI
@@ -258,8 +272,12 @@ def main():
         Te = min(args.steps, 10)
         zs_e = simulate(cfg, T=Te + 1)["z"]
         z_pin = torch.tensor(zs_e, dtype=torch.float64).pin_memory()
+        if sharded and world > 1:
+            obj = [pmf.nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            fkw = dict(world=world, rank=rank, unique_id=obj[0])
         fe = pmf.Filter(cfg.nx, cfg.n, cfg.A, cfg.Q, batch=cfg.batch, dtype=dtype, path=args.path,
-                        device=local, stream=stream.cuda_stream)
+                        device=local, stream=stream.cuda_stream, **fkw)
         fe.set_gaussian(cfg.prior_mean, np.broadcast_to(cfg.prior_cov, (cfg.batch, cfg.nx, cfg.nx)), cfg.k_sigma)
         mean = np.empty((cfg.batch, cfg.nx))
         cov = np.empty((cfg.batch, cfg.nx, cfg.nx))
@@ -282,7 +300,7 @@ def main():
         e1.record(stream)
         e1.synchronize()
         te = max_over_ranks(e0.elapsed_time(e1), device=f"cuda:{local}")
-        e2e = {"value": world * points_step * Te / (te * 1e-3), "unit": "grid-point updates/s",
+        e2e = {"value": ranks_work * points_step * Te / (te * 1e-3), "unit": "grid-point updates/s",
                "h2d_bytes_per_step": cfg.batch * cfg.nz * 8,
                "d2h_bytes_per_step": fe.moments_bytes, "steps": Te}
         fe.close()
@@ -314,14 +332,17 @@ def main():
 
     line = {"metric": "grid-point FPE updates/sec (fp64)" if dtype == "f64" else "grid-point FPE updates/sec (fp32)",
             "value": value, "unit": "grid-point updates/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "strong" if sharded else "weak",
             "vs_baseline": None, "dtype": dtype, "data": "synthetic",
             "config": {"workload": f"{args.workload}: {cfg.batch} x {'x'.join(map(str, cfg.n))} {cfg.nx}-D CV filters "
                                    f"per GPU, l={cfg.l}, tau={cfg.tau}, k_sigma={cfg.k_sigma}",
                        "step": "regrid + predict (Alg. 1-6) + update + moments, every filter",
                        "l2": f"inputs larger than L2 ({alg_bytes / 2 / 1e6:.0f} MB of weights per GPU)",
                        "path": "resident" if f.path == pmf.PATH_RESIDENT else "pencil",
-                       "parallelism": f"filter-sharded x{world} (no data-path collective)"},
+                       "parallelism": (f"slab-sharded x{world if world > 1 else args.virtual_ranks} along the last "
+                                       "axis (2 all-to-all per predict, all-reduce per update)" if sharded
+                                       else f"filter-sharded x{world} (no data-path collective)")},
             "e2e": e2e, "gpu_launches": launches, "roofline": roof, "cpu_baseline": cpu, "clocks": clk}
     if rank == 0:
         print(json.dumps(line), flush=True)

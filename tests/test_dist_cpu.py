@@ -23,8 +23,11 @@ def _worker(rank, world, port, q):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     r, w, lr = D.env()
     t = D.max_over_ranks(1.5 + rank)          # per-rank "time"
+    # the sharded filter's NCCL id travels from rank 0 exactly as bench.py sends it
+    obj = [bytes(range(128)) if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
     dist.barrier()
-    q.put((r, w, lr, t, D.rank_seed(5, r), D.shard(4096, r, w)))
+    q.put((r, w, lr, t, D.rank_seed(5, r), D.shard(4096, r, w), obj[0]))
     dist.destroy_process_group()
 
 
@@ -43,6 +46,32 @@ def test_gloo_world2_max_over_ranks_and_sharding():
     assert all(o[3] == 2.5 for o in out)                 # max over ranks, seen by every rank
     assert out[0][4] != out[1][4]                         # distinct per-rank seeds (weak scaling)
     assert out[0][5] == (0, 2048) and out[1][5] == (2048, 4096)
+    assert out[0][6] == out[1][6] == bytes(range(128))      # id broadcast for pmf_create_sharded
+
+
+def test_create_sharded_validates_before_touching_a_gpu():
+    """pmf_create_sharded argument checks run on the host (CPU box): slab divisibility,
+    batch, nx; a real (non-virtual) create without a device fails loudly."""
+    import ctypes as C
+    import numpy as np
+    from paper_2412_07240_b200 import pmf
+    lib = pmf.load_library()
+    cfg = pmf.pmf_config()
+    cfg.nx, cfg.batch = 4, 1
+    for i, v in enumerate((8, 6, 12, 8)):
+        cfg.n[i] = v
+    A = np.zeros(16)
+    Q = np.eye(4).reshape(-1)
+    h = C.c_void_p()
+    uid = C.create_string_buffer(128)
+    rc = lib.pmf_create_sharded(C.byref(cfg), pmf._dptr(A), pmf._dptr(Q), 0, 3, uid, C.byref(h))
+    assert rc == -1                                   # 8 planes cannot split into 3 slabs
+    cfg.batch = 2
+    rc = lib.pmf_create_sharded(C.byref(cfg), pmf._dptr(A), pmf._dptr(Q), 0, 2, uid, C.byref(h))
+    assert rc == -1                                   # one filter per sharded context
+    cfg.batch = 1
+    rc = lib.pmf_create_sharded(C.byref(cfg), pmf._dptr(A), pmf._dptr(Q), 5, 2, uid, C.byref(h))
+    assert rc == -1                                   # rank out of range
 
 
 @pytest.mark.parametrize("batch,world", [(4096, 8), (7, 3), (1, 2)])
