@@ -73,6 +73,7 @@ int pmf_prepare_model(pmf_ctx* c, double dt, int steps);
 int pmf_make_lik(pmf_ctx* c, const pmf_likelihood* lik, pmf::LikParams& lp);
 double pmf_det_inv(int n, const double* A, double* Ai);
 void pmf_unpack(int n, const double* src, double* dst);
+void pmf_profile_events(pmf_ctx* c, cudaEvent_t* e0, cudaEvent_t* e1);   // null when not profiling
 int pmf_validate_model(const pmf_config* cfg, const double* A, const double* Q, double* Qs);
 template <typename T>
 void pmf_make_twiddles(int N, std::vector<T>& out);

@@ -366,6 +366,12 @@ int pmf_validate_model(const pmf_config* cfg, const double* A, const double* Q, 
 }
 
 // ---------------------------------------------------------------- shared helpers (pmf_ctx_impl.h)
+void pmf_profile_events(pmf_ctx* c, cudaEvent_t* e0, cudaEvent_t* e1) {
+    PencilBufs b;
+    attach_events(c, b);
+    *e0 = b.ev0;
+    *e1 = b.ev1;
+}
 int pmf_fail(pmf_ctx* c, int code, const std::string& msg) { return fail(c, code, msg); }
 int pmf_cuda_fail(pmf_ctx* c, cudaError_t e, const char* where) { return cuda_fail(c, e, where); }
 int pmf_dalloc(pmf_ctx* c, void** p, size_t bytes) { return dalloc(c, p, bytes); }

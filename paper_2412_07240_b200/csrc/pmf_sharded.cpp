@@ -121,7 +121,7 @@ struct ShardSet {
 static int exchange(pmf_ctx* c, const std::vector<Xfer>& xs, void* (*sbuf)(Shard&), void* (*rbuf)(Shard&)) {
     ShardSet& S = *c->sh;
     if (S.virt) {
-        for (const Xfer& x : S.virt ? xs : xs) {
+        for (const Xfer& x : xs) {
             char* src = (char*)sbuf(S.sh[x.src]) + x.so;
             char* dst = (char*)rbuf(S.sh[x.dst]) + x.dof;
             if (x.bytes) {
@@ -571,8 +571,12 @@ int sh_flush(pmf_ctx* c, const LikParams* lp) {
         if (r) return r;
     }
     if (c->pend.predict) {
+        cudaEvent_t e0 = nullptr, e1 = nullptr;
+        pmf_profile_events(c, &e0, &e1);          // time the whole sharded predict (+update)
+        if (e0) cudaEventRecord(e0, c->stream);
         int r = sh_predict_all(c, lp);
         if (r) return r;
+        if (e1) cudaEventRecord(e1, c->stream);
     } else if (lp) {
         for (Shard& sd : S.sh) {
             PencilBufs b = shard_bufs(c, sd);
