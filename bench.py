@@ -187,6 +187,7 @@ def main():
     ap.add_argument("--l", type=int, default=None, help="override Euler substeps")
     ap.add_argument("--path", type=int, default=0, help="0 auto, 1 pencil, 2 resident")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-time-update", action="store_true")
     ap.add_argument("--virtual-ranks", type=int, default=1,
                     help="split one filter into this many slabs on one GPU (exercises the sharded path)")
     ap.add_argument("--no-cpu", action="store_true")
@@ -266,6 +267,36 @@ def main():
     value = ranks_work * points_step * args.steps / (t_max * 1e-3)
     ms_step = t_max / args.steps
 
+    # ---------------------------------------------------------------- FPE time update alone (Alg. 1-6)
+    # north_star's "FPE time update at >= 60% of the HBM roofline": predict-only steps
+    # (no likelihood, no regrid) on the same resident state; 16 B/point algorithmic.
+    tu = None
+    if not args.no_time_update:
+        for _ in range(2):
+            f.predict(dt, cfg.l)
+            f.sync()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        f.profile(True)
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        for _ in range(args.steps):
+            f.predict(dt, cfg.l)
+            f.sync()
+        t1.record(stream)
+        t1.synchronize()
+        km_ms, km_n = f.profile_read()
+        f.profile(False)
+        tt = max_over_ranks(t0.elapsed_time(t1), device=f"cuda:{local}") / args.steps
+        hbm_gbs = peaks()[0]
+        esz = 8 if dtype == "f64" else 4
+        pts = (1 if sharded else world) * cfg.batch * cfg.points
+        tu = {"ms_per_step": tt, "value": pts / (tt * 1e-3), "unit": "grid-point updates/s",
+              "kernel_ms": km_ms / max(km_n, 1),
+              "hbm_frac": 2 * esz * cfg.batch * cfg.points / (km_ms / max(km_n, 1) * 1e-3) / 1e9 / hbm_gbs,
+              "what": "predict only (prep + transform/Psi kernel + closed-form normalisation), same filters"}
+
     # ---------------------------------------------------------------- e2e: host buffers through the C ABI
     e2e = None
     if not args.no_e2e:
@@ -343,7 +374,8 @@ def main():
                        "parallelism": (f"slab-sharded x{world if world > 1 else args.virtual_ranks} along the last "
                                        "axis (2 all-to-all per predict, all-reduce per update)" if sharded
                                        else f"filter-sharded x{world} (no data-path collective)")},
-            "e2e": e2e, "gpu_launches": launches, "roofline": roof, "cpu_baseline": cpu, "clocks": clk}
+            "e2e": e2e, "gpu_launches": launches, "roofline": roof, "cpu_baseline": cpu, "clocks": clk,
+            "time_update": tu}
     if rank == 0:
         print(json.dumps(line), flush=True)
         if args.json_out:
