@@ -304,23 +304,25 @@ __device__ __forceinline__ void zero_ring(void* Xr, int tid) {
     }
 }
 
-// Stage filter `filt` (called by all of warp 0): its 128 weight rows into the X
-// region at pitch StagePitch, and its constants into pbuf, completing on `bar`.
+// Stage filter `filt` (called by ALL threads of the CTA): its 128 weight rows into
+// the X region at pitch StagePitch (one bulk copy per thread of the first 128), and its
+// constants into pbuf, completing on `bar`. Thread 0 arrives with the expected byte
+// count; the mbarrier phase cannot complete before that arrival, whatever the order.
 template <typename T>
 __device__ __forceinline__ void stage(const ResArgs<T>& a, int filt, void* Xr, double* pbuf,
-                                      unsigned long long* bar, int lane) {
+                                      unsigned long long* bar, int tid) {
     constexpr unsigned RB = N * sizeof(T);
     const unsigned pbytes = a.pstride * sizeof(double);
-    if (lane == 0) {
+    if (tid < N) {
         fence_proxy_async();
-        mbar_expect_tx(bar, N * RB + pbytes);
+        if (tid == 0) {
+            mbar_expect_tx(bar, N * RB + pbytes);
+            bulk_g2s(pbuf, a.prm + (long long)filt * a.pstride, pbytes, bar);
+        }
+        const char* src = reinterpret_cast<const char*>(a.W + (long long)filt * (N * N));
+        bulk_g2s(reinterpret_cast<char*>(Xr) + (tid + 1) * StagePitch<T>::B + StagePitch<T>::OFF * sizeof(T),
+                 src + tid * RB, RB, bar);
     }
-    __syncwarp();
-    const char* src = reinterpret_cast<const char*>(a.W + (long long)filt * (N * N));
-    for (int r = lane; r < N; r += 32)
-        bulk_g2s(reinterpret_cast<char*>(Xr) + (r + 1) * StagePitch<T>::B + StagePitch<T>::OFF * sizeof(T), src + r * RB,
-                 RB, bar);
-    if (lane == 0) bulk_g2s(pbuf, a.prm + (long long)filt * a.pstride, pbytes, bar);
 }
 
 // ============================================================================ the fused epoch kernel
@@ -354,7 +356,7 @@ __global__ void __launch_bounds__(NT, 1) k_resident_epoch(ResArgs<T> a) {
     if (tid == 0) mbar_init(bar, 1);
     zero_ring<T>(smem_raw, tid);
     __syncthreads();
-    if (warp == 0 && (int)blockIdx.x < a.batch) stage(a, blockIdx.x, smem_raw, pb0, bar, lane);
+    if ((int)blockIdx.x < a.batch) stage(a, blockIdx.x, smem_raw, pb0, bar, tid);
 
     int it = 0;
     for (int filt = blockIdx.x; filt < a.batch; filt += gridDim.x, ++it) {
@@ -373,7 +375,7 @@ __global__ void __launch_bounds__(NT, 1) k_resident_epoch(ResArgs<T> a) {
         }
         if (P[P_SKIP] != 0.0) {                 // failed filter: leave it untouched
             __syncthreads();
-            if (warp == 0 && nxt < a.batch) stage(a, nxt, smem_raw, Pn, bar, lane);
+            if (nxt < a.batch) stage(a, nxt, smem_raw, Pn, bar, tid);
             continue;
         }
         // ---------------------------------------------------------------- P1: (regrid-)load, FFT along axis 1
@@ -669,7 +671,7 @@ __global__ void __launch_bounds__(NT, 1) k_resident_epoch(ResArgs<T> a) {
             }
             __syncthreads();                      // X is consumed
             zero_ring<T>(smem_raw, tid);          // visible to the gather after the end-of-filter barrier
-            if (warp == 0 && nxt < a.batch) stage(a, nxt, smem_raw, Pn, bar, lane);   // overlaps the rest of P3
+            if (nxt < a.batch) stage(a, nxt, smem_raw, Pn, bar, tid);   // overlaps the rest of P3
 #pragma unroll
             for (int s = 1; s < 16; ++s) {
                 V w = tw[s * 8 + t];
