@@ -71,9 +71,12 @@ extern "C" {
 #define PMF_TRACE_PHYSICAL (-1)   /* R5: s = (1 - dt tr A)^l   (eq:easyFPE P:92)                                   */
 #define PMF_TRACE_PRINTED    1    /* Alg. 4 as printed: s = (1 + dt tr A)^l; normalised output identical   */
 
-#define PMF_PATH_AUTO     0  /* resident per-filter kernel when it fits, else the pencil path                    */
+#define PMF_PATH_AUTO     0  /* resident kernel when it fits, else the plane path when it fits, else pencil      */
 #define PMF_PATH_PENCIL   1  /* multi-pass per-axis pencil kernels (any nx <= 4)                                */
 #define PMF_PATH_RESIDENT 2  /* one CTA per filter, whole half-spectrum in shared memory (nx = 2, N0 = N1 = 128)   */
+#define PMF_PATH_PLANE    3  /* (i0,i1)-plane kernels + strided passes with the regrid fused into the forward pass:
+                                nx = 3, 4; N0 = N1 in {32, 64, 96, 128}; N_m in {16, 32, 64, 96, 128} for m >= 2;
+                                substeps <= 64 per predict (longer intervals run on the pencil kernels)       */
 
 #define PMF_LIK_LINEAR_GAUSS 0   /* z = H x + v, v ~ N(0, R), nz <= 4 (eq:meas P:36)                               */
 #define PMF_LIK_RANGE_GAUSS  1   /* z = ||x|| + v, v ~ N(0, sigma^2), nz = 1 (C3)                                   */
@@ -217,7 +220,7 @@ int pmf_profile_read(pmf_ctx* ctx, double* total_ms, int64_t* count);
 /* Bytes of device memory owned by the context. */
 int64_t pmf_device_bytes(const pmf_ctx* ctx);
 
-/* Kernel path the context uses (PMF_PATH_PENCIL or PMF_PATH_RESIDENT). */
+/* Kernel path the context uses (PMF_PATH_PENCIL, PMF_PATH_RESIDENT or PMF_PATH_PLANE). */
 int pmf_path(const pmf_ctx* ctx);
 
 /* Library version string. */

@@ -75,6 +75,9 @@ __device__ inline double mat_inv4(int nx, const double* A, double* Ai) {
     return det;
 }
 
+// packed (a <= b) index 0..9 for nx <= 4 (row stride 4 whatever nx)
+__host__ __device__ __forceinline__ int tri(int a, int b) { return a * 4 - a * (a - 1) / 2 + (b - a); }
+
 __device__ __forceinline__ int pair_index(int nx, int a, int b) {
     // packed order: diagonal 0..nx-1, then (0,1),(0,2),(0,3),(1,2),(1,3),(2,3) restricted to nx
     int idx = nx;
@@ -92,37 +95,40 @@ __device__ __forceinline__ int pair_index(int nx, int a, int b) {
 // with cf_diag = dt/2 D_n,aa and cf_pair = dt D_n,ab (the 2 of the symmetric
 // cross term folded in), D_n = B^-1 E_n B^-T (FULL) or diag(Q_mm/||B_n[:,m]||^2)
 // (AXIS_LITERAL). Writes 10 doubles per substep (packed as pair_index).
+// One substep n (Bi = B^-1 precomputed by the caller; 10 doubles to `o`).
+__device__ inline void substep_coefs(int nx, const double* B, const double* Bi, const ModelParams& mp,
+                                     const SubstepEntry& e, double* o) {
+    double D[16];
+    if (mp.diff_mode == 0) {
+        double T1[16], BiT[16];
+        for (int i = 0; i < 4; ++i)
+            for (int j = 0; j < 4; ++j) BiT[i * 4 + j] = Bi[j * 4 + i];
+        mat_mul4(nx, Bi, e.E, T1);
+        mat_mul4(nx, T1, BiT, D);
+    } else {
+        double Bn[16];
+        mat_mul4(nx, e.P, B, Bn);
+        for (int i = 0; i < 16; ++i) D[i] = 0.0;
+        for (int m = 0; m < nx; ++m) {
+            double len2 = 0.0;
+            for (int r = 0; r < nx; ++r) len2 = fma(Bn[r * 4 + m], Bn[r * 4 + m], len2);
+            D[m * 4 + m] = mp.Q[m * 4 + m] / len2;
+        }
+    }
+    for (int k = 0; k < 10; ++k) o[k] = 0.0;
+    int idx = nx;
+    for (int a = 0; a < nx; ++a) {
+        o[a] = 0.5 * mp.dt * D[a * 4 + a];
+        for (int b = a + 1; b < nx; ++b) o[idx++] = mp.dt * 0.5 * (D[a * 4 + b] + D[b * 4 + a]);
+    }
+}
+
 __device__ inline void epoch_coefs(const double* B, const ModelParams& mp,
                                    const SubstepEntry* sub, double* out) {
     const int nx = mp.nx;
     double Bi[16];
     mat_inv4(nx, B, Bi);
-    for (int s = 0; s < mp.l; ++s) {
-        double D[16];
-        if (mp.diff_mode == 0) {
-            double T1[16], BiT[16];
-            for (int i = 0; i < 4; ++i)
-                for (int j = 0; j < 4; ++j) BiT[i * 4 + j] = Bi[j * 4 + i];
-            mat_mul4(nx, Bi, sub[s].E, T1);
-            mat_mul4(nx, T1, BiT, D);
-        } else {
-            double Bn[16];
-            mat_mul4(nx, sub[s].P, B, Bn);
-            for (int i = 0; i < 16; ++i) D[i] = 0.0;
-            for (int m = 0; m < nx; ++m) {
-                double len2 = 0.0;
-                for (int r = 0; r < nx; ++r) len2 = fma(Bn[r * 4 + m], Bn[r * 4 + m], len2);
-                D[m * 4 + m] = mp.Q[m * 4 + m] / len2;
-            }
-        }
-        double* o = out + 10 * s;
-        for (int k = 0; k < 10; ++k) o[k] = 0.0;
-        int idx = nx;
-        for (int a = 0; a < nx; ++a) {
-            o[a] = 0.5 * mp.dt * D[a * 4 + a];
-            for (int b = a + 1; b < nx; ++b) o[idx++] = mp.dt * 0.5 * (D[a * 4 + b] + D[b * 4 + a]);
-        }
-    }
+    for (int s = 0; s < mp.l; ++s) substep_coefs(nx, B, Bi, mp, sub[s], out + 10 * s);
 }
 
 __device__ __forceinline__ double det4(int nx, const double* B) {

@@ -118,5 +118,60 @@ __device__ __forceinline__ void dft8(V* x) {
     x[7] = csub(a3, b3);
 }
 
+// radix 3 (forward: W3 = e^{-2 pi i/3}), natural order
+template <bool INV, typename V>
+__device__ __forceinline__ void r3(V& a0, V& a1, V& a2) {
+    using T = decltype(a0.x);
+    const T h = T(0.86602540378443864676);     // sin(2 pi/3)
+    const V t1 = cadd(a1, a2);
+    const V t2 = V{fma(T(-0.5), t1.x, a0.x), fma(T(-0.5), t1.y, a0.y)};
+    const V d = csub(a1, a2);
+    const V t3 = mul_mi<INV>(V{h * d.x, h * d.y});
+    a0 = cadd(a0, t1);
+    a1 = cadd(t2, t3);
+    a2 = csub(t2, t3);
+}
+
+// multiply by W12^E (forward e^{-2 pi i E/12}; inverse: conjugate), E in {1,2,3,4,6}
+template <int E, bool INV, typename V>
+__device__ __forceinline__ V w12(V a) {
+    using T = decltype(a.x);
+    if constexpr (E == 3) return mul_mi<INV>(a);
+    else if constexpr (E == 6) return V{-a.x, -a.y};
+    else {
+        constexpr T h = T(0.86602540378443864676);
+        constexpr T c = E == 1 ? h : (E == 2 ? T(0.5) : T(-0.5));
+        constexpr T s = E == 1 ? T(0.5) : h;
+        const T si = INV ? s : -s;
+        return V{fma(a.x, c, -a.y * si), fma(a.x, si, a.y * c)};
+    }
+}
+
+// in-place 12-point DFT (4 x 3 Cooley-Tukey), natural order in and out:
+// r = r1 + 4 r2 -> radix 3 over r2, twiddle W12^{r1 s2}, radix 4 over r1 -> k = s2 + 3 s1
+template <bool INV, typename V>
+__device__ __forceinline__ void dft12(V* x) {
+#pragma unroll
+    for (int r1 = 0; r1 < 4; ++r1) r3<INV>(x[r1], x[r1 + 4], x[r1 + 8]);
+    x[5] = w12<1, INV>(x[5]);
+    x[9] = w12<2, INV>(x[9]);
+    x[6] = w12<2, INV>(x[6]);
+    x[10] = w12<4, INV>(x[10]);
+    x[7] = w12<3, INV>(x[7]);
+    x[11] = w12<6, INV>(x[11]);
+    V y[12];
+#pragma unroll
+    for (int s2 = 0; s2 < 3; ++s2) {
+        V a0 = x[4 * s2], a1 = x[4 * s2 + 1], a2 = x[4 * s2 + 2], a3 = x[4 * s2 + 3];
+        r4<INV>(a0, a1, a2, a3);
+        y[s2] = a0;
+        y[s2 + 3] = a1;
+        y[s2 + 6] = a2;
+        y[s2 + 9] = a3;
+    }
+#pragma unroll
+    for (int i = 0; i < 12; ++i) x[i] = y[i];
+}
+
 }  // namespace reg
 }  // namespace pmf

@@ -125,8 +125,6 @@ __device__ __forceinline__ void acc_mom(double w, const double* u, double* acc) 
 // coordinates: e(u) = q[0] + sum_a q[1+a] u_a + sum_{a<=b} q[5+tri(a,b)] u_a u_b
 __host__ __device__ __forceinline__ int lq_off(int l) { return 4 + 10 * l; }
 
-// packed (a <= b) index 0..9 for nx <= 4
-__host__ __device__ __forceinline__ int tri(int a, int b) { return a * 4 - a * (a - 1) / 2 + (b - a); }
 
 // ============================================================================ prep
 // One thread per filter: Euler-factor coefficients (epoch_coefs), the input

@@ -1,0 +1,1148 @@
+// kernels_plane.cu -- the plane path for large single grids (nx >= 3 with
+// N_0 = N_1 in {32, 64, 96, 128}: BASELINE configs[2] (C3, 128^3) and
+// configs[3] (C4, 96^4)). One prediction interval + measurement update is
+//
+//   prep   per filter: regrid map (R12), grid motion e^{A tau} (eq:gridMov
+//          P:142-148), Euler-factor coefficients of the l substeps (Alg. 3
+//          P:333-336, R3/R4), likelihood quadratic form on the moved grid (R13)
+//   fwd    per (i0, i1)-plane: [multilinear regrid gather of the previous
+//          posterior, R12] -> forward DFT along axes 1 and 0 (Alg. 1, eq:fourtrsf
+//          P:221) in registers + one shared-memory exchange per axis -> the plane's
+//          half spectrum (k1 = 0..N/2) to HBM; the plane's DC (sum of its weights)
+//   mid    per strided axis m >= 2: pencils of the spectrum; the last axis runs
+//          forward DFT x s Psi / N_tot (Alg. 3-4) x inverse DFT (Alg. 5) in
+//          registers; the others forward before / inverse after it
+//   inv    per plane: inverse DFT along axes 0 and 1, likelihood at the moved
+//          points (eq:filt P:46, R13), store, index-space moment partials
+//   fin    per filter: DC and moment sums in a fixed order -> normaliser C
+//          (P:49), closed-form predict normalisation (Alg. 6: sum w' = s DC),
+//          mean and covariance (R14)
+//
+// HBM traffic per interval: (2 + 2 (nx - 2)) passes over the spectrum -- 3 for
+// nx = 3, 5 for nx = 4 -- instead of 2 nx - 1 per-axis passes plus a regrid pass.
+//
+// Register FFT of length N = 8 R1 held by a team of 8 threads (element j = t + 8r
+// in register r of thread t): DFT_R1 over r, twiddle W_N^{ts}, exchange, DFT_8
+// over t for the s values thread t owns (s = t and R1 - t; thread 0: 0 and R1/2),
+// giving X[s + R1 q]. The pairing (s, R1 - s) puts X[k] and X[-k] in the same
+// thread, so Hermitian (un)packing of real data is thread-local.
+#include <algorithm>
+#include <cmath>
+#include <type_traits>
+
+#include "device_common.cuh"
+#include "fft_reg.cuh"
+
+namespace pmf {
+namespace pln {
+
+template <int N>
+struct Cfg {
+    static constexpr int R1 = N / 8;           // stage-1 radix
+    static constexpr int H = N / 2 + 1;        // rows of a plane's half spectrum (k1 = 0..N/2)
+    static constexpr int PITCH = N + 2;        // complex per shared-memory row (= 2 mod 8: conflict-free)
+    static constexpr int TEAMS = N / 2;        // column pairs (P1, P3) = rows (P2)
+    static constexpr int NT = 8 * TEAMS;
+    static constexpr int SP = N + 2;           // real staging pitch (separable regrid)
+    static constexpr int MINB = N >= 96 ? 1 : (N == 64 ? 2 : 4);
+};
+
+constexpr int LCAP = 64;                       // substeps held per pencil (mid pass, Psi)
+constexpr int MID_TEAMS = 32;                  // pencils per CTA in the mid pass
+
+// per-filter coefficient block (doubles), stride >= PL_EU + 10 l (coef_stride)
+enum {
+    PL_M = 0,       // 16: regrid map v = o + M u' (old index coordinates of new point u'), row stride 4
+    PL_O = 16,      // 4
+    PL_FLAG = 20,   // 0: no regrid, 1: row-separable map (M[a][0] = 0, a >= 1), 2: general gather
+    PL_SKIP = 21,   // 1: filter failed (status) or degenerate regrid target: leave untouched
+    PL_SN = 22,     // s / N_tot (trace factor and the transform scales, folded into Psi)
+    PL_VOL = 23,    // |det B_l|
+    PL_CL = 24,     // 4: moved grid centre c_l
+    PL_BL = 28,     // 16: moved grid matrix B_l
+    PL_LQ = 44,     // 16: linear-Gauss exponent e(u) = q0 + q_a u_a + sum_{a<=b} q_ab u_a u_b (tri order)
+    PL_LGN = 60,    // log normalising constant of the likelihood
+    PL_ISG = 61,    // 1 / sigma (range likelihood)
+    PL_ZR = 62,     // range measurement
+    PL_S = 63,      // s
+    PL_EU = 64      // 10 per substep: Euler-factor coefficients (substep_coefs order)
+};
+
+__device__ __forceinline__ int xcol(int k1, int j0) { return j0 ^ ((k1 >> 2) & 1); }
+__device__ __forceinline__ int rslot(int s, int t) { return s * 8 + (t ^ (s & 7)); }
+template <int N>
+__device__ __forceinline__ int cslot(int s, int t, int m) {
+    const int row = 4 * s + ((t >> 1) ^ (s & 3));
+    const int col = (t & 1) ^ ((s >> 2) & 1);
+    return row * Cfg<N>::PITCH + 2 * m + col;
+}
+
+// stage-2 ownership (R1 >= 2)
+template <int R1> __device__ __forceinline__ bool s_on(int t) { return t < R1 / 2; }
+template <int R1> __device__ __forceinline__ int s_a(int t) { return t; }
+template <int R1> __device__ __forceinline__ int s_b(int t) { return t == 0 ? R1 / 2 : R1 - t; }
+
+template <int R1, bool INV, typename V>
+__device__ __forceinline__ void dftR(V* x) {
+    if constexpr (R1 == 16) reg::dft16<INV>(x);
+    else if constexpr (R1 == 12) reg::dft12<INV>(x);
+    else if constexpr (R1 == 8) reg::dft8<INV>(x);
+    else if constexpr (R1 == 4) reg::r4<INV>(x[0], x[1], x[2], x[3]);
+    else if constexpr (R1 == 2) {
+        const V a = x[0];
+        x[0] = cadd(a, x[1]);
+        x[1] = csub(a, x[1]);
+    }
+}
+
+// W_N^{ts} for s < R1, t < 8 at tw[s * 8 + t]
+template <int N, typename V>
+__device__ __forceinline__ void init_tw(V* tw) {
+    using T = decltype(tw[0].x);
+    for (int i = threadIdx.x; i < N; i += blockDim.x) {
+        const int s = i >> 3, t = i & 7;
+        double sn, cs;
+        sincospi(2.0 * (double)(t * s) / (double)N, &sn, &cs);
+        tw[i] = V{(T)cs, (T)(-sn)};
+    }
+}
+
+template <bool INV, typename V>
+__device__ __forceinline__ V twid(V a, V w) {
+    if (INV) w.y = -w.y;
+    return cmul(a, w);
+}
+
+// Team DFT, DIT order: in x[r] = element t + 8r (registers), out pa[q] = X[sa + R1 q],
+// pb[q] = X[sb + R1 q] on the threads with s_on(t). `ex` is the team's exchange area,
+// `slot(s, t)` its conflict-free layout.
+template <int R1, bool INV, typename V, typename SLOT>
+__device__ __forceinline__ void team_dft(V* x, V* pa, V* pb, V* ex, const V* tw, int t, SLOT slot) {
+    dftR<R1, INV>(x);
+#pragma unroll
+    for (int s = 1; s < R1; ++s) x[s] = twid<INV>(x[s], tw[s * 8 + t]);
+    __syncwarp();
+#pragma unroll
+    for (int s = 0; s < R1; ++s) ex[slot(s, t)] = x[s];
+    __syncwarp();
+    if (s_on<R1>(t)) {
+        const int sa = s_a<R1>(t), sb = s_b<R1>(t);
+#pragma unroll
+        for (int tt = 0; tt < 8; ++tt) {
+            pa[tt] = ex[slot(sa, tt)];
+            pb[tt] = ex[slot(sb, tt)];
+        }
+        reg::dft8<INV>(pa);
+        reg::dft8<INV>(pb);
+    }
+    __syncwarp();
+}
+
+// Team DFT, DIF order (the inverse of team_dft's layout): in pa[q] = X[sa + R1 q],
+// pb[q] = X[sb + R1 q] (threads with s_on), out x[r] = element t + 8r.
+template <int R1, bool INV, typename V, typename SLOT>
+__device__ __forceinline__ void team_dft_dif(V* pa, V* pb, V* x, V* ex, const V* tw, int t, SLOT slot) {
+    __syncwarp();
+    if (s_on<R1>(t)) {
+        const int sa = s_a<R1>(t), sb = s_b<R1>(t);
+        reg::dft8<INV>(pa);
+        reg::dft8<INV>(pb);
+#pragma unroll
+        for (int tt = 0; tt < 8; ++tt) {
+            ex[slot(sa, tt)] = pa[tt];
+            ex[slot(sb, tt)] = pb[tt];
+        }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int s = 0; s < R1; ++s) x[s] = ex[slot(s, t)];
+#pragma unroll
+    for (int s = 1; s < R1; ++s) x[s] = twid<INV>(x[s], tw[s * 8 + t]);
+    dftR<R1, INV>(x);
+    __syncwarp();
+}
+
+template <typename T>
+struct PlaneArgs {
+    const T* Wsrc;          // weights read by the forward pass (old grid when regridding)
+    T* W;                   // weights written by the inverse pass
+    typename C2<T>::type* S;
+    const double* coef;
+    int cs;
+    double* dcpart;         // [plane]
+    double* part;           // [plane][6]
+    int nplanes;            // batch * ppf
+    int ppf;                // planes per filter
+    int n2, n3;             // sizes of axes 2, 3 (1 if absent)
+    int l;
+    int range;              // likelihood kind 1
+};
+
+// plane p of its filter -> (j2, j3)
+__device__ __forceinline__ void plane_j(int pl, int n2, int& j2, int& j3) {
+    j3 = pl / n2;
+    j2 = pl - j3 * n2;
+}
+
+// multilinear interpolation (R12) of the old weights Wf (grid sizes n) at old index
+// coordinates v, zero ghost nodes
+template <typename T, int NX>
+__device__ __forceinline__ double gather_point(const T* __restrict__ Wf, const int* n, const double* v) {
+    int i[4];
+    double fr[4];
+    bool lo[4], hi[4];
+    long long base = 0, stride[4];
+    stride[0] = 1;
+#pragma unroll
+    for (int a = 1; a < NX; ++a) stride[a] = stride[a - 1] * n[a - 1];
+#pragma unroll
+    for (int a = 0; a < NX; ++a) {
+        const double fl = floor(v[a]);
+        i[a] = __double2int_rz(fl);
+        fr[a] = v[a] - fl;
+        lo[a] = i[a] >= 0 && i[a] <= n[a] - 1;
+        hi[a] = i[a] >= -1 && i[a] <= n[a] - 2;
+        base += (long long)i[a] * stride[a];
+    }
+    double val = 0.0;
+#pragma unroll
+    for (int c = 0; c < (1 << NX); ++c) {
+        double wt = 1.0;
+        long long off = base;
+        bool ok = true;
+#pragma unroll
+        for (int a = 0; a < NX; ++a) {
+            const bool bit = (c >> a) & 1;
+            wt *= bit ? fr[a] : 1.0 - fr[a];
+            ok = ok && (bit ? hi[a] : lo[a]);
+            if (bit) off += stride[a];
+        }
+        if (ok) val = fma(wt, (double)__ldg(Wf + off), val);
+    }
+    return val;
+}
+
+// ============================================================================ prep (one warp per filter)
+template <int NX>
+__global__ void k_plane_prep(FilterState* st, double* coef, int cs, ModelParams mp,
+                             const SubstepEntry* __restrict__ sub, LikParams lp, const double* __restrict__ z,
+                             double ks, int update, Dims d) {
+    const int b = blockIdx.x, lane = threadIdx.x;
+    FilterState& f = st[b];
+    double* P = coef + (long long)b * cs;
+    double c0[4] = {0, 0, 0, 0}, B0[16];
+    for (int i = 0; i < 16; ++i) B0[i] = f.B[i];
+    for (int a = 0; a < NX; ++a) c0[a] = f.c[a];
+    bool skip = f.status != 0;
+    int flag = 0;
+    if (ks > 0.0) {
+        double cn[4], Bn[16], Bi[16], M[16];
+        if (!regrid_target(NX, d.ng, f, ks, cn, Bn)) skip = true;
+        mat_inv4(NX, B0, Bi);
+        for (int i = 0; i < 16; ++i) M[i] = 0.0;
+        mat_mul4(NX, Bi, Bn, M);
+        bool sep = true;
+        for (int a = 1; a < NX; ++a) sep = sep && M[a * 4] == 0.0;
+        flag = sep ? 1 : 2;
+        if (lane == 0) {
+            for (int i = 0; i < 16; ++i) P[PL_M + i] = M[i];
+            for (int a = 0; a < NX; ++a) {
+                double s = 0.5 * (d.ng[a] - 1);
+                for (int k = 0; k < NX; ++k) s = fma(Bi[a * 4 + k], cn[k] - c0[k], s);
+                P[PL_O + a] = s;
+            }
+        }
+        for (int a = 0; a < NX; ++a) c0[a] = cn[a];
+        for (int i = 0; i < 16; ++i) B0[i] = Bn[i];
+    }
+    __syncwarp();
+    if (lane == 0) {
+        P[PL_FLAG] = flag;
+        P[PL_SKIP] = skip ? 1.0 : 0.0;
+        if (skip) f.status = -6;
+    }
+    if (skip) return;
+    double Bi0[16];
+    mat_inv4(NX, B0, Bi0);
+    for (int n = lane; n < mp.l; n += 32) substep_coefs(NX, B0, Bi0, mp, sub[n], P + PL_EU + 10 * n);
+    if (lane != 0) return;
+    double Bl[16], cl[4];
+    for (int i = 0; i < 16; ++i) Bl[i] = 0.0;
+    mat_mul4(NX, mp.Mtau, B0, Bl);
+    for (int a = 0; a < NX; ++a) {
+        double s = 0.0;
+        for (int k = 0; k < NX; ++k) s = fma(mp.Mtau[a * 4 + k], c0[k], s);
+        cl[a] = s;
+    }
+    double ntot = 1.0;
+    for (int a = 0; a < NX; ++a) ntot *= d.ng[a];
+    P[PL_SN] = mp.s / ntot;
+    P[PL_S] = mp.s;
+    P[PL_VOL] = fabs(det4(NX, Bl));
+    for (int a = 0; a < 4; ++a) P[PL_CL + a] = a < NX ? cl[a] : 0.0;
+    for (int i = 0; i < 16; ++i) P[PL_BL + i] = Bl[i];
+    P[PL_LGN] = lp.lognorm;
+    P[PL_ISG] = lp.inv_sigma;
+    double* q = P + PL_LQ;
+    for (int i = 0; i < 16; ++i) q[i] = 0.0;
+    if (update && lp.kind == 0) {
+        const double* zf = z + (long long)b * lp.nz;
+        double r0[4], G[16], w[4];
+        for (int i = 0; i < lp.nz; ++i) {
+            double hc = 0.0;
+            for (int a = 0; a < NX; ++a) hc = fma(lp.H[i * 4 + a], cl[a], hc);
+            r0[i] = zf[i] - hc;
+            for (int a = 0; a < NX; ++a) {
+                double g = 0.0;
+                for (int k = 0; k < NX; ++k) g = fma(lp.H[i * 4 + k], Bl[k * 4 + a], g);
+                G[i * 4 + a] = g;
+            }
+        }
+        for (int i = 0; i < lp.nz; ++i) {
+            double s = 0.0;
+            for (int j = 0; j < lp.nz; ++j) s = fma(lp.Rinv[i * 4 + j], r0[j], s);
+            w[i] = s;
+        }
+        double qa = 0.0;
+        for (int i = 0; i < lp.nz; ++i) qa = fma(r0[i], w[i], qa);
+        q[0] = qa;
+        for (int a = 0; a < NX; ++a) {
+            double s = 0.0;
+            for (int i = 0; i < lp.nz; ++i) s = fma(G[i * 4 + a], w[i], s);
+            q[1 + a] = -2.0 * s;
+        }
+        for (int a = 0; a < NX; ++a)
+            for (int c = a; c < NX; ++c) {
+                double s = 0.0;
+                for (int i = 0; i < lp.nz; ++i)
+                    for (int j = 0; j < lp.nz; ++j) s = fma(G[i * 4 + a] * lp.Rinv[i * 4 + j], G[j * 4 + c], s);
+                q[5 + tri(a, c)] = (a == c) ? s : 2.0 * s;
+            }
+    } else if (update) {
+        P[PL_ZR] = z[b];
+    }
+    for (int a = 0; a < NX; ++a) f.c[a] = cl[a];
+    for (int i = 0; i < 16; ++i) f.B[i] = Bl[i];
+}
+
+// ============================================================================ forward plane pass
+template <typename T, int N, int NX, bool RG>
+__global__ void __launch_bounds__(Cfg<N>::NT, Cfg<N>::MINB) k_plane_fwd(PlaneArgs<T> a) {
+    using V = typename C2<T>::type;
+    using C = Cfg<N>;
+    constexpr int R1 = C::R1, H = C::H, PITCH = C::PITCH, NT = C::NT, SP = C::SP;
+    constexpr int NC = 1 << (NX - 1);                       // old rows blended per new row
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    V* X = reinterpret_cast<V*>(smem_raw);                    // [H][PITCH]; also the regrid staging area
+    T* stg = reinterpret_cast<T*>(smem_raw);                  // [N][SP] (ghost columns 0 and N+1)
+    V* tw = X + H * PITCH;
+    int* roff = reinterpret_cast<int*>(tw + N);               // [N][NC] old-row offsets
+    double* rwt = reinterpret_cast<double*>(roff + N * NC);   // [N][NC] corner weights
+    double* rv0 = rwt + N * NC;                               // [N] v0 at u0' = 0
+
+    const int tid = threadIdx.x, m = tid >> 3, t = tid & 7;
+    init_tw<N>(tw);
+    const int nsz[4] = {N, N, a.n2, a.n3};
+    const long long ntot = (long long)N * N * a.n2 * a.n3;
+    __syncthreads();
+    for (int p = blockIdx.x; p < a.nplanes; p += gridDim.x) {
+        const int filt = p / a.ppf, pl = p - filt * a.ppf;
+        const double* P = a.coef + (long long)filt * a.cs;
+        if (P[PL_SKIP] != 0.0) continue;                      // uniform
+        int j2, j3;
+        plane_j(pl, a.n2, j2, j3);
+        const double u2 = j2 - 0.5 * (a.n2 - 1), u3 = j3 - 0.5 * (a.n3 - 1);
+        const T* Wf = a.Wsrc + filt * ntot;
+        const int flag = RG ? (int)P[PL_FLAG] : 0;
+        V z[R1];
+        // ------------------------------------------------------------ P1 input: column pair (2m, 2m+1)
+        if (RG && flag == 1) {
+            // row-separable map: every new row blends the same NC old rows (coalesced), then a
+            // linear interpolation along axis 0 (zero ghosts) -- R12 up to rounding order
+            if (tid < N) {
+                const double u1 = tid - 0.5 * (N - 1);
+                const double uu[4] = {0.0, u1, u2, u3};
+                double v0 = P[PL_O];
+#pragma unroll
+                for (int b2 = 1; b2 < NX; ++b2) v0 = fma(P[PL_M + b2], uu[b2], v0);
+                rv0[tid] = v0;
+                int i0[4];
+                double fr[4];
+#pragma unroll
+                for (int a2 = 1; a2 < NX; ++a2) {
+                    double v = P[PL_O + a2];
+#pragma unroll
+                    for (int b2 = 1; b2 < NX; ++b2) v = fma(P[PL_M + a2 * 4 + b2], uu[b2], v);
+                    const double fl = floor(v);
+                    i0[a2] = __double2int_rz(fl);
+                    fr[a2] = v - fl;
+                }
+#pragma unroll
+                for (int c = 0; c < NC; ++c) {
+                    double wt = 1.0;
+                    long long off = 0, stride = N;
+                    bool ok = true;
+#pragma unroll
+                    for (int a2 = 1; a2 < NX; ++a2) {
+                        const int bit = (c >> (a2 - 1)) & 1;
+                        const int ia = i0[a2] + bit;
+                        wt *= bit ? fr[a2] : 1.0 - fr[a2];
+                        ok = ok && ia >= 0 && ia <= nsz[a2] - 1;
+                        off += (long long)ia * stride;
+                        stride *= nsz[a2];
+                    }
+                    rwt[tid * NC + c] = ok ? wt : 0.0;
+                    roff[tid * NC + c] = ok ? (int)off : 0;
+                }
+            }
+            __syncthreads();
+            for (int e = tid; e < N * N; e += NT) {
+                const int row = e / N, i = e - row * N;
+                double v = 0.0;
+#pragma unroll
+                for (int c = 0; c < NC; ++c) v = fma(rwt[row * NC + c], (double)__ldg(Wf + roff[row * NC + c] + i), v);
+                stg[row * SP + i + 1] = (T)v;
+            }
+            for (int e = tid; e < 2 * N; e += NT) stg[(e >> 1) * SP + ((e & 1) ? N + 1 : 0)] = T(0);
+            __syncthreads();
+            const double M00 = P[PL_M];
+#pragma unroll
+            for (int r = 0; r < R1; ++r) {
+                const int j1 = t + 8 * r;
+                T val[2];
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const double v0 = fma(M00, (2 * m + e) - 0.5 * (N - 1), rv0[j1]);
+                    const double fl = floor(v0);
+                    const int fi = __double2int_rz(fl);
+                    const int i = min(max(fi, -1), N);
+                    const double fa = (fi == i) ? v0 - fl : 0.0;
+                    const double lo = (double)stg[j1 * SP + i + 1];
+                    const double hi = (i < N) ? (double)stg[j1 * SP + i + 2] : 0.0;
+                    val[e] = (T)fma(fa, hi - lo, lo);
+                }
+                z[r] = V{val[0], val[1]};
+            }
+        } else if (RG && flag == 2) {
+            // general map: 2^nx-tap gather per point from the old weights (L2)
+            double vb[2][4], st1[4];
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const double uu[4] = {(2 * m + e) - 0.5 * (N - 1), t - 0.5 * (N - 1), u2, u3};
+#pragma unroll
+                for (int a2 = 0; a2 < NX; ++a2) {
+                    double v = P[PL_O + a2];
+#pragma unroll
+                    for (int b2 = 0; b2 < NX; ++b2) v = fma(P[PL_M + a2 * 4 + b2], uu[b2], v);
+                    vb[e][a2] = v;
+                }
+            }
+#pragma unroll
+            for (int a2 = 0; a2 < NX; ++a2) st1[a2] = 8.0 * P[PL_M + a2 * 4 + 1];
+            // each thread stages its own points (no barrier needed), then reads them back
+            V* own = reinterpret_cast<V*>(stg);
+#pragma unroll 1
+            for (int r = 0; r < R1; ++r) {
+                T val[2];
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    double v[4];
+#pragma unroll
+                    for (int a2 = 0; a2 < NX; ++a2) v[a2] = fma((double)r, st1[a2], vb[e][a2]);
+                    val[e] = (T)gather_point<T, NX>(Wf, nsz, v);
+                }
+                own[(t + 8 * r) * (N / 2) + m] = V{val[0], val[1]};
+            }
+#pragma unroll
+            for (int r = 0; r < R1; ++r) z[r] = own[(t + 8 * r) * (N / 2) + m];
+        } else {
+            const T* Wp = Wf + (long long)pl * N * N;
+#pragma unroll
+            for (int r = 0; r < R1; ++r)
+                z[r] = __ldcs(reinterpret_cast<const V*>(Wp + (long long)(t + 8 * r) * N + 2 * m));
+        }
+        __syncthreads();                                      // staging consumed: X is free
+        // ------------------------------------------------------------ P1: axis-1 FFT of the packed pair
+        {
+            V pa[8], pb[8];
+            team_dft<R1, false>(z, pa, pb, X, tw, t, [&](int s, int tt) { return cslot<N>(s, tt, m); });
+            if (s_on<R1>(t)) {
+                const int sa = s_a<R1>(t), sb = s_b<R1>(t);
+                // unpack the two real columns: Wa = (Z(k) + conj Z(-k))/2, Wb = (Z(k) - conj Z(-k))/(2i)
+                auto store_pair = [&](int k1, V zk, V zp) {
+                    X[k1 * PITCH + xcol(k1, 2 * m)] = V{T(0.5) * (zk.x + zp.x), T(0.5) * (zk.y - zp.y)};
+                    X[k1 * PITCH + xcol(k1, 2 * m + 1)] = V{T(0.5) * (zk.y + zp.y), T(0.5) * (zp.x - zk.x)};
+                };
+                if (t == 0) {
+#pragma unroll
+                    for (int q = 0; q <= 4; ++q) store_pair(R1 * q, pa[q], pa[(8 - q) & 7]);
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) store_pair(R1 / 2 + R1 * q, pb[q], pb[7 - q]);
+                } else {
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        store_pair(sa + R1 * q, pa[q], pb[7 - q]);
+                        store_pair(sb + R1 * q, pb[q], pa[7 - q]);
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        // ------------------------------------------------------------ P2: axis-0 FFT of row k1 = m
+        {
+            V x[R1], pa[8], pb[8];
+            V* row = X + m * PITCH;
+            if (m == 0) {
+#pragma unroll
+                for (int r = 0; r < R1; ++r) x[r] = V{X[t + 8 * r].x, X[(N / 2) * PITCH + t + 8 * r].x};
+            } else {
+#pragma unroll
+                for (int r = 0; r < R1; ++r) x[r] = row[xcol(m, t + 8 * r)];
+            }
+            team_dft<R1, false>(x, pa, pb, row, tw, t, [](int s, int tt) { return rslot(s, tt); });
+            if (s_on<R1>(t)) {
+                const int sa = s_a<R1>(t), sb = s_b<R1>(t);
+                if (m == 0) {
+                    // rows 0 and N/2 were packed as one complex row R = A + i B (both real in j0)
+                    auto unpack = [&](int k, V rk, V rm) {
+                        X[k] = V{T(0.5) * (rk.x + rm.x), T(0.5) * (rk.y - rm.y)};
+                        X[(N / 2) * PITCH + k] = V{T(0.5) * (rk.y + rm.y), T(0.5) * (rm.x - rk.x)};
+                    };
+                    if (t == 0) {
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) unpack(R1 * q, pa[q], pa[(8 - q) & 7]);
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) unpack(R1 / 2 + R1 * q, pb[q], pb[7 - q]);
+                    } else {
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) {
+                            unpack(sa + R1 * q, pa[q], pb[7 - q]);
+                            unpack(sb + R1 * q, pb[q], pa[7 - q]);
+                        }
+                    }
+                } else {
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        row[sa + R1 * q] = pa[q];
+                        row[sb + R1 * q] = pb[q];
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        if (tid == 0) a.dcpart[p] = (double)X[0].x;           // sum of the plane's input weights
+        V* Sp = a.S + (long long)p * (H * N);
+        for (int e = tid; e < H * N; e += NT) {
+            const int r = e / N, c = e - r * N;
+            __stcg(Sp + e, X[r * PITCH + c]);
+        }
+        __syncthreads();
+    }
+}
+
+// ============================================================================ strided pass (axes >= 2)
+// Pencils along one axis of the spectrum [o][j][i] (stride I). MODE 0 forward,
+// 1 inverse, 2 forward x s Psi / N_tot x inverse (last axis; Alg. 3-5). Psi per
+// substep n: f_n = gam_n + bet_n kx_L + alp_n kap_L^2, (gam_n, bet_n) per pencil.
+template <typename T>
+struct MidArgs {
+    typename C2<T>::type* S;
+    const double* coef;
+    int cs;
+    long long I, O;          // inner stride (pencils per o) and outer count
+    int ocpf;                // o values per filter (MODE 2: 1)
+    int N0, H1, n2;          // plane sizes and axis-2 size (wavenumber decode)
+    int l;
+};
+
+template <typename T, int NA, int MODE, int NX>
+__global__ void __launch_bounds__(256, 2) k_plane_mid(MidArgs<T> a) {
+    using V = typename C2<T>::type;
+    constexpr int R1 = NA / 8;
+    constexpr int L = NX - 1;                                 // this pass's axis when MODE == 2
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    V* E = reinterpret_cast<V*>(smem_raw);                    // [MID_TEAMS][NA]
+    V* tw = E + MID_TEAMS * NA;                               // [NA]
+    double2* psi = reinterpret_cast<double2*>(tw + NA);       // [MID_TEAMS][LCAP] (gam, bet)
+    const int tid = threadIdx.x, p = tid >> 3, t = tid & 7;
+    init_tw<NA>(tw);
+    __syncthreads();
+    V* ex = E + p * NA;
+    auto slot = [](int s, int tt) { return rslot(s, tt); };
+    const long long tiles = (a.I + MID_TEAMS - 1) / MID_TEAMS;
+    for (long long blk = blockIdx.x; blk < a.O * tiles; blk += gridDim.x) {
+        const long long o = blk / tiles;
+        const long long i = (blk - o * tiles) * MID_TEAMS + p;
+        const bool valid = i < a.I;
+        V* base = a.S + o * (long long)NA * a.I + (valid ? i : 0);
+        V x[R1];
+#pragma unroll
+        for (int r = 0; r < R1; ++r) x[r] = valid ? __ldcs(base + (long long)(t + 8 * r) * a.I) : V{T(0), T(0)};
+        V pa[8], pb[8];
+        team_dft<R1, MODE == 1>(x, pa, pb, ex, tw, t, slot);
+        if (MODE != 2) {
+            if (valid && s_on<R1>(t)) {
+                const int sa = s_a<R1>(t), sb = s_b<R1>(t);
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    __stcg(base + (long long)(sa + R1 * q) * a.I, pa[q]);
+                    __stcg(base + (long long)(sb + R1 * q) * a.I, pb[q]);
+                }
+            }
+            continue;
+        }
+        // ---------------------------------------------------------------- s Psi / N_tot (Alg. 3-4)
+        const long long filt = o / a.ocpf;
+        const double* P = a.coef + filt * a.cs;
+        const double* cf = P + PL_EU;
+        {
+            // wavenumbers of the pencil's other axes: inner i = (j2 *) H1 N0 + k1 N0 + k0
+            double kap[3] = {0, 0, 0}, kx[3] = {0, 0, 0};
+            const long long ii = valid ? i : 0;
+            const int k0 = (int)(ii % a.N0);
+            const long long r1 = ii / a.N0;
+            const int k1 = (int)(r1 % a.H1);
+            const int k2 = (int)(r1 / a.H1);
+            const int N1 = 2 * (a.H1 - 1);
+            {
+                const int ks0 = k0 < a.N0 / 2 ? k0 : k0 - a.N0;
+                kap[0] = 2.0 * PMF_PI * ks0 / a.N0;
+                kx[0] = (2 * k0 == a.N0) ? 0.0 : kap[0];
+                kap[1] = 2.0 * PMF_PI * k1 / N1;                // k1 in [0, N1/2]: the half axis
+                kx[1] = (2 * k1 == N1) ? 0.0 : kap[1];
+                if (L == 3) {
+                    const int ks2 = k2 < a.n2 / 2 ? k2 : k2 - a.n2;
+                    kap[2] = 2.0 * PMF_PI * ks2 / a.n2;
+                    kx[2] = (2 * k2 == a.n2) ? 0.0 : kap[2];
+                }
+            }
+            for (int n = t; n < a.l; n += 8) {
+                const double* c = cf + 10 * n;
+                double g = 1.0, bb = 0.0;
+#pragma unroll
+                for (int a2 = 0; a2 < L; ++a2) {
+                    g = fma(c[a2], kap[a2] * kap[a2], g);
+#pragma unroll
+                    for (int b2 = a2 + 1; b2 < L; ++b2) g = fma(c[pair_index(NX, a2, b2)], kx[a2] * kx[b2], g);
+                    bb = fma(c[pair_index(NX, a2, L)], kx[a2], bb);
+                }
+                psi[p * LCAP + n] = double2{g, bb};
+            }
+        }
+        __syncwarp();
+        if (s_on<R1>(t)) {
+            const double mult = P[PL_SN];
+            auto mul8 = [&](V* v, int s0) {
+                double kk[8], kxl[8], den[8];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const int k = s0 + R1 * q;
+                    const int ks = k < NA / 2 ? k : k - NA;
+                    const double kp = 2.0 * PMF_PI * ks / NA;
+                    kk[q] = kp * kp;
+                    kxl[q] = (2 * k == NA) ? 0.0 : kp;
+                    den[q] = 1.0;
+                }
+                for (int n = 0; n < a.l; ++n) {
+                    const double2 gb = psi[p * LCAP + n];
+                    const double al = cf[10 * n + L];
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) den[q] *= fma(al, kk[q], fma(gb.y, kxl[q], gb.x));
+                }
+                double pre[8];
+                pre[0] = den[0];
+#pragma unroll
+                for (int q = 1; q < 8; ++q) pre[q] = pre[q - 1] * den[q];
+                double ps[8];
+                if (pre[7] < 1e300) {
+                    double inv = mult / pre[7];
+#pragma unroll
+                    for (int q = 7; q > 0; --q) {
+                        ps[q] = inv * pre[q - 1];
+                        inv *= den[q];
+                    }
+                    ps[0] = inv;
+                } else {
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) ps[q] = mult / den[q];
+                }
+#pragma unroll
+                for (int q = 0; q < 8; ++q) v[q] = V{(T)(v[q].x * ps[q]), (T)(v[q].y * ps[q])};
+            };
+            mul8(pa, s_a<R1>(t));
+            mul8(pb, s_b<R1>(t));
+        }
+        team_dft_dif<R1, true>(pa, pb, x, ex, tw, t, slot);
+        if (valid) {
+#pragma unroll
+            for (int r = 0; r < R1; ++r) __stcg(base + (long long)(t + 8 * r) * a.I, x[r]);
+        }
+    }
+}
+
+// ============================================================================ inverse plane pass (+ update)
+template <typename T, int N, int NX, bool UP>
+__global__ void __launch_bounds__(Cfg<N>::NT, Cfg<N>::MINB) k_plane_inv(PlaneArgs<T> a) {
+    using V = typename C2<T>::type;
+    using C = Cfg<N>;
+    constexpr int R1 = C::R1, H = C::H, PITCH = C::PITCH, NT = C::NT, NW = NT / 32;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    V* X = reinterpret_cast<V*>(smem_raw);
+    V* tw = X + H * PITCH;
+    double* red = reinterpret_cast<double*>(tw + N);          // [NW][6]
+    const int tid = threadIdx.x, m = tid >> 3, t = tid & 7, lane = tid & 31, warp = tid >> 5;
+    init_tw<N>(tw);
+    const long long ntot = (long long)N * N * a.n2 * a.n3;
+    __syncthreads();
+    for (int p = blockIdx.x; p < a.nplanes; p += gridDim.x) {
+        const int filt = p / a.ppf, pl = p - filt * a.ppf;
+        const double* P = a.coef + (long long)filt * a.cs;
+        if (P[PL_SKIP] != 0.0) continue;
+        const V* Sp = a.S + (long long)p * (H * N);
+        for (int e = tid; e < H * N; e += NT) {
+            const int r = e / N, c = e - r * N;
+            X[r * PITCH + c] = __ldcs(Sp + e);
+        }
+        __syncthreads();
+        // ------------------------------------------------------------ P2: inverse axis 0 of row k1 = m
+        {
+            V x[R1], pa[8], pb[8];
+            V* row = X + m * PITCH;
+            if (m == 0) {
+                // rows 0 and N/2 are Hermitian in k0: pack R = A + i B, the inverse is a + i b
+#pragma unroll
+                for (int r = 0; r < R1; ++r) {
+                    const V A = X[t + 8 * r], B = X[(N / 2) * PITCH + t + 8 * r];
+                    x[r] = V{A.x - B.y, A.y + B.x};
+                }
+            } else {
+#pragma unroll
+                for (int r = 0; r < R1; ++r) x[r] = row[t + 8 * r];
+            }
+            team_dft<R1, true>(x, pa, pb, row, tw, t, [](int s, int tt) { return rslot(s, tt); });
+            if (s_on<R1>(t)) {
+                const int sa = s_a<R1>(t), sb = s_b<R1>(t);
+                if (m == 0) {
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        X[sa + R1 * q] = V{pa[q].x, T(0)};
+                        X[(N / 2) * PITCH + sa + R1 * q] = V{pa[q].y, T(0)};
+                        X[sb + R1 * q] = V{pb[q].x, T(0)};
+                        X[(N / 2) * PITCH + sb + R1 * q] = V{pb[q].y, T(0)};
+                    }
+                } else {
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        row[xcol(m, sa + R1 * q)] = pa[q];
+                        row[xcol(m, sb + R1 * q)] = pb[q];
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        // ------------------------------------------------------------ P3: inverse axis 1 of the column pair
+        V x[R1];
+        {
+            V pa[8], pb[8];
+            auto ld = [&](int k1, int col) -> V { return X[k1 * PITCH + xcol(k1, 2 * m + col)]; };
+            auto zdir = [&](int k1) -> V {
+                const V wa = ld(k1, 0), wb = ld(k1, 1);
+                return V{wa.x - wb.y, wa.y + wb.x};
+            };
+            auto zmir = [&](int kp) -> V {      // Z(N - kp) = conj Wa(kp) + i conj Wb(kp)
+                const V wa = ld(kp, 0), wb = ld(kp, 1);
+                return V{wa.x + wb.y, wb.x - wa.y};
+            };
+            if (s_on<R1>(t)) {
+                const int sa = s_a<R1>(t), sb = s_b<R1>(t);
+                if (t == 0) {
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) pa[q] = (q <= 4) ? zdir(R1 * q) : zmir(R1 * (8 - q));
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) pb[q] = (q < 4) ? zdir(R1 / 2 + R1 * q) : zmir(R1 / 2 + R1 * (7 - q));
+                } else {
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        pa[q] = (q < 4) ? zdir(sa + R1 * q) : zmir(sb + R1 * (7 - q));
+                        pb[q] = (q < 4) ? zdir(sb + R1 * q) : zmir(sa + R1 * (7 - q));
+                    }
+                }
+            }
+            team_dft_dif<R1, true>(pa, pb, x, X, tw, t, [&](int s, int tt) { return cslot<N>(s, tt, m); });
+        }
+        // x[r] = w(2m, t + 8r) + i w(2m+1, t + 8r), unnormalised
+        int j2, j3;
+        plane_j(pl, a.n2, j2, j3);
+        T* Wp = a.W + filt * ntot + (long long)pl * N * N;
+        if (!UP) {
+#pragma unroll
+            for (int r = 0; r < R1; ++r) *reinterpret_cast<V*>(Wp + (long long)(t + 8 * r) * N + 2 * m) = x[r];
+            __syncthreads();
+            continue;
+        }
+        const double u2 = j2 - 0.5 * (a.n2 - 1), u3 = (NX == 4) ? j3 - 0.5 * (a.n3 - 1) : 0.0;
+        const double u10 = t - 0.5 * (N - 1);
+        const double lgn = P[PL_LGN];
+        double S[2] = {0, 0}, Tm[2] = {0, 0}, U[2] = {0, 0};
+        auto emit = [&](int r, int e, double w) -> T {
+            const T wt = (T)w;
+            const double u1 = fma(8.0, (double)r, u10);
+            const double wd = (double)wt, wu = wd * u1;
+            S[e] += wd;
+            Tm[e] += wu;
+            U[e] = fma(wu, u1, U[e]);
+            return wt;
+        };
+        bool rec = !a.range;
+        double Lr[2], Rr[2], Gr[2];
+        if (!a.range) {
+            // linear Gauss: along a column the exponent is quadratic in r (u1 = u10 + 8 r):
+            // E(r) = E0 + E1 r + E2 r^2, L(r+1) = L(r) R(r), R(r+1) = R(r) exp(2 E2)
+            const double* q = P + PL_LQ;
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const double u0 = (2 * m + e) - 0.5 * (N - 1);
+                const double c2 = q[5 + tri(1, 1)];
+                double c1 = fma(q[5 + tri(0, 1)], u0, q[2]);
+                double c0 = fma(u0, fma(q[5 + tri(0, 0)], u0, q[1]), q[0]);
+                c1 = fma(q[5 + tri(1, 2)], u2, c1);
+                c0 = fma(u2, fma(q[5 + tri(2, 2)], u2, fma(q[5 + tri(0, 2)], u0, q[3])), c0);
+                if (NX == 4) {
+                    c1 = fma(q[5 + tri(1, 3)], u3, c1);
+                    c0 = fma(u3, fma(q[5 + tri(3, 3)], u3,
+                                     fma(q[5 + tri(2, 3)], u2, fma(q[5 + tri(0, 3)], u0, q[4]))), c0);
+                }
+                const double E0 = fma(-0.5, fma(u10, fma(c2, u10, c1), c0), lgn);
+                const double E1 = -0.5 * (8.0 * c1 + 16.0 * c2 * u10);
+                const double E2 = -32.0 * c2;
+                rec = rec && (fabs(E0) + (R1 - 1) * fabs(E1) + (R1 - 1) * (R1 - 1) * fabs(E2) < 650.0);
+                Lr[e] = exp_fast(E0);
+                Rr[e] = exp_fast(E1 + E2);
+                Gr[e] = exp_fast(2.0 * E2);
+            }
+        }
+        if (rec) {
+#pragma unroll
+            for (int r = 0; r < R1; ++r) {
+                const T o0 = emit(r, 0, (double)x[r].x * Lr[0]);
+                const T o1 = emit(r, 1, (double)x[r].y * Lr[1]);
+                Lr[0] *= Rr[0];
+                Rr[0] *= Gr[0];
+                Lr[1] *= Rr[1];
+                Rr[1] *= Gr[1];
+                *reinterpret_cast<V*>(Wp + (long long)(t + 8 * r) * N + 2 * m) = V{o0, o1};
+            }
+        } else {
+            const double* q = P + PL_LQ;
+#pragma unroll
+            for (int r = 0; r < R1; ++r) {
+                const double u1 = fma(8.0, (double)r, u10);
+                const double uu[4] = {0.0, u1, u2, u3};
+                T o[2];
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    double uv[4] = {(2 * m + e) - 0.5 * (N - 1), uu[1], uu[2], uu[3]};
+                    double ll;
+                    if (!a.range) {
+                        double ee = q[0];
+#pragma unroll
+                        for (int a2 = 0; a2 < NX; ++a2) {
+                            ee = fma(q[1 + a2], uv[a2], ee);
+#pragma unroll
+                            for (int b2 = a2; b2 < NX; ++b2) ee = fma(q[5 + tri(a2, b2)] * uv[a2], uv[b2], ee);
+                        }
+                        ll = fma(-0.5, ee, lgn);
+                    } else {
+                        double r2 = 0.0;
+#pragma unroll
+                        for (int a2 = 0; a2 < NX; ++a2) {
+                            double y = P[PL_CL + a2];
+#pragma unroll
+                            for (int b2 = 0; b2 < NX; ++b2) y = fma(P[PL_BL + a2 * 4 + b2], uv[b2], y);
+                            r2 = fma(y, y, r2);
+                        }
+                        const double d = (P[PL_ZR] - sqrt(r2)) * P[PL_ISG];
+                        ll = fma(-0.5 * d, d, lgn);
+                    }
+                    const double w = (double)(e == 0 ? x[r].x : x[r].y);
+                    o[e] = emit(r, e, w * exp_fast(ll));
+                }
+                *reinterpret_cast<V*>(Wp + (long long)(t + 8 * r) * N + 2 * m) = V{o[0], o[1]};
+            }
+        }
+        double acc[6];
+        {
+            const double ua = (2 * m) - 0.5 * (N - 1), ub = ua + 1.0;
+            acc[0] = S[0] + S[1];
+            acc[1] = fma(ua, S[0], ub * S[1]);
+            acc[2] = Tm[0] + Tm[1];
+            acc[3] = fma(ua * ua, S[0], ub * ub * S[1]);
+            acc[4] = fma(ua, Tm[0], ub * Tm[1]);
+            acc[5] = U[0] + U[1];
+        }
+#pragma unroll
+        for (int i = 0; i < 6; ++i) {
+            double v = acc[i];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+            acc[i] = v;
+        }
+        if (lane == 0)
+#pragma unroll
+            for (int i = 0; i < 6; ++i) red[warp * 6 + i] = acc[i];
+        __syncthreads();
+        if (tid < 6) {
+            double v = 0.0;
+            for (int w = 0; w < NW; ++w) v += red[w * 6 + tid];
+            a.part[(long long)p * 6 + tid] = v;
+        }
+        __syncthreads();
+    }
+}
+
+// ============================================================================ finalise (one block per filter)
+template <int NX>
+__global__ void k_plane_fin(FilterState* st, const double* __restrict__ coef, int cs, const double* __restrict__ dcpart,
+                            const double* __restrict__ part, int ppf, int n2, int n3, int update) {
+    __shared__ double red[32 * 16];
+    const int filt = blockIdx.x;
+    const double* P = coef + (long long)filt * cs;
+    if (P[PL_SKIP] != 0.0) return;
+    double acc[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) acc[i] = 0.0;
+    for (int pl = threadIdx.x; pl < ppf; pl += blockDim.x) {
+        const long long p = (long long)filt * ppf + pl;
+        acc[15] += dcpart[p];
+        if (!update) continue;
+        const double* pp = part + p * 6;
+        int j2, j3;
+        plane_j(pl, n2, j2, j3);
+        const double u[4] = {0.0, 0.0, j2 - 0.5 * (n2 - 1), j3 - 0.5 * (n3 - 1)};
+        const double S = pp[0];
+        double m1[4];
+        m1[0] = pp[1];
+        m1[1] = pp[2];
+#pragma unroll
+        for (int a2 = 2; a2 < NX; ++a2) m1[a2] = u[a2] * S;
+        acc[0] += S;
+#pragma unroll
+        for (int a2 = 0; a2 < NX; ++a2) acc[1 + a2] += m1[a2];
+        int k = 1 + NX;
+#pragma unroll
+        for (int a2 = 0; a2 < NX; ++a2)
+#pragma unroll
+            for (int b2 = a2; b2 < NX; ++b2) {
+                double v;
+                if (a2 >= 2) v = u[a2] * u[b2] * S;
+                else if (b2 >= 2) v = u[b2] * m1[a2];
+                else v = (a2 == 0 && b2 == 0) ? pp[3] : (a2 == 0) ? pp[4] : pp[5];
+                acc[k++] += v;
+            }
+    }
+    block_sum<16>(acc, red);
+    if (threadIdx.x != 0) return;
+    FilterState& f = st[filt];
+    const double s = P[PL_S], vol = P[PL_VOL], dc = acc[15];
+    if (!update) {
+        f.scale = 1.0 / (vol * s * dc);
+        return;
+    }
+    // stored weights: unnormalised prior (sum = s DC) times the likelihood
+    const double C = acc[0] / (s * dc);
+    f.mass = acc[0];
+    f.has_moments = 1;
+    if (!(C > 0.0) || !isfinite(C) || !(acc[0] > 0.0)) {
+        f.status = -6;
+        f.logC = -INFINITY;
+        return;
+    }
+    f.status = 0;
+    f.logC = log(C);
+    f.scale = 1.0 / (vol * acc[0]);
+    finish_moments(NX, acc, f.c, f.B, f.mean, f.cov);
+}
+
+}  // namespace pln
+
+using namespace pln;
+
+bool plane_supported(const Dims& d, int l) {
+    if (d.nx < 3 || d.n[0] != d.n[1] || l > LCAP) return false;
+    const int N = d.n[0];
+    if (N != 32 && N != 64 && N != 96 && N != 128) return false;
+    for (int m = 2; m < d.nx; ++m) {
+        const int n = d.n[m];
+        if (n != 16 && n != 32 && n != 64 && n != 96 && n != 128) return false;
+    }
+    return d.nx <= 4;
+}
+
+template <typename K>
+static cudaError_t occ_grid(K kern, int nt, size_t smem, long long work, int* grid) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    int dev = 0, nsm = 148, occ = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, nt, smem);
+    if (e != cudaSuccess) return e;
+    if (occ < 1) return cudaErrorInvalidConfiguration;
+    *grid = (int)std::max(1LL, std::min(work, (long long)nsm * occ));
+    return cudaSuccess;
+}
+
+template <typename T, int NA, int NX>
+static cudaError_t mid_na(MidArgs<T> ma, int mode, cudaStream_t s) {
+    using V = typename C2<T>::type;
+    const size_t smem = sizeof(V) * (MID_TEAMS + 1) * NA + sizeof(double2) * MID_TEAMS * LCAP;
+    const long long work = ma.O * ((ma.I + MID_TEAMS - 1) / MID_TEAMS);
+    int grid = 1;
+    cudaError_t e;
+    if (mode == 0) {
+        e = occ_grid(k_plane_mid<T, NA, 0, NX>, 256, smem, work, &grid);
+        if (e == cudaSuccess) k_plane_mid<T, NA, 0, NX><<<grid, 256, smem, s>>>(ma);
+    } else if (mode == 1) {
+        e = occ_grid(k_plane_mid<T, NA, 1, NX>, 256, smem, work, &grid);
+        if (e == cudaSuccess) k_plane_mid<T, NA, 1, NX><<<grid, 256, smem, s>>>(ma);
+    } else {
+        e = occ_grid(k_plane_mid<T, NA, 2, NX>, 256, smem, work, &grid);
+        if (e == cudaSuccess) k_plane_mid<T, NA, 2, NX><<<grid, 256, smem, s>>>(ma);
+    }
+    if (e != cudaSuccess) return e;
+    return cudaGetLastError();
+}
+
+template <typename T, int NX>
+static cudaError_t mid_pass(MidArgs<T> ma, int na, int mode, cudaStream_t s) {
+    switch (na) {
+        case 16: return mid_na<T, 16, NX>(ma, mode, s);
+        case 32: return mid_na<T, 32, NX>(ma, mode, s);
+        case 64: return mid_na<T, 64, NX>(ma, mode, s);
+        case 96: return mid_na<T, 96, NX>(ma, mode, s);
+        case 128: return mid_na<T, 128, NX>(ma, mode, s);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+template <typename T, int N, int NX>
+static cudaError_t plane_t(const Dims& d, PencilBufs& b, const ModelParams& mp, const LikParams* lp, double ks,
+                           cudaStream_t s, int64_t* launches) {
+    using V = typename C2<T>::type;
+    using Cf = Cfg<N>;
+    const int cs = coef_stride(mp.l);
+    LikParams lpv = lp ? *lp : LikParams{};
+    k_plane_prep<NX><<<d.batch, 32, 0, s>>>(b.st, b.coef, cs, mp, b.sub, lpv, b.z, ks, lp ? 1 : 0, d);
+    ++*launches;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    const int n2 = d.n[2], n3 = NX == 4 ? d.n[3] : 1;
+    const int ppf = n2 * n3;
+    PlaneArgs<T> pa;
+    pa.Wsrc = (const T*)b.W;
+    pa.W = (T*)b.W;
+    pa.S = (V*)b.S;
+    pa.coef = b.coef;
+    pa.cs = cs;
+    pa.ppf = ppf;
+    pa.nplanes = ppf * d.batch;
+    pa.dcpart = b.partials;
+    pa.part = b.partials + pa.nplanes;
+    pa.n2 = n2;
+    pa.n3 = n3;
+    pa.l = mp.l;
+    pa.range = lpv.kind == 1;
+    // forward plane pass
+    {
+        constexpr int NC = 1 << (NX - 1);
+        const size_t smem = sizeof(V) * (Cf::H * Cf::PITCH + N) + (size_t)N * NC * (sizeof(int) + sizeof(double)) +
+                            sizeof(double) * N;
+        int grid = 1;
+        if (ks > 0.0) {
+            e = occ_grid(k_plane_fwd<T, N, NX, true>, Cf::NT, smem, pa.nplanes, &grid);
+            if (e == cudaSuccess) k_plane_fwd<T, N, NX, true><<<grid, Cf::NT, smem, s>>>(pa);
+        } else {
+            e = occ_grid(k_plane_fwd<T, N, NX, false>, Cf::NT, smem, pa.nplanes, &grid);
+            if (e == cudaSuccess) k_plane_fwd<T, N, NX, false><<<grid, Cf::NT, smem, s>>>(pa);
+        }
+        if (e != cudaSuccess) return e;
+        ++*launches;
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    }
+    // strided axes: forward 2..nx-2, last axis with Psi, inverse nx-2..2
+    auto mid = [&](int m, int mode) -> cudaError_t {
+        MidArgs<T> ma;
+        ma.S = (V*)b.S;
+        ma.coef = b.coef;
+        ma.cs = cs;
+        ma.I = (long long)Cf::H * N;
+        for (int q = 2; q < m; ++q) ma.I *= d.n[q];
+        ma.O = d.batch;
+        ma.ocpf = 1;
+        for (int q = m + 1; q < NX; ++q) {
+            ma.O *= d.n[q];
+            ma.ocpf *= d.n[q];
+        }
+        ma.N0 = N;
+        ma.H1 = Cf::H;
+        ma.n2 = n2;
+        ma.l = mp.l;
+        ++*launches;
+        return mid_pass<T, NX>(ma, d.n[m], mode, s);
+    };
+    for (int m = 2; m < NX - 1; ++m)
+        if ((e = mid(m, 0)) != cudaSuccess) return e;
+    if (b.ev0) cudaEventRecord(b.ev0, s);
+    if ((e = mid(NX - 1, 2)) != cudaSuccess) return e;
+    if (b.ev1) cudaEventRecord(b.ev1, s);
+    for (int m = NX - 2; m >= 2; --m)
+        if ((e = mid(m, 1)) != cudaSuccess) return e;
+    // inverse plane pass (+ update)
+    {
+        const size_t smem = sizeof(V) * (Cf::H * Cf::PITCH + N) + sizeof(double) * 6 * (Cf::NT / 32);
+        int grid = 1;
+        if (lp) {
+            e = occ_grid(k_plane_inv<T, N, NX, true>, Cf::NT, smem, pa.nplanes, &grid);
+            if (e == cudaSuccess) k_plane_inv<T, N, NX, true><<<grid, Cf::NT, smem, s>>>(pa);
+        } else {
+            e = occ_grid(k_plane_inv<T, N, NX, false>, Cf::NT, smem, pa.nplanes, &grid);
+            if (e == cudaSuccess) k_plane_inv<T, N, NX, false><<<grid, Cf::NT, smem, s>>>(pa);
+        }
+        if (e != cudaSuccess) return e;
+        ++*launches;
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    }
+    k_plane_fin<NX><<<d.batch, 256, 0, s>>>(b.st, b.coef, cs, pa.dcpart, pa.part, ppf, n2, n3, lp ? 1 : 0);
+    ++*launches;
+    return cudaGetLastError();
+}
+
+template <typename T, int NX>
+static cudaError_t plane_n(const Dims& d, PencilBufs& b, const ModelParams& mp, const LikParams* lp, double ks,
+                           cudaStream_t s, int64_t* launches) {
+    switch (d.n[0]) {
+        case 32: return plane_t<T, 32, NX>(d, b, mp, lp, ks, s, launches);
+        case 64: return plane_t<T, 64, NX>(d, b, mp, lp, ks, s, launches);
+        case 96: return plane_t<T, 96, NX>(d, b, mp, lp, ks, s, launches);
+        case 128: return plane_t<T, 128, NX>(d, b, mp, lp, ks, s, launches);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+cudaError_t launch_plane(const Dims& d, int dtype, PencilBufs& b, const ModelParams& mp, const LikParams* lp,
+                         double ks, cudaStream_t s, int64_t* launches) {
+    if (d.nx == 3) {
+        if (dtype == 0) return plane_n<double, 3>(d, b, mp, lp, ks, s, launches);
+        return plane_n<float, 3>(d, b, mp, lp, ks, s, launches);
+    }
+    if (dtype == 0) return plane_n<double, 4>(d, b, mp, lp, ks, s, launches);
+    return plane_n<float, 4>(d, b, mp, lp, ks, s, launches);
+}
+
+size_t plane_partials_doubles(const Dims& d) {
+    long long ppf = 1;
+    for (int m = 2; m < d.nx; ++m) ppf *= d.n[m];
+    return (size_t)(7 * ppf * d.batch);
+}
+
+}  // namespace pmf

@@ -294,6 +294,15 @@ static int flush(pmf_ctx* c, const LikParams* lp) {
         c->pend = Pending{};
         return PMF_OK;
     }
+    // plane path: regrid (if pending) fused into the forward pass, predict, update
+    if (c->path == PMF_PATH_PLANE && c->pend.predict && plane_supported(c->d, c->pend.steps)) {
+        attach_events(c, b);
+        e = launch_plane(c->d, c->dtype, b, c->mp, lp, c->pend.regrid ? c->pend.k_sigma : -1.0, c->stream,
+                         &c->launches);
+        if (e != cudaSuccess) return cuda_fail(c, e, "plane path");
+        c->pend = Pending{};
+        return PMF_OK;
+    }
     if (c->pend.regrid) {
         e = launch_regrid(c->d, c->dtype, b, c->pend.k_sigma, c->stream, &c->launches);
         if (e != cudaSuccess) return cuda_fail(c, e, "regrid");
@@ -440,17 +449,25 @@ int pmf_create(const pmf_config* cfg, const double* A, const double* Q, pmf_ctx*
     d.src_n = d.n[nx - 1];
 
     bool res_ok = resident_supported(d, c->dtype);
+    bool plane_ok = plane_supported(d, 1);
     if (cfg->path == PMF_PATH_RESIDENT && !res_ok) {
         delete c;
         return fail(nullptr, PMF_E_ARG, "resident path not supported for this grid/dtype");
     }
-    c->path = (cfg->path == PMF_PATH_PENCIL || !res_ok) ? PMF_PATH_PENCIL : PMF_PATH_RESIDENT;
+    if (cfg->path == PMF_PATH_PLANE && !plane_ok) {
+        delete c;
+        return fail(nullptr, PMF_E_ARG, "plane path not supported for this grid");
+    }
+    if (cfg->path == PMF_PATH_PENCIL) c->path = PMF_PATH_PENCIL;
+    else if (cfg->path == PMF_PATH_RESIDENT || (cfg->path == PMF_PATH_AUTO && res_ok)) c->path = PMF_PATH_RESIDENT;
+    else if (cfg->path == PMF_PATH_PLANE || (cfg->path == PMF_PATH_AUTO && plane_ok)) c->path = PMF_PATH_PLANE;
+    else c->path = PMF_PATH_PENCIL;
 
     const size_t wbytes = c->esize * (size_t)d.ntot * d.batch;
     int r = PMF_OK;
     if (!r) r = dalloc(c, &c->W, wbytes);
     if (!r) r = dalloc(c, &c->W2, wbytes);
-    if (!r && c->path == PMF_PATH_PENCIL && nx > 1) r = dalloc(c, &c->S, 2 * c->esize * (size_t)d.nspec * d.batch);
+    if (!r && c->path != PMF_PATH_RESIDENT && nx > 1) r = dalloc(c, &c->S, 2 * c->esize * (size_t)d.nspec * d.batch);
     if (!r) r = dalloc(c, (void**)&c->st, sizeof(FilterState) * d.batch);
     // reduction scratch: the largest per-pass block count (pencil C2R rows / points kernels)
     size_t nblk = (size_t)d.batch * 1024;

@@ -65,7 +65,8 @@ struct Dims {
 // Number of doubles per filter in the pencil path's epoch-coefficient buffer.
 // pencil path: 4 + 10 l + 16 (scale, Euler factors, likelihood quadratic form);
 // resident path: 24 + 3 l rounded up to even (kernels_resident.cu)
-inline int coef_stride(int l) { return (20 + 10 * l) > (26 + 3 * l) ? (20 + 10 * l) : (26 + 3 * l); }
+// plane path: 64 + 10 l (kernels_plane.cu)
+inline int coef_stride(int l) { return 64 + 10 * l; }
 
 // ---------------------------------------------------------------------------
 // launchers (implemented in the .cu files); all return a cudaError_t and
@@ -119,6 +120,12 @@ cudaError_t sh_regrid(const Dims& d, int dtype, const void* src, void* dst, Penc
 cudaError_t launch_finalize_tot(const Dims& d, FilterState* st, const double* tot, int mode, double ks,
                                 cudaStream_t s, int64_t* launches);
 cudaError_t launch_sum_ranks(const double* in, double* out, int world, int n, cudaStream_t s, int64_t* launches);
+
+// plane path (nx >= 3, N_0 = N_1 in {32, 64, 96, 128}): fused regrid + predict + update
+bool plane_supported(const Dims& d, int l);
+size_t plane_partials_doubles(const Dims& d);
+cudaError_t launch_plane(const Dims& d, int dtype, PencilBufs& b, const ModelParams& mp, const LikParams* lp,
+                         double k_sigma /* < 0 = no regrid */, cudaStream_t s, int64_t* launches);
 
 // resident (one CTA per filter) fused epoch kernel
 bool resident_supported(const Dims& d, int dtype);

@@ -23,7 +23,7 @@ ERRORS = {-1: "PMF_E_ARG", -2: "PMF_E_ODD_N", -3: "PMF_E_RADIX", -4: "PMF_E_Q_NO
 F64, F32 = 0, 1
 DIFF_FULL, DIFF_AXIS_LITERAL = 0, 1
 TRACE_PHYSICAL, TRACE_PRINTED = -1, 1
-PATH_AUTO, PATH_PENCIL, PATH_RESIDENT = 0, 1, 2
+PATH_AUTO, PATH_PENCIL, PATH_RESIDENT, PATH_PLANE = 0, 1, 2, 3
 LIK_LINEAR_GAUSS, LIK_RANGE_GAUSS = 0, 1
 
 # every symbol include/pmf.h declares (checked by tests/test_abi.py)
