@@ -28,10 +28,12 @@
 // thread, so Hermitian (un)packing of real data is thread-local.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <type_traits>
 
 #include "device_common.cuh"
 #include "fft_reg.cuh"
+#include "tma.cuh"
 
 namespace pmf {
 namespace pln {
@@ -48,13 +50,12 @@ struct Cfg {
 };
 
 constexpr int LCAP = 64;                       // substeps held per pencil (mid pass, Psi)
-constexpr int MID_TEAMS = 32;                  // pencils per CTA in the mid pass
 
 // per-filter coefficient block (doubles), stride >= PL_EU + 10 l (coef_stride)
 enum {
     PL_M = 0,       // 16: regrid map v = o + M u' (old index coordinates of new point u'), row stride 4
     PL_O = 16,      // 4
-    PL_FLAG = 20,   // 0: no regrid, 1: row-separable map (M[a][0] = 0, a >= 1), 2: general gather
+    PL_FLAG = 20,   // 0: no regrid, 2: general map (gather pre-pass), 4: split map (nx = 4 CV structure)
     PL_SKIP = 21,   // 1: filter failed (status) or degenerate regrid target: leave untouched
     PL_SN = 22,     // s / N_tot (trace factor and the transform scales, folded into Psi)
     PL_VOL = 23,    // |det B_l|
@@ -165,11 +166,14 @@ __device__ __forceinline__ void team_dft_dif(V* pa, V* pb, V* x, V* ex, const V*
 template <typename T>
 struct PlaneArgs {
     const T* Wsrc;          // weights read by the forward pass (old grid when regridding)
+    const T* W2src;         // pre-regridded weights (general regrid map, flag 2)
     T* W;                   // weights written by the inverse pass
-    typename C2<T>::type* S;
+    typename C2<T>::type* S;      // spectrum written by the forward pass
+    typename C2<T>::type* Sinv;   // spectrum read by the inverse pass (S, or S2 after an out-of-place pass)
     const double* coef;
     int cs;
-    double* dcpart;         // [plane]
+    double* dcpart;         // [plane] sums of the forward pass's input planes
+    double* dc3;            // [filter][n3] slab sums after the split regrid (flag 4)
     double* part;           // [plane][6]
     int nplanes;            // batch * ppf
     int ppf;                // planes per filter
@@ -241,9 +245,15 @@ __global__ void k_plane_prep(FilterState* st, double* coef, int cs, ModelParams 
         mat_inv4(NX, B0, Bi);
         for (int i = 0; i < 16; ++i) M[i] = 0.0;
         mat_mul4(NX, Bi, Bn, M);
-        bool sep = true;
-        for (int a = 1; a < NX; ++a) sep = sep && M[a * 4] == 0.0;
-        flag = sep ? 1 : 2;
+        // split map (nx = 4): v_0 = f(u'_0, u'_1), v_1 = f(u'_1), v_2 = f(u'_2, u'_3), v_3 = f(u'_3),
+        // i.e. block-diagonal (01)(23) with zero lower entries -- the CV models after an
+        // axis-aligned regrid: the in-plane part runs in the forward pass, the (2,3) part in
+        // the first strided pass (flag 4). Anything else: 2^nx-tap gather pre-pass (flag 2).
+        bool split = NX == 4;
+        const int zero_ix[10] = {1 * 4 + 0, 0 * 4 + 2, 0 * 4 + 3, 1 * 4 + 2, 1 * 4 + 3,
+                                 2 * 4 + 0, 2 * 4 + 1, 3 * 4 + 0, 3 * 4 + 1, 3 * 4 + 2};
+        for (int q = 0; q < 10; ++q) split = split && M[zero_ix[q]] == 0.0;
+        flag = split ? 4 : 2;
         if (lane == 0) {
             for (int i = 0; i < 16; ++i) P[PL_M + i] = M[i];
             for (int a = 0; a < NX; ++a) {
@@ -325,147 +335,171 @@ __global__ void k_plane_prep(FilterState* st, double* coef, int cs, ModelParams 
     for (int i = 0; i < 16; ++i) f.B[i] = Bl[i];
 }
 
+// ============================================================================ general regrid pre-pass
+// Filters whose regrid map is neither absent nor split (flag 2): multilinear
+// interpolation (R12, zero ghosts) of the old weights at every new point into W2,
+// which the forward pass then reads plainly.
+template <typename T, int NX>
+__global__ void __launch_bounds__(256) k_plane_pre(const T* __restrict__ W, T* __restrict__ W2,
+                                                   const double* __restrict__ coef, int cs, Dims d, int bpf) {
+    const int filt = blockIdx.x / bpf, qb = blockIdx.x - filt * bpf;
+    const double* P = coef + (long long)filt * cs;
+    if (P[PL_SKIP] != 0.0 || (int)P[PL_FLAG] != 2) return;
+    const long long ntot = d.ntot;
+    const T* Wf = W + filt * ntot;
+    T* Wn = W2 + filt * ntot;
+    const int nsz[4] = {d.n[0], d.n[1], d.n[2], NX == 4 ? d.n[3] : 1};
+    for (long long pt = (long long)qb * blockDim.x + threadIdx.x; pt < ntot; pt += (long long)bpf * blockDim.x) {
+        double u[4];
+        long long r = pt;
+#pragma unroll
+        for (int a2 = 0; a2 < NX; ++a2) {
+            const long long q = r / nsz[a2];
+            u[a2] = (double)(r - q * nsz[a2]) - 0.5 * (nsz[a2] - 1);
+            r = q;
+        }
+        double v[4];
+#pragma unroll
+        for (int a2 = 0; a2 < NX; ++a2) {
+            double x = P[PL_O + a2];
+#pragma unroll
+            for (int b2 = 0; b2 < NX; ++b2) x = fma(P[PL_M + a2 * 4 + b2], u[b2], x);
+            v[a2] = x;
+        }
+        Wn[pt] = (T)gather_point<T, NX>(Wf, nsz, v);
+    }
+}
+
 // ============================================================================ forward plane pass
+// Staged real plane: element (j0, j1), j in [-1, N+1], at stg[(j1 + 1) * SP + j0 + OFF];
+// the ring j = -1, N, N+1 is zero (the zero ghost nodes of R12). SP/2 odd (fp64) keeps
+// the 8 rows a team reads in distinct 16-byte bank groups; interior rows are 16-byte
+// aligned for the bulk copies.
+template <typename T, int N> struct SPitch;
+template <int N> struct SPitch<double, N> { static constexpr int SP = N + 6, OFF = 2; };
+template <int N> struct SPitch<float, N> { static constexpr int SP = N + 12, OFF = 4; };
+template <typename T, int N>
+__host__ __device__ constexpr size_t stage_bytes() { return (size_t)(N + 3) * SPitch<T, N>::SP * sizeof(T); }
+template <typename T, int N>
+__host__ __device__ constexpr size_t xbytes() { return 2 * sizeof(T) * Cfg<N>::H * Cfg<N>::PITCH; }
+// separate staging buffer (the next plane's copy overlaps this plane's FFTs) when both fit
+template <typename T, int N>
+__host__ __device__ constexpr bool fwd_sep() { return stage_bytes<T, N>() + xbytes<T, N>() <= 200 * 1024; }
+template <typename T, int N>
+static size_t fwd_smem() {
+    const size_t xs = fwd_sep<T, N>() ? stage_bytes<T, N>() + xbytes<T, N>()
+                                      : std::max(stage_bytes<T, N>(), xbytes<T, N>());
+    return xs + 2 * sizeof(T) * N + 16;
+}
+
+template <typename T, int N>
+__device__ __forceinline__ void zero_ring(T* stg, int tid, int nt) {
+    constexpr int SP = SPitch<T, N>::SP, OFF = SPitch<T, N>::OFF, W = N + 3;
+    for (int i = tid; i < 3 * W + 3 * N; i += nt) {
+        int row, col;
+        if (i < 3 * W) {
+            const int rr = i / W;
+            row = rr == 0 ? -1 : N - 1 + rr;
+            col = i - rr * W - 1;
+        } else {
+            const int k = i - 3 * W;
+            row = k / 3;
+            const int cc = k - 3 * row;
+            col = cc == 0 ? -1 : N - 1 + cc;
+        }
+        stg[(row + 1) * SP + col + OFF] = T(0);
+    }
+}
+
 template <typename T, int N, int NX, bool RG>
 __global__ void __launch_bounds__(Cfg<N>::NT, Cfg<N>::MINB) k_plane_fwd(PlaneArgs<T> a) {
     using V = typename C2<T>::type;
     using C = Cfg<N>;
-    constexpr int R1 = C::R1, H = C::H, PITCH = C::PITCH, NT = C::NT, SP = C::SP;
-    constexpr int NC = 1 << (NX - 1);                       // old rows blended per new row
+    constexpr int R1 = C::R1, H = C::H, PITCH = C::PITCH, NT = C::NT;
+    constexpr int SP = SPitch<T, N>::SP, OFF = SPitch<T, N>::OFF;
+    constexpr bool SEP = fwd_sep<T, N>();
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    V* X = reinterpret_cast<V*>(smem_raw);                    // [H][PITCH]; also the regrid staging area
-    T* stg = reinterpret_cast<T*>(smem_raw);                  // [N][SP] (ghost columns 0 and N+1)
-    V* tw = X + H * PITCH;
-    int* roff = reinterpret_cast<int*>(tw + N);               // [N][NC] old-row offsets
-    double* rwt = reinterpret_cast<double*>(roff + N * NC);   // [N][NC] corner weights
-    double* rv0 = rwt + N * NC;                               // [N] v0 at u0' = 0
+    V* X = reinterpret_cast<V*>(smem_raw);                    // [H][PITCH]
+    T* stg = SEP ? reinterpret_cast<T*>(smem_raw + xbytes<T, N>()) : reinterpret_cast<T*>(smem_raw);
+    constexpr size_t XS = SEP ? stage_bytes<T, N>() + xbytes<T, N>()
+                              : (stage_bytes<T, N>() > xbytes<T, N>() ? stage_bytes<T, N>() : xbytes<T, N>());
+    V* tw = reinterpret_cast<V*>(smem_raw + XS);
+    unsigned long long* bar = reinterpret_cast<unsigned long long*>(tw + N);
 
     const int tid = threadIdx.x, m = tid >> 3, t = tid & 7;
     init_tw<N>(tw);
-    const int nsz[4] = {N, N, a.n2, a.n3};
+    if (tid == 0) tma::mbar_init(bar, 1);
+    zero_ring<T, N>(stg, tid, NT);
     const long long ntot = (long long)N * N * a.n2 * a.n3;
     __syncthreads();
-    for (int p = blockIdx.x; p < a.nplanes; p += gridDim.x) {
+    // stage plane p (all threads call; rows issued by the first N threads)
+    auto issue = [&](int p) {
+        if (p >= a.nplanes || tid >= N) return;
         const int filt = p / a.ppf, pl = p - filt * a.ppf;
         const double* P = a.coef + (long long)filt * a.cs;
-        if (P[PL_SKIP] != 0.0) continue;                      // uniform
-        int j2, j3;
-        plane_j(pl, a.n2, j2, j3);
-        const double u2 = j2 - 0.5 * (a.n2 - 1), u3 = j3 - 0.5 * (a.n3 - 1);
-        const T* Wf = a.Wsrc + filt * ntot;
+        const T* src = ((RG && (int)P[PL_FLAG] == 2) ? a.W2src : a.Wsrc) + filt * ntot + (long long)pl * N * N;
+        tma::fence_proxy_async();
+        if (tid == 0) tma::mbar_expect_tx(bar, (unsigned)(N * N * sizeof(T)));
+        tma::bulk_g2s(stg + (tid + 1) * SP + OFF, src + (long long)tid * N, (unsigned)(N * sizeof(T)), bar);
+    };
+    if (SEP) issue(blockIdx.x);
+    int k = 0;
+    for (int p = blockIdx.x; p < a.nplanes; p += gridDim.x, ++k) {
+        if (!SEP) {
+            if (k > 0) {
+                zero_ring<T, N>(stg, tid, NT);
+                __syncthreads();
+            }
+            issue(p);
+        }
+        const int filt = p / a.ppf;
+        const double* P = a.coef + (long long)filt * a.cs;
         const int flag = RG ? (int)P[PL_FLAG] : 0;
-        V z[R1];
+        tma::mbar_wait(bar, (unsigned)(k & 1));
         // ------------------------------------------------------------ P1 input: column pair (2m, 2m+1)
-        if (RG && flag == 1) {
-            // row-separable map: every new row blends the same NC old rows (coalesced), then a
-            // linear interpolation along axis 0 (zero ghosts) -- R12 up to rounding order
-            if (tid < N) {
-                const double u1 = tid - 0.5 * (N - 1);
-                const double uu[4] = {0.0, u1, u2, u3};
-                double v0 = P[PL_O];
-#pragma unroll
-                for (int b2 = 1; b2 < NX; ++b2) v0 = fma(P[PL_M + b2], uu[b2], v0);
-                rv0[tid] = v0;
-                int i0[4];
-                double fr[4];
-#pragma unroll
-                for (int a2 = 1; a2 < NX; ++a2) {
-                    double v = P[PL_O + a2];
-#pragma unroll
-                    for (int b2 = 1; b2 < NX; ++b2) v = fma(P[PL_M + a2 * 4 + b2], uu[b2], v);
-                    const double fl = floor(v);
-                    i0[a2] = __double2int_rz(fl);
-                    fr[a2] = v - fl;
-                }
-#pragma unroll
-                for (int c = 0; c < NC; ++c) {
-                    double wt = 1.0;
-                    long long off = 0, stride = N;
-                    bool ok = true;
-#pragma unroll
-                    for (int a2 = 1; a2 < NX; ++a2) {
-                        const int bit = (c >> (a2 - 1)) & 1;
-                        const int ia = i0[a2] + bit;
-                        wt *= bit ? fr[a2] : 1.0 - fr[a2];
-                        ok = ok && ia >= 0 && ia <= nsz[a2] - 1;
-                        off += (long long)ia * stride;
-                        stride *= nsz[a2];
-                    }
-                    rwt[tid * NC + c] = ok ? wt : 0.0;
-                    roff[tid * NC + c] = ok ? (int)off : 0;
-                }
-            }
-            __syncthreads();
-            for (int e = tid; e < N * N; e += NT) {
-                const int row = e / N, i = e - row * N;
-                double v = 0.0;
-#pragma unroll
-                for (int c = 0; c < NC; ++c) v = fma(rwt[row * NC + c], (double)__ldg(Wf + roff[row * NC + c] + i), v);
-                stg[row * SP + i + 1] = (T)v;
-            }
-            for (int e = tid; e < 2 * N; e += NT) stg[(e >> 1) * SP + ((e & 1) ? N + 1 : 0)] = T(0);
-            __syncthreads();
-            const double M00 = P[PL_M];
+        V z[R1];
+        if (RG && flag == 4) {
+            // in-plane part of the split regrid map (R12): bilinear from the staged old plane,
+            // v1 = o1 + M11 u1', v0 = o0 + M00 u0' + M01 u1'; zero ghosts via the staged ring
+            const double M00 = P[PL_M], M01 = P[PL_M + 1], M11 = P[PL_M + 5], o0 = P[PL_O], o1 = P[PL_O + 1];
+            auto split = [&](double v, int& i, double& fr) {
+                const double f = floor(v);
+                const int fi = __double2int_rz(f);
+                i = min(max(fi, -1), N);
+                fr = (fi == i) ? v - f : 0.0;
+            };
 #pragma unroll
             for (int r = 0; r < R1; ++r) {
-                const int j1 = t + 8 * r;
+                const double u1 = (t + 8 * r) - 0.5 * (N - 1);
+                int i1;
+                double a1;
+                split(fma(M11, u1, o1), i1, a1);
+                const double vb = fma(M01, u1, o0);
                 T val[2];
 #pragma unroll
                 for (int e = 0; e < 2; ++e) {
-                    const double v0 = fma(M00, (2 * m + e) - 0.5 * (N - 1), rv0[j1]);
-                    const double fl = floor(v0);
-                    const int fi = __double2int_rz(fl);
-                    const int i = min(max(fi, -1), N);
-                    const double fa = (fi == i) ? v0 - fl : 0.0;
-                    const double lo = (double)stg[j1 * SP + i + 1];
-                    const double hi = (i < N) ? (double)stg[j1 * SP + i + 2] : 0.0;
-                    val[e] = (T)fma(fa, hi - lo, lo);
+                    int i0;
+                    double a0;
+                    split(fma(M00, (2 * m + e) - 0.5 * (N - 1), vb), i0, a0);
+                    const T* r0 = stg + (i1 + 1) * SP + i0 + OFF;
+                    const double w00 = (double)r0[0], w01 = (double)r0[1];
+                    const double w10 = (double)r0[SP], w11 = (double)r0[SP + 1];
+                    const double lo = fma(a0, w01 - w00, w00), hi = fma(a0, w11 - w10, w10);
+                    val[e] = (T)fma(a1, hi - lo, lo);
                 }
                 z[r] = V{val[0], val[1]};
             }
-        } else if (RG && flag == 2) {
-            // general map: 2^nx-tap gather per point from the old weights (L2)
-            double vb[2][4], st1[4];
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-                const double uu[4] = {(2 * m + e) - 0.5 * (N - 1), t - 0.5 * (N - 1), u2, u3};
-#pragma unroll
-                for (int a2 = 0; a2 < NX; ++a2) {
-                    double v = P[PL_O + a2];
-#pragma unroll
-                    for (int b2 = 0; b2 < NX; ++b2) v = fma(P[PL_M + a2 * 4 + b2], uu[b2], v);
-                    vb[e][a2] = v;
-                }
-            }
-#pragma unroll
-            for (int a2 = 0; a2 < NX; ++a2) st1[a2] = 8.0 * P[PL_M + a2 * 4 + 1];
-            // each thread stages its own points (no barrier needed), then reads them back
-            V* own = reinterpret_cast<V*>(stg);
-#pragma unroll 1
-            for (int r = 0; r < R1; ++r) {
-                T val[2];
-#pragma unroll
-                for (int e = 0; e < 2; ++e) {
-                    double v[4];
-#pragma unroll
-                    for (int a2 = 0; a2 < NX; ++a2) v[a2] = fma((double)r, st1[a2], vb[e][a2]);
-                    val[e] = (T)gather_point<T, NX>(Wf, nsz, v);
-                }
-                own[(t + 8 * r) * (N / 2) + m] = V{val[0], val[1]};
-            }
-#pragma unroll
-            for (int r = 0; r < R1; ++r) z[r] = own[(t + 8 * r) * (N / 2) + m];
         } else {
-            const T* Wp = Wf + (long long)pl * N * N;
 #pragma unroll
-            for (int r = 0; r < R1; ++r)
-                z[r] = __ldcs(reinterpret_cast<const V*>(Wp + (long long)(t + 8 * r) * N + 2 * m));
+            for (int r = 0; r < R1; ++r) z[r] = *reinterpret_cast<const V*>(stg + (t + 8 * r + 1) * SP + 2 * m + OFF);
         }
-        __syncthreads();                                      // staging consumed: X is free
+        __syncthreads();                                      // staged plane consumed
+        if (SEP) issue(p + gridDim.x);                        // overlaps the FFTs below
+        if (P[PL_SKIP] != 0.0) continue;                      // uniform; the stage ring stays intact
         // ------------------------------------------------------------ P1: axis-1 FFT of the packed pair
         {
             V pa[8], pb[8];
-            team_dft<R1, false>(z, pa, pb, X, tw, t, [&](int s, int tt) { return cslot<N>(s, tt, m); });
+            team_dft<R1, false>(z, pa, pb, X, tw, t, [&](int s2, int tt) { return cslot<N>(s2, tt, m); });
             if (s_on<R1>(t)) {
                 const int sa = s_a<R1>(t), sb = s_b<R1>(t);
                 // unpack the two real columns: Wa = (Z(k) + conj Z(-k))/2, Wb = (Z(k) - conj Z(-k))/(2i)
@@ -499,14 +533,14 @@ __global__ void __launch_bounds__(Cfg<N>::NT, Cfg<N>::MINB) k_plane_fwd(PlaneArg
 #pragma unroll
                 for (int r = 0; r < R1; ++r) x[r] = row[xcol(m, t + 8 * r)];
             }
-            team_dft<R1, false>(x, pa, pb, row, tw, t, [](int s, int tt) { return rslot(s, tt); });
+            team_dft<R1, false>(x, pa, pb, row, tw, t, [](int s2, int tt) { return rslot(s2, tt); });
             if (s_on<R1>(t)) {
                 const int sa = s_a<R1>(t), sb = s_b<R1>(t);
                 if (m == 0) {
                     // rows 0 and N/2 were packed as one complex row R = A + i B (both real in j0)
-                    auto unpack = [&](int k, V rk, V rm) {
-                        X[k] = V{T(0.5) * (rk.x + rm.x), T(0.5) * (rk.y - rm.y)};
-                        X[(N / 2) * PITCH + k] = V{T(0.5) * (rk.y + rm.y), T(0.5) * (rm.x - rk.x)};
+                    auto unpack = [&](int kk, V rk, V rm) {
+                        X[kk] = V{T(0.5) * (rk.x + rm.x), T(0.5) * (rk.y - rm.y)};
+                        X[(N / 2) * PITCH + kk] = V{T(0.5) * (rk.y + rm.y), T(0.5) * (rm.x - rk.x)};
                     };
                     if (t == 0) {
 #pragma unroll
@@ -544,42 +578,183 @@ __global__ void __launch_bounds__(Cfg<N>::NT, Cfg<N>::MINB) k_plane_fwd(PlaneArg
 // Pencils along one axis of the spectrum [o][j][i] (stride I). MODE 0 forward,
 // 1 inverse, 2 forward x s Psi / N_tot x inverse (last axis; Alg. 3-5). Psi per
 // substep n: f_n = gam_n + bet_n kx_L + alp_n kap_L^2, (gam_n, bet_n) per pencil.
+// Persistent CTAs; a tile (TP consecutive pencils x NA rows) is staged into
+// shared memory by NA bulk row copies completing on the stage's mbarrier, NS
+// stages deep, so the HBM reads of the next tiles overlap this tile's FFTs. Team
+// p's staged column doubles as its exchange area (pitch TP + 1: conflict-free).
 template <typename T>
 struct MidArgs {
-    typename C2<T>::type* S;
+    typename C2<T>::type* S;      // input spectrum
+    typename C2<T>::type* Sout;   // output (== S: in place)
     const double* coef;
     int cs;
     long long I, O;          // inner stride (pencils per o) and outer count
     int ocpf;                // o values per filter (MODE 2: 1)
-    int N0, H1, n2;          // plane sizes and axis-2 size (wavenumber decode)
+    int N0, H1, n2, n3;      // plane sizes, axis-2/3 sizes (wavenumber decode, split regrid)
     int l;
+    int skip4;               // MODE 0: leave filters with a split regrid map (flag 4) to MODE 3
+    double* dc3;             // MODE 3: [filter][n3] slab sums of the regridded weights
 };
 
-template <typename T, int NA, int MODE, int NX>
-__global__ void __launch_bounds__(256, 2) k_plane_mid(MidArgs<T> a) {
+// tile shape / pipeline variants: TP pencils per tile, NS stages, MINB CTAs per SM
+template <int V_> struct MidVar;
+template <> struct MidVar<0> { static constexpr int TP = 32, NS = 2, MINB = 2; };   // small pencils
+template <> struct MidVar<1> { static constexpr int TP = 32, NS = 4, MINB = 1; };   // 96: 4-deep ring
+template <> struct MidVar<2> { static constexpr int TP = 32, NS = 2, MINB = 1; };   // 96, MODE 3 (2 sets)
+template <> struct MidVar<3> { static constexpr int TP = 32, NS = 3, MINB = 1; };   // 128
+template <> struct MidVar<4> { static constexpr int TP = 16, NS = 2, MINB = 1; };   // 128, MODE 3
+
+template <typename T, int NA, int VAR>
+struct MidCfg {
+    static constexpr int TP = MidVar<VAR>::TP;                      // pencils (teams) per tile
+    static constexpr int PP = sizeof(T) == 8 ? TP + 1 : TP + 2;     // staged row pitch (complex), 16-B rows
+    static constexpr int NS = MidVar<VAR>::NS;                      // pipeline stages
+    static constexpr int MINB = MidVar<VAR>::MINB;
+    static constexpr int NT = 8 * TP;
+};
+
+template <typename T, int NA, int VAR>
+static size_t mid_smem(int l, int sets) {
+    using C = MidCfg<T, NA, VAR>;
+    return sizeof(typename C2<T>::type) * ((size_t)sets * C::NS * NA * C::PP + NA) + 16 * 4 +
+           sizeof(double2) * C::TP * l;
+}
+
+template <typename T, int NA, int MODE, int NX, int VAR>
+__global__ void __launch_bounds__(MidCfg<T, NA, VAR>::NT, MidCfg<T, NA, VAR>::MINB) k_plane_mid(MidArgs<T> a) {
     using V = typename C2<T>::type;
-    constexpr int R1 = NA / 8;
+    using C = MidCfg<T, NA, VAR>;
+    constexpr int R1 = NA / 8, TP = C::TP, PP = C::PP, NS = C::NS;
     constexpr int L = NX - 1;                                 // this pass's axis when MODE == 2
+    constexpr int SETS = MODE == 3 ? 2 : 1;                   // MODE 3 stages the two j3 rows it blends
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    V* E = reinterpret_cast<V*>(smem_raw);                    // [MID_TEAMS][NA]
-    V* tw = E + MID_TEAMS * NA;                               // [NA]
-    double2* psi = reinterpret_cast<double2*>(tw + NA);       // [MID_TEAMS][LCAP] (gam, bet)
+    V* stg = reinterpret_cast<V*>(smem_raw);                  // [NS][SETS][NA][PP]
+    V* tw = stg + NS * SETS * NA * PP;                        // [NA]
+    unsigned long long* bar = reinterpret_cast<unsigned long long*>(tw + NA);   // [NS] (<= 4)
+    double2* psi = reinterpret_cast<double2*>(bar + 4);       // [TP][l] (gam, bet)
     const int tid = threadIdx.x, p = tid >> 3, t = tid & 7;
     init_tw<NA>(tw);
+    if (tid == 0)
+        for (int q = 0; q < NS; ++q) tma::mbar_init(&bar[q], 1);
     __syncthreads();
-    V* ex = E + p * NA;
-    auto slot = [](int s, int tt) { return rslot(s, tt); };
-    const long long tiles = (a.I + MID_TEAMS - 1) / MID_TEAMS;
-    for (long long blk = blockIdx.x; blk < a.O * tiles; blk += gridDim.x) {
-        const long long o = blk / tiles;
-        const long long i = (blk - o * tiles) * MID_TEAMS + p;
-        const bool valid = i < a.I;
-        V* base = a.S + o * (long long)NA * a.I + (valid ? i : 0);
-        V x[R1];
+    const long long tiles = (a.I + TP - 1) / TP, ntile = a.O * tiles;
+    // does this pass transform the tiles of filter f? (MODE 0 / 3 split the filters by regrid kind)
+    long long act_f = -1;                                     // one-filter cache (filters span many tiles)
+    bool act_v = true;
+    auto active = [&](long long f) -> bool {
+        if (MODE != 3 && !(MODE == 0 && a.skip4)) return true;
+        if (f != act_f) {
+            const double* P = a.coef + f * a.cs;
+            const bool split = P[PL_SKIP] == 0.0 && (int)P[PL_FLAG] == 4;
+            act_v = MODE == 3 ? split : !split;
+            act_f = f;
+        }
+        return act_v;
+    };
+    // old-grid rows j3 blended into output slab u3' (MODE 3): weights and validity
+    auto rows3 = [&](const double* P, long long u3i, int& j3, double& w3) {
+        const double v3 = fma(P[PL_M + 15], (double)u3i - 0.5 * (a.n3 - 1), P[PL_O + 3]);
+        const double f = floor(v3);
+        const int fi = __double2int_rz(f);
+        j3 = min(max(fi, -2), a.n3);
+        w3 = (fi == j3) ? v3 - f : 0.0;
+    };
+    // tiles of inactive filters are neither staged nor waited for (their stage's phase is not used)
+    auto issue = [&](long long blk, int st) {
+        if (blk >= ntile || tid >= NA) return;
+        const long long o = blk / tiles, i0 = (blk - o * tiles) * TP;
+        const long long cnt = a.I - i0 < TP ? a.I - i0 : TP;
+        const unsigned bytes = ((unsigned)(cnt * sizeof(V)) + 15u) & ~15u;
+        const long long filt = o / a.ocpf;
+        if (!active(filt)) return;
+        tma::fence_proxy_async();
+        if (MODE == 3) {
+            const double* P = a.coef + filt * a.cs;
+            int j3;
+            double w3;
+            rows3(P, o - filt * a.ocpf, j3, w3);
+            const bool va = j3 >= 0 && j3 < a.n3, vb = j3 + 1 >= 0 && j3 + 1 < a.n3;
+            if (tid == 0) tma::mbar_expect_tx(&bar[st], bytes * NA * ((va ? 1 : 0) + (vb ? 1 : 0)));
+            const long long ob = filt * a.ocpf + j3;
+            if (va) tma::bulk_g2s(stg + ((st * 2) * NA + tid) * PP, a.S + (ob * NA + tid) * a.I + i0, bytes, &bar[st]);
+            if (vb)
+                tma::bulk_g2s(stg + ((st * 2 + 1) * NA + tid) * PP, a.S + ((ob + 1) * NA + tid) * a.I + i0, bytes,
+                              &bar[st]);
+            return;
+        }
+        if (tid == 0) tma::mbar_expect_tx(&bar[st], bytes * NA);
+        tma::bulk_g2s(stg + (st * NA + tid) * PP, a.S + (o * NA + tid) * a.I + i0, bytes, &bar[st]);
+    };
 #pragma unroll
-        for (int r = 0; r < R1; ++r) x[r] = valid ? __ldcs(base + (long long)(t + 8 * r) * a.I) : V{T(0), T(0)};
-        V pa[8], pb[8];
-        team_dft<R1, MODE == 1>(x, pa, pb, ex, tw, t, slot);
+    for (int j = 0; j < NS - 1; ++j) issue(blockIdx.x + (long long)j * gridDim.x, j);
+    auto slot = [](int s2, int tt) { return rslot(s2, tt) * PP; };
+    int k = 0;
+    unsigned phase = 0;                                       // bit q: parity of stage q's next wait
+    for (long long blk = blockIdx.x; blk < ntile; blk += gridDim.x, ++k) {
+        const int st = k % NS;
+        issue(blk + (long long)(NS - 1) * gridDim.x, (k + NS - 1) % NS);
+        const long long o = blk / tiles;
+        const long long i = (blk - o * tiles) * TP + p;
+        const bool valid = i < a.I;
+        const long long filt = o / a.ocpf;
+        if (!active(filt)) continue;                          // uniform; nothing was staged
+        tma::mbar_wait(&bar[st], (phase >> st) & 1u);
+        phase ^= 1u << st;
+        V* base = a.Sout + o * (long long)NA * a.I + (valid ? i : 0);
+        V* col = stg + st * SETS * NA * PP + p;
+        V x[R1], pa[8], pb[8];
+        if (MODE == 3) {
+            // split regrid (R12), axes 3 then 2: Z(j2) = (1 - w3) S(j2, j3) + w3 S(j2, j3 + 1), then
+            // Y(u2') = linear interpolation of Z at v2 = o2 + M22 u2' + M23 u3' (zero ghosts)
+            const double* P = a.coef + filt * a.cs;
+            const long long u3i = o - filt * a.ocpf;
+            int j3;
+            double w3;
+            rows3(P, u3i, j3, w3);
+            const bool va = j3 >= 0 && j3 < a.n3, vb = j3 + 1 >= 0 && j3 + 1 < a.n3;
+            const V* colb = col + NA * PP;
+#pragma unroll
+            for (int r = 0; r < R1; ++r) {
+                const int j2 = t + 8 * r;
+                V zz = V{T(0), T(0)};
+                if (va) {
+                    const V v = col[j2 * PP];
+                    zz = V{(T)((1.0 - w3) * v.x), (T)((1.0 - w3) * v.y)};
+                }
+                if (vb) {
+                    const V v = colb[j2 * PP];
+                    zz = V{(T)fma(w3, (double)v.x, (double)zz.x), (T)fma(w3, (double)v.y, (double)zz.y)};
+                }
+                col[j2 * PP] = zz;
+            }
+            __syncwarp();
+            const double M22 = P[PL_M + 10], M23 = P[PL_M + 11], o2 = P[PL_O + 2];
+            const double vb2 = fma(M23, (double)u3i - 0.5 * (a.n3 - 1), o2);
+            double dcs = 0.0;
+#pragma unroll
+            for (int r = 0; r < R1; ++r) {
+                const double v2 = fma(M22, (t + 8 * r) - 0.5 * (NA - 1), vb2);
+                const double f = floor(v2);
+                const int fi = __double2int_rz(f);
+                const double fr = v2 - f;
+                const V lo = (fi >= 0 && fi < NA) ? col[fi * PP] : V{T(0), T(0)};
+                const V hi = (fi + 1 >= 0 && fi + 1 < NA) ? col[(fi + 1) * PP] : V{T(0), T(0)};
+                x[r] = V{(T)fma(fr, (double)hi.x - (double)lo.x, (double)lo.x),
+                         (T)fma(fr, (double)hi.y - (double)lo.y, (double)lo.y)};
+                dcs += (double)x[r].x;
+            }
+            if (i == 0) {      // pencil k0 = k1 = 0: sum of this slab's regridded weights
+                const unsigned tm = 0xFFu << ((tid & 31) & ~7);   // this team's 8 lanes
+                dcs += __shfl_xor_sync(tm, dcs, 1);
+                dcs += __shfl_xor_sync(tm, dcs, 2);
+                dcs += __shfl_xor_sync(tm, dcs, 4);
+                if (t == 0) a.dc3[filt * a.n3 + u3i] = dcs;
+            }
+        } else {
+#pragma unroll
+            for (int r = 0; r < R1; ++r) x[r] = col[(t + 8 * r) * PP];
+        }
+        team_dft<R1, MODE == 1>(x, pa, pb, col, tw, t, slot);
         if (MODE != 2) {
             if (valid && s_on<R1>(t)) {
                 const int sa = s_a<R1>(t), sb = s_b<R1>(t);
@@ -589,22 +764,20 @@ __global__ void __launch_bounds__(256, 2) k_plane_mid(MidArgs<T> a) {
                     __stcg(base + (long long)(sb + R1 * q) * a.I, pb[q]);
                 }
             }
-            continue;
-        }
-        // ---------------------------------------------------------------- s Psi / N_tot (Alg. 3-4)
-        const long long filt = o / a.ocpf;
-        const double* P = a.coef + filt * a.cs;
-        const double* cf = P + PL_EU;
-        {
-            // wavenumbers of the pencil's other axes: inner i = (j2 *) H1 N0 + k1 N0 + k0
-            double kap[3] = {0, 0, 0}, kx[3] = {0, 0, 0};
-            const long long ii = valid ? i : 0;
-            const int k0 = (int)(ii % a.N0);
-            const long long r1 = ii / a.N0;
-            const int k1 = (int)(r1 % a.H1);
-            const int k2 = (int)(r1 / a.H1);
-            const int N1 = 2 * (a.H1 - 1);
+        } else {
+            // ------------------------------------------------------------ s Psi / N_tot (Alg. 3-4)
+            const long long filt = o / a.ocpf;
+            const double* P = a.coef + filt * a.cs;
+            const double* cf = P + PL_EU;
             {
+                // wavenumbers of the pencil's other axes: inner i = (j2 *) H1 N0 + k1 N0 + k0
+                double kap[3] = {0, 0, 0}, kx[3] = {0, 0, 0};
+                const long long ii = valid ? i : 0;
+                const int k0 = (int)(ii % a.N0);
+                const long long r1 = ii / a.N0;
+                const int k1 = (int)(r1 % a.H1);
+                const int k2 = (int)(r1 / a.H1);
+                const int N1 = 2 * (a.H1 - 1);
                 const int ks0 = k0 < a.N0 / 2 ? k0 : k0 - a.N0;
                 kap[0] = 2.0 * PMF_PI * ks0 / a.N0;
                 kx[0] = (2 * k0 == a.N0) ? 0.0 : kap[0];
@@ -615,95 +788,123 @@ __global__ void __launch_bounds__(256, 2) k_plane_mid(MidArgs<T> a) {
                     kap[2] = 2.0 * PMF_PI * ks2 / a.n2;
                     kx[2] = (2 * k2 == a.n2) ? 0.0 : kap[2];
                 }
-            }
-            for (int n = t; n < a.l; n += 8) {
-                const double* c = cf + 10 * n;
-                double g = 1.0, bb = 0.0;
+                for (int n = t; n < a.l; n += 8) {
+                    const double* c = cf + 10 * n;
+                    double g = 1.0, bb = 0.0;
 #pragma unroll
-                for (int a2 = 0; a2 < L; ++a2) {
-                    g = fma(c[a2], kap[a2] * kap[a2], g);
+                    for (int a2 = 0; a2 < L; ++a2) {
+                        g = fma(c[a2], kap[a2] * kap[a2], g);
 #pragma unroll
-                    for (int b2 = a2 + 1; b2 < L; ++b2) g = fma(c[pair_index(NX, a2, b2)], kx[a2] * kx[b2], g);
-                    bb = fma(c[pair_index(NX, a2, L)], kx[a2], bb);
-                }
-                psi[p * LCAP + n] = double2{g, bb};
-            }
-        }
-        __syncwarp();
-        if (s_on<R1>(t)) {
-            const double mult = P[PL_SN];
-            auto mul8 = [&](V* v, int s0) {
-                double kk[8], kxl[8], den[8];
-#pragma unroll
-                for (int q = 0; q < 8; ++q) {
-                    const int k = s0 + R1 * q;
-                    const int ks = k < NA / 2 ? k : k - NA;
-                    const double kp = 2.0 * PMF_PI * ks / NA;
-                    kk[q] = kp * kp;
-                    kxl[q] = (2 * k == NA) ? 0.0 : kp;
-                    den[q] = 1.0;
-                }
-                for (int n = 0; n < a.l; ++n) {
-                    const double2 gb = psi[p * LCAP + n];
-                    const double al = cf[10 * n + L];
-#pragma unroll
-                    for (int q = 0; q < 8; ++q) den[q] *= fma(al, kk[q], fma(gb.y, kxl[q], gb.x));
-                }
-                double pre[8];
-                pre[0] = den[0];
-#pragma unroll
-                for (int q = 1; q < 8; ++q) pre[q] = pre[q - 1] * den[q];
-                double ps[8];
-                if (pre[7] < 1e300) {
-                    double inv = mult / pre[7];
-#pragma unroll
-                    for (int q = 7; q > 0; --q) {
-                        ps[q] = inv * pre[q - 1];
-                        inv *= den[q];
+                        for (int b2 = a2 + 1; b2 < L; ++b2) g = fma(c[pair_index(NX, a2, b2)], kx[a2] * kx[b2], g);
+                        bb = fma(c[pair_index(NX, a2, L)], kx[a2], bb);
                     }
-                    ps[0] = inv;
-                } else {
-#pragma unroll
-                    for (int q = 0; q < 8; ++q) ps[q] = mult / den[q];
+                    psi[p * a.l + n] = double2{g, bb};
                 }
+            }
+            __syncwarp();
+            if (s_on<R1>(t)) {
+                const double mult = P[PL_SN];
+                auto mul8 = [&](V* v, int s0) {
+                    double den[8], k2[8], kxl[8];
 #pragma unroll
-                for (int q = 0; q < 8; ++q) v[q] = V{(T)(v[q].x * ps[q]), (T)(v[q].y * ps[q])};
-            };
-            mul8(pa, s_a<R1>(t));
-            mul8(pb, s_b<R1>(t));
-        }
-        team_dft_dif<R1, true>(pa, pb, x, ex, tw, t, slot);
-        if (valid) {
+                    for (int q = 0; q < 8; ++q) {
+                        const int kk = s0 + R1 * q;
+                        const double kp = (2.0 * PMF_PI / NA) * (kk < NA / 2 ? kk : kk - NA);
+                        k2[q] = kp * kp;
+                        kxl[q] = (2 * kk == NA) ? 0.0 : kp;
+                        den[q] = 1.0;
+                    }
+                    for (int n = 0; n < a.l; ++n) {
+                        const double2 gb = psi[p * a.l + n];
+                        const double al = cf[10 * n + L];
 #pragma unroll
-            for (int r = 0; r < R1; ++r) __stcg(base + (long long)(t + 8 * r) * a.I, x[r]);
+                        for (int q = 0; q < 8; ++q) den[q] *= fma(al, k2[q], fma(gb.y, kxl[q], gb.x));
+                    }
+                    double pre[8];
+                    pre[0] = den[0];
+#pragma unroll
+                    for (int q = 1; q < 8; ++q) pre[q] = pre[q - 1] * den[q];
+                    if (pre[7] < 1e300) {
+                        double inv = mult / pre[7];
+#pragma unroll
+                        for (int q = 7; q > 0; --q) {
+                            const double ps = inv * pre[q - 1];
+                            inv *= den[q];
+                            v[q] = V{(T)(v[q].x * ps), (T)(v[q].y * ps)};
+                        }
+                        v[0] = V{(T)(v[0].x * inv), (T)(v[0].y * inv)};
+                    } else {
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) {
+                            const double ps = mult / den[q];
+                            v[q] = V{(T)(v[q].x * ps), (T)(v[q].y * ps)};
+                        }
+                    }
+                };
+                mul8(pa, s_a<R1>(t));
+                mul8(pb, s_b<R1>(t));
+            }
+            team_dft_dif<R1, true>(pa, pb, x, col, tw, t, slot);
+            if (valid) {
+#pragma unroll
+                for (int r = 0; r < R1; ++r) __stcg(base + (long long)(t + 8 * r) * a.I, x[r]);
+            }
         }
+        __syncthreads();                  // stage st is consumed: it is refilled next iteration
     }
 }
 
 // ============================================================================ inverse plane pass (+ update)
+template <typename T, int N>
+__host__ __device__ constexpr bool inv_dbl() { return 2 * xbytes<T, N>() <= 200 * 1024; }
+template <typename T, int N>
+static size_t inv_smem() {
+    return (inv_dbl<T, N>() ? 2 : 1) * xbytes<T, N>() + 2 * sizeof(T) * N + sizeof(double) * 6 * (Cfg<N>::NT / 32) +
+           16;
+}
+
+// The plane's spectrum rows are staged by H bulk copies; with two buffers (N <= 96)
+// the next plane's copy overlaps this plane's transforms and likelihood.
 template <typename T, int N, int NX, bool UP>
 __global__ void __launch_bounds__(Cfg<N>::NT, Cfg<N>::MINB) k_plane_inv(PlaneArgs<T> a) {
     using V = typename C2<T>::type;
     using C = Cfg<N>;
     constexpr int R1 = C::R1, H = C::H, PITCH = C::PITCH, NT = C::NT, NW = NT / 32;
+    constexpr bool DBL = inv_dbl<T, N>();
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    V* X = reinterpret_cast<V*>(smem_raw);
-    V* tw = X + H * PITCH;
+    V* X0 = reinterpret_cast<V*>(smem_raw);
+    V* tw = X0 + (DBL ? 2 : 1) * H * PITCH;
     double* red = reinterpret_cast<double*>(tw + N);          // [NW][6]
+    unsigned long long* bar = reinterpret_cast<unsigned long long*>(red + 6 * NW);
     const int tid = threadIdx.x, m = tid >> 3, t = tid & 7, lane = tid & 31, warp = tid >> 5;
     init_tw<N>(tw);
+    if (tid == 0) {
+        tma::mbar_init(&bar[0], 1);
+        tma::mbar_init(&bar[1], 1);
+    }
     const long long ntot = (long long)N * N * a.n2 * a.n3;
     __syncthreads();
-    for (int p = blockIdx.x; p < a.nplanes; p += gridDim.x) {
+    auto issue = [&](int p, int buf) {
+        if (p >= a.nplanes || tid >= H) return;
+        tma::fence_proxy_async();
+        if (tid == 0) tma::mbar_expect_tx(&bar[buf], (unsigned)(H * N * sizeof(V)));
+        tma::bulk_g2s(X0 + (buf * H + tid) * PITCH, a.Sinv + (long long)p * (H * N) + (long long)tid * N,
+                      (unsigned)(N * sizeof(V)), &bar[buf]);
+    };
+    issue(blockIdx.x, 0);
+    int k = 0;
+    for (int p = blockIdx.x; p < a.nplanes; p += gridDim.x, ++k) {
+        const int buf = DBL ? (k & 1) : 0;
+        if (DBL) issue(p + gridDim.x, buf ^ 1);
+        else if (k > 0) issue(p, 0);
+        tma::mbar_wait(&bar[buf], (unsigned)(DBL ? ((k >> 1) & 1) : (k & 1)));
+        V* X = X0 + buf * H * PITCH;
         const int filt = p / a.ppf, pl = p - filt * a.ppf;
         const double* P = a.coef + (long long)filt * a.cs;
-        if (P[PL_SKIP] != 0.0) continue;
-        const V* Sp = a.S + (long long)p * (H * N);
-        for (int e = tid; e < H * N; e += NT) {
-            const int r = e / N, c = e - r * N;
-            X[r * PITCH + c] = __ldcs(Sp + e);
+        if (P[PL_SKIP] != 0.0) {
+            __syncthreads();
+            continue;
         }
-        __syncthreads();
         // ------------------------------------------------------------ P2: inverse axis 0 of row k1 = m
         {
             V x[R1], pa[8], pb[8];
@@ -903,17 +1104,20 @@ __global__ void __launch_bounds__(Cfg<N>::NT, Cfg<N>::MINB) k_plane_inv(PlaneArg
 // ============================================================================ finalise (one block per filter)
 template <int NX>
 __global__ void k_plane_fin(FilterState* st, const double* __restrict__ coef, int cs, const double* __restrict__ dcpart,
-                            const double* __restrict__ part, int ppf, int n2, int n3, int update) {
+                            const double* __restrict__ dc3, const double* __restrict__ part, int ppf, int n2, int n3,
+                            int update) {
     __shared__ double red[32 * 16];
     const int filt = blockIdx.x;
     const double* P = coef + (long long)filt * cs;
     if (P[PL_SKIP] != 0.0) return;
+    const bool split = (int)P[PL_FLAG] == 4;     // the regridded sums come from the split pass (per slab)
     double acc[16];
 #pragma unroll
     for (int i = 0; i < 16; ++i) acc[i] = 0.0;
     for (int pl = threadIdx.x; pl < ppf; pl += blockDim.x) {
         const long long p = (long long)filt * ppf + pl;
-        acc[15] += dcpart[p];
+        if (!split) acc[15] += dcpart[p];
+        else if (pl < n3) acc[15] += dc3[(long long)filt * n3 + pl];
         if (!update) continue;
         const double* pp = part + p * 6;
         int j2, j3;
@@ -992,25 +1196,54 @@ static cudaError_t occ_grid(K kern, int nt, size_t smem, long long work, int* gr
     return cudaSuccess;
 }
 
+template <typename T, int NA, int NX, int VAR, int MODE>
+static cudaError_t mid_launch(MidArgs<T> ma, cudaStream_t s) {
+    using C = MidCfg<T, NA, VAR>;
+    const size_t smem = mid_smem<T, NA, VAR>(MODE == 2 ? ma.l : 0, MODE == 3 ? 2 : 1);
+    const long long work = ma.O * ((ma.I + C::TP - 1) / C::TP);
+    int grid = 1;
+    cudaError_t e = occ_grid(k_plane_mid<T, NA, MODE, NX, VAR>, C::NT, smem, work, &grid);
+    if (e != cudaSuccess) return e;
+    k_plane_mid<T, NA, MODE, NX, VAR><<<grid, C::NT, smem, s>>>(ma);
+    return cudaGetLastError();
+}
+
+template <typename T, int NA, int NX, int VAR>
+static cudaError_t mid_var(MidArgs<T> ma, int mode, cudaStream_t s) {
+    switch (mode) {
+        case 0: return mid_launch<T, NA, NX, VAR, 0>(ma, s);
+        case 1: return mid_launch<T, NA, NX, VAR, 1>(ma, s);
+        case 2: return mid_launch<T, NA, NX, VAR, 2>(ma, s);
+        default:
+            if constexpr (NX == 4) return mid_launch<T, NA, NX, VAR, 3>(ma, s);
+            return cudaErrorInvalidValue;
+    }
+}
+
+static int mid_variant(int mode) {
+    static int v[4] = {-2, -2, -2, -2};
+    if (v[mode] == -2) {
+        const char* names[4] = {"PMF_MID_VAR_FWD", "PMF_MID_VAR_INV", "PMF_MID_VAR_PSI", "PMF_MID_VAR_SPLIT"};
+        const char* e = getenv(names[mode]);
+        v[mode] = e ? atoi(e) : -1;
+    }
+    return v[mode];
+}
+
+// measured on B200 (C4 96^4): a 4-deep ring at one CTA per SM beats 2 x (2-deep) by 20 %
 template <typename T, int NA, int NX>
 static cudaError_t mid_na(MidArgs<T> ma, int mode, cudaStream_t s) {
-    using V = typename C2<T>::type;
-    const size_t smem = sizeof(V) * (MID_TEAMS + 1) * NA + sizeof(double2) * MID_TEAMS * LCAP;
-    const long long work = ma.O * ((ma.I + MID_TEAMS - 1) / MID_TEAMS);
-    int grid = 1;
-    cudaError_t e;
-    if (mode == 0) {
-        e = occ_grid(k_plane_mid<T, NA, 0, NX>, 256, smem, work, &grid);
-        if (e == cudaSuccess) k_plane_mid<T, NA, 0, NX><<<grid, 256, smem, s>>>(ma);
-    } else if (mode == 1) {
-        e = occ_grid(k_plane_mid<T, NA, 1, NX>, 256, smem, work, &grid);
-        if (e == cudaSuccess) k_plane_mid<T, NA, 1, NX><<<grid, 256, smem, s>>>(ma);
-    } else {
-        e = occ_grid(k_plane_mid<T, NA, 2, NX>, 256, smem, work, &grid);
-        if (e == cudaSuccess) k_plane_mid<T, NA, 2, NX><<<grid, 256, smem, s>>>(ma);
+    const int over = mid_variant(mode);
+    if (NA == 96) {
+        if (mode == 3) return mid_var<T, NA, NX, 2>(ma, mode, s);
+        if (over == 0) return mid_var<T, NA, NX, 0>(ma, mode, s);
+        return mid_var<T, NA, NX, 1>(ma, mode, s);
     }
-    if (e != cudaSuccess) return e;
-    return cudaGetLastError();
+    if (NA == 128) {
+        if (mode == 3) return mid_var<T, NA, NX, 4>(ma, mode, s);
+        return mid_var<T, NA, NX, 3>(ma, mode, s);
+    }
+    return mid_var<T, NA, NX, 0>(ma, mode, s);
 }
 
 template <typename T, int NX>
@@ -1038,27 +1271,38 @@ static cudaError_t plane_t(const Dims& d, PencilBufs& b, const ModelParams& mp, 
     if (e != cudaSuccess) return e;
     const int n2 = d.n[2], n3 = NX == 4 ? d.n[3] : 1;
     const int ppf = n2 * n3;
+    const bool rg = ks > 0.0;
+    V* S = (V*)b.S;
+    V* S2 = NX == 4 ? (V*)b.S2 : S;              // nx = 4: the first strided pass runs out of place
     PlaneArgs<T> pa;
     pa.Wsrc = (const T*)b.W;
+    pa.W2src = (const T*)b.W2;
     pa.W = (T*)b.W;
-    pa.S = (V*)b.S;
+    pa.S = S;
+    pa.Sinv = S2;
     pa.coef = b.coef;
     pa.cs = cs;
     pa.ppf = ppf;
     pa.nplanes = ppf * d.batch;
     pa.dcpart = b.partials;
     pa.part = b.partials + pa.nplanes;
+    pa.dc3 = b.partials + 7LL * pa.nplanes;
     pa.n2 = n2;
     pa.n3 = n3;
     pa.l = mp.l;
     pa.range = lpv.kind == 1;
+    // general regrid maps: gather pre-pass into W2 (exits at once for the other filters)
+    if (rg) {
+        const int bpf = (int)std::max(1LL, std::min(1024LL, (d.ntot + 2047) / 2048));
+        k_plane_pre<T, NX><<<(unsigned)(bpf * d.batch), 256, 0, s>>>((const T*)b.W, (T*)b.W2, b.coef, cs, d, bpf);
+        ++*launches;
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    }
     // forward plane pass
     {
-        constexpr int NC = 1 << (NX - 1);
-        const size_t smem = sizeof(V) * (Cf::H * Cf::PITCH + N) + (size_t)N * NC * (sizeof(int) + sizeof(double)) +
-                            sizeof(double) * N;
+        const size_t smem = fwd_smem<T, N>();
         int grid = 1;
-        if (ks > 0.0) {
+        if (rg) {
             e = occ_grid(k_plane_fwd<T, N, NX, true>, Cf::NT, smem, pa.nplanes, &grid);
             if (e == cudaSuccess) k_plane_fwd<T, N, NX, true><<<grid, Cf::NT, smem, s>>>(pa);
         } else {
@@ -1069,10 +1313,12 @@ static cudaError_t plane_t(const Dims& d, PencilBufs& b, const ModelParams& mp, 
         ++*launches;
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
-    // strided axes: forward 2..nx-2, last axis with Psi, inverse nx-2..2
-    auto mid = [&](int m, int mode) -> cudaError_t {
+    // strided axes: forward 2..nx-2 (the first out of place, + the split regrid's (2,3) part),
+    // the last axis with Psi, inverse nx-2..2
+    auto mid = [&](int m, int mode, V* in, V* out, int skip4) -> cudaError_t {
         MidArgs<T> ma;
-        ma.S = (V*)b.S;
+        ma.S = in;
+        ma.Sout = out;
         ma.coef = b.coef;
         ma.cs = cs;
         ma.I = (long long)Cf::H * N;
@@ -1086,20 +1332,24 @@ static cudaError_t plane_t(const Dims& d, PencilBufs& b, const ModelParams& mp, 
         ma.N0 = N;
         ma.H1 = Cf::H;
         ma.n2 = n2;
+        ma.n3 = n3;
         ma.l = mp.l;
+        ma.skip4 = skip4;
+        ma.dc3 = pa.dc3;
         ++*launches;
         return mid_pass<T, NX>(ma, d.n[m], mode, s);
     };
-    for (int m = 2; m < NX - 1; ++m)
-        if ((e = mid(m, 0)) != cudaSuccess) return e;
+    if (NX == 4) {
+        if ((e = mid(2, 0, S, S2, rg ? 1 : 0)) != cudaSuccess) return e;
+        if (rg && (e = mid(2, 3, S, S2, 0)) != cudaSuccess) return e;
+    }
     if (b.ev0) cudaEventRecord(b.ev0, s);
-    if ((e = mid(NX - 1, 2)) != cudaSuccess) return e;
+    if ((e = mid(NX - 1, 2, S2, S2, 0)) != cudaSuccess) return e;
     if (b.ev1) cudaEventRecord(b.ev1, s);
-    for (int m = NX - 2; m >= 2; --m)
-        if ((e = mid(m, 1)) != cudaSuccess) return e;
+    if (NX == 4 && (e = mid(2, 1, S2, S2, 0)) != cudaSuccess) return e;
     // inverse plane pass (+ update)
     {
-        const size_t smem = sizeof(V) * (Cf::H * Cf::PITCH + N) + sizeof(double) * 6 * (Cf::NT / 32);
+        const size_t smem = inv_smem<T, N>();
         int grid = 1;
         if (lp) {
             e = occ_grid(k_plane_inv<T, N, NX, true>, Cf::NT, smem, pa.nplanes, &grid);
@@ -1112,7 +1362,7 @@ static cudaError_t plane_t(const Dims& d, PencilBufs& b, const ModelParams& mp, 
         ++*launches;
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
-    k_plane_fin<NX><<<d.batch, 256, 0, s>>>(b.st, b.coef, cs, pa.dcpart, pa.part, ppf, n2, n3, lp ? 1 : 0);
+    k_plane_fin<NX><<<d.batch, 256, 0, s>>>(b.st, b.coef, cs, pa.dcpart, pa.dc3, pa.part, ppf, n2, n3, lp ? 1 : 0);
     ++*launches;
     return cudaGetLastError();
 }
@@ -1142,7 +1392,7 @@ cudaError_t launch_plane(const Dims& d, int dtype, PencilBufs& b, const ModelPar
 size_t plane_partials_doubles(const Dims& d) {
     long long ppf = 1;
     for (int m = 2; m < d.nx; ++m) ppf *= d.n[m];
-    return (size_t)(7 * ppf * d.batch);
+    return (size_t)((7 * ppf + d.n[3]) * d.batch);
 }
 
 }  // namespace pmf

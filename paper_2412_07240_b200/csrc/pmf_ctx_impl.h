@@ -34,6 +34,7 @@ struct pmf_ctx {
     void* W = nullptr;
     void* W2 = nullptr;
     void* S = nullptr;
+    void* S2 = nullptr;
     pmf::FilterState* st = nullptr;
     double* partials = nullptr;
     size_t partials_bytes = 0;

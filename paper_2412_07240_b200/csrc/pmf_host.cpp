@@ -163,7 +163,7 @@ static int dalloc(pmf_ctx* c, void** p, size_t bytes) {
 
 static PencilBufs bufs(pmf_ctx* c) {
     PencilBufs b;
-    b.W = c->W; b.W2 = c->W2; b.S = c->S; b.st = c->st; b.partials = c->partials; b.coef = c->coef;
+    b.W = c->W; b.W2 = c->W2; b.S = c->S; b.S2 = c->S2; b.st = c->st; b.partials = c->partials; b.coef = c->coef;
     b.sub = c->sub; b.z = c->z; b.gauss = c->gauss;
     return b;
 }
@@ -468,6 +468,7 @@ int pmf_create(const pmf_config* cfg, const double* A, const double* Q, pmf_ctx*
     if (!r) r = dalloc(c, &c->W, wbytes);
     if (!r) r = dalloc(c, &c->W2, wbytes);
     if (!r && c->path != PMF_PATH_RESIDENT && nx > 1) r = dalloc(c, &c->S, 2 * c->esize * (size_t)d.nspec * d.batch);
+    if (!r && c->path == PMF_PATH_PLANE && nx == 4) r = dalloc(c, &c->S2, 2 * c->esize * (size_t)d.nspec * d.batch);
     if (!r) r = dalloc(c, (void**)&c->st, sizeof(FilterState) * d.batch);
     // reduction scratch: the largest per-pass block count (pencil C2R rows / points kernels)
     size_t nblk = (size_t)d.batch * 1024;
@@ -516,7 +517,7 @@ void pmf_destroy(pmf_ctx* c) {
     if (c->sh) sh_destroy(c);
     cudaSetDevice(c->cfg.device);
     cudaStreamSynchronize(c->stream);
-    void* ptrs[] = {c->W, c->W2, c->S, c->st, c->partials, c->coef, c->sub, c->z, c->gauss, c->mom_dev,
+    void* ptrs[] = {c->W, c->W2, c->S, c->S2, c->st, c->partials, c->coef, c->sub, c->z, c->gauss, c->mom_dev,
                     c->tw[0], c->tw[1], c->tw[2], c->tw[3]};
     for (void* p : ptrs)
         if (p) cudaFree(p);

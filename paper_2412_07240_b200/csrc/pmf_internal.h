@@ -80,6 +80,7 @@ struct PencilBufs {
     void* W;             // real weights [batch][ntot]
     void* W2;            // second real buffer (regrid target)
     void* S;             // complex half spectrum [batch][nspec]
+    void* S2 = nullptr;  // second spectrum buffer (plane path, nx = 4: out-of-place strided pass)
     FilterState* st;
     double* partials;    // reduction scratch
     double* coef;        // [batch][coef_stride(l)]

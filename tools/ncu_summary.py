@@ -68,7 +68,10 @@ def main():
         p(f"    {k:24s} {v:.3f}")
     allrows = ncu_csv(a.rep, "--page", "source", "--print-source", "sass")
     starts = [i for i, r in enumerate(allrows) if r and r[0] == "Kernel Name"]
-    rows = allrows[starts[a.idx]:(starts[a.idx + 1] if a.idx + 1 < len(starts) else None)] if starts else []
+    # newer ncu prints every kernel's SASS section twice: keep one section per kernel name change
+    firsts = [i for j, i in enumerate(starts) if j == 0 or allrows[i][1] != allrows[starts[j - 1]][1]]
+    ends = {i: (starts[starts.index(i) + 1] if starts.index(i) + 1 < len(starts) else None) for i in firsts}
+    rows = allrows[firsts[a.idx]:ends[firsts[a.idx]]] if a.idx < len(firsts) else []
     if len(rows) > 2:
         hh = rows[1]
         si, ni = hh.index("Source"), hh.index("Warp Stall Sampling (All Samples)")
