@@ -493,7 +493,8 @@ __global__ void __launch_bounds__(Cfg<N>::NT, Cfg<N>::MINB) k_plane_fwd(PlaneArg
 #pragma unroll
             for (int r = 0; r < R1; ++r) z[r] = *reinterpret_cast<const V*>(stg + (t + 8 * r + 1) * SP + 2 * m + OFF);
         }
-        __syncthreads();                                      // staged plane consumed
+        if (tid < H) tma::bulk_wait_read();                   // the previous plane's X rows are out
+        __syncthreads();                                      // staged plane consumed, X free
         if (SEP) issue(p + gridDim.x);                        // overlaps the FFTs below
         if (P[PL_SKIP] != 0.0) continue;                      // uniform; the stage ring stays intact
         // ------------------------------------------------------------ P1: axis-1 FFT of the packed pair
@@ -565,13 +566,18 @@ __global__ void __launch_bounds__(Cfg<N>::NT, Cfg<N>::MINB) k_plane_fwd(PlaneArg
         }
         __syncthreads();
         if (tid == 0) a.dcpart[p] = (double)X[0].x;           // sum of the plane's input weights
-        V* Sp = a.S + (long long)p * (H * N);
-        for (int e = tid; e < H * N; e += NT) {
-            const int r = e / N, c = e - r * N;
-            __stcg(Sp + e, X[r * PITCH + c]);
+        if (tid < H) {                                        // one bulk store per spectrum row
+            tma::fence_proxy_async();
+            tma::bulk_s2g(a.S + (long long)p * (H * N) + (long long)tid * N, X + tid * PITCH,
+                          (unsigned)(N * sizeof(V)));
+            tma::bulk_commit();
         }
-        __syncthreads();
+        if (!SEP) {
+            if (tid < H) tma::bulk_wait_read();               // the staging area aliases X
+            __syncthreads();
+        }
     }
+    if (tid < H) tma::bulk_wait_all();
 }
 
 // ============================================================================ strided pass (axes >= 2)
@@ -617,7 +623,7 @@ template <typename T, int NA, int VAR>
 static size_t mid_smem(int l, int sets) {
     using C = MidCfg<T, NA, VAR>;
     return sizeof(typename C2<T>::type) * ((size_t)sets * C::NS * NA * C::PP + NA) + 16 * 4 +
-           sizeof(double2) * C::TP * l;
+           sizeof(double2) * C::TP * 3 * ((l + 1) / 2);
 }
 
 template <typename T, int NA, int MODE, int NX, int VAR>
@@ -766,9 +772,15 @@ __global__ void __launch_bounds__(MidCfg<T, NA, VAR>::NT, MidCfg<T, NA, VAR>::MI
             }
         } else {
             // ------------------------------------------------------------ s Psi / N_tot (Alg. 3-4)
+            // Euler factors f_n(kap) = gam_n + bet_n kx + alp_n kap^2 (kx = kap but 0 at the Nyquist
+            // wavenumber, R7), multiplied in pairs: f_n f_{n+1} is a quartic in kap (Horner, 4 FMA)
+            // whose per-pencil coefficients the team tabulates first. Every factor is >= 1 (D_n is
+            // PSD), so the quartic evaluation is well conditioned.
             const long long filt = o / a.ocpf;
             const double* P = a.coef + filt * a.cs;
             const double* cf = P + PL_EU;
+            const int npair = a.l >> 1, nq = (a.l + 1) >> 1;
+            double2* qt = psi + p * 3 * nq;                   // [nq][3]: (c0,c1) (c2,c3) (c4,-)
             {
                 // wavenumbers of the pencil's other axes: inner i = (j2 *) H1 N0 + k1 N0 + k0
                 double kap[3] = {0, 0, 0}, kx[3] = {0, 0, 0};
@@ -788,9 +800,10 @@ __global__ void __launch_bounds__(MidCfg<T, NA, VAR>::NT, MidCfg<T, NA, VAR>::MI
                     kap[2] = 2.0 * PMF_PI * ks2 / a.n2;
                     kx[2] = (2 * k2 == a.n2) ? 0.0 : kap[2];
                 }
-                for (int n = t; n < a.l; n += 8) {
+                auto gam_bet = [&](int n, double& g, double& bb) {
                     const double* c = cf + 10 * n;
-                    double g = 1.0, bb = 0.0;
+                    g = 1.0;
+                    bb = 0.0;
 #pragma unroll
                     for (int a2 = 0; a2 < L; ++a2) {
                         g = fma(c[a2], kap[a2] * kap[a2], g);
@@ -798,51 +811,84 @@ __global__ void __launch_bounds__(MidCfg<T, NA, VAR>::NT, MidCfg<T, NA, VAR>::MI
                         for (int b2 = a2 + 1; b2 < L; ++b2) g = fma(c[pair_index(NX, a2, b2)], kx[a2] * kx[b2], g);
                         bb = fma(c[pair_index(NX, a2, L)], kx[a2], bb);
                     }
-                    psi[p * a.l + n] = double2{g, bb};
+                };
+                for (int j = t; j < nq; j += 8) {
+                    double g0, b0, g1 = 1.0, b1 = 0.0, a1 = 0.0;
+                    gam_bet(2 * j, g0, b0);
+                    const double a0 = cf[10 * (2 * j) + L];
+                    if (2 * j + 1 < a.l) {
+                        gam_bet(2 * j + 1, g1, b1);
+                        a1 = cf[10 * (2 * j + 1) + L];
+                    }
+                    // the Nyquist wavenumber has kx = 0 in the first-order terms (R7): its pair value
+                    constexpr double kn2 = PMF_PI * PMF_PI;
+                    qt[3 * j] = double2{g0 * g1, fma(g0, b1, b0 * g1)};
+                    qt[3 * j + 1] = double2{fma(g0, a1, fma(b0, b1, a0 * g1)), fma(b0, a1, a0 * b1)};
+                    qt[3 * j + 2] = double2{a0 * a1, fma(a0, kn2, g0) * fma(a1, kn2, g1)};
                 }
             }
             __syncwarp();
-            if (s_on<R1>(t)) {
+            {
+                // Psi at k = t + 8r on all 8 threads of the team, then to the owners via the
+                // (now free) staged column
+                double kp[R1], den[R1];
+#pragma unroll
+                for (int r = 0; r < R1; ++r) {
+                    const int k = t + 8 * r;
+                    kp[r] = (2.0 * PMF_PI / NA) * (k < NA / 2 ? k : k - NA);
+                    den[r] = 1.0;
+                }
+                for (int j = 0; j < nq; ++j) {
+                    const double2 q01 = qt[3 * j], q23 = qt[3 * j + 1], q4 = qt[3 * j + 2];
+#pragma unroll
+                    for (int r = 0; r < R1; ++r) {
+                        const double x1 = kp[r];
+                        den[r] *= fma(fma(fma(fma(q4.x, x1, q23.y), x1, q23.x), x1, q01.y), x1, q01.x);
+                    }
+                }
+                if (t == ((NA / 2) & 7)) {
+                    constexpr int rn = (NA / 2) >> 3;
+                    double d = 1.0;
+                    for (int j = 0; j < nq; ++j) d *= qt[3 * j + 2].y;
+                    den[rn] = d;
+                }
                 const double mult = P[PL_SN];
-                auto mul8 = [&](V* v, int s0) {
-                    double den[8], k2[8], kxl[8];
+                double ps[R1];
+                if constexpr (R1 % 4 != 0) {
 #pragma unroll
-                    for (int q = 0; q < 8; ++q) {
-                        const int kk = s0 + R1 * q;
-                        const double kp = (2.0 * PMF_PI / NA) * (kk < NA / 2 ? kk : kk - NA);
-                        k2[q] = kp * kp;
-                        kxl[q] = (2 * kk == NA) ? 0.0 : kp;
-                        den[q] = 1.0;
-                    }
-                    for (int n = 0; n < a.l; ++n) {
-                        const double2 gb = psi[p * a.l + n];
-                        const double al = cf[10 * n + L];
+                    for (int r = 0; r < R1; ++r) ps[r] = mult / den[r];
+                } else {
+                    // one division per 4 values (prefix products), unless the product leaves range
 #pragma unroll
-                        for (int q = 0; q < 8; ++q) den[q] *= fma(al, k2[q], fma(gb.y, kxl[q], gb.x));
-                    }
-                    double pre[8];
-                    pre[0] = den[0];
+                    for (int g = 0; g < R1; g += 4) {
+                        const double p1 = den[g] * den[g + 1], p2 = p1 * den[g + 2], p3 = p2 * den[g + 3];
+                        if (p3 < 1e300) {
+                            double inv = mult / p3;
+                            ps[g + 3] = inv * p2;
+                            inv *= den[g + 3];
+                            ps[g + 2] = inv * p1;
+                            inv *= den[g + 2];
+                            ps[g + 1] = inv * den[g];
+                            ps[g] = inv * den[g + 1];
+                        } else {
 #pragma unroll
-                    for (int q = 1; q < 8; ++q) pre[q] = pre[q - 1] * den[q];
-                    if (pre[7] < 1e300) {
-                        double inv = mult / pre[7];
-#pragma unroll
-                        for (int q = 7; q > 0; --q) {
-                            const double ps = inv * pre[q - 1];
-                            inv *= den[q];
-                            v[q] = V{(T)(v[q].x * ps), (T)(v[q].y * ps)};
-                        }
-                        v[0] = V{(T)(v[0].x * inv), (T)(v[0].y * inv)};
-                    } else {
-#pragma unroll
-                        for (int q = 0; q < 8; ++q) {
-                            const double ps = mult / den[q];
-                            v[q] = V{(T)(v[q].x * ps), (T)(v[q].y * ps)};
+                            for (int q = 0; q < 4; ++q) ps[g + q] = mult / den[g + q];
                         }
                     }
-                };
-                mul8(pa, s_a<R1>(t));
-                mul8(pb, s_b<R1>(t));
+                }
+#pragma unroll
+                for (int r = 0; r < R1; ++r) reinterpret_cast<double*>(col + (t + 8 * r) * PP)[0] = ps[r];
+            }
+            __syncwarp();
+            if (s_on<R1>(t)) {
+                const int sa = s_a<R1>(t), sb = s_b<R1>(t);
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const double fa = reinterpret_cast<const double*>(col + (sa + R1 * q) * PP)[0];
+                    const double fb = reinterpret_cast<const double*>(col + (sb + R1 * q) * PP)[0];
+                    pa[q] = V{(T)(pa[q].x * fa), (T)(pa[q].y * fa)};
+                    pb[q] = V{(T)(pb[q].x * fb), (T)(pb[q].y * fb)};
+                }
             }
             team_dft_dif<R1, true>(pa, pb, x, col, tw, t, slot);
             if (valid) {
@@ -854,13 +900,141 @@ __global__ void __launch_bounds__(MidCfg<T, NA, VAR>::NT, MidCfg<T, NA, VAR>::MI
     }
 }
 
+// ============================================================================ split regrid, axes 3 -> 2 (nx = 4)
+// For filters with a split regrid map (flag 4): Y(k0, k1, u2', u3') = linear interpolation
+// along axis 2 (v2 = o2 + M22 u2' + M23 u3') of Z(j2) = (1 - w3) S(j2, j3) + w3 S(j2, j3 + 1)
+// (v3 = o3 + M33 u3'), zero ghosts (R12), then the forward DFT along axis 2, into S2.
+// Each CTA owns TP pencils (k0, k1) of one filter and walks u3' = 0..n3-1; the old slabs
+// j3 stream once through a ring of RS staged row sets (v3 is monotone in u3').
+template <typename T, int NA>
+struct SplitCfg {
+    static constexpr int TP = NA >= 128 ? 16 : 32;
+    static constexpr int PP = sizeof(T) == 8 ? TP + 1 : TP + 2;
+    static constexpr int RS = 3;
+    static constexpr int NT = 8 * TP;
+};
+template <typename T, int NA>
+static size_t split_smem() {
+    using C = SplitCfg<T, NA>;
+    return sizeof(typename C2<T>::type) * ((size_t)(C::RS + 1) * NA * C::PP + NA) + 8 * C::RS + 16;
+}
+
+template <typename T, int NA>
+__global__ void __launch_bounds__(SplitCfg<T, NA>::NT, 1) k_plane_split(MidArgs<T> a) {
+    using V = typename C2<T>::type;
+    using C = SplitCfg<T, NA>;
+    constexpr int R1 = NA / 8, TP = C::TP, PP = C::PP, RS = C::RS;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    V* ring = reinterpret_cast<V*>(smem_raw);                 // [RS][NA][PP]
+    V* scr = ring + RS * NA * PP;                             // [NA][PP] blended Z, then the exchange
+    V* tw = scr + NA * PP;
+    unsigned long long* bar = reinterpret_cast<unsigned long long*>(tw + NA);
+    const int tid = threadIdx.x, p = tid >> 3, t = tid & 7;
+    const long long tiles = (a.I + TP - 1) / TP;
+    const long long filt = blockIdx.x / tiles, i0 = (blockIdx.x - filt * tiles) * TP;
+    const double* P = a.coef + filt * a.cs;
+    if (P[PL_SKIP] != 0.0 || (int)P[PL_FLAG] != 4) return;   // uniform
+    init_tw<NA>(tw);
+    if (tid == 0)
+        for (int q = 0; q < RS; ++q) tma::mbar_init(&bar[q], 1);
+    __syncthreads();
+    const long long i = i0 + p;
+    const bool valid = i < a.I;
+    const long long cnt = a.I - i0 < TP ? a.I - i0 : TP;
+    const unsigned bytes = ((unsigned)(cnt * sizeof(V)) + 15u) & ~15u;
+    const int n3 = a.n3;
+    const double M33 = P[PL_M + 15], o3 = P[PL_O + 3], M22 = P[PL_M + 10], M23 = P[PL_M + 11], o2 = P[PL_O + 2];
+    auto row_of = [&](int u3) {                               // first old slab of output slab u3
+        const double v3 = fma(M33, (double)u3 - 0.5 * (n3 - 1), o3);
+        const double f = floor(v3);
+        const int fi = __double2int_rz(f);
+        return min(max(fi, -2), n3);
+    };
+    // rows r0, r0+1, ... are loaded in order into slot (r - r0) % RS, none skipped
+    const int r0 = max(row_of(0), 0);
+    int next = r0;
+    auto issue = [&](int r) {
+        if (tid >= NA) return;
+        const int sl = (r - r0) % RS;
+        tma::fence_proxy_async();
+        if (tid == 0) tma::mbar_expect_tx(&bar[sl], bytes * NA);
+        tma::bulk_g2s(ring + (sl * NA + tid) * PP, a.S + ((filt * n3 + r) * (long long)NA + tid) * a.I + i0, bytes,
+                      &bar[sl]);
+    };
+    auto slab = [&](int r) -> const V* { return ring + ((r - r0) % RS) * NA * PP + p; };
+    auto wait_row = [&](int r) { tma::mbar_wait(&bar[(r - r0) % RS], (unsigned)(((r - r0) / RS) & 1)); };
+    V* col = scr + p;
+    auto slot = [](int s2, int tt) { return rslot(s2, tt) * PP; };
+    for (int u3 = 0; u3 < n3; ++u3) {
+        const int ja = row_of(u3);
+        const double v3 = fma(M33, (double)u3 - 0.5 * (n3 - 1), o3);
+        const double w3 = (ja == __double2int_rz(floor(v3))) ? v3 - floor(v3) : 0.0;
+        // rows below ja are never needed again: their slots take the rows ahead
+        const int lim = min(max(ja, r0) + RS, n3);
+        while (next < lim) issue(next++);
+        const bool va = ja >= 0 && ja < n3, vb = ja + 1 >= 0 && ja + 1 < n3;
+        if (va) wait_row(ja);
+        if (vb) wait_row(ja + 1);
+#pragma unroll
+        for (int r = 0; r < R1; ++r) {
+            const int j2 = t + 8 * r;
+            double zx = 0.0, zy = 0.0;
+            if (va) {
+                const V v = slab(ja)[j2 * PP];
+                zx = (1.0 - w3) * (double)v.x;
+                zy = (1.0 - w3) * (double)v.y;
+            }
+            if (vb) {
+                const V v = slab(ja + 1)[j2 * PP];
+                zx = fma(w3, (double)v.x, zx);
+                zy = fma(w3, (double)v.y, zy);
+            }
+            col[j2 * PP] = V{(T)zx, (T)zy};
+        }
+        __syncwarp();
+        const double vb2 = fma(M23, (double)u3 - 0.5 * (n3 - 1), o2);
+        V x[R1], pa[8], pb[8];
+        double dcs = 0.0;
+#pragma unroll
+        for (int r = 0; r < R1; ++r) {
+            const double v2 = fma(M22, (t + 8 * r) - 0.5 * (NA - 1), vb2);
+            const double f = floor(v2);
+            const int fi = __double2int_rz(f);
+            const double fr = v2 - f;
+            const V lo = (fi >= 0 && fi < NA) ? col[fi * PP] : V{T(0), T(0)};
+            const V hi = (fi + 1 >= 0 && fi + 1 < NA) ? col[(fi + 1) * PP] : V{T(0), T(0)};
+            x[r] = V{(T)fma(fr, (double)hi.x - (double)lo.x, (double)lo.x),
+                     (T)fma(fr, (double)hi.y - (double)lo.y, (double)lo.y)};
+            dcs += (double)x[r].x;
+        }
+        if (i == 0) {      // pencil k0 = k1 = 0: sum of this slab's regridded weights
+            const unsigned tm = 0xFFu << ((tid & 31) & ~7);
+            dcs += __shfl_xor_sync(tm, dcs, 1);
+            dcs += __shfl_xor_sync(tm, dcs, 2);
+            dcs += __shfl_xor_sync(tm, dcs, 4);
+            if (t == 0) a.dc3[filt * n3 + u3] = dcs;
+        }
+        team_dft<R1, false>(x, pa, pb, col, tw, t, slot);
+        if (valid && s_on<R1>(t)) {
+            V* base = a.Sout + (filt * n3 + u3) * (long long)NA * a.I + i;
+            const int sa = s_a<R1>(t), sb = s_b<R1>(t);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                __stcg(base + (long long)(sa + R1 * q) * a.I, pa[q]);
+                __stcg(base + (long long)(sb + R1 * q) * a.I, pb[q]);
+            }
+        }
+        __syncthreads();                  // ring slots below the next ja may be refilled
+    }
+}
+
 // ============================================================================ inverse plane pass (+ update)
 template <typename T, int N>
 __host__ __device__ constexpr bool inv_dbl() { return 2 * xbytes<T, N>() <= 200 * 1024; }
 template <typename T, int N>
 static size_t inv_smem() {
-    return (inv_dbl<T, N>() ? 2 : 1) * xbytes<T, N>() + 2 * sizeof(T) * N + sizeof(double) * 6 * (Cfg<N>::NT / 32) +
-           16;
+    return (inv_dbl<T, N>() ? 2 : 1) * xbytes<T, N>() + 2 * sizeof(T) * N +
+           sizeof(double) * NMOM * (Cfg<N>::NT / 32) + 16 + sizeof(double) * NMOM * Cfg<N>::NT;
 }
 
 // The plane's spectrum rows are staged by H bulk copies; with two buffers (N <= 96)
@@ -874,8 +1048,8 @@ __global__ void __launch_bounds__(Cfg<N>::NT, Cfg<N>::MINB) k_plane_inv(PlaneArg
     extern __shared__ __align__(16) unsigned char smem_raw[];
     V* X0 = reinterpret_cast<V*>(smem_raw);
     V* tw = X0 + (DBL ? 2 : 1) * H * PITCH;
-    double* red = reinterpret_cast<double*>(tw + N);          // [NW][6]
-    unsigned long long* bar = reinterpret_cast<unsigned long long*>(red + 6 * NW);
+    double* red = reinterpret_cast<double*>(tw + N);          // [NW][NMOM]
+    unsigned long long* bar = reinterpret_cast<unsigned long long*>(red + NMOM * NW);
     const int tid = threadIdx.x, m = tid >> 3, t = tid & 7, lane = tid & 31, warp = tid >> 5;
     init_tw<N>(tw);
     if (tid == 0) {
@@ -884,6 +1058,30 @@ __global__ void __launch_bounds__(Cfg<N>::NT, Cfg<N>::MINB) k_plane_inv(PlaneArg
     }
     const long long ntot = (long long)N * N * a.n2 * a.n3;
     __syncthreads();
+    constexpr int NM = 1 + NX + NX * (NX + 1) / 2;           // moment sums of a filter
+    double* mom = reinterpret_cast<double*>(bar + 2) + tid;  // this thread's sums, stride NT (shared)
+#pragma unroll
+    for (int q = 0; q < NM; ++q) mom[q * NT] = 0.0;
+    int curf = -1;
+    // one CTA reduction per (filter, CTA): fixed order (warp tree, then warps in order)
+    auto flush = [&]() {
+        if (curf < 0) return;
+#pragma unroll
+        for (int q = 0; q < NM; ++q) {
+            double v = mom[q * NT];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+            if (lane == 0) red[warp * NM + q] = v;
+            mom[q * NT] = 0.0;
+        }
+        __syncthreads();
+        if (tid < NM) {
+            double v = 0.0;
+            for (int w = 0; w < NW; ++w) v += red[w * NM + tid];
+            a.part[((long long)curf * gridDim.x + blockIdx.x) * NMOM + tid] = v;
+        }
+        __syncthreads();
+    };
     auto issue = [&](int p, int buf) {
         if (p >= a.nplanes || tid >= H) return;
         tma::fence_proxy_async();
@@ -900,6 +1098,10 @@ __global__ void __launch_bounds__(Cfg<N>::NT, Cfg<N>::MINB) k_plane_inv(PlaneArg
         tma::mbar_wait(&bar[buf], (unsigned)(DBL ? ((k >> 1) & 1) : (k & 1)));
         V* X = X0 + buf * H * PITCH;
         const int filt = p / a.ppf, pl = p - filt * a.ppf;
+        if (UP && filt != curf) {                             // uniform
+            flush();
+            curf = filt;
+        }
         const double* P = a.coef + (long long)filt * a.cs;
         if (P[PL_SKIP] != 0.0) {
             __syncthreads();
@@ -1071,41 +1273,42 @@ __global__ void __launch_bounds__(Cfg<N>::NT, Cfg<N>::MINB) k_plane_inv(PlaneArg
                 *reinterpret_cast<V*>(Wp + (long long)(t + 8 * r) * N + 2 * m) = V{o[0], o[1]};
             }
         }
-        double acc[6];
         {
+            // this thread's two columns of the plane -> the filter's index-space moment sums
+            // (R14): u0 fixed per column, u1 = t + 8r - (N-1)/2, u2, u3 fixed per plane
             const double ua = (2 * m) - 0.5 * (N - 1), ub = ua + 1.0;
-            acc[0] = S[0] + S[1];
-            acc[1] = fma(ua, S[0], ub * S[1]);
-            acc[2] = Tm[0] + Tm[1];
-            acc[3] = fma(ua * ua, S[0], ub * ub * S[1]);
-            acc[4] = fma(ua, Tm[0], ub * Tm[1]);
-            acc[5] = U[0] + U[1];
-        }
+            const double s0 = S[0] + S[1], su0 = fma(ua, S[0], ub * S[1]), st = Tm[0] + Tm[1];
+            const double m1[4] = {su0, st, u2 * s0, u3 * s0};
+            mom[0] += s0;
 #pragma unroll
-        for (int i = 0; i < 6; ++i) {
-            double v = acc[i];
+            for (int a2 = 0; a2 < NX; ++a2) mom[(1 + a2) * NT] += m1[a2];
+            int kk = 1 + NX;
+            const double uu[4] = {0.0, 0.0, u2, u3};
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
-            acc[i] = v;
-        }
-        if (lane == 0)
+            for (int a2 = 0; a2 < NX; ++a2)
 #pragma unroll
-            for (int i = 0; i < 6; ++i) red[warp * 6 + i] = acc[i];
-        __syncthreads();
-        if (tid < 6) {
-            double v = 0.0;
-            for (int w = 0; w < NW; ++w) v += red[w * 6 + tid];
-            a.part[(long long)p * 6 + tid] = v;
+                for (int b2 = a2; b2 < NX; ++b2) {
+                    double v;
+                    if (a2 >= 2) v = uu[a2] * uu[b2] * s0;
+                    else if (b2 >= 2) v = uu[b2] * m1[a2];
+                    else if (a2 == 0 && b2 == 0) v = fma(ua * ua, S[0], ub * ub * S[1]);
+                    else if (a2 == 0) v = fma(ua, Tm[0], ub * Tm[1]);
+                    else v = U[0] + U[1];
+                    mom[(kk++) * NT] += v;
+                }
         }
-        __syncthreads();
+        __syncthreads();                  // X is consumed
     }
+    if (UP) flush();
+    (void)lane;
+    (void)warp;
 }
 
 // ============================================================================ finalise (one block per filter)
 template <int NX>
 __global__ void k_plane_fin(FilterState* st, const double* __restrict__ coef, int cs, const double* __restrict__ dcpart,
-                            const double* __restrict__ dc3, const double* __restrict__ part, int ppf, int n2, int n3,
-                            int update) {
+                            const double* __restrict__ dc3, const double* __restrict__ part, int ppf, int n3,
+                            int ginv, int update) {
     __shared__ double red[32 * 16];
     const int filt = blockIdx.x;
     const double* P = coef + (long long)filt * cs;
@@ -1115,35 +1318,15 @@ __global__ void k_plane_fin(FilterState* st, const double* __restrict__ coef, in
 #pragma unroll
     for (int i = 0; i < 16; ++i) acc[i] = 0.0;
     for (int pl = threadIdx.x; pl < ppf; pl += blockDim.x) {
-        const long long p = (long long)filt * ppf + pl;
-        if (!split) acc[15] += dcpart[p];
+        if (!split) acc[15] += dcpart[(long long)filt * ppf + pl];
         else if (pl < n3) acc[15] += dc3[(long long)filt * n3 + pl];
-        if (!update) continue;
-        const double* pp = part + p * 6;
-        int j2, j3;
-        plane_j(pl, n2, j2, j3);
-        const double u[4] = {0.0, 0.0, j2 - 0.5 * (n2 - 1), j3 - 0.5 * (n3 - 1)};
-        const double S = pp[0];
-        double m1[4];
-        m1[0] = pp[1];
-        m1[1] = pp[2];
-#pragma unroll
-        for (int a2 = 2; a2 < NX; ++a2) m1[a2] = u[a2] * S;
-        acc[0] += S;
-#pragma unroll
-        for (int a2 = 0; a2 < NX; ++a2) acc[1 + a2] += m1[a2];
-        int k = 1 + NX;
-#pragma unroll
-        for (int a2 = 0; a2 < NX; ++a2)
-#pragma unroll
-            for (int b2 = a2; b2 < NX; ++b2) {
-                double v;
-                if (a2 >= 2) v = u[a2] * u[b2] * S;
-                else if (b2 >= 2) v = u[b2] * m1[a2];
-                else v = (a2 == 0 && b2 == 0) ? pp[3] : (a2 == 0) ? pp[4] : pp[5];
-                acc[k++] += v;
-            }
     }
+    if (update)
+        for (int c = threadIdx.x; c < ginv; c += blockDim.x) {
+            const double* pp = part + ((long long)filt * ginv + c) * NMOM;
+#pragma unroll
+            for (int i = 0; i < NMOM; ++i) acc[i] += pp[i];
+        }
     block_sum<16>(acc, red);
     if (threadIdx.x != 0) return;
     FilterState& f = st[filt];
@@ -1258,6 +1441,40 @@ static cudaError_t mid_pass(MidArgs<T> ma, int na, int mode, cudaStream_t s) {
     }
 }
 
+template <typename T, int NA>
+static cudaError_t split_na(MidArgs<T> ma, long long nblk, cudaStream_t s) {
+    const size_t smem = split_smem<T, NA>();
+    cudaError_t e = cudaFuncSetAttribute(k_plane_split<T, NA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    k_plane_split<T, NA><<<(unsigned)nblk, SplitCfg<T, NA>::NT, smem, s>>>(ma);
+    return cudaGetLastError();
+}
+
+template <typename T>
+static cudaError_t split_pass(const Dims& d, PencilBufs& b, int cs, typename C2<T>::type* S,
+                              typename C2<T>::type* S2, double* dc3, int l, cudaStream_t s, int64_t* launches) {
+    MidArgs<T> ma{};
+    ma.S = S;
+    ma.Sout = S2;
+    ma.coef = b.coef;
+    ma.cs = cs;
+    ma.I = (long long)(d.n[1] / 2 + 1) * d.n[0];
+    ma.n2 = d.n[2];
+    ma.n3 = d.n[3];
+    ma.l = l;
+    ma.dc3 = dc3;
+    ++*launches;
+    auto nblk = [&](int tp) { return ((ma.I + tp - 1) / tp) * d.batch; };
+    switch (d.n[2]) {
+        case 16: return split_na<T, 16>(ma, nblk(SplitCfg<T, 16>::TP), s);
+        case 32: return split_na<T, 32>(ma, nblk(SplitCfg<T, 32>::TP), s);
+        case 64: return split_na<T, 64>(ma, nblk(SplitCfg<T, 64>::TP), s);
+        case 96: return split_na<T, 96>(ma, nblk(SplitCfg<T, 96>::TP), s);
+        case 128: return split_na<T, 128>(ma, nblk(SplitCfg<T, 128>::TP), s);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
 template <typename T, int N, int NX>
 static cudaError_t plane_t(const Dims& d, PencilBufs& b, const ModelParams& mp, const LikParams* lp, double ks,
                            cudaStream_t s, int64_t* launches) {
@@ -1284,9 +1501,9 @@ static cudaError_t plane_t(const Dims& d, PencilBufs& b, const ModelParams& mp, 
     pa.cs = cs;
     pa.ppf = ppf;
     pa.nplanes = ppf * d.batch;
-    pa.dcpart = b.partials;
-    pa.part = b.partials + pa.nplanes;
-    pa.dc3 = b.partials + 7LL * pa.nplanes;
+    pa.dcpart = b.partials;                                   // [nplanes]
+    pa.dc3 = b.partials + pa.nplanes;                         // [batch][n3]
+    pa.part = pa.dc3 + (long long)d.batch * n3;               // [batch][inverse CTAs][NMOM]
     pa.n2 = n2;
     pa.n3 = n3;
     pa.l = mp.l;
@@ -1341,18 +1558,21 @@ static cudaError_t plane_t(const Dims& d, PencilBufs& b, const ModelParams& mp, 
     };
     if (NX == 4) {
         if ((e = mid(2, 0, S, S2, rg ? 1 : 0)) != cudaSuccess) return e;
-        if (rg && (e = mid(2, 3, S, S2, 0)) != cudaSuccess) return e;
+        if (rg && (e = split_pass<T>(d, b, cs, S, S2, pa.dc3, mp.l, s, launches)) != cudaSuccess) return e;
     }
     if (b.ev0) cudaEventRecord(b.ev0, s);
     if ((e = mid(NX - 1, 2, S2, S2, 0)) != cudaSuccess) return e;
     if (b.ev1) cudaEventRecord(b.ev1, s);
     if (NX == 4 && (e = mid(2, 1, S2, S2, 0)) != cudaSuccess) return e;
     // inverse plane pass (+ update)
+    int ginv = 1;
     {
         const size_t smem = inv_smem<T, N>();
-        int grid = 1;
+        int& grid = ginv;
         if (lp) {
             e = occ_grid(k_plane_inv<T, N, NX, true>, Cf::NT, smem, pa.nplanes, &grid);
+            if (e == cudaSuccess && d.batch > 1)
+                e = cudaMemsetAsync(pa.part, 0, sizeof(double) * NMOM * grid * (size_t)d.batch, s);
             if (e == cudaSuccess) k_plane_inv<T, N, NX, true><<<grid, Cf::NT, smem, s>>>(pa);
         } else {
             e = occ_grid(k_plane_inv<T, N, NX, false>, Cf::NT, smem, pa.nplanes, &grid);
@@ -1362,7 +1582,8 @@ static cudaError_t plane_t(const Dims& d, PencilBufs& b, const ModelParams& mp, 
         ++*launches;
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
-    k_plane_fin<NX><<<d.batch, 256, 0, s>>>(b.st, b.coef, cs, pa.dcpart, pa.dc3, pa.part, ppf, n2, n3, lp ? 1 : 0);
+    k_plane_fin<NX><<<d.batch, 256, 0, s>>>(b.st, b.coef, cs, pa.dcpart, pa.dc3, pa.part, ppf, n3, ginv,
+                                            lp ? 1 : 0);
     ++*launches;
     return cudaGetLastError();
 }
@@ -1392,7 +1613,7 @@ cudaError_t launch_plane(const Dims& d, int dtype, PencilBufs& b, const ModelPar
 size_t plane_partials_doubles(const Dims& d) {
     long long ppf = 1;
     for (int m = 2; m < d.nx; ++m) ppf *= d.n[m];
-    return (size_t)((7 * ppf + d.n[3]) * d.batch);
+    return (size_t)((ppf + d.n[3] + 1024 * NMOM) * d.batch);
 }
 
 }  // namespace pmf
