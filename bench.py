@@ -177,36 +177,12 @@ def run_reference(args):
     return 0
 
 
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
-    ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--workload", default="C5", choices=sorted(WORKLOADS))
-    ap.add_argument("--impl", default="cuda", choices=["cuda", "reference"])
-    ap.add_argument("--l", type=int, default=None, help="override Euler substeps")
-    ap.add_argument("--path", type=int, default=0, help="0 auto, 1 pencil, 2 resident")
-    ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--no-time-update", action="store_true")
-    ap.add_argument("--virtual-ranks", type=int, default=1,
-                    help="split one filter into this many slabs on one GPU (exercises the sharded path)")
-    ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--cpu-budget", type=float, default=15.0)
-    ap.add_argument("--ref-budget", type=float, default=8.0)
-    ap.add_argument("--json-out", default=None)
-    args = ap.parse_args()
-    if args.impl == "reference":
-        return run_reference(args)
-
+def run_workload(args, workload, rank, world, local, secondary=False):
+    """One bench measurement of `workload`; returns the JSON-line dict (rank 0 prints it)."""
     import torch
     import torch.distributed as dist
     from paper_2412_07240_b200 import pmf
-
-    rank, world, local = dist_env()
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    wl = WORKLOADS[args.workload]
+    wl = WORKLOADS[workload]
     cfg = make_config(wl["cid"], **wl["over"])
     if args.l:
         cfg = cfg.replace(l=args.l)
@@ -341,18 +317,27 @@ def main():
     # average duration comes from CUDA events the library records around it on its stream.
     hbm, hbm_src, sm_max = peaks()
     esize = 8 if dtype == "f64" else 4
-    alg_bytes = 2 * esize * points_step
     kern_ms = kern_total_ms / max(kern_n, 1)
+    tname = "double" if dtype == "f64" else "float"
     if f.path == pmf.PATH_RESIDENT:
-        kname = f"k_resident_epoch<{'double' if dtype == 'f64' else 'float'}, 1, 1>"
+        # the fused epoch kernel: read + write every weight once
+        kname = f"k_resident_epoch<{tname}, 1, 1>"
+        alg_bytes, per = 2 * esize * points_step, f"{2 * esize} B per grid point"
+    elif f.path == pmf.PATH_PLANE:
+        # the last-axis pass (forward DFT x s Psi x inverse DFT, Alg. 3-5): read + write the
+        # half spectrum once, nspec = (N1/2+1) N0 N2 (N3) complex points per filter
+        nspec = cfg.batch * cfg.points // cfg.n[1] * (cfg.n[1] // 2 + 1)
+        kname = f"k_plane_mid<{tname}, {cfg.n[-1]}, 2, {cfg.nx}, {1 if cfg.n[-1] == 96 else 3}>"
+        alg_bytes, per = 2 * 2 * esize * nspec, f"{4 * esize} B per half-spectrum point"
     else:
         kname = "pencil predict (prep .. finalize)"
+        alg_bytes, per = 2 * esize * points_step, f"{2 * esize} B per grid point (whole predict)"
     km = kernel_metrics(kname)
     achieved = alg_bytes / (kern_ms * 1e-3) / 1e9
     roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
             "traffic": km.get("dram_bytes"), "kernel": kname, "kernel_ms": kern_ms, "timed_launches": kern_n,
             "share_of_step": kern_ms / ms_step, "peak_source": hbm_src, "alg_bytes_per_launch": alg_bytes,
-            "alg_bytes_per_point": 2 * esize,
+            "alg_bytes_per_unit": per,
             "fp64_pipe_frac_ncu": (km["fp64_pipe_pct"] / 100.0) if "fp64_pipe_pct" in km else None,
             "ncu_source": km.get("source")}
     cpu = None
@@ -366,22 +351,73 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "strong" if sharded else "weak",
             "vs_baseline": None, "dtype": dtype, "data": "synthetic",
-            "config": {"workload": f"{args.workload}: {cfg.batch} x {'x'.join(map(str, cfg.n))} {cfg.nx}-D CV filters "
+            "config": {"workload": f"{workload}: {cfg.batch} x {'x'.join(map(str, cfg.n))} {cfg.nx}-D CV filters "
                                    f"per GPU, l={cfg.l}, tau={cfg.tau}, k_sigma={cfg.k_sigma}",
                        "step": "regrid + predict (Alg. 1-6) + update + moments, every filter",
-                       "l2": f"inputs larger than L2 ({alg_bytes / 2 / 1e6:.0f} MB of weights per GPU)",
-                       "path": "resident" if f.path == pmf.PATH_RESIDENT else "pencil",
+                       "l2": (f"inputs larger than L2 ({esize * points_step / 1e6:.0f} MB of weights per GPU)"
+                              if esize * points_step > 126e6 else
+                              f"weights ({esize * points_step / 1e6:.0f} MB) fit in the 126 MB L2: L2-resident workload"),
+                       "path": {pmf.PATH_RESIDENT: "resident", pmf.PATH_PLANE: "plane"}.get(f.path, "pencil"),
                        "parallelism": (f"slab-sharded x{world if world > 1 else args.virtual_ranks} along the last "
                                        "axis (2 all-to-all per predict, all-reduce per update)" if sharded
                                        else f"filter-sharded x{world} (no data-path collective)")},
             "e2e": e2e, "gpu_launches": launches, "roofline": roof, "cpu_baseline": cpu, "clocks": clk,
             "time_update": tu}
+    f.close()
+    return line
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--workload", default="C5", choices=sorted(WORKLOADS))
+    ap.add_argument("--impl", default="cuda", choices=["cuda", "reference"])
+    ap.add_argument("--l", type=int, default=None, help="override Euler substeps")
+    ap.add_argument("--path", type=int, default=0, help="0 auto, 1 pencil, 2 resident, 3 plane")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-time-update", action="store_true")
+    ap.add_argument("--virtual-ranks", type=int, default=1,
+                    help="split one filter into this many slabs on one GPU (exercises the sharded path)")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--ref-budget", type=float, default=8.0)
+    ap.add_argument("--json-out", default=None)
+    ap.add_argument("--also", default="auto",
+                    help="comma list of further workloads measured compactly into the line's 'also' (N=1); "
+                         "auto: C4,C3 with the default C5 workload")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+    from paper_2412_07240_b200 import pmf
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    line = run_workload(args, args.workload, rank, world, local)
+    also_list = ("C4,C3" if args.workload == "C5" else "") if args.also == "auto" else args.also
+    if also_list and world == 1:
+        # the other large single-GPU configurations, measured the same way (compact)
+        also = {}
+        for w in also_list.split(","):
+            sub = argparse.Namespace(**{**vars(args), "steps": max(5, min(args.steps, 10)), "warmup": 3,
+                                        "no_e2e": True, "no_cpu": True, "path": 0, "virtual_ranks": 1})
+            r = run_workload(sub, w, rank, world, local, secondary=True)
+            also[w] = {k: r[k] for k in ("value", "unit", "ms_per_step", "dtype")}
+            also[w].update(workload=r["config"]["workload"], path=r["config"]["path"],
+                           roofline=r["roofline"], time_update=r["time_update"], gpu_launches=r["gpu_launches"],
+                           clocks=r["clocks"])
+        line["also"] = also
     if rank == 0:
         print(json.dumps(line), flush=True)
         if args.json_out:
             with open(args.json_out, "w") as fh:
                 json.dump(line, fh, indent=1)
-    f.close()
     if world > 1:
         dist.destroy_process_group()
     return 0

@@ -668,10 +668,10 @@ __global__ void __launch_bounds__(MidCfg<T, NA, VAR>::NT, MidCfg<T, NA, VAR>::MI
     // tiles of inactive filters are neither staged nor waited for (their stage's phase is not used)
     auto issue = [&](long long blk, int st) {
         if (blk >= ntile || tid >= NA) return;
-        const long long o = blk / tiles, i0 = (blk - o * tiles) * TP;
+        const long long o = (unsigned)blk / (unsigned)tiles, i0 = ((unsigned)blk - (unsigned)o * (unsigned)tiles) * TP;
         const long long cnt = a.I - i0 < TP ? a.I - i0 : TP;
         const unsigned bytes = ((unsigned)(cnt * sizeof(V)) + 15u) & ~15u;
-        const long long filt = o / a.ocpf;
+        const long long filt = (unsigned)o / (unsigned)a.ocpf;
         if (!active(filt)) return;
         tma::fence_proxy_async();
         if (MODE == 3) {
@@ -691,6 +691,11 @@ __global__ void __launch_bounds__(MidCfg<T, NA, VAR>::NT, MidCfg<T, NA, VAR>::MI
         if (tid == 0) tma::mbar_expect_tx(&bar[st], bytes * NA);
         tma::bulk_g2s(stg + (st * NA + tid) * PP, a.S + (o * NA + tid) * a.I + i0, bytes, &bar[st]);
     };
+    if (MODE == 0 && a.skip4 && a.O / a.ocpf <= 64) {         // every filter left to the split pass: done
+        bool any = false;
+        for (long long f = 0; f < a.O / a.ocpf && !any; ++f) any = active(f);
+        if (!any) return;
+    }
 #pragma unroll
     for (int j = 0; j < NS - 1; ++j) issue(blockIdx.x + (long long)j * gridDim.x, j);
     auto slot = [](int s2, int tt) { return rslot(s2, tt) * PP; };
@@ -699,10 +704,10 @@ __global__ void __launch_bounds__(MidCfg<T, NA, VAR>::NT, MidCfg<T, NA, VAR>::MI
     for (long long blk = blockIdx.x; blk < ntile; blk += gridDim.x, ++k) {
         const int st = k % NS;
         issue(blk + (long long)(NS - 1) * gridDim.x, (k + NS - 1) % NS);
-        const long long o = blk / tiles;
-        const long long i = (blk - o * tiles) * TP + p;
+        const long long o = (unsigned)blk / (unsigned)tiles;   // 32-bit: ntile < 2^31
+        const long long i = ((unsigned)blk - (unsigned)o * (unsigned)tiles) * TP + p;
         const bool valid = i < a.I;
-        const long long filt = o / a.ocpf;
+        const long long filt = (unsigned)o / (unsigned)a.ocpf;
         if (!active(filt)) continue;                          // uniform; nothing was staged
         tma::mbar_wait(&bar[st], (phase >> st) & 1u);
         phase ^= 1u << st;
@@ -776,7 +781,6 @@ __global__ void __launch_bounds__(MidCfg<T, NA, VAR>::NT, MidCfg<T, NA, VAR>::MI
             // wavenumber, R7), multiplied in pairs: f_n f_{n+1} is a quartic in kap (Horner, 4 FMA)
             // whose per-pencil coefficients the team tabulates first. Every factor is >= 1 (D_n is
             // PSD), so the quartic evaluation is well conditioned.
-            const long long filt = o / a.ocpf;
             const double* P = a.coef + filt * a.cs;
             const double* cf = P + PL_EU;
             const int npair = a.l >> 1, nq = (a.l + 1) >> 1;
@@ -785,10 +789,11 @@ __global__ void __launch_bounds__(MidCfg<T, NA, VAR>::NT, MidCfg<T, NA, VAR>::MI
                 // wavenumbers of the pencil's other axes: inner i = (j2 *) H1 N0 + k1 N0 + k0
                 double kap[3] = {0, 0, 0}, kx[3] = {0, 0, 0};
                 const long long ii = valid ? i : 0;
-                const int k0 = (int)(ii % a.N0);
-                const long long r1 = ii / a.N0;
-                const int k1 = (int)(r1 % a.H1);
-                const int k2 = (int)(r1 / a.H1);
+                const unsigned r1 = (unsigned)ii / (unsigned)a.N0;      // I < 2^31
+                const int k0 = (int)((unsigned)ii - r1 * (unsigned)a.N0);
+                const unsigned r2 = r1 / (unsigned)a.H1;
+                const int k1 = (int)(r1 - r2 * (unsigned)a.H1);
+                const int k2 = (int)r2;
                 const int N1 = 2 * (a.H1 - 1);
                 const int ks0 = k0 < a.N0 / 2 ? k0 : k0 - a.N0;
                 kap[0] = 2.0 * PMF_PI * ks0 / a.N0;
@@ -931,7 +936,7 @@ __global__ void __launch_bounds__(SplitCfg<T, NA>::NT, 1) k_plane_split(MidArgs<
     unsigned long long* bar = reinterpret_cast<unsigned long long*>(tw + NA);
     const int tid = threadIdx.x, p = tid >> 3, t = tid & 7;
     const long long tiles = (a.I + TP - 1) / TP;
-    const long long filt = blockIdx.x / tiles, i0 = (blockIdx.x - filt * tiles) * TP;
+    const long long filt = blockIdx.x / (unsigned)tiles, i0 = (blockIdx.x - (unsigned)filt * (unsigned)tiles) * TP;
     const double* P = a.coef + filt * a.cs;
     if (P[PL_SKIP] != 0.0 || (int)P[PL_FLAG] != 4) return;   // uniform
     init_tw<NA>(tw);

@@ -14,10 +14,11 @@ ap = argparse.ArgumentParser()
 ap.add_argument("rep")
 ap.add_argument("--name", required=True)
 ap.add_argument("--source", default=None)
+ap.add_argument("--idx", type=int, default=0, help="which profiled launch in the report")
 a = ap.parse_args()
 out = subprocess.run(["ncu", "-i", a.rep, "--csv", "--page", "raw"], capture_output=True, text=True).stdout
 r = list(csv.reader(io.StringIO(out)))
-h, u, v = r[0], r[1], r[2]
+h, u, v = r[0], r[1], r[2 + a.idx]
 d = dict(zip(h, v))
 unit = dict(zip(h, u))
 
