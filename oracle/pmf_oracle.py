@@ -39,6 +39,7 @@ TRACE_SIGN_PHYSICAL = -1   # R5: s = (1 - dt tr A)^l  (eq:easyFPE P:92, b_t P:16
 TRACE_SIGN_PRINTED = +1    # Alg. 4 as printed: (1 + dt tr A)^l
 DIFF_FULL = 0              # R3: D_n = B_n^{-1} Q B_n^{-T} with cross terms
 DIFF_AXIS_LITERAL = 1      # Alg. 2/3 literally: per-axis L^(m), no cross terms
+DIFF_FDM = 2               # NEXT-1: the paper's FDM baseline (eq:FDM), in its FST form (eq:FST)
 
 
 class NoSupportError(RuntimeError):
@@ -287,9 +288,114 @@ def predict_unnormalised(w, c, B, A, Q, tau, l, diff_mode=DIFF_FULL,
 
 def predict(w, c, B, A, Q, tau, l, diff_mode=DIFF_FULL, trace_sign=TRACE_SIGN_PHYSICAL):
     """Alg. 1-6: the unnormalised update followed by normalisation by explicit
-    summation on the moved grid (Alg. 6, R9). Returns (w, c_l, B_l)."""
-    wu, cl, Bl = predict_unnormalised(w, c, B, A, Q, tau, l, diff_mode, trace_sign)
+    summation on the moved grid (Alg. 6, R9). Returns (w, c_l, B_l).
+    diff_mode DIFF_FDM: the FDM baseline in its FST form (eq:FST), same normalisation."""
+    if diff_mode == DIFF_FDM:
+        wu, cl, Bl = fst_predict_unnormalised(w, c, B, A, Q, tau, l, trace_sign)
+    else:
+        wu, cl, Bl = predict_unnormalised(w, c, B, A, Q, tau, l, diff_mode, trace_sign)
     return normalise(wu, Bl), cl, Bl
+
+
+# ----------------------------------------------------------------------------
+# NEXT-1 baseline: explicit finite differences (eq:FDM P:144-150) and their
+# eigenvalue / fast-sine-transform form (eq:fdiff P:158-164, eq:FKEnumSol P:167-170,
+# P:178-196, eq:FST P:199-202). Readings (DESIGN.md §3): R23 l factors (n = 0..l-1,
+# as R4) although eq:FKEnumSol prints l+1; R24 zero Dirichlet boundary (F_diff is the
+# finite tridiagonal matrix, rows truncated at the grid edge); R25 multi-D = one
+# central difference per axis with that axis's spacing delta_m = ||B_n[:, m]|| and
+# Q_mm (P:150), the trace term (1 - dt tr A) per step (b_t P:164, physical sign R5).
+# ----------------------------------------------------------------------------
+def fdm_axis_spacing(Bn) -> np.ndarray:
+    """delta_m of the moving grid: length of B_n's m-th column (1-D: delta_n =
+    e^{A dt} delta_{n-1})."""
+    return np.linalg.norm(np.asarray(Bn, dtype=np.float64), axis=0)
+
+
+def fdm_matrix(N: int, a: float, b: float) -> np.ndarray:
+    """F_diff (eq:fdiff P:158-162): tridiagonal Toeplitz, b on the diagonal, a on
+    both off-diagonals, zero Dirichlet boundary (R24). Pinned by the closed-form
+    eigenvalues and by fst == fdm."""
+    return b * np.eye(N) + a * (np.eye(N, k=1) + np.eye(N, k=-1))
+
+
+def fdm_step_coeffs(Bn, A, Q, dt, sign: int = TRACE_SIGN_PHYSICAL):
+    """Per axis a_m = Q_mm dt / (2 delta_m^2) and the diagonal b =
+    1 + sign dt tr(A) - sum_m 2 a_m (b_t P:164; R5, R25)."""
+    delta = fdm_axis_spacing(Bn)
+    a = np.diag(np.asarray(Q, dtype=np.float64)) * dt / (2.0 * delta ** 2)
+    b = 1.0 + sign * dt * float(np.trace(np.asarray(A))) - 2.0 * float(np.sum(a))
+    return a, b
+
+
+def fdm_predict_unnormalised(w, c, B, A, Q, tau, l, trace_sign=TRACE_SIGN_PHYSICAL):
+    """eq:FDM literally: l explicit steps P_{n+1} = F_n P_n with the central
+    difference along every axis,
+        F_n P = b_n P + sum_m a_{m,n} (P shifted +1 along m + P shifted -1 along m),
+    zero outside the grid (R24), coefficients on the grid at the start of step n,
+    B_n = e^{A n dt} B (R23). Each shift-sum is the dense off-diagonal part of F_diff
+    applied along axis m. The grid moves with the drift (eq:gridMov P:142)."""
+    w = np.asarray(w, dtype=np.float64)
+    n = w.shape
+    dt = tau / l
+    P = w.copy()
+    for s_ in range(l):
+        Bn = expm(np.asarray(A) * (s_ * dt)) @ B
+        a, b = fdm_step_coeffs(Bn, A, Q, dt, trace_sign)
+        out = b * P
+        for m in range(len(n)):
+            off = fdm_matrix(n[m], 1.0, 0.0)                  # the a-pattern of F_diff, unit weight
+            out = out + a[m] * np.moveaxis(np.tensordot(off, np.moveaxis(P, m, 0), axes=(1, 0)), 0, m)
+        P = out
+    M = expm(np.asarray(A) * tau)
+    return P, M @ np.asarray(c), M @ np.asarray(B)
+
+
+def dst1_matrix(N: int) -> np.ndarray:
+    """Eigenvector matrix R of F_diff, R[j, i] = sin((i+1)(j+1) pi/(N+1)) (P:187-190);
+    R^{-1} = 2/(N+1) R. Pinned by the orthogonality test."""
+    j = np.arange(1, N + 1)
+    return np.sin(np.outer(j, j) * math.pi / (N + 1))
+
+
+def fdm_eigenvalues(N: int, a: float, b: float) -> np.ndarray:
+    """lambda^{(j-1)} = b + 2a cos(j pi/(N+1)), j = 1..N. Pinned against a
+    library eigensolver."""
+    j = np.arange(1, N + 1)
+    return b + 2.0 * a * np.cos(j * math.pi / (N + 1))
+
+
+def fst_predict_unnormalised(w, c, B, A, Q, tau, l, trace_sign=TRACE_SIGN_PHYSICAL):
+    """eq:FST, multi-D: sine transform along every axis (R_m applied along
+    axis m), multiply by Lambda = prod_{n<l} lambda_n with the eigenvalue of the
+    per-step operator at multi-index j,
+        lambda_n(j) = b_n + sum_m 2 a_{m,n} cos((j_m+1) pi/(N_m+1))
+    (the axes' difference operators share the DST eigenvectors), inverse transform
+    R^{-1} = 2/(N_m+1) R_m per axis. Equal to fdm_predict_unnormalised
+    (T_k = R Lambda R^{-1})."""
+    w = np.asarray(w, dtype=np.float64)
+    n = w.shape
+    nx = len(n)
+    dt = tau / l
+    S = w.copy()
+    for m in range(nx):
+        S = np.moveaxis(np.tensordot(dst1_matrix(n[m]), np.moveaxis(S, m, 0), axes=(1, 0)), 0, m)
+    Lam = np.ones(n)
+    for s_ in range(l):
+        Bn = expm(np.asarray(A) * (s_ * dt)) @ B
+        a, b = fdm_step_coeffs(Bn, A, Q, dt, trace_sign)
+        lam = np.full(n, b)
+        for m in range(nx):
+            shape = [1] * nx
+            shape[m] = n[m]
+            lam = lam + (fdm_eigenvalues(n[m], a[m], 0.0)).reshape(shape)
+        Lam = Lam * lam
+    S = S * Lam
+    for m in range(nx):
+        R = dst1_matrix(n[m]) * (2.0 / (n[m] + 1))
+        S = np.moveaxis(np.tensordot(R, np.moveaxis(S, m, 0), axes=(1, 0)), 0, m)
+    M = expm(np.asarray(A) * tau)
+    return S, M @ np.asarray(c), M @ np.asarray(B)
 
 
 # ----------------------------------------------------------------------------

@@ -1,0 +1,78 @@
+"""Pins of the oracle's FDM baseline (PAPER §III.A-B)
+against what the paper and the mathematics fix, independently of the oracle's own
+formulas:
+
+* P15 the closed-form eigenvalues of F_diff = a library eigensolver's;
+* P16 the DST-I eigenvector matrix satisfies R^{-1} = 2/(N+1) R;
+* P17 the fast-sine-transform predictor (eq:FST P:199-202) = literal explicit FDM
+      stepping (eq:FDM P:146-150) on sheared, moving grids, nx = 1..3;
+* P18 the FDM spatial error falls as O(1/N^2) against the exact heat-kernel
+      solution of the pure-diffusion FPE (a Gaussian of variance sigma^2 + q tau);
+* P19 spectral differentiation beats the FDM at equal N on a smooth density (the
+      paper's central claim): a qualitative ordering, not a tolerance.
+"""
+import math
+
+import numpy as np
+import pytest
+
+from oracle import pmf_oracle as O
+
+
+@pytest.mark.parametrize("N,a,b", [(5, 0.3, 0.1), (12, -0.7, 2.0), (33, 0.25, 0.5)])
+def test_p15_fdm_eigenvalues_closed_form(N, a, b):
+    ev = np.sort(np.linalg.eigvalsh(O.fdm_matrix(N, a, b)))
+    assert np.max(np.abs(ev - np.sort(O.fdm_eigenvalues(N, a, b)))) < 1e-13
+
+
+@pytest.mark.parametrize("N", [4, 7, 32, 97])
+def test_p16_dst_orthogonality(N):
+    R = O.dst1_matrix(N)
+    assert np.max(np.abs(R @ R * (2.0 / (N + 1)) - np.eye(N))) < 1e-13
+    # and R diagonalises F_diff with the closed-form eigenvalues (columns = eigenvectors)
+    F = O.fdm_matrix(N, 0.4, 0.3)
+    lam = O.fdm_eigenvalues(N, 0.4, 0.3)
+    assert np.max(np.abs(F @ R - R * lam[None, :])) < 1e-12
+
+
+@pytest.mark.parametrize("nx,n", [(1, (9,)), (2, (7, 6)), (3, (5, 6, 4))])
+def test_p17_fst_equals_explicit_fdm(nx, n):
+    rng = np.random.default_rng(40 + nx)
+    A = 0.3 * rng.standard_normal((nx, nx))
+    Q = np.diag(rng.uniform(0.05, 0.2, nx))
+    B = np.diag(rng.uniform(0.2, 0.4, nx)) + 0.02 * rng.standard_normal((nx, nx))
+    c = rng.standard_normal(nx)
+    w = rng.random(n)
+    a, ca, Ba = O.fdm_predict_unnormalised(w, c, B, A, Q, 0.3, 7)
+    b, cb, Bb = O.fst_predict_unnormalised(w, c, B, A, Q, 0.3, 7)
+    assert np.max(np.abs(a - b)) / np.max(np.abs(a)) < 1e-13
+    assert np.allclose(ca, cb) and np.allclose(Ba, Bb)
+
+
+def _heat_errors(N, method, q=1.0, tau=0.1, l=20000, sigma=1.0, half_width=8.0):
+    """Max error (relative to the peak) of one predict of N(0, sigma^2) under pure
+    diffusion q against the exact N(0, sigma^2 + q tau) on a grid of +-half_width sigma."""
+    delta = 2.0 * half_width * sigma / N
+    c, B = np.zeros(1), np.array([[delta]])
+    x = O.grid_points(c, B, (N,))[0]
+    w = np.exp(-0.5 * x ** 2 / sigma ** 2)
+    A = np.zeros((1, 1))
+    Q = np.array([[q]])
+    if method == "fdm":
+        out, _, _ = O.fst_predict_unnormalised(w, c, B, A, Q, tau, l)
+    else:
+        out, _, _ = O.predict_unnormalised(w, c, B, A, Q, tau, l)
+    out = out / (np.sum(out) * delta)
+    s2 = sigma ** 2 + q * tau
+    exact = np.exp(-0.5 * x ** 2 / s2) / math.sqrt(2 * math.pi * s2)
+    return float(np.max(np.abs(out - exact)) / np.max(exact))
+
+
+def test_p18_fdm_second_order_in_space():
+    e1, e2, e3 = (_heat_errors(N, "fdm") for N in (32, 64, 128))
+    assert 3.3 < e1 / e2 < 4.7 and 3.3 < e2 / e3 < 4.7, (e1, e2, e3)
+
+
+def test_p19_spectral_beats_fdm_at_equal_n():
+    for N in (32, 64):
+        assert _heat_errors(N, "spectral") < 0.2 * _heat_errors(N, "fdm")
