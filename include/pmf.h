@@ -67,6 +67,10 @@ extern "C" {
 
 #define PMF_DIFF_FULL          0  /* R3: index-space diffusion D_n = B_n^-1 Q B_n^-T, cross terms kept (default) */
 #define PMF_DIFF_AXIS_LITERAL  1  /* Alg. 2-3 literally: per-axis L^(m) = N ||B_n[:,m]||, no cross    */
+#define PMF_DIFF_FDM           2  /* the paper's FDM baseline (eq:FDM P:146-150, zero Dirichlet boundary) in its
+                                     eigen / sine-transform form (eq:FST P:199-202): diagonal Q, fp64,
+                                     N_m in {32, 64, 96, 128}, <= 64 substeps; not sharded. DST-I on FP64
+                                     tensor cores; regrid and update as for the other modes             */
 
 #define PMF_TRACE_PHYSICAL (-1)   /* R5: s = (1 - dt tr A)^l   (eq:easyFPE P:92)                                   */
 #define PMF_TRACE_PRINTED    1    /* Alg. 4 as printed: s = (1 + dt tr A)^l; normalised output identical   */
@@ -88,7 +92,7 @@ typedef struct {
     int   n[4];        /* points per axis N_m (even, 2^a 3^b, 4 <= N_m <= 1024; n[m] for m>=nx ignored) */
     int   batch;       /* number of independent filters sharing A, Q and the likelihood kind       */
     int   dtype;       /* PMF_F64 or PMF_F32 (storage + transform precision; reductions are fp64)   */
-    int   diff_mode;   /* PMF_DIFF_FULL (default 0) or PMF_DIFF_AXIS_LITERAL                       */
+    int   diff_mode;   /* PMF_DIFF_FULL (default 0), PMF_DIFF_AXIS_LITERAL or PMF_DIFF_FDM         */
     int   trace_sign;  /* PMF_TRACE_PHYSICAL (0 is read as PHYSICAL) or PMF_TRACE_PRINTED          */
     int   path;        /* PMF_PATH_AUTO / PENCIL / RESIDENT                                         */
     int   device;      /* CUDA device ordinal the context lives on                                 */

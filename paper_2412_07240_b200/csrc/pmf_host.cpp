@@ -228,6 +228,7 @@ static int prepare_model(pmf_ctx* c, double dt, int steps) {
         c->sub_bytes = need;
     }
     size_t cneed = sizeof(double) * coef_stride(steps) * (size_t)c->d.batch;
+    cneed = std::max(cneed, sizeof(double) * fdm_coef_doubles(c->d.batch));
     if (cneed > c->coef_bytes) {
         if (c->coef) { cudaFree(c->coef); c->bytes -= (int64_t)c->coef_bytes; c->coef = nullptr; }
         int r = dalloc(c, (void**)&c->coef, cneed);
@@ -284,6 +285,34 @@ static int flush(pmf_ctx* c, const LikParams* lp) {
     if (c->sh) return sh_flush(c, lp);
     PencilBufs b = bufs(c);
     cudaError_t e = cudaSuccess;
+    if (c->cfg.diff_mode == PMF_DIFF_FDM) {
+        // FDM baseline: [regrid] -> DST-I predict (eq:FST) -> normalise by summation -> [update]
+        if (c->pend.regrid) {
+            e = launch_regrid(c->d, c->dtype, b, c->pend.k_sigma, c->stream, &c->launches);
+            if (e != cudaSuccess) return cuda_fail(c, e, "regrid");
+            std::swap(c->W, c->W2);
+            b = bufs(c);
+        }
+        if (c->pend.predict) {
+            if (!fdm_supported(c->d, c->dtype, c->pend.steps))
+                return fail(c, PMF_E_DT, "FDM predictor: at most 64 substeps per predict");
+            double trA = 0.0;
+            for (int a = 0; a < c->d.nx; ++a) trA += c->A[a * 4 + a];
+            const int sgn = (c->cfg.trace_sign == PMF_TRACE_PRINTED) ? 1 : -1;
+            attach_events(c, b);
+            e = launch_fdm_predict(c->d, c->dtype, b, c->mp, 1.0 + sgn * c->mp.dt * trA, c->stream, &c->launches);
+            if (e != cudaSuccess) return cuda_fail(c, e, "FDM predict");
+            b.ev0 = b.ev1 = nullptr;
+            e = launch_normalise_state(c->d, c->dtype, b, c->stream, &c->launches);
+            if (e != cudaSuccess) return cuda_fail(c, e, "FDM normalise");
+        }
+        if (lp) {
+            e = launch_update(c->d, c->dtype, b, *lp, c->stream, &c->launches);
+            if (e != cudaSuccess) return cuda_fail(c, e, "update");
+        }
+        c->pend = Pending{};
+        return PMF_OK;
+    }
     // the resident kernel keeps 3 coefficients per substep in shared memory
     const bool resident = c->path == PMF_PATH_RESIDENT && c->pend.predict && c->pend.steps <= 2048;
     if (resident) {
@@ -342,8 +371,14 @@ int pmf_validate_model(const pmf_config* cfg, const double* A, const double* Q, 
     if (nx < 1 || nx > PMF_MAX_NX) return fail(nullptr, PMF_E_ARG, "nx must be 1..4");
     if (cfg->batch < 1) return fail(nullptr, PMF_E_ARG, "batch must be >= 1");
     if (cfg->dtype != PMF_F64 && cfg->dtype != PMF_F32) return fail(nullptr, PMF_E_ARG, "bad dtype");
-    if (cfg->diff_mode != PMF_DIFF_FULL && cfg->diff_mode != PMF_DIFF_AXIS_LITERAL)
+    if (cfg->diff_mode != PMF_DIFF_FULL && cfg->diff_mode != PMF_DIFF_AXIS_LITERAL && cfg->diff_mode != PMF_DIFF_FDM)
         return fail(nullptr, PMF_E_ARG, "bad diff_mode");
+    if (cfg->diff_mode == PMF_DIFF_FDM) {
+        if (cfg->dtype != PMF_F64) return fail(nullptr, PMF_E_ARG, "FDM predictor: fp64 only");
+        for (int m = 0; m < nx; ++m)
+            if (cfg->n[m] != 32 && cfg->n[m] != 64 && cfg->n[m] != 96 && cfg->n[m] != 128)
+                return fail(nullptr, PMF_E_RADIX, "FDM predictor: N per axis in {32, 64, 96, 128}");
+    }
     for (int m = 0; m < nx; ++m) {
         if (cfg->n[m] % 2) return fail(nullptr, PMF_E_ODD_N, "points per axis must be even (P:219)");
         if (!radix_ok(cfg->n[m])) return fail(nullptr, PMF_E_RADIX, "N must be 2^a 3^b in [4, 1024]");
@@ -365,11 +400,12 @@ int pmf_validate_model(const pmf_config* cfg, const double* A, const double* Q, 
     for (int i = 0; i < nx; ++i) qmax = std::max(qmax, std::fabs(ev[i]));
     for (int i = 0; i < nx; ++i)
         if (ev[i] < -1e-12 * std::max(qmax, 1e-300)) return fail(nullptr, PMF_E_Q_NOT_PSD, "Q must be PSD");
-    if (cfg->diff_mode == PMF_DIFF_AXIS_LITERAL)
+    if (cfg->diff_mode == PMF_DIFF_AXIS_LITERAL || cfg->diff_mode == PMF_DIFF_FDM)
         for (int i = 0; i < nx; ++i)
             for (int j = 0; j < nx; ++j)
                 if (i != j && Qs[i * 4 + j] != 0.0)
-                    return fail(nullptr, PMF_E_ARG, "AXIS_LITERAL needs a diagonal Q (Alg. 3 uses Q^(m,m))");
+                    return fail(nullptr, PMF_E_ARG,
+                                "AXIS_LITERAL / FDM need a diagonal Q (Alg. 3 uses Q^(m,m); eq:FDM per axis)");
 
     return PMF_OK;
 }

@@ -128,6 +128,13 @@ size_t plane_partials_doubles(const Dims& d);
 cudaError_t launch_plane(const Dims& d, int dtype, PencilBufs& b, const ModelParams& mp, const LikParams* lp,
                          double k_sigma /* < 0 = no regrid */, cudaStream_t s, int64_t* launches);
 
+// FDM baseline predictor (eq:FST; kernels_fdm.cu): prep + DST-I passes on FP64 tensor
+// cores; the caller normalises (explicit sum) and runs the update
+bool fdm_supported(const Dims& d, int dtype, int l);
+size_t fdm_coef_doubles(int batch);
+cudaError_t launch_fdm_predict(const Dims& d, int dtype, PencilBufs& b, const ModelParams& mp, double trace_base,
+                               cudaStream_t s, int64_t* launches);
+
 // resident (one CTA per filter) fused epoch kernel
 bool resident_supported(const Dims& d, int dtype);
 cudaError_t launch_resident(const Dims& d, int dtype, PencilBufs& b, const Twiddles& tw,

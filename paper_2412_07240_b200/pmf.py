@@ -21,7 +21,7 @@ ERRORS = {-1: "PMF_E_ARG", -2: "PMF_E_ODD_N", -3: "PMF_E_RADIX", -4: "PMF_E_Q_NO
           -5: "PMF_E_SINGULAR_GRID", -6: "PMF_E_NO_SUPPORT", -7: "PMF_E_DT", -8: "PMF_E_STATE",
           -9: "PMF_E_CUDA", -10: "PMF_E_NOMEM"}
 F64, F32 = 0, 1
-DIFF_FULL, DIFF_AXIS_LITERAL = 0, 1
+DIFF_FULL, DIFF_AXIS_LITERAL, DIFF_FDM = 0, 1, 2
 TRACE_PHYSICAL, TRACE_PRINTED = -1, 1
 PATH_AUTO, PATH_PENCIL, PATH_RESIDENT, PATH_PLANE = 0, 1, 2, 3
 LIK_LINEAR_GAUSS, LIK_RANGE_GAUSS = 0, 1
