@@ -40,6 +40,8 @@ WORKLOADS = {
     "C3": dict(cid="C3", over={}),
     "C2": dict(cid="C2", over={}),
     "C1": dict(cid="C1", over={}),
+    # NEXT-1: the paper's FDM baseline (eq:FST) on the C5 batch, DST-I on FP64 tensor cores
+    "C5fdm": dict(cid="C5", over={}, diff_mode=2),
 }
 
 
@@ -204,8 +206,9 @@ def run_workload(args, workload, rank, world, local, secondary=False):
         fkw = dict(world=world, rank=rank, unique_id=obj[0])
     elif sharded:
         fkw = dict(world=args.virtual_ranks, sharded=True)
+    diff_mode = wl.get("diff_mode", 0)
     f = pmf.Filter(cfg.nx, cfg.n, cfg.A, cfg.Q, batch=cfg.batch, dtype=dtype, path=args.path,
-                   device=local, stream=stream.cuda_stream, **fkw)
+                   device=local, stream=stream.cuda_stream, diff_mode=diff_mode, **fkw)
     lik = (pmf.make_likelihood(pmf.LIK_RANGE_GAUSS, cfg.nx, sigma=cfg.sigma) if cfg.lik_kind == 1
            else pmf.make_likelihood(pmf.LIK_LINEAR_GAUSS, cfg.nx, H=cfg.H, R=cfg.R))
     f.set_gaussian(cfg.prior_mean, np.broadcast_to(cfg.prior_cov, (cfg.batch, cfg.nx, cfg.nx)), cfg.k_sigma)
@@ -284,7 +287,7 @@ def run_workload(args, workload, rank, world, local, secondary=False):
             dist.broadcast_object_list(obj, src=0)
             fkw = dict(world=world, rank=rank, unique_id=obj[0])
         fe = pmf.Filter(cfg.nx, cfg.n, cfg.A, cfg.Q, batch=cfg.batch, dtype=dtype, path=args.path,
-                        device=local, stream=stream.cuda_stream, **fkw)
+                        device=local, stream=stream.cuda_stream, diff_mode=diff_mode, **fkw)
         fe.set_gaussian(cfg.prior_mean, np.broadcast_to(cfg.prior_cov, (cfg.batch, cfg.nx, cfg.nx)), cfg.k_sigma)
         mean = np.empty((cfg.batch, cfg.nx))
         cov = np.empty((cfg.batch, cfg.nx, cfg.nx))
@@ -319,6 +322,22 @@ def run_workload(args, workload, rank, world, local, secondary=False):
     esize = 8 if dtype == "f64" else 4
     kern_ms = kern_total_ms / max(kern_n, 1)
     tname = "double" if dtype == "f64" else "float"
+    roof_extra = None
+    if diff_mode == 2:
+        # FDM: the last-axis DST kernel = two dense GEMMs (forward, inverse) per pencil on the
+        # FP64 tensor cores: 2 x 2 x N_L flops per grid point (FMA = 2 flops)
+        NL = cfg.n[-1]
+        kname = f"k_dst<{NL}, {'true' if cfg.nx == 1 else 'false'}, 2>"
+        flops = 2 * 2 * NL * points_step
+        bf16 = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))).get("bf16_tflops", 1648.2) \
+            if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 1648.2
+        peak_t = bf16 * 45.0 / 2250.0     # FP64 tensor: measured bf16 x the nominal ratio 45/2250 TF
+        ach_t = flops / (kern_ms * 1e-3) / 1e12
+        roof_extra = {"bound": "tensor", "achieved": ach_t, "peak": peak_t, "unit": "TFLOP/s",
+                      "frac": ach_t / peak_t, "traffic": None, "kernel": kname, "kernel_ms": kern_ms,
+                      "timed_launches": kern_n, "share_of_step": kern_ms / ms_step,
+                      "peak_source": "MEASURED_PEAKS.json bf16_tflops x nominal FP64-tensor/bf16 ratio 45/2250",
+                      "alg_flops_per_launch": flops, "alg_flops_per_unit": f"{4 * NL} flop per grid point"}
     if f.path == pmf.PATH_RESIDENT:
         # the fused epoch kernel: read + write every weight once
         kname = f"k_resident_epoch<{tname}, 1, 1>"
@@ -340,6 +359,8 @@ def run_workload(args, workload, rank, world, local, secondary=False):
             "alg_bytes_per_unit": per,
             "fp64_pipe_frac_ncu": (km["fp64_pipe_pct"] / 100.0) if "fp64_pipe_pct" in km else None,
             "ncu_source": km.get("source")}
+    if roof_extra is not None:
+        roof = roof_extra
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         v, nf, ts = oracle_sample(cfg, zs, budget_s=args.cpu_budget, max_filters=cfg.batch)
@@ -357,7 +378,8 @@ def run_workload(args, workload, rank, world, local, secondary=False):
                        "l2": (f"inputs larger than L2 ({esize * points_step / 1e6:.0f} MB of weights per GPU)"
                               if esize * points_step > 126e6 else
                               f"weights ({esize * points_step / 1e6:.0f} MB) fit in the 126 MB L2: L2-resident workload"),
-                       "path": {pmf.PATH_RESIDENT: "resident", pmf.PATH_PLANE: "plane"}.get(f.path, "pencil"),
+                       "path": ("fdm: DST-I GEMMs on FP64 tensor cores" if diff_mode == 2 else
+                                {pmf.PATH_RESIDENT: "resident", pmf.PATH_PLANE: "plane"}.get(f.path, "pencil")),
                        "parallelism": (f"slab-sharded x{world if world > 1 else args.virtual_ranks} along the last "
                                        "axis (2 all-to-all per predict, all-reduce per update)" if sharded
                                        else f"filter-sharded x{world} (no data-path collective)")},
@@ -400,7 +422,7 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     line = run_workload(args, args.workload, rank, world, local)
-    also_list = ("C4,C3" if args.workload == "C5" else "") if args.also == "auto" else args.also
+    also_list = ("C4,C3,C5fdm" if args.workload == "C5" else "") if args.also == "auto" else args.also
     if also_list and world == 1:
         # the other large single-GPU configurations, measured the same way (compact)
         also = {}
