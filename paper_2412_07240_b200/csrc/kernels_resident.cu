@@ -325,6 +325,29 @@ __device__ __forceinline__ void stage(const ResArgs<T>& a, int filt, void* Xr, d
     }
 }
 
+// Warp reduce-scatter of 8 doubles per lane: halving exchanges at offsets 16, 8, 4 (each
+// lane keeps half of its values, adds the partner's matching half), then a 2-level sum.
+// Returns, in lane L, the warp-wide sum of value 4 b16 + 2 b8 + b4 (b_k = bit k of L), so
+// lane 4v holds the sum of value v. Fixed order: deterministic.
+__device__ __forceinline__ double warp_sum8(const double* v, int lane) {
+    const bool b16 = (lane >> 4) & 1, b8 = (lane >> 3) & 1, b4 = (lane >> 2) & 1;
+    double h[4], q[2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const double keep = b16 ? v[4 + i] : v[i], send = b16 ? v[i] : v[4 + i];
+        h[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+    }
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+        const double keep = b8 ? h[2 + i] : h[i], send = b8 ? h[i] : h[2 + i];
+        q[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+    }
+    double r = (b4 ? q[1] : q[0]) + __shfl_xor_sync(0xffffffffu, b4 ? q[0] : q[1], 4);
+    r += __shfl_xor_sync(0xffffffffu, r, 2);
+    r += __shfl_xor_sync(0xffffffffu, r, 1);
+    return r;
+}
+
 // ============================================================================ the fused epoch kernel
 template <typename T, bool REGRID, bool UPDATE>
 __global__ void __launch_bounds__(NT, 1) k_resident_epoch(ResArgs<T> a) {
@@ -408,15 +431,21 @@ __global__ void __launch_bounds__(NT, 1) k_resident_epoch(ResArgs<T> a) {
                     i = min(max(fi, -1), N);
                     a = (fi == i) ? v - f : 0.0;
                 };
+                // upper-triangular map (CV drift after an axis-aligned regrid): v1 does not
+                // depend on the column, one split per row serves both columns
+                const bool tri = M2 == 0.0;
 #pragma unroll
                 for (int r = 0; r < 16; ++r) {
                     T val[2];
+                    int i1r;
+                    double a1r;
+                    split(fma((double)r, s1, b1[0]), i1r, a1r);
 #pragma unroll
                     for (int e = 0; e < 2; ++e) {
-                        int i0, i1;
-                        double a0, a1;
+                        int i0, i1 = i1r;
+                        double a0, a1 = a1r;
                         split(fma((double)r, s0, b0[e]), i0, a0);
-                        split(fma((double)r, s1, b1[e]), i1, a1);
+                        if (e == 1 && !tri) split(fma((double)r, s1, b1[e]), i1, a1);
                         const T* row0 = reinterpret_cast<const T*>(Xs + i1 * (int)StagePitch<T>::B) + i0;
                         const T* row1 = reinterpret_cast<const T*>(reinterpret_cast<const char*>(row0) + StagePitch<T>::B);
                         const double w00 = (double)row0[0], w01 = (double)row0[1];
@@ -778,14 +807,11 @@ __global__ void __launch_bounds__(NT, 1) k_resident_epoch(ResArgs<T> a) {
                 acc[5] = U[0] + U[1];
             }
             if (UPDATE) {
-#pragma unroll
-                for (int i = 0; i < 6; ++i) {
-                    double v = acc[i];
-                    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
-                    acc[i] = v;
-                }
-                if (lane == 0)
-                    for (int i = 0; i < 6; ++i) red[warp * 6 + i] = acc[i];
+                // transposed warp reduction (reduce-scatter): 9 double shuffles instead of 30;
+                // afterwards lane 4v holds the warp sum of accumulator v (fixed order)
+                double v8[8] = {acc[0], acc[1], acc[2], acc[3], acc[4], acc[5], 0.0, 0.0};
+                const double ws = warp_sum8(v8, lane);
+                if ((lane & 3) == 0 && (lane >> 2) < 6) red[warp * 6 + (lane >> 2)] = ws;
             }
             __syncthreads();
             if (warp == 0) {

@@ -76,3 +76,23 @@ def test_p18_fdm_second_order_in_space():
 def test_p19_spectral_beats_fdm_at_equal_n():
     for N in (32, 64):
         assert _heat_errors(N, "spectral") < 0.2 * _heat_errors(N, "fdm")
+
+
+def test_p20_heat_kernel_reference_solves_the_fpe():
+    """The convergence experiment's reference (tools/convergence.py: the mixture with
+    every variance + q t) solves dp/dt = (q/2) d2p/dx2 (eq:fokker P:55 with A = 0):
+    central differences in t and x agree to O(h^2)."""
+    import importlib.util
+    import os
+    spec = importlib.util.spec_from_file_location(
+        "convergence", os.path.join(os.path.dirname(os.path.dirname(__file__)), "tools", "convergence.py"))
+    conv = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(conv)
+    comps = conv.DENSITIES["gm3"]
+    x = np.linspace(-4, 4, 41)
+    t, h, q = 0.1, 1e-4, conv.Q
+    dpdt = (conv.mixture(x, comps, q * (t + h)) - conv.mixture(x, comps, q * (t - h))) / (2 * h)
+    hx = 1e-3
+    p0 = conv.mixture(x, comps, q * t)
+    d2 = (conv.mixture(x + hx, comps, q * t) - 2 * p0 + conv.mixture(x - hx, comps, q * t)) / hx ** 2
+    assert np.max(np.abs(dpdt - 0.5 * q * d2)) < 1e-5 * np.max(np.abs(dpdt))
