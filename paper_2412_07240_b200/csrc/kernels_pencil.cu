@@ -133,15 +133,24 @@ __host__ __device__ __forceinline__ int lq_off(int l) { return 4 + 10 * l; }
 // coefficient is multiplied by exactly s because psi(0) = 1). With an update
 // pending, the linear-Gaussian exponent is expanded around the moved grid
 // (r(u) = (z - H c_l) - (H B_l) u; e = r^T R^-1 r, R13).
+// One warp per filter: lane n computes substep n's coefficients (n = lane, lane + 32, ...),
+// lane 0 the rest (was one serial thread: 30-80 us per epoch for a single filter).
 __global__ void k_predict_prep(FilterState* st, double* coef, int cstride, ModelParams mp,
                                const SubstepEntry* __restrict__ sub, int batch, LikParams lp,
                                const double* __restrict__ z, int update) {
-    int b = blockIdx.x * blockDim.x + threadIdx.x;
+    const int b = blockIdx.x, lane = threadIdx.x;
     if (b >= batch) return;
     FilterState& f = st[b];
     double* cf = coef + (long long)b * cstride;
+    {
+        double B0[16], Bi[16];
+        for (int i = 0; i < 16; ++i) B0[i] = f.B[i];
+        mat_inv4(mp.nx, B0, Bi);
+        for (int n = lane; n < mp.l; n += 32) substep_coefs(mp.nx, B0, Bi, mp, sub[n], cf + 4 + 10 * n);
+    }
+    __syncwarp();
+    if (lane != 0) return;
     cf[0] = f.scale;
-    epoch_coefs(f.B, mp, sub, cf + 4);
     const int nx = mp.nx;
     double vol0 = fabs(det4(nx, f.B));
     double Bn[16], cn[4];
@@ -1108,7 +1117,7 @@ static cudaError_t predict_pencil_t(const Dims& d, PencilBufs& b, const Twiddles
     LikParams lpv{};
     if (lp) lpv = *lp;
     if (b.ev0) cudaEventRecord(b.ev0, s);
-    k_predict_prep<<<(d.batch + 127) / 128, 128, 0, s>>>(b.st, b.coef, cs, mp, b.sub, d.batch, lpv, b.z,
+    k_predict_prep<<<d.batch, 32, 0, s>>>(b.st, b.coef, cs, mp, b.sub, d.batch, lpv, b.z,
                                                          lp ? 1 : 0);
     ++*launches;
     PMF_TRY(cudaGetLastError());
@@ -1246,7 +1255,7 @@ cudaError_t sh_prep(const Dims& d, PencilBufs& b, const ModelParams& mp, const L
                     int64_t* launches) {
     LikParams lpv{};
     if (lp) lpv = *lp;
-    k_predict_prep<<<(d.batch + 127) / 128, 128, 0, s>>>(b.st, b.coef, coef_stride(mp.l), mp, b.sub, d.batch, lpv,
+    k_predict_prep<<<d.batch, 32, 0, s>>>(b.st, b.coef, coef_stride(mp.l), mp, b.sub, d.batch, lpv,
                                                          b.z, lp ? 1 : 0);
     ++*launches;
     return cudaGetLastError();
