@@ -298,6 +298,10 @@ def run_workload(args, workload, rank, world, local, secondary=False):
         fe.lib.pmf_update(fe.h, C.c_void_p(zp), 0, C.byref(lik))
         fe.regrid(cfg.k_sigma)
         fe.moments_into(mean, cov, logc)
+        for _ in range(2):                                    # warm-up (graph capture happens here)
+            rc = fe.lib.pmf_step(fe.h, dt, cfg.l, C.c_void_p(zp + zstride), 0, C.byref(lik), cfg.k_sigma)
+            assert rc == 0, fe.lib.pmf_last_error(fe.h)
+            fe.moments_into(mean, cov, logc)
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()

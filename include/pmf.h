@@ -221,6 +221,14 @@ int64_t pmf_launch_count(const pmf_ctx* ctx);
 int pmf_profile(pmf_ctx* ctx, int enable);
 int pmf_profile_read(pmf_ctx* ctx, double* total_ms, int64_t* count);
 
+/* CUDA-graph replay of the launch sequence of a flush (default on; env PMF_NO_GRAPHS=1
+   turns it off at creation). When the pending work, the likelihood and the buffers
+   equal those of an earlier flush, the captured graph is replayed instead of
+   re-launching every kernel (an epoch of pmf_step repeats the same sequence). Needs a
+   non-legacy stream (cfg.stream != NULL); capture failures fall back to direct
+   launches. Results are bitwise identical either way. */
+int pmf_use_graphs(pmf_ctx* ctx, int enable);
+
 /* Bytes of device memory owned by the context. */
 int64_t pmf_device_bytes(const pmf_ctx* ctx);
 

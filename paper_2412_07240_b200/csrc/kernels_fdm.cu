@@ -311,9 +311,9 @@ cudaError_t launch_fdm_predict(const Dims& d, int dtype, PencilBufs& b, const Mo
         if ((e = dst_axis(d, b, m, 0, mp.l, s)) != cudaSuccess) return e;
         ++*launches;
     }
-    if (b.ev0) cudaEventRecord(b.ev0, s);
+    if (b.ev0) cudaEventRecordWithFlags(b.ev0, s, cudaEventRecordExternal);
     if ((e = dst_axis(d, b, L, 2, mp.l, s)) != cudaSuccess) return e;
-    if (b.ev1) cudaEventRecord(b.ev1, s);
+    if (b.ev1) cudaEventRecordWithFlags(b.ev1, s, cudaEventRecordExternal);
     ++*launches;
     for (int m = L - 1; m >= 0; --m) {
         if ((e = dst_axis(d, b, m, 1, mp.l, s)) != cudaSuccess) return e;

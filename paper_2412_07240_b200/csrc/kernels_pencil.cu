@@ -1116,7 +1116,7 @@ static cudaError_t predict_pencil_t(const Dims& d, PencilBufs& b, const Twiddles
     const int cs = coef_stride(mp.l);
     LikParams lpv{};
     if (lp) lpv = *lp;
-    if (b.ev0) cudaEventRecord(b.ev0, s);
+    if (b.ev0) cudaEventRecordWithFlags(b.ev0, s, cudaEventRecordExternal);
     k_predict_prep<<<d.batch, 32, 0, s>>>(b.st, b.coef, cs, mp, b.sub, d.batch, lpv, b.z,
                                                          lp ? 1 : 0);
     ++*launches;
@@ -1150,7 +1150,7 @@ static cudaError_t predict_pencil_t(const Dims& d, PencilBufs& b, const Twiddles
     } else {
         e = predict_nd<T, 4>(d, b, tw, mp, lp, lpv, cs, s, launches);
     }
-    if (b.ev1) cudaEventRecord(b.ev1, s);
+    if (b.ev1) cudaEventRecordWithFlags(b.ev1, s, cudaEventRecordExternal);
     return e;
 }
 

@@ -1565,9 +1565,9 @@ static cudaError_t plane_t(const Dims& d, PencilBufs& b, const ModelParams& mp, 
         if ((e = mid(2, 0, S, S2, rg ? 1 : 0)) != cudaSuccess) return e;
         if (rg && (e = split_pass<T>(d, b, cs, S, S2, pa.dc3, mp.l, s, launches)) != cudaSuccess) return e;
     }
-    if (b.ev0) cudaEventRecord(b.ev0, s);
+    if (b.ev0) cudaEventRecordWithFlags(b.ev0, s, cudaEventRecordExternal);
     if ((e = mid(NX - 1, 2, S2, S2, 0)) != cudaSuccess) return e;
-    if (b.ev1) cudaEventRecord(b.ev1, s);
+    if (b.ev1) cudaEventRecordWithFlags(b.ev1, s, cudaEventRecordExternal);
     if (NX == 4 && (e = mid(2, 1, S2, S2, 0)) != cudaSuccess) return e;
     // inverse plane pass (+ update)
     int ginv = 1;

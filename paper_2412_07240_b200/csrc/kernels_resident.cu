@@ -849,9 +849,9 @@ static cudaError_t launch_t(ResArgs<T> a, cudaStream_t s, int64_t* launches, cud
     if (e != cudaSuccess) return e;
     if (occ < 1) return cudaErrorInvalidConfiguration;
     const int grid = std::min(a.batch, nsm * occ);
-    if (ev0) cudaEventRecord(ev0, s);
+    if (ev0) cudaEventRecordWithFlags(ev0, s, cudaEventRecordExternal);
     kern<<<grid, NT, smem, s>>>(a);
-    if (ev1) cudaEventRecord(ev1, s);
+    if (ev1) cudaEventRecordWithFlags(ev1, s, cudaEventRecordExternal);
     ++*launches;
     return cudaGetLastError();
 }

@@ -22,6 +22,24 @@ struct Pending {
     double k_sigma = 0.0;
 };
 
+// A captured flush (CUDA graph) and what replaying it must redo on the host.
+struct GraphKey {
+    int path, predict, steps, regrid, has_lp, prof, diff_mode, pad;
+    double dt, k_sigma;
+    pmf::LikParams lp;
+    void* W;
+    void* W2;
+    void* S;
+};
+struct GraphEntry {
+    GraphKey key;
+    cudaGraph_t graph = nullptr;                        // kept: its node handles address the exec
+    cudaGraphExec_t exec = nullptr;
+    cudaGraphNode_t ev_node[2] = {nullptr, nullptr};   // event-record nodes (profiling)
+    bool swaps = false;                                 // the flush swapped W / W2
+    int64_t launches = 0;                               // kernels per replay
+};
+
 struct pmf_ctx {
     pmf_config cfg{};
     pmf::Dims d{};
@@ -62,6 +80,9 @@ struct pmf_ctx {
     std::vector<cudaEvent_t> evs;
     int nev = 0;
     std::string err;
+    // CUDA-graph replay of flushes (pmf_step loops launch the same sequence every epoch)
+    bool graphs = true;
+    std::vector<GraphEntry> gcache;
     // sharded context (slab decomposition along the last axis), else null
     pmf::ShardSet* sh = nullptr;
 };

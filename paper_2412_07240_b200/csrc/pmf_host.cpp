@@ -13,6 +13,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -280,8 +281,8 @@ static int upload_z(pmf_ctx* c, const double* z, int on_device, int nz) {
     return PMF_OK;
 }
 
-// Execute pending regrid/predict, optionally fused with an update.
-static int flush(pmf_ctx* c, const LikParams* lp) {
+// Execute pending regrid/predict, optionally fused with an update (launches directly).
+static int flush_direct(pmf_ctx* c, const LikParams* lp) {
     if (c->sh) return sh_flush(c, lp);
     PencilBufs b = bufs(c);
     cudaError_t e = cudaSuccess;
@@ -352,6 +353,104 @@ static int flush(pmf_ctx* c, const LikParams* lp) {
     }
     c->pend = Pending{};
     return PMF_OK;
+}
+
+// Replay the flush as a CUDA graph when the same work was captured before: an epoch of
+// pmf_step launches the identical kernel sequence with identical arguments (the buffers
+// are fixed; the pencil regrid alternates W / W2, which is part of the key). Capture
+// needs a non-legacy stream; any capture failure falls back to direct launches.
+static void graph_key(const pmf_ctx* c, const LikParams* lp, GraphKey& k) {
+    std::memset(&k, 0, sizeof(k));
+    k.path = c->path;
+    k.predict = c->pend.predict;
+    k.steps = c->pend.steps;
+    k.regrid = c->pend.regrid;
+    k.has_lp = lp != nullptr;
+    k.prof = c->prof;
+    k.diff_mode = c->cfg.diff_mode;
+    k.dt = c->pend.dt;
+    k.k_sigma = c->pend.k_sigma;
+    if (lp) std::memcpy(&k.lp, lp, sizeof(LikParams));
+    k.W = c->W;
+    k.W2 = c->W2;
+    k.S = c->S;
+}
+
+static int flush(pmf_ctx* c, const LikParams* lp) {
+    const bool work = c->pend.predict || c->pend.regrid || lp;
+    if (c->sh || !c->graphs || c->stream == nullptr || !work) return flush_direct(c, lp);
+    GraphKey key;
+    graph_key(c, lp, key);
+    GraphEntry* hit = nullptr;
+    for (auto& g : c->gcache)
+        if (std::memcmp(&g.key, &key, sizeof(key)) == 0) hit = &g;
+    if (hit) {
+        if (c->prof && hit->ev_node[0] && hit->ev_node[1]) {
+            // a fresh event pair per replay (pmf_profile_read sums the pairs)
+            PencilBufs b;
+            attach_events(c, b);
+            CK(c, cudaGraphExecEventRecordNodeSetEvent(hit->exec, hit->ev_node[0], b.ev0), "graph event");
+            CK(c, cudaGraphExecEventRecordNodeSetEvent(hit->exec, hit->ev_node[1], b.ev1), "graph event");
+        }
+        CK(c, cudaGraphLaunch(hit->exec, c->stream), "graph launch");
+        if (hit->swaps) std::swap(c->W, c->W2);
+        c->launches += hit->launches;
+        c->pend = Pending{};
+        return PMF_OK;
+    }
+    if (c->gcache.size() >= 8) return flush_direct(c, lp);
+    // capture this flush
+    const Pending saved = c->pend;
+    void* W0 = c->W;
+    const int64_t l0 = c->launches;
+    const int nev0 = c->nev;
+    if (cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeRelaxed) != cudaSuccess) {
+        cudaGetLastError();
+        c->graphs = false;
+        return flush_direct(c, lp);
+    }
+    int r = flush_direct(c, lp);
+    cudaGraph_t g = nullptr;
+    cudaError_t ec = cudaStreamEndCapture(c->stream, &g);
+    cudaGraphExec_t exec = nullptr;
+    if (r == PMF_OK && ec == cudaSuccess && g && cudaGraphInstantiate(&exec, g, 0) == cudaSuccess) {
+        GraphEntry e;
+        e.key = key;
+        e.exec = exec;
+        e.swaps = c->W != W0;
+        e.launches = c->launches - l0;
+        if (c->prof && c->nev > nev0) {
+            // the event-record nodes of the pair this flush attached (retargeted per replay)
+            cudaEvent_t want[2] = {c->evs[2 * nev0], c->evs[2 * nev0 + 1]};
+            size_t n = 0;
+            cudaGraphGetNodes(g, nullptr, &n);
+            std::vector<cudaGraphNode_t> nodes(n);
+            cudaGraphGetNodes(g, nodes.data(), &n);
+            for (auto nd : nodes) {
+                cudaGraphNodeType ty;
+                cudaGraphNodeGetType(nd, &ty);
+                if (ty != cudaGraphNodeTypeEventRecord) continue;
+                cudaEvent_t ev;
+                cudaGraphEventRecordNodeGetEvent(nd, &ev);
+                for (int q = 0; q < 2; ++q)
+                    if (ev == want[q]) e.ev_node[q] = nd;
+            }
+        }
+        e.graph = g;
+        c->gcache.push_back(e);
+        CK(c, cudaGraphLaunch(exec, c->stream), "graph launch");
+        return PMF_OK;
+    }
+    // capture failed: undo the host-side effects and launch directly
+    cudaGetLastError();
+    if (g) cudaGraphDestroy(g);
+    if (exec) cudaGraphExecDestroy(exec);
+    c->graphs = false;
+    c->pend = saved;
+    if (c->W != W0) std::swap(c->W, c->W2);
+    c->launches = l0;
+    c->nev = nev0;
+    return flush_direct(c, lp);
 }
 
 template <typename T>
@@ -467,6 +566,7 @@ int pmf_create(const pmf_config* cfg, const double* A, const double* Q, pmf_ctx*
     c->dtype = cfg->dtype;
     c->esize = cfg->dtype == PMF_F64 ? 8 : 4;
     c->stream = (cudaStream_t)cfg->stream;
+    c->graphs = std::getenv("PMF_NO_GRAPHS") == nullptr;
     unpack(nx, A, c->A);
     std::memcpy(c->Q, Qs, sizeof(Qs));
     Dims& d = c->d;
@@ -553,6 +653,10 @@ void pmf_destroy(pmf_ctx* c) {
     if (c->sh) sh_destroy(c);
     cudaSetDevice(c->cfg.device);
     cudaStreamSynchronize(c->stream);
+    for (auto& g : c->gcache) {
+        if (g.exec) cudaGraphExecDestroy(g.exec);
+        if (g.graph) cudaGraphDestroy(g.graph);
+    }
     void* ptrs[] = {c->W, c->W2, c->S, c->S2, c->st, c->partials, c->coef, c->sub, c->z, c->gauss, c->mom_dev,
                     c->tw[0], c->tw[1], c->tw[2], c->tw[3]};
     for (void* p : ptrs)
@@ -782,6 +886,12 @@ int pmf_sync(pmf_ctx* c) {
 }
 
 int64_t pmf_launch_count(const pmf_ctx* c) { return c ? c->launches : 0; }
+
+int pmf_use_graphs(pmf_ctx* c, int enable) {
+    if (!c) return fail(c, PMF_E_ARG, "null context");
+    c->graphs = enable != 0;
+    return PMF_OK;
+}
 
 int pmf_profile(pmf_ctx* c, int enable) {
     if (!c) return fail(c, PMF_E_ARG, "null context");

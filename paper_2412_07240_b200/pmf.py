@@ -30,7 +30,7 @@ LIK_LINEAR_GAUSS, LIK_RANGE_GAUSS = 0, 1
 SYMBOLS = ["pmf_create", "pmf_destroy", "pmf_last_error", "pmf_set_gaussian", "pmf_set_state",
            "pmf_predict", "pmf_update", "pmf_moments", "pmf_regrid", "pmf_step", "pmf_get_weights",
            "pmf_get_grid", "pmf_sync", "pmf_launch_count", "pmf_moments_bytes", "pmf_nccl_unique_id",
-           "pmf_create_sharded", "pmf_world", "pmf_profile", "pmf_profile_read", "pmf_device_bytes", "pmf_path", "pmf_version"]
+           "pmf_create_sharded", "pmf_world", "pmf_profile", "pmf_profile_read", "pmf_use_graphs", "pmf_device_bytes", "pmf_path", "pmf_version"]
 
 
 class PMFError(RuntimeError):
@@ -83,6 +83,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         "pmf_create_sharded": (I, [C.POINTER(pmf_config), D, D, I, I, V, C.POINTER(P)]),
         "pmf_world": (I, [P]),
         "pmf_profile": (I, [P, I]),
+        "pmf_use_graphs": (I, [P, I]),
         "pmf_profile_read": (I, [P, C.POINTER(C.c_double), C.POINTER(C.c_int64)]),
         "pmf_device_bytes": (C.c_int64, [P]),
         "pmf_path": (I, [P]),
@@ -264,6 +265,10 @@ class Filter:
     @property
     def launches(self) -> int:
         return int(self.lib.pmf_launch_count(self.h))
+
+    def use_graphs(self, enable: bool = True):
+        """CUDA-graph replay of repeated flushes (needs a non-default stream)."""
+        self._check(self.lib.pmf_use_graphs(self.h, 1 if enable else 0))
 
     def profile(self, enable: bool = True):
         self._check(self.lib.pmf_profile(self.h, 1 if enable else 0))
