@@ -26,6 +26,7 @@ namespace fdm {
 constexpr int TP = 32;      // pencils per tile
 constexpr int NTH = 128;    // 4 warps; warp w owns output rows [w NA/4, (w+1) NA/4)
 constexpr int LMAX = 64;    // substeps held per filter in shared memory
+constexpr int GLP = LMAX + 1;   // per-pencil table pitch (odd: lanes of different pencils in distinct banks)
 
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
@@ -94,7 +95,7 @@ __global__ void __launch_bounds__(NTH, 1) k_dst(DstArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     double* S = reinterpret_cast<double*>(smem_raw);          // [NA][SP]
     double* X = S + NA * SP;                                  // [NA][IP] tile (j or k rows, t columns)
-    double* gl = X + NA * IP;                                 // [TP][LMAX] per-pencil Lambda terms
+    double* gl = X + NA * IP;                                 // [TP][GLP] per-pencil Lambda terms
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     for (int e = tid; e < NA * NA; e += NTH) {
         const int k = e / NA, j = e - k * NA;
@@ -171,7 +172,7 @@ __global__ void __launch_bounds__(NTH, 1) k_dst(DstArgs a) {
                     }
                     g = fma(2.0 * cf[n * 4 + m], cospi((double)(jm + 1) / (double)(a.n[m] + 1)), g);
                 }
-                gl[t * LMAX + n] = g;
+                gl[t * GLP + n] = g;
             }
         }
         __syncthreads();
@@ -191,7 +192,7 @@ __global__ void __launch_bounds__(NTH, 1) k_dst(DstArgs a) {
                     for (int e = 0; e < 2; ++e) {
                         const int t = 8 * ni + 2 * (lane & 3) + e;
                         double lam = 1.0;
-                        for (int n = 0; n < a.l; ++n) lam *= fma(cf[n * 4 + a.axis], ck, gl[t * LMAX + n]);
+                        for (int n = 0; n < a.l; ++n) lam *= fma(cf[n * 4 + a.axis], ck, gl[t * GLP + n]);
                         acc[mi][ni][e] *= lam;
                     }
             }
@@ -235,7 +236,7 @@ size_t fdm_coef_doubles(int batch) { return (size_t)cstride() * batch; }
 
 template <int NA>
 static cudaError_t dst_pass(DstArgs a, bool ax0, int mode, cudaStream_t s) {
-    const size_t smem = sizeof(double) * ((size_t)NA * (NA + 4) + (size_t)NA * (TP + 8) + (size_t)TP * LMAX);
+    const size_t smem = sizeof(double) * ((size_t)NA * (NA + 4) + (size_t)NA * (TP + 8) + (size_t)TP * GLP);
     auto launch = [&](auto kern) -> cudaError_t {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
