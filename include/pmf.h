@@ -51,7 +51,7 @@ extern "C" {
 #define PMF_OK               0
 #define PMF_E_ARG           -1  /* bad argument (null pointer, bad enum, nx/nz range, non-diagonal Q in AXIS_LITERAL mode) */
 #define PMF_E_ODD_N         -2  /* points per axis odd (the spectral interpolant needs even N)             */
-#define PMF_E_RADIX         -3  /* N not of the form 2^a 3^b with 4 <= N <= PMF max (see pmf_create)             */
+#define PMF_E_RADIX         -3  /* N has a prime factor other than 2,3,5,7,11,13,17, or N outside [4, 1024]     */
 #define PMF_E_Q_NOT_PSD     -4  /* Q not symmetric positive semi-definite                                         */
 #define PMF_E_SINGULAR_GRID -5  /* grid matrix B not invertible                                                    */
 #define PMF_E_NO_SUPPORT    -6  /* normaliser zero/non-finite: measurement incompatible with grid support,       */
@@ -89,7 +89,8 @@ typedef struct pmf_ctx pmf_ctx;
 
 typedef struct {
     int   nx;          /* state dimension, 1..4                                                    */
-    int   n[4];        /* points per axis N_m (even, 2^a 3^b, 4 <= N_m <= 1024; n[m] for m>=nx ignored) */
+    int   n[4];        /* points per axis N_m (even, factors 2,3,5,7,11,13,17 only, 4 <= N_m <= 1024;
+                          n[m] for m>=nx ignored)                                                   */
     int   batch;       /* number of independent filters sharing A, Q and the likelihood kind       */
     int   dtype;       /* PMF_F64 or PMF_F32 (storage + transform precision; reductions are fp64)   */
     int   diff_mode;   /* PMF_DIFF_FULL (default 0), PMF_DIFF_AXIS_LITERAL or PMF_DIFF_FDM         */

@@ -1,4 +1,4 @@
-// fft_smem.cuh -- mixed-radix (2, 3, 4) Stockham autosort FFT on a tile of P
+// fft_smem.cuh -- mixed-radix (2, 3, 4 + direct 5, 7, 11, 13, 17) Stockham autosort FFT on a tile of P
 // pencils held in shared memory (pencil p at offset p*PS, PS >= N).
 // Forward uses e^{-2 pi i js/N} (eq:fourtrsf P:221) WITHOUT the 1/N (the
 // scales of all axes are folded into the spectral multiplier); the inverse uses
@@ -51,6 +51,29 @@ template <bool INV, typename V> struct SmallDFT<3, INV, V> {
     }
 };
 
+// Direct DFT of a small odd prime size R (5, 7, 11, 13, 17): X[k] = sum_j v[j] W_R^{jk},
+// W_R^{m} = tw[(N/R) m] from the length-N table (the paper's grids N_pa = 34, 80, 200
+// are not 2^a 3^b: P:413).
+template <int R, bool INV, typename V>
+__device__ __forceinline__ void prime_dft(V* v, const V* __restrict__ tw, int N) {
+    V out[R];
+    const int st = N / R;
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+        V acc = v[0];
+#pragma unroll
+        for (int j = 1; j < R; ++j) {
+            V w = tw[st * ((j * k) % R)];
+            if (INV) w.y = -w.y;
+            const V t = cmul(v[j], w);
+            acc = cadd(acc, t);
+        }
+        out[k] = acc;
+    }
+#pragma unroll
+    for (int k = 0; k < R; ++k) v[k] = out[k];
+}
+
 template <int R, bool INV, typename V>
 __device__ __forceinline__ void stockham_stage(const V* __restrict__ src, V* __restrict__ dst, int N,
                                                int Ns, int P, int PS, const V* __restrict__ tw) {
@@ -76,7 +99,8 @@ __device__ __forceinline__ void stockham_stage(const V* __restrict__ src, V* __r
                 v[r] = cmul(v[r], w);
             }
         }
-        SmallDFT<R, INV, V>::run(v);
+        if constexpr (R == 2 || R == 3 || R == 4) SmallDFT<R, INV, V>::run(v);
+        else prime_dft<R, INV>(v, tw, N);
         const int idxD = jq * Ns * R + k;
         V* d = dst + p * PS;
 #pragma unroll
@@ -94,7 +118,12 @@ __device__ V* smem_fft(V* a, V* b, int P, int PS, const FFTPlan& pl, const V* __
         const int R = pl.r[s];
         if (R == 4) stockham_stage<4, INV>(a, b, pl.N, Ns, P, PS, tw);
         else if (R == 2) stockham_stage<2, INV>(a, b, pl.N, Ns, P, PS, tw);
-        else stockham_stage<3, INV>(a, b, pl.N, Ns, P, PS, tw);
+        else if (R == 3) stockham_stage<3, INV>(a, b, pl.N, Ns, P, PS, tw);
+        else if (R == 5) stockham_stage<5, INV>(a, b, pl.N, Ns, P, PS, tw);
+        else if (R == 7) stockham_stage<7, INV>(a, b, pl.N, Ns, P, PS, tw);
+        else if (R == 11) stockham_stage<11, INV>(a, b, pl.N, Ns, P, PS, tw);
+        else if (R == 13) stockham_stage<13, INV>(a, b, pl.N, Ns, P, PS, tw);
+        else stockham_stage<17, INV>(a, b, pl.N, Ns, P, PS, tw);
         __syncthreads();
         V* t = a; a = b; b = t;
         Ns *= R;

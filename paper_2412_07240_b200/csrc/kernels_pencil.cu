@@ -1,5 +1,5 @@
 // kernels_pencil.cu -- the general multi-pass path (any nx <= 4, any
-// N = 2^a 3^b per axis, any batch), plus the per-filter kernels shared with the
+// N with factors 2, 3, 5, 7, 11, 13, 17 per axis, any batch), plus the per-filter kernels shared with the
 // resident path: initial density, standalone likelihood update, reductions
 // into per-filter moments, and the multilinear regrid.
 //
@@ -31,6 +31,8 @@ static FFTPlan make_plan(int N) {
     while (m % 4 == 0) { p.r[k++] = 4; m /= 4; }
     if (m % 2 == 0) { p.r[k++] = 2; m /= 2; }
     while (m % 3 == 0) { p.r[k++] = 3; m /= 3; }
+    for (int q : {5, 7, 11, 13, 17})
+        while (m % q == 0) { p.r[k++] = q; m /= q; }
     p.nst = k;
     return p;
 }

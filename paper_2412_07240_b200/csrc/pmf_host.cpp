@@ -149,8 +149,8 @@ static void unpack(int n, const double* src, double* dst) {  // packed n x n -> 
 static bool radix_ok(int N) {
     if (N < 4 || N > 1024) return false;
     int m = N;
-    while (m % 2 == 0) m /= 2;
-    while (m % 3 == 0) m /= 3;
+    for (int q : {2, 3, 5, 7, 11, 13, 17})
+        while (m % q == 0) m /= q;
     return m == 1;
 }
 
@@ -480,7 +480,7 @@ int pmf_validate_model(const pmf_config* cfg, const double* A, const double* Q, 
     }
     for (int m = 0; m < nx; ++m) {
         if (cfg->n[m] % 2) return fail(nullptr, PMF_E_ODD_N, "points per axis must be even (P:219)");
-        if (!radix_ok(cfg->n[m])) return fail(nullptr, PMF_E_RADIX, "N must be 2^a 3^b in [4, 1024]");
+        if (!radix_ok(cfg->n[m])) return fail(nullptr, PMF_E_RADIX, "N must be a product of 2, 3, 5, 7, 11, 13, 17 in [4, 1024]");
     }
     unpack(nx, Q, Qs);
     for (int i = 0; i < nx; ++i) {

@@ -46,7 +46,7 @@ def _create(nx, n, A, Q, **kw):
 def test_argument_validation_without_gpu():
     eye = np.eye(2)
     assert _create(2, (31, 32), eye, eye)[0] == -2          # PMF_E_ODD_N
-    assert _create(2, (20, 32), eye, eye)[0] == -3          # PMF_E_RADIX (20 = 2^2 5)
+    assert _create(2, (38, 32), eye, eye)[0] == -3          # PMF_E_RADIX (38 = 2 x 19)
     assert _create(2, (2048, 32), eye, eye)[0] == -3        # too large
     assert _create(5, (8,), np.eye(5), np.eye(5))[0] == -1  # nx range
     assert _create(2, (8, 8), eye, np.array([[1.0, 0.0], [0.5, 1.0]]))[0] == -4   # not symmetric

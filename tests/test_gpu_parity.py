@@ -20,6 +20,14 @@ CASES = {
     "C3s": ("C3", {"n": (16, 12, 24)}, 4),
     "C4s": ("C4", {"n": (8, 6, 12, 8)}, 3),
     "C5s": ("C5", {"batch": 5, "n": (24, 32)}, 4),
+    # the paper's own grid sizes (N_pa = 34; N = 80, 200 in Figs. 2-3):
+    # radix 17, 5 and 5^2 stages, and 7, 11, 13
+    "C1_34": ("C1", {"n": (34,)}, 5),
+    "C1_80": ("C1", {"n": (80,)}, 4),
+    "C1_200": ("C1", {"n": (200,)}, 3),
+    "C5_34x28": ("C5", {"batch": 2, "n": (34, 28)}, 3),
+    "C3_22x26x14": ("C3", {"n": (22, 26, 14)}, 2),
+    "C4_34x10x34x10": ("C4", {"n": (34, 10, 34, 10)}, 2),
 }
 
 
