@@ -42,6 +42,8 @@ WORKLOADS = {
     "C1": dict(cid="C1", over={}),
     # NEXT-1: the paper's FDM baseline (eq:FST) on the C5 batch, DST-I on FP64 tensor cores
     "C5fdm": dict(cid="C5", over={}, diff_mode=2),
+    # NEXT-3: the paper's §VI scenario (coordinated turn, terrain altitude + GM noise, N_pa = 34)
+    "C6": dict(cid="C6", over={}),
 }
 
 
@@ -209,8 +211,13 @@ def run_workload(args, workload, rank, world, local, secondary=False):
     diff_mode = wl.get("diff_mode", 0)
     f = pmf.Filter(cfg.nx, cfg.n, cfg.A, cfg.Q, batch=cfg.batch, dtype=dtype, path=args.path,
                    device=local, stream=stream.cuda_stream, diff_mode=diff_mode, **fkw)
-    lik = (pmf.make_likelihood(pmf.LIK_RANGE_GAUSS, cfg.nx, sigma=cfg.sigma) if cfg.lik_kind == 1
-           else pmf.make_likelihood(pmf.LIK_LINEAR_GAUSS, cfg.nx, H=cfg.H, R=cfg.R))
+    if cfg.lik_kind == 2:
+        from workloads import terrain_table
+        lik = pmf.make_likelihood(pmf.LIK_TERRAIN_GM, cfg.nx, gm=cfg.extra["gm"])
+        f.set_terrain(*terrain_table(cfg))
+    else:
+        lik = (pmf.make_likelihood(pmf.LIK_RANGE_GAUSS, cfg.nx, sigma=cfg.sigma) if cfg.lik_kind == 1
+               else pmf.make_likelihood(pmf.LIK_LINEAR_GAUSS, cfg.nx, H=cfg.H, R=cfg.R))
     f.set_gaussian(cfg.prior_mean, np.broadcast_to(cfg.prior_cov, (cfg.batch, cfg.nx, cfg.nx)), cfg.k_sigma)
     z_dev = torch.tensor(zs, dtype=torch.float64, device=f"cuda:{local}")   # inputs resident in HBM
     dt = cfg.tau / cfg.l
@@ -280,7 +287,7 @@ def run_workload(args, workload, rank, world, local, secondary=False):
     e2e = None
     if not args.no_e2e:
         Te = min(args.steps, 10)
-        zs_e = simulate(cfg, T=Te + 1)["z"]
+        zs_e = simulate(cfg, T=Te + 3)["z"]
         z_pin = torch.tensor(zs_e, dtype=torch.float64).pin_memory()
         if sharded and world > 1:
             obj = [pmf.nccl_unique_id() if rank == 0 else None]
@@ -288,6 +295,8 @@ def run_workload(args, workload, rank, world, local, secondary=False):
             fkw = dict(world=world, rank=rank, unique_id=obj[0])
         fe = pmf.Filter(cfg.nx, cfg.n, cfg.A, cfg.Q, batch=cfg.batch, dtype=dtype, path=args.path,
                         device=local, stream=stream.cuda_stream, diff_mode=diff_mode, **fkw)
+        if cfg.lik_kind == 2:
+            fe.set_terrain(*terrain_table(cfg))
         fe.set_gaussian(cfg.prior_mean, np.broadcast_to(cfg.prior_cov, (cfg.batch, cfg.nx, cfg.nx)), cfg.k_sigma)
         mean = np.empty((cfg.batch, cfg.nx))
         cov = np.empty((cfg.batch, cfg.nx, cfg.nx))
@@ -298,8 +307,8 @@ def run_workload(args, workload, rank, world, local, secondary=False):
         fe.lib.pmf_update(fe.h, C.c_void_p(zp), 0, C.byref(lik))
         fe.regrid(cfg.k_sigma)
         fe.moments_into(mean, cov, logc)
-        for _ in range(2):                                    # warm-up (graph capture happens here)
-            rc = fe.lib.pmf_step(fe.h, dt, cfg.l, C.c_void_p(zp + zstride), 0, C.byref(lik), cfg.k_sigma)
+        for i in range(2):                                    # warm-up (graph capture happens here)
+            rc = fe.lib.pmf_step(fe.h, dt, cfg.l, C.c_void_p(zp + (i + 1) * zstride), 0, C.byref(lik), cfg.k_sigma)
             assert rc == 0, fe.lib.pmf_last_error(fe.h)
             fe.moments_into(mean, cov, logc)
         torch.cuda.synchronize()
@@ -308,7 +317,7 @@ def run_workload(args, workload, rank, world, local, secondary=False):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for i in range(Te):
-            rc = fe.lib.pmf_step(fe.h, dt, cfg.l, C.c_void_p(zp + (i + 1) * zstride), 0, C.byref(lik), cfg.k_sigma)
+            rc = fe.lib.pmf_step(fe.h, dt, cfg.l, C.c_void_p(zp + (i + 3) * zstride), 0, C.byref(lik), cfg.k_sigma)
             assert rc == 0, fe.lib.pmf_last_error(fe.h)
             fe.moments_into(mean, cov, logc)                  # D2H read of the step's result
         e1.record(stream)
@@ -376,7 +385,7 @@ def run_workload(args, workload, rank, world, local, secondary=False):
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "strong" if sharded else "weak",
             "vs_baseline": None, "dtype": dtype, "data": "synthetic",
-            "config": {"workload": f"{workload}: {cfg.batch} x {'x'.join(map(str, cfg.n))} {cfg.nx}-D CV filters "
+            "config": {"workload": f"{workload}: {cfg.batch} x {'x'.join(map(str, cfg.n))} {cfg.nx}-D filters "
                                    f"per GPU, l={cfg.l}, tau={cfg.tau}, k_sigma={cfg.k_sigma}",
                        "step": "regrid + predict (Alg. 1-6) + update + moments, every filter",
                        "l2": (f"inputs larger than L2 ({esize * points_step / 1e6:.0f} MB of weights per GPU)"
@@ -426,7 +435,7 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     line = run_workload(args, args.workload, rank, world, local)
-    also_list = ("C4,C3,C5fdm" if args.workload == "C5" else "") if args.also == "auto" else args.also
+    also_list = ("C4,C3,C5fdm,C6" if args.workload == "C5" else "") if args.also == "auto" else args.also
     if also_list and world == 1:
         # the other large single-GPU configurations, measured the same way (compact)
         also = {}

@@ -84,6 +84,9 @@ extern "C" {
 
 #define PMF_LIK_LINEAR_GAUSS 0   /* z = H x + v, v ~ N(0, R), nz <= 4 (eq:meas P:36)                               */
 #define PMF_LIK_RANGE_GAUSS  1   /* z = ||x|| + v, v ~ N(0, sigma^2), nz = 1 (C3)                                   */
+#define PMF_LIK_TERRAIN_GM   2   /* the paper's §VI model: z = h(x[ix], x[iy]) + v, h the terrain table
+                                    of pmf_set_terrain (bilinear, clamped to the table), v ~ sum_g w_g N(mu_g, var_g),
+                                    ncomp <= 4 components; nz = 1                                                 */
 
 typedef struct pmf_ctx pmf_ctx;
 
@@ -106,6 +109,10 @@ typedef struct {
     double H[16];      /* LINEAR_GAUSS: nz x nx row-major, packed                                  */
     double R[16];      /* LINEAR_GAUSS: nz x nz noise covariance, symmetric positive definite       */
     double sigma;      /* RANGE_GAUSS: noise standard deviation > 0                                 */
+    int    ncomp;      /* TERRAIN_GM: mixture components 1..4                                      */
+    double gm_w[4];    /* TERRAIN_GM: weights >= 0 (normalised by the library)                     */
+    double gm_mu[4];   /* TERRAIN_GM: component means                                              */
+    double gm_var[4];  /* TERRAIN_GM: component variances > 0                                     */
 } pmf_likelihood;
 
 /* Create a context: validates sizes (PMF_E_ODD_N, PMF_E_RADIX), A (nx x nx) and
@@ -131,6 +138,15 @@ int pmf_set_gaussian(pmf_ctx* ctx, const double* mean, const double* cov, double
  * and weights (batch x N_total in dtype, host or device per weights_on_device;
  * a device pointer must be on cfg->device). The weights are normalised on
  * entry (vol * sum w = 1). PMF_E_SINGULAR_GRID if some B is singular. */
+/* Terrain table for PMF_LIK_TERRAIN_GM ("a table function that assigns
+ * altitude to each combination of ... it covers"): heights[r * ncol + c] is the
+ * altitude at (x0 + c dx, y0 + r dy); state components ix, iy are the horizontal
+ * position. Between nodes h is bilinear; outside the table the nearest edge value is
+ * used (reading R26). The host array is copied to the device (the caller keeps
+ * ownership). Errors: PMF_E_ARG for nrow/ncol < 2, dx/dy <= 0, ix/iy outside the state. */
+int pmf_set_terrain(pmf_ctx* ctx, const double* heights, int nrow, int ncol, double x0, double y0, double dx,
+                    double dy, int ix, int iy);
+
 int pmf_set_state(pmf_ctx* ctx, const double* center, const double* B,
                   const void* weights, int weights_on_device);
 

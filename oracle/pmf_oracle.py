@@ -420,6 +420,35 @@ def lik_range_gauss(X, z, sigma) -> np.ndarray:
     return np.exp(-0.5 * ((z - rng) / sigma) ** 2) / (sigma * math.sqrt(2 * math.pi))
 
 
+def terrain_height(px, py, heights, x0, y0, dx, dy):
+    """The map h of the paper's §VI measurement ("a table function that assigns
+    vertical position to each combination of latitude and longitude it covers"): bilinear
+    between the table nodes heights[r, c] at (x0 + c dx, y0 + r dy), the nearest edge value
+    outside the table (R26). Pinned by exactness on bilinear fields and the node values."""
+    H = np.asarray(heights, dtype=np.float64)
+    nrow, ncol = H.shape
+    u = np.clip((np.asarray(px, dtype=np.float64) - x0) / dx, 0.0, ncol - 1)
+    v = np.clip((np.asarray(py, dtype=np.float64) - y0) / dy, 0.0, nrow - 1)
+    c = np.minimum(np.floor(u).astype(np.int64), ncol - 2)
+    r = np.minimum(np.floor(v).astype(np.int64), nrow - 2)
+    fu, fv = u - c, v - r
+    return ((1 - fu) * (1 - fv) * H[r, c] + fu * (1 - fv) * H[r, c + 1]
+            + (1 - fu) * fv * H[r + 1, c] + fu * fv * H[r + 1, c + 1])
+
+
+def lik_terrain_gm(X, z, table, gm) -> np.ndarray:
+    """p(z | x) for z = h(x_ix, x_iy) + v with the 2-component (here: any) Gaussian-mixture
+    noise of eq:ex1_PDF: sum_g w_g N(z - h; mu_g, var_g), weights normalised.
+    ``table`` = (heights, x0, y0, dx, dy, ix, iy); ``gm`` = ((w, mu, var), ...)."""
+    heights, x0, y0, dx, dy, ix, iy = table
+    d = float(np.asarray(z).reshape(-1)[0]) - terrain_height(X[ix], X[iy], heights, x0, y0, dx, dy)
+    wsum = sum(g[0] for g in gm)
+    out = np.zeros_like(d)
+    for w, mu, var in gm:
+        out = out + (w / wsum) * np.exp(-0.5 * (d - mu) ** 2 / var) / math.sqrt(2 * math.pi * var)
+    return out
+
+
 def update(w, c, B, lik_values):
     """Bayes' rule eq:filt: posterior = prior x likelihood / normaliser,
     normaliser p(z_k|z^{k-1}) = int prior x lik dx by quadrature over
@@ -504,6 +533,9 @@ def regrid(w, c, B, c_new, B_new):
 def make_likelihood(cfg, X, z):
     if cfg.lik_kind == 1:
         return lik_range_gauss(X, z, cfg.sigma)
+    if cfg.lik_kind == 2:
+        from workloads import terrain_table      # the map is an input (seeded synthetic field)
+        return lik_terrain_gm(X, z, terrain_table(cfg), cfg.extra["gm"])
     return lik_linear_gauss(X, z, cfg.H, cfg.R)
 
 

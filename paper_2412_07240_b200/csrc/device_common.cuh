@@ -170,6 +170,30 @@ __device__ __forceinline__ double exp_fast(double x) {
 }
 
 // ---------------------------------------------------------------- likelihood at a physical point
+// Terrain table function: bilinear between nodes, nearest edge outside (R26).
+__device__ __forceinline__ double terrain_height(const LikParams& lp, double px, double py) {
+    double u = (px - lp.tx0) * lp.tidx, v = (py - lp.ty0) * lp.tidy;
+    u = fmin(fmax(u, 0.0), (double)(lp.tcol - 1));
+    v = fmin(fmax(v, 0.0), (double)(lp.trow - 1));
+    const int c = min((int)u, lp.tcol - 2), r = min((int)v, lp.trow - 2);
+    const double fu = u - c, fv = v - r;
+    const double* t0 = lp.terrain + (long long)r * lp.tcol + c;
+    const double lo = fma(fu, t0[1] - t0[0], t0[0]);
+    const double hi = fma(fu, t0[lp.tcol + 1] - t0[lp.tcol], t0[lp.tcol]);
+    return fma(fv, hi - lo, lo);
+}
+
+// p(z | x) for z = h(x) + v, v ~ sum_g w_g N(mu_g, var_g) (eq:ex1_PDF P:413-418)
+__device__ __forceinline__ double lik_terrain_gm(const LikParams& lp, const double* x, const double* z) {
+    const double d = z[0] - terrain_height(lp, x[lp.ix], x[lp.iy]);
+    double s = 0.0;
+    for (int g = 0; g < lp.ncomp; ++g) {
+        const double e = d - lp.gm_mu[g];
+        s += exp_fast(fma(-0.5 * e * lp.gm_ivar[g], e, lp.gm_logc[g]));
+    }
+    return s;
+}
+
 __device__ __forceinline__ double log_lik(const LikParams& lp, const double* x, const double* z) {
     if (lp.kind == 1) {
         double r2 = 0.0;

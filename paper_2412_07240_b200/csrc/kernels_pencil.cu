@@ -554,7 +554,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_points(T* __restrict__ W, const
             phys<NX>(f, u, x);
         }
         if (MODE == 0) {
-            const double w = (double)Wf[pt] * f.scale * exp_fast(log_lik(lp, x, zf));
+            const double lk = lp.kind == 2 ? lik_terrain_gm(lp, x, zf) : exp_fast(log_lik(lp, x, zf));
+            const double w = (double)Wf[pt] * f.scale * lk;
             const T wt = (T)w;
             Wf[pt] = wt;
             acc_mom<NX>((double)wt, u, acc);

@@ -53,6 +53,9 @@ struct pmf_ctx {
     void* W2 = nullptr;
     void* S = nullptr;
     void* S2 = nullptr;
+    double* terrain = nullptr;       // TERRAIN_GM likelihood table (pmf_set_terrain)
+    int t_rows = 0, t_cols = 0, t_ix = 0, t_iy = 0;
+    double t_x0 = 0, t_y0 = 0, t_dx = 1, t_dy = 1;
     pmf::FilterState* st = nullptr;
     double* partials = nullptr;
     size_t partials_bytes = 0;

@@ -258,6 +258,34 @@ static int make_lik(pmf_ctx* c, const pmf_likelihood* lik, LikParams& lp) {
         lp.lognorm = -std::log(lik->sigma * std::sqrt(2.0 * M_PI));
         return PMF_OK;
     }
+    if (lik->kind == PMF_LIK_TERRAIN_GM) {
+        if (!c->terrain) return fail(c, PMF_E_STATE, "TERRAIN_GM likelihood needs pmf_set_terrain first");
+        if (lik->ncomp < 1 || lik->ncomp > 4) return fail(c, PMF_E_ARG, "TERRAIN_GM: ncomp must be 1..4");
+        double wsum = 0.0;
+        for (int g = 0; g < lik->ncomp; ++g) {
+            if (!(lik->gm_w[g] >= 0.0) || !(lik->gm_var[g] > 0.0) || !std::isfinite(lik->gm_mu[g]))
+                return fail(c, PMF_E_ARG, "TERRAIN_GM: weights >= 0, variances > 0, finite means");
+            wsum += lik->gm_w[g];
+        }
+        if (!(wsum > 0.0)) return fail(c, PMF_E_ARG, "TERRAIN_GM: weights sum to zero");
+        lp.nz = 1;
+        lp.ncomp = lik->ncomp;
+        for (int g = 0; g < lik->ncomp; ++g) {
+            lp.gm_logc[g] = std::log(lik->gm_w[g] / wsum) - 0.5 * std::log(2.0 * M_PI * lik->gm_var[g]);
+            lp.gm_mu[g] = lik->gm_mu[g];
+            lp.gm_ivar[g] = 1.0 / lik->gm_var[g];
+        }
+        lp.ix = c->t_ix;
+        lp.iy = c->t_iy;
+        lp.trow = c->t_rows;
+        lp.tcol = c->t_cols;
+        lp.tx0 = c->t_x0;
+        lp.ty0 = c->t_y0;
+        lp.tidx = 1.0 / c->t_dx;
+        lp.tidy = 1.0 / c->t_dy;
+        lp.terrain = c->terrain;
+        return PMF_OK;
+    }
     if (lik->kind != PMF_LIK_LINEAR_GAUSS) return fail(c, PMF_E_ARG, "unknown likelihood kind");
     const int nz = lik->nz;
     if (nz < 1 || nz > PMF_MAX_NZ) return fail(c, PMF_E_ARG, "nz must be 1..4");
@@ -284,6 +312,18 @@ static int upload_z(pmf_ctx* c, const double* z, int on_device, int nz) {
 // Execute pending regrid/predict, optionally fused with an update (launches directly).
 static int flush_direct(pmf_ctx* c, const LikParams* lp) {
     if (c->sh) return sh_flush(c, lp);
+    if (lp && lp->kind == PMF_LIK_TERRAIN_GM) {
+        // the table likelihood is not fused into the transform kernels: predict (+ regrid)
+        // first, then the standalone point update
+        if (c->pend.predict || c->pend.regrid) {
+            int r = flush_direct(c, nullptr);
+            if (r) return r;
+        }
+        PencilBufs b = bufs(c);
+        cudaError_t e = launch_update(c->d, c->dtype, b, *lp, c->stream, &c->launches);
+        if (e != cudaSuccess) return cuda_fail(c, e, "update");
+        return PMF_OK;
+    }
     PencilBufs b = bufs(c);
     cudaError_t e = cudaSuccess;
     if (c->cfg.diff_mode == PMF_DIFF_FDM) {
@@ -657,7 +697,7 @@ void pmf_destroy(pmf_ctx* c) {
         if (g.exec) cudaGraphExecDestroy(g.exec);
         if (g.graph) cudaGraphDestroy(g.graph);
     }
-    void* ptrs[] = {c->W, c->W2, c->S, c->S2, c->st, c->partials, c->coef, c->sub, c->z, c->gauss, c->mom_dev,
+    void* ptrs[] = {c->W, c->W2, c->S, c->S2, c->terrain, c->st, c->partials, c->coef, c->sub, c->z, c->gauss, c->mom_dev,
                     c->tw[0], c->tw[1], c->tw[2], c->tw[3]};
     for (void* p : ptrs)
         if (p) cudaFree(p);
@@ -886,6 +926,34 @@ int pmf_sync(pmf_ctx* c) {
 }
 
 int64_t pmf_launch_count(const pmf_ctx* c) { return c ? c->launches : 0; }
+
+int pmf_set_terrain(pmf_ctx* c, const double* heights, int nrow, int ncol, double x0, double y0, double dx,
+                    double dy, int ix, int iy) {
+    if (!c || !heights) return fail(c, PMF_E_ARG, "null argument");
+    if (c->sh) return fail(c, PMF_E_ARG, "terrain likelihood: not for sharded contexts");
+    if (nrow < 2 || ncol < 2 || !(dx > 0.0) || !(dy > 0.0) || ix < 0 || iy < 0 || ix >= c->d.nx ||
+        iy >= c->d.nx || ix == iy)
+        return fail(c, PMF_E_ARG, "terrain: nrow, ncol >= 2; dx, dy > 0; ix != iy state components");
+    CK(c, cudaSetDevice(c->cfg.device), "cudaSetDevice");
+    const size_t bytes = sizeof(double) * (size_t)nrow * ncol;
+    if (c->terrain) {
+        CK(c, cudaStreamSynchronize(c->stream), "sync");
+        cudaFree(c->terrain);
+        c->terrain = nullptr;
+    }
+    int r = dalloc(c, (void**)&c->terrain, bytes);
+    if (r) return r;
+    CK(c, cudaMemcpy(c->terrain, heights, bytes, cudaMemcpyHostToDevice), "terrain upload");
+    c->t_rows = nrow;
+    c->t_cols = ncol;
+    c->t_x0 = x0;
+    c->t_y0 = y0;
+    c->t_dx = dx;
+    c->t_dy = dy;
+    c->t_ix = ix;
+    c->t_iy = iy;
+    return PMF_OK;
+}
 
 int pmf_use_graphs(pmf_ctx* c, int enable) {
     if (!c) return fail(c, PMF_E_ARG, "null context");

@@ -48,6 +48,13 @@ struct LikParams {
     double Rinv[16];    // nz x nz, row stride 4
     double lognorm;     // -0.5 log((2 pi)^nz det R)  or  -log(sigma sqrt(2 pi))
     double inv_sigma;
+    // TERRAIN_GM (kind 2): h = bilinear(terrain) at (x[ix], x[iy]); GM noise
+    int ncomp, ix, iy, trow, tcol, pad2;
+    double gm_logc[4];  // log w_g - 0.5 log(2 pi var_g)
+    double gm_mu[4];
+    double gm_ivar[4];  // 1 / var_g
+    double tx0, ty0, tidx, tidy;   // table origin and inverse spacings
+    const double* terrain;         // device table [trow][tcol]
 };
 
 struct Dims {

@@ -24,13 +24,14 @@ F64, F32 = 0, 1
 DIFF_FULL, DIFF_AXIS_LITERAL, DIFF_FDM = 0, 1, 2
 TRACE_PHYSICAL, TRACE_PRINTED = -1, 1
 PATH_AUTO, PATH_PENCIL, PATH_RESIDENT, PATH_PLANE = 0, 1, 2, 3
-LIK_LINEAR_GAUSS, LIK_RANGE_GAUSS = 0, 1
+LIK_LINEAR_GAUSS, LIK_RANGE_GAUSS, LIK_TERRAIN_GM = 0, 1, 2
 
 # every symbol include/pmf.h declares (checked by tests/test_abi.py)
 SYMBOLS = ["pmf_create", "pmf_destroy", "pmf_last_error", "pmf_set_gaussian", "pmf_set_state",
            "pmf_predict", "pmf_update", "pmf_moments", "pmf_regrid", "pmf_step", "pmf_get_weights",
            "pmf_get_grid", "pmf_sync", "pmf_launch_count", "pmf_moments_bytes", "pmf_nccl_unique_id",
-           "pmf_create_sharded", "pmf_world", "pmf_profile", "pmf_profile_read", "pmf_use_graphs", "pmf_device_bytes", "pmf_path", "pmf_version"]
+           "pmf_create_sharded", "pmf_world", "pmf_profile", "pmf_profile_read", "pmf_use_graphs",
+           "pmf_set_terrain", "pmf_device_bytes", "pmf_path", "pmf_version"]
 
 
 class PMFError(RuntimeError):
@@ -47,7 +48,8 @@ class pmf_config(C.Structure):
 
 class pmf_likelihood(C.Structure):
     _fields_ = [("kind", C.c_int), ("nz", C.c_int), ("H", C.c_double * 16), ("R", C.c_double * 16),
-                ("sigma", C.c_double)]
+                ("sigma", C.c_double), ("ncomp", C.c_int), ("gm_w", C.c_double * 4), ("gm_mu", C.c_double * 4),
+                ("gm_var", C.c_double * 4)]
 
 
 _lib = None
@@ -84,6 +86,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         "pmf_world": (I, [P]),
         "pmf_profile": (I, [P, I]),
         "pmf_use_graphs": (I, [P, I]),
+        "pmf_set_terrain": (I, [P, D, I, I, C.c_double, C.c_double, C.c_double, C.c_double, I, I]),
         "pmf_profile_read": (I, [P, C.POINTER(C.c_double), C.POINTER(C.c_int64)]),
         "pmf_device_bytes": (C.c_int64, [P]),
         "pmf_path": (I, [P]),
@@ -111,9 +114,16 @@ def _dptr(a: np.ndarray):
     return a.ctypes.data_as(C.POINTER(C.c_double))
 
 
-def make_likelihood(kind: int, nx: int, H=None, R=None, sigma: float = 0.0) -> pmf_likelihood:
+def make_likelihood(kind: int, nx: int, H=None, R=None, sigma: float = 0.0, gm=None) -> pmf_likelihood:
+    """gm (TERRAIN_GM): sequence of (weight, mean, variance) noise components."""
     lk = pmf_likelihood()
     lk.kind = kind
+    if kind == LIK_TERRAIN_GM:
+        lk.nz = 1
+        lk.ncomp = len(gm)
+        for g, (w, mu, var) in enumerate(gm):
+            lk.gm_w[g], lk.gm_mu[g], lk.gm_var[g] = float(w), float(mu), float(var)
+        return lk
     if kind == LIK_RANGE_GAUSS:
         lk.nz = 1
         lk.sigma = float(sigma)
@@ -265,6 +275,12 @@ class Filter:
     @property
     def launches(self) -> int:
         return int(self.lib.pmf_launch_count(self.h))
+
+    def set_terrain(self, heights, x0: float, y0: float, dx: float, dy: float, ix: int, iy: int):
+        """Terrain table for LIK_TERRAIN_GM: heights[r, c] at (x0 + c dx, y0 + r dy)."""
+        h = np.ascontiguousarray(np.asarray(heights, dtype=np.float64))
+        self._check(self.lib.pmf_set_terrain(self.h, _dptr(h), int(h.shape[0]), int(h.shape[1]), float(x0),
+                                             float(y0), float(dx), float(dy), int(ix), int(iy)))
 
     def use_graphs(self, enable: bool = True):
         """CUDA-graph replay of repeated flushes (needs a non-default stream)."""

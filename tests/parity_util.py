@@ -12,6 +12,8 @@ TOL = {"f64": 1e-10, "f32": 1e-4}     # north_star: relative L-inf normalised by
 def lik_of(cfg):
     if cfg.lik_kind == 1:
         return pmf.make_likelihood(pmf.LIK_RANGE_GAUSS, cfg.nx, sigma=cfg.sigma)
+    if cfg.lik_kind == 2:
+        return pmf.make_likelihood(pmf.LIK_TERRAIN_GM, cfg.nx, gm=cfg.extra["gm"])
     return pmf.make_likelihood(pmf.LIK_LINEAR_GAUSS, cfg.nx, H=cfg.H, R=cfg.R)
 
 
@@ -23,6 +25,9 @@ def rel_linf(gpu, ref):
 
 def make_filter(cfg, dtype="f64", path=pmf.PATH_AUTO, **kw):
     f = pmf.Filter(cfg.nx, cfg.n, cfg.A, cfg.Q, batch=cfg.batch, dtype=dtype, path=path, **kw)
+    if cfg.lik_kind == 2:
+        from workloads import terrain_table
+        f.set_terrain(*terrain_table(cfg))
     f.set_gaussian(cfg.prior_mean, np.broadcast_to(cfg.prior_cov, (cfg.batch, cfg.nx, cfg.nx)), cfg.k_sigma)
     return f
 

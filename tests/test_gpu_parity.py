@@ -28,6 +28,10 @@ CASES = {
     "C5_34x28": ("C5", {"batch": 2, "n": (34, 28)}, 3),
     "C3_22x26x14": ("C3", {"n": (22, 26, 14)}, 2),
     "C4_34x10x34x10": ("C4", {"n": (34, 10, 34, 10)}, 2),
+    # the paper's §VI scenario (NEXT-3): coordinated turn, terrain-map altitude with
+    # Gaussian-mixture noise, N_pa = 34 (full size) and a thinner variant
+    "C6_34x18x34x18": ("C6", {"n": (34, 18, 34, 18)}, 3),
+    "C6": ("C6", {}, 1),
 }
 
 

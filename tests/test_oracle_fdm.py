@@ -96,3 +96,28 @@ def test_p20_heat_kernel_reference_solves_the_fpe():
     p0 = conv.mixture(x, comps, q * t)
     d2 = (conv.mixture(x + hx, comps, q * t) - 2 * p0 + conv.mixture(x - hx, comps, q * t)) / hx ** 2
     assert np.max(np.abs(dpdt - 0.5 * q * d2)) < 1e-5 * np.max(np.abs(dpdt))
+
+
+def test_p21_terrain_table_function():
+    """R26 table function: exact on bilinear fields, reproduces the nodes, clamps outside;
+    the GM likelihood integrates to one over z and reduces to a Gaussian for one component."""
+    rng = np.random.default_rng(3)
+    a, b, cxy, d = rng.standard_normal(4)
+    x0, y0, dx, dy = 10.0, -5.0, 2.0, 3.0
+    xs, ys = x0 + dx * np.arange(7), y0 + dy * np.arange(5)
+    X, Y = np.meshgrid(xs, ys)
+    H = a + b * X + cxy * Y + d * X * Y
+    px, py = rng.uniform(xs[0], xs[-1], 50), rng.uniform(ys[0], ys[-1], 50)
+    exact = a + b * px + cxy * py + d * px * py
+    assert np.max(np.abs(O.terrain_height(px, py, H, x0, y0, dx, dy) - exact)) < 1e-12
+    assert np.max(np.abs(O.terrain_height(X, Y, H, x0, y0, dx, dy) - H)) < 1e-12
+    assert abs(O.terrain_height(xs[0] - 50, ys[-1] + 9, H, x0, y0, dx, dy) - H[-1, 0]) < 1e-12
+    table = (H, x0, y0, dx, dy, 0, 1)
+    gm = ((0.5, 0.0, 1.0), (0.5, 20.0, 1.0))
+    pt = np.array([[15.3], [2.2]])
+    h = O.terrain_height(15.3, 2.2, H, x0, y0, dx, dy)
+    zs = np.linspace(h - 15, h + 40, 20001)
+    vals = np.array([O.lik_terrain_gm(pt, z, table, gm)[0] for z in zs])
+    assert abs(np.sum(vals) * (zs[1] - zs[0]) - 1.0) < 1e-6
+    g1 = O.lik_terrain_gm(pt, h + 0.7, table, ((1.0, 0.0, 4.0),))[0]
+    assert abs(g1 - math.exp(-0.5 * 0.49 / 4.0) / math.sqrt(2 * math.pi * 4.0)) < 1e-15

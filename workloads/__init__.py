@@ -21,6 +21,13 @@ SURVEY.md §8(c) (R15-R19) for what the configs leave unspecified:
        R=0.25 I, tau=0.05, 20 epochs                       (configs[3], R18)
 * C5  4096 independent C2-model filters on 128^2, prior means ~ N(0, I),
        cov diag(1,.25), tau=0.05, 50 epochs                (configs[4], R19)
+* C6  the paper's §VI tracking scenario: coordinated turn
+       [px,vx,py,vy] with alpha = 30 deg/s, Q = G G^T = diag(0,1,0,1), prior
+       N((36569,50,55581,50), diag(90,160,5,5)), T_s = 1 s, N_pa = 34; measurement =
+       terrain altitude below the vehicle + 2-component GM noise 1/2 N(0,1) + 1/2
+       N(20,1). The SRTM map is unavailable: the terrain is a seeded analytic field
+       (three sinusoids, ~ +-90 m) sampled on a 10 m table; the truth measurement
+       uses the analytic field, the filter only the table.
 
 Every config uses k_sigma = 6 (R10) and l = 10 Euler substeps per prediction
 interval (R15). Sizes can be overridden to build small parity cases.
@@ -28,6 +35,7 @@ interval (R15). Sizes can be overridden to build small parity cases.
 from __future__ import annotations
 
 import dataclasses
+import math
 from dataclasses import dataclass, field
 from typing import Optional
 
@@ -35,6 +43,7 @@ import numpy as np
 
 LIK_LINEAR_GAUSS = 0
 LIK_RANGE_GAUSS = 1
+LIK_TERRAIN_GM = 2
 
 
 @dataclass
@@ -61,7 +70,7 @@ class Config:
 
     @property
     def nz(self) -> int:
-        return 1 if self.lik_kind == LIK_RANGE_GAUSS else int(self.H.shape[0])
+        return 1 if self.lik_kind in (LIK_RANGE_GAUSS, LIK_TERRAIN_GM) else int(self.H.shape[0])
 
     @property
     def points(self) -> int:
@@ -115,6 +124,18 @@ def make_config(cid: str, **over) -> Config:
                      tau=0.05, l=10, T=20, lik_kind=LIK_LINEAR_GAUSS,
                      H=np.array([[1.0, 0, 0, 0], [0, 0, 1.0, 0]]),
                      R=0.25 * np.eye(2), seed=4)
+    elif cid == "C6":
+        alpha = math.pi / 6.0
+        A = np.zeros((4, 4))
+        A[0, 1] = 1.0
+        A[1, 3] = -alpha
+        A[2, 3] = 1.0
+        A[3, 1] = alpha
+        cfg = Config(name="C6", nx=4, n=(34, 34, 34, 34), batch=1, A=A, Q=np.diag([0.0, 1.0, 0.0, 1.0]),
+                     prior_mean=np.array([[36569.0, 50.0, 55581.0, 50.0]]),
+                     prior_cov=np.diag([90.0, 160.0, 5.0, 5.0]), k_sigma=6.0, tau=1.0, l=10, T=20,
+                     lik_kind=LIK_TERRAIN_GM, seed=6,
+                     extra={"gm": ((0.5, 0.0, 1.0), (0.5, 20.0, 1.0))})
     elif cid == "C5":
         cfg = Config(name="C5", nx=2, n=(128, 128), batch=4096, A=_cv_A(),
                      Q=np.diag([0.0, 0.1]), prior_mean=None,
@@ -127,6 +148,26 @@ def make_config(cid: str, **over) -> Config:
     if cfg.prior_mean is None or cfg.prior_mean.shape[0] != cfg.batch:
         cfg = dataclasses.replace(cfg, prior_mean=_prior_means(cfg))
     return cfg
+
+
+def terrain_field(cfg: Config, x, y):
+    """The C6 synthetic terrain (analytic; seeded phases): altitude [m] at (x, y) [m]."""
+    rng = np.random.Generator(np.random.PCG64(np.random.SeedSequence([cfg.seed, 7])))
+    ph = rng.uniform(0.0, 2.0 * math.pi, 3)
+    return (300.0 + 60.0 * np.sin(2 * math.pi * x / 350.0 + ph[0]) * np.cos(2 * math.pi * y / 420.0 + ph[1])
+            + 25.0 * np.sin(2 * math.pi * (x + y) / 180.0 + ph[2]))
+
+
+def terrain_table(cfg: Config, spacing: float = 10.0, half: float = 900.0):
+    """The map the filter gets: the C6 field sampled on a square table around the prior
+    mean. Returns (heights[r, c], x0, y0, dx, dy, ix, iy): heights[r, c] at
+    (x0 + c dx, y0 + r dy); state components ix = 0 (px), iy = 2 (py)."""
+    mx, my = cfg.prior_mean[0, 0], cfg.prior_mean[0, 2]
+    n = int(round(2 * half / spacing)) + 1
+    xs = mx - half + spacing * np.arange(n)
+    ys = my - half + spacing * np.arange(n)
+    X, Y = np.meshgrid(xs, ys)
+    return terrain_field(cfg, X, Y), float(xs[0]), float(ys[0]), spacing, spacing, 0, 2
 
 
 def _prior_means(cfg: Config) -> np.ndarray:
@@ -191,6 +232,10 @@ def simulate(cfg: Config, T: Optional[int] = None) -> dict:
             xk = truth[b, k]
             if cfg.lik_kind == LIK_RANGE_GAUSS:
                 z[k, b, 0] = np.linalg.norm(xk) + cfg.sigma * rng.standard_normal()
+            elif cfg.lik_kind == LIK_TERRAIN_GM:
+                gm = cfg.extra["gm"]
+                g = rng.choice(len(gm), p=[c[0] for c in gm])
+                z[k, b, 0] = terrain_field(cfg, xk[0], xk[2]) + gm[g][1] + math.sqrt(gm[g][2]) * rng.standard_normal()
             else:
                 z[k, b] = cfg.H @ xk + _psd_sqrt(cfg.R) @ rng.standard_normal(cfg.nz)
     return {"truth": truth, "z": z}
