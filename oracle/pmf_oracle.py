@@ -40,6 +40,8 @@ TRACE_SIGN_PRINTED = +1    # Alg. 4 as printed: (1 + dt tr A)^l
 DIFF_FULL = 0              # R3: D_n = B_n^{-1} Q B_n^{-T} with cross terms
 DIFF_AXIS_LITERAL = 1      # Alg. 2/3 literally: per-axis L^(m), no cross terms
 DIFF_FDM = 2               # NEXT-1: the paper's FDM baseline (eq:FDM), in its FST form (eq:FST)
+STEP_EULER = 0             # the paper's semi-implicit Euler substeps (Alg. 3)
+STEP_CN = 1                # NEXT-4: Crank-Nicolson substeps ("higher order time stepping"; R27)
 
 
 class NoSupportError(RuntimeError):
@@ -256,8 +258,30 @@ def trace_factor(A, dt: float, l: int, sign: int = TRACE_SIGN_PHYSICAL) -> float
     return base ** l
 
 
+def quad_form(D: np.ndarray, n: tuple) -> np.ndarray:
+    """q(k) = sum_m D_mm kappa_m^2 + 2 sum_{m<m'} D_mm' kx_m kx_m' over the full
+    wavenumber grid (kappa = 2 pi k / N, kx = kappa with Nyquist zeroed, R7): the symbol of
+    -div(D grad) in index coordinates, so psi_factor = 1 / (1 + dt/2 q)."""
+    nx = len(n)
+    kap, kapx = [], []
+    for m, N in enumerate(n):
+        k = 2.0 * math.pi * wavenumbers(N) / N
+        kx = k.copy()
+        kx[N // 2] = 0.0
+        shape = [1] * nx
+        shape[m] = N
+        kap.append(k.reshape(shape))
+        kapx.append(kx.reshape(shape))
+    q = np.zeros(n)
+    for a in range(nx):
+        q = q + D[a, a] * kap[a] ** 2
+        for b in range(a + 1, nx):
+            q = q + 2.0 * D[a, b] * kapx[a] * kapx[b]
+    return q
+
+
 def predict_unnormalised(w, c, B, A, Q, tau, l, diff_mode=DIFF_FULL,
-                         trace_sign=TRACE_SIGN_PHYSICAL):
+                         trace_sign=TRACE_SIGN_PHYSICAL, step=STEP_EULER):
     """Alg. 1-5 over one prediction interval tau with l Euler
     substeps dt = tau/l.
 
@@ -274,7 +298,15 @@ def predict_unnormalised(w, c, B, A, Q, tau, l, diff_mode=DIFF_FULL,
     dt = tau / l
     S = dftn(w)
     Psi = np.ones(n)
-    for s_ in range(l):
+    if step == STEP_CN:
+        # R27 Crank-Nicolson for the diffusion d P/dt = -(1/2) q(t) P per wavenumber, with the
+        # moving grid's time-dependent q: P_{n+1} (1 + dt/4 q_{n+1}) = P_n (1 - dt/4 q_n),
+        # q_n on the grid at t_n = n dt (l + 1 grids); second order in dt
+        for s_ in range(l):
+            qa = quad_form(index_diffusion(expm(np.asarray(A) * (s_ * dt)) @ B, Q, diff_mode), n)
+            qb = quad_form(index_diffusion(expm(np.asarray(A) * ((s_ + 1) * dt)) @ B, Q, diff_mode), n)
+            Psi = Psi * (1.0 - 0.25 * dt * qa) / (1.0 + 0.25 * dt * qb)
+    for s_ in range(l if step == STEP_EULER else 0):
         Bn = expm(np.asarray(A) * (s_ * dt)) @ B
         Psi = Psi * psi_factor(index_diffusion(Bn, Q, diff_mode), dt, n)
     S = S * (Psi * trace_factor(A, dt, l, trace_sign))
@@ -286,14 +318,14 @@ def predict_unnormalised(w, c, B, A, Q, tau, l, diff_mode=DIFF_FULL,
     return out.real.copy(), M @ np.asarray(c), M @ np.asarray(B)
 
 
-def predict(w, c, B, A, Q, tau, l, diff_mode=DIFF_FULL, trace_sign=TRACE_SIGN_PHYSICAL):
+def predict(w, c, B, A, Q, tau, l, diff_mode=DIFF_FULL, trace_sign=TRACE_SIGN_PHYSICAL, step=STEP_EULER):
     """Alg. 1-6: the unnormalised update followed by normalisation by explicit
     summation on the moved grid (Alg. 6, R9). Returns (w, c_l, B_l).
     diff_mode DIFF_FDM: the FDM baseline in its FST form (eq:FST), same normalisation."""
     if diff_mode == DIFF_FDM:
         wu, cl, Bl = fst_predict_unnormalised(w, c, B, A, Q, tau, l, trace_sign)
     else:
-        wu, cl, Bl = predict_unnormalised(w, c, B, A, Q, tau, l, diff_mode, trace_sign)
+        wu, cl, Bl = predict_unnormalised(w, c, B, A, Q, tau, l, diff_mode, trace_sign, step)
     return normalise(wu, Bl), cl, Bl
 
 
@@ -540,7 +572,7 @@ def make_likelihood(cfg, X, z):
 
 
 def run_filter(cfg, zs, b: int = 0, T: int | None = None, keep_weights: bool = False,
-               diff_mode: int = DIFF_FULL, trace_sign: int = TRACE_SIGN_PHYSICAL):
+               diff_mode: int = DIFF_FULL, trace_sign: int = TRACE_SIGN_PHYSICAL, step: int = STEP_EULER):
     """Run filter ``b`` of config ``cfg`` on measurements ``zs`` (T+1, batch, nz).
 
     Epoch k: [k>0: predict(tau, l)] -> update(z_k) -> moments -> regrid.
@@ -552,7 +584,7 @@ def run_filter(cfg, zs, b: int = 0, T: int | None = None, keep_weights: bool = F
     rec = {"mean": [], "cov": [], "logC": [], "c": [], "B": [], "w": []}
     for k in range(T + 1):
         if k > 0:
-            w, c, B = predict(w, c, B, cfg.A, cfg.Q, cfg.tau, cfg.l, diff_mode, trace_sign)
+            w, c, B = predict(w, c, B, cfg.A, cfg.Q, cfg.tau, cfg.l, diff_mode, trace_sign, step)
         lik = make_likelihood(cfg, grid_points(c, B, n), zs[k, b])
         w, logC = update(w, c, B, lik)
         mean, cov = moments(w, c, B)

@@ -121,3 +121,51 @@ def test_p21_terrain_table_function():
     assert abs(np.sum(vals) * (zs[1] - zs[0]) - 1.0) < 1e-6
     g1 = O.lik_terrain_gm(pt, h + 0.7, table, ((1.0, 0.0, 4.0),))[0]
     assert abs(g1 - math.exp(-0.5 * 0.49 / 4.0) / math.sqrt(2 * math.pi * 4.0)) < 1e-15
+
+
+def _cn_heat_error(l, step, N=128, q=1.0, tau=0.2, sigma=1.0, half_width=10.0):
+    delta = 2.0 * half_width * sigma / N
+    c, B = np.zeros(1), np.array([[delta]])
+    x = O.grid_points(c, B, (N,))[0]
+    w = np.exp(-0.5 * x ** 2 / sigma ** 2)
+    out, _, _ = O.predict_unnormalised(w, c, B, np.zeros((1, 1)), np.array([[q]]), tau, l, step=step)
+    out = out / (np.sum(out) * delta)
+    s2 = sigma ** 2 + q * tau
+    exact = np.exp(-0.5 * x ** 2 / s2) / math.sqrt(2 * math.pi * s2)
+    return float(np.max(np.abs(out - exact)) / np.max(exact))
+
+
+def test_p22_crank_nicolson_second_order_vs_heat_kernel():
+    """NEXT-4 (R27): Crank-Nicolson substeps converge at second order in dt to the exact
+    heat-kernel solution (the paper's semi-implicit Euler at first order)."""
+    e = [_cn_heat_error(l, O.STEP_CN) for l in (4, 8, 16)]
+    assert 3.5 < e[0] / e[1] < 4.5 and 3.5 < e[1] / e[2] < 4.5, e
+    u = [_cn_heat_error(l, O.STEP_EULER) for l in (4, 8, 16)]
+    assert 1.7 < u[0] / u[1] < 2.3, u
+    assert e[2] < 0.05 * u[2]
+
+
+def test_p23_crank_nicolson_moving_grid_covariance():
+    """On a moving, shearing grid (CV drift) the CN predictor's covariance converges at
+    second order to the continuous-time Kalman-Bucy covariance e^{A t} P e^{A^T t} +
+    int_0^t e^{A s} Q e^{A^T s} ds (Van Loan): the time-dependent diffusion is handled
+    explicit-at-t_n / implicit-at-t_{n+1}."""
+    from scipy.linalg import expm
+    A = np.array([[0.0, 1.0], [0.0, 0.0]])
+    Q = np.diag([0.0, 0.4])
+    P0 = np.diag([1.0, 0.25])
+    n = (96, 96)
+    tau = 1.0
+    c, B = O.design_grid(np.zeros(2), np.diag([4.0, 1.2]), n, 8.0)
+    w = O.gaussian_pdf(O.grid_points(c, B, n), np.zeros(2), P0)
+    M = np.zeros((4, 4))
+    M[:2, :2], M[:2, 2:], M[2:, 2:] = -A, Q, A.T
+    E = expm(M * tau)
+    F = E[2:, 2:].T
+    Pex = F @ P0 @ F.T + F @ E[:2, 2:]
+    errs = []
+    for l in (4, 8, 16):
+        wp, cp, Bp = O.predict(w, c, B, A, Q, tau, l, step=O.STEP_CN)
+        _, cov = O.moments(wp, cp, Bp)
+        errs.append(float(np.max(np.abs(cov - Pex))))
+    assert 3.3 < errs[0] / errs[1] < 4.7 and 3.3 < errs[1] / errs[2] < 4.7, errs
