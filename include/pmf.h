@@ -82,6 +82,9 @@ extern "C" {
                                 nx = 3, 4; N0 = N1 in {32, 64, 96, 128}; N_m in {16, 32, 64, 96, 128} for m >= 2;
                                 substeps <= 64 per predict (longer intervals run on the pencil kernels)       */
 
+#define PMF_STEP_EULER 0
+#define PMF_STEP_CN    1
+
 #define PMF_LIK_LINEAR_GAUSS 0   /* z = H x + v, v ~ N(0, R), nz <= 4 (eq:meas P:36)                               */
 #define PMF_LIK_RANGE_GAUSS  1   /* z = ||x|| + v, v ~ N(0, sigma^2), nz = 1 (C3)                                   */
 #define PMF_LIK_TERRAIN_GM   2   /* the paper's §VI model: z = h(x[ix], x[iy]) + v, h the terrain table
@@ -101,6 +104,10 @@ typedef struct {
     int   path;        /* PMF_PATH_AUTO / PENCIL / RESIDENT                                         */
     int   device;      /* CUDA device ordinal the context lives on                                 */
     void* stream;      /* cudaStream_t to enqueue on; NULL = the legacy default stream             */
+    int   step;        /* PMF_STEP_EULER (0, the paper's semi-implicit Euler substeps)
+                          or PMF_STEP_CN (Crank-Nicolson, second order in dt; R27, "higher order
+                          time stepping" = the paper's future work). CN runs on the plane or
+                          pencil kernels and is not combined with PMF_DIFF_FDM                  */
 } pmf_config;
 
 typedef struct {

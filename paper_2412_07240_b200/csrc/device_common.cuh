@@ -116,10 +116,13 @@ __device__ inline void substep_coefs(int nx, const double* B, const double* Bi, 
         }
     }
     for (int k = 0; k < 10; ++k) o[k] = 0.0;
+    // f_n = 1 + h kappa^T D_n kappa: h = dt/2 (Euler factor 1/f_n), dt/4 (Crank-Nicolson:
+    // (2 - f_n) / f_{n+1})
+    const double h = mp.step ? 0.25 * mp.dt : 0.5 * mp.dt;
     int idx = nx;
     for (int a = 0; a < nx; ++a) {
-        o[a] = 0.5 * mp.dt * D[a * 4 + a];
-        for (int b = a + 1; b < nx; ++b) o[idx++] = mp.dt * 0.5 * (D[a * 4 + b] + D[b * 4 + a]);
+        o[a] = h * D[a * 4 + a];
+        for (int b = a + 1; b < nx; ++b) o[idx++] = h * (D[a * 4 + b] + D[b * 4 + a]);
     }
 }
 
@@ -128,7 +131,7 @@ __device__ inline void epoch_coefs(const double* B, const ModelParams& mp,
     const int nx = mp.nx;
     double Bi[16];
     mat_inv4(nx, B, Bi);
-    for (int s = 0; s < mp.l; ++s) substep_coefs(nx, B, Bi, mp, sub[s], out + 10 * s);
+    for (int s = 0; s < mp.l + (mp.step ? 1 : 0); ++s) substep_coefs(nx, B, Bi, mp, sub[s], out + 10 * s);
 }
 
 __device__ __forceinline__ double det4(int nx, const double* B) {

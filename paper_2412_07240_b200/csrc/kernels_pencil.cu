@@ -125,7 +125,7 @@ __device__ __forceinline__ void acc_mom(double w, const double* u, double* acc) 
 // coefficient block per filter: [0] input scale, [4 .. 4+10l) Euler factors (epoch_coefs),
 // [lq(l) .. +16) likelihood exponent as a quadratic form in the moved grid's index
 // coordinates: e(u) = q[0] + sum_a q[1+a] u_a + sum_{a<=b} q[5+tri(a,b)] u_a u_b
-__host__ __device__ __forceinline__ int lq_off(int l) { return 4 + 10 * l; }
+__host__ __device__ __forceinline__ int lq_off(int l) { return 4 + 10 * (l + 1); }   // room for CN's l + 1 sets
 
 
 // ============================================================================ prep
@@ -148,7 +148,8 @@ __global__ void k_predict_prep(FilterState* st, double* coef, int cstride, Model
         double B0[16], Bi[16];
         for (int i = 0; i < 16; ++i) B0[i] = f.B[i];
         mat_inv4(mp.nx, B0, Bi);
-        for (int n = lane; n < mp.l; n += 32) substep_coefs(mp.nx, B0, Bi, mp, sub[n], cf + 4 + 10 * n);
+        const int nsets = mp.l + (mp.step ? 1 : 0);
+        for (int n = lane; n < nsets; n += 32) substep_coefs(mp.nx, B0, Bi, mp, sub[n], cf + 4 + 10 * n);
     }
     __syncwarp();
     if (lane != 0) return;
@@ -283,8 +284,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_axis_c2c(typename C2<T>::type* 
 #pragma unroll
             for (int q = 0; q < NX; ++q) ntot *= d.ng[q];
             const double mult = mp.s / ntot;
-            const int l = mp.l;
-            const bool cached = l <= LCAP;
+            const int l = mp.l, nsets = l + (mp.step ? 1 : 0);
+            const bool cached = nsets <= LCAP;
             double* pg = reinterpret_cast<double*>(b + P * PS);    // [P][l][2]: gam, bet
             constexpr int L = NX - 1;
             auto pencil_k = [&](long long i, double* kap, double* kx) {
@@ -313,8 +314,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_axis_c2c(typename C2<T>::type* 
                 bet = bb;
             };
             if (cached) {
-                for (int t = threadIdx.x; t < P * l; t += blockDim.x) {
-                    const int p = t / l, n = t - p * l;
+                for (int t = threadIdx.x; t < P * nsets; t += blockDim.x) {
+                    const int p = t / nsets, n = t - p * nsets;
                     const long long i = i0 + p;
                     double kap[4] = {0, 0, 0, 0}, kx[4] = {0, 0, 0, 0};
                     if (i < I) pencil_k(i, kap, kx);
@@ -332,21 +333,28 @@ __global__ void __launch_bounds__(kThreads, 2) k_axis_c2c(typename C2<T>::type* 
                 double kapL, kxL;
                 wavenum(j, N, kapL, kxL);
                 const double kL2 = kapL * kapL;
-                double prod = 1.0;
-                if (cached) {
-                    const double* g = pg + 2 * p * l;
-                    for (int n = 0; n < l; ++n)
-                        prod *= fma(cf[10 * n + L], kL2, fma(g[2 * n + 1], kxL, g[2 * n]));
-                } else {
-                    double kap[4] = {0, 0, 0, 0}, kx[4] = {0, 0, 0, 0};
-                    pencil_k(i, kap, kx);
-                    for (int n = 0; n < l; ++n) {
-                        double g, bb;
-                        gam_bet(kap, kx, n, g, bb);
-                        prod *= fma(cf[10 * n + L], kL2, fma(bb, kxL, g));
+                // Euler: 1 / prod_{n<l} f_n; Crank-Nicolson: prod_{n<l} (2 - f_n) / prod_{n=1..l} f_n
+                double prod = 1.0, num = 1.0;
+                const double* g = pg + 2 * p * nsets;
+                double kap[4] = {0, 0, 0, 0}, kx[4] = {0, 0, 0, 0};
+                if (!cached) pencil_k(i, kap, kx);
+                for (int n = 0; n < nsets; ++n) {
+                    double gg, bb;
+                    if (cached) {
+                        gg = g[2 * n];
+                        bb = g[2 * n + 1];
+                    } else {
+                        gam_bet(kap, kx, n, gg, bb);
+                    }
+                    const double fn = fma(cf[10 * n + L], kL2, fma(bb, kxL, gg));
+                    if (!mp.step) {
+                        prod *= fn;
+                    } else {
+                        if (n < l) num *= 2.0 - fn;
+                        if (n > 0) prod *= fn;
                     }
                 }
-                const T ps = (T)(mult / prod);
+                const T ps = (T)(mult * num / prod);
                 V v = r[p * PS + sx<NC>(j)];
                 r[p * PS + sx<NC>(j)] = V{v.x * ps, v.y * ps};
             }
@@ -492,9 +500,14 @@ __global__ void __launch_bounds__(kThreads, 2) k_line_psi(T* __restrict__ W, Fil
     for (int k = threadIdx.x; k < N; k += blockDim.x) {
         double kap, kx;
         wavenum(k, N, kap, kx);
-        double prod = 1.0;
-        for (int n = 0; n < mp.l; ++n) prod *= fma(cf[4 + 10 * n], kap * kap, 1.0);
-        const T ps = (T)(mult / prod);
+        double prod = 1.0, num = 1.0;
+        if (!mp.step) {
+            for (int n = 0; n < mp.l; ++n) prod *= fma(cf[4 + 10 * n], kap * kap, 1.0);
+        } else {          // Crank-Nicolson (R27)
+            for (int n = 0; n < mp.l; ++n) num *= 1.0 - cf[4 + 10 * n] * kap * kap;
+            for (int n = 1; n <= mp.l; ++n) prod *= fma(cf[4 + 10 * n], kap * kap, 1.0);
+        }
+        const T ps = (T)(mult * num / prod);
         V v = r[sx<NC>(k)];
         r[sx<NC>(k)] = V{v.x * ps, v.y * ps};
     }
@@ -1040,7 +1053,7 @@ static cudaError_t predict_nd(const Dims& d, PencilBufs& b, const Twiddles& tw, 
         const int P = pencils_per_cta(N);
         FFTPlan pl = make_plan(N);
         size_t sm = 2 * (size_t)P * pstride_host(N) * sizeof(V);
-        if (mode == 2) sm += sizeof(double) * 2 * P * std::min(mp.l, LCAP);
+        if (mode == 2) sm += sizeof(double) * 2 * P * std::min(mp.l + (mp.step ? 1 : 0), LCAP);
         long long nblk = O * ((I + P - 1) / P);
         if (nblk == 0) return cudaSuccess;
         cudaError_t e = with_nc(N, [&](auto nc) -> cudaError_t {

@@ -274,7 +274,7 @@ __global__ void k_plane_prep(FilterState* st, double* coef, int cs, ModelParams 
     if (skip) return;
     double Bi0[16];
     mat_inv4(NX, B0, Bi0);
-    for (int n = lane; n < mp.l; n += 32) substep_coefs(NX, B0, Bi0, mp, sub[n], P + PL_EU + 10 * n);
+    for (int n = lane; n < mp.l + (mp.step ? 1 : 0); n += 32) substep_coefs(NX, B0, Bi0, mp, sub[n], P + PL_EU + 10 * n);
     if (lane != 0) return;
     double Bl[16], cl[4];
     for (int i = 0; i < 16; ++i) Bl[i] = 0.0;
@@ -598,6 +598,7 @@ struct MidArgs {
     int ocpf;                // o values per filter (MODE 2: 1)
     int N0, H1, n2, n3;      // plane sizes, axis-2/3 sizes (wavenumber decode, split regrid)
     int l;
+    int step;                // 0 Euler, 1 Crank-Nicolson (R27)
     int skip4;               // MODE 0: leave filters with a split regrid map (flag 4) to MODE 3
     double* dc3;             // MODE 3: [filter][n3] slab sums of the regridded weights
 };
@@ -623,7 +624,7 @@ template <typename T, int NA, int VAR>
 static size_t mid_smem(int l, int sets) {
     using C = MidCfg<T, NA, VAR>;
     return sizeof(typename C2<T>::type) * ((size_t)sets * C::NS * NA * C::PP + NA) + 16 * 4 +
-           sizeof(double2) * C::TP * 3 * ((l + 1) / 2);
+           sizeof(double2) * C::TP * 3 * ((l + 1) / 2) * 2;   // den (+ CN num) quartic tables
 }
 
 template <typename T, int NA, int MODE, int NX, int VAR>
@@ -783,8 +784,10 @@ __global__ void __launch_bounds__(MidCfg<T, NA, VAR>::NT, MidCfg<T, NA, VAR>::MI
             // PSD), so the quartic evaluation is well conditioned.
             const double* P = a.coef + filt * a.cs;
             const double* cf = P + PL_EU;
-            const int npair = a.l >> 1, nq = (a.l + 1) >> 1;
-            double2* qt = psi + p * 3 * nq;                   // [nq][3]: (c0,c1) (c2,c3) (c4,-)
+            // Euler: den factors f_n, n < l. Crank-Nicolson (R27): den f_n, n = 1..l, and num
+            // (2 - f_n), n < l -- each list paired into quartics
+            const int nq = (a.l + 1) >> 1, cn = a.step;
+            double2* qt = psi + p * 3 * nq * (1 + cn);         // [1+cn][nq][3]: (c0,c1) (c2,c3) (c4,nyq)
             {
                 // wavenumbers of the pencil's other axes: inner i = (j2 *) H1 N0 + k1 N0 + k0
                 double kap[3] = {0, 0, 0}, kx[3] = {0, 0, 0};
@@ -817,19 +820,33 @@ __global__ void __launch_bounds__(MidCfg<T, NA, VAR>::NT, MidCfg<T, NA, VAR>::MI
                         bb = fma(c[pair_index(NX, a2, L)], kx[a2], bb);
                     }
                 };
-                for (int j = t; j < nq; j += 8) {
+                for (int jj = t; jj < nq * (1 + cn); jj += 8) {
+                    const int list = jj / nq, j = jj - list * nq;       // list 0: den, 1: num
+                    const int base = (list == 0 && cn) ? 1 : 0;       // CN den: f_1 .. f_l
                     double g0, b0, g1 = 1.0, b1 = 0.0, a1 = 0.0;
-                    gam_bet(2 * j, g0, b0);
-                    const double a0 = cf[10 * (2 * j) + L];
-                    if (2 * j + 1 < a.l) {
-                        gam_bet(2 * j + 1, g1, b1);
-                        a1 = cf[10 * (2 * j + 1) + L];
+                    gam_bet(base + 2 * j, g0, b0);
+                    double a0 = cf[10 * (base + 2 * j) + L];
+                    const bool two = 2 * j + 1 < a.l;
+                    if (two) {
+                        gam_bet(base + 2 * j + 1, g1, b1);
+                        a1 = cf[10 * (base + 2 * j + 1) + L];
+                    }
+                    if (list == 1) {                                  // 2 - f = (2 - g) - b k - a k^2
+                        g0 = 2.0 - g0;
+                        b0 = -b0;
+                        a0 = -a0;
+                        if (two) {
+                            g1 = 2.0 - g1;
+                            b1 = -b1;
+                            a1 = -a1;
+                        }
                     }
                     // the Nyquist wavenumber has kx = 0 in the first-order terms (R7): its pair value
                     constexpr double kn2 = PMF_PI * PMF_PI;
-                    qt[3 * j] = double2{g0 * g1, fma(g0, b1, b0 * g1)};
-                    qt[3 * j + 1] = double2{fma(g0, a1, fma(b0, b1, a0 * g1)), fma(b0, a1, a0 * b1)};
-                    qt[3 * j + 2] = double2{a0 * a1, fma(a0, kn2, g0) * fma(a1, kn2, g1)};
+                    double2* q = qt + 3 * jj;
+                    q[0] = double2{g0 * g1, fma(g0, b1, b0 * g1)};
+                    q[1] = double2{fma(g0, a1, fma(b0, b1, a0 * g1)), fma(b0, a1, a0 * b1)};
+                    q[2] = double2{a0 * a1, fma(a0, kn2, g0) * fma(a1, kn2, g1)};
                 }
             }
             __syncwarp();
@@ -843,20 +860,27 @@ __global__ void __launch_bounds__(MidCfg<T, NA, VAR>::NT, MidCfg<T, NA, VAR>::MI
                     kp[r] = (2.0 * PMF_PI / NA) * (k < NA / 2 ? k : k - NA);
                     den[r] = 1.0;
                 }
-                for (int j = 0; j < nq; ++j) {
-                    const double2 q01 = qt[3 * j], q23 = qt[3 * j + 1], q4 = qt[3 * j + 2];
+                auto prodq = [&](const double2* tb, double* acc) {
+                    for (int j = 0; j < nq; ++j) {
+                        const double2 q01 = tb[3 * j], q23 = tb[3 * j + 1], q4 = tb[3 * j + 2];
 #pragma unroll
-                    for (int r = 0; r < R1; ++r) {
-                        const double x1 = kp[r];
-                        den[r] *= fma(fma(fma(fma(q4.x, x1, q23.y), x1, q23.x), x1, q01.y), x1, q01.x);
+                        for (int r = 0; r < R1; ++r) {
+                            const double x1 = kp[r];
+                            acc[r] *= fma(fma(fma(fma(q4.x, x1, q23.y), x1, q23.x), x1, q01.y), x1, q01.x);
+                        }
                     }
-                }
-                if (t == ((NA / 2) & 7)) {
-                    constexpr int rn = (NA / 2) >> 3;
-                    double d = 1.0;
-                    for (int j = 0; j < nq; ++j) d *= qt[3 * j + 2].y;
-                    den[rn] = d;
-                }
+                    if (t == ((NA / 2) & 7)) {
+                        constexpr int rn = (NA / 2) >> 3;
+                        double d = 1.0;
+                        for (int j = 0; j < nq; ++j) d *= tb[3 * j + 2].y;
+                        acc[rn] = d;
+                    }
+                };
+                prodq(qt, den);
+                double numr[R1];
+#pragma unroll
+                for (int r = 0; r < R1; ++r) numr[r] = 1.0;
+                if (cn) prodq(qt + 3 * nq, numr);
                 const double mult = P[PL_SN];
                 double ps[R1];
                 if constexpr (R1 % 4 != 0) {
@@ -882,7 +906,7 @@ __global__ void __launch_bounds__(MidCfg<T, NA, VAR>::NT, MidCfg<T, NA, VAR>::MI
                     }
                 }
 #pragma unroll
-                for (int r = 0; r < R1; ++r) reinterpret_cast<double*>(col + (t + 8 * r) * PP)[0] = ps[r];
+                for (int r = 0; r < R1; ++r) reinterpret_cast<double*>(col + (t + 8 * r) * PP)[0] = ps[r] * numr[r];
             }
             __syncwarp();
             if (s_on<R1>(t)) {
@@ -1360,7 +1384,7 @@ __global__ void k_plane_fin(FilterState* st, const double* __restrict__ coef, in
 using namespace pln;
 
 bool plane_supported(const Dims& d, int l) {
-    if (d.nx < 3 || d.n[0] != d.n[1] || l > LCAP) return false;
+    if (d.nx < 3 || d.n[0] != d.n[1] || l + 1 > LCAP) return false;
     const int N = d.n[0];
     if (N != 32 && N != 64 && N != 96 && N != 128) return false;
     for (int m = 2; m < d.nx; ++m) {
@@ -1556,6 +1580,7 @@ static cudaError_t plane_t(const Dims& d, PencilBufs& b, const ModelParams& mp, 
         ma.n2 = n2;
         ma.n3 = n3;
         ma.l = mp.l;
+        ma.step = mp.step;
         ma.skip4 = skip4;
         ma.dc3 = pa.dc3;
         ++*launches;

@@ -200,6 +200,8 @@ static int prepare_model(pmf_ctx* c, double dt, int steps) {
     mp.nx = nx;
     mp.l = steps;
     mp.diff_mode = c->cfg.diff_mode;
+    mp.step = c->cfg.step;
+    const int nsets = steps + (mp.step ? 1 : 0);      // Crank-Nicolson: grids t_0 .. t_l
     mp.dt = dt;
     double trA = 0.0;
     for (int a = 0; a < nx; ++a) trA += c->A[a * 4 + a];
@@ -209,8 +211,8 @@ static int prepare_model(pmf_ctx* c, double dt, int steps) {
     for (int i = 0; i < 16; ++i) M[i] = c->A[i] * (dt * steps);
     expm4(nx, M, mp.Mtau);
     std::memcpy(mp.Q, c->Q, sizeof(mp.Q));
-    std::vector<SubstepEntry> tab(steps);
-    for (int s = 0; s < steps; ++s) {
+    std::vector<SubstepEntry> tab(nsets);
+    for (int s = 0; s < nsets; ++s) {
         double Mn[16], En[16], EnT[16], T1[16];
         for (int i = 0; i < 16; ++i) Mn[i] = -c->A[i] * (dt * s);
         expm4(nx, Mn, En);                            // e^{-A n dt}
@@ -221,7 +223,7 @@ static int prepare_model(pmf_ctx* c, double dt, int steps) {
         for (int i = 0; i < 16; ++i) Mn[i] = c->A[i] * (dt * s);
         expm4(nx, Mn, tab[s].P);
     }
-    size_t need = sizeof(SubstepEntry) * steps;
+    size_t need = sizeof(SubstepEntry) * nsets;
     if (need > c->sub_bytes) {
         if (c->sub) { cudaFree(c->sub); c->bytes -= (int64_t)c->sub_bytes; c->sub = nullptr; }
         int r = dalloc(c, (void**)&c->sub, need);
@@ -512,7 +514,9 @@ int pmf_validate_model(const pmf_config* cfg, const double* A, const double* Q, 
     if (cfg->dtype != PMF_F64 && cfg->dtype != PMF_F32) return fail(nullptr, PMF_E_ARG, "bad dtype");
     if (cfg->diff_mode != PMF_DIFF_FULL && cfg->diff_mode != PMF_DIFF_AXIS_LITERAL && cfg->diff_mode != PMF_DIFF_FDM)
         return fail(nullptr, PMF_E_ARG, "bad diff_mode");
+    if (cfg->step != PMF_STEP_EULER && cfg->step != PMF_STEP_CN) return fail(nullptr, PMF_E_ARG, "bad step");
     if (cfg->diff_mode == PMF_DIFF_FDM) {
+        if (cfg->step != PMF_STEP_EULER) return fail(nullptr, PMF_E_ARG, "FDM predictor: explicit steps only");
         if (cfg->dtype != PMF_F64) return fail(nullptr, PMF_E_ARG, "FDM predictor: fp64 only");
         for (int m = 0; m < nx; ++m)
             if (cfg->n[m] != 32 && cfg->n[m] != 64 && cfg->n[m] != 96 && cfg->n[m] != 128)
@@ -624,7 +628,7 @@ int pmf_create(const pmf_config* cfg, const double* A, const double* Q, pmf_ctx*
     d.src_lo = 0;
     d.src_n = d.n[nx - 1];
 
-    bool res_ok = resident_supported(d, c->dtype);
+    bool res_ok = resident_supported(d, c->dtype) && cfg->step == PMF_STEP_EULER;
     bool plane_ok = plane_supported(d, 1);
     if (cfg->path == PMF_PATH_RESIDENT && !res_ok) {
         delete c;

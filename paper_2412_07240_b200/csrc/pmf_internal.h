@@ -26,14 +26,16 @@ struct FilterState {
 
 // Model constants of one prediction interval (host computed, kernel param).
 struct ModelParams {
-    int nx, l, diff_mode, pad;
+    int nx, l, diff_mode, step;   // step: 0 semi-implicit Euler, 1 Crank-Nicolson (R27):
+                                  // then l + 1 coefficient sets (grids t_0 .. t_l) scaled dt/4
     double dt;          // Euler substep
     double s;           // trace factor (1 -/+ dt tr A)^l (R5)
     double Mtau[16];    // e^{A tau}, row stride 4
     double Q[16];
 };
 
-// Device table, one entry per substep n < l (host computed, uploaded per predict):
+// Device table, one entry per substep n < l (n <= l for Crank-Nicolson; host computed,
+// uploaded per predict):
 //   E_n = e^{-A n dt} Q e^{-A^T n dt}   (so D_n = B^-1 E_n B^-T, R3)
 //   P_n = e^{A n dt}                    (B_n = P_n B, for AXIS_LITERAL)
 struct SubstepEntry {
@@ -73,7 +75,7 @@ struct Dims {
 // pencil path: 4 + 10 l + 16 (scale, Euler factors, likelihood quadratic form);
 // resident path: 24 + 3 l rounded up to even (kernels_resident.cu)
 // plane path: 64 + 10 l (kernels_plane.cu)
-inline int coef_stride(int l) { return 64 + 10 * l; }
+inline int coef_stride(int l) { return 80 + 10 * l; }   // (Crank-Nicolson: l + 1 coefficient sets)
 
 // ---------------------------------------------------------------------------
 // launchers (implemented in the .cu files); all return a cudaError_t and

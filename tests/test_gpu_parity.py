@@ -250,3 +250,18 @@ def test_graph_replay_bitwise_equal(cid, over):
     a, b = outs
     assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1]) and np.array_equal(a[3], b[3])
     assert a[4] == b[4]
+
+
+@pytest.mark.parametrize("name", ["C1", "C2s", "C3s", "C4s", "C5s", "C3_plane_32", "C4_plane_32"])
+def test_crank_nicolson_parity(name):
+    """NEXT-4: Crank-Nicolson substeps (R27) through the C ABI vs the oracle's STEP_CN on
+    the pencil kernels (resident falls back to them) and the plane kernels."""
+    extra = {"C3_plane_32": ("C3", {"n": (32, 32, 16)}, 2), "C4_plane_32": ("C4", {"n": (32, 32, 16, 16)}, 2)}
+    cid, over, T = extra.get(name) or CASES[name]
+    cfg = make_config(cid, **over)
+    zs = simulate(cfg, T=T)["z"]
+    g = run_gpu(cfg, zs, T, step=pmf.STEP_CN)
+    orc = {b: O.run_filter(cfg, zs, b=b, T=T, keep_weights=True, step=O.STEP_CN) for b in range(cfg.batch)}
+    e = compare_runs(cfg, g, orc, T, 1e-10)
+    assert e["w"] <= 1e-10, e
+    assert e["mean"] <= 1e-10 and e["cov"] <= 1e-10 and e["logC"] <= 1e-10 and e["grid"] <= 1e-10, e
