@@ -599,17 +599,15 @@ struct MidArgs {
     int N0, H1, n2, n3;      // plane sizes, axis-2/3 sizes (wavenumber decode, split regrid)
     int l;
     int step;                // 0 Euler, 1 Crank-Nicolson (R27)
-    int skip4;               // MODE 0: leave filters with a split regrid map (flag 4) to MODE 3
-    double* dc3;             // MODE 3: [filter][n3] slab sums of the regridded weights
+    int skip4;               // MODE 0: leave filters with a split regrid map (flag 4) to k_plane_split
+    double* dc3;             // k_plane_split: [filter][n3] slab sums of the regridded weights
 };
 
 // tile shape / pipeline variants: TP pencils per tile, NS stages, MINB CTAs per SM
 template <int V_> struct MidVar;
 template <> struct MidVar<0> { static constexpr int TP = 32, NS = 2, MINB = 2; };   // small pencils
 template <> struct MidVar<1> { static constexpr int TP = 32, NS = 4, MINB = 1; };   // 96: 4-deep ring
-template <> struct MidVar<2> { static constexpr int TP = 32, NS = 2, MINB = 1; };   // 96, MODE 3 (2 sets)
 template <> struct MidVar<3> { static constexpr int TP = 32, NS = 3, MINB = 1; };   // 128
-template <> struct MidVar<4> { static constexpr int TP = 16, NS = 2, MINB = 1; };   // 128, MODE 3
 
 template <typename T, int NA, int VAR>
 struct MidCfg {
@@ -633,10 +631,9 @@ __global__ void __launch_bounds__(MidCfg<T, NA, VAR>::NT, MidCfg<T, NA, VAR>::MI
     using C = MidCfg<T, NA, VAR>;
     constexpr int R1 = NA / 8, TP = C::TP, PP = C::PP, NS = C::NS;
     constexpr int L = NX - 1;                                 // this pass's axis when MODE == 2
-    constexpr int SETS = MODE == 3 ? 2 : 1;                   // MODE 3 stages the two j3 rows it blends
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    V* stg = reinterpret_cast<V*>(smem_raw);                  // [NS][SETS][NA][PP]
-    V* tw = stg + NS * SETS * NA * PP;                        // [NA]
+    V* stg = reinterpret_cast<V*>(smem_raw);                  // [NS][NA][PP]
+    V* tw = stg + NS * NA * PP;                               // [NA]
     unsigned long long* bar = reinterpret_cast<unsigned long long*>(tw + NA);   // [NS] (<= 4)
     double2* psi = reinterpret_cast<double2*>(bar + 4);       // [TP][l] (gam, bet)
     const int tid = threadIdx.x, p = tid >> 3, t = tid & 7;
@@ -649,22 +646,14 @@ __global__ void __launch_bounds__(MidCfg<T, NA, VAR>::NT, MidCfg<T, NA, VAR>::MI
     long long act_f = -1;                                     // one-filter cache (filters span many tiles)
     bool act_v = true;
     auto active = [&](long long f) -> bool {
-        if (MODE != 3 && !(MODE == 0 && a.skip4)) return true;
+        if (!(MODE == 0 && a.skip4)) return true;
         if (f != act_f) {
             const double* P = a.coef + f * a.cs;
-            const bool split = P[PL_SKIP] == 0.0 && (int)P[PL_FLAG] == 4;
-            act_v = MODE == 3 ? split : !split;
+            const bool split = P[PL_SKIP] == 0.0 && (int)P[PL_FLAG] == 4;   // handled by k_plane_split
+            act_v = !split;
             act_f = f;
         }
         return act_v;
-    };
-    // old-grid rows j3 blended into output slab u3' (MODE 3): weights and validity
-    auto rows3 = [&](const double* P, long long u3i, int& j3, double& w3) {
-        const double v3 = fma(P[PL_M + 15], (double)u3i - 0.5 * (a.n3 - 1), P[PL_O + 3]);
-        const double f = floor(v3);
-        const int fi = __double2int_rz(f);
-        j3 = min(max(fi, -2), a.n3);
-        w3 = (fi == j3) ? v3 - f : 0.0;
     };
     // tiles of inactive filters are neither staged nor waited for (their stage's phase is not used)
     auto issue = [&](long long blk, int st) {
@@ -675,20 +664,6 @@ __global__ void __launch_bounds__(MidCfg<T, NA, VAR>::NT, MidCfg<T, NA, VAR>::MI
         const long long filt = (unsigned)o / (unsigned)a.ocpf;
         if (!active(filt)) return;
         tma::fence_proxy_async();
-        if (MODE == 3) {
-            const double* P = a.coef + filt * a.cs;
-            int j3;
-            double w3;
-            rows3(P, o - filt * a.ocpf, j3, w3);
-            const bool va = j3 >= 0 && j3 < a.n3, vb = j3 + 1 >= 0 && j3 + 1 < a.n3;
-            if (tid == 0) tma::mbar_expect_tx(&bar[st], bytes * NA * ((va ? 1 : 0) + (vb ? 1 : 0)));
-            const long long ob = filt * a.ocpf + j3;
-            if (va) tma::bulk_g2s(stg + ((st * 2) * NA + tid) * PP, a.S + (ob * NA + tid) * a.I + i0, bytes, &bar[st]);
-            if (vb)
-                tma::bulk_g2s(stg + ((st * 2 + 1) * NA + tid) * PP, a.S + ((ob + 1) * NA + tid) * a.I + i0, bytes,
-                              &bar[st]);
-            return;
-        }
         if (tid == 0) tma::mbar_expect_tx(&bar[st], bytes * NA);
         tma::bulk_g2s(stg + (st * NA + tid) * PP, a.S + (o * NA + tid) * a.I + i0, bytes, &bar[st]);
     };
@@ -713,59 +688,10 @@ __global__ void __launch_bounds__(MidCfg<T, NA, VAR>::NT, MidCfg<T, NA, VAR>::MI
         tma::mbar_wait(&bar[st], (phase >> st) & 1u);
         phase ^= 1u << st;
         V* base = a.Sout + o * (long long)NA * a.I + (valid ? i : 0);
-        V* col = stg + st * SETS * NA * PP + p;
+        V* col = stg + st * NA * PP + p;
         V x[R1], pa[8], pb[8];
-        if (MODE == 3) {
-            // split regrid (R12), axes 3 then 2: Z(j2) = (1 - w3) S(j2, j3) + w3 S(j2, j3 + 1), then
-            // Y(u2') = linear interpolation of Z at v2 = o2 + M22 u2' + M23 u3' (zero ghosts)
-            const double* P = a.coef + filt * a.cs;
-            const long long u3i = o - filt * a.ocpf;
-            int j3;
-            double w3;
-            rows3(P, u3i, j3, w3);
-            const bool va = j3 >= 0 && j3 < a.n3, vb = j3 + 1 >= 0 && j3 + 1 < a.n3;
-            const V* colb = col + NA * PP;
 #pragma unroll
-            for (int r = 0; r < R1; ++r) {
-                const int j2 = t + 8 * r;
-                V zz = V{T(0), T(0)};
-                if (va) {
-                    const V v = col[j2 * PP];
-                    zz = V{(T)((1.0 - w3) * v.x), (T)((1.0 - w3) * v.y)};
-                }
-                if (vb) {
-                    const V v = colb[j2 * PP];
-                    zz = V{(T)fma(w3, (double)v.x, (double)zz.x), (T)fma(w3, (double)v.y, (double)zz.y)};
-                }
-                col[j2 * PP] = zz;
-            }
-            __syncwarp();
-            const double M22 = P[PL_M + 10], M23 = P[PL_M + 11], o2 = P[PL_O + 2];
-            const double vb2 = fma(M23, (double)u3i - 0.5 * (a.n3 - 1), o2);
-            double dcs = 0.0;
-#pragma unroll
-            for (int r = 0; r < R1; ++r) {
-                const double v2 = fma(M22, (t + 8 * r) - 0.5 * (NA - 1), vb2);
-                const double f = floor(v2);
-                const int fi = __double2int_rz(f);
-                const double fr = v2 - f;
-                const V lo = (fi >= 0 && fi < NA) ? col[fi * PP] : V{T(0), T(0)};
-                const V hi = (fi + 1 >= 0 && fi + 1 < NA) ? col[(fi + 1) * PP] : V{T(0), T(0)};
-                x[r] = V{(T)fma(fr, (double)hi.x - (double)lo.x, (double)lo.x),
-                         (T)fma(fr, (double)hi.y - (double)lo.y, (double)lo.y)};
-                dcs += (double)x[r].x;
-            }
-            if (i == 0) {      // pencil k0 = k1 = 0: sum of this slab's regridded weights
-                const unsigned tm = 0xFFu << ((tid & 31) & ~7);   // this team's 8 lanes
-                dcs += __shfl_xor_sync(tm, dcs, 1);
-                dcs += __shfl_xor_sync(tm, dcs, 2);
-                dcs += __shfl_xor_sync(tm, dcs, 4);
-                if (t == 0) a.dc3[filt * a.n3 + u3i] = dcs;
-            }
-        } else {
-#pragma unroll
-            for (int r = 0; r < R1; ++r) x[r] = col[(t + 8 * r) * PP];
-        }
+        for (int r = 0; r < R1; ++r) x[r] = col[(t + 8 * r) * PP];
         team_dft<R1, MODE == 1>(x, pa, pb, col, tw, t, slot);
         if (MODE != 2) {
             if (valid && s_on<R1>(t)) {
@@ -1411,7 +1337,7 @@ static cudaError_t occ_grid(K kern, int nt, size_t smem, long long work, int* gr
 template <typename T, int NA, int NX, int VAR, int MODE>
 static cudaError_t mid_launch(MidArgs<T> ma, cudaStream_t s) {
     using C = MidCfg<T, NA, VAR>;
-    const size_t smem = mid_smem<T, NA, VAR>(MODE == 2 ? ma.l : 0, MODE == 3 ? 2 : 1);
+    const size_t smem = mid_smem<T, NA, VAR>(MODE == 2 ? ma.l : 0, 1);
     const long long work = ma.O * ((ma.I + C::TP - 1) / C::TP);
     int grid = 1;
     cudaError_t e = occ_grid(k_plane_mid<T, NA, MODE, NX, VAR>, C::NT, smem, work, &grid);
@@ -1425,36 +1351,15 @@ static cudaError_t mid_var(MidArgs<T> ma, int mode, cudaStream_t s) {
     switch (mode) {
         case 0: return mid_launch<T, NA, NX, VAR, 0>(ma, s);
         case 1: return mid_launch<T, NA, NX, VAR, 1>(ma, s);
-        case 2: return mid_launch<T, NA, NX, VAR, 2>(ma, s);
-        default:
-            if constexpr (NX == 4) return mid_launch<T, NA, NX, VAR, 3>(ma, s);
-            return cudaErrorInvalidValue;
+        default: return mid_launch<T, NA, NX, VAR, 2>(ma, s);
     }
-}
-
-static int mid_variant(int mode) {
-    static int v[4] = {-2, -2, -2, -2};
-    if (v[mode] == -2) {
-        const char* names[4] = {"PMF_MID_VAR_FWD", "PMF_MID_VAR_INV", "PMF_MID_VAR_PSI", "PMF_MID_VAR_SPLIT"};
-        const char* e = getenv(names[mode]);
-        v[mode] = e ? atoi(e) : -1;
-    }
-    return v[mode];
 }
 
 // measured on B200 (C4 96^4): a 4-deep ring at one CTA per SM beats 2 x (2-deep) by 20 %
 template <typename T, int NA, int NX>
 static cudaError_t mid_na(MidArgs<T> ma, int mode, cudaStream_t s) {
-    const int over = mid_variant(mode);
-    if (NA == 96) {
-        if (mode == 3) return mid_var<T, NA, NX, 2>(ma, mode, s);
-        if (over == 0) return mid_var<T, NA, NX, 0>(ma, mode, s);
-        return mid_var<T, NA, NX, 1>(ma, mode, s);
-    }
-    if (NA == 128) {
-        if (mode == 3) return mid_var<T, NA, NX, 4>(ma, mode, s);
-        return mid_var<T, NA, NX, 3>(ma, mode, s);
-    }
+    if (NA == 96) return mid_var<T, NA, NX, 1>(ma, mode, s);
+    if (NA == 128) return mid_var<T, NA, NX, 3>(ma, mode, s);
     return mid_var<T, NA, NX, 0>(ma, mode, s);
 }
 
