@@ -42,6 +42,7 @@ WORKLOADS = {
     "C2": dict(cid="C2", over={}),
     "C1": dict(cid="C1", over={}),
     # NEXT-1: the paper's FDM baseline (eq:FST) on the C5 batch, DST-I on FP64 tensor cores
+    "C5l1": dict(cid="C5", over={"l": 1}),      # report l = 1 next to l = 10
     "C5fdm": dict(cid="C5", over={}, diff_mode=2),
     # NEXT-3: the paper's §VI scenario (coordinated turn, terrain altitude + GM noise, N_pa = 34)
     "C6": dict(cid="C6", over={}),
@@ -461,7 +462,7 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     line = run_workload(args, args.workload, rank, world, local)
-    also_list = ("C4,C3,C5fdm,C6" if args.workload == "C5" else "") if args.also == "auto" else args.also
+    also_list = ("C5l1,C4,C3,C5fdm,C6" if args.workload == "C5" else "") if args.also == "auto" else args.also
     if also_list and world == 1:
         # the other large single-GPU configurations, measured the same way (compact)
         also = {}

@@ -101,7 +101,7 @@ typedef struct {
     int   dtype;       /* PMF_F64 or PMF_F32 (storage + transform precision; reductions are fp64)   */
     int   diff_mode;   /* PMF_DIFF_FULL (default 0), PMF_DIFF_AXIS_LITERAL or PMF_DIFF_FDM         */
     int   trace_sign;  /* PMF_TRACE_PHYSICAL (0 is read as PHYSICAL) or PMF_TRACE_PRINTED          */
-    int   path;        /* PMF_PATH_AUTO / PENCIL / RESIDENT                                         */
+    int   path;        /* PMF_PATH_AUTO / PENCIL / RESIDENT / PLANE                                 */
     int   device;      /* CUDA device ordinal the context lives on                                 */
     void* stream;      /* cudaStream_t to enqueue on; NULL = the legacy default stream             */
     int   step;        /* PMF_STEP_EULER (0, the paper's semi-implicit Euler substeps)
@@ -141,10 +141,6 @@ const char* pmf_last_error(const pmf_ctx* ctx);
  * mean: host batch x nx; cov: host batch x nx x nx (SPD). */
 int pmf_set_gaussian(pmf_ctx* ctx, const double* mean, const double* cov, double k_sigma);
 
-/* Set an arbitrary state: grid (center: host batch x nx, B: host batch x nx x nx)
- * and weights (batch x N_total in dtype, host or device per weights_on_device;
- * a device pointer must be on cfg->device). The weights are normalised on
- * entry (vol * sum w = 1). PMF_E_SINGULAR_GRID if some B is singular. */
 /* Terrain table for PMF_LIK_TERRAIN_GM ("a table function that assigns
  * altitude to each combination of ... it covers"): heights[r * ncol + c] is the
  * altitude at (x0 + c dx, y0 + r dy); state components ix, iy are the horizontal
@@ -154,6 +150,10 @@ int pmf_set_gaussian(pmf_ctx* ctx, const double* mean, const double* cov, double
 int pmf_set_terrain(pmf_ctx* ctx, const double* heights, int nrow, int ncol, double x0, double y0, double dx,
                     double dy, int ix, int iy);
 
+/* Set an arbitrary state: grid (center: host batch x nx, B: host batch x nx x nx)
+ * and weights (batch x N_total in dtype, host or device per weights_on_device;
+ * a device pointer must be on cfg->device). The weights are normalised on
+ * entry (vol * sum w = 1). PMF_E_SINGULAR_GRID if some B is singular. */
 int pmf_set_state(pmf_ctx* ctx, const double* center, const double* B,
                   const void* weights, int weights_on_device);
 
@@ -164,13 +164,20 @@ int pmf_set_state(pmf_ctx* ctx, const double* center, const double* B,
  * (R2-R4, R7) on the grid at the start of substep n, inverse DFT,
  * normalise (Alg. 6; closed form, R9). The grid moves: c <- e^{A tau} c,
  * B <- e^{A tau} B (eq:gridMov P:142-148). Lazy (see LAZINESS).
- * PMF_E_DT if dt <= 0, steps < 1 or 1 -/+ dt tr(A) <= 0. */
+ * cfg.step = PMF_STEP_CN: psi_n = (1 - dt/4 q_n) / (1 + dt/4 q_{n+1}) (R27).
+ * cfg.diff_mode = PMF_DIFF_FDM: the explicit FDM instead (eq:FST), normalised by
+ * summation (it does not conserve mass).
+ * PMF_E_DT if dt <= 0, steps < 1 or 1 -/+ dt tr(A) <= 0 (FDM / plane: also steps > 64
+ * where those kernels are required). */
 int pmf_predict(pmf_ctx* ctx, double dt, int steps);
 
 /* Measurement update (Bayes, eq:filt P:46): w_i <- w_i p(z - h(xi_i)) at the
  * (moved) grid points (R13), normaliser C = vol sum w_i p(z|xi_i),
  * w <- w / C; the moments of the posterior (R14) are computed on
- * the device in the same pass. z: batch x nz doubles, host or device.
+ * the device in the same pass (fused into the inverse transform for the Gaussian
+ * kinds; PMF_LIK_TERRAIN_GM runs as its own point pass after the predict).
+ * z: batch x nz doubles, host or device. PMF_E_STATE for TERRAIN_GM without a
+ * terrain table.
  * Per-filter failure (C == 0 or non-finite) is reported by pmf_moments
  * (PMF_E_NO_SUPPORT). */
 int pmf_update(pmf_ctx* ctx, const double* z, int z_on_device, const pmf_likelihood* lik);
@@ -239,7 +246,8 @@ int64_t pmf_launch_count(const pmf_ctx* ctx);
 
 /* Kernel timing: while enabled, CUDA events are recorded on the context's stream
  * around the dominant kernel of every executed prediction (the resident epoch
- * kernel, or the whole pencil predict); pmf_profile_read waits for them and
+ * kernel, the plane path's last-axis Psi pass, the FDM's last-axis DST kernel, or
+ * the whole pencil predict); pmf_profile_read waits for them and
  * returns the summed milliseconds and the number of timed launches, then resets.
  * pmf_profile(ctx, 1) also resets. */
 int pmf_profile(pmf_ctx* ctx, int enable);
