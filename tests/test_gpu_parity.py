@@ -265,3 +265,48 @@ def test_crank_nicolson_parity(name):
     e = compare_runs(cfg, g, orc, T, 1e-10)
     assert e["w"] <= 1e-10, e
     assert e["mean"] <= 1e-10 and e["cov"] <= 1e-10 and e["logC"] <= 1e-10 and e["grid"] <= 1e-10, e
+
+
+def _terrain_cfg_2d():
+    """A 2-D variant of the §VI measurement (C6): state [px, py] with a CV-free drift,
+    altitude from C6's synthetic map, Gaussian-mixture noise; resident-kernel size."""
+    import dataclasses
+    import workloads as W
+    c6 = make_config("C6")
+    cfg = make_config("C5", batch=2, n=(128, 128))
+    return dataclasses.replace(cfg, A=np.array([[0.0, 0.0], [0.0, 0.0]]), Q=np.diag([4.0, 4.0]),
+                               prior_mean=np.tile(c6.prior_mean[0, [0, 2]], (2, 1)),
+                               prior_cov=np.diag([90.0, 60.0]), tau=1.0, lik_kind=W.LIK_TERRAIN_GM,
+                               H=None, R=None, extra={"gm": c6.extra["gm"]}, seed=6)
+
+
+def test_terrain_likelihood_resident_and_plane():
+    """The terrain-GM likelihood (PMF_LIK_TERRAIN_GM) after the resident kernel (2-D,
+    128^2) and after the plane kernels (C6 at 32x32x16x16), against the oracle."""
+    import workloads as W
+    orig_table = W.terrain_table
+    c6 = make_config("C6")
+    # 2-D: the C6 map with (ix, iy) = (0, 1)
+    W.terrain_table = lambda cfg, **kw: orig_table(c6)[:5] + (0, 1)
+    try:
+        cfg = _terrain_cfg_2d()
+        T = 2
+        # static truth 3 m / 2 m off the prior mean: altitude + the mixture's two components
+        px, py = cfg.prior_mean[0, 0] + 3.0, cfg.prior_mean[0, 1] - 2.0
+        h = float(W.terrain_field(c6, px, py))
+        zs = np.array([h + 0.3, h + 20.0 - 0.5, h - 0.2])[:, None, None] * np.ones((1, cfg.batch, 1))
+        g = run_gpu(cfg, zs, T)
+        assert g["filter"].path == pmf.PATH_RESIDENT
+        orc = {b: O.run_filter(cfg, zs, b=b, T=T, keep_weights=True) for b in range(cfg.batch)}
+        e = compare_runs(cfg, g, orc, T, 1e-10)
+        assert e["w"] <= 1e-10 and e["mean"] <= 1e-10 and e["logC"] <= 1e-10, e
+    finally:
+        W.terrain_table = orig_table
+    cfg = make_config("C6", n=(32, 32, 16, 16))
+    T = 2
+    zs = simulate(cfg, T=T)["z"]
+    g = run_gpu(cfg, zs, T)
+    assert g["filter"].path == pmf.PATH_PLANE
+    orc = {0: O.run_filter(cfg, zs, b=0, T=T, keep_weights=True)}
+    e = compare_runs(cfg, g, orc, T, 1e-10)
+    assert e["w"] <= 1e-10 and e["mean"] <= 1e-10 and e["logC"] <= 1e-10, e

@@ -84,3 +84,14 @@ def test_sharded_argument_errors():
         pmf.Filter(4, cfg.n, cfg.A, cfg.Q, world=3)            # 8 planes do not split in 3
     with pytest.raises(pmf.PMFError):
         pmf.Filter(4, cfg.n, cfg.A, cfg.Q, batch=2, world=2)   # one filter per sharded context
+
+
+def test_sharded_crank_nicolson():
+    """Crank-Nicolson substeps (R27) through the sharded (virtual-rank) path."""
+    cfg = make_config("C4", n=(8, 6, 12, 8))
+    T = 2
+    zs = simulate(cfg, T=T)["z"]
+    orc = {0: O.run_filter(cfg, zs, b=0, T=T, keep_weights=True, step=O.STEP_CN)}
+    g = run_gpu(cfg, zs, T, path=pmf.PATH_PENCIL, world=2, step=pmf.STEP_CN)
+    e = compare_runs(cfg, g, orc, T, TOL["f64"])
+    assert e["w"] <= 1e-10 and e["mean"] <= 1e-10 and e["cov"] <= 1e-10 and e["logC"] <= 1e-10, e
