@@ -983,6 +983,373 @@ __global__ void __launch_bounds__(SplitCfg<T, NA>::NT, 1) k_plane_split(MidArgs<
     }
 }
 
+// ============================================================================ fused (2,3)-plane pass (nx = 4)
+// One launch replaces the three strided passes of nx = 4 (forward axis 2 [+ split
+// regrid], axis 3 with Psi, inverse axis 2) when n2 = n3 = NQ and an (i2, i3)-plane
+// fits in shared memory: HBM traffic per interval drops from 5 to 3 passes over
+// the spectrum. Work item = one (filter, k1, k0): its NQ x NQ values S(j3, j2)
+// (stride I = H1 N0 in the spectrum [filter][j3][j2][k1][k0]) sit in shared memory
+// as rows j3 of pitch NQ + 1 (conflict-free for rows and columns). Team q (8
+// threads) owns rows and columns q and q + NQ/2:
+//   F2  forward DFT along axis 2 of the rows (Alg. 1). Split regrid map (flag 4,
+//       R12): the rows are first re-sampled from the staged old plane --
+//       Z(j2) = (1 - w3) S(ja) + w3 S(ja + 1) at v3 = o3 + M33 u3', then linear along
+//       j2 at v2 = o2 + M22 u2' + M23 u3', zero ghosts -- exact because the axis-0/1
+//       DFT commutes with interpolation along axes 2, 3.
+//   F3  per column k2: forward DFT along axis 3, x s Psi / N_tot (Alg. 3-4, Euler
+//       factors paired into quartics in kap_3, R27 lists for Crank-Nicolson),
+//       inverse DFT along axis 3 (Alg. 5).
+//   I2  inverse DFT along axis 2 of the rows, stored to Sout; each freed row is
+//       refilled at once with the next item's row by per-thread cp.async copies,
+//       so the next plane's loads overlap this plane's stores and transforms.
+template <int NQ, int TM = (NQ >= 64 ? 32 : NQ / 2)>
+struct QCfg {
+    static constexpr int R = NQ / 8;
+    static constexpr int TEAMS = TM;            // team q owns rows / columns q + TEAMS j
+    static constexpr int NT = 8 * TEAMS;
+    static constexpr int P = NQ + 1;            // row pitch (complex)
+};
+template <typename T, int NQ>
+static size_t quad_smem() {
+    return sizeof(typename C2<T>::type) * ((size_t)NQ * QCfg<NQ>::P + NQ);
+}
+
+template <typename T>
+struct QuadArgs {
+    const typename C2<T>::type* S;   // input spectrum [filter][j3][j2][i]
+    typename C2<T>::type* Sout;      // output (same layout)
+    const double* coef;
+    int cs;
+    int I;                           // H1 N0 (k1, k0) pencil-planes per filter
+    int N0, H1;
+    int l, step;
+    int items;                       // batch * I
+    double* dc3;                     // [filter][n3]: the regridded filter's weight sum (split maps)
+};
+
+// Euler factors of pair j of list `list` (0: denominators, 1: Crank-Nicolson numerators
+// 2 - f_n, R27) as a quartic in kap_L: q[0] = (c0, c1), q[1] = (c2, c3), q[2] = (c4, value at
+// the Nyquist wavenumber, where kx_L = 0, R7). f_n = gam_n + bet_n kx_L + alp_n kap_L^2 with
+// gam_n, bet_n from the other axes' wavenumbers kap[a], kx[a] (a < L).
+template <int NX, int L>
+__device__ __forceinline__ void psi_pair(const double* cf, int l, int cn, int list, int j, const double* kap,
+                                         const double* kx, double2* q) {
+    auto gam_bet = [&](int n, double& g, double& bb) {
+        const double* c = cf + 10 * n;
+        g = 1.0;
+        bb = 0.0;
+#pragma unroll
+        for (int a2 = 0; a2 < L; ++a2) {
+            g = fma(c[a2], kap[a2] * kap[a2], g);
+#pragma unroll
+            for (int b2 = a2 + 1; b2 < L; ++b2) g = fma(c[pair_index(NX, a2, b2)], kx[a2] * kx[b2], g);
+            bb = fma(c[pair_index(NX, a2, L)], kx[a2], bb);
+        }
+    };
+    const int base = (list == 0 && cn) ? 1 : 0;        // CN den: f_1 .. f_l
+    double g0, b0, g1 = 1.0, b1 = 0.0, a1 = 0.0;
+    gam_bet(base + 2 * j, g0, b0);
+    double a0 = cf[10 * (base + 2 * j) + L];
+    const bool two = 2 * j + 1 < l;
+    if (two) {
+        gam_bet(base + 2 * j + 1, g1, b1);
+        a1 = cf[10 * (base + 2 * j + 1) + L];
+    }
+    if (list == 1) {                                   // 2 - f = (2 - g) - b k - a k^2
+        g0 = 2.0 - g0;
+        b0 = -b0;
+        a0 = -a0;
+        if (two) {
+            g1 = 2.0 - g1;
+            b1 = -b1;
+            a1 = -a1;
+        }
+    }
+    constexpr double kn2 = PMF_PI * PMF_PI;
+    q[0] = double2{g0 * g1, fma(g0, b1, b0 * g1)};
+    q[1] = double2{fma(g0, a1, fma(b0, b1, a0 * g1)), fma(b0, a1, a0 * b1)};
+    q[2] = double2{a0 * a1, fma(a0, kn2, g0) * fma(a1, kn2, g1)};
+}
+
+// ps[r] = mult / den[r], one division per 4 values (prefix products) unless out of range
+template <int R>
+__device__ __forceinline__ void psi_div(const double* den, double mult, double* ps) {
+    if constexpr (R % 4 != 0) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) ps[r] = mult / den[r];
+    } else {
+#pragma unroll
+        for (int g = 0; g < R; g += 4) {
+            const double p1 = den[g] * den[g + 1], p2 = p1 * den[g + 2], p3 = p2 * den[g + 3];
+            if (p3 < 1e300) {
+                double inv = mult / p3;
+                ps[g + 3] = inv * p2;
+                inv *= den[g + 3];
+                ps[g + 2] = inv * p1;
+                inv *= den[g + 2];
+                ps[g + 1] = inv * den[g];
+                ps[g] = inv * den[g + 1];
+            } else {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) ps[g + q] = mult / den[g + q];
+            }
+        }
+    }
+}
+
+// F2 of one row: forward DFT along axis 2 of x (element t + 8r), result in place in the row
+template <int NQ, typename V>
+__device__ __forceinline__ void quad_f2_row(V (&x)[NQ / 8], V* row, const V* tw, int t) {
+    constexpr int R = NQ / 8;
+    V pa[8], pb[8];
+    team_dft<R, false>(x, pa, pb, row, tw, t, [](int s2, int tt) { return rslot(s2, tt); });
+    if (s_on<R>(t)) {
+        const int sa = s_a<R>(t), sb = s_b<R>(t);
+#pragma unroll
+        for (int qq = 0; qq < 8; ++qq) {
+            row[sa + R * qq] = pa[qq];
+            row[sb + R * qq] = pb[qq];
+        }
+    }
+}
+
+// Split regrid (R12) of the staged plane, in place, in two steps that each read only
+// the team's own column / row. Step A, column j2: Z(u3') = (1 - w3) S(ja) + w3 S(ja + 1),
+// v3 = o3 + M33 u3' (zero ghosts); all reads precede the writes (warp sync).
+template <typename T, int NQ, typename V>
+__device__ __forceinline__ void quad_regrid_col(V* col, int t, double M33, double o3) {
+    constexpr int R = NQ / 8, P = QCfg<NQ>::P;
+    V z[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const double v3 = fma(M33, (double)(t + 8 * r) - 0.5 * (NQ - 1), o3), f3 = floor(v3);
+        const int fi3 = __double2int_rz(f3);
+        const int ja = min(max(fi3, -2), NQ);
+        const double w3 = (ja == fi3) ? v3 - f3 : 0.0;
+        double zx = 0.0, zy = 0.0;
+        if (ja >= 0 && ja < NQ) {
+            const V v = col[ja * P];
+            zx = (1.0 - w3) * (double)v.x;
+            zy = (1.0 - w3) * (double)v.y;
+        }
+        if (ja + 1 >= 0 && ja + 1 < NQ) {
+            const V v = col[(ja + 1) * P];
+            zx = fma(w3, (double)v.x, zx);
+            zy = fma(w3, (double)v.y, zy);
+        }
+        z[r] = V{(T)zx, (T)zy};
+    }
+    __syncwarp();
+#pragma unroll
+    for (int r = 0; r < R; ++r) col[(t + 8 * r) * P] = z[r];
+}
+
+// Step B, row u3': x[r] = linear interpolation of Z along j2 at v2 = o2 + M22 u2' + M23 u3'
+// (u2' = t + 8r, zero ghosts), read from the team's own row
+template <typename T, int NQ, typename V>
+__device__ __forceinline__ void quad_regrid_row(V (&x)[NQ / 8], const V* row, int u3, int t, double M22, double M23,
+                                                double o2) {
+    const double vb2 = fma(M23, (double)u3 - 0.5 * (NQ - 1), o2);
+#pragma unroll
+    for (int r = 0; r < NQ / 8; ++r) {
+        const double v2 = fma(M22, (t + 8 * r) - 0.5 * (NQ - 1), vb2), fl = floor(v2);
+        const int fi = min(max(__double2int_rz(fl), -2), NQ);
+        const double fr = v2 - fl;
+        const V lo = (fi >= 0 && fi < NQ) ? row[fi] : V{T(0), T(0)};
+        const V hi = (fi + 1 >= 0 && fi + 1 < NQ) ? row[fi + 1] : V{T(0), T(0)};
+        x[r] = V{(T)fma(fr, (double)hi.x - (double)lo.x, (double)lo.x),
+                 (T)fma(fr, (double)hi.y - (double)lo.y, (double)lo.y)};
+    }
+}
+
+// acc[r] *= product of list `list`'s Euler-factor pairs at kap_3 = kp[r]; pair j's quartic is
+// computed by thread j % 8 of the team and broadcast by shuffles (full warp, width 8)
+template <int NQ>
+__device__ __forceinline__ void quad_psi_prod(double (&acc)[NQ / 8], const double (&kp)[NQ / 8], const double* cf,
+                                              int l, int cn, int list, const double* kap, const double* kx, int t) {
+    constexpr int R = NQ / 8;
+    const int nq = (l + 1) >> 1;
+    double nyq = 1.0;
+    for (int jb = 0; jb < nq; jb += 8) {
+        double2 c[3] = {double2{1.0, 0.0}, double2{0.0, 0.0}, double2{0.0, 1.0}};
+        if (jb + t < nq) psi_pair<4, 3>(cf, l, cn, list, jb + t, kap, kx, c);
+        const int cnt = min(8, nq - jb);
+        for (int jj = 0; jj < cnt; ++jj) {
+            const double c0 = __shfl_sync(0xffffffffu, c[0].x, jj, 8);
+            const double c1 = __shfl_sync(0xffffffffu, c[0].y, jj, 8);
+            const double c2 = __shfl_sync(0xffffffffu, c[1].x, jj, 8);
+            const double c3 = __shfl_sync(0xffffffffu, c[1].y, jj, 8);
+            const double c4 = __shfl_sync(0xffffffffu, c[2].x, jj, 8);
+            nyq *= __shfl_sync(0xffffffffu, c[2].y, jj, 8);
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const double x1 = kp[r];
+                acc[r] *= fma(fma(fma(fma(c4, x1, c3), x1, c2), x1, c1), x1, c0);
+            }
+        }
+    }
+    if (t == ((NQ / 2) & 7)) acc[(NQ / 2) >> 3] = nyq;
+}
+
+template <typename T, int NQ, int TM>
+__global__ void __launch_bounds__(QCfg<NQ, TM>::NT, 1) k_plane_quad(QuadArgs<T> a) {
+    using V = typename C2<T>::type;
+    using C = QCfg<NQ, TM>;
+    constexpr int R = C::R, TEAMS = C::TEAMS, P = C::P;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    V* X = reinterpret_cast<V*>(smem_raw);                    // [NQ][P]: row j3
+    V* tw = X + NQ * P;                                       // [NQ]
+    const int tid = threadIdx.x, q = tid >> 3, t = tid & 7;
+    init_tw<NQ>(tw);
+    const unsigned I = (unsigned)a.I;
+    auto rs = [](int s2, int tt) { return rslot(s2, tt); };
+    auto cs = [](int s2, int tt) { return rslot(s2, tt) * P; };
+    // element (f, j3, j2, i) at ((f NQ + j3) NQ + j2) I + i: a 64-bit base per (f, i) and
+    // 32-bit offsets inside the filter (NQ^2 I < 2^31)
+    auto fbase = [&](const V* S, int item) -> const V* {
+        const unsigned f = (unsigned)item / I, i = (unsigned)item - f * I;
+        return S + (long long)f * (NQ * NQ) * (long long)I + i;
+    };
+    const unsigned step8 = 8u * I;
+    auto load_row = [&](const V* src, int j3) {
+        V* dst = X + j3 * P + t;
+        unsigned off = (unsigned)(j3 * NQ + t) * I;
+#pragma unroll
+        for (int r = 0; r < R; ++r, off += step8) tma::cp_async<sizeof(V)>(dst + 8 * r, src + off);
+    };
+    if ((int)blockIdx.x < a.items) {
+        const V* src = fbase(a.S, blockIdx.x);
+        for (int j3 = q; j3 < NQ; j3 += TEAMS) load_row(src, j3);
+    }
+    tma::cp_async_commit();
+    for (int item = blockIdx.x; item < a.items; item += gridDim.x) {
+        const int nxt = item + gridDim.x;
+        const unsigned f = (unsigned)item / I, i = (unsigned)item - f * I;
+        const double* Pc = a.coef + (long long)f * a.cs;
+        tma::cp_async_wait_all();
+        __syncthreads();                                      // the plane is in shared memory
+        if (Pc[PL_SKIP] != 0.0) {                             // uniform: failed filter, left untouched
+            if (nxt < a.items) {
+                const V* src = fbase(a.S, nxt);
+                for (int j3 = q; j3 < NQ; j3 += TEAMS) load_row(src, j3);
+            }
+            tma::cp_async_commit();
+            continue;
+        }
+        const int flag = (int)Pc[PL_FLAG];
+        // ---------------------------------------------------------------- F2 [+ split regrid]
+        const bool rg = flag == 4;
+        if (rg) {
+            const double M33 = Pc[PL_M + 15], o3 = Pc[PL_O + 3];
+#pragma unroll 1
+            for (int j2 = q; j2 < NQ; j2 += TEAMS) quad_regrid_col<T, NQ>(X + j2, t, M33, o3);
+            __syncthreads();
+        }
+        {
+            const double M22 = Pc[PL_M + 10], M23 = Pc[PL_M + 11], o2 = Pc[PL_O + 2];
+#pragma unroll 1
+            for (int j3 = q; j3 < NQ; j3 += TEAMS) {
+                V x[R];
+                if (rg) {
+                    quad_regrid_row<T, NQ>(x, X + j3 * P, j3, t, M22, M23, o2);
+                } else {
+#pragma unroll
+                    for (int r = 0; r < R; ++r) x[r] = X[j3 * P + t + 8 * r];
+                }
+                quad_f2_row<NQ>(x, X + j3 * P, tw, t);
+            }
+        }
+        __syncthreads();
+        // ---------------------------------------------------------------- F3: axis 3, s Psi / N_tot, inverse
+        {
+            const double* cf = Pc + PL_EU;
+            const int cn = a.step;
+            const unsigned k1 = i / (unsigned)a.N0;
+            const int k0 = (int)(i - k1 * (unsigned)a.N0);
+            const int N1 = 2 * (a.H1 - 1);
+            double kap[3], kx[3];
+            kap[0] = (2.0 * PMF_PI / a.N0) * (k0 < a.N0 / 2 ? k0 : k0 - a.N0);
+            kx[0] = (2 * k0 == a.N0) ? 0.0 : kap[0];
+            kap[1] = (2.0 * PMF_PI / N1) * (int)k1;
+            kx[1] = (2 * (int)k1 == N1) ? 0.0 : kap[1];
+            const double mult = Pc[PL_SN];
+#pragma unroll 1
+            for (int k2 = q; k2 < NQ; k2 += TEAMS) {
+                V* col = X + k2;
+                // Psi at k3 = t + 8r first (it needs no data: fewer live registers)
+                kap[2] = (2.0 * PMF_PI / NQ) * (k2 < NQ / 2 ? k2 : k2 - NQ);
+                kx[2] = (2 * k2 == NQ) ? 0.0 : kap[2];
+                double ps[R];
+                {
+                    double kp[R], den[R], num[R];
+#pragma unroll
+                    for (int r = 0; r < R; ++r) {
+                        const int k = t + 8 * r;
+                        kp[r] = (2.0 * PMF_PI / NQ) * (k < NQ / 2 ? k : k - NQ);
+                        den[r] = 1.0;
+                        num[r] = 1.0;
+                    }
+                    quad_psi_prod<NQ>(den, kp, cf, a.l, cn, 0, kap, kx, t);
+                    if (cn) quad_psi_prod<NQ>(num, kp, cf, a.l, cn, 1, kap, kx, t);
+                    psi_div<R>(den, mult, ps);
+#pragma unroll
+                    for (int r = 0; r < R; ++r) ps[r] *= num[r];
+                }
+                V x[R], pa[8], pb[8];
+#pragma unroll
+                for (int r = 0; r < R; ++r) x[r] = col[(t + 8 * r) * P];
+                team_dft<R, false>(x, pa, pb, col, tw, t, cs);
+                if (flag == 4 && i == 0 && k2 == 0 && t == 0) {
+                    // (k0, k1, k2, k3) = 0: the sum of the regridded weights (the split pass's DC)
+                    a.dc3[(long long)f * NQ] = (double)pa[0].x;
+                    for (int j = 1; j < NQ; ++j) a.dc3[(long long)f * NQ + j] = 0.0;
+                }
+                // Psi at k3 = t + 8r -> the owners of X[k3] via the (free) exchange column
+#pragma unroll
+                for (int r = 0; r < R; ++r) reinterpret_cast<double*>(col + (t + 8 * r) * P)[0] = ps[r];
+                __syncwarp();
+                if (s_on<R>(t)) {
+                    const int sa = s_a<R>(t), sb = s_b<R>(t);
+#pragma unroll
+                    for (int qq = 0; qq < 8; ++qq) {
+                        const double fa = reinterpret_cast<const double*>(col + (sa + R * qq) * P)[0];
+                        const double fb = reinterpret_cast<const double*>(col + (sb + R * qq) * P)[0];
+                        pa[qq] = V{(T)(pa[qq].x * fa), (T)(pa[qq].y * fa)};
+                        pb[qq] = V{(T)(pb[qq].x * fb), (T)(pb[qq].y * fb)};
+                    }
+                }
+                team_dft_dif<R, true>(pa, pb, x, col, tw, t, cs);
+#pragma unroll
+                for (int r = 0; r < R; ++r) col[(t + 8 * r) * P] = x[r];
+            }
+        }
+        __syncthreads();
+        // ---------------------------------------------------------------- I2: inverse axis 2, store, refill
+        const V* nsrc = nxt < a.items ? fbase(a.S, nxt) : nullptr;
+        V* dst = const_cast<V*>(fbase(a.Sout, item));
+#pragma unroll 1
+        for (int j3 = q; j3 < NQ; j3 += TEAMS) {
+            V* row = X + j3 * P;
+            V x[R], pa[8], pb[8];
+            if (s_on<R>(t)) {
+                const int sa = s_a<R>(t), sb = s_b<R>(t);
+#pragma unroll
+                for (int qq = 0; qq < 8; ++qq) {
+                    pa[qq] = row[sa + R * qq];
+                    pb[qq] = row[sb + R * qq];
+                }
+            }
+            team_dft_dif<R, true>(pa, pb, x, row, tw, t, rs);   // x[r] = element j2 = t + 8r
+            if (nsrc) load_row(nsrc, j3);                     // the row is free (the DFT ends with a warp sync)
+            unsigned off = (unsigned)(j3 * NQ + t) * I;
+#pragma unroll
+            for (int r = 0; r < R; ++r, off += step8) __stcg(dst + off, x[r]);
+        }
+        tma::cp_async_commit();
+    }
+    tma::cp_async_wait_all();
+}
+
 // ============================================================================ inverse plane pass (+ update)
 template <typename T, int N>
 __host__ __device__ constexpr bool inv_dbl() { return 2 * xbytes<T, N>() <= 200 * 1024; }
@@ -1409,6 +1776,50 @@ static cudaError_t split_pass(const Dims& d, PencilBufs& b, int cs, typename C2<
     }
 }
 
+// fused (2,3)-plane pass: n2 = n3 with the plane in shared memory (fp64 up to 96^2,
+// fp32 up to 128^2). Opt-in (PMF_PLANE_FUSED23=1, read per call): on B200 at C4 (96^4)
+// it moves 40 % less HBM data than the three strided passes but runs 1.51 ms against
+// their 1.39 ms -- its per-element 16-byte gathers/scatters (stride H1 N0) and 8 warps
+// per SM leave it latency-bound.
+template <typename T>
+static bool quad_ok(const Dims& d) {
+    const char* e = std::getenv("PMF_PLANE_FUSED23");
+    if (!(e && e[0] == '1') || d.nx != 4 || d.n[2] != d.n[3]) return false;
+    const int n = d.n[2];
+    return n == 16 || n == 32 || n == 64 || n == 96 || (n == 128 && sizeof(T) == 4);
+}
+
+template <typename T, int NQ, int TM>
+static cudaError_t quad_tm(QuadArgs<T> qa, cudaStream_t s) {
+    using C = QCfg<NQ, TM>;
+    const size_t smem = quad_smem<T, NQ>();
+    int grid = 1;
+    cudaError_t e = occ_grid(k_plane_quad<T, NQ, TM>, C::NT, smem, qa.items, &grid);
+    if (e != cudaSuccess) return e;
+    k_plane_quad<T, NQ, TM><<<grid, C::NT, smem, s>>>(qa);
+    return cudaGetLastError();
+}
+
+// (48 teams at NQ = 96 -- 12 warps, 168 registers -- measured 12 % slower than 32 teams)
+template <typename T, int NQ>
+static cudaError_t quad_na(QuadArgs<T> qa, cudaStream_t s) {
+    return quad_tm<T, NQ, QCfg<NQ>::TEAMS>(qa, s);
+}
+
+template <typename T>
+static cudaError_t quad_pass(QuadArgs<T> qa, int nq, cudaStream_t s) {
+    switch (nq) {
+        case 16: return quad_na<T, 16>(qa, s);
+        case 32: return quad_na<T, 32>(qa, s);
+        case 64: return quad_na<T, 64>(qa, s);
+        case 96: return quad_na<T, 96>(qa, s);
+        case 128:
+            if constexpr (sizeof(T) == 4) return quad_na<T, 128>(qa, s);
+            return cudaErrorInvalidValue;
+        default: return cudaErrorInvalidValue;
+    }
+}
+
 template <typename T, int N, int NX>
 static cudaError_t plane_t(const Dims& d, PencilBufs& b, const ModelParams& mp, const LikParams* lp, double ks,
                            cudaStream_t s, int64_t* launches) {
@@ -1491,14 +1902,34 @@ static cudaError_t plane_t(const Dims& d, PencilBufs& b, const ModelParams& mp, 
         ++*launches;
         return mid_pass<T, NX>(ma, d.n[m], mode, s);
     };
-    if (NX == 4) {
-        if ((e = mid(2, 0, S, S2, rg ? 1 : 0)) != cudaSuccess) return e;
-        if (rg && (e = split_pass<T>(d, b, cs, S, S2, pa.dc3, mp.l, s, launches)) != cudaSuccess) return e;
+    if (NX == 4 && quad_ok<T>(d)) {
+        // one fused pass over the (i2, i3)-planes instead of three strided passes
+        QuadArgs<T> qa;
+        qa.S = S;
+        qa.Sout = S2;
+        qa.coef = b.coef;
+        qa.cs = cs;
+        qa.I = Cf::H * N;
+        qa.N0 = N;
+        qa.H1 = Cf::H;
+        qa.l = mp.l;
+        qa.step = mp.step;
+        qa.items = qa.I * d.batch;
+        qa.dc3 = pa.dc3;
+        if (b.ev0) cudaEventRecordWithFlags(b.ev0, s, cudaEventRecordExternal);
+        if ((e = quad_pass<T>(qa, d.n[2], s)) != cudaSuccess) return e;
+        if (b.ev1) cudaEventRecordWithFlags(b.ev1, s, cudaEventRecordExternal);
+        ++*launches;
+    } else {
+        if (NX == 4) {
+            if ((e = mid(2, 0, S, S2, rg ? 1 : 0)) != cudaSuccess) return e;
+            if (rg && (e = split_pass<T>(d, b, cs, S, S2, pa.dc3, mp.l, s, launches)) != cudaSuccess) return e;
+        }
+        if (b.ev0) cudaEventRecordWithFlags(b.ev0, s, cudaEventRecordExternal);
+        if ((e = mid(NX - 1, 2, S2, S2, 0)) != cudaSuccess) return e;
+        if (b.ev1) cudaEventRecordWithFlags(b.ev1, s, cudaEventRecordExternal);
+        if (NX == 4 && (e = mid(2, 1, S2, S2, 0)) != cudaSuccess) return e;
     }
-    if (b.ev0) cudaEventRecordWithFlags(b.ev0, s, cudaEventRecordExternal);
-    if ((e = mid(NX - 1, 2, S2, S2, 0)) != cudaSuccess) return e;
-    if (b.ev1) cudaEventRecordWithFlags(b.ev1, s, cudaEventRecordExternal);
-    if (NX == 4 && (e = mid(2, 1, S2, S2, 0)) != cudaSuccess) return e;
     // inverse plane pass (+ update)
     int ginv = 1;
     {

@@ -54,5 +54,18 @@ __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wa
 // order this thread's earlier generic-proxy shared accesses before later async-proxy ones
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
+// per-thread asynchronous global -> shared copies of one element (8 or 16 bytes; LDGSTS):
+// for gathers whose pieces are too small for bulk copies. Completion per thread's groups.
+template <int BYTES>
+__device__ __forceinline__ void cp_async(void* dst, const void* src) {
+    static_assert(BYTES == 8 || BYTES == 16, "cp.async element size");
+    if constexpr (BYTES == 16)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+    else
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
 }  // namespace tma
 }  // namespace pmf

@@ -26,7 +26,20 @@ CASES = {
     "C4_96x96x16x32": ("C4", {"n": (96, 96, 16, 32)}, 1),
     "C4_64x64x32x16": ("C4", {"n": (64, 64, 32, 16)}, 2),
     "C4_b2_32": ("C4", {"n": (32, 32, 16, 16), "batch": 2}, 2),
+    # n2 = n3: the fused (2,3)-plane pass (split regrid + axis 2/3 DFTs + Psi in one kernel)
+    "C4_32x32x32x32": ("C4", {"n": (32, 32, 32, 32)}, 2),
+    "C4_32x32x64x64": ("C4", {"n": (32, 32, 64, 64)}, 1),
+    "C4_32x32x96x96": ("C4", {"n": (32, 32, 96, 96)}, 1),
 }
+
+
+FUSED = ("C4_32x32x16x16", "C4_b2_32", "C4_32x32x32x32", "C4_32x32x64x64", "C4_32x32x96x96")
+
+
+@pytest.fixture
+def fused23(monkeypatch):
+    """Opt into the fused (2,3)-plane pass (read by the library on every call)."""
+    monkeypatch.setenv("PMF_PLANE_FUSED23", "1")
 
 
 @pytest.mark.parametrize("name", list(CASES))
@@ -42,7 +55,19 @@ def test_plane_run_parity_f64(name):
     assert e["mean"] <= 1e-10 and e["cov"] <= 1e-10 and e["logC"] <= 1e-10 and e["grid"] <= 1e-10, e
 
 
-@pytest.mark.parametrize("name", ["C3_32x32x16", "C4_32x32x16x16"])
+@pytest.mark.parametrize("name", FUSED)
+def test_plane_fused23_parity_f64(name, fused23):
+    """n2 = n3: one fused pass (split regrid + axis-2/3 DFTs + Psi) replaces the three
+    strided passes; same bar against the oracle."""
+    test_plane_run_parity_f64(name)
+
+
+@pytest.mark.parametrize("name", ["C4_32x32x16x16", "C4_32x32x32x32"])
+def test_plane_fused23_parity_f32(name, fused23):
+    test_plane_run_parity_f32(name)
+
+
+@pytest.mark.parametrize("name", ["C3_32x32x16", "C4_32x32x16x16", "C4_32x32x32x32"])
 def test_plane_run_parity_f32(name):
     cid, over, T = CASES[name]
     cfg = make_config(cid, **over)
