@@ -863,7 +863,7 @@ __global__ void __launch_bounds__(MidCfg<T, NA, VAR>::NT, MidCfg<T, NA, VAR>::MI
 // j3 stream once through a ring of RS staged row sets (v3 is monotone in u3').
 template <typename T, int NA>
 struct SplitCfg {
-    static constexpr int TP = NA >= 128 ? 16 : 32;
+    static constexpr int TP = NA >= 96 ? 16 : 32;
     static constexpr int PP = sizeof(T) == 8 ? TP + 1 : TP + 2;
     static constexpr int RS = 3;
     static constexpr int NT = 8 * TP;
