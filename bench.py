@@ -284,11 +284,11 @@ def run_workload(args, workload, rank, world, local, secondary=False):
               "kernel_ms": km_ms / max(km_n, 1),
               "hbm_frac": 2 * esz * cfg.batch * cfg.points / (km_ms / max(km_n, 1) * 1e-3) / 1e9 / hbm_gbs,
               "what": "predict only (prep + transform/Psi kernel + closed-form normalisation), same filters"}
-        if f.path == pmf.PATH_RESIDENT and dtype == "f64":
-            # the predict's algorithmic FP64 issue slots against the FP64 issue peak
+        if f.path == pmf.PATH_RESIDENT:
+            # the predict's algorithmic issue slots against the FP64 (FP32) issue peak
             spp = 0.5 * 4 * 3.5 * math.log2(cfg.n[0]) + (3 * cfg.l + 10) * (cfg.n[1] // 2 + 1) / cfg.n[1]
             tu["alu_frac"] = (spp * cfg.batch * cfg.points / (km_ms / max(km_n, 1) * 1e-3)) / \
-                (148 * 64 * peaks()[2] * 1e6)
+                (148 * (64 if dtype == "f64" else 128) * peaks()[2] * 1e6)
 
     # ---------------------------------------------------------------- e2e: host buffers through the C ABI
     e2e = None
@@ -381,22 +381,24 @@ def run_workload(args, workload, rank, world, local, secondary=False):
             "ncu_source": km.get("source")}
     if roof_extra is not None:
         roof = roof_extra
-    elif f.path == pmf.PATH_RESIDENT and dtype == "f64":
+    elif f.path == pmf.PATH_RESIDENT:
         # The fused epoch kernel is FP64-issue bound (ALU roofline below the HBM one): per
         # grid point the predict alone needs ~70 FP64 issue slots (FFT 3.3e9 +
         # Psi 1.4e9 slots for 4096 x 128^2, i.e. 3.5 log2 N per complex point per axis and
         # direction, halved for real data, and 3 l + 10 per spectral point) against 16 B of
         # HBM traffic, while B200 issues 148 x 64 FP64 lanes per clock. Peak = that issue
         # rate at the max SM clock; the HBM fraction is kept alongside.
+        # fp32: the same slots on the FP32 pipe (128 lanes per SM per clock)
         slots_pp = 0.5 * 4 * 3.5 * math.log2(cfg.n[0]) + (3 * cfg.l + 10) * (cfg.n[1] // 2 + 1) / cfg.n[1]
         slots = slots_pp * points_step
-        peak_alu = 148 * 64 * sm_max * 1e6 / 1e12
+        lanes, pname = (64, "FP64") if dtype == "f64" else (128, "FP32")
+        peak_alu = 148 * lanes * sm_max * 1e6 / 1e12
         ach = slots / (kern_ms * 1e-3) / 1e12
-        roof = {"bound": "alu", "achieved": ach, "peak": peak_alu, "unit": "T FP64 issue slots/s",
+        roof = {"bound": "alu", "achieved": ach, "peak": peak_alu, "unit": f"T {pname} issue slots/s",
                 "frac": ach / peak_alu, "traffic": km.get("dram_bytes"), "kernel": kname, "kernel_ms": kern_ms,
                 "timed_launches": kern_n, "share_of_step": kern_ms / ms_step,
-                "peak_source": "148 SMs x 64 FP64 lanes x max SM clock (B200_PROFILING / B300 guide unit counts)",
-                "alg_units_per_launch": slots, "alg_units_per_unit": f"{slots_pp:.1f} FP64 issue slots per grid point",
+                "peak_source": f"148 SMs x {lanes} {pname} lanes x max SM clock (B200_PROFILING / B300 guide unit counts)",
+                "alg_units_per_launch": slots, "alg_units_per_unit": f"{slots_pp:.1f} {pname} issue slots per grid point",
                 "fp64_pipe_frac_ncu": (km["fp64_pipe_pct"] / 100.0) if "fp64_pipe_pct" in km else None,
                 "ncu_source": km.get("source"),
                 "hbm": {"achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
@@ -462,7 +464,7 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     line = run_workload(args, args.workload, rank, world, local)
-    also_list = ("C5l1,C4,C3,C5fdm,C6" if args.workload == "C5" else "") if args.also == "auto" else args.also
+    also_list = ("C5l1,C5f32,C4,C3,C5fdm,C6" if args.workload == "C5" else "") if args.also == "auto" else args.also
     if also_list and world == 1:
         # the other large single-GPU configurations, measured the same way (compact)
         also = {}
