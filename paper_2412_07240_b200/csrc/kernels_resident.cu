@@ -478,18 +478,18 @@ __global__ void __launch_bounds__(NT, 1) k_resident_epoch(ResArgs<T> a) {
                 X[k1 * PITCH + xcol(k1, 2 * m)] = V{T(0.5) * (zk.x + zp.x), T(0.5) * (zk.y - zp.y)};
                 X[k1 * PITCH + xcol(k1, 2 * m + 1)] = V{T(0.5) * (zk.y + zp.y), T(0.5) * (zp.x - zk.x)};
             };
-            if (t == 0) {
+            // k1 = sa + 16q and sb + 16q (q < 4) on every thread; only the mirror partner
+            // differs on t = 0 (its pairs are s = 0 and 8, both self-mirrored): register
+            // selects instead of a divergent branch. t = 0 also owns the Nyquist row 64.
+            const bool t0 = t == 0;
 #pragma unroll
-                for (int q = 0; q <= 4; ++q) store_pair(16 * q, pa[q], pa[(8 - q) & 7]);
-#pragma unroll
-                for (int q = 0; q < 4; ++q) store_pair(8 + 16 * q, pb[q], pb[7 - q]);
-            } else {
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    store_pair(sa + 16 * q, pa[q], pb[7 - q]);
-                    store_pair(sb + 16 * q, pb[q], pa[7 - q]);
-                }
+            for (int q = 0; q < 4; ++q) {
+                const V ma = t0 ? pa[(8 - q) & 7] : pb[7 - q];
+                const V mb = t0 ? pb[7 - q] : pa[7 - q];
+                store_pair(sa + 16 * q, pa[q], ma);
+                store_pair(sb + 16 * q, pb[q], mb);
             }
+            if (t0) store_pair(64, pa[4], pa[4]);
         }
         __syncthreads();
 
@@ -665,17 +665,14 @@ __global__ void __launch_bounds__(NT, 1) k_resident_epoch(ResArgs<T> a) {
                 const V wa = ld(kp, 0), wb = ld(kp, 1);
                 return V{wa.x + wb.y, wb.x - wa.y};
             };
-            if (t == 0) {
+            // one index formula for every thread (no divergent branch): the mirrored halves
+            // start at 16 - t (pa; t = 0: 16 (8 - q), with zmir(64) = zdir(64) since the
+            // Nyquist row is real) and at t, or 8 on t = 0 (pb)
+            const int ma = 16 - t, mb = (t == 0) ? 8 : t;
 #pragma unroll
-                for (int q = 0; q < 8; ++q) pa[q] = (q <= 4) ? zdir(16 * q) : zmir(16 * (8 - q));
-#pragma unroll
-                for (int q = 0; q < 8; ++q) pb[q] = (q < 4) ? zdir(8 + 16 * q) : zmir(8 + 16 * (7 - q));
-            } else {
-#pragma unroll
-                for (int q = 0; q < 8; ++q) {
-                    pa[q] = (q < 4) ? zdir(sa + 16 * q) : zmir(sb + 16 * (7 - q));
-                    pb[q] = (q < 4) ? zdir(sb + 16 * q) : zmir(sa + 16 * (7 - q));
-                }
+            for (int q = 0; q < 8; ++q) {
+                pa[q] = (q < 4) ? zdir(sa + 16 * q) : zmir(ma + 16 * (7 - q));
+                pb[q] = (q < 4) ? zdir(sb + 16 * q) : zmir(mb + 16 * (7 - q));
             }
             dft8<true>(pa);
             dft8<true>(pb);
