@@ -50,7 +50,7 @@ __device__ __forceinline__ int cslot(int s, int t, int m) {
 }
 
 // ---------------------------------------------------------------------------
-// Per-filter constants of one epoch, written by k_res_prep (one thread per
+// Per-filter constants of one epoch, written by k_res_prep (one warp per
 // filter) into a global table and staged into shared memory by TMA together
 // with the filter's weights. Layout (doubles), stride PRM_FIXED + 3 l (even):
 enum {
@@ -75,16 +75,17 @@ inline int prm_stride(int l) { return (PRM_FIXED + 3 * l + 1) & ~1; }
 
 using namespace res;
 
-// ============================================================================ prep (1 thread per filter)
+// ============================================================================ prep (one warp per filter)
 // Grid constants of the epoch: regrid target (R12), start-of-interval grid
 // (c0, B0), moved grid B_l = e^{A tau} B0 (eq:gridMov P:142-148), Euler-factor
 // coefficients on B0 for the l substeps (Alg. 3, R3/R4), and the
 // likelihood exponent as a quadratic form in the moved grid's index
 // coordinates (eq:meas P:36, R13). The state's grid becomes (c_l, B_l).
+// One warp per filter: the lanes share the substeps, lane 0 does the rest.
 __global__ void k_res_prep(FilterState* st, double* prm, int pstride, ModelParams mp,
                            const SubstepEntry* __restrict__ sub, LikParams lp, const double* __restrict__ z,
                            double ks, int update, int batch) {
-    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    const int b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
     if (b >= batch) return;
     FilterState& f = st[b];
     double* P = prm + (long long)b * pstride;
@@ -103,19 +104,50 @@ __global__ void k_res_prep(FilterState* st, double* prm, int pstride, ModelParam
         B0[3] = 2.0 * ks * sqrt(v1) / N;
         const double det = B[0] * B[3] - B[1] * B[2];
         const double Bi[4] = {B[3] / det, -B[1] / det, -B[2] / det, B[0] / det};
-        P[P_M + 0] = Bi[0] * B0[0] + Bi[1] * B0[2];
-        P[P_M + 1] = Bi[0] * B0[1] + Bi[1] * B0[3];
-        P[P_M + 2] = Bi[2] * B0[0] + Bi[3] * B0[2];
-        P[P_M + 3] = Bi[2] * B0[1] + Bi[3] * B0[3];
-        const double d0 = c0[0] - c[0], d1 = c0[1] - c[1];
-        P[P_O + 0] = fma(Bi[0], d0, fma(Bi[1], d1, 0.5 * (N - 1)));
-        P[P_O + 1] = fma(Bi[2], d0, fma(Bi[3], d1, 0.5 * (N - 1)));
+        if (lane == 0) {
+            P[P_M + 0] = Bi[0] * B0[0] + Bi[1] * B0[2];
+            P[P_M + 1] = Bi[0] * B0[1] + Bi[1] * B0[3];
+            P[P_M + 2] = Bi[2] * B0[0] + Bi[3] * B0[2];
+            P[P_M + 3] = Bi[2] * B0[1] + Bi[3] * B0[3];
+            const double d0 = c0[0] - c[0], d1 = c0[1] - c[1];
+            P[P_O + 0] = fma(Bi[0], d0, fma(Bi[1], d1, 0.5 * (N - 1)));
+            P[P_O + 1] = fma(Bi[2], d0, fma(Bi[3], d1, 0.5 * (N - 1)));
+        }
     }
-    P[P_SKIP] = skip ? 1.0 : 0.0;
+    __syncwarp();                            // every lane has read the state
+    if (lane == 0) P[P_SKIP] = skip ? 1.0 : 0.0;
     if (skip) {
-        f.status = -6;
+        if (lane == 0) f.status = -6;
         return;
     }
+    const double det0 = B0[0] * B0[3] - B0[1] * B0[2];
+    const double Bi0[4] = {B0[3] / det0, -B0[1] / det0, -B0[2] / det0, B0[0] / det0};
+    for (int n = lane; n < mp.l; n += 32) {
+        double D00, D01, D11;
+        if (mp.diff_mode == 0) {           // R3: D_n = B0^-1 E_n B0^-T
+            const double* E = sub[n].E;
+            const double t00 = fma(Bi0[0], E[0], Bi0[1] * E[4]);
+            const double t01 = fma(Bi0[0], E[1], Bi0[1] * E[5]);
+            const double t10 = fma(Bi0[2], E[0], Bi0[3] * E[4]);
+            const double t11 = fma(Bi0[2], E[1], Bi0[3] * E[5]);
+            D00 = fma(t00, Bi0[0], t01 * Bi0[1]);
+            D01 = 0.5 * (fma(t00, Bi0[2], t01 * Bi0[3]) + fma(t10, Bi0[0], t11 * Bi0[1]));
+            D11 = fma(t10, Bi0[2], t11 * Bi0[3]);
+        } else {                           // Alg. 3 literally: per-axis L^(m) = N ||B_n[:,m]||
+            const double* Pn = sub[n].P;
+            const double b00 = fma(Pn[0], B0[0], Pn[1] * B0[2]);
+            const double b01 = fma(Pn[0], B0[1], Pn[1] * B0[3]);
+            const double b10 = fma(Pn[4], B0[0], Pn[5] * B0[2]);
+            const double b11 = fma(Pn[4], B0[1], Pn[5] * B0[3]);
+            D00 = mp.Q[0] / fma(b00, b00, b10 * b10);
+            D11 = mp.Q[5] / fma(b01, b01, b11 * b11);
+            D01 = 0.0;
+        }
+        P[PRM_FIXED + 3 * n] = 0.5 * mp.dt * D00;
+        P[PRM_FIXED + 3 * n + 1] = 0.5 * mp.dt * D11;
+        P[PRM_FIXED + 3 * n + 2] = mp.dt * D01;
+    }
+    if (lane != 0) return;
     const double* Mt = mp.Mtau;      // stride 4
     double Bl[4], cl[2];
     Bl[0] = fma(Mt[0], B0[0], Mt[1] * B0[2]);
@@ -159,33 +191,6 @@ __global__ void k_res_prep(FilterState* st, double* prm, int pstride, ModelParam
         P[P_QG + 2] = g11;
     } else if (update) {
         P[P_ZR] = z[b];
-    }
-    const double det0 = B0[0] * B0[3] - B0[1] * B0[2];
-    const double Bi0[4] = {B0[3] / det0, -B0[1] / det0, -B0[2] / det0, B0[0] / det0};
-    for (int n = 0; n < mp.l; ++n) {
-        double D00, D01, D11;
-        if (mp.diff_mode == 0) {           // R3: D_n = B0^-1 E_n B0^-T
-            const double* E = sub[n].E;
-            const double t00 = fma(Bi0[0], E[0], Bi0[1] * E[4]);
-            const double t01 = fma(Bi0[0], E[1], Bi0[1] * E[5]);
-            const double t10 = fma(Bi0[2], E[0], Bi0[3] * E[4]);
-            const double t11 = fma(Bi0[2], E[1], Bi0[3] * E[5]);
-            D00 = fma(t00, Bi0[0], t01 * Bi0[1]);
-            D01 = 0.5 * (fma(t00, Bi0[2], t01 * Bi0[3]) + fma(t10, Bi0[0], t11 * Bi0[1]));
-            D11 = fma(t10, Bi0[2], t11 * Bi0[3]);
-        } else {                           // Alg. 3 literally: per-axis L^(m) = N ||B_n[:,m]||
-            const double* Pn = sub[n].P;
-            const double b00 = fma(Pn[0], B0[0], Pn[1] * B0[2]);
-            const double b01 = fma(Pn[0], B0[1], Pn[1] * B0[3]);
-            const double b10 = fma(Pn[4], B0[0], Pn[5] * B0[2]);
-            const double b11 = fma(Pn[4], B0[1], Pn[5] * B0[3]);
-            D00 = mp.Q[0] / fma(b00, b00, b10 * b10);
-            D11 = mp.Q[5] / fma(b01, b01, b11 * b11);
-            D01 = 0.0;
-        }
-        P[PRM_FIXED + 3 * n] = 0.5 * mp.dt * D00;
-        P[PRM_FIXED + 3 * n + 1] = 0.5 * mp.dt * D11;
-        P[PRM_FIXED + 3 * n + 2] = mp.dt * D01;
     }
     f.c[0] = cl[0];
     f.c[1] = cl[1];
@@ -858,7 +863,7 @@ static cudaError_t launch_dt(const Dims& d, PencilBufs& b, const ModelParams& mp
                              cudaStream_t s, int64_t* launches) {
     const int ps = prm_stride(mp.l);
     LikParams lpv = lp ? *lp : LikParams{};
-    k_res_prep<<<(d.batch + 127) / 128, 128, 0, s>>>(b.st, b.coef, ps, mp, b.sub, lpv, b.z, ks, lp ? 1 : 0, d.batch);
+    k_res_prep<<<(d.batch + 3) / 4, 128, 0, s>>>(b.st, b.coef, ps, mp, b.sub, lpv, b.z, ks, lp ? 1 : 0, d.batch);
     ++*launches;
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
