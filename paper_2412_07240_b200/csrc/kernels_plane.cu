@@ -508,18 +508,17 @@ __global__ void __launch_bounds__(Cfg<N>::NT, Cfg<N>::MINB) k_plane_fwd(PlaneArg
                     X[k1 * PITCH + xcol(k1, 2 * m)] = V{T(0.5) * (zk.x + zp.x), T(0.5) * (zk.y - zp.y)};
                     X[k1 * PITCH + xcol(k1, 2 * m + 1)] = V{T(0.5) * (zk.y + zp.y), T(0.5) * (zp.x - zk.x)};
                 };
-                if (t == 0) {
+                // k1 = sa + R1 q and sb + R1 q on every thread; only the mirror partner differs
+                // on t = 0 (s = 0 and R1/2 are self-mirrored): selects, not a divergent branch
+                const bool t0 = t == 0;
 #pragma unroll
-                    for (int q = 0; q <= 4; ++q) store_pair(R1 * q, pa[q], pa[(8 - q) & 7]);
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) store_pair(R1 / 2 + R1 * q, pb[q], pb[7 - q]);
-                } else {
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        store_pair(sa + R1 * q, pa[q], pb[7 - q]);
-                        store_pair(sb + R1 * q, pb[q], pa[7 - q]);
-                    }
+                for (int q = 0; q < 4; ++q) {
+                    const V ma = t0 ? pa[(8 - q) & 7] : pb[7 - q];
+                    const V mb = t0 ? pb[7 - q] : pa[7 - q];
+                    store_pair(sa + R1 * q, pa[q], ma);
+                    store_pair(sb + R1 * q, pb[q], mb);
                 }
+                if (t0) store_pair(R1 * 4, pa[4], pa[4]);
             }
         }
         __syncthreads();
@@ -527,12 +526,12 @@ __global__ void __launch_bounds__(Cfg<N>::NT, Cfg<N>::MINB) k_plane_fwd(PlaneArg
         {
             V x[R1], pa[8], pb[8];
             V* row = X + m * PITCH;
-            if (m == 0) {
+            const bool m0 = m == 0;                 // team 0 packs rows 0 and N/2 (both real in j0)
 #pragma unroll
-                for (int r = 0; r < R1; ++r) x[r] = V{X[t + 8 * r].x, X[(N / 2) * PITCH + t + 8 * r].x};
-            } else {
-#pragma unroll
-                for (int r = 0; r < R1; ++r) x[r] = row[xcol(m, t + 8 * r)];
+            for (int r = 0; r < R1; ++r) {
+                const V A = row[xcol(m, t + 8 * r)];
+                const T B = m0 ? X[(N / 2) * PITCH + t + 8 * r].x : T(0);
+                x[r] = m0 ? V{A.x, B} : A;
             }
             team_dft<R1, false>(x, pa, pb, row, tw, t, [](int s2, int tt) { return rslot(s2, tt); });
             if (s_on<R1>(t)) {
@@ -543,17 +542,11 @@ __global__ void __launch_bounds__(Cfg<N>::NT, Cfg<N>::MINB) k_plane_fwd(PlaneArg
                         X[kk] = V{T(0.5) * (rk.x + rm.x), T(0.5) * (rk.y - rm.y)};
                         X[(N / 2) * PITCH + kk] = V{T(0.5) * (rk.y + rm.y), T(0.5) * (rm.x - rk.x)};
                     };
-                    if (t == 0) {
+                    const bool t0 = t == 0;
 #pragma unroll
-                        for (int q = 0; q < 8; ++q) unpack(R1 * q, pa[q], pa[(8 - q) & 7]);
-#pragma unroll
-                        for (int q = 0; q < 8; ++q) unpack(R1 / 2 + R1 * q, pb[q], pb[7 - q]);
-                    } else {
-#pragma unroll
-                        for (int q = 0; q < 8; ++q) {
-                            unpack(sa + R1 * q, pa[q], pb[7 - q]);
-                            unpack(sb + R1 * q, pb[q], pa[7 - q]);
-                        }
+                    for (int q = 0; q < 8; ++q) {
+                        unpack(sa + R1 * q, pa[q], t0 ? pa[(8 - q) & 7] : pb[7 - q]);
+                        unpack(sb + R1 * q, pb[q], t0 ? pb[7 - q] : pa[7 - q]);
                     }
                 } else {
 #pragma unroll
@@ -1433,33 +1426,26 @@ __global__ void __launch_bounds__(Cfg<N>::NT, Cfg<N>::MINB) k_plane_inv(PlaneArg
         {
             V x[R1], pa[8], pb[8];
             V* row = X + m * PITCH;
-            if (m == 0) {
-                // rows 0 and N/2 are Hermitian in k0: pack R = A + i B, the inverse is a + i b
+            // rows 0 and N/2 are Hermitian in k0: team 0 packs R = A + i B (its inverse is
+            // a + i b); every other team has B = 0. One instruction stream for all teams
+            // (no divergent branch in warp 0); rows 0 and N/2 are unswizzled (xcol = id).
+            const bool m0 = m == 0;
 #pragma unroll
-                for (int r = 0; r < R1; ++r) {
-                    const V A = X[t + 8 * r], B = X[(N / 2) * PITCH + t + 8 * r];
-                    x[r] = V{A.x - B.y, A.y + B.x};
-                }
-            } else {
-#pragma unroll
-                for (int r = 0; r < R1; ++r) x[r] = row[t + 8 * r];
+            for (int r = 0; r < R1; ++r) {
+                const V A = row[t + 8 * r];
+                const V B = m0 ? X[(N / 2) * PITCH + t + 8 * r] : V{T(0), T(0)};
+                x[r] = V{A.x - B.y, A.y + B.x};
             }
             team_dft<R1, true>(x, pa, pb, row, tw, t, [](int s, int tt) { return rslot(s, tt); });
             if (s_on<R1>(t)) {
                 const int sa = s_a<R1>(t), sb = s_b<R1>(t);
-                if (m == 0) {
 #pragma unroll
-                    for (int q = 0; q < 8; ++q) {
-                        X[sa + R1 * q] = V{pa[q].x, T(0)};
+                for (int q = 0; q < 8; ++q) {
+                    row[xcol(m, sa + R1 * q)] = m0 ? V{pa[q].x, T(0)} : pa[q];
+                    row[xcol(m, sb + R1 * q)] = m0 ? V{pb[q].x, T(0)} : pb[q];
+                    if (m0) {
                         X[(N / 2) * PITCH + sa + R1 * q] = V{pa[q].y, T(0)};
-                        X[sb + R1 * q] = V{pb[q].x, T(0)};
                         X[(N / 2) * PITCH + sb + R1 * q] = V{pb[q].y, T(0)};
-                    }
-                } else {
-#pragma unroll
-                    for (int q = 0; q < 8; ++q) {
-                        row[xcol(m, sa + R1 * q)] = pa[q];
-                        row[xcol(m, sb + R1 * q)] = pb[q];
                     }
                 }
             }
@@ -1479,18 +1465,14 @@ __global__ void __launch_bounds__(Cfg<N>::NT, Cfg<N>::MINB) k_plane_inv(PlaneArg
                 return V{wa.x + wb.y, wb.x - wa.y};
             };
             if (s_on<R1>(t)) {
-                const int sa = s_a<R1>(t), sb = s_b<R1>(t);
-                if (t == 0) {
+                // one index formula for every thread: the mirrored halves start at R1 - t
+                // (t = 0: k1 = N/2 for q = 4, where zmir = zdir since that row is real) and
+                // at t, or R1/2 on t = 0
+                const int sa = s_a<R1>(t), sb = s_b<R1>(t), ma = R1 - t, mb = (t == 0) ? R1 / 2 : t;
 #pragma unroll
-                    for (int q = 0; q < 8; ++q) pa[q] = (q <= 4) ? zdir(R1 * q) : zmir(R1 * (8 - q));
-#pragma unroll
-                    for (int q = 0; q < 8; ++q) pb[q] = (q < 4) ? zdir(R1 / 2 + R1 * q) : zmir(R1 / 2 + R1 * (7 - q));
-                } else {
-#pragma unroll
-                    for (int q = 0; q < 8; ++q) {
-                        pa[q] = (q < 4) ? zdir(sa + R1 * q) : zmir(sb + R1 * (7 - q));
-                        pb[q] = (q < 4) ? zdir(sb + R1 * q) : zmir(sa + R1 * (7 - q));
-                    }
+                for (int q = 0; q < 8; ++q) {
+                    pa[q] = (q < 4) ? zdir(sa + R1 * q) : zmir(ma + R1 * (7 - q));
+                    pb[q] = (q < 4) ? zdir(sb + R1 * q) : zmir(mb + R1 * (7 - q));
                 }
             }
             team_dft_dif<R1, true>(pa, pb, x, X, tw, t, [&](int s, int tt) { return cslot<N>(s, tt, m); });
