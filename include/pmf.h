@@ -85,6 +85,12 @@ extern "C" {
 #define PMF_STEP_EULER 0
 #define PMF_STEP_CN    1
 
+#define PMF_GRID_AXIS  0   /* R12: regrid target axis-aligned, B' = diag(2 k_sigma sqrt(cov_mm) / N_m)            */
+#define PMF_GRID_EIGEN 1   /* R28: aligned with the covariance eigenvectors (the refs of P:346): B' columns =
+                              eigenvectors v_j * 2 k_sigma sqrt(lambda_j) / N_m, eigenvector j (decreasing lambda)
+                              on the free axis of its largest |component|, that component > 0. Also used for the
+                              initial grid of pmf_set_gaussian. PMF_DIFF_FULL only; not sharded                  */
+
 #define PMF_LIK_LINEAR_GAUSS 0   /* z = H x + v, v ~ N(0, R), nz <= 4 (eq:meas P:36)                               */
 #define PMF_LIK_RANGE_GAUSS  1   /* z = ||x|| + v, v ~ N(0, sigma^2), nz = 1 (C3)                                   */
 #define PMF_LIK_TERRAIN_GM   2   /* the paper's §VI model: z = h(x[ix], x[iy]) + v, h the terrain table
@@ -108,6 +114,8 @@ typedef struct {
                           or PMF_STEP_CN (Crank-Nicolson, second order in dt; R27, "higher order
                           time stepping" = the paper's future work). CN runs on the plane or
                           pencil kernels and is not combined with PMF_DIFF_FDM                  */
+    int   grid;        /* PMF_GRID_AXIS (0) or PMF_GRID_EIGEN: how pmf_set_gaussian and pmf_regrid
+                          design a grid from a covariance                                           */
 } pmf_config;
 
 typedef struct {

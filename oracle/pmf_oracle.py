@@ -42,6 +42,8 @@ DIFF_AXIS_LITERAL = 1      # Alg. 2/3 literally: per-axis L^(m), no cross terms
 DIFF_FDM = 2               # NEXT-1: the paper's FDM baseline (eq:FDM), in its FST form (eq:FST)
 STEP_EULER = 0             # the paper's semi-implicit Euler substeps (Alg. 3)
 STEP_CN = 1                # NEXT-4: Crank-Nicolson substeps ("higher order time stepping"; R27)
+GRID_AXIS = 0              # R12: grids designed axis-aligned from a covariance
+GRID_EIGEN = 1             # R28 (NEXT-4): grids aligned with the covariance eigenvectors (refs of P:346)
 
 
 class NoSupportError(RuntimeError):
@@ -114,10 +116,43 @@ def gaussian_pdf(X, m, P) -> np.ndarray:
     return np.exp(-0.5 * e) / math.sqrt((2 * math.pi) ** nx * np.linalg.det(P))
 
 
-def initial_density(mean, cov, n, k_sigma):
+def eigen_grid(mean, cov, n, k_sigma):
+    """R28 (the covariance-aligned grids of the refs of P:346):
+    c = mean, B's columns along the eigenvectors of cov, each spanning
+    +-k_sigma sqrt(lambda): cov = V diag(lambda) V^T (LAPACK symmetric eigensolver);
+    eigenvector j in order of decreasing lambda (lower index first on ties) takes the
+    still free axis a of its largest |V[a, j]| (lowest axis on ties), with the sign
+    that makes V[a, j] > 0; B[:, a] = v_j 2 k_sigma sqrt(lambda_j) / N_a.
+    Pinned by test_oracle_eigen_grid (B diag(N) (B diag(N))^T = 4 k_sigma^2 cov;
+    diagonal cov -> design_grid; a known rotation)."""
+    mean = np.asarray(mean, dtype=np.float64)
+    cov = np.asarray(cov, dtype=np.float64)
+    nx = len(n)
+    lam, V = np.linalg.eigh(0.5 * (cov + cov.T))
+    if not np.all(np.isfinite(lam)) or np.any(lam <= 0.0):
+        raise NoSupportError("covariance not positive definite: cannot design grid")
+    order = sorted(range(nx), key=lambda j: (-lam[j], j))
+    free = list(range(nx))
+    B = np.zeros((nx, nx))
+    for j in order:
+        a = max(free, key=lambda k: (abs(V[k, j]), -k))
+        free.remove(a)
+        v = V[:, j] if V[a, j] > 0.0 else -V[:, j]
+        B[:, a] = v * 2.0 * k_sigma * math.sqrt(lam[j]) / n[a]
+    return mean.copy(), B
+
+
+def grid_design(mean, cov, n, k_sigma, grid=GRID_AXIS):
+    """The grid a covariance designs: R12/R10 axis-aligned or R28 eigen-aligned."""
+    if grid == GRID_EIGEN:
+        return eigen_grid(mean, cov, n, k_sigma)
+    return design_grid(mean, cov, n, k_sigma)
+
+
+def initial_density(mean, cov, n, k_sigma, grid=GRID_AXIS):
     """p(x_0) sampled on the designed grid and normalised (P:48 footnote:
     the first predictive PDF is p(x_0)). Returns (w, c, B)."""
-    c, B = design_grid(mean, cov, n, k_sigma)
+    c, B = grid_design(mean, cov, n, k_sigma, grid)
     w = gaussian_pdf(grid_points(c, B, n), mean, cov)
     return normalise(w, B), c, B
 
@@ -515,13 +550,14 @@ def moments(w, c, B):
 # ----------------------------------------------------------------------------
 # re-centring the grid (paper silent; north_star "re-centre the grid"; R12)
 # ----------------------------------------------------------------------------
-def regrid_target(mean, cov, n, k_sigma):
-    """New axis-aligned grid at the posterior mean, +-k_sigma sqrt(cov_mm) (R12).
-    parity unpinned (policy invented; SURVEY 'Parity unpinned')."""
+def regrid_target(mean, cov, n, k_sigma, grid=GRID_AXIS):
+    """New grid at the posterior mean: axis-aligned, +-k_sigma sqrt(cov_mm) (R12), or
+    eigen-aligned (R28, eigen_grid). parity unpinned (policy invented; SURVEY
+    'Parity unpinned')."""
     cov = np.asarray(cov)
     if any((not np.isfinite(cov[m, m])) or cov[m, m] <= 0.0 for m in range(len(n))):
         raise NoSupportError("degenerate covariance: cannot design grid")
-    return design_grid(mean, cov, n, k_sigma)
+    return grid_design(mean, cov, n, k_sigma, grid)
 
 
 def interpolate(w, c, B, X) -> np.ndarray:
@@ -572,7 +608,8 @@ def make_likelihood(cfg, X, z):
 
 
 def run_filter(cfg, zs, b: int = 0, T: int | None = None, keep_weights: bool = False,
-               diff_mode: int = DIFF_FULL, trace_sign: int = TRACE_SIGN_PHYSICAL, step: int = STEP_EULER):
+               diff_mode: int = DIFF_FULL, trace_sign: int = TRACE_SIGN_PHYSICAL, step: int = STEP_EULER,
+               grid: int = GRID_AXIS):
     """Run filter ``b`` of config ``cfg`` on measurements ``zs`` (T+1, batch, nz).
 
     Epoch k: [k>0: predict(tau, l)] -> update(z_k) -> moments -> regrid.
@@ -580,7 +617,7 @@ def run_filter(cfg, zs, b: int = 0, T: int | None = None, keep_weights: bool = F
     (optionally) the posterior weights before regrid."""
     T = cfg.T if T is None else T
     n = tuple(cfg.n)
-    w, c, B = initial_density(cfg.prior_mean[b], cfg.prior_cov, n, cfg.k_sigma)
+    w, c, B = initial_density(cfg.prior_mean[b], cfg.prior_cov, n, cfg.k_sigma, grid)
     rec = {"mean": [], "cov": [], "logC": [], "c": [], "B": [], "w": []}
     for k in range(T + 1):
         if k > 0:
@@ -595,7 +632,7 @@ def run_filter(cfg, zs, b: int = 0, T: int | None = None, keep_weights: bool = F
         rec["B"].append(np.array(B))
         if keep_weights:
             rec["w"].append(w.copy())
-        c2, B2 = regrid_target(mean, cov, n, cfg.k_sigma)
+        c2, B2 = regrid_target(mean, cov, n, cfg.k_sigma, grid)
         w = regrid(w, c, B, c2, B2)
         c, B = c2, B2
     rec["final"] = (w, c, B)

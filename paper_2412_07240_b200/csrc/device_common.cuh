@@ -299,7 +299,11 @@ __device__ inline void finish_moments(int nx, const double* acc, const double* c
 // New grid of the re-centring policy (R12): c' = mean, B' = diag(2 ks sqrt(cov_mm)/N_m).
 // Returns false when some variance is non-finite or <= 0.
 __device__ inline bool regrid_target(int nx, const int* n, const FilterState& st, double ks,
-                                     double* cn, double* Bn) {
+                                     double* cn, double* Bn, int grid = 0) {
+    if (grid == 1) {                          // R28: eigen-aligned
+        for (int a = 0; a < nx; ++a) cn[a] = st.mean[a];
+        return eigen_grid(nx, n, st.cov, ks, Bn);
+    }
     for (int i = 0; i < 16; ++i) Bn[i] = 0.0;
     bool ok = true;
     for (int a = 0; a < nx; ++a) {

@@ -616,7 +616,7 @@ __device__ inline void finalize_from(FilterState& f, const double* acc, const Di
     const int nx = d.nx;
     if (mode == 2) {
         double cn[4], Bn[16];
-        bool ok = regrid_target(nx, d.ng, f, ks, cn, Bn);
+        bool ok = regrid_target(nx, d.ng, f, ks, cn, Bn, d.grid);
         for (int a = 0; a < nx; ++a) f.c[a] = cn[a];
         for (int i = 0; i < 16; ++i) f.B[i] = Bn[i];
         double C = fabs(det4(nx, Bn)) * acc[0];
@@ -702,7 +702,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_regrid_gather(const T* __restri
     const FilterState& f = st[filt];
     if (threadIdx.x == 0) {
         double cn[4], Bn[16], Bi[16];
-        regrid_target(NX, d.ng, f, ks, cn, Bn);
+        regrid_target(NX, d.ng, f, ks, cn, Bn, d.grid);
         mat_inv4(NX, f.B, Bi);
         double M[16];
         for (int i = 0; i < 16; ++i) M[i] = 0.0;
@@ -803,7 +803,7 @@ __global__ void __launch_bounds__(128, 4) k_regrid_rows(const T* __restrict__ Wo
     const int N0 = d.n[0];
     if (threadIdx.x == 0) {
         double cn[4], Bn[16], Bi[16];
-        regrid_target(NX, d.ng, f, ks, cn, Bn);
+        regrid_target(NX, d.ng, f, ks, cn, Bn, d.grid);
         mat_inv4(NX, f.B, Bi);
         double M[16];
         for (int i = 0; i < 16; ++i) M[i] = 0.0;

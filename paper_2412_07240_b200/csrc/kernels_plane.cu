@@ -241,7 +241,7 @@ __global__ void k_plane_prep(FilterState* st, double* coef, int cs, ModelParams 
     int flag = 0;
     if (ks > 0.0) {
         double cn[4], Bn[16], Bi[16], M[16];
-        if (!regrid_target(NX, d.ng, f, ks, cn, Bn)) skip = true;
+        if (!regrid_target(NX, d.ng, f, ks, cn, Bn, d.grid)) skip = true;
         mat_inv4(NX, B0, Bi);
         for (int i = 0; i < 16; ++i) M[i] = 0.0;
         mat_mul4(NX, Bi, Bn, M);

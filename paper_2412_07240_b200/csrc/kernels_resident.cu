@@ -84,7 +84,7 @@ using namespace res;
 // One warp per filter: the lanes share the substeps, lane 0 does the rest.
 __global__ void k_res_prep(FilterState* st, double* prm, int pstride, ModelParams mp,
                            const SubstepEntry* __restrict__ sub, LikParams lp, const double* __restrict__ z,
-                           double ks, int update, int batch) {
+                           double ks, int update, int batch, int grid) {
     const int b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
     if (b >= batch) return;
     FilterState& f = st[b];
@@ -98,10 +98,20 @@ __global__ void k_res_prep(FilterState* st, double* prm, int pstride, ModelParam
         if (!(v0 > 0.0) || !(v1 > 0.0) || !isfinite(v0) || !isfinite(v1)) skip = true;
         c0[0] = f.mean[0];
         c0[1] = f.mean[1];
-        B0[0] = 2.0 * ks * sqrt(v0) / N;
-        B0[1] = 0.0;
-        B0[2] = 0.0;
-        B0[3] = 2.0 * ks * sqrt(v1) / N;
+        if (grid == 1) {                      // R28: eigen-aligned target
+            const int nn[2] = {N, N};
+            double Be[16];
+            if (!eigen_grid(2, nn, f.cov, ks, Be)) skip = true;
+            B0[0] = Be[0];
+            B0[1] = Be[1];
+            B0[2] = Be[4];
+            B0[3] = Be[5];
+        } else {                              // R12: axis-aligned target
+            B0[0] = 2.0 * ks * sqrt(v0) / N;
+            B0[1] = 0.0;
+            B0[2] = 0.0;
+            B0[3] = 2.0 * ks * sqrt(v1) / N;
+        }
         const double det = B[0] * B[3] - B[1] * B[2];
         const double Bi[4] = {B[3] / det, -B[1] / det, -B[2] / det, B[0] / det};
         if (lane == 0) {
@@ -863,7 +873,8 @@ static cudaError_t launch_dt(const Dims& d, PencilBufs& b, const ModelParams& mp
                              cudaStream_t s, int64_t* launches) {
     const int ps = prm_stride(mp.l);
     LikParams lpv = lp ? *lp : LikParams{};
-    k_res_prep<<<(d.batch + 3) / 4, 128, 0, s>>>(b.st, b.coef, ps, mp, b.sub, lpv, b.z, ks, lp ? 1 : 0, d.batch);
+    k_res_prep<<<(d.batch + 3) / 4, 128, 0, s>>>(b.st, b.coef, ps, mp, b.sub, lpv, b.z, ks, lp ? 1 : 0, d.batch,
+                                                d.grid);
     ++*launches;
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;

@@ -515,6 +515,9 @@ int pmf_validate_model(const pmf_config* cfg, const double* A, const double* Q, 
     if (cfg->diff_mode != PMF_DIFF_FULL && cfg->diff_mode != PMF_DIFF_AXIS_LITERAL && cfg->diff_mode != PMF_DIFF_FDM)
         return fail(nullptr, PMF_E_ARG, "bad diff_mode");
     if (cfg->step != PMF_STEP_EULER && cfg->step != PMF_STEP_CN) return fail(nullptr, PMF_E_ARG, "bad step");
+    if (cfg->grid != PMF_GRID_AXIS && cfg->grid != PMF_GRID_EIGEN) return fail(nullptr, PMF_E_ARG, "bad grid");
+    if (cfg->grid == PMF_GRID_EIGEN && cfg->diff_mode != PMF_DIFF_FULL)
+        return fail(nullptr, PMF_E_ARG, "eigen-aligned grids need PMF_DIFF_FULL (cross terms)");
     if (cfg->diff_mode == PMF_DIFF_FDM) {
         if (cfg->step != PMF_STEP_EULER) return fail(nullptr, PMF_E_ARG, "FDM predictor: explicit steps only");
         if (cfg->dtype != PMF_F64) return fail(nullptr, PMF_E_ARG, "FDM predictor: fp64 only");
@@ -627,6 +630,7 @@ int pmf_create(const pmf_config* cfg, const double* A, const double* Q, pmf_ctx*
     }
     d.src_lo = 0;
     d.src_n = d.n[nx - 1];
+    d.grid = cfg->grid;
 
     bool res_ok = resident_supported(d, c->dtype) && cfg->step == PMF_STEP_EULER;
     bool plane_ok = plane_supported(d, 1);
@@ -731,6 +735,8 @@ int pmf_set_gaussian(pmf_ctx* c, const double* mean, const double* cov, double k
             f.B[a * 4 + a] = 2.0 * k_sigma * std::sqrt(P[a * 4 + a]) / d.n[a];   // R10
             g[21 * (size_t)b + a] = mean[(size_t)b * nx + a];
         }
+        if (d.grid == PMF_GRID_EIGEN && !eigen_grid(nx, d.n, P, k_sigma, f.B))   // R28
+            return fail(c, PMF_E_ARG, "cov must be positive definite");
         for (int i = 0; i < 16; ++i) g[21 * (size_t)b + 4 + i] = Pi[i];
         g[21 * (size_t)b + 20] = -0.5 * (nx * std::log(2.0 * M_PI) + std::log(det));
         f.scale = 1.0;

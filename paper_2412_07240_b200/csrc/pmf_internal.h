@@ -1,6 +1,7 @@
 // pmf_internal.h -- structures shared by the host runtime (pmf_host.cpp) and the
 // CUDA kernels. Not part of the ABI (include/pmf.h is).
 #pragma once
+#include <cmath>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -69,7 +70,68 @@ struct Dims {
     int ng[4];              // global grid sizes (== n unless sharded along the last axis)
     int lo[4];              // global index of the block's first point per axis
     int src_lo, src_n;      // regrid source window along the last axis (global start, planes)
+    int grid;               // grid design from a covariance: 0 axis-aligned (R12), 1 eigen-aligned (R28)
 };
+
+// R28 (the covariance-aligned grids of the refs of P:346): grid matrix
+// whose columns are the eigenvectors of cov (stride 4, symmetric) scaled to +-ks standard
+// deviations: cov = V diag(lam) V^T by cyclic Jacobi rotations; eigenvector j, in order of
+// decreasing lam (lower index first on ties), takes the still free axis a of its largest
+// |V[a][j]| (lowest axis on ties), signed so that V[a][j] > 0; B[:, a] = v_j 2 ks sqrt(lam_j) / n[a].
+// A diagonal cov gives the axis-aligned grid of R12. Returns false unless every lam > 0.
+__host__ __device__ inline bool eigen_grid(int nx, const int* n, const double* cov, double ks, double* B) {
+    double a[16], v[16];
+    for (int i = 0; i < 16; ++i) {
+        a[i] = cov[i];
+        v[i] = (i % 5 == 0) ? 1.0 : 0.0;
+        B[i] = 0.0;
+    }
+    for (int sweep = 0; sweep < 32; ++sweep) {
+        double off = 0.0, dia = 0.0;
+        for (int p = 0; p < nx; ++p) {
+            dia += a[p * 4 + p] * a[p * 4 + p];
+            for (int q = p + 1; q < nx; ++q) off += a[p * 4 + q] * a[p * 4 + q];
+        }
+        if (!(off > 1e-36 * dia)) break;
+        for (int p = 0; p < nx; ++p)
+            for (int q = p + 1; q < nx; ++q) {
+                const double apq = a[p * 4 + q];
+                if (apq == 0.0) continue;
+                const double th = (a[q * 4 + q] - a[p * 4 + p]) / (2.0 * apq);
+                const double t = (th >= 0.0 ? 1.0 : -1.0) / (fabs(th) + sqrt(fma(th, th, 1.0)));
+                const double c = 1.0 / sqrt(fma(t, t, 1.0)), s = t * c;
+                for (int k = 0; k < nx; ++k) {         // A <- A J, V <- V J
+                    const double akp = a[k * 4 + p], akq = a[k * 4 + q];
+                    a[k * 4 + p] = c * akp - s * akq;
+                    a[k * 4 + q] = s * akp + c * akq;
+                    const double vkp = v[k * 4 + p], vkq = v[k * 4 + q];
+                    v[k * 4 + p] = c * vkp - s * vkq;
+                    v[k * 4 + q] = s * vkp + c * vkq;
+                }
+                for (int k = 0; k < nx; ++k) {         // A <- J^T A
+                    const double apk = a[p * 4 + k], aqk = a[q * 4 + k];
+                    a[p * 4 + k] = c * apk - s * aqk;
+                    a[q * 4 + k] = s * apk + c * aqk;
+                }
+            }
+    }
+    bool done[4] = {false, false, false, false}, used[4] = {false, false, false, false};
+    for (int r = 0; r < nx; ++r) {
+        int j = -1;
+        for (int jj = 0; jj < nx; ++jj)
+            if (!done[jj] && (j < 0 || a[jj * 4 + jj] > a[j * 4 + j])) j = jj;
+        done[j] = true;
+        const double lam = a[j * 4 + j];
+        if (!(lam > 0.0 && lam < 1e300)) return false;
+        int ax = -1;
+        for (int k = 0; k < nx; ++k)
+            if (!used[k] && (ax < 0 || fabs(v[k * 4 + j]) > fabs(v[ax * 4 + j]))) ax = k;
+        used[ax] = true;
+        const double sc = (v[ax * 4 + j] < 0.0 ? -2.0 : 2.0) * ks * sqrt(lam) / n[ax];
+        for (int k = 0; k < nx; ++k) B[k * 4 + ax] = sc * v[k * 4 + j];
+    }
+    return true;
+}
 
 // Number of doubles per filter in the pencil path's epoch-coefficient buffer.
 // pencil path: 4 + 10 l + 16 (scale, Euler factors, likelihood quadratic form);

@@ -225,6 +225,7 @@ extern "C" int pmf_create_sharded(const pmf_config* cfg, const double* A, const 
     double Qs[16];
     int rv = pmf_validate_model(cfg, A, Q, Qs);
     if (!rv && cfg->diff_mode == PMF_DIFF_FDM) rv = pmf_fail(nullptr, PMF_E_ARG, "FDM predictor: not sharded");
+    if (!rv && cfg->grid != PMF_GRID_AXIS) rv = pmf_fail(nullptr, PMF_E_ARG, "eigen-aligned grids: not sharded");
     if (rv) return rv;
     const int nx = cfg->nx, L = nx - 1;
     if (nx < 2) return pmf_fail(nullptr, PMF_E_ARG, "sharding needs nx >= 2 (slabs along the last axis)");

@@ -23,6 +23,7 @@ ERRORS = {-1: "PMF_E_ARG", -2: "PMF_E_ODD_N", -3: "PMF_E_RADIX", -4: "PMF_E_Q_NO
 F64, F32 = 0, 1
 DIFF_FULL, DIFF_AXIS_LITERAL, DIFF_FDM = 0, 1, 2
 STEP_EULER, STEP_CN = 0, 1
+GRID_AXIS, GRID_EIGEN = 0, 1   # grid design from a covariance: axis-aligned (R12) / eigenvector-aligned (R28)
 TRACE_PHYSICAL, TRACE_PRINTED = -1, 1
 PATH_AUTO, PATH_PENCIL, PATH_RESIDENT, PATH_PLANE = 0, 1, 2, 3
 LIK_LINEAR_GAUSS, LIK_RANGE_GAUSS, LIK_TERRAIN_GM = 0, 1, 2
@@ -44,7 +45,7 @@ class PMFError(RuntimeError):
 class pmf_config(C.Structure):
     _fields_ = [("nx", C.c_int), ("n", C.c_int * 4), ("batch", C.c_int), ("dtype", C.c_int),
                 ("diff_mode", C.c_int), ("trace_sign", C.c_int), ("path", C.c_int), ("device", C.c_int),
-                ("stream", C.c_void_p), ("step", C.c_int)]
+                ("stream", C.c_void_p), ("step", C.c_int), ("grid", C.c_int)]
 
 
 class pmf_likelihood(C.Structure):
@@ -145,7 +146,8 @@ class Filter:
     def __init__(self, nx: int, n, A, Q, batch: int = 1, dtype: str = "f64", diff_mode: int = DIFF_FULL,
                  trace_sign: int = TRACE_PHYSICAL, path: int = PATH_AUTO, device: int = 0,
                  stream: Optional[int] = None, world: int = 1, rank: int = 0,
-                 unique_id: Optional[bytes] = None, sharded: bool = False, step: int = STEP_EULER):
+                 unique_id: Optional[bytes] = None, sharded: bool = False, step: int = STEP_EULER,
+                 grid: int = GRID_AXIS):
         """world > 1 (or sharded=True): one filter split into `world` slabs along the last
         axis -- with `unique_id` (from nccl_unique_id(), broadcast to all ranks) this
         process is `rank` over NCCL; without it all slabs are "virtual ranks" here."""
@@ -164,6 +166,7 @@ class Filter:
         cfg.path = path
         cfg.device = device
         cfg.step = step
+        cfg.grid = grid
         if stream is None:
             try:
                 import torch

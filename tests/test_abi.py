@@ -36,6 +36,7 @@ def _create(nx, n, A, Q, **kw):
     cfg.batch = kw.get("batch", 1)
     cfg.dtype = kw.get("dtype", 0)
     cfg.diff_mode = kw.get("diff_mode", 0)
+    cfg.grid = kw.get("grid", 0)
     h = C.c_void_p()
     A = np.ascontiguousarray(np.asarray(A, dtype=np.float64))
     Q = np.ascontiguousarray(np.asarray(Q, dtype=np.float64))
@@ -53,6 +54,8 @@ def test_argument_validation_without_gpu():
     assert _create(2, (8, 8), eye, np.diag([1.0, -1.0]))[0] == -4               # not PSD
     assert _create(2, (8, 8), eye, np.array([[1.0, 0.2], [0.2, 1.0]]), diff_mode=1)[0] == -1
     assert _create(1, (8,), [[0.0]], [[1.0]], dtype=7)[0] == -1
+    assert _create(2, (8, 8), eye, eye, grid=5)[0] == -1                               # bad grid policy
+    assert _create(2, (32, 32), eye, eye, grid=pmf.GRID_EIGEN, diff_mode=2)[0] == -1    # eigen grid + FDM
 
 
 def test_no_cpu_fallback():
