@@ -144,7 +144,8 @@ void pmf_destroy(pmf_ctx* ctx);
 const char* pmf_last_error(const pmf_ctx* ctx);
 
 /* Initial density p(x_0) (P:48 footnote): for each filter b, the grid
- * c = mean_b, B = diag(2 k_sigma sqrt(cov_b[m][m]) / N_m) (R10), weights
+ * c = mean_b, B = diag(2 k_sigma sqrt(cov_b[m][m]) / N_m) (R10; with PMF_GRID_EIGEN
+ * the eigenvector-aligned B of R28), weights
  * N(xi; mean_b, cov_b) normalised so vol * sum w = 1 (vol = |det B|, R9).
  * mean: host batch x nx; cov: host batch x nx x nx (SPD). */
 int pmf_set_gaussian(pmf_ctx* ctx, const double* mean, const double* cov, double k_sigma);
@@ -201,7 +202,8 @@ int pmf_moments(pmf_ctx* ctx, double* mean, double* cov, double* log_norm);
 int64_t pmf_moments_bytes(const pmf_ctx* ctx);
 
 /* Re-centre every filter's grid on its last posterior (R12; the paper is silent,
- * north_star "re-centre the grid"): c' = mean, B' = diag(2 k_sigma sqrt(cov_mm)/N_m),
+ * north_star "re-centre the grid"): c' = mean, B' = diag(2 k_sigma sqrt(cov_mm)/N_m)
+ * (PMF_GRID_EIGEN: the eigenvector-aligned B' of R28, see pmf_config.grid),
  * multilinear interpolation of the old weights at the new points with zero
  * ghost nodes, renormalised. Lazy. PMF_E_STATE before the first update. */
 int pmf_regrid(pmf_ctx* ctx, double k_sigma);
