@@ -13,7 +13,7 @@
 // DST-I sizes 2(N+1) (194 for N = 96) do not suit an FFT, so each axis transform is
 // a dense batched GEMM on the FP64 tensor cores (mma.sync m8n8k4 .f64, DMMA):
 // out[k][t] = sum_j S[k][j] in[j][t] over tiles of 32 pencils, S[k][j] =
-// sin((k+1)(j+1) pi/(N+1)) resident in shared memory. The last axis fuses forward
+// sin((k+1)(j+1) pi/(N+1)) read from its 2(N+1)-entry sine table. The last axis fuses forward
 // transform, Lambda and inverse transform in one pass. fp64 only.
 #include <algorithm>
 #include <cmath>
@@ -87,29 +87,41 @@ struct DstArgs {
     int axis;
 };
 
+// S[k][j] = sin((k+1)(j+1) pi/(N+1)) takes only 2(N+1) distinct values: the A fragments
+// are read from the table T[m] = sin(m pi/(N+1)), m = (k+1)(j+1) mod 2(N+1), advanced by
+// an integer step per k-slice, instead of a resident N x N matrix (135 KB at N = 128):
+// the CTA needs ~45 KB of shared memory and two fit on an SM.
 template <int NA, bool AX0, int MODE>
-__global__ void __launch_bounds__(NTH, 1) k_dst(DstArgs a) {
-    constexpr int SP = NA + 4;                 // S pitch (doubles)
+__global__ void __launch_bounds__(NTH, 3) k_dst(DstArgs a) {
+    constexpr int M2 = 2 * (NA + 1);           // period of the sine table
     constexpr int IP = TP + 8;                 // tile pitch: B-fragment rows 8 doubles apart
     constexpr int MT = NA / 32;                // m8 tiles per warp (NA / 4 rows / 8)
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    double* S = reinterpret_cast<double*>(smem_raw);          // [NA][SP]
-    double* X = S + NA * SP;                                  // [NA][IP] tile (j or k rows, t columns)
+    double* X = reinterpret_cast<double*>(smem_raw);          // [NA][IP] tile (j or k rows, t columns)
     double* gl = X + NA * IP;                                 // [TP][GLP] per-pencil Lambda terms
+    double* Ts = gl + TP * GLP;                               // [M2] sine table
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    for (int e = tid; e < NA * NA; e += NTH) {
-        const int k = e / NA, j = e - k * NA;
-        const int mm = ((k + 1) * (j + 1)) % (2 * (NA + 1));
-        S[k * SP + j] = sinpi((double)mm / (double)(NA + 1));
-    }
+    for (int m = tid; m < M2; m += NTH) Ts[m] = sinpi((double)m / (double)(NA + 1));
     __syncthreads();
     const long long tiles = (a.I + TP - 1) / TP, ntile = a.O * tiles;
     const int r0 = warp * (NA / 4);            // this warp's output rows
-    auto gemm = [&](double acc[MT][4][2]) {
+    // table index of this lane's A-fragment element (row r0 + 8 mi + lane/4, column kk + lane%4)
+    // at kk = 0, and its advance per k-slice of 4 columns
+    int idx0[MT], step[MT];
 #pragma unroll
-        for (int mi = 0; mi < MT; ++mi)
+    for (int mi = 0; mi < MT; ++mi) {
+        const int r1 = r0 + 8 * mi + (lane >> 2) + 1;
+        idx0[mi] = (r1 * ((lane & 3) + 1)) % M2;
+        step[mi] = (4 * r1) % M2;
+    }
+    auto gemm = [&](double acc[MT][4][2]) {
+        int idx[MT];
+#pragma unroll
+        for (int mi = 0; mi < MT; ++mi) {
+            idx[mi] = idx0[mi];
 #pragma unroll
             for (int ni = 0; ni < 4; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+        }
 #pragma unroll 4
         for (int kk = 0; kk < NA; kk += 4) {
             double bf[4];
@@ -117,7 +129,9 @@ __global__ void __launch_bounds__(NTH, 1) k_dst(DstArgs a) {
             for (int ni = 0; ni < 4; ++ni) bf[ni] = X[(kk + (lane & 3)) * IP + 8 * ni + (lane >> 2)];
 #pragma unroll
             for (int mi = 0; mi < MT; ++mi) {
-                const double af = S[(r0 + 8 * mi + (lane >> 2)) * SP + kk + (lane & 3)];
+                const double af = Ts[idx[mi]];
+                idx[mi] += step[mi];
+                idx[mi] -= (idx[mi] >= M2) ? M2 : 0;
 #pragma unroll
                 for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], af, bf[ni]);
             }
@@ -236,7 +250,7 @@ size_t fdm_coef_doubles(int batch) { return (size_t)cstride() * batch; }
 
 template <int NA>
 static cudaError_t dst_pass(DstArgs a, bool ax0, int mode, cudaStream_t s) {
-    const size_t smem = sizeof(double) * ((size_t)NA * (NA + 4) + (size_t)NA * (TP + 8) + (size_t)TP * GLP);
+    const size_t smem = sizeof(double) * ((size_t)NA * (TP + 8) + (size_t)TP * GLP + 2 * (NA + 1));
     auto launch = [&](auto kern) -> cudaError_t {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
