@@ -573,6 +573,29 @@ __global__ void __launch_bounds__(Cfg<N>::NT, Cfg<N>::MINB) k_plane_fwd(PlaneArg
     if (tid < H) tma::bulk_wait_all();
 }
 
+// ps[r] = mult / den[r] with ONE division for all R values (prefix products, kept in ps
+// itself), every den >= 1; when the product of the R values leaves the range, one
+// division per value
+template <int R>
+__device__ __forceinline__ void psi_div(const double* den, double mult, double* ps) {
+    ps[0] = den[0];
+#pragma unroll
+    for (int r = 1; r < R; ++r) ps[r] = ps[r - 1] * den[r];
+    if (ps[R - 1] < 1e300) {
+        double inv = mult / ps[R - 1];
+#pragma unroll
+        for (int r = R - 1; r > 0; --r) {
+            const double v = inv * ps[r - 1];
+            inv *= den[r];
+            ps[r] = v;
+        }
+        ps[0] = inv;
+    } else {
+#pragma unroll
+        for (int r = 0; r < R; ++r) ps[r] = mult / den[r];
+    }
+}
+
 // ============================================================================ strided pass (axes >= 2)
 // Pencils along one axis of the spectrum [o][j][i] (stride I). MODE 0 forward,
 // 1 inverse, 2 forward x s Psi / N_tot x inverse (last axis; Alg. 3-5). Psi per
@@ -718,13 +741,13 @@ __global__ void __launch_bounds__(MidCfg<T, NA, VAR>::NT, MidCfg<T, NA, VAR>::MI
                 const int k2 = (int)r2;
                 const int N1 = 2 * (a.H1 - 1);
                 const int ks0 = k0 < a.N0 / 2 ? k0 : k0 - a.N0;
-                kap[0] = 2.0 * PMF_PI * ks0 / a.N0;
+                kap[0] = (2.0 * PMF_PI / a.N0) * ks0;
                 kx[0] = (2 * k0 == a.N0) ? 0.0 : kap[0];
-                kap[1] = 2.0 * PMF_PI * k1 / N1;                // k1 in [0, N1/2]: the half axis
+                kap[1] = (2.0 * PMF_PI / N1) * k1;              // k1 in [0, N1/2]: the half axis
                 kx[1] = (2 * k1 == N1) ? 0.0 : kap[1];
                 if (L == 3) {
                     const int ks2 = k2 < a.n2 / 2 ? k2 : k2 - a.n2;
-                    kap[2] = 2.0 * PMF_PI * ks2 / a.n2;
+                    kap[2] = (2.0 * PMF_PI / a.n2) * ks2;
                     kx[2] = (2 * k2 == a.n2) ? 0.0 : kap[2];
                 }
                 auto gam_bet = [&](int n, double& g, double& bb) {
@@ -802,28 +825,7 @@ __global__ void __launch_bounds__(MidCfg<T, NA, VAR>::NT, MidCfg<T, NA, VAR>::MI
                 if (cn) prodq(qt + 3 * nq, numr);
                 const double mult = P[PL_SN];
                 double ps[R1];
-                if constexpr (R1 % 4 != 0) {
-#pragma unroll
-                    for (int r = 0; r < R1; ++r) ps[r] = mult / den[r];
-                } else {
-                    // one division per 4 values (prefix products), unless the product leaves range
-#pragma unroll
-                    for (int g = 0; g < R1; g += 4) {
-                        const double p1 = den[g] * den[g + 1], p2 = p1 * den[g + 2], p3 = p2 * den[g + 3];
-                        if (p3 < 1e300) {
-                            double inv = mult / p3;
-                            ps[g + 3] = inv * p2;
-                            inv *= den[g + 3];
-                            ps[g + 2] = inv * p1;
-                            inv *= den[g + 2];
-                            ps[g + 1] = inv * den[g];
-                            ps[g] = inv * den[g + 1];
-                        } else {
-#pragma unroll
-                            for (int q = 0; q < 4; ++q) ps[g + q] = mult / den[g + q];
-                        }
-                    }
-                }
+                psi_div<R1>(den, mult, ps);
 #pragma unroll
                 for (int r = 0; r < R1; ++r) reinterpret_cast<double*>(col + (t + 8 * r) * PP)[0] = ps[r] * numr[r];
             }
@@ -1062,32 +1064,6 @@ __device__ __forceinline__ void psi_pair(const double* cf, int l, int cn, int li
     q[0] = double2{g0 * g1, fma(g0, b1, b0 * g1)};
     q[1] = double2{fma(g0, a1, fma(b0, b1, a0 * g1)), fma(b0, a1, a0 * b1)};
     q[2] = double2{a0 * a1, fma(a0, kn2, g0) * fma(a1, kn2, g1)};
-}
-
-// ps[r] = mult / den[r], one division per 4 values (prefix products) unless out of range
-template <int R>
-__device__ __forceinline__ void psi_div(const double* den, double mult, double* ps) {
-    if constexpr (R % 4 != 0) {
-#pragma unroll
-        for (int r = 0; r < R; ++r) ps[r] = mult / den[r];
-    } else {
-#pragma unroll
-        for (int g = 0; g < R; g += 4) {
-            const double p1 = den[g] * den[g + 1], p2 = p1 * den[g + 2], p3 = p2 * den[g + 3];
-            if (p3 < 1e300) {
-                double inv = mult / p3;
-                ps[g + 3] = inv * p2;
-                inv *= den[g + 3];
-                ps[g + 2] = inv * p1;
-                inv *= den[g + 2];
-                ps[g + 1] = inv * den[g];
-                ps[g] = inv * den[g + 1];
-            } else {
-#pragma unroll
-                for (int q = 0; q < 4; ++q) ps[g + q] = mult / den[g + q];
-            }
-        }
-    }
 }
 
 // F2 of one row: forward DFT along axis 2 of x (element t + 8r), result in place in the row
