@@ -112,8 +112,8 @@ typedef struct {
     void* stream;      /* cudaStream_t to enqueue on; NULL = the legacy default stream             */
     int   step;        /* PMF_STEP_EULER (0, the paper's semi-implicit Euler substeps)
                           or PMF_STEP_CN (Crank-Nicolson, second order in dt; R27, "higher order
-                          time stepping" = the paper's future work). CN runs on the plane or
-                          pencil kernels and is not combined with PMF_DIFF_FDM                  */
+                          time stepping" = the paper's future work). CN runs on every path
+                          (resident, plane, pencil) and is not combined with PMF_DIFF_FDM       */
     int   grid;        /* PMF_GRID_AXIS (0) or PMF_GRID_EIGEN: how pmf_set_gaussian and pmf_regrid
                           design a grid from a covariance                                           */
 } pmf_config;

@@ -67,9 +67,10 @@ enum {
     P_S = 21,       // s / N^2 (trace factor and the transform scales)
     P_LGN = 22,     // log normalising constant of the likelihood
     P_ISG = 23,     // 1 / sigma (range likelihood)
-    PRM_FIXED = 24  // then 3 doubles per Euler substep: dt/2 D00, dt/2 D11, dt D01
+    PRM_FIXED = 24  // then 3 doubles per coefficient set: h D00, h D11, 2h D01 with h = dt/2 (Euler,
+                    // l sets) or dt/4 (Crank-Nicolson, R27: l + 1 sets, grids t_0 .. t_l)
 };
-inline int prm_stride(int l) { return (PRM_FIXED + 3 * l + 1) & ~1; }
+inline int prm_stride(int nsets) { return (PRM_FIXED + 3 * nsets + 1) & ~1; }
 
 }  // namespace res
 
@@ -132,7 +133,8 @@ __global__ void k_res_prep(FilterState* st, double* prm, int pstride, ModelParam
     }
     const double det0 = B0[0] * B0[3] - B0[1] * B0[2];
     const double Bi0[4] = {B0[3] / det0, -B0[1] / det0, -B0[2] / det0, B0[0] / det0};
-    for (int n = lane; n < mp.l; n += 32) {
+    const double h = mp.step ? 0.25 * mp.dt : 0.5 * mp.dt;
+    for (int n = lane; n < mp.l + (mp.step ? 1 : 0); n += 32) {
         double D00, D01, D11;
         if (mp.diff_mode == 0) {           // R3: D_n = B0^-1 E_n B0^-T
             const double* E = sub[n].E;
@@ -153,9 +155,9 @@ __global__ void k_res_prep(FilterState* st, double* prm, int pstride, ModelParam
             D11 = mp.Q[5] / fma(b01, b01, b11 * b11);
             D01 = 0.0;
         }
-        P[PRM_FIXED + 3 * n] = 0.5 * mp.dt * D00;
-        P[PRM_FIXED + 3 * n + 1] = 0.5 * mp.dt * D11;
-        P[PRM_FIXED + 3 * n + 2] = mp.dt * D01;
+        P[PRM_FIXED + 3 * n] = h * D00;
+        P[PRM_FIXED + 3 * n + 1] = h * D11;
+        P[PRM_FIXED + 3 * n + 2] = 2.0 * h * D01;
     }
     if (lane != 0) return;
     const double* Mt = mp.Mtau;      // stride 4
@@ -364,7 +366,7 @@ __device__ __forceinline__ double warp_sum8(const double* v, int lane) {
 }
 
 // ============================================================================ the fused epoch kernel
-template <typename T, bool REGRID, bool UPDATE>
+template <typename T, bool REGRID, bool UPDATE, bool CN>
 __global__ void __launch_bounds__(NT, 1) k_resident_epoch(ResArgs<T> a) {
     using V = typename C2<T>::type;
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -556,12 +558,31 @@ __global__ void __launch_bounds__(NT, 1) k_resident_epoch(ResArgs<T> a) {
                     kx[q] = (k0[q] == N / 2) ? T(0) : kap0;
                     den[q] = T(1);
                 }
-                for (int n = 0; n < l; ++n) {
-                    const T ca = (T)cfp[3 * n], cb = (T)cfp[3 * n + 1], cc = (T)cfp[3 * n + 2];
-                    const T gam = fma(cb, k1sq, T(1));
-                    const T bet = cc * kx1;
+                T num[8];
+                if constexpr (!CN) {
+                    for (int n = 0; n < l; ++n) {
+                        const T ca = (T)cfp[3 * n], cb = (T)cfp[3 * n + 1], cc = (T)cfp[3 * n + 2];
+                        const T gam = fma(cb, k1sq, T(1));
+                        const T bet = cc * kx1;
 #pragma unroll
-                    for (int q = 0; q < 8; ++q) den[q] *= fma(ca, kk[q], fma(bet, kx[q], gam));
+                        for (int q = 0; q < 8; ++q) den[q] *= fma(ca, kk[q], fma(bet, kx[q], gam));
+                    }
+                } else {
+                    // Crank-Nicolson (R27): prod_{n<l} (2 - f_n) / prod_{n=1..l} f_n, f_n on the
+                    // grid at t_n (l + 1 coefficient sets scaled dt/4)
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) num[q] = T(1);
+                    for (int n = 0; n <= l; ++n) {
+                        const T ca = (T)cfp[3 * n], cb = (T)cfp[3 * n + 1], cc = (T)cfp[3 * n + 2];
+                        const T gam = fma(cb, k1sq, T(1));
+                        const T bet = cc * kx1;
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) {
+                            const T fq = fma(ca, kk[q], fma(bet, kx[q], gam));
+                            if (n > 0) den[q] *= fq;
+                            if (n < l) num[q] *= T(2) - fq;
+                        }
+                    }
                 }
                 if constexpr (sizeof(T) == 8) {
                     // one division for the 8 values (prefix products), unless the product leaves range
@@ -577,11 +598,19 @@ __global__ void __launch_bounds__(NT, 1) k_resident_epoch(ResArgs<T> a) {
                             inv *= den[q];
                         }
                         ps[0] = inv;
+                        if constexpr (CN) {
+#pragma unroll
+                            for (int q = 0; q < 8; ++q) ps[q] *= num[q];
+                        }
                         return;
                     }
                 }
 #pragma unroll
                 for (int q = 0; q < 8; ++q) ps[q] = sn2 / den[q];
+                if constexpr (CN) {
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) ps[q] *= num[q];
+                }
             };
             // packed rows k1 = 0 (A) and 64 (B): R = A + i B with A, B Hermitian in k0.
             // A(k) = (R(k) + conj R(-k))/2, B(k) = (R(k) - conj R(-k))/(2i); after the multiply
@@ -620,17 +649,25 @@ __global__ void __launch_bounds__(NT, 1) k_resident_epoch(ResArgs<T> a) {
 #pragma unroll
                 for (int q = 0; q < 8; ++q) packed(pa[q], pb[7 - q], false, px[q], py[q], false);
             } else {
-                // k0 = 64 (self-paired, both rows): scalar Euler product
-                T dA = T(1), dB = T(1);
+                // k0 = 64 (self-paired, both rows): scalar product (kx = 0 at the Nyquist
+                // wavenumbers: no cross term)
+                T dA = T(1), dB = T(1), nA = T(1), nB = T(1);
                 const T kN = kscale * (T)(-N / 2);
-                for (int n = 0; n < l; ++n) {
+                for (int n = 0; n < (CN ? l + 1 : l); ++n) {
                     const T ca = (T)cfp[3 * n], cb = (T)cfp[3 * n + 1];
-                    dA *= fma(ca, kN * kN, T(1));
-                    dB *= fma(ca, kN * kN, fma(cb, kN * kN, T(1)));
+                    const T fA = fma(ca, kN * kN, T(1)), fB = fma(ca, kN * kN, fma(cb, kN * kN, T(1)));
+                    if (!CN || n > 0) {
+                        dA *= fA;
+                        dB *= fB;
+                    }
+                    if (CN && n < l) {
+                        nA *= T(2) - fA;
+                        nB *= T(2) - fB;
+                    }
                 }
 #pragma unroll
                 for (int q = 0; q < 4; ++q) packed(pa[q], pa[(8 - q) & 7], q == 0, px[q], py[q], q == 0);
-                packed(pa[4], pa[4], true, sn2 / dA, sn2 / dB, false);
+                packed(pa[4], pa[4], true, sn2 * nA / dA, sn2 * nB / dB, false);
 #pragma unroll
                 for (int q = 0; q < 4; ++q) packed(pb[q], pb[7 - q], false, px[4 + q], py[4 + q], false);
             }
@@ -845,13 +882,13 @@ bool resident_supported(const Dims& d, int dtype) {
 
 size_t resident_param_bytes(int l, int batch) { return sizeof(double) * (size_t)prm_stride(l) * batch; }
 
-template <typename T, bool RG, bool UP>
+template <typename T, bool RG, bool UP, bool CN>
 static cudaError_t launch_t(ResArgs<T> a, cudaStream_t s, int64_t* launches, cudaEvent_t ev0, cudaEvent_t ev1) {
     using V = typename C2<T>::type;
     const size_t xbytes = std::max<size_t>(sizeof(V) * H * PITCH, stage_bytes<T>());
     const size_t smem = xbytes + sizeof(V) * 128 + 16 * 6 * sizeof(double) + 2 * sizeof(double) +
                         2 * sizeof(unsigned long long) + 2 * sizeof(double) * (size_t)a.pstride;
-    auto kern = k_resident_epoch<T, RG, UP>;
+    auto kern = k_resident_epoch<T, RG, UP, CN>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int dev = 0, nsm = 148, occ = 1;
@@ -871,7 +908,7 @@ static cudaError_t launch_t(ResArgs<T> a, cudaStream_t s, int64_t* launches, cud
 template <typename T>
 static cudaError_t launch_dt(const Dims& d, PencilBufs& b, const ModelParams& mp, const LikParams* lp, double ks,
                              cudaStream_t s, int64_t* launches) {
-    const int ps = prm_stride(mp.l);
+    const int ps = prm_stride(mp.l + (mp.step ? 1 : 0));
     LikParams lpv = lp ? *lp : LikParams{};
     k_res_prep<<<(d.batch + 3) / 4, 128, 0, s>>>(b.st, b.coef, ps, mp, b.sub, lpv, b.z, ks, lp ? 1 : 0, d.batch,
                                                 d.grid);
@@ -887,10 +924,17 @@ static cudaError_t launch_dt(const Dims& d, PencilBufs& b, const ModelParams& mp
     a.batch = d.batch;
     a.range = lpv.kind == 1;
     const bool rg = ks > 0.0;
-    if (rg && lp) e = launch_t<T, true, true>(a, s, launches, b.ev0, b.ev1);
-    else if (rg) e = launch_t<T, true, false>(a, s, launches, b.ev0, b.ev1);
-    else if (lp) e = launch_t<T, false, true>(a, s, launches, b.ev0, b.ev1);
-    else e = launch_t<T, false, false>(a, s, launches, b.ev0, b.ev1);
+    if (mp.step) {
+        if (rg && lp) e = launch_t<T, true, true, true>(a, s, launches, b.ev0, b.ev1);
+        else if (rg) e = launch_t<T, true, false, true>(a, s, launches, b.ev0, b.ev1);
+        else if (lp) e = launch_t<T, false, true, true>(a, s, launches, b.ev0, b.ev1);
+        else e = launch_t<T, false, false, true>(a, s, launches, b.ev0, b.ev1);
+    } else {
+        if (rg && lp) e = launch_t<T, true, true, false>(a, s, launches, b.ev0, b.ev1);
+        else if (rg) e = launch_t<T, true, false, false>(a, s, launches, b.ev0, b.ev1);
+        else if (lp) e = launch_t<T, false, true, false>(a, s, launches, b.ev0, b.ev1);
+        else e = launch_t<T, false, false, false>(a, s, launches, b.ev0, b.ev1);
+    }
     if (e != cudaSuccess) return e;
     k_res_finalize<<<(d.batch + 127) / 128, 128, 0, s>>>(b.st, b.partials, b.coef, ps, mp.s, lp ? 1 : 0, d.batch);
     ++*launches;

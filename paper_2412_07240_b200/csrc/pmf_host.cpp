@@ -356,8 +356,9 @@ static int flush_direct(pmf_ctx* c, const LikParams* lp) {
         c->pend = Pending{};
         return PMF_OK;
     }
-    // the resident kernel keeps 3 coefficients per substep in shared memory
-    const bool resident = c->path == PMF_PATH_RESIDENT && c->pend.predict && c->pend.steps <= 2048;
+    // the resident kernel keeps 3 coefficients per substep (l + 1 sets for Crank-Nicolson) in
+    // two shared-memory buffers next to its 141 KB spectrum: up to 1024 substeps per call
+    const bool resident = c->path == PMF_PATH_RESIDENT && c->pend.predict && c->pend.steps <= 1024;
     if (resident) {
         attach_events(c, b);
         e = launch_resident(c->d, c->dtype, b, twid(c), &c->mp, lp, c->pend.regrid ? c->pend.k_sigma : -1.0,
@@ -632,7 +633,7 @@ int pmf_create(const pmf_config* cfg, const double* A, const double* Q, pmf_ctx*
     d.src_n = d.n[nx - 1];
     d.grid = cfg->grid;
 
-    bool res_ok = resident_supported(d, c->dtype) && cfg->step == PMF_STEP_EULER;
+    bool res_ok = resident_supported(d, c->dtype);
     bool plane_ok = plane_supported(d, 1);
     if (cfg->path == PMF_PATH_RESIDENT && !res_ok) {
         delete c;

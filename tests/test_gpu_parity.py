@@ -252,15 +252,19 @@ def test_graph_replay_bitwise_equal(cid, over):
     assert a[4] == b[4]
 
 
-@pytest.mark.parametrize("name", ["C1", "C2s", "C3s", "C4s", "C5s", "C3_plane_32", "C4_plane_32"])
+@pytest.mark.parametrize("name", ["C1", "C2s", "C3s", "C4s", "C5s", "C3_plane_32", "C4_plane_32", "C5_resident",
+                                  "C5_resident_step"])
 def test_crank_nicolson_parity(name):
     """NEXT-4: Crank-Nicolson substeps (R27) through the C ABI vs the oracle's STEP_CN on
-    the pencil kernels (resident falls back to them) and the plane kernels."""
-    extra = {"C3_plane_32": ("C3", {"n": (32, 32, 16)}, 2), "C4_plane_32": ("C4", {"n": (32, 32, 16, 16)}, 2)}
+    the pencil, plane and resident kernels (the latter eager and through pmf_step)."""
+    extra = {"C3_plane_32": ("C3", {"n": (32, 32, 16)}, 2), "C4_plane_32": ("C4", {"n": (32, 32, 16, 16)}, 2),
+             "C5_resident": ("C5", {"batch": 3}, 3), "C5_resident_step": ("C5", {"batch": 3}, 3)}
     cid, over, T = extra.get(name) or CASES[name]
     cfg = make_config(cid, **over)
     zs = simulate(cfg, T=T)["z"]
-    g = run_gpu(cfg, zs, T, step=pmf.STEP_CN)
+    g = run_gpu(cfg, zs, T, step=pmf.STEP_CN, use_step=name.endswith("_step"))
+    if name.startswith("C5_resident"):
+        assert g["filter"].path == pmf.PATH_RESIDENT
     orc = {b: O.run_filter(cfg, zs, b=b, T=T, keep_weights=True, step=O.STEP_CN) for b in range(cfg.batch)}
     e = compare_runs(cfg, g, orc, T, 1e-10)
     assert e["w"] <= 1e-10, e
