@@ -689,6 +689,146 @@ __global__ void k_pack_blocks(const V* __restrict__ S, V* __restrict__ send, lon
     }
 }
 
+// ============================================================================ nx = 1: one launch per epoch
+// The whole epoch of a 1-D filter in one CTA (BASELINE C1 is launch-latency bound):
+// [regrid of the previous posterior (R12): target grid, linear interpolation of the stored
+// weights with zero ghosts, renormalisation by summation] -> per-substep Euler (or CN)
+// coefficients on the start grid (Alg. 3, R3/R4) -> grid motion (eq:gridMov) and the
+// closed-form predict normalisation (Alg. 6) -> forward DFT, s Psi / N, inverse (Alg. 1-5)
+// -> likelihood at the moved points (eq:filt P:46) -> normaliser, moments.
+// Same arithmetic as k_regrid_gather + k_finalize_regrid + k_predict_prep + k_line_psi +
+// k_finalize, without the four kernel boundaries. cfs: nsets coefficients in shared memory.
+template <typename T, bool UPDATE, bool RG, int NC>
+__global__ void __launch_bounds__(kThreads, 2) k_line_epoch(T* __restrict__ W, FilterState* st, Dims d,
+                                                          FFTPlan pl, const typename C2<T>::type* __restrict__ tw,
+                                                          ModelParams mp, const SubstepEntry* __restrict__ sub,
+                                                          LikParams lp, const double* __restrict__ z, double ks) {
+    using V = typename C2<T>::type;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int N = NC > 0 ? NC : d.n[0], PS = pencil_stride<NC>(N);
+    V* a = reinterpret_cast<V*>(smem_raw);
+    V* b = a + PS;
+    double* red = reinterpret_cast<double*>(b + PS);
+    double* cfs = red + 32 * NMOM;                          // [nsets] h D_n (nx = 1)
+    // M, o, input scale, skip flag, moved grid c_l, B_l, closed-form scale: written by thread
+    // 0, read by all through shared memory
+    __shared__ double sh[8];
+    const int filt = blockIdx.x, tid = threadIdx.x;
+    FilterState& f = st[filt];
+    T* row = W + (long long)filt * N;
+    double acc[NMOM];
+    if (RG) {
+        // ------------------------------------------------------------ regrid (R12)
+        if (tid == 0) {
+            double cn[4], Bn[16], Bi[16], M[16];
+            regrid_target(1, d.ng, f, ks, cn, Bn, d.grid);
+            mat_inv4(1, f.B, Bi);
+            for (int i = 0; i < 16; ++i) M[i] = 0.0;
+            mat_mul4(1, Bi, Bn, M);
+            sh[0] = M[0];
+            sh[1] = fma(Bi[0], cn[0] - f.c[0], 0.5 * (d.ng[0] - 1));
+        }
+        for (int j = tid; j < N; j += blockDim.x) b[j] = V{row[j], T(0)};
+        __syncthreads();
+        const double M0 = sh[0], o0 = sh[1];
+#pragma unroll
+        for (int i = 0; i < NMOM; ++i) acc[i] = 0.0;
+        for (int j = tid; j < N; j += blockDim.x) {
+            const double v = fma(M0, (double)j - 0.5 * (N - 1), o0), fl = floor(v);
+            const int i0 = __double2int_rz(fl);
+            const double fr = v - fl;
+            double val = 0.0;
+            if (i0 >= 0 && i0 <= N - 1) val = fma(1.0 - fr, (double)b[i0].x, val);
+            if (i0 >= -1 && i0 <= N - 2) val = fma(fr, (double)b[i0 + 1].x, val);
+            const T vt = (T)val;
+            a[sx<NC>(j)] = V{vt, T(0)};
+            acc[0] += (double)vt;
+        }
+        block_sum<NMOM>(acc, red);                          // ends with a barrier
+        if (tid == 0) {
+            finalize_from(f, acc, d, 2, ks);                // new grid, scale = 1 / (vol' sum)
+            sh[3] = f.status != 0 ? 1.0 : 0.0;
+        }
+        __syncthreads();
+        if (sh[3] != 0.0) {                                 // degenerate target: weights kept
+            return;
+        }
+    }
+    // ---------------------------------------------------------------- prep (k_predict_prep)
+    const int nsets = mp.l + (mp.step ? 1 : 0);
+    {
+        double B0[16], Bi[16];
+        for (int i = 0; i < 16; ++i) B0[i] = f.B[i];
+        mat_inv4(1, B0, Bi);
+        for (int n = tid; n < nsets; n += blockDim.x) {
+            double o[10];
+            substep_coefs(1, B0, Bi, mp, sub[n], o);
+            cfs[n] = o[0];
+        }
+    }
+    __syncthreads();                                        // every thread has read f.B
+    if (tid == 0) {
+        sh[2] = f.scale;                                    // input scale
+        const double vol0 = fabs(f.B[0]);
+        const double Bn = mp.Mtau[0] * f.B[0], cn = mp.Mtau[0] * f.c[0];
+        f.B[0] = Bn;
+        f.c[0] = cn;
+        f.scale = vol0 / (fabs(Bn) * mp.s);
+        sh[4] = cn;
+        sh[5] = Bn;
+        sh[6] = f.scale;
+    }
+    if (!RG)
+        for (int j = tid; j < N; j += blockDim.x) a[sx<NC>(j)] = V{row[j], T(0)};
+    __syncthreads();
+    // ---------------------------------------------------------------- predict (k_line_psi)
+    const T sc = (T)sh[2];
+    for (int j = tid; j < N; j += blockDim.x) {
+        const V v = a[sx<NC>(j)];
+        a[sx<NC>(j)] = V{v.x * sc, T(0)};
+    }
+    __syncthreads();
+    V* r = fft_any<NC, false>(a, b, 1, PS, pl, tw);
+    const double mult = mp.s / N;
+    for (int k = tid; k < N; k += blockDim.x) {
+        double kap, kx;
+        wavenum(k, N, kap, kx);
+        double prod = 1.0, num = 1.0;
+        if (!mp.step) {
+            for (int n = 0; n < mp.l; ++n) prod *= fma(cfs[n], kap * kap, 1.0);
+        } else {          // Crank-Nicolson (R27)
+            for (int n = 0; n < mp.l; ++n) num *= 1.0 - cfs[n] * kap * kap;
+            for (int n = 1; n <= mp.l; ++n) prod *= fma(cfs[n], kap * kap, 1.0);
+        }
+        const T ps = (T)(mult * num / prod);
+        V v = r[sx<NC>(k)];
+        r[sx<NC>(k)] = V{v.x * ps, v.y * ps};
+    }
+    __syncthreads();
+    r = fft_any<NC, true>(r, (r == a) ? b : a, 1, PS, pl, tw);
+#pragma unroll
+    for (int i = 0; i < NMOM; ++i) acc[i] = 0.0;
+    const double scale = sh[6], cl = sh[4], Bl = sh[5];
+    const double* zf = z + (long long)filt * lp.nz;
+    for (int j = tid; j < N; j += blockDim.x) {
+        double w = (double)r[sx<NC>(j)].x;
+        if (UPDATE) {
+            double u = j - 0.5 * (N - 1);
+            double x = fma(Bl, u, cl);                      // the moved point (R13)
+            w = w * scale * exp_fast(log_lik(lp, &x, zf));
+            T wt = (T)w;
+            row[j] = wt;
+            acc_mom<1>((double)wt, &u, acc);
+        } else {
+            row[j] = (T)w;
+        }
+    }
+    if (UPDATE) {
+        block_sum<NMOM>(acc, red);
+        if (tid == 0) finalize_from(f, acc, d, 0, 0.0);    // normaliser, log C, moments
+    }
+}
+
 // ============================================================================ regrid
 // Multilinear interpolation with zero ghost nodes at the points of the new grid
 // (R12). v = B^-1 (x' - c) + (N-1)/2 = o + M u' with M = B^-1 B', o = B^-1(c'-c)+(N-1)/2.
@@ -1168,6 +1308,44 @@ static cudaError_t predict_pencil_t(const Dims& d, PencilBufs& b, const Twiddles
     }
     if (b.ev1) cudaEventRecordWithFlags(b.ev1, s, cudaEventRecordExternal);
     return e;
+}
+
+template <typename T>
+static cudaError_t line_epoch_t(const Dims& d, PencilBufs& b, const Twiddles& tw, const ModelParams& mp,
+                                const LikParams* lp, double ks, cudaStream_t s, int64_t* launches) {
+    using V = typename C2<T>::type;
+    const int nsets = mp.l + (mp.step ? 1 : 0);
+    FFTPlan pl = make_plan(d.n[0]);
+    const size_t sm = 2 * pstride_host(d.n[0]) * sizeof(V) + 32 * NMOM * sizeof(double) + nsets * sizeof(double);
+    LikParams lpv{};
+    if (lp) lpv = *lp;
+    if (b.ev0) cudaEventRecordWithFlags(b.ev0, s, cudaEventRecordExternal);
+    PMF_TRY(with_nc(d.n[0], [&](auto nc) -> cudaError_t {
+        constexpr int NC = decltype(nc)::value;
+        auto go = [&](auto kern) -> cudaError_t {
+            PMF_TRY(smem_attr(kern, sm));
+            kern<<<d.batch, kThreads, sm, s>>>((T*)b.W, b.st, d, pl, (const V*)tw.tw[0], mp, b.sub, lpv, b.z, ks);
+            return cudaGetLastError();
+        };
+        if (lp && ks > 0.0) return go(k_line_epoch<T, true, true, NC>);
+        if (lp) return go(k_line_epoch<T, true, false, NC>);
+        if (ks > 0.0) return go(k_line_epoch<T, false, true, NC>);
+        return go(k_line_epoch<T, false, false, NC>);
+    }));
+    ++*launches;
+    if (b.ev1) cudaEventRecordWithFlags(b.ev1, s, cudaEventRecordExternal);
+    return cudaGetLastError();
+}
+
+// nx = 1 whole epoch in one launch; nsets coefficients must fit next to the two lines
+bool line_epoch_supported(const Dims& d, int nsets) {
+    return d.nx == 1 && nsets <= 4096 && d.n[0] <= 4096;
+}
+
+cudaError_t launch_line_epoch(const Dims& d, int dtype, PencilBufs& b, const Twiddles& tw, const ModelParams& mp,
+                              const LikParams* lp, double ks, cudaStream_t s, int64_t* launches) {
+    if (dtype == 0) return line_epoch_t<double>(d, b, tw, mp, lp, ks, s, launches);
+    return line_epoch_t<float>(d, b, tw, mp, lp, ks, s, launches);
 }
 
 cudaError_t launch_predict_pencil(const Dims& d, int dtype, PencilBufs& b, const Twiddles& tw,

@@ -356,6 +356,16 @@ static int flush_direct(pmf_ctx* c, const LikParams* lp) {
         c->pend = Pending{};
         return PMF_OK;
     }
+    // nx = 1: regrid + predict + update + moments of every filter in ONE launch
+    if (c->d.nx == 1 && c->pend.predict && line_epoch_supported(c->d, c->pend.steps + (c->mp.step ? 1 : 0)) &&
+        std::getenv("PMF_NO_LINE_EPOCH") == nullptr) {
+        attach_events(c, b);
+        e = launch_line_epoch(c->d, c->dtype, b, twid(c), c->mp, lp, c->pend.regrid ? c->pend.k_sigma : -1.0,
+                              c->stream, &c->launches);
+        if (e != cudaSuccess) return cuda_fail(c, e, "line epoch kernel");
+        c->pend = Pending{};
+        return PMF_OK;
+    }
     // the resident kernel keeps 3 coefficients per substep (l + 1 sets for Crank-Nicolson) in
     // two shared-memory buffers next to its 141 KB spectrum: up to 1024 substeps per call
     const bool resident = c->path == PMF_PATH_RESIDENT && c->pend.predict && c->pend.steps <= 1024;
