@@ -719,14 +719,17 @@ __global__ void __launch_bounds__(kThreads, 2) k_line_epoch(T* __restrict__ W, F
     double acc[NMOM];
     if (RG) {
         // ------------------------------------------------------------ regrid (R12)
+        // scalar tails (nx = 1): thread 0 only, no local arrays on the critical path
+        double cn1 = 0.0, Bn1 = 0.0;
+        bool ok = true;
         if (tid == 0) {
-            double cn[4], Bn[16], Bi[16], M[16];
-            regrid_target(1, d.ng, f, ks, cn, Bn, d.grid);
-            mat_inv4(1, f.B, Bi);
-            for (int i = 0; i < 16; ++i) M[i] = 0.0;
-            mat_mul4(1, Bi, Bn, M);
-            sh[0] = M[0];
-            sh[1] = fma(Bi[0], cn[0] - f.c[0], 0.5 * (d.ng[0] - 1));
+            double cn[4], Bn[16];
+            ok = regrid_target(1, d.ng, f, ks, cn, Bn, d.grid);
+            cn1 = cn[0];
+            Bn1 = Bn[0];
+            const double Bi = 1.0 / f.B[0];
+            sh[0] = Bi * Bn1;                                  // M = B^-1 B'
+            sh[1] = fma(Bi, cn1 - f.c[0], 0.5 * (d.ng[0] - 1));  // o = B^-1 (c' - c) + (N-1)/2
         }
         for (int j = tid; j < N; j += blockDim.x) b[j] = V{row[j], T(0)};
         __syncthreads();
@@ -746,7 +749,12 @@ __global__ void __launch_bounds__(kThreads, 2) k_line_epoch(T* __restrict__ W, F
         }
         block_sum<NMOM>(acc, red);                          // ends with a barrier
         if (tid == 0) {
-            finalize_from(f, acc, d, 2, ks);                // new grid, scale = 1 / (vol' sum)
+            // commit the regrid (finalize_from mode 2): new grid, scale = 1 / (vol' sum)
+            const double C = fabs(Bn1) * acc[0];
+            f.c[0] = cn1;
+            f.B[0] = Bn1;
+            if (!ok || !(C > 0.0) || !isfinite(C)) f.status = -6;
+            else f.scale = 1.0 / C;
             sh[3] = f.status != 0 ? 1.0 : 0.0;
         }
         __syncthreads();
@@ -825,7 +833,24 @@ __global__ void __launch_bounds__(kThreads, 2) k_line_epoch(T* __restrict__ W, F
     }
     if (UPDATE) {
         block_sum<NMOM>(acc, red);
-        if (tid == 0) finalize_from(f, acc, d, 0, 0.0);    // normaliser, log C, moments
+        if (tid == 0) {
+            // normaliser C = vol sum, log C, scale, moments (R14): finalize_from mode 0
+            const double C = fabs(Bl) * acc[0];
+            f.mass = acc[0];
+            f.has_moments = 1;
+            if (!(C > 0.0) || !isfinite(C)) {
+                f.status = -6;
+                f.logC = -INFINITY;
+            } else {
+                f.status = 0;
+                f.logC = log(C);
+                f.scale = 1.0 / C;
+                const double ub = acc[1] / acc[0];
+                const double su = acc[2] / acc[0] - ub * ub;
+                f.mean[0] = fma(Bl, ub, cl);
+                f.cov[0] = fma(fma(Bl, su, 0.0), Bl, 0.0);
+            }
+        }
     }
 }
 
