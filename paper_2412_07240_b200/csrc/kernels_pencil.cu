@@ -47,7 +47,7 @@ static int rows_per_cta(int N, long long rows_per_filter) {
 }
 
 static int pstride_host(int N) {
-    const bool ct = N == 64 || N == 96 || N == 128 || N == 256;   // with_nc's compile-time sizes
+    const bool ct = N == 34 || N == 64 || N == 96 || N == 128 || N == 256;   // with_nc's compile-time sizes
     return ct ? N + N / 8 + 1 : N + 1;
 }
 
@@ -1179,6 +1179,7 @@ static cudaError_t smem_attr(K kernel, size_t bytes) {
 template <typename F>
 static cudaError_t with_nc(int N, F&& f) {
     switch (N) {
+        case 34: return f(std::integral_constant<int, 34>{});   // the paper's N_pa = 34
         case 64: return f(std::integral_constant<int, 64>{});
         case 96: return f(std::integral_constant<int, 96>{});
         case 128: return f(std::integral_constant<int, 128>{});
