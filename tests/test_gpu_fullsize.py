@@ -1,7 +1,7 @@
 """Parity at BASELINE.json's FULL sizes, through the C ABI in the
 launch configuration bench.py times where it applies:
 
-* C2 (one 256^2 filter, 10 epochs) and C3 (one 128^3 filter, 2 epochs): the oracle
+* C2 (one 256^2 filter, all 100 epochs) and C3 (one 128^3 filter, 2 epochs): the oracle
   runs them whole; every epoch's weights, moments, normaliser and grid are compared.
 * C5 (4096 filters x 128^2, the bench workload): the whole batch runs on the GPU with
   the fused pmf_step API (as bench.py), the oracle runs a sample of filters one by one;
@@ -25,7 +25,7 @@ from parity_util import TOL, compare_runs, lik_of, make_filter, rel_linf, run_gp
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("cid, T", [("C2", 10), ("C3", 2)])
+@pytest.mark.parametrize("cid, T", [("C2", 100), ("C3", 2)])
 def test_full_size_whole_filter_vs_oracle(cid, T):
     cfg = make_config(cid)
     zs = simulate(cfg, T=T)["z"]
@@ -33,6 +33,21 @@ def test_full_size_whole_filter_vs_oracle(cid, T):
     orc = run_oracle(cfg, zs, T)
     e = compare_runs(cfg, g, orc, T, TOL["f64"])
     assert max(e.values()) <= 1e-10, e
+
+
+def test_c5_all_epochs_resident_vs_oracle():
+    """BASELINE C5's full run length (50 epochs) on the resident kernel for two filters:
+    no drift of the GPU filter away from the oracle over the whole run."""
+    cfg = make_config("C5", batch=2)
+    T = cfg.T
+    assert T == 50
+    zs = simulate(cfg, T=T)["z"]
+    g = run_gpu(cfg, zs, T, path=pmf.PATH_RESIDENT, keep_weights=False)
+    orc = run_oracle(cfg, zs, T)
+    e = compare_runs(cfg, g, orc, T, TOL["f64"], check_weights=False)
+    assert max(e.values()) <= 1e-10, e
+    wo = O.to_lib(orc[1]["final"][0])
+    assert rel_linf(g["filter"].weights()[1], wo) < 1e-10
 
 
 def test_full_size_c5_batch_sampled_vs_oracle():
