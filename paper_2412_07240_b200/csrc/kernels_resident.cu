@@ -451,27 +451,33 @@ __global__ void __launch_bounds__(NT, 1) k_resident_epoch(ResArgs<T> a) {
                 // upper-triangular map (CV drift after an axis-aligned regrid): v1 does not
                 // depend on the column, one split per row serves both columns
                 const bool tri = M2 == 0.0;
+                // odd teams gather their second column first: the 4 teams of a warp then read
+                // columns of both parities in each load, which halves the bank conflicts of
+                // the even staging pitch (4 -> 2 wavefronts per 8-byte gather)
+                const bool sw = m & 1;
+                const double b0a = sw ? b0[1] : b0[0], b0b = sw ? b0[0] : b0[1];
+                const double b1a = sw ? b1[1] : b1[0], b1b = sw ? b1[0] : b1[1];
 #pragma unroll
                 for (int r = 0; r < 16; ++r) {
                     T val[2];
                     int i1r;
                     double a1r;
-                    split(fma((double)r, s1, b1[0]), i1r, a1r);
+                    split(fma((double)r, s1, b1a), i1r, a1r);
 #pragma unroll
-                    for (int e = 0; e < 2; ++e) {
+                    for (int q = 0; q < 2; ++q) {
                         int i0, i1 = i1r;
                         double a0, a1 = a1r;
-                        split(fma((double)r, s0, b0[e]), i0, a0);
-                        if (e == 1 && !tri) split(fma((double)r, s1, b1[e]), i1, a1);
+                        split(fma((double)r, s0, q ? b0b : b0a), i0, a0);
+                        if (q == 1 && !tri) split(fma((double)r, s1, b1b), i1, a1);
                         const T* row0 = reinterpret_cast<const T*>(Xs + i1 * (int)StagePitch<T>::B) + i0;
                         const T* row1 = reinterpret_cast<const T*>(reinterpret_cast<const char*>(row0) + StagePitch<T>::B);
                         const double w00 = (double)row0[0], w01 = (double)row0[1];
                         const double w10 = (double)row1[0], w11 = (double)row1[1];
                         const double lo = fma(a0, w01 - w00, w00);
                         const double hi = fma(a0, w11 - w10, w10);
-                        val[e] = (T)fma(a1, hi - lo, lo);
+                        val[q] = (T)fma(a1, hi - lo, lo);
                     }
-                    z[r] = V{val[0], val[1]};
+                    z[r] = sw ? V{val[1], val[0]} : V{val[0], val[1]};
                 }
             }
             __syncthreads();                      // the staged weights are consumed: X is free
