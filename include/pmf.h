@@ -201,6 +201,15 @@ int pmf_moments(pmf_ctx* ctx, double* mean, double* cov, double* log_norm);
 /* Bytes pmf_moments copies device -> host per call ((nx + nx^2 + 2) doubles per filter). */
 int64_t pmf_moments_bytes(const pmf_ctx* ctx);
 
+/* Asynchronous form of pmf_moments for pipelined callers: enqueues the packing and the
+ * device -> host copy of the last update's moments into `dst` (pmf_moments_bytes bytes,
+ * host memory the caller owns -- pinned for a truly asynchronous copy) on the context's
+ * stream and returns at once. Record of filter b at dst + b (nx + nx^2 + 2) doubles:
+ * mean[nx], cov[nx*nx] (row-major), log normaliser, failure flag (nonzero: that filter's
+ * last update failed, the PMF_E_NO_SUPPORT of pmf_moments). Valid after pmf_sync (or any
+ * synchronising call). PMF_E_STATE before the first update. */
+int pmf_moments_async(pmf_ctx* ctx, double* dst);
+
 /* Re-centre every filter's grid on its last posterior (R12; the paper is silent,
  * north_star "re-centre the grid"): c' = mean, B' = diag(2 k_sigma sqrt(cov_mm)/N_m)
  * (PMF_GRID_EIGEN: the eigenvector-aligned B' of R28, see pmf_config.grid),

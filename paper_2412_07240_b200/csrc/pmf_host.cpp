@@ -880,6 +880,20 @@ int pmf_moments(pmf_ctx* c, double* mean, double* cov, double* log_norm) {
     return PMF_OK;
 }
 
+int pmf_moments_async(pmf_ctx* c, double* dst) {
+    if (!c || !dst) return fail(c, PMF_E_ARG, "null argument");
+    if (c->sh) return fail(c, PMF_E_ARG, "pmf_moments_async: not for sharded contexts");
+    if (!c->have_update) return fail(c, PMF_E_STATE, "no update has run");
+    CK(c, cudaSetDevice(c->cfg.device), "cudaSetDevice");
+    // (a recorded regrid / predict stays pending, as with pmf_moments: the moments are the
+    // last update's, and the pending work fuses into the next epoch's launch)
+    cudaError_t e = launch_pack_moments(c->d, c->st, c->mom_dev, c->stream, &c->launches);
+    if (e != cudaSuccess) return cuda_fail(c, e, "pack moments");
+    CK(c, cudaMemcpyAsync(dst, c->mom_dev, (size_t)pmf_moments_bytes(c), cudaMemcpyDeviceToHost, c->stream),
+       "moments download");
+    return PMF_OK;
+}
+
 int64_t pmf_moments_bytes(const pmf_ctx* c) {
     return c ? (int64_t)sizeof(double) * (c->d.nx + c->d.nx * c->d.nx + 2) * c->d.batch : 0;
 }

@@ -33,7 +33,7 @@ SYMBOLS = ["pmf_create", "pmf_destroy", "pmf_last_error", "pmf_set_gaussian", "p
            "pmf_predict", "pmf_update", "pmf_moments", "pmf_regrid", "pmf_step", "pmf_get_weights",
            "pmf_get_grid", "pmf_sync", "pmf_launch_count", "pmf_moments_bytes", "pmf_nccl_unique_id",
            "pmf_create_sharded", "pmf_world", "pmf_profile", "pmf_profile_read", "pmf_use_graphs",
-           "pmf_set_terrain", "pmf_device_bytes", "pmf_path", "pmf_version"]
+           "pmf_set_terrain", "pmf_device_bytes", "pmf_path", "pmf_version", "pmf_moments_async"]
 
 
 class PMFError(RuntimeError):
@@ -83,6 +83,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         "pmf_sync": (I, [P]),
         "pmf_launch_count": (C.c_int64, [P]),
         "pmf_moments_bytes": (C.c_int64, [P]),
+        "pmf_moments_async": (I, [P, V]),
         "pmf_nccl_unique_id": (I, [V]),
         "pmf_create_sharded": (I, [C.POINTER(pmf_config), D, D, I, I, V, C.POINTER(P)]),
         "pmf_world": (I, [P]),
@@ -299,6 +300,13 @@ class Filter:
         ms, n = C.c_double(), C.c_int64()
         self._check(self.lib.pmf_profile_read(self.h, C.byref(ms), C.byref(n)))
         return ms.value, n.value
+
+    def moments_async(self, dst) -> None:
+        """Enqueue the last update's moments into ``dst`` (pinned host memory, a torch tensor
+        or numpy array of moments_bytes bytes): records of (nx + nx^2 + 2) doubles per
+        filter -- mean, cov, log normaliser, failure flag. Read after sync()."""
+        ptr = dst.data_ptr() if hasattr(dst, "data_ptr") else dst.ctypes.data
+        self._check(self.lib.pmf_moments_async(self.h, C.c_void_p(ptr)))
 
     @property
     def moments_bytes(self) -> int:

@@ -8,7 +8,7 @@ from oracle import pmf_oracle as O
 from paper_2412_07240_b200 import pmf
 from workloads import make_config, random_density, simulate
 
-from parity_util import TOL, compare_runs, lik_of, rel_linf, run_gpu, run_oracle
+from parity_util import TOL, compare_runs, lik_of, make_filter, rel_linf, run_gpu, run_oracle
 
 pytestmark = pytest.mark.gpu
 
@@ -314,3 +314,28 @@ def test_terrain_likelihood_resident_and_plane():
     orc = {0: O.run_filter(cfg, zs, b=0, T=T, keep_weights=True)}
     e = compare_runs(cfg, g, orc, T, 1e-10)
     assert e["w"] <= 1e-10 and e["mean"] <= 1e-10 and e["logC"] <= 1e-10, e
+
+
+def test_moments_async_matches_moments():
+    """pmf_moments_async: the same records as pmf_moments (mean, cov, log C, flag), read
+    after a sync, with the pending regrid left pending (the next step still fuses it)."""
+    import torch
+    cfg = make_config("C5", batch=3)
+    zs = simulate(cfg, T=2)["z"]
+    f = make_filter(cfg)
+    lik = lik_of(cfg)
+    f.update(zs[0], lik)
+    f.regrid(cfg.k_sigma)
+    f.step(cfg.tau / cfg.l, cfg.l, zs[1], lik, cfg.k_sigma)
+    n0 = f.launches
+    buf = torch.empty(f.moments_bytes // 8, dtype=torch.float64).pin_memory()
+    f.moments_async(buf)
+    assert f.launches - n0 == 1          # the pack only: the recorded regrid stays pending
+    torch.cuda.synchronize()
+    mean, cov, logc = f.moments()
+    rec = buf.numpy().reshape(cfg.batch, -1)
+    nx = cfg.nx
+    assert np.array_equal(rec[:, :nx], mean)
+    assert np.array_equal(rec[:, nx:nx + nx * nx].reshape(cfg.batch, nx, nx), cov)
+    assert np.array_equal(rec[:, nx + nx * nx], logc)
+    assert np.all(rec[:, -1] == 0.0)
