@@ -66,3 +66,22 @@ def test_eigen_grid_plane_4d():
 def test_eigen_grid_pencil_4d():
     cfg = make_config("C4", n=(16, 16, 16, 16), prior_cov=P4)
     _check(cfg, 2, pmf.PATH_PENCIL)
+
+
+@pytest.mark.parametrize("cid, n, path, P", [("C5", (128, 128), pmf.PATH_RESIDENT, P2),
+                                             ("C4", (32, 32, 16, 16), pmf.PATH_PLANE, P4),
+                                             ("C1", (64,), pmf.PATH_AUTO, np.array([[0.3]]))])
+def test_eigen_grid_with_crank_nicolson(cid, n, path, P):
+    """R28 combined with Crank-Nicolson substeps (R27): both options at once, every path
+    that takes them (nx = 1 runs the single-kernel epoch)."""
+    over = {"n": n, "prior_cov": P}
+    if cid == "C5":
+        over["batch"] = 2
+    cfg = make_config(cid, **over)
+    T = 2
+    zs = simulate(cfg, T=T)["z"]
+    g = run_gpu(cfg, zs, T, path=path, grid=pmf.GRID_EIGEN, step=pmf.STEP_CN)
+    orc = {b: O.run_filter(cfg, zs, b=b, T=T, keep_weights=True, grid=O.GRID_EIGEN, step=O.STEP_CN)
+           for b in range(cfg.batch)}
+    e = compare_runs(cfg, g, orc, T, TOL["f64"])
+    assert max(e.values()) <= 1e-10, e
