@@ -339,3 +339,43 @@ def test_moments_async_matches_moments():
     assert np.array_equal(rec[:, nx:nx + nx * nx].reshape(cfg.batch, nx, nx), cov)
     assert np.array_equal(rec[:, nx + nx * nx], logc)
     assert np.all(rec[:, -1] == 0.0)
+
+
+@pytest.mark.parametrize("cid, over, path", [("C5", {"batch": 3}, pmf.PATH_RESIDENT),
+                                             ("C4", {"n": (32, 32, 16, 16)}, pmf.PATH_PLANE),
+                                             ("C1", {}, pmf.PATH_AUTO)])
+def test_checkpoint_resume(cid, over, path):
+    """Checkpoint / resume through the ABI: the weights and grid of a run (pmf_get_weights,
+    pmf_get_grid) loaded into a NEW context (pmf_set_state) continue the run as if it had
+    not stopped."""
+    cfg = make_config(cid, **over)
+    T = 4
+    zs = simulate(cfg, T=T)["z"]
+    lik = lik_of(cfg)
+    dt = cfg.tau / cfg.l
+
+    def epochs(f, ks):
+        out = []
+        for k in ks:
+            if k > 0:
+                f.predict(dt, cfg.l)
+            f.update(zs[k], lik)
+            out.append(f.moments())
+            f.regrid(cfg.k_sigma)
+        return out
+
+    a = make_filter(cfg, path=path)
+    ra = epochs(a, range(T + 1))
+    b = make_filter(cfg, path=path)
+    rb = epochs(b, range(3))
+    w, (c, B) = b.weights(), b.grid()                 # checkpoint after epoch 2's regrid
+    b.close()
+    r = pmf.Filter(cfg.nx, cfg.n, cfg.A, cfg.Q, batch=cfg.batch, path=path)
+    r.set_state(c, B, w)
+    rb += epochs(r, range(3, T + 1))
+    for k in range(T + 1):
+        for x, y in zip(ra[k][:2], rb[k][:2]):
+            assert np.max(np.abs(x - y)) <= 1e-12 * max(1.0, np.max(np.abs(x))), (k, x, y)
+        assert np.max(np.abs(ra[k][2] - rb[k][2])) <= 1e-12
+    wa, wr = a.weights(), r.weights()
+    assert rel_linf(wr, wa) <= 1e-12
