@@ -44,6 +44,9 @@ WORKLOADS = {
     # NEXT-1: the paper's FDM baseline (eq:FST) on the C5 batch, DST-I on FP64 tensor cores
     "C5l1": dict(cid="C5", over={"l": 1}),      # report l = 1 next to l = 10
     "C5fdm": dict(cid="C5", over={}, diff_mode=2),
+    # NEXT-4: Crank-Nicolson substeps (R27) and eigenvector-aligned grids (R28) on the C5 batch
+    "C5cn": dict(cid="C5", over={}, step=1),
+    "C5eig": dict(cid="C5", over={}, grid=1),
     # NEXT-3: the paper's §VI scenario (coordinated turn, terrain altitude + GM noise, N_pa = 34)
     "C6": dict(cid="C6", over={}),
 }
@@ -146,6 +149,13 @@ def oracle_sample(cfg, zs, budget_s: float, max_filters: int):
     return done * cfg.points / t_tot, done, t_tot
 
 
+def psi_slots(cfg, wl):
+    """Issue slots of the spectral multiplier per half-spectrum point: Euler
+    3 l + 10 (per substep one factor, two FMA + one multiply); Crank-Nicolson (R27) 5 l + 12
+    (l + 1 factors, each also entering the numerator product as 2 - f)."""
+    return 5 * cfg.l + 12 if wl.get("step", 0) else 3 * cfg.l + 10
+
+
 def threads_used():
     try:
         from threadpoolctl import threadpool_info
@@ -211,6 +221,7 @@ def run_workload(args, workload, rank, world, local, secondary=False):
     elif sharded:
         fkw = dict(world=args.virtual_ranks, sharded=True)
     diff_mode = wl.get("diff_mode", 0)
+    fkw.update(step=wl.get("step", 0), grid=wl.get("grid", 0))
     f = pmf.Filter(cfg.nx, cfg.n, cfg.A, cfg.Q, batch=cfg.batch, dtype=dtype, path=args.path,
                    device=local, stream=stream.cuda_stream, diff_mode=diff_mode, **fkw)
     if cfg.lik_kind == 2:
@@ -286,7 +297,7 @@ def run_workload(args, workload, rank, world, local, secondary=False):
               "what": "predict only (prep + transform/Psi kernel + closed-form normalisation), same filters"}
         if f.path == pmf.PATH_RESIDENT:
             # the predict's algorithmic issue slots against the FP64 (FP32) issue peak
-            spp = 0.5 * 4 * 3.5 * math.log2(cfg.n[0]) + (3 * cfg.l + 10) * (cfg.n[1] // 2 + 1) / cfg.n[1]
+            spp = 0.5 * 4 * 3.5 * math.log2(cfg.n[0]) + psi_slots(cfg, wl) * (cfg.n[1] // 2 + 1) / cfg.n[1]
             tu["alu_frac"] = (spp * cfg.batch * cfg.points / (km_ms / max(km_n, 1) * 1e-3)) / \
                 (148 * (64 if dtype == "f64" else 128) * peaks()[2] * 1e6)
 
@@ -300,6 +311,7 @@ def run_workload(args, workload, rank, world, local, secondary=False):
             obj = [pmf.nccl_unique_id() if rank == 0 else None]
             dist.broadcast_object_list(obj, src=0)
             fkw = dict(world=world, rank=rank, unique_id=obj[0])
+        fkw.update(step=wl.get("step", 0), grid=wl.get("grid", 0))
         fe = pmf.Filter(cfg.nx, cfg.n, cfg.A, cfg.Q, batch=cfg.batch, dtype=dtype, path=args.path,
                         device=local, stream=stream.cuda_stream, diff_mode=diff_mode, **fkw)
         if cfg.lik_kind == 2:
@@ -400,7 +412,7 @@ def run_workload(args, workload, rank, world, local, secondary=False):
         # HBM traffic, while B200 issues 148 x 64 FP64 lanes per clock. Peak = that issue
         # rate at the max SM clock; the HBM fraction is kept alongside.
         # fp32: the same slots on the FP32 pipe (128 lanes per SM per clock)
-        slots_pp = 0.5 * 4 * 3.5 * math.log2(cfg.n[0]) + (3 * cfg.l + 10) * (cfg.n[1] // 2 + 1) / cfg.n[1]
+        slots_pp = 0.5 * 4 * 3.5 * math.log2(cfg.n[0]) + psi_slots(cfg, wl) * (cfg.n[1] // 2 + 1) / cfg.n[1]
         slots = slots_pp * points_step
         lanes, pname = (64, "FP64") if dtype == "f64" else (128, "FP32")
         peak_alu = 148 * lanes * sm_max * 1e6 / 1e12
@@ -428,6 +440,8 @@ def run_workload(args, workload, rank, world, local, secondary=False):
             "config": {"workload": f"{workload}: {cfg.batch} x {'x'.join(map(str, cfg.n))} {cfg.nx}-D filters "
                                    f"per GPU, l={cfg.l}, tau={cfg.tau}, k_sigma={cfg.k_sigma}",
                        "step": "regrid + predict (Alg. 1-6) + update + moments, every filter",
+                       "substeps": "crank-nicolson (R27)" if wl.get("step", 0) else "semi-implicit euler (P:313-318)",
+                       "grid": "eigenvector-aligned (R28)" if wl.get("grid", 0) else "axis-aligned (R12)",
                        "l2": (f"inputs larger than L2 ({esize * points_step / 1e6:.0f} MB of weights per GPU)"
                               if esize * points_step > 126e6 else
                               f"weights ({esize * points_step / 1e6:.0f} MB) fit in the 126 MB L2: L2-resident workload"),
@@ -475,7 +489,7 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     line = run_workload(args, args.workload, rank, world, local)
-    also_list = ("C5l1,C5f32,C4,C3,C5fdm,C6" if args.workload == "C5" else "") if args.also == "auto" else args.also
+    also_list = ("C5l1,C5f32,C5cn,C4,C3,C5fdm,C6" if args.workload == "C5" else "") if args.also == "auto" else args.also
     if also_list and world == 1:
         # the other large single-GPU configurations, measured the same way (compact)
         also = {}
