@@ -16,7 +16,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libpmf.so")
-SOURCES = ["pmf_host.cpp", "pmf_sharded.cpp", "kernels_pencil.cu", "kernels_resident.cu", "kernels_plane.cu", "kernels_fdm.cu"]
+SOURCES = ["pmf_host.cpp", "pmf_sharded.cpp", "kernels_pencil.cu", "kernels_resident.cu", "kernels_plane.cu", "kernels_fdm.cu",
+           "kernels_cluster.cu"]
 HEADERS = ["pmf_internal.h", "pmf_ctx_impl.h", "device_common.cuh", "fft_smem.cuh", "fft_reg.cuh", "tma.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -366,6 +366,17 @@ static int flush_direct(pmf_ctx* c, const LikParams* lp) {
         c->pend = Pending{};
         return PMF_OK;
     }
+    // nx = 2 at 256^2 (fp64, Euler): the whole epoch in ONE launch of an 8-CTA cluster that
+    // keeps the half spectrum in distributed shared memory (kernels_cluster.cu)
+    if (c->path == PMF_PATH_PENCIL && c->pend.predict && cluster_epoch_supported(c->d, c->dtype, c->mp) &&
+        std::getenv("PMF_NO_CLUSTER") == nullptr) {
+        attach_events(c, b);
+        e = launch_cluster_epoch(c->d, b, twid(c), c->mp, lp, c->pend.regrid ? c->pend.k_sigma : -1.0, c->stream,
+                                 &c->launches);
+        if (e != cudaSuccess) return cuda_fail(c, e, "cluster epoch kernel");
+        c->pend = Pending{};
+        return PMF_OK;
+    }
     // the resident kernel keeps 3 coefficients per substep (l + 1 sets for Crank-Nicolson) in
     // two shared-memory buffers next to its 141 KB spectrum: up to 1024 substeps per call
     const bool resident = c->path == PMF_PATH_RESIDENT && c->pend.predict && c->pend.steps <= 1024;

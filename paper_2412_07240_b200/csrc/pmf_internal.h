@@ -167,6 +167,9 @@ cudaError_t launch_update(const Dims& d, int dtype, PencilBufs& b, const LikPara
                           cudaStream_t s, int64_t* launches);
 cudaError_t launch_regrid(const Dims& d, int dtype, PencilBufs& b, double k_sigma,
                           cudaStream_t s, int64_t* launches);   // swaps b.W / b.W2
+bool cluster_epoch_supported(const Dims& d, int dtype, const ModelParams& mp);
+cudaError_t launch_cluster_epoch(const Dims& d, PencilBufs& b, const Twiddles& tw, const ModelParams& mp,
+                                 const LikParams* lp, double ks, cudaStream_t s, int64_t* launches);
 bool line_epoch_supported(const Dims& d, int nsets);
 cudaError_t launch_line_epoch(const Dims& d, int dtype, PencilBufs& b, const Twiddles& tw, const ModelParams& mp,
                               const LikParams* lp, double ks, cudaStream_t s, int64_t* launches);
