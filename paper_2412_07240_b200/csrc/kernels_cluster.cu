@@ -90,8 +90,10 @@ __global__ void __launch_bounds__(NT, 1) k_cluster_epoch(Args a) {
     V* Bf = A + RMAX * PS;
     double* cfs = reinterpret_cast<double*>(Bf + RMAX * PS);  // [LMAX][3] h D00, h D11, h (D01 + D10)
     double* sh = cfs + 3 * LMAX;                              // scalars (below)
-    double* red = sh + 24;                                    // [8 warps][8] -> CTA sums [8]
-    // sh: 0..3 M, 4..5 o, 6..7 c_l, 8..11 B_l, 12 vol_l, 13 skip, 14..15 c0, 16..19 B0
+    double* red = sh + 40;                                    // [8 warps][8] -> CTA sums [8]
+    // sh: 0..3 M, 4..5 o, 6..7 c_l, 8..11 B_l, 12 vol_l, 13 skip, 14..15 c0, 16..19 B0,
+    //     24..29 linear-Gaussian exponent e(u) = q0 + q1 u0 + q2 u1 + q3 u0^2 + q4 u0 u1 + q5 u1^2
+    //     in the moved grid's index coordinates (R13), 30 log normalising constant
     FilterState& f = a.st[filt];
     double* Wf = a.W + (long long)filt * N * N;
     const double* zf = a.z + (long long)filt * a.lp.nz;
@@ -114,20 +116,57 @@ __global__ void __launch_bounds__(NT, 1) k_cluster_epoch(Args a) {
             sh[5] = fma(Bi[2], d0, fma(Bi[3], d1, 0.5 * (N - 1)));
         }
         const double* Mt = a.mp.Mtau;
+        const double Bl[4] = {fma(Mt[0], Bn[0], Mt[1] * Bn[4]), fma(Mt[0], Bn[1], Mt[1] * Bn[5]),
+                              fma(Mt[4], Bn[0], Mt[5] * Bn[4]), fma(Mt[4], Bn[1], Mt[5] * Bn[5])};
+        const double cl[2] = {fma(Mt[0], cn[0], Mt[1] * cn[1]), fma(Mt[4], cn[0], Mt[5] * cn[1])};
         sh[14] = cn[0];
         sh[15] = cn[1];
         sh[16] = Bn[0];
         sh[17] = Bn[1];
         sh[18] = Bn[4];
         sh[19] = Bn[5];
-        sh[8] = fma(Mt[0], Bn[0], Mt[1] * Bn[4]);
-        sh[9] = fma(Mt[0], Bn[1], Mt[1] * Bn[5]);
-        sh[10] = fma(Mt[4], Bn[0], Mt[5] * Bn[4]);
-        sh[11] = fma(Mt[4], Bn[1], Mt[5] * Bn[5]);
-        sh[6] = fma(Mt[0], cn[0], Mt[1] * cn[1]);
-        sh[7] = fma(Mt[4], cn[0], Mt[5] * cn[1]);
-        sh[12] = fabs(sh[8] * sh[11] - sh[9] * sh[10]);
+        sh[6] = cl[0];
+        sh[7] = cl[1];
+        sh[8] = Bl[0];
+        sh[9] = Bl[1];
+        sh[10] = Bl[2];
+        sh[11] = Bl[3];
+        sh[12] = fabs(Bl[0] * Bl[3] - Bl[1] * Bl[2]);
         sh[13] = ok ? 0.0 : 1.0;
+        if (UPDATE && a.lp.kind == 0) {
+            // r(u) = (z - H c_l) - (H B_l) u, e = r^T R^-1 r expanded in u (as the resident prep)
+            double r0[4] = {0, 0, 0, 0}, G0[4] = {0, 0, 0, 0}, G1[4] = {0, 0, 0, 0};
+            const int nz = a.lp.nz;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                if (i >= nz) break;
+                const double h0 = a.lp.H[i * 4], h1 = a.lp.H[i * 4 + 1];
+                r0[i] = zf[i] - fma(h0, cl[0], h1 * cl[1]);
+                G0[i] = fma(h0, Bl[0], h1 * Bl[2]);
+                G1[i] = fma(h0, Bl[1], h1 * Bl[3]);
+            }
+            double qa = 0, qb0 = 0, qb1 = 0, g00 = 0, g01 = 0, g11 = 0;
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    if (i >= nz || j >= nz) continue;
+                    const double R = a.lp.Rinv[i * 4 + j];
+                    qa = fma(r0[i] * R, r0[j], qa);
+                    qb0 = fma(-2.0 * G0[i] * R, r0[j], qb0);
+                    qb1 = fma(-2.0 * G1[i] * R, r0[j], qb1);
+                    g00 = fma(G0[i] * R, G0[j], g00);
+                    g01 = fma(G0[i] * R, G1[j], g01);
+                    g11 = fma(G1[i] * R, G1[j], g11);
+                }
+            sh[24] = qa;
+            sh[25] = qb0;
+            sh[26] = qb1;
+            sh[27] = g00;
+            sh[28] = 2.0 * g01;
+            sh[29] = g11;
+            sh[30] = a.lp.lognorm;
+        }
     }
     __syncthreads();
     if (sh[13] != 0.0) {                  // failed filter / degenerate target (uniform per cluster)
@@ -229,7 +268,8 @@ __global__ void __launch_bounds__(NT, 1) k_cluster_epoch(Args a) {
     {
         V* r = fft_any<N, true>(A, Bf, PAIRS, PS, FFTPlan{}, a.tw);
         const double cl0 = sh[6], cl1 = sh[7], B00 = sh[8], B01 = sh[9], B10 = sh[10], B11 = sh[11];
-#pragma unroll 2
+        const bool quad = a.lp.kind == 0;
+        const double q0 = sh[24], q1 = sh[25], q2 = sh[26], q3 = sh[27], q4 = sh[28], q5 = sh[29], lgn = sh[30];
         for (int e = tid; e < PAIRS * N; e += NT) {
             const int m = e / N, j1 = e - m * N;
             const int j0 = c * COLS + 2 * m;
@@ -240,8 +280,13 @@ __global__ void __launch_bounds__(NT, 1) k_cluster_epoch(Args a) {
                 const double u0 = (j0 + h) - 0.5 * (N - 1);
                 double w = h ? v.y : v.x;
                 if (UPDATE) {
-                    const double x[2] = {fma(B00, u0, fma(B01, u1, cl0)), fma(B10, u0, fma(B11, u1, cl1))};
-                    w *= exp_fast(log_lik(a.lp, x, zf));
+                    if (quad) {
+                        const double ee = fma(u0, fma(q3, u0, fma(q4, u1, q1)), fma(u1, fma(q5, u1, q2), q0));
+                        w *= exp_fast(fma(-0.5, ee, lgn));
+                    } else {
+                        const double x[2] = {fma(B00, u0, fma(B01, u1, cl0)), fma(B10, u0, fma(B11, u1, cl1))};
+                        w *= exp_fast(log_lik(a.lp, x, zf));
+                    }
                     const double wu0 = w * u0;
                     acc[0] += w;
                     acc[1] += wu0;
