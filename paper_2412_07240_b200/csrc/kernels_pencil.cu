@@ -1350,7 +1350,10 @@ static cudaError_t line_epoch_t(const Dims& d, PencilBufs& b, const Twiddles& tw
         constexpr int NC = decltype(nc)::value;
         auto go = [&](auto kern) -> cudaError_t {
             PMF_TRY(smem_attr(kern, sm));
-            kern<<<d.batch, kThreads, sm, s>>>((T*)b.W, b.st, d, pl, (const V*)tw.tw[0], mp, b.sub, lpv, b.z, ks);
+            // one thread per point up to kThreads: short lines keep their reductions and
+            // barriers cheap
+            const int nt = std::min(kThreads, std::max(64, (d.n[0] + 31) / 32 * 32));
+            kern<<<d.batch, nt, sm, s>>>((T*)b.W, b.st, d, pl, (const V*)tw.tw[0], mp, b.sub, lpv, b.z, ks);
             return cudaGetLastError();
         };
         if (lp && ks > 0.0) return go(k_line_epoch<T, true, true, NC>);
