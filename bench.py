@@ -256,6 +256,7 @@ def run_workload(args, workload, rank, world, local, secondary=False):
     ev1.synchronize()
     clk = clocks.stop()
     launches = f.launches - launches0
+    epoch_kernel = f.epoch_kernel                    # kernel family of the timed epochs
     kern_total_ms, kern_n = f.profile_read()
     f.profile(False)
     t_ms = ev0.elapsed_time(ev1)
@@ -391,6 +392,12 @@ def run_workload(args, workload, rank, world, local, secondary=False):
         nspec = cfg.batch * cfg.points // cfg.n[1] * (cfg.n[1] // 2 + 1)
         kname = f"k_plane_mid<{tname}, {cfg.n[-1]}, 2, {cfg.nx}, {1 if cfg.n[-1] == 96 else 3}>"
         alg_bytes, per = 2 * 2 * esize * nspec, f"{4 * esize} B per half-spectrum point"
+    elif epoch_kernel == "cluster":
+        kname = "k_cluster_epoch<true, true, 16>"
+        alg_bytes, per = 2 * esize * points_step, f"{2 * esize} B per grid point (whole epoch)"
+    elif epoch_kernel == "line":
+        kname = f"k_line_epoch<{tname}, true, true, {cfg.n[0]}>"
+        alg_bytes, per = 2 * esize * points_step, f"{2 * esize} B per grid point (whole epoch)"
     else:
         kname = "pencil predict (prep .. finalize)"
         alg_bytes, per = 2 * esize * points_step, f"{2 * esize} B per grid point (whole predict)"
@@ -445,8 +452,7 @@ def run_workload(args, workload, rank, world, local, secondary=False):
                        "l2": (f"inputs larger than L2 ({esize * points_step / 1e6:.0f} MB of weights per GPU)"
                               if esize * points_step > 126e6 else
                               f"weights ({esize * points_step / 1e6:.0f} MB) fit in the 126 MB L2: L2-resident workload"),
-                       "path": ("fdm: DST-I GEMMs on FP64 tensor cores" if diff_mode == 2 else
-                                {pmf.PATH_RESIDENT: "resident", pmf.PATH_PLANE: "plane"}.get(f.path, "pencil")),
+                       "path": ("fdm: DST-I GEMMs on FP64 tensor cores" if diff_mode == 2 else epoch_kernel),
                        "parallelism": (f"slab-sharded x{world if world > 1 else args.virtual_ranks} along the last "
                                        "axis (2 all-to-all per predict, all-reduce per update)" if sharded
                                        else f"filter-sharded x{world} (no data-path collective)")},
@@ -489,7 +495,7 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     line = run_workload(args, args.workload, rank, world, local)
-    also_list = ("C5l1,C5f32,C5cn,C4,C3,C5fdm,C6" if args.workload == "C5" else "") if args.also == "auto" else args.also
+    also_list = ("C5l1,C5f32,C5cn,C4,C3,C2,C1,C5fdm,C6" if args.workload == "C5" else "") if args.also == "auto" else args.also
     if also_list and world == 1:
         # the other large single-GPU configurations, measured the same way (compact)
         also = {}

@@ -286,6 +286,26 @@ int64_t pmf_device_bytes(const pmf_ctx* ctx);
 /* Kernel path the context uses (PMF_PATH_PENCIL, PMF_PATH_RESIDENT or PMF_PATH_PLANE). */
 int pmf_path(const pmf_ctx* ctx);
 
+/* Kernel family that ran the predict of the most recent flush (a CUDA-graph replay repeats
+   the captured one): PMF_EPOCH_NONE before any predict, else one of
+     PMF_EPOCH_PENCIL   multi-kernel pencil predict (prep, per-axis transforms, finalize)
+     PMF_EPOCH_LINE     nx = 1: regrid + predict + update + moments in one launch
+     PMF_EPOCH_CLUSTER  nx = 2 at 256^2: the whole epoch in one 16- (or 8-) CTA cluster launch
+     PMF_EPOCH_RESIDENT nx = 2 at 128^2: one CTA per filter, the whole epoch in one launch
+     PMF_EPOCH_PLANE    nx = 3, 4: plane kernels + strided passes
+     PMF_EPOCH_FDM      the FDM / DST-I baseline predictor (diff_mode = PMF_DIFF_FDM)
+     PMF_EPOCH_SHARDED  slab-sharded context (pmf_create_sharded)
+   Returns -1 for a null context. Diagnostic only: results do not depend on it. */
+#define PMF_EPOCH_NONE     0
+#define PMF_EPOCH_PENCIL   1
+#define PMF_EPOCH_LINE     2
+#define PMF_EPOCH_CLUSTER  3
+#define PMF_EPOCH_RESIDENT 4
+#define PMF_EPOCH_PLANE    5
+#define PMF_EPOCH_FDM      6
+#define PMF_EPOCH_SHARDED  7
+int pmf_epoch_kernel(const pmf_ctx* ctx);
+
 /* Library version string. */
 const char* pmf_version(void);
 

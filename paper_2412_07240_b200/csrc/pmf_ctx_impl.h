@@ -45,6 +45,7 @@ struct pmf_ctx {
     pmf::Dims d{};
     int dtype = 0;
     int path = PMF_PATH_PENCIL;
+    int epoch_kernel = PMF_EPOCH_NONE;   // kernel family of the last flush that ran a predict
     size_t esize = 8;
     double A[16]{}, Q[16]{};
     cudaStream_t stream = nullptr;

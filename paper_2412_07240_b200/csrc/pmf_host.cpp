@@ -313,7 +313,10 @@ static int upload_z(pmf_ctx* c, const double* z, int on_device, int nz) {
 
 // Execute pending regrid/predict, optionally fused with an update (launches directly).
 static int flush_direct(pmf_ctx* c, const LikParams* lp) {
-    if (c->sh) return sh_flush(c, lp);
+    if (c->sh) {
+        if (c->pend.predict) c->epoch_kernel = PMF_EPOCH_SHARDED;
+        return sh_flush(c, lp);
+    }
     if (lp && lp->kind == PMF_LIK_TERRAIN_GM) {
         // the table likelihood is not fused into the transform kernels: predict (+ regrid)
         // first, then the standalone point update
@@ -343,6 +346,7 @@ static int flush_direct(pmf_ctx* c, const LikParams* lp) {
             for (int a = 0; a < c->d.nx; ++a) trA += c->A[a * 4 + a];
             const int sgn = (c->cfg.trace_sign == PMF_TRACE_PRINTED) ? 1 : -1;
             attach_events(c, b);
+            c->epoch_kernel = PMF_EPOCH_FDM;
             e = launch_fdm_predict(c->d, c->dtype, b, c->mp, 1.0 + sgn * c->mp.dt * trA, c->stream, &c->launches);
             if (e != cudaSuccess) return cuda_fail(c, e, "FDM predict");
             b.ev0 = b.ev1 = nullptr;
@@ -360,6 +364,7 @@ static int flush_direct(pmf_ctx* c, const LikParams* lp) {
     if (c->d.nx == 1 && c->pend.predict && line_epoch_supported(c->d, c->pend.steps + (c->mp.step ? 1 : 0)) &&
         std::getenv("PMF_NO_LINE_EPOCH") == nullptr) {
         attach_events(c, b);
+        c->epoch_kernel = PMF_EPOCH_LINE;
         e = launch_line_epoch(c->d, c->dtype, b, twid(c), c->mp, lp, c->pend.regrid ? c->pend.k_sigma : -1.0,
                               c->stream, &c->launches);
         if (e != cudaSuccess) return cuda_fail(c, e, "line epoch kernel");
@@ -371,6 +376,7 @@ static int flush_direct(pmf_ctx* c, const LikParams* lp) {
     if (c->path == PMF_PATH_PENCIL && c->pend.predict && cluster_epoch_supported(c->d, c->dtype, c->mp) &&
         std::getenv("PMF_NO_CLUSTER") == nullptr) {
         attach_events(c, b);
+        c->epoch_kernel = PMF_EPOCH_CLUSTER;
         e = launch_cluster_epoch(c->d, b, twid(c), c->mp, lp, c->pend.regrid ? c->pend.k_sigma : -1.0, c->stream,
                                  &c->launches);
         if (e != cudaSuccess) return cuda_fail(c, e, "cluster epoch kernel");
@@ -382,6 +388,7 @@ static int flush_direct(pmf_ctx* c, const LikParams* lp) {
     const bool resident = c->path == PMF_PATH_RESIDENT && c->pend.predict && c->pend.steps <= 1024;
     if (resident) {
         attach_events(c, b);
+        c->epoch_kernel = PMF_EPOCH_RESIDENT;
         e = launch_resident(c->d, c->dtype, b, twid(c), &c->mp, lp, c->pend.regrid ? c->pend.k_sigma : -1.0,
                             c->stream, &c->launches);
         if (e != cudaSuccess) return cuda_fail(c, e, "resident epoch kernel");
@@ -391,6 +398,7 @@ static int flush_direct(pmf_ctx* c, const LikParams* lp) {
     // plane path: regrid (if pending) fused into the forward pass, predict, update
     if (c->path == PMF_PATH_PLANE && c->pend.predict && plane_supported(c->d, c->pend.steps)) {
         attach_events(c, b);
+        c->epoch_kernel = PMF_EPOCH_PLANE;
         e = launch_plane(c->d, c->dtype, b, c->mp, lp, c->pend.regrid ? c->pend.k_sigma : -1.0, c->stream,
                          &c->launches);
         if (e != cudaSuccess) return cuda_fail(c, e, "plane path");
@@ -409,6 +417,7 @@ static int flush_direct(pmf_ctx* c, const LikParams* lp) {
     b = bufs(c);
     if (c->pend.predict) {
         attach_events(c, b);
+        c->epoch_kernel = PMF_EPOCH_PENCIL;
         e = launch_predict_pencil(c->d, c->dtype, b, twid(c), c->mp, lp, c->stream, &c->launches);
         if (e != cudaSuccess) return cuda_fail(c, e, "predict");
     } else if (lp) {
@@ -1031,5 +1040,6 @@ int pmf_profile_read(pmf_ctx* c, double* total_ms, int64_t* count) {
 }
 int64_t pmf_device_bytes(const pmf_ctx* c) { return c ? c->bytes : 0; }
 int pmf_path(const pmf_ctx* c) { return c ? c->path : -1; }
+int pmf_epoch_kernel(const pmf_ctx* c) { return c ? c->epoch_kernel : -1; }
 
 }  // extern "C"

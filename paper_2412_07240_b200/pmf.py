@@ -26,6 +26,9 @@ STEP_EULER, STEP_CN = 0, 1
 GRID_AXIS, GRID_EIGEN = 0, 1   # grid design from a covariance: axis-aligned (R12) / eigenvector-aligned (R28)
 TRACE_PHYSICAL, TRACE_PRINTED = -1, 1
 PATH_AUTO, PATH_PENCIL, PATH_RESIDENT, PATH_PLANE = 0, 1, 2, 3
+# kernel family of the last predict (pmf_epoch_kernel)
+EPOCH_KERNELS = {0: "none", 1: "pencil", 2: "line", 3: "cluster", 4: "resident", 5: "plane", 6: "fdm",
+                 7: "sharded"}
 LIK_LINEAR_GAUSS, LIK_RANGE_GAUSS, LIK_TERRAIN_GM = 0, 1, 2
 
 # every symbol include/pmf.h declares (checked by tests/test_abi.py)
@@ -33,7 +36,8 @@ SYMBOLS = ["pmf_create", "pmf_destroy", "pmf_last_error", "pmf_set_gaussian", "p
            "pmf_predict", "pmf_update", "pmf_moments", "pmf_regrid", "pmf_step", "pmf_get_weights",
            "pmf_get_grid", "pmf_sync", "pmf_launch_count", "pmf_moments_bytes", "pmf_nccl_unique_id",
            "pmf_create_sharded", "pmf_world", "pmf_profile", "pmf_profile_read", "pmf_use_graphs",
-           "pmf_set_terrain", "pmf_device_bytes", "pmf_path", "pmf_version", "pmf_moments_async"]
+           "pmf_set_terrain", "pmf_device_bytes", "pmf_path", "pmf_version", "pmf_moments_async",
+           "pmf_epoch_kernel"]
 
 
 class PMFError(RuntimeError):
@@ -93,6 +97,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         "pmf_profile_read": (I, [P, C.POINTER(C.c_double), C.POINTER(C.c_int64)]),
         "pmf_device_bytes": (C.c_int64, [P]),
         "pmf_path": (I, [P]),
+        "pmf_epoch_kernel": (I, [P]),
         "pmf_version": (C.c_char_p, []),
     }
     for name, (res, args) in sig.items():
@@ -319,3 +324,8 @@ class Filter:
     @property
     def path(self) -> int:
         return int(self.lib.pmf_path(self.h))
+
+    @property
+    def epoch_kernel(self) -> str:
+        """Kernel family that ran the last predict ("resident", "cluster", "line", ...)."""
+        return EPOCH_KERNELS[int(self.lib.pmf_epoch_kernel(self.h))]
