@@ -231,9 +231,25 @@ __global__ void __launch_bounds__(kThreads, 2) k_axis0_r2c(const T* __restrict__
     const T sc = (T)coef[(long long)filt * cstride];
     const T* src = W + row0 * N;
     const float invN = 1.0f / N;
-    for (int i = threadIdx.x; i < P * N; i += blockDim.x) {
-        const int p = (int)((i + 0.5f) * invN), j = i - p * N;
-        a[p * PS + sx<NC>(j)] = V{src[i] * sc, T(0)};
+    {
+        constexpr int UNR = 8;                       // loads in flight per thread (see k_axis_c2c)
+        const int PN = P * N;
+        for (int i0 = threadIdx.x; i0 < PN; i0 += UNR * blockDim.x) {
+            T v[UNR];
+#pragma unroll
+            for (int u = 0; u < UNR; ++u) {
+                const int i = i0 + u * blockDim.x;
+                v[u] = i < PN ? src[i] : T(0);
+            }
+#pragma unroll
+            for (int u = 0; u < UNR; ++u) {
+                const int i = i0 + u * blockDim.x;
+                if (i < PN) {
+                    const int p = (int)((i + 0.5f) * invN), j = i - p * N;
+                    a[p * PS + sx<NC>(j)] = V{v[u] * sc, T(0)};
+                }
+            }
+        }
     }
     __syncthreads();
     V* r = fft_any<NC, false>(a, b, P, PS, pl, tw);
@@ -267,10 +283,26 @@ __global__ void __launch_bounds__(kThreads, 2) k_axis_c2c(typename C2<T>::type* 
     const long long o = blockIdx.x / ntile;
     const long long i0 = (blockIdx.x - o * ntile) * P;
     V* base = S + o * (long long)N * I;
-    for (int t = threadIdx.x; t < P * N; t += blockDim.x) {
-        const int j = t / P, p = t - j * P;     // P is a power of two
-        long long i = i0 + p;
-        a[p * PS + sx<NC>(j)] = (i < I) ? base[(long long)j * I + i] : V{T(0), T(0)};
+    {
+        // UNR independent loads in flight per thread before the shared stores (the
+        // one-load-per-iteration loop serialised on the L2 / HBM latency)
+        constexpr int UNR = 8;
+        const int PN = P * N, lp2 = __ffs(P) - 1;    // P is a power of two
+        for (int t0 = threadIdx.x; t0 < PN; t0 += UNR * blockDim.x) {
+            V v[UNR];
+#pragma unroll
+            for (int u = 0; u < UNR; ++u) {
+                const int t = t0 + u * blockDim.x;
+                const int j = t >> lp2, p = t & (P - 1);
+                const long long i = i0 + p;
+                v[u] = (t < PN && i < I) ? base[(long long)j * I + i] : V{T(0), T(0)};
+            }
+#pragma unroll
+            for (int u = 0; u < UNR; ++u) {
+                const int t = t0 + u * blockDim.x;
+                if (t < PN) a[(t & (P - 1)) * PS + sx<NC>(t >> lp2)] = v[u];
+            }
+        }
     }
     __syncthreads();
     V* r;
@@ -405,12 +437,26 @@ __global__ void __launch_bounds__(kThreads, 2) k_axis0_c2r(const typename C2<T>:
         const long long rloc = (long long)tile * P;                  // first row of the tile in the filter
         const long long row0 = (long long)filt * rpf + rloc;
         const V* src = S + row0 * d.H0;
-        for (int i = threadIdx.x; i < P * N; i += blockDim.x) {
-            const int p = (int)((i + 0.5f) * invN), k = i - p * N;
-            V v;
-            if (k < d.H0) v = src[p * d.H0 + k];
-            else { v = src[p * d.H0 + (N - k)]; v.y = -v.y; }
-            a[p * PS + sx<NC>(k)] = v;
+        {
+            constexpr int UNR = 8;                   // loads in flight per thread (see k_axis_c2c)
+            const int PN = P * N;
+            for (int i0 = threadIdx.x; i0 < PN; i0 += UNR * blockDim.x) {
+                V v[UNR];
+#pragma unroll
+                for (int u = 0; u < UNR; ++u) {
+                    const int i = i0 + u * blockDim.x;
+                    const int p = (int)((i + 0.5f) * invN), k = i - p * N;
+                    v[u] = i < PN ? src[p * d.H0 + (k < d.H0 ? k : N - k)] : V{T(0), T(0)};
+                }
+#pragma unroll
+                for (int u = 0; u < UNR; ++u) {
+                    const int i = i0 + u * blockDim.x;
+                    if (i < PN) {
+                        const int p = (int)((i + 0.5f) * invN), k = i - p * N;
+                        a[p * PS + sx<NC>(k)] = k < d.H0 ? v[u] : V{v[u].x, -v[u].y};
+                    }
+                }
+            }
         }
         if (UPDATE) {
             for (int p = threadIdx.x; p < P; p += blockDim.x) {
