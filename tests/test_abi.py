@@ -70,3 +70,21 @@ def test_no_cpu_fallback():
     assert rc == -9 and "no CPU fallback" in msg
     with pytest.raises(pmf.PMFError):
         pmf.Filter(1, (64,), [[-0.5]], [[1.0]])
+
+
+def _header_defines(prefix):
+    txt = open(os.path.join(ROOT, "include", "pmf.h")).read()
+    return {m[0]: int(m[1]) for m in re.findall(rf"#define\s+({prefix}[A-Z_0-9]+)\s+(-?\d+)", txt)}
+
+
+def test_binding_constants_match_header():
+    """The binding's constants are the header's (the ctypes layer has no other source)."""
+    ep = _header_defines("PMF_EPOCH_")
+    assert {v: k[len("PMF_EPOCH_"):].lower() for k, v in ep.items()} == pmf.EPOCH_KERNELS
+    paths = _header_defines("PMF_PATH_")
+    assert (paths["PMF_PATH_AUTO"], paths["PMF_PATH_PENCIL"], paths["PMF_PATH_RESIDENT"],
+            paths["PMF_PATH_PLANE"]) == (pmf.PATH_AUTO, pmf.PATH_PENCIL, pmf.PATH_RESIDENT, pmf.PATH_PLANE)
+    grids = _header_defines("PMF_GRID_")
+    assert (grids["PMF_GRID_AXIS"], grids["PMF_GRID_EIGEN"]) == (pmf.GRID_AXIS, pmf.GRID_EIGEN)
+    lib = pmf.load_library()
+    assert lib.pmf_epoch_kernel(None) == -1 and lib.pmf_path(None) == -1
