@@ -164,6 +164,12 @@ def threads_used():
         return os.cpu_count() or 1
 
 
+def workload_name(workload, cfg):
+    """config.workload, identical on both arms."""
+    return (f"{workload}: {cfg.batch} x {'x'.join(map(str, cfg.n))} {cfg.nx}-D filters per GPU, "
+            f"l={cfg.l}, tau={cfg.tau}, k_sigma={cfg.k_sigma}")
+
+
 def run_reference(args):
     """--impl reference: the CPU oracle timed as the reference arm (rank 0 only)."""
     rank, world, _ = dist_env()
@@ -180,11 +186,13 @@ def run_reference(args):
     timed = per_step[args.warmup:]
     val = statistics.median(v for v, _, _ in timed)
     nf = timed[0][1]
-    line = {"impl": "reference", "metric": "grid-point FPE updates/sec (fp64)", "value": val,
+    # the arm's metric name (the oracle itself always computes in fp64)
+    metric = "grid-point FPE updates/sec (fp64)" if cfg.dtype == "f64" else "grid-point FPE updates/sec (fp32)"
+    line = {"impl": "reference", "metric": metric, "value": val,
             "unit": "grid-point updates/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * cfg.batch * cfg.points / val, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"{args.workload}: {cfg.batch} x {cfg.n} {cfg.nx}-D filters, l={cfg.l}",
+            "config": {"workload": workload_name(args.workload, cfg),
                        "sample": f"{nf} filter-epochs per step (oracle is O(N^2) naive DFT)"},
             "cpu_baseline": {"value": val, "unit": "grid-point updates/s", "cores": threads_used(), "kind": "oracle",
                              "sample": f"{nf} of {cfg.batch} filters x 1 epoch per step"},
@@ -444,8 +452,7 @@ def run_workload(args, workload, rank, world, local, secondary=False):
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "strong" if sharded else "weak",
             "vs_baseline": None, "dtype": dtype, "data": "synthetic",
-            "config": {"workload": f"{workload}: {cfg.batch} x {'x'.join(map(str, cfg.n))} {cfg.nx}-D filters "
-                                   f"per GPU, l={cfg.l}, tau={cfg.tau}, k_sigma={cfg.k_sigma}",
+            "config": {"workload": workload_name(workload, cfg),
                        "step": "regrid + predict (Alg. 1-6) + update + moments, every filter",
                        "substeps": "crank-nicolson (R27)" if wl.get("step", 0) else "semi-implicit euler (P:313-318)",
                        "grid": "eigenvector-aligned (R28)" if wl.get("grid", 0) else "axis-aligned (R12)",
