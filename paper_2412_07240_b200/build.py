@@ -11,14 +11,15 @@ from __future__ import annotations
 import os
 import subprocess
 import sys
+from concurrent.futures import ThreadPoolExecutor
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libpmf.so")
 SOURCES = ["pmf_host.cpp", "pmf_sharded.cpp", "kernels_pencil.cu", "kernels_resident.cu", "kernels_plane.cu", "kernels_fdm.cu",
-           "kernels_cluster.cu"]
-HEADERS = ["pmf_internal.h", "pmf_ctx_impl.h", "device_common.cuh", "fft_smem.cuh", "fft_reg.cuh", "tma.cuh"]
+           "kernels_cluster.cu", "kernels_quad.cu"]
+HEADERS = ["plane_common.cuh", "pmf_internal.h", "pmf_ctx_impl.h", "device_common.cuh", "fft_smem.cuh", "fft_reg.cuh", "tma.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "--expt-relaxed-constexpr",
@@ -36,7 +37,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     hdrs = [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(ROOT, "include", "pmf.h")]
     objdir = os.path.join(HERE, "build_obj")
     os.makedirs(objdir, exist_ok=True)
-    objs = []
+    objs, cmds = [], []
     for src in SOURCES:
         sp = os.path.join(CSRC, src)
         op = os.path.join(objdir, src + ".o")
@@ -48,7 +49,12 @@ def build(force: bool = False, verbose: bool = False) -> str:
                 cmd.insert(2, "cu")
             if verbose:
                 print(" ".join(cmd))
-            subprocess.run(cmd, check=True)
+            cmds.append(cmd)
+    # the translation units are independent: compile them in parallel
+    with ThreadPoolExecutor(max_workers=max(1, min(len(cmds), os.cpu_count() or 1))) as ex:
+        for r in list(ex.map(lambda c: subprocess.run(c), cmds)):
+            if r.returncode != 0:
+                raise subprocess.CalledProcessError(r.returncode, r.args)
     if force or _stale(LIB, objs):
         cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-Xcompiler", "-fPIC"]
         if verbose:

@@ -34,197 +34,11 @@
 #include "device_common.cuh"
 #include "fft_reg.cuh"
 #include "tma.cuh"
+#include "plane_common.cuh"
 
 namespace pmf {
 namespace pln {
 
-template <int N>
-struct Cfg {
-    static constexpr int R1 = N / 8;           // stage-1 radix
-    static constexpr int H = N / 2 + 1;        // rows of a plane's half spectrum (k1 = 0..N/2)
-    static constexpr int PITCH = N + 2;        // complex per shared-memory row (= 2 mod 8: conflict-free)
-    static constexpr int TEAMS = N / 2;        // column pairs (P1, P3) = rows (P2)
-    static constexpr int NT = 8 * TEAMS;
-    static constexpr int SP = N + 2;           // real staging pitch (separable regrid)
-    static constexpr int MINB = N >= 96 ? 1 : (N == 64 ? 2 : 4);
-};
-
-constexpr int LCAP = 64;                       // substeps held per pencil (mid pass, Psi)
-
-// per-filter coefficient block (doubles), stride >= PL_EU + 10 l (coef_stride)
-enum {
-    PL_M = 0,       // 16: regrid map v = o + M u' (old index coordinates of new point u'), row stride 4
-    PL_O = 16,      // 4
-    PL_FLAG = 20,   // 0: no regrid, 2: general map (gather pre-pass), 4: split map (nx = 4 CV structure)
-    PL_SKIP = 21,   // 1: filter failed (status) or degenerate regrid target: leave untouched
-    PL_SN = 22,     // s / N_tot (trace factor and the transform scales, folded into Psi)
-    PL_VOL = 23,    // |det B_l|
-    PL_CL = 24,     // 4: moved grid centre c_l
-    PL_BL = 28,     // 16: moved grid matrix B_l
-    PL_LQ = 44,     // 16: linear-Gauss exponent e(u) = q0 + q_a u_a + sum_{a<=b} q_ab u_a u_b (tri order)
-    PL_LGN = 60,    // log normalising constant of the likelihood
-    PL_ISG = 61,    // 1 / sigma (range likelihood)
-    PL_ZR = 62,     // range measurement
-    PL_S = 63,      // s
-    PL_EU = 64      // 10 per substep: Euler-factor coefficients (substep_coefs order)
-};
-
-__device__ __forceinline__ int xcol(int k1, int j0) { return j0 ^ ((k1 >> 2) & 1); }
-__device__ __forceinline__ int rslot(int s, int t) { return s * 8 + (t ^ (s & 7)); }
-template <int N>
-__device__ __forceinline__ int cslot(int s, int t, int m) {
-    const int row = 4 * s + ((t >> 1) ^ (s & 3));
-    const int col = (t & 1) ^ ((s >> 2) & 1);
-    return row * Cfg<N>::PITCH + 2 * m + col;
-}
-
-// stage-2 ownership (R1 >= 2)
-template <int R1> __device__ __forceinline__ bool s_on(int t) { return t < R1 / 2; }
-template <int R1> __device__ __forceinline__ int s_a(int t) { return t; }
-template <int R1> __device__ __forceinline__ int s_b(int t) { return t == 0 ? R1 / 2 : R1 - t; }
-
-template <int R1, bool INV, typename V>
-__device__ __forceinline__ void dftR(V* x) {
-    if constexpr (R1 == 16) reg::dft16<INV>(x);
-    else if constexpr (R1 == 12) reg::dft12<INV>(x);
-    else if constexpr (R1 == 8) reg::dft8<INV>(x);
-    else if constexpr (R1 == 4) reg::r4<INV>(x[0], x[1], x[2], x[3]);
-    else if constexpr (R1 == 2) {
-        const V a = x[0];
-        x[0] = cadd(a, x[1]);
-        x[1] = csub(a, x[1]);
-    }
-}
-
-// W_N^{ts} for s < R1, t < 8 at tw[s * 8 + t]
-template <int N, typename V>
-__device__ __forceinline__ void init_tw(V* tw) {
-    using T = decltype(tw[0].x);
-    for (int i = threadIdx.x; i < N; i += blockDim.x) {
-        const int s = i >> 3, t = i & 7;
-        double sn, cs;
-        sincospi(2.0 * (double)(t * s) / (double)N, &sn, &cs);
-        tw[i] = V{(T)cs, (T)(-sn)};
-    }
-}
-
-template <bool INV, typename V>
-__device__ __forceinline__ V twid(V a, V w) {
-    if (INV) w.y = -w.y;
-    return cmul(a, w);
-}
-
-// Team DFT, DIT order: in x[r] = element t + 8r (registers), out pa[q] = X[sa + R1 q],
-// pb[q] = X[sb + R1 q] on the threads with s_on(t). `ex` is the team's exchange area,
-// `slot(s, t)` its conflict-free layout.
-template <int R1, bool INV, typename V, typename SLOT>
-__device__ __forceinline__ void team_dft(V* x, V* pa, V* pb, V* ex, const V* tw, int t, SLOT slot) {
-    dftR<R1, INV>(x);
-#pragma unroll
-    for (int s = 1; s < R1; ++s) x[s] = twid<INV>(x[s], tw[s * 8 + t]);
-    __syncwarp();
-#pragma unroll
-    for (int s = 0; s < R1; ++s) ex[slot(s, t)] = x[s];
-    __syncwarp();
-    if (s_on<R1>(t)) {
-        const int sa = s_a<R1>(t), sb = s_b<R1>(t);
-#pragma unroll
-        for (int tt = 0; tt < 8; ++tt) {
-            pa[tt] = ex[slot(sa, tt)];
-            pb[tt] = ex[slot(sb, tt)];
-        }
-        reg::dft8<INV>(pa);
-        reg::dft8<INV>(pb);
-    }
-    __syncwarp();
-}
-
-// Team DFT, DIF order (the inverse of team_dft's layout): in pa[q] = X[sa + R1 q],
-// pb[q] = X[sb + R1 q] (threads with s_on), out x[r] = element t + 8r.
-template <int R1, bool INV, typename V, typename SLOT>
-__device__ __forceinline__ void team_dft_dif(V* pa, V* pb, V* x, V* ex, const V* tw, int t, SLOT slot) {
-    __syncwarp();
-    if (s_on<R1>(t)) {
-        const int sa = s_a<R1>(t), sb = s_b<R1>(t);
-        reg::dft8<INV>(pa);
-        reg::dft8<INV>(pb);
-#pragma unroll
-        for (int tt = 0; tt < 8; ++tt) {
-            ex[slot(sa, tt)] = pa[tt];
-            ex[slot(sb, tt)] = pb[tt];
-        }
-    }
-    __syncwarp();
-#pragma unroll
-    for (int s = 0; s < R1; ++s) x[s] = ex[slot(s, t)];
-#pragma unroll
-    for (int s = 1; s < R1; ++s) x[s] = twid<INV>(x[s], tw[s * 8 + t]);
-    dftR<R1, INV>(x);
-    __syncwarp();
-}
-
-template <typename T>
-struct PlaneArgs {
-    const T* Wsrc;          // weights read by the forward pass (old grid when regridding)
-    const T* W2src;         // pre-regridded weights (general regrid map, flag 2)
-    T* W;                   // weights written by the inverse pass
-    typename C2<T>::type* S;      // spectrum written by the forward pass
-    typename C2<T>::type* Sinv;   // spectrum read by the inverse pass (S, or S2 after an out-of-place pass)
-    const double* coef;
-    int cs;
-    double* dcpart;         // [plane] sums of the forward pass's input planes
-    double* dc3;            // [filter][n3] slab sums after the split regrid (flag 4)
-    double* part;           // [plane][6]
-    int nplanes;            // batch * ppf
-    int ppf;                // planes per filter
-    int n2, n3;             // sizes of axes 2, 3 (1 if absent)
-    int l;
-    int range;              // likelihood kind 1
-};
-
-// plane p of its filter -> (j2, j3)
-__device__ __forceinline__ void plane_j(int pl, int n2, int& j2, int& j3) {
-    j3 = pl / n2;
-    j2 = pl - j3 * n2;
-}
-
-// multilinear interpolation (R12) of the old weights Wf (grid sizes n) at old index
-// coordinates v, zero ghost nodes
-template <typename T, int NX>
-__device__ __forceinline__ double gather_point(const T* __restrict__ Wf, const int* n, const double* v) {
-    int i[4];
-    double fr[4];
-    bool lo[4], hi[4];
-    long long base = 0, stride[4];
-    stride[0] = 1;
-#pragma unroll
-    for (int a = 1; a < NX; ++a) stride[a] = stride[a - 1] * n[a - 1];
-#pragma unroll
-    for (int a = 0; a < NX; ++a) {
-        const double fl = floor(v[a]);
-        i[a] = __double2int_rz(fl);
-        fr[a] = v[a] - fl;
-        lo[a] = i[a] >= 0 && i[a] <= n[a] - 1;
-        hi[a] = i[a] >= -1 && i[a] <= n[a] - 2;
-        base += (long long)i[a] * stride[a];
-    }
-    double val = 0.0;
-#pragma unroll
-    for (int c = 0; c < (1 << NX); ++c) {
-        double wt = 1.0;
-        long long off = base;
-        bool ok = true;
-#pragma unroll
-        for (int a = 0; a < NX; ++a) {
-            const bool bit = (c >> a) & 1;
-            wt *= bit ? fr[a] : 1.0 - fr[a];
-            ok = ok && (bit ? hi[a] : lo[a]);
-            if (bit) off += stride[a];
-        }
-        if (ok) val = fma(wt, (double)__ldg(Wf + off), val);
-    }
-    return val;
-}
 
 // ============================================================================ prep (one warp per filter)
 template <int NX>
@@ -573,28 +387,6 @@ __global__ void __launch_bounds__(Cfg<N>::NT, Cfg<N>::MINB) k_plane_fwd(PlaneArg
     if (tid < H) tma::bulk_wait_all();
 }
 
-// ps[r] = mult / den[r] with ONE division for all R values (prefix products, kept in ps
-// itself), every den >= 1; when the product of the R values leaves the range, one
-// division per value
-template <int R>
-__device__ __forceinline__ void psi_div(const double* den, double mult, double* ps) {
-    ps[0] = den[0];
-#pragma unroll
-    for (int r = 1; r < R; ++r) ps[r] = ps[r - 1] * den[r];
-    if (ps[R - 1] < 1e300) {
-        double inv = mult / ps[R - 1];
-#pragma unroll
-        for (int r = R - 1; r > 0; --r) {
-            const double v = inv * ps[r - 1];
-            inv *= den[r];
-            ps[r] = v;
-        }
-        ps[0] = inv;
-    } else {
-#pragma unroll
-        for (int r = 0; r < R; ++r) ps[r] = mult / den[r];
-    }
-}
 
 // ============================================================================ strided pass (axes >= 2)
 // Pencils along one axis of the spectrum [o][j][i] (stride I). MODE 0 forward,
@@ -976,347 +768,6 @@ __global__ void __launch_bounds__(SplitCfg<T, NA>::NT, 1) k_plane_split(MidArgs<
         }
         __syncthreads();                  // ring slots below the next ja may be refilled
     }
-}
-
-// ============================================================================ fused (2,3)-plane pass (nx = 4)
-// One launch replaces the three strided passes of nx = 4 (forward axis 2 [+ split
-// regrid], axis 3 with Psi, inverse axis 2) when n2 = n3 = NQ and an (i2, i3)-plane
-// fits in shared memory: HBM traffic per interval drops from 5 to 3 passes over
-// the spectrum. Work item = one (filter, k1, k0): its NQ x NQ values S(j3, j2)
-// (stride I = H1 N0 in the spectrum [filter][j3][j2][k1][k0]) sit in shared memory
-// as rows j3 of pitch NQ + 1 (conflict-free for rows and columns). Team q (8
-// threads) owns rows and columns q and q + NQ/2:
-//   F2  forward DFT along axis 2 of the rows (Alg. 1). Split regrid map (flag 4,
-//       R12): the rows are first re-sampled from the staged old plane --
-//       Z(j2) = (1 - w3) S(ja) + w3 S(ja + 1) at v3 = o3 + M33 u3', then linear along
-//       j2 at v2 = o2 + M22 u2' + M23 u3', zero ghosts -- exact because the axis-0/1
-//       DFT commutes with interpolation along axes 2, 3.
-//   F3  per column k2: forward DFT along axis 3, x s Psi / N_tot (Alg. 3-4, Euler
-//       factors paired into quartics in kap_3, R27 lists for Crank-Nicolson),
-//       inverse DFT along axis 3 (Alg. 5).
-//   I2  inverse DFT along axis 2 of the rows, stored to Sout; each freed row is
-//       refilled at once with the next item's row by per-thread cp.async copies,
-//       so the next plane's loads overlap this plane's stores and transforms.
-template <int NQ, int TM = (NQ >= 64 ? 32 : NQ / 2)>
-struct QCfg {
-    static constexpr int R = NQ / 8;
-    static constexpr int TEAMS = TM;            // team q owns rows / columns q + TEAMS j
-    static constexpr int NT = 8 * TEAMS;
-    static constexpr int P = NQ + 1;            // row pitch (complex)
-};
-template <typename T, int NQ>
-static size_t quad_smem() {
-    return sizeof(typename C2<T>::type) * ((size_t)NQ * QCfg<NQ>::P + NQ);
-}
-
-template <typename T>
-struct QuadArgs {
-    const typename C2<T>::type* S;   // input spectrum [filter][j3][j2][i]
-    typename C2<T>::type* Sout;      // output (same layout)
-    const double* coef;
-    int cs;
-    int I;                           // H1 N0 (k1, k0) pencil-planes per filter
-    int N0, H1;
-    int l, step;
-    int items;                       // batch * I
-    double* dc3;                     // [filter][n3]: the regridded filter's weight sum (split maps)
-};
-
-// Euler factors of pair j of list `list` (0: denominators, 1: Crank-Nicolson numerators
-// 2 - f_n, R27) as a quartic in kap_L: q[0] = (c0, c1), q[1] = (c2, c3), q[2] = (c4, value at
-// the Nyquist wavenumber, where kx_L = 0, R7). f_n = gam_n + bet_n kx_L + alp_n kap_L^2 with
-// gam_n, bet_n from the other axes' wavenumbers kap[a], kx[a] (a < L).
-template <int NX, int L>
-__device__ __forceinline__ void psi_pair(const double* cf, int l, int cn, int list, int j, const double* kap,
-                                         const double* kx, double2* q) {
-    auto gam_bet = [&](int n, double& g, double& bb) {
-        const double* c = cf + 10 * n;
-        g = 1.0;
-        bb = 0.0;
-#pragma unroll
-        for (int a2 = 0; a2 < L; ++a2) {
-            g = fma(c[a2], kap[a2] * kap[a2], g);
-#pragma unroll
-            for (int b2 = a2 + 1; b2 < L; ++b2) g = fma(c[pair_index(NX, a2, b2)], kx[a2] * kx[b2], g);
-            bb = fma(c[pair_index(NX, a2, L)], kx[a2], bb);
-        }
-    };
-    const int base = (list == 0 && cn) ? 1 : 0;        // CN den: f_1 .. f_l
-    double g0, b0, g1 = 1.0, b1 = 0.0, a1 = 0.0;
-    gam_bet(base + 2 * j, g0, b0);
-    double a0 = cf[10 * (base + 2 * j) + L];
-    const bool two = 2 * j + 1 < l;
-    if (two) {
-        gam_bet(base + 2 * j + 1, g1, b1);
-        a1 = cf[10 * (base + 2 * j + 1) + L];
-    }
-    if (list == 1) {                                   // 2 - f = (2 - g) - b k - a k^2
-        g0 = 2.0 - g0;
-        b0 = -b0;
-        a0 = -a0;
-        if (two) {
-            g1 = 2.0 - g1;
-            b1 = -b1;
-            a1 = -a1;
-        }
-    }
-    constexpr double kn2 = PMF_PI * PMF_PI;
-    q[0] = double2{g0 * g1, fma(g0, b1, b0 * g1)};
-    q[1] = double2{fma(g0, a1, fma(b0, b1, a0 * g1)), fma(b0, a1, a0 * b1)};
-    q[2] = double2{a0 * a1, fma(a0, kn2, g0) * fma(a1, kn2, g1)};
-}
-
-// F2 of one row: forward DFT along axis 2 of x (element t + 8r), result in place in the row
-template <int NQ, typename V>
-__device__ __forceinline__ void quad_f2_row(V (&x)[NQ / 8], V* row, const V* tw, int t) {
-    constexpr int R = NQ / 8;
-    V pa[8], pb[8];
-    team_dft<R, false>(x, pa, pb, row, tw, t, [](int s2, int tt) { return rslot(s2, tt); });
-    if (s_on<R>(t)) {
-        const int sa = s_a<R>(t), sb = s_b<R>(t);
-#pragma unroll
-        for (int qq = 0; qq < 8; ++qq) {
-            row[sa + R * qq] = pa[qq];
-            row[sb + R * qq] = pb[qq];
-        }
-    }
-}
-
-// Split regrid (R12) of the staged plane, in place, in two steps that each read only
-// the team's own column / row. Step A, column j2: Z(u3') = (1 - w3) S(ja) + w3 S(ja + 1),
-// v3 = o3 + M33 u3' (zero ghosts); all reads precede the writes (warp sync).
-template <typename T, int NQ, typename V>
-__device__ __forceinline__ void quad_regrid_col(V* col, int t, double M33, double o3) {
-    constexpr int R = NQ / 8, P = QCfg<NQ>::P;
-    V z[R];
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-        const double v3 = fma(M33, (double)(t + 8 * r) - 0.5 * (NQ - 1), o3), f3 = floor(v3);
-        const int fi3 = __double2int_rz(f3);
-        const int ja = min(max(fi3, -2), NQ);
-        const double w3 = (ja == fi3) ? v3 - f3 : 0.0;
-        double zx = 0.0, zy = 0.0;
-        if (ja >= 0 && ja < NQ) {
-            const V v = col[ja * P];
-            zx = (1.0 - w3) * (double)v.x;
-            zy = (1.0 - w3) * (double)v.y;
-        }
-        if (ja + 1 >= 0 && ja + 1 < NQ) {
-            const V v = col[(ja + 1) * P];
-            zx = fma(w3, (double)v.x, zx);
-            zy = fma(w3, (double)v.y, zy);
-        }
-        z[r] = V{(T)zx, (T)zy};
-    }
-    __syncwarp();
-#pragma unroll
-    for (int r = 0; r < R; ++r) col[(t + 8 * r) * P] = z[r];
-}
-
-// Step B, row u3': x[r] = linear interpolation of Z along j2 at v2 = o2 + M22 u2' + M23 u3'
-// (u2' = t + 8r, zero ghosts), read from the team's own row
-template <typename T, int NQ, typename V>
-__device__ __forceinline__ void quad_regrid_row(V (&x)[NQ / 8], const V* row, int u3, int t, double M22, double M23,
-                                                double o2) {
-    const double vb2 = fma(M23, (double)u3 - 0.5 * (NQ - 1), o2);
-#pragma unroll
-    for (int r = 0; r < NQ / 8; ++r) {
-        const double v2 = fma(M22, (t + 8 * r) - 0.5 * (NQ - 1), vb2), fl = floor(v2);
-        const int fi = min(max(__double2int_rz(fl), -2), NQ);
-        const double fr = v2 - fl;
-        const V lo = (fi >= 0 && fi < NQ) ? row[fi] : V{T(0), T(0)};
-        const V hi = (fi + 1 >= 0 && fi + 1 < NQ) ? row[fi + 1] : V{T(0), T(0)};
-        x[r] = V{(T)fma(fr, (double)hi.x - (double)lo.x, (double)lo.x),
-                 (T)fma(fr, (double)hi.y - (double)lo.y, (double)lo.y)};
-    }
-}
-
-// acc[r] *= product of list `list`'s Euler-factor pairs at kap_3 = kp[r]; pair j's quartic is
-// computed by thread j % 8 of the team and broadcast by shuffles (full warp, width 8)
-template <int NQ>
-__device__ __forceinline__ void quad_psi_prod(double (&acc)[NQ / 8], const double (&kp)[NQ / 8], const double* cf,
-                                              int l, int cn, int list, const double* kap, const double* kx, int t) {
-    constexpr int R = NQ / 8;
-    const int nq = (l + 1) >> 1;
-    double nyq = 1.0;
-    for (int jb = 0; jb < nq; jb += 8) {
-        double2 c[3] = {double2{1.0, 0.0}, double2{0.0, 0.0}, double2{0.0, 1.0}};
-        if (jb + t < nq) psi_pair<4, 3>(cf, l, cn, list, jb + t, kap, kx, c);
-        const int cnt = min(8, nq - jb);
-        for (int jj = 0; jj < cnt; ++jj) {
-            const double c0 = __shfl_sync(0xffffffffu, c[0].x, jj, 8);
-            const double c1 = __shfl_sync(0xffffffffu, c[0].y, jj, 8);
-            const double c2 = __shfl_sync(0xffffffffu, c[1].x, jj, 8);
-            const double c3 = __shfl_sync(0xffffffffu, c[1].y, jj, 8);
-            const double c4 = __shfl_sync(0xffffffffu, c[2].x, jj, 8);
-            nyq *= __shfl_sync(0xffffffffu, c[2].y, jj, 8);
-#pragma unroll
-            for (int r = 0; r < R; ++r) {
-                const double x1 = kp[r];
-                acc[r] *= fma(fma(fma(fma(c4, x1, c3), x1, c2), x1, c1), x1, c0);
-            }
-        }
-    }
-    if (t == ((NQ / 2) & 7)) acc[(NQ / 2) >> 3] = nyq;
-}
-
-template <typename T, int NQ, int TM>
-__global__ void __launch_bounds__(QCfg<NQ, TM>::NT, 1) k_plane_quad(QuadArgs<T> a) {
-    using V = typename C2<T>::type;
-    using C = QCfg<NQ, TM>;
-    constexpr int R = C::R, TEAMS = C::TEAMS, P = C::P;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    V* X = reinterpret_cast<V*>(smem_raw);                    // [NQ][P]: row j3
-    V* tw = X + NQ * P;                                       // [NQ]
-    const int tid = threadIdx.x, q = tid >> 3, t = tid & 7;
-    init_tw<NQ>(tw);
-    const unsigned I = (unsigned)a.I;
-    auto rs = [](int s2, int tt) { return rslot(s2, tt); };
-    auto cs = [](int s2, int tt) { return rslot(s2, tt) * P; };
-    // element (f, j3, j2, i) at ((f NQ + j3) NQ + j2) I + i: a 64-bit base per (f, i) and
-    // 32-bit offsets inside the filter (NQ^2 I < 2^31)
-    auto fbase = [&](const V* S, int item) -> const V* {
-        const unsigned f = (unsigned)item / I, i = (unsigned)item - f * I;
-        return S + (long long)f * (NQ * NQ) * (long long)I + i;
-    };
-    const unsigned step8 = 8u * I;
-    auto load_row = [&](const V* src, int j3) {
-        V* dst = X + j3 * P + t;
-        unsigned off = (unsigned)(j3 * NQ + t) * I;
-#pragma unroll
-        for (int r = 0; r < R; ++r, off += step8) tma::cp_async<sizeof(V)>(dst + 8 * r, src + off);
-    };
-    if ((int)blockIdx.x < a.items) {
-        const V* src = fbase(a.S, blockIdx.x);
-        for (int j3 = q; j3 < NQ; j3 += TEAMS) load_row(src, j3);
-    }
-    tma::cp_async_commit();
-    for (int item = blockIdx.x; item < a.items; item += gridDim.x) {
-        const int nxt = item + gridDim.x;
-        const unsigned f = (unsigned)item / I, i = (unsigned)item - f * I;
-        const double* Pc = a.coef + (long long)f * a.cs;
-        tma::cp_async_wait_all();
-        __syncthreads();                                      // the plane is in shared memory
-        if (Pc[PL_SKIP] != 0.0) {                             // uniform: failed filter, left untouched
-            if (nxt < a.items) {
-                const V* src = fbase(a.S, nxt);
-                for (int j3 = q; j3 < NQ; j3 += TEAMS) load_row(src, j3);
-            }
-            tma::cp_async_commit();
-            continue;
-        }
-        const int flag = (int)Pc[PL_FLAG];
-        // ---------------------------------------------------------------- F2 [+ split regrid]
-        const bool rg = flag == 4;
-        if (rg) {
-            const double M33 = Pc[PL_M + 15], o3 = Pc[PL_O + 3];
-#pragma unroll 1
-            for (int j2 = q; j2 < NQ; j2 += TEAMS) quad_regrid_col<T, NQ>(X + j2, t, M33, o3);
-            __syncthreads();
-        }
-        {
-            const double M22 = Pc[PL_M + 10], M23 = Pc[PL_M + 11], o2 = Pc[PL_O + 2];
-#pragma unroll 1
-            for (int j3 = q; j3 < NQ; j3 += TEAMS) {
-                V x[R];
-                if (rg) {
-                    quad_regrid_row<T, NQ>(x, X + j3 * P, j3, t, M22, M23, o2);
-                } else {
-#pragma unroll
-                    for (int r = 0; r < R; ++r) x[r] = X[j3 * P + t + 8 * r];
-                }
-                quad_f2_row<NQ>(x, X + j3 * P, tw, t);
-            }
-        }
-        __syncthreads();
-        // ---------------------------------------------------------------- F3: axis 3, s Psi / N_tot, inverse
-        {
-            const double* cf = Pc + PL_EU;
-            const int cn = a.step;
-            const unsigned k1 = i / (unsigned)a.N0;
-            const int k0 = (int)(i - k1 * (unsigned)a.N0);
-            const int N1 = 2 * (a.H1 - 1);
-            double kap[3], kx[3];
-            kap[0] = (2.0 * PMF_PI / a.N0) * (k0 < a.N0 / 2 ? k0 : k0 - a.N0);
-            kx[0] = (2 * k0 == a.N0) ? 0.0 : kap[0];
-            kap[1] = (2.0 * PMF_PI / N1) * (int)k1;
-            kx[1] = (2 * (int)k1 == N1) ? 0.0 : kap[1];
-            const double mult = Pc[PL_SN];
-#pragma unroll 1
-            for (int k2 = q; k2 < NQ; k2 += TEAMS) {
-                V* col = X + k2;
-                // Psi at k3 = t + 8r first (it needs no data: fewer live registers)
-                kap[2] = (2.0 * PMF_PI / NQ) * (k2 < NQ / 2 ? k2 : k2 - NQ);
-                kx[2] = (2 * k2 == NQ) ? 0.0 : kap[2];
-                double ps[R];
-                {
-                    double kp[R], den[R], num[R];
-#pragma unroll
-                    for (int r = 0; r < R; ++r) {
-                        const int k = t + 8 * r;
-                        kp[r] = (2.0 * PMF_PI / NQ) * (k < NQ / 2 ? k : k - NQ);
-                        den[r] = 1.0;
-                        num[r] = 1.0;
-                    }
-                    quad_psi_prod<NQ>(den, kp, cf, a.l, cn, 0, kap, kx, t);
-                    if (cn) quad_psi_prod<NQ>(num, kp, cf, a.l, cn, 1, kap, kx, t);
-                    psi_div<R>(den, mult, ps);
-#pragma unroll
-                    for (int r = 0; r < R; ++r) ps[r] *= num[r];
-                }
-                V x[R], pa[8], pb[8];
-#pragma unroll
-                for (int r = 0; r < R; ++r) x[r] = col[(t + 8 * r) * P];
-                team_dft<R, false>(x, pa, pb, col, tw, t, cs);
-                if (flag == 4 && i == 0 && k2 == 0 && t == 0) {
-                    // (k0, k1, k2, k3) = 0: the sum of the regridded weights (the split pass's DC)
-                    a.dc3[(long long)f * NQ] = (double)pa[0].x;
-                    for (int j = 1; j < NQ; ++j) a.dc3[(long long)f * NQ + j] = 0.0;
-                }
-                // Psi at k3 = t + 8r -> the owners of X[k3] via the (free) exchange column
-#pragma unroll
-                for (int r = 0; r < R; ++r) reinterpret_cast<double*>(col + (t + 8 * r) * P)[0] = ps[r];
-                __syncwarp();
-                if (s_on<R>(t)) {
-                    const int sa = s_a<R>(t), sb = s_b<R>(t);
-#pragma unroll
-                    for (int qq = 0; qq < 8; ++qq) {
-                        const double fa = reinterpret_cast<const double*>(col + (sa + R * qq) * P)[0];
-                        const double fb = reinterpret_cast<const double*>(col + (sb + R * qq) * P)[0];
-                        pa[qq] = V{(T)(pa[qq].x * fa), (T)(pa[qq].y * fa)};
-                        pb[qq] = V{(T)(pb[qq].x * fb), (T)(pb[qq].y * fb)};
-                    }
-                }
-                team_dft_dif<R, true>(pa, pb, x, col, tw, t, cs);
-#pragma unroll
-                for (int r = 0; r < R; ++r) col[(t + 8 * r) * P] = x[r];
-            }
-        }
-        __syncthreads();
-        // ---------------------------------------------------------------- I2: inverse axis 2, store, refill
-        const V* nsrc = nxt < a.items ? fbase(a.S, nxt) : nullptr;
-        V* dst = const_cast<V*>(fbase(a.Sout, item));
-#pragma unroll 1
-        for (int j3 = q; j3 < NQ; j3 += TEAMS) {
-            V* row = X + j3 * P;
-            V x[R], pa[8], pb[8];
-            if (s_on<R>(t)) {
-                const int sa = s_a<R>(t), sb = s_b<R>(t);
-#pragma unroll
-                for (int qq = 0; qq < 8; ++qq) {
-                    pa[qq] = row[sa + R * qq];
-                    pb[qq] = row[sb + R * qq];
-                }
-            }
-            team_dft_dif<R, true>(pa, pb, x, row, tw, t, rs);   // x[r] = element j2 = t + 8r
-            if (nsrc) load_row(nsrc, j3);                     // the row is free (the DFT ends with a warp sync)
-            unsigned off = (unsigned)(j3 * NQ + t) * I;
-#pragma unroll
-            for (int r = 0; r < R; ++r, off += step8) __stcg(dst + off, x[r]);
-        }
-        tma::cp_async_commit();
-    }
-    tma::cp_async_wait_all();
 }
 
 // ============================================================================ inverse plane pass (+ update)
@@ -1734,50 +1185,6 @@ static cudaError_t split_pass(const Dims& d, PencilBufs& b, int cs, typename C2<
     }
 }
 
-// fused (2,3)-plane pass: n2 = n3 with the plane in shared memory (fp64 up to 96^2,
-// fp32 up to 128^2). Opt-in (PMF_PLANE_FUSED23=1, read per call): on B200 at C4 (96^4)
-// it moves 40 % less HBM data than the three strided passes but runs 1.51 ms against
-// their 1.39 ms -- its per-element 16-byte gathers/scatters (stride H1 N0) and 8 warps
-// per SM leave it latency-bound.
-template <typename T>
-static bool quad_ok(const Dims& d) {
-    const char* e = std::getenv("PMF_PLANE_FUSED23");
-    if (!(e && e[0] == '1') || d.nx != 4 || d.n[2] != d.n[3]) return false;
-    const int n = d.n[2];
-    return n == 16 || n == 32 || n == 64 || n == 96 || (n == 128 && sizeof(T) == 4);
-}
-
-template <typename T, int NQ, int TM>
-static cudaError_t quad_tm(QuadArgs<T> qa, cudaStream_t s) {
-    using C = QCfg<NQ, TM>;
-    const size_t smem = quad_smem<T, NQ>();
-    int grid = 1;
-    cudaError_t e = occ_grid(k_plane_quad<T, NQ, TM>, C::NT, smem, qa.items, &grid);
-    if (e != cudaSuccess) return e;
-    k_plane_quad<T, NQ, TM><<<grid, C::NT, smem, s>>>(qa);
-    return cudaGetLastError();
-}
-
-// (48 teams at NQ = 96 -- 12 warps, 168 registers -- measured 12 % slower than 32 teams)
-template <typename T, int NQ>
-static cudaError_t quad_na(QuadArgs<T> qa, cudaStream_t s) {
-    return quad_tm<T, NQ, QCfg<NQ>::TEAMS>(qa, s);
-}
-
-template <typename T>
-static cudaError_t quad_pass(QuadArgs<T> qa, int nq, cudaStream_t s) {
-    switch (nq) {
-        case 16: return quad_na<T, 16>(qa, s);
-        case 32: return quad_na<T, 32>(qa, s);
-        case 64: return quad_na<T, 64>(qa, s);
-        case 96: return quad_na<T, 96>(qa, s);
-        case 128:
-            if constexpr (sizeof(T) == 4) return quad_na<T, 128>(qa, s);
-            return cudaErrorInvalidValue;
-        default: return cudaErrorInvalidValue;
-    }
-}
-
 template <typename T, int N, int NX>
 static cudaError_t plane_t(const Dims& d, PencilBufs& b, const ModelParams& mp, const LikParams* lp, double ks,
                            cudaStream_t s, int64_t* launches) {
@@ -1817,6 +1224,18 @@ static cudaError_t plane_t(const Dims& d, PencilBufs& b, const ModelParams& mp, 
         k_plane_pre<T, NX><<<(unsigned)(bpf * d.batch), 256, 0, s>>>((const T*)b.W, (T*)b.W2, b.coef, cs, d, bpf);
         ++*launches;
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    }
+    // nx = 4, fp64: the three-pass transposed-spectrum route (kernels_quad.cu)
+    if constexpr (NX == 4 && std::is_same<T, double>::value && N <= 96) {
+        if (quad_supported(d, 0)) {
+            int ginv = 1;
+            e = launch_quad(d, b, mp, pa.range, rg, lp != nullptr, pa.dcpart, pa.dc3, pa.part, s, launches, &ginv);
+            if (e != cudaSuccess) return e;
+            k_plane_fin<NX><<<d.batch, 256, 0, s>>>(b.st, b.coef, cs, pa.dcpart, pa.dc3, pa.part, ppf, n3, ginv,
+                                                    lp ? 1 : 0);
+            ++*launches;
+            return cudaGetLastError();
+        }
     }
     // forward plane pass
     {
@@ -1860,34 +1279,14 @@ static cudaError_t plane_t(const Dims& d, PencilBufs& b, const ModelParams& mp, 
         ++*launches;
         return mid_pass<T, NX>(ma, d.n[m], mode, s);
     };
-    if (NX == 4 && quad_ok<T>(d)) {
-        // one fused pass over the (i2, i3)-planes instead of three strided passes
-        QuadArgs<T> qa;
-        qa.S = S;
-        qa.Sout = S2;
-        qa.coef = b.coef;
-        qa.cs = cs;
-        qa.I = Cf::H * N;
-        qa.N0 = N;
-        qa.H1 = Cf::H;
-        qa.l = mp.l;
-        qa.step = mp.step;
-        qa.items = qa.I * d.batch;
-        qa.dc3 = pa.dc3;
-        if (b.ev0) cudaEventRecordWithFlags(b.ev0, s, cudaEventRecordExternal);
-        if ((e = quad_pass<T>(qa, d.n[2], s)) != cudaSuccess) return e;
-        if (b.ev1) cudaEventRecordWithFlags(b.ev1, s, cudaEventRecordExternal);
-        ++*launches;
-    } else {
-        if (NX == 4) {
-            if ((e = mid(2, 0, S, S2, rg ? 1 : 0)) != cudaSuccess) return e;
-            if (rg && (e = split_pass<T>(d, b, cs, S, S2, pa.dc3, mp.l, s, launches)) != cudaSuccess) return e;
-        }
-        if (b.ev0) cudaEventRecordWithFlags(b.ev0, s, cudaEventRecordExternal);
-        if ((e = mid(NX - 1, 2, S2, S2, 0)) != cudaSuccess) return e;
-        if (b.ev1) cudaEventRecordWithFlags(b.ev1, s, cudaEventRecordExternal);
-        if (NX == 4 && (e = mid(2, 1, S2, S2, 0)) != cudaSuccess) return e;
+    if (NX == 4) {
+        if ((e = mid(2, 0, S, S2, rg ? 1 : 0)) != cudaSuccess) return e;
+        if (rg && (e = split_pass<T>(d, b, cs, S, S2, pa.dc3, mp.l, s, launches)) != cudaSuccess) return e;
     }
+    if (b.ev0) cudaEventRecordWithFlags(b.ev0, s, cudaEventRecordExternal);
+    if ((e = mid(NX - 1, 2, S2, S2, 0)) != cudaSuccess) return e;
+    if (b.ev1) cudaEventRecordWithFlags(b.ev1, s, cudaEventRecordExternal);
+    if (NX == 4 && (e = mid(2, 1, S2, S2, 0)) != cudaSuccess) return e;
     // inverse plane pass (+ update)
     int ginv = 1;
     {

@@ -1,0 +1,886 @@
+// kernels_quad.cu -- the three-pass ("transposed spectrum") time update for nx = 4
+// grids (BASELINE configs[3], C4: 96^4 fp64).
+//
+// The 4-D half spectrum is kept in HBM in the layout
+//
+//     Y[filter][k1 (0..N/2)][k0 (0..N-1)][j3][j2]          (complex fp64)
+//
+// so that, for every axis-0/1 wavenumber pair (k0, k1), the (j2, j3)-plane that the
+// axis-2/3 transforms need is ONE contiguous n3 x n2 block (147 KB at 96^2). One
+// prediction interval + measurement update is then three passes over HBM:
+//
+//   K1 k_q_fwd   per PAIR of (j0, j1)-planes (j2, j2 + 1; same j3): [split regrid,
+//                in-plane part, R12] -> forward DFT along axes 1 and 0 (Alg. 1,
+//                eq:fourtrsf P:221) of both planes in shared memory -> the two
+//                planes' coefficients (k1, k0) leave as one 32-byte store each
+//                (both j2 of the pair are adjacent in Y)
+//   K2 k_q_mid   per (filter, k1, k0): the contiguous (j3, j2)-plane by bulk copies
+//                -> [split regrid, axes-2/3 part] -> forward DFT along axes 2, 3 ->
+//                s Psi / N_tot (Alg. 3-4, Euler factors paired into quartics) ->
+//                inverse DFT along axes 3, 2 (Alg. 5) -> back in place
+//   K3 k_q_inv   per (j0, j1)-plane: gather of its coefficients (16-byte cp.async,
+//                neighbouring planes on neighbouring CTAs share the 32-byte sectors
+//                in L2) -> inverse DFT along axes 0, 1 -> likelihood at the moved
+//                points (eq:filt P:46, R13), store, index-space moment partials
+//
+// against five passes on the per-plane layout of kernels_plane.cu. Prep, the general
+// regrid pre-pass and the finaliser are shared with that path. fp64 only (the pair
+// store is one 32-byte sector); N_0 = N_1 in {32, 64, 96}, n2 = n3 in {16, .., 96}.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+
+#include "device_common.cuh"
+#include "fft_reg.cuh"
+#include "plane_common.cuh"
+#include "tma.cuh"
+
+namespace pmf {
+namespace pln {
+
+using V = double2;
+
+struct QArgs {
+    const double* Wsrc;      // weights read by K1 (old grid when regridding)
+    const double* W2src;     // pre-regridded weights (general regrid map, flag 2)
+    double* W;               // weights written by K3
+    V* Y;                    // spectrum, layout [filter][k1][k0][j3][j2]
+    const double* coef;
+    int cs;
+    double* dcpart;          // [plane] sums of K1's input planes
+    double* dc3;             // [filter][n3] the regridded sums (split maps; K2)
+    double* part;            // [filter][K3 CTAs][NMOM]
+    int batch;
+    int n2, n3;              // plane sizes (n2 == n3 == NQ)
+    int l, step;
+    int range;               // likelihood kind 1 (range), else linear Gauss
+};
+
+// ============================================================================ K1: forward plane pairs
+// shared memory: X_A, X_B [H][PITCH] complex, a 16-byte zero guard, the staged real plane
+// [N][SP2] (pitch N + 2: 16-byte rows, the 8 rows a team reads in distinct bank groups;
+// the two padding columns stay zero and are the zero ghost nodes of R12 -- column N of
+// row r and column -1 of row r + 1, the guard being column -1 of row 0), twiddles, one
+// mbarrier. At N = 96: 2 x 76.8 KB + 75.3 KB + 1.5 KB = 230.5 KB.
+template <int N> struct F1 {
+    static constexpr int SP2 = N + 2;
+    static constexpr size_t XB = sizeof(V) * Cfg<N>::H * Cfg<N>::PITCH;
+    static constexpr size_t SB = sizeof(double) * N * SP2 + 16;
+    static constexpr size_t SMEM = 2 * XB + SB + sizeof(V) * N + 16;
+    static constexpr int MINB = SMEM <= 113 * 1024 ? 2 : 1;
+};
+
+// forward DFT along axis 1 (column pairs, packed complex) and axis 0 (rows) of one
+// real plane whose column pair (2m, 2m+1) is in z[r] = (w(2m, t+8r), w(2m+1, t+8r));
+// result: X[k1][k0] natural order, k1 = 0..N/2 (as k_plane_fwd)
+template <int N>
+__device__ __forceinline__ void fwd_plane(V* X, V (&z)[N / 8], const V* tw, int m, int t) {
+    constexpr int R1 = N / 8, PITCH = Cfg<N>::PITCH;
+    {
+        V pa[8], pb[8];
+        team_dft<R1, false>(z, pa, pb, X, tw, t, [&](int s2, int tt) { return cslot<N>(s2, tt, m); });
+        if (s_on<R1>(t)) {
+            const int sa = s_a<R1>(t), sb = s_b<R1>(t);
+            auto store_pair = [&](int k1, V zk, V zp) {
+                X[k1 * PITCH + xcol(k1, 2 * m)] = V{0.5 * (zk.x + zp.x), 0.5 * (zk.y - zp.y)};
+                X[k1 * PITCH + xcol(k1, 2 * m + 1)] = V{0.5 * (zk.y + zp.y), 0.5 * (zp.x - zk.x)};
+            };
+            const bool t0 = t == 0;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const V ma = t0 ? pa[(8 - q) & 7] : pb[7 - q];
+                const V mb = t0 ? pb[7 - q] : pa[7 - q];
+                store_pair(sa + R1 * q, pa[q], ma);
+                store_pair(sb + R1 * q, pb[q], mb);
+            }
+            if (t0) store_pair(R1 * 4, pa[4], pa[4]);
+        }
+    }
+    __syncthreads();
+    {
+        V x[R1], pa[8], pb[8];
+        V* row = X + m * PITCH;
+        const bool m0 = m == 0;
+#pragma unroll
+        for (int r = 0; r < R1; ++r) {
+            const V A = row[xcol(m, t + 8 * r)];
+            const double B = m0 ? X[(N / 2) * PITCH + t + 8 * r].x : 0.0;
+            x[r] = m0 ? V{A.x, B} : A;
+        }
+        team_dft<R1, false>(x, pa, pb, row, tw, t, [](int s2, int tt) { return rslot(s2, tt); });
+        if (s_on<R1>(t)) {
+            const int sa = s_a<R1>(t), sb = s_b<R1>(t);
+            if (m == 0) {
+                auto unpack = [&](int kk, V rk, V rm) {
+                    X[kk] = V{0.5 * (rk.x + rm.x), 0.5 * (rk.y - rm.y)};
+                    X[(N / 2) * PITCH + kk] = V{0.5 * (rk.y + rm.y), 0.5 * (rm.x - rk.x)};
+                };
+                const bool t0 = t == 0;
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    unpack(sa + R1 * q, pa[q], t0 ? pa[(8 - q) & 7] : pb[7 - q]);
+                    unpack(sb + R1 * q, pb[q], t0 ? pb[7 - q] : pa[7 - q]);
+                }
+            } else {
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    row[sa + R1 * q] = pa[q];
+                    row[sb + R1 * q] = pb[q];
+                }
+            }
+        }
+    }
+    __syncthreads();
+}
+
+template <int N, bool RG>
+__global__ void __launch_bounds__(Cfg<N>::NT, F1<N>::MINB) k_q_fwd(QArgs a) {
+    using C = Cfg<N>;
+    constexpr int R1 = C::R1, H = C::H, PITCH = C::PITCH, NT = C::NT, SP2 = F1<N>::SP2;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    V* XA = reinterpret_cast<V*>(smem_raw);
+    V* XB = XA + H * PITCH;
+    double* stg = reinterpret_cast<double*>(XB + H * PITCH) + 2;   // after the zero guard
+    V* tw = reinterpret_cast<V*>(stg + N * SP2);
+    unsigned long long* bar = reinterpret_cast<unsigned long long*>(tw + N);
+    const int tid = threadIdx.x, m = tid >> 3, t = tid & 7;
+    init_tw<N>(tw);
+    if (tid == 0) tma::mbar_init(bar, 1);
+    for (int i = tid; i < 2 * N + 2; i += NT) {               // ghost columns and guard: zero
+        if (i < 2) stg[i - 2] = 0.0;
+        else stg[((i - 2) >> 1) * SP2 + N + ((i - 2) & 1)] = 0.0;
+    }
+    const int n2 = a.n2, n3 = a.n3, ppf = n2 * n3, hp = n2 / 2;
+    const long long ntot = (long long)N * N * ppf, nq = (long long)n2 * n3;
+    const int units = a.batch * n3 * hp;
+    __syncthreads();
+    // stage plane pl of filter f (rows issued by the first N threads)
+    auto issue = [&](int f, int pl) {
+        if (tid >= N) return;
+        const double* P = a.coef + (long long)f * a.cs;
+        const double* src = ((RG && (int)P[PL_FLAG] == 2) ? a.W2src : a.Wsrc) + f * ntot + (long long)pl * N * N;
+        tma::fence_proxy_async();
+        if (tid == 0) tma::mbar_expect_tx(bar, (unsigned)(N * N * sizeof(double)));
+        tma::bulk_g2s(stg + tid * SP2, src + (long long)tid * N, (unsigned)(N * sizeof(double)), bar);
+    };
+    auto decode = [&](int u, int& f, int& j3, int& j2) {
+        f = u / (n3 * hp);
+        const int r = u - f * n3 * hp;
+        j3 = r / hp;
+        j2 = 2 * (r - j3 * hp);
+    };
+    if ((int)blockIdx.x < units) {
+        int f, j3, j2;
+        decode(blockIdx.x, f, j3, j2);
+        issue(f, j3 * n2 + j2);
+    }
+    int k = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        int f, j3, j2;
+        decode(u, f, j3, j2);
+        const double* P = a.coef + (long long)f * a.cs;
+        const int flag = RG ? (int)P[PL_FLAG] : 0;
+        const bool skip = P[PL_SKIP] != 0.0;
+#pragma unroll 1
+        for (int h = 0; h < 2; ++h, ++k) {
+            tma::mbar_wait(bar, (unsigned)(k & 1));
+            V z[R1];
+            if (RG && flag == 4) {
+                // in-plane part of the split regrid map (R12): bilinear from the staged old
+                // plane, v1 = o1 + M11 u1', v0 = o0 + M00 u0' + M01 u1'; zero ghost nodes
+                const double M00 = P[PL_M], M01 = P[PL_M + 1], M11 = P[PL_M + 5], o0 = P[PL_O], o1 = P[PL_O + 1];
+                auto split = [&](double v, int& i, double& fr) {
+                    const double fl = floor(v);
+                    const int fi = __double2int_rz(fl);
+                    i = min(max(fi, -1), N);
+                    fr = (fi == i) ? v - fl : 0.0;
+                };
+#pragma unroll
+                for (int r = 0; r < R1; ++r) {
+                    const double u1 = (t + 8 * r) - 0.5 * (N - 1);
+                    int i1;
+                    double a1;
+                    split(fma(M11, u1, o1), i1, a1);
+                    // ghost rows -1 and N: selected to zero (the ghost columns are in the buffer)
+                    const bool va = (unsigned)i1 < (unsigned)N, vb = (unsigned)(i1 + 1) < (unsigned)N;
+                    const double* ra = stg + (va ? i1 : 0) * SP2;              // in-bounds addresses
+                    const double* rb = stg + (vb ? i1 + 1 : 0) * SP2;
+                    const double vbase = fma(M01, u1, o0);
+                    double val[2];
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) {
+                        int i0;
+                        double a0;
+                        split(fma(M00, (2 * m + e) - 0.5 * (N - 1), vbase), i0, a0);
+                        const double w00 = va ? ra[i0] : 0.0, w01 = va ? ra[i0 + 1] : 0.0;
+                        const double w10 = vb ? rb[i0] : 0.0, w11 = vb ? rb[i0 + 1] : 0.0;
+                        const double lo = fma(a0, w01 - w00, w00), hi = fma(a0, w11 - w10, w10);
+                        val[e] = fma(a1, hi - lo, lo);
+                    }
+                    z[r] = V{val[0], val[1]};
+                }
+            } else {
+#pragma unroll
+                for (int r = 0; r < R1; ++r) z[r] = *reinterpret_cast<const V*>(stg + (t + 8 * r) * SP2 + 2 * m);
+            }
+            __syncthreads();                                  // staged plane consumed
+            if (h == 0) issue(f, j3 * n2 + j2 + 1);
+            else if (u + (int)gridDim.x < units) {
+                int f2, j32, j22;
+                decode(u + gridDim.x, f2, j32, j22);
+                issue(f2, j32 * n2 + j22);
+            }
+            if (skip) continue;                               // uniform
+            fwd_plane<N>(h ? XB : XA, z, tw, m, t);
+        }
+        if (skip) continue;
+        // both planes' coefficients (k1, k0) as one 32-byte store each: Y[f][k1][k0][j3][j2, j2+1]
+        if (tid == 0) {
+            a.dcpart[(long long)f * ppf + j3 * n2 + j2] = XA[0].x;      // sums of the input planes
+            a.dcpart[(long long)f * ppf + j3 * n2 + j2 + 1] = XB[0].x;
+        }
+        double* yb = reinterpret_cast<double*>(a.Y + (long long)f * H * N * nq + (long long)j3 * n2 + j2);
+        for (int e = tid; e < H * N; e += NT) {
+            const int k1 = e / N, k0 = e - k1 * N;
+            const V va = XA[k1 * PITCH + k0], vb = XB[k1 * PITCH + k0];
+            double* g = yb + 2 * (long long)e * nq;
+            asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(g), "d"(va.x), "d"(va.y), "d"(vb.x),
+                         "d"(vb.y)
+                         : "memory");
+        }
+        __syncthreads();                                      // X_A, X_B free
+    }
+}
+
+// ============================================================================ K2: contiguous (j3, j2)-planes
+// Work item = (filter, k1, k0); its plane Y[f][k1][k0][.][.] (NQ rows of NQ complex) is
+// staged row by row (bulk copies completing on one mbarrier) into rows of pitch NQ + 1
+// (conflict-free along rows and columns). Team q owns rows / columns q + TEAMS j.
+//   [split regrid, axes 3 then 2 (R12), in place]
+//   F2  forward DFT along axis 2 of every row
+//   F3  per column k2: forward DFT along axis 3, x s Psi / N_tot (Alg. 3-4), inverse
+//   I2  inverse DFT along axis 2 of every row, stored back in place from registers;
+//       each freed row is refilled at once with the next item's row (its bulk copy
+//       overlaps the rest of this item)
+// shared memory: X [NQ][P] complex, the item's s Psi / N_tot table [NQ (k2)][PSP (k3)],
+// the axis-3 regrid taps per output row (split maps), twiddles, one mbarrier.
+template <int NQ> struct Q2 {
+    static constexpr int PSP = NQ + 1;                       // Psi table pitch (doubles)
+    static constexpr int R3 = (NQ + 31) / 32;                // k3 values per lane in the table phase
+    static constexpr size_t SMEM = sizeof(V) * NQ * QCfg<NQ>::P + sizeof(double) * NQ * PSP +
+                                   (sizeof(double) + sizeof(int)) * NQ + sizeof(V) * NQ + 16;
+};
+template <int NQ>
+static size_t qmid_smem() { return Q2<NQ>::SMEM; }
+
+template <int NQ, int TM>
+__global__ void __launch_bounds__(QCfg<NQ, TM>::NT, 1) k_q_mid(QArgs a, int I, int N0, int H1) {
+    using C = QCfg<NQ, TM>;
+    constexpr int R = C::R, TEAMS = C::TEAMS, P = C::P;
+    constexpr int PSP = Q2<NQ>::PSP;
+    constexpr unsigned PLANE = NQ * NQ * sizeof(V);
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    V* X = reinterpret_cast<V*>(smem_raw);                    // [NQ][P]: row j3
+    double* psi = reinterpret_cast<double*>(X + NQ * P);      // [k2][PSP]
+    double* w3t = psi + NQ * PSP;                             // [u3'] axis-3 weight (split regrid)
+    int* j3t = reinterpret_cast<int*>(w3t + NQ);              // [u3'] first old row
+    V* tw = reinterpret_cast<V*>(j3t + NQ);
+    unsigned long long* bar = reinterpret_cast<unsigned long long*>(tw + NQ);
+    const int tid = threadIdx.x, q = tid >> 3, t = tid & 7;
+    init_tw<NQ>(tw);
+    if (tid == 0) tma::mbar_init(bar, 1);
+    const int items = a.batch * I;
+    __syncthreads();
+    auto rs = [](int s2, int tt) { return rslot(s2, tt); };
+    auto cs = [](int s2, int tt) { return rslot(s2, tt) * P; };
+    auto load_row = [&](int it, int j3) {
+        tma::bulk_g2s(X + j3 * P, a.Y + (long long)it * (NQ * NQ) + j3 * NQ, NQ * sizeof(V), bar);
+    };
+    if ((int)blockIdx.x < items) {
+        if (tid == 0) tma::mbar_expect_tx(bar, PLANE);
+        __syncthreads();
+        if (tid < NQ) load_row(blockIdx.x, tid);
+    }
+    int k = 0;
+    for (int item = blockIdx.x; item < items; item += gridDim.x, ++k) {
+        const int nxt = item + gridDim.x;
+        const unsigned f = (unsigned)item / (unsigned)I, i = (unsigned)item - f * (unsigned)I;
+        const double* Pc = a.coef + (long long)f * a.cs;
+        const bool skip = Pc[PL_SKIP] != 0.0;
+        const int flag = (int)Pc[PL_FLAG];
+        if (!skip) {
+            // ------------------------------------------------------------ tables (while the plane loads)
+            // s Psi / N_tot at every (k2, k3) of this (k0, k1) (Alg. 3-4): Euler factors
+            // f_n = gam_n + bet_n kx3 + alp_n kap3^2 multiplied in pairs as quartics in kap3;
+            // warp w owns columns k2 = w + NW j, lane owns k3 = lane + 32 r; pair j's quartic is
+            // computed by lane j % 32 and broadcast
+            const double* cf = Pc + PL_EU;
+            const int cn = a.step, l = a.l, nq = (l + 1) >> 1;
+            const unsigned k1 = i / (unsigned)N0;
+            const int k0 = (int)(i - k1 * (unsigned)N0);
+            const int N1 = 2 * (H1 - 1);
+            double kap[3], kx[3];
+            kap[0] = (2.0 * PMF_PI / N0) * (k0 < N0 / 2 ? k0 : k0 - N0);
+            kx[0] = (2 * k0 == N0) ? 0.0 : kap[0];
+            kap[1] = (2.0 * PMF_PI / N1) * (int)k1;
+            kx[1] = (2 * (int)k1 == N1) ? 0.0 : kap[1];
+            const double mult = Pc[PL_SN];
+            double kp[R];
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const int kk = t + 8 * r;
+                kp[r] = (2.0 * PMF_PI / NQ) * (kk < NQ / 2 ? kk : kk - NQ);
+            }
+            // team q: columns k2 = q + TEAMS j; thread t: k3 = t + 8 r (pair quartics by
+            // width-8 shuffles, quad_psi_prod)
+#pragma unroll 1
+            for (int k2 = q; k2 < NQ; k2 += TEAMS) {
+                kap[2] = (2.0 * PMF_PI / NQ) * (k2 < NQ / 2 ? k2 : k2 - NQ);
+                kx[2] = (2 * k2 == NQ) ? 0.0 : kap[2];
+                double den[R], ps[R];
+#pragma unroll
+                for (int r = 0; r < R; ++r) den[r] = 1.0;
+                quad_psi_prod<NQ>(den, kp, cf, l, cn, 0, kap, kx, t);
+                psi_div<R>(den, mult, ps);
+                if (cn) {                                     // Crank-Nicolson numerators (R27)
+#pragma unroll
+                    for (int r = 0; r < R; ++r) den[r] = 1.0;
+                    quad_psi_prod<NQ>(den, kp, cf, l, cn, 1, kap, kx, t);
+#pragma unroll
+                    for (int r = 0; r < R; ++r) ps[r] *= den[r];
+                }
+#pragma unroll
+                for (int r = 0; r < R; ++r) psi[k2 * PSP + t + 8 * r] = ps[r];
+            }
+            if (flag == 4 && tid < NQ) {
+                // axis-3 part of the split regrid (R12): output row u3' reads old rows ja, ja + 1
+                const double v3 = fma(Pc[PL_M + 15], (double)tid - 0.5 * (NQ - 1), Pc[PL_O + 3]), f3 = floor(v3);
+                const int fi3 = __double2int_rz(f3);
+                const int ja = min(max(fi3, -2), NQ);
+                j3t[tid] = ja;
+                w3t[tid] = (ja == fi3) ? v3 - f3 : 0.0;
+            }
+        }
+        tma::mbar_wait(bar, (unsigned)(k & 1));               // the plane is in shared memory
+        __syncthreads();                                      // (and the tables are written)
+        if (!skip) {
+            // ------------------------------------------------------------ [split regrid] + F2
+            const bool rg = flag == 4;
+            if (rg) {
+#pragma unroll 1
+                for (int j2 = q; j2 < NQ; j2 += TEAMS) {
+                    V* col = X + j2;
+                    V z[R];
+#pragma unroll
+                    for (int r = 0; r < R; ++r) {
+                        const int u3 = t + 8 * r, ja = j3t[u3];
+                        const double w3 = w3t[u3];
+                        double zx = 0.0, zy = 0.0;
+                        if (ja >= 0 && ja < NQ) {
+                            const V v = col[ja * P];
+                            zx = (1.0 - w3) * v.x;
+                            zy = (1.0 - w3) * v.y;
+                        }
+                        if (ja + 1 >= 0 && ja + 1 < NQ) {
+                            const V v = col[(ja + 1) * P];
+                            zx = fma(w3, v.x, zx);
+                            zy = fma(w3, v.y, zy);
+                        }
+                        z[r] = V{zx, zy};
+                    }
+                    __syncwarp();
+#pragma unroll
+                    for (int r = 0; r < R; ++r) col[(t + 8 * r) * P] = z[r];
+                }
+                __syncthreads();
+            }
+            {
+                const double M22 = Pc[PL_M + 10], M23 = Pc[PL_M + 11], o2 = Pc[PL_O + 2];
+#pragma unroll 1
+                for (int j3 = q; j3 < NQ; j3 += TEAMS) {
+                    V x[R];
+                    if (rg) {
+                        quad_regrid_row<double, NQ>(x, X + j3 * P, j3, t, M22, M23, o2);
+                    } else {
+#pragma unroll
+                        for (int r = 0; r < R; ++r) x[r] = X[j3 * P + t + 8 * r];
+                    }
+                    quad_f2_row<NQ>(x, X + j3 * P, tw, t);
+                }
+            }
+            __syncthreads();
+            // ------------------------------------------------------------ F3: axis 3, x table, inverse
+#pragma unroll 1
+            for (int k2 = q; k2 < NQ; k2 += TEAMS) {
+                V* col = X + k2;
+                const double* pr = psi + k2 * PSP;
+                V x[R], pa[8], pb[8];
+#pragma unroll
+                for (int r = 0; r < R; ++r) x[r] = col[(t + 8 * r) * P];
+                team_dft<R, false>(x, pa, pb, col, tw, t, cs);
+                if (flag == 4 && i == 0 && k2 == 0 && t == 0) {
+                    // (k0, k1, k2, k3) = 0: the sum of the regridded weights
+                    a.dc3[(long long)f * a.n3] = pa[0].x;
+                    for (int j = 1; j < a.n3; ++j) a.dc3[(long long)f * a.n3 + j] = 0.0;
+                }
+                if (s_on<R>(t)) {
+                    const int sa = s_a<R>(t), sb = s_b<R>(t);
+#pragma unroll
+                    for (int qq = 0; qq < 8; ++qq) {
+                        const double fa = pr[sa + R * qq], fb = pr[sb + R * qq];
+                        pa[qq] = V{pa[qq].x * fa, pa[qq].y * fa};
+                        pb[qq] = V{pb[qq].x * fb, pb[qq].y * fb};
+                    }
+                }
+                team_dft_dif<R, true>(pa, pb, x, col, tw, t, cs);
+#pragma unroll
+                for (int r = 0; r < R; ++r) col[(t + 8 * r) * P] = x[r];
+            }
+        }
+        if (tid == 0 && nxt < items) tma::mbar_expect_tx(bar, PLANE);   // the next phase's bytes
+        __syncthreads();
+        // ---------------------------------------------------------------- I2: inverse axis 2, store, refill
+        V* dst = a.Y + (long long)item * (NQ * NQ);
+#pragma unroll 1
+        for (int j3 = q; j3 < NQ; j3 += TEAMS) {
+            V* row = X + j3 * P;
+            if (!skip) {
+                V x[R], pa[8], pb[8];
+                if (s_on<R>(t)) {
+                    const int sa = s_a<R>(t), sb = s_b<R>(t);
+#pragma unroll
+                    for (int qq = 0; qq < 8; ++qq) {
+                        pa[qq] = row[sa + R * qq];
+                        pb[qq] = row[sb + R * qq];
+                    }
+                }
+                team_dft_dif<R, true>(pa, pb, x, row, tw, t, rs);   // x[r] = element j2 = t + 8r
+#pragma unroll
+                for (int r = 0; r < R; ++r) __stcg(dst + j3 * NQ + t + 8 * r, x[r]);
+            }
+            if (nxt < items) {
+                tma::fence_proxy_async();                     // this lane's reads of the row precede the copy
+                __syncwarp();
+                if (t == 0) load_row(nxt, j3);
+            }
+        }
+    }
+}
+
+// ============================================================================ K3: inverse plane pass (+ update)
+// Plane p's coefficients Y[f][k1][k0][j3][j2] arrive by ONE tensor-map TMA load (box
+// 2 x 1 x 1 x (N + 2) x H doubles over the map (re/im, j2, j3, k0, filter*k1)): the two
+// out-of-range k0 per row are zero-filled, so the box lands as [H][PITCH = N + 2] -- the
+// conflict-free pitch of the transforms. Two buffers: the next plane's load overlaps this
+// plane's work. The rest is k_plane_inv's arithmetic; the filter's coefficient block is
+// cached in shared memory.
+template <int N> struct Q3 {
+    static constexpr size_t XS = (sizeof(V) * Cfg<N>::H * Cfg<N>::PITCH + 127) / 128 * 128;   // TMA: 128-B aligned
+    static constexpr size_t SMEM = 2 * XS + sizeof(V) * N + sizeof(double) * NMOM * (Cfg<N>::NT / 32) + 16 +
+                                   sizeof(double) * NMOM * Cfg<N>::NT + sizeof(double) * PL_EU;
+};
+template <int N>
+static size_t qinv_smem() { return Q3<N>::SMEM; }
+
+template <int N, bool UP>
+__global__ void __launch_bounds__(Cfg<N>::NT, 1) k_q_inv(QArgs a, const __grid_constant__ CUtensorMap ymap) {
+    using C = Cfg<N>;
+    constexpr int R1 = C::R1, H = C::H, PITCH = C::PITCH, NT = C::NT, NW = NT / 32, NX = 4;
+    constexpr int XSV = (int)(Q3<N>::XS / sizeof(V));
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    V* X0 = reinterpret_cast<V*>(smem_raw);
+    V* tw = X0 + 2 * XSV;
+    double* red = reinterpret_cast<double*>(tw + N);          // [NW][NMOM]
+    unsigned long long* bar = reinterpret_cast<unsigned long long*>(red + NMOM * NW);
+    double* cfs = reinterpret_cast<double*>(bar + 2) + NMOM * NT;   // the current filter's coefficients
+    const int tid = threadIdx.x, m = tid >> 3, t = tid & 7, lane = tid & 31, warp = tid >> 5;
+    init_tw<N>(tw);
+    if (tid == 0) {
+        tma::mbar_init(&bar[0], 1);
+        tma::mbar_init(&bar[1], 1);
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&ymap) : "memory");
+    }
+    const int n2 = a.n2, n3 = a.n3, ppf = n2 * n3;
+    const long long ntot = (long long)N * N * ppf, nq = (long long)n2 * n3;
+    const int nplanes = a.batch * ppf;
+    __syncthreads();
+    constexpr int NM = 1 + NX + NX * (NX + 1) / 2;
+    double* mom = reinterpret_cast<double*>(bar + 2) + tid;  // this thread's sums, stride NT (shared)
+#pragma unroll
+    for (int q = 0; q < NM; ++q) mom[q * NT] = 0.0;
+    int curf = -1;
+    auto flush = [&]() {
+        if (curf < 0) return;
+#pragma unroll
+        for (int q = 0; q < NM; ++q) {
+            double v = mom[q * NT];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+            if (lane == 0) red[warp * NM + q] = v;
+            mom[q * NT] = 0.0;
+        }
+        __syncthreads();
+        if (tid < NM) {
+            double v = 0.0;
+            for (int w = 0; w < NW; ++w) v += red[w * NM + tid];
+            a.part[((long long)curf * gridDim.x + blockIdx.x) * NMOM + tid] = v;
+        }
+        __syncthreads();
+    };
+    // plane p (filter f, (j2, j3)) into buffer buf: one TMA tensor load
+    auto issue = [&](int p, int buf) {
+        if (p >= nplanes || tid != 0) return;
+        const int f = p / ppf, pl = p - f * ppf, j3 = pl / n2, j2 = pl - j3 * n2;
+        tma::fence_proxy_async();
+        tma::mbar_expect_tx(&bar[buf], (unsigned)(H * PITCH * sizeof(V)));
+        asm volatile(
+            "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, "
+            "%6}], [%7];" ::"r"(tma::smem_u32(X0 + buf * XSV)),
+            "l"(&ymap), "r"(0), "r"(j2), "r"(j3), "r"(0), "r"(f * H), "r"(tma::smem_u32(&bar[buf]))
+            : "memory");
+    };
+    issue(blockIdx.x, 0);
+    int k = 0;
+    for (int p = blockIdx.x; p < nplanes; p += gridDim.x, ++k) {
+        const int buf = k & 1;
+        issue(p + gridDim.x, buf ^ 1);
+        tma::mbar_wait(&bar[buf], (unsigned)((k >> 1) & 1));
+        V* X = X0 + buf * XSV;
+        const int filt = p / ppf, pl = p - filt * ppf;
+        if (filt != curf) {                                   // uniform
+            if (UP) flush();
+            curf = filt;
+            if (tid < PL_EU) cfs[tid] = a.coef[(long long)filt * a.cs + tid];
+            __syncthreads();
+        }
+        const double* P = cfs;
+        if (P[PL_SKIP] != 0.0) {
+            __syncthreads();
+            continue;
+        }
+        // ------------------------------------------------------------ inverse axis 0 of row k1 = m
+        {
+            V x[R1], pa[8], pb[8];
+            V* row = X + m * PITCH;
+            const bool m0 = m == 0;
+#pragma unroll
+            for (int r = 0; r < R1; ++r) {
+                const V A = row[t + 8 * r];
+                const V B = m0 ? X[(N / 2) * PITCH + t + 8 * r] : V{0.0, 0.0};
+                x[r] = V{A.x - B.y, A.y + B.x};
+            }
+            team_dft<R1, true>(x, pa, pb, row, tw, t, [](int s, int tt) { return rslot(s, tt); });
+            if (s_on<R1>(t)) {
+                const int sa = s_a<R1>(t), sb = s_b<R1>(t);
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    row[xcol(m, sa + R1 * q)] = m0 ? V{pa[q].x, 0.0} : pa[q];
+                    row[xcol(m, sb + R1 * q)] = m0 ? V{pb[q].x, 0.0} : pb[q];
+                    if (m0) {
+                        X[(N / 2) * PITCH + sa + R1 * q] = V{pa[q].y, 0.0};
+                        X[(N / 2) * PITCH + sb + R1 * q] = V{pb[q].y, 0.0};
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        // ------------------------------------------------------------ inverse axis 1 of the column pair
+        V x[R1];
+        {
+            V pa[8], pb[8];
+            auto ld = [&](int k1, int col) -> V { return X[k1 * PITCH + xcol(k1, 2 * m + col)]; };
+            auto zdir = [&](int k1) -> V {
+                const V wa = ld(k1, 0), wb = ld(k1, 1);
+                return V{wa.x - wb.y, wa.y + wb.x};
+            };
+            auto zmir = [&](int kp) -> V {
+                const V wa = ld(kp, 0), wb = ld(kp, 1);
+                return V{wa.x + wb.y, wb.x - wa.y};
+            };
+            if (s_on<R1>(t)) {
+                const int sa = s_a<R1>(t), sb = s_b<R1>(t), ma = R1 - t, mb = (t == 0) ? R1 / 2 : t;
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    pa[q] = (q < 4) ? zdir(sa + R1 * q) : zmir(ma + R1 * (7 - q));
+                    pb[q] = (q < 4) ? zdir(sb + R1 * q) : zmir(mb + R1 * (7 - q));
+                }
+            }
+            team_dft_dif<R1, true>(pa, pb, x, X, tw, t, [&](int s, int tt) { return cslot<N>(s, tt, m); });
+        }
+        int j2, j3;
+        plane_j(pl, n2, j2, j3);
+        double* Wp = a.W + filt * ntot + (long long)pl * N * N;
+        if (!UP) {
+#pragma unroll
+            for (int r = 0; r < R1; ++r) *reinterpret_cast<V*>(Wp + (long long)(t + 8 * r) * N + 2 * m) = x[r];
+            __syncthreads();
+            continue;
+        }
+        const double u2 = j2 - 0.5 * (n2 - 1), u3 = j3 - 0.5 * (n3 - 1);
+        const double u10 = t - 0.5 * (N - 1);
+        const double lgn = P[PL_LGN];
+        double S[2] = {0, 0}, Tm[2] = {0, 0}, U[2] = {0, 0};
+        auto emit = [&](int r, int e, double w) -> double {
+            const double u1 = fma(8.0, (double)r, u10);
+            const double wu = w * u1;
+            S[e] += w;
+            Tm[e] += wu;
+            U[e] = fma(wu, u1, U[e]);
+            return w;
+        };
+        bool rec = !a.range;
+        double Lr[2], Rr[2], Gr[2];
+        if (!a.range) {
+            const double* q = P + PL_LQ;
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const double u0 = (2 * m + e) - 0.5 * (N - 1);
+                const double c2 = q[5 + tri(1, 1)];
+                double c1 = fma(q[5 + tri(0, 1)], u0, q[2]);
+                double c0 = fma(u0, fma(q[5 + tri(0, 0)], u0, q[1]), q[0]);
+                c1 = fma(q[5 + tri(1, 2)], u2, c1);
+                c0 = fma(u2, fma(q[5 + tri(2, 2)], u2, fma(q[5 + tri(0, 2)], u0, q[3])), c0);
+                c1 = fma(q[5 + tri(1, 3)], u3, c1);
+                c0 = fma(u3, fma(q[5 + tri(3, 3)], u3, fma(q[5 + tri(2, 3)], u2, fma(q[5 + tri(0, 3)], u0, q[4]))),
+                         c0);
+                const double E0 = fma(-0.5, fma(u10, fma(c2, u10, c1), c0), lgn);
+                const double E1 = -0.5 * (8.0 * c1 + 16.0 * c2 * u10);
+                const double E2 = -32.0 * c2;
+                rec = rec && (fabs(E0) + (R1 - 1) * fabs(E1) + (R1 - 1) * (R1 - 1) * fabs(E2) < 650.0);
+                Lr[e] = exp_fast(E0);
+                Rr[e] = exp_fast(E1 + E2);
+                Gr[e] = exp_fast(2.0 * E2);
+            }
+        }
+        if (rec) {
+#pragma unroll
+            for (int r = 0; r < R1; ++r) {
+                const double o0 = emit(r, 0, x[r].x * Lr[0]);
+                const double o1 = emit(r, 1, x[r].y * Lr[1]);
+                Lr[0] *= Rr[0];
+                Rr[0] *= Gr[0];
+                Lr[1] *= Rr[1];
+                Rr[1] *= Gr[1];
+                *reinterpret_cast<V*>(Wp + (long long)(t + 8 * r) * N + 2 * m) = V{o0, o1};
+            }
+        } else {
+            const double* q = P + PL_LQ;
+#pragma unroll
+            for (int r = 0; r < R1; ++r) {
+                const double u1 = fma(8.0, (double)r, u10);
+                const double uu[4] = {0.0, u1, u2, u3};
+                double o[2];
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    double uv[4] = {(2 * m + e) - 0.5 * (N - 1), uu[1], uu[2], uu[3]};
+                    double ll;
+                    if (!a.range) {
+                        double ee = q[0];
+#pragma unroll
+                        for (int a2 = 0; a2 < NX; ++a2) {
+                            ee = fma(q[1 + a2], uv[a2], ee);
+#pragma unroll
+                            for (int b2 = a2; b2 < NX; ++b2) ee = fma(q[5 + tri(a2, b2)] * uv[a2], uv[b2], ee);
+                        }
+                        ll = fma(-0.5, ee, lgn);
+                    } else {
+                        double r2 = 0.0;
+#pragma unroll
+                        for (int a2 = 0; a2 < NX; ++a2) {
+                            double y = P[PL_CL + a2];
+#pragma unroll
+                            for (int b2 = 0; b2 < NX; ++b2) y = fma(P[PL_BL + a2 * 4 + b2], uv[b2], y);
+                            r2 = fma(y, y, r2);
+                        }
+                        const double d = (P[PL_ZR] - sqrt(r2)) * P[PL_ISG];
+                        ll = fma(-0.5 * d, d, lgn);
+                    }
+                    const double w = e == 0 ? x[r].x : x[r].y;
+                    o[e] = emit(r, e, w * exp_fast(ll));
+                }
+                *reinterpret_cast<V*>(Wp + (long long)(t + 8 * r) * N + 2 * m) = V{o[0], o[1]};
+            }
+        }
+        {
+            const double ua = (2 * m) - 0.5 * (N - 1), ub = ua + 1.0;
+            const double s0 = S[0] + S[1], su0 = fma(ua, S[0], ub * S[1]), st = Tm[0] + Tm[1];
+            const double m1[4] = {su0, st, u2 * s0, u3 * s0};
+            mom[0] += s0;
+#pragma unroll
+            for (int a2 = 0; a2 < NX; ++a2) mom[(1 + a2) * NT] += m1[a2];
+            int kk = 1 + NX;
+            const double uu[4] = {0.0, 0.0, u2, u3};
+#pragma unroll
+            for (int a2 = 0; a2 < NX; ++a2)
+#pragma unroll
+                for (int b2 = a2; b2 < NX; ++b2) {
+                    double v;
+                    if (a2 >= 2) v = uu[a2] * uu[b2] * s0;
+                    else if (b2 >= 2) v = uu[b2] * m1[a2];
+                    else if (a2 == 0 && b2 == 0) v = fma(ua * ua, S[0], ub * ub * S[1]);
+                    else if (a2 == 0) v = fma(ua, Tm[0], ub * Tm[1]);
+                    else v = U[0] + U[1];
+                    mom[(kk++) * NT] += v;
+                }
+        }
+        __syncthreads();                  // X is consumed
+    }
+    if (UP) flush();
+    (void)lane;
+    (void)warp;
+}
+
+}  // namespace pln
+
+using namespace pln;
+
+bool quad_supported(const Dims& d, int dtype) {
+    if (dtype != 0 || d.nx != 4 || d.n[0] != d.n[1] || d.n[2] != d.n[3]) return false;
+    const int N = d.n[0], NQ = d.n[2];
+    if (N != 32 && N != 64 && N != 96) return false;
+    if (NQ != 16 && NQ != 32 && NQ != 64 && NQ != 96) return false;
+    const char* e = std::getenv("PMF_NO_QUAD");
+    return !(e && e[0] == '1');
+}
+
+template <typename K>
+static cudaError_t q_grid(K kern, int nt, size_t smem, long long work, int* grid) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    int dev = 0, nsm = 148, occ = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, nt, smem);
+    if (e != cudaSuccess) return e;
+    if (occ < 1) return cudaErrorInvalidConfiguration;
+    *grid = (int)std::max(1LL, std::min(work, (long long)nsm * occ));
+    return cudaSuccess;
+}
+
+// Tensor map of the spectrum for K3's plane loads: doubles, dims (innermost first)
+// re/im 2, j2 n2, j3 n3, k0 N, (filter, k1) batch*H; box 2 x 1 x 1 x (N + 2) x H -- the
+// two k0 beyond N are out of range (zero-filled) and pad each shared-memory row to N + 2.
+static cudaError_t y_map(const QArgs& qa, int N, int H, CUtensorMap* m) {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    if (!encode) {
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&encode, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess || !encode) {
+            encode = nullptr;
+            return cudaErrorNotSupported;
+        }
+    }
+    const cuuint64_t n2 = qa.n2, n3 = qa.n3;
+    cuuint64_t dims[5] = {2, n2, n3, (cuuint64_t)N, (cuuint64_t)qa.batch * H};
+    cuuint64_t str[4] = {16, 16 * n2, 16 * n2 * n3, 16 * n2 * n3 * (cuuint64_t)N};
+    cuuint32_t box[5] = {2, 1, 1, (cuuint32_t)(N + 2), (cuuint32_t)H};
+    cuuint32_t es[5] = {1, 1, 1, 1, 1};
+    CUresult r = encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, (void*)qa.Y, dims, str, box, es,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
+template <int NQ, int TM>
+static cudaError_t qmid_tm(const QArgs& qa, int I, int N0, int H1, cudaStream_t s) {
+    using Cq = QCfg<NQ, TM>;
+    const size_t smem = qmid_smem<NQ>();
+    int grid = 1;
+    cudaError_t e = q_grid(k_q_mid<NQ, TM>, Cq::NT, smem, (long long)qa.batch * I, &grid);
+    if (e != cudaSuccess) return e;
+    k_q_mid<NQ, TM><<<grid, Cq::NT, smem, s>>>(qa, I, N0, H1);
+    return cudaGetLastError();
+}
+
+// (48 teams at NQ = 96 -- 12 warps, 168 registers -- measured 7 % slower than 32 teams)
+template <int NQ>
+static cudaError_t qmid_launch(const QArgs& qa, int I, int N0, int H1, cudaStream_t s) {
+    return qmid_tm<NQ, QCfg<NQ>::TEAMS>(qa, I, N0, H1, s);
+}
+
+// K1 -> K2 -> K3 (prep, the general-map pre-pass and the finaliser are the plane path's;
+// launch_plane calls this between them). Returns the K3 grid (its partials per filter).
+template <int N>
+static cudaError_t quad_n(const Dims& d, PencilBufs& b, QArgs qa, bool rg, bool up, cudaStream_t s, int64_t* launches,
+                          int* ginv) {
+    using Cf = Cfg<N>;
+    cudaError_t e;
+    {
+        const size_t smem = F1<N>::SMEM;
+        int grid = 1;
+        const long long units = (long long)d.batch * d.n[3] * (d.n[2] / 2);
+        if (rg) {
+            e = q_grid(k_q_fwd<N, true>, Cf::NT, smem, units, &grid);
+            if (e == cudaSuccess) k_q_fwd<N, true><<<grid, Cf::NT, smem, s>>>(qa);
+        } else {
+            e = q_grid(k_q_fwd<N, false>, Cf::NT, smem, units, &grid);
+            if (e == cudaSuccess) k_q_fwd<N, false><<<grid, Cf::NT, smem, s>>>(qa);
+        }
+        if (e != cudaSuccess) return e;
+        ++*launches;
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    }
+    if (b.ev0) cudaEventRecordWithFlags(b.ev0, s, cudaEventRecordExternal);
+    {
+        const int I = Cf::H * N;
+        switch (d.n[2]) {
+            case 16: e = qmid_launch<16>(qa, I, N, Cf::H, s); break;
+            case 32: e = qmid_launch<32>(qa, I, N, Cf::H, s); break;
+            case 64: e = qmid_launch<64>(qa, I, N, Cf::H, s); break;
+            case 96: e = qmid_launch<96>(qa, I, N, Cf::H, s); break;
+            default: e = cudaErrorInvalidValue;
+        }
+        if (e != cudaSuccess) return e;
+        ++*launches;
+    }
+    if (b.ev1) cudaEventRecordWithFlags(b.ev1, s, cudaEventRecordExternal);
+    {
+        CUtensorMap ymap;
+        if ((e = y_map(qa, N, Cf::H, &ymap)) != cudaSuccess) return e;
+        const size_t smem = qinv_smem<N>();
+        const long long nplanes = (long long)d.batch * d.n[2] * d.n[3];
+        if (up) {
+            e = q_grid(k_q_inv<N, true>, Cf::NT, smem, nplanes, ginv);
+            if (e == cudaSuccess && d.batch > 1)
+                e = cudaMemsetAsync(qa.part, 0, sizeof(double) * NMOM * (*ginv) * (size_t)d.batch, s);
+            if (e == cudaSuccess) k_q_inv<N, true><<<*ginv, Cf::NT, smem, s>>>(qa, ymap);
+        } else {
+            e = q_grid(k_q_inv<N, false>, Cf::NT, smem, nplanes, ginv);
+            if (e == cudaSuccess) k_q_inv<N, false><<<*ginv, Cf::NT, smem, s>>>(qa, ymap);
+        }
+        if (e != cudaSuccess) return e;
+        ++*launches;
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_quad(const Dims& d, PencilBufs& b, const ModelParams& mp, int range, bool rg, bool up,
+                        double* dcpart, double* dc3, double* part, cudaStream_t s, int64_t* launches, int* ginv) {
+    QArgs qa;
+    qa.Wsrc = (const double*)b.W;
+    qa.W2src = (const double*)b.W2;
+    qa.W = (double*)b.W;
+    qa.Y = (V*)b.S;
+    qa.coef = b.coef;
+    qa.cs = coef_stride(mp.l);
+    qa.dcpart = dcpart;
+    qa.dc3 = dc3;
+    qa.part = part;
+    qa.batch = d.batch;
+    qa.n2 = d.n[2];
+    qa.n3 = d.n[3];
+    qa.l = mp.l;
+    qa.step = mp.step;
+    qa.range = range;
+    switch (d.n[0]) {
+        case 32: return quad_n<32>(d, b, qa, rg, up, s, launches, ginv);
+        case 64: return quad_n<64>(d, b, qa, rg, up, s, launches, ginv);
+        case 96: return quad_n<96>(d, b, qa, rg, up, s, launches, ginv);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+}  // namespace pmf

@@ -26,20 +26,23 @@ CASES = {
     "C4_96x96x16x32": ("C4", {"n": (96, 96, 16, 32)}, 1),
     "C4_64x64x32x16": ("C4", {"n": (64, 64, 32, 16)}, 2),
     "C4_b2_32": ("C4", {"n": (32, 32, 16, 16), "batch": 2}, 2),
-    # n2 = n3: the fused (2,3)-plane pass (split regrid + axis 2/3 DFTs + Psi in one kernel)
+    # n2 = n3, fp64: the three-pass transposed-spectrum route (kernels_quad.cu)
     "C4_32x32x32x32": ("C4", {"n": (32, 32, 32, 32)}, 2),
     "C4_32x32x64x64": ("C4", {"n": (32, 32, 64, 64)}, 1),
     "C4_32x32x96x96": ("C4", {"n": (32, 32, 96, 96)}, 1),
+    "C4_64x64x16x16": ("C4", {"n": (64, 64, 16, 16)}, 2),
+    "C4_96x96x16x16": ("C4", {"n": (96, 96, 16, 16)}, 2),
+    "C4_b3_96x96x32x32": ("C4", {"n": (96, 96, 32, 32), "batch": 3}, 1),
 }
 
 
-FUSED = ("C4_32x32x16x16", "C4_b2_32", "C4_32x32x32x32", "C4_32x32x64x64", "C4_32x32x96x96")
+QUAD = ("C4_32x32x16x16", "C4_b2_32", "C4_32x32x32x32", "C4_96x96x16x16", "C4_b3_96x96x32x32")
 
 
 @pytest.fixture
-def fused23(monkeypatch):
-    """Opt into the fused (2,3)-plane pass (read by the library on every call)."""
-    monkeypatch.setenv("PMF_PLANE_FUSED23", "1")
+def five_pass(monkeypatch):
+    """Force the per-plane-layout five-pass route (read by the library on every call)."""
+    monkeypatch.setenv("PMF_NO_QUAD", "1")
 
 
 @pytest.mark.parametrize("name", list(CASES))
@@ -55,16 +58,27 @@ def test_plane_run_parity_f64(name):
     assert e["mean"] <= 1e-10 and e["cov"] <= 1e-10 and e["logC"] <= 1e-10 and e["grid"] <= 1e-10, e
 
 
-@pytest.mark.parametrize("name", FUSED)
-def test_plane_fused23_parity_f64(name, fused23):
-    """n2 = n3: one fused pass (split regrid + axis-2/3 DFTs + Psi) replaces the three
-    strided passes; same bar against the oracle."""
+@pytest.mark.parametrize("name", QUAD)
+def test_plane_five_pass_parity_f64(name, five_pass):
+    """The per-plane-layout five-pass route (the fallback for shapes the three-pass route
+    does not take) on the three-pass route's shapes: same bar against the oracle."""
     test_plane_run_parity_f64(name)
 
 
-@pytest.mark.parametrize("name", ["C4_32x32x16x16", "C4_32x32x32x32"])
-def test_plane_fused23_parity_f32(name, fused23):
-    test_plane_run_parity_f32(name)
+@pytest.mark.parametrize("name", ["C4_32x32x16x16", "C4_96x96x16x16"])
+def test_plane_three_vs_five_pass(name, monkeypatch):
+    """The two nx = 4 routes agree to rounding (1e-12) on weights, moments and normaliser."""
+    cid, over, T = CASES[name]
+    cfg = make_config(cid, **over)
+    zs = simulate(cfg, T=T)["z"]
+    a = run_gpu(cfg, zs, T, path=pmf.PATH_PLANE)
+    monkeypatch.setenv("PMF_NO_QUAD", "1")
+    b = run_gpu(cfg, zs, T, path=pmf.PATH_PLANE)
+    wa, wb = a["filter"].weights(), b["filter"].weights()
+    assert float(np.max(np.abs(wa - wb)) / np.max(np.abs(wb))) < 1e-12
+    for k in range(T + 1):
+        assert np.max(np.abs(a["mean"][k] - b["mean"][k])) < 1e-12
+        assert abs(float(a["logC"][k][0]) - float(b["logC"][k][0])) < 1e-12
 
 
 @pytest.mark.parametrize("name", ["C3_32x32x16", "C4_32x32x16x16", "C4_32x32x32x32"])
