@@ -32,7 +32,8 @@
  *
  * ERRORS: every int-returning call returns PMF_OK (0) or a negative PMF_E_*
  * code; pmf_last_error() gives a message. A failed call leaves the context
- * unchanged unless the code is PMF_E_CUDA (the context is then unusable).
+ * unchanged unless the code is PMF_E_CUDA or PMF_E_NCCL (the context is then
+ * unusable).
  * There is no CPU fallback: the library requires a CUDA device (sm_100a).
  */
 #ifndef PMF_H
@@ -60,6 +61,9 @@ extern "C" {
 #define PMF_E_STATE         -8  /* call out of order (e.g. predict before a density was set)                     */
 #define PMF_E_CUDA          -9  /* CUDA runtime failure or no usable device                                        */
 #define PMF_E_NOMEM        -10  /* device allocation failed                                                        */
+#define PMF_E_NCCL         -11  /* NCCL failure (sharded contexts): libnccl.so.2 missing, communicator init, a     */
+                                /* collective's enqueue, or an asynchronous communicator error (polled with      */
+                                /* ncclCommGetAsyncError after every exchange); the context is then unusable      */
 
 /* enums */
 #define PMF_F64 0
@@ -232,7 +236,7 @@ int pmf_step(pmf_ctx* ctx, double dt, int steps, const double* z, int z_on_devic
  *
  * pmf_nccl_unique_id: rank 0 creates the NCCL id (128 bytes) that every rank
  * passes to pmf_create_sharded (broadcast it, e.g. with torch.distributed).
- * libnccl.so.2 is loaded on first use (dlopen); PMF_E_CUDA if unavailable.
+ * libnccl.so.2 is loaded on first use (dlopen); PMF_E_NCCL if unavailable.
  *
  * pmf_create_sharded: cfg->n are the GLOBAL sizes. unique_id != NULL: this
  * process is `rank` of `world` (one GPU each, NCCL over NVLink). unique_id ==

@@ -27,9 +27,17 @@ struct GraphKey {
     int path, predict, steps, regrid, has_lp, prof, diff_mode, pad;
     double dt, k_sigma;
     pmf::LikParams lp;
+    // every device pointer a captured kernel takes as an argument: a reallocation (e.g.
+    // prepare_model growing sub / coef for more substeps) must miss the cache
     void* W;
     void* W2;
     void* S;
+    void* S2;
+    void* sub;
+    void* coef;
+    void* terrain;
+    void* partials;
+    void* z;
 };
 struct GraphEntry {
     GraphKey key;
@@ -65,6 +73,12 @@ struct pmf_ctx {
     pmf::SubstepEntry* sub = nullptr;
     size_t sub_bytes = 0;
     double* z = nullptr;
+    // pinned staging of host measurements (pmf_update/pmf_step with z in host memory): the
+    // caller's array is copied on the host during the call, the H2D copy reads the staging
+    // slot; a slot is reused only after its previous copy completed (event)
+    double* z_stage[2] = {nullptr, nullptr};
+    cudaEvent_t z_ev[2] = {nullptr, nullptr};
+    int z_slot = 0;
     double* gauss = nullptr;
     double* mom_dev = nullptr;       // compact moments [batch][nx + nx^2 + 2]
     double* mom_host = nullptr;      // pinned host mirror

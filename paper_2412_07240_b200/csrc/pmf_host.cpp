@@ -303,11 +303,28 @@ static int make_lik(pmf_ctx* c, const pmf_likelihood* lik, LikParams& lp) {
     return PMF_OK;
 }
 
+// The caller's z is read during the call only (pmf.h OWNERSHIP): host arrays are copied
+// into a context-owned pinned staging slot (double-buffered, each slot fenced by an event)
+// and the asynchronous H2D copy reads that slot, never the caller's memory after return.
 static int upload_z(pmf_ctx* c, const double* z, int on_device, int nz) {
     if (!z) return fail(c, PMF_E_ARG, "z is NULL");
     size_t bytes = sizeof(double) * nz * (size_t)c->d.batch;
-    CK(c, cudaMemcpyAsync(c->z, z, bytes, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
-                          c->stream), "upload z");
+    if (on_device) {
+        CK(c, cudaMemcpyAsync(c->z, z, bytes, cudaMemcpyDeviceToDevice, c->stream), "upload z");
+        return PMF_OK;
+    }
+    const int k = c->z_slot;
+    if (!c->z_stage[k]) {
+        CK(c, cudaMallocHost((void**)&c->z_stage[k], sizeof(double) * PMF_MAX_NZ * (size_t)c->d.batch),
+           "cudaMallocHost (z staging)");
+        CK(c, cudaEventCreateWithFlags(&c->z_ev[k], cudaEventDisableTiming), "z staging event");
+    } else {
+        CK(c, cudaEventSynchronize(c->z_ev[k]), "z staging slot reuse");   // its previous copy is done
+    }
+    std::memcpy(c->z_stage[k], z, bytes);
+    CK(c, cudaMemcpyAsync(c->z, c->z_stage[k], bytes, cudaMemcpyHostToDevice, c->stream), "upload z");
+    CK(c, cudaEventRecord(c->z_ev[k], c->stream), "z staging event");
+    c->z_slot ^= 1;
     return PMF_OK;
 }
 
@@ -447,6 +464,12 @@ static void graph_key(const pmf_ctx* c, const LikParams* lp, GraphKey& k) {
     k.W = c->W;
     k.W2 = c->W2;
     k.S = c->S;
+    k.S2 = c->S2;
+    k.sub = c->sub;
+    k.coef = c->coef;
+    k.terrain = c->terrain;
+    k.partials = c->partials;
+    k.z = c->z;
 }
 
 static int flush(pmf_ctx* c, const LikParams* lp) {
@@ -741,6 +764,10 @@ void pmf_destroy(pmf_ctx* c) {
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (c->mom_host) cudaFreeHost(c->mom_host);
+    for (int k = 0; k < 2; ++k) {
+        if (c->z_stage[k]) cudaFreeHost(c->z_stage[k]);
+        if (c->z_ev[k]) cudaEventDestroy(c->z_ev[k]);
+    }
     for (cudaEvent_t e : c->evs) cudaEventDestroy(e);
     delete c;
 }
@@ -829,6 +856,8 @@ int pmf_predict(pmf_ctx* c, double dt, int steps) {
         int r = flush(c, nullptr);
         if (r) return r;
     }
+    if (c->cfg.diff_mode == PMF_DIFF_FDM && !c->sh && !fdm_supported(c->d, c->dtype, steps))
+        return fail(c, PMF_E_DT, "FDM predictor: at most 64 substeps per predict");
     int r = prepare_model(c, dt, steps);
     if (r) return r;
     c->pend.predict = true;

@@ -46,6 +46,7 @@ struct NcclApi {
     Res (*AllReduce)(const void*, void*, size_t, int, int, Comm, cudaStream_t) = nullptr;
     Res (*GroupStart)() = nullptr;
     Res (*GroupEnd)() = nullptr;
+    Res (*CommGetAsyncError)(Comm, Res*) = nullptr;
     const char* (*GetErrorString)(Res) = nullptr;
     bool ok = false;
     std::string why;
@@ -70,13 +71,22 @@ struct NcclApi {
         a.GroupStart = (Res(*)())sym("ncclGroupStart");
         a.GroupEnd = (Res(*)())sym("ncclGroupEnd");
         a.GetErrorString = (const char* (*)(Res))sym("ncclGetErrorString");
+        a.CommGetAsyncError = (Res(*)(Comm, Res*))sym("ncclCommGetAsyncError");
         a.ok = a.GetUniqueId && a.CommInitRank && a.CommDestroy && a.Send && a.Recv && a.AllReduce && a.GroupStart &&
-               a.GroupEnd;
+               a.GroupEnd && a.CommGetAsyncError;
         if (!a.ok) a.why = "libnccl.so.2 lacks a required symbol";
         return a;
     }
 };
-constexpr int NCCL_INT8 = 0, NCCL_FLOAT64 = 8, NCCL_SUM = 0;
+constexpr int NCCL_INT8 = 0, NCCL_FLOAT64 = 8, NCCL_SUM = 0, NCCL_IN_PROGRESS = 7;
+
+// an NCCL call's failure (r != 0), with the library's message
+static int nccl_fail(pmf_ctx* c, int r, const char* what) {
+    NcclApi& api = NcclApi::get();
+    std::string m = std::string(what) + " failed";
+    if (api.GetErrorString) m += std::string(": ") + api.GetErrorString(r);
+    return pmf_fail(c, PMF_E_NCCL, m);
+}
 
 struct Shard {
     int rank = 0;
@@ -118,6 +128,16 @@ struct ShardSet {
 }  // namespace pmf
 
 // ============================================================================ exchanger
+// asynchronous communicator errors (a peer died, a network/NVLink fault): polled after
+// every enqueued exchange -- non-blocking; ncclInProgress is not an error
+static int nccl_poll(pmf_ctx* c) {
+    NcclApi& api = NcclApi::get();
+    int ae = 0;
+    if (int r = api.CommGetAsyncError(c->sh->comm, &ae)) return nccl_fail(c, r, "ncclCommGetAsyncError");
+    if (ae != 0 && ae != NCCL_IN_PROGRESS) return nccl_fail(c, ae, "NCCL communicator (asynchronous error)");
+    return PMF_OK;
+}
+
 static int exchange(pmf_ctx* c, const std::vector<Xfer>& xs, void* (*sbuf)(Shard&), void* (*rbuf)(Shard&)) {
     ShardSet& S = *c->sh;
     if (S.virt) {
@@ -142,14 +162,14 @@ static int exchange(pmf_ctx* c, const std::vector<Xfer>& xs, void* (*sbuf)(Shard
             if (e != cudaSuccess) { api.GroupEnd(); return pmf_cuda_fail(c, e, "local exchange"); }
         } else if (x.src == S.rank) {
             int r = api.Send((char*)sbuf(me) + x.so, x.bytes, NCCL_INT8, x.dst, S.comm, c->stream);
-            if (r) { api.GroupEnd(); return pmf_fail(c, PMF_E_CUDA, "ncclSend failed"); }
+            if (r) { api.GroupEnd(); return nccl_fail(c, r, "ncclSend"); }
         } else if (x.dst == S.rank) {
             int r = api.Recv((char*)rbuf(me) + x.dof, x.bytes, NCCL_INT8, x.src, S.comm, c->stream);
-            if (r) { api.GroupEnd(); return pmf_fail(c, PMF_E_CUDA, "ncclRecv failed"); }
+            if (r) { api.GroupEnd(); return nccl_fail(c, r, "ncclRecv"); }
         }
     }
-    if (api.GroupEnd()) return pmf_fail(c, PMF_E_CUDA, "ncclGroupEnd failed");
-    return PMF_OK;
+    if (int r = api.GroupEnd()) return nccl_fail(c, r, "ncclGroupEnd");
+    return nccl_poll(c);
 }
 
 // sum of the shards' tot[0..NMOM) over ranks, written back to every shard
@@ -157,9 +177,9 @@ static int allreduce_tot(pmf_ctx* c) {
     ShardSet& S = *c->sh;
     if (!S.virt) {
         NcclApi& api = NcclApi::get();
-        if (api.AllReduce(S.sh[0].tot, S.sh[0].tot, NMOM, NCCL_FLOAT64, NCCL_SUM, S.comm, c->stream))
-            return pmf_fail(c, PMF_E_CUDA, "ncclAllReduce failed");
-        return PMF_OK;
+        if (int r = api.AllReduce(S.sh[0].tot, S.sh[0].tot, NMOM, NCCL_FLOAT64, NCCL_SUM, S.comm, c->stream))
+            return nccl_fail(c, r, "ncclAllReduce");
+        return nccl_poll(c);
     }
     // virtual: host-free reduction in rank order -- gather, sum on device, scatter
     for (int r = 0; r < S.world; ++r) {
@@ -211,9 +231,9 @@ static int finalize_all(pmf_ctx* c, int mode, double ks) {
 extern "C" int pmf_nccl_unique_id(void* out128) {
     if (!out128) return pmf_fail(nullptr, PMF_E_ARG, "null argument");
     NcclApi& api = NcclApi::get();
-    if (!api.ok) return pmf_fail(nullptr, PMF_E_CUDA, api.why);
+    if (!api.ok) return pmf_fail(nullptr, PMF_E_NCCL, api.why);
     NcclApi::UniqueId id;
-    if (api.GetUniqueId(&id)) return pmf_fail(nullptr, PMF_E_CUDA, "ncclGetUniqueId failed");
+    if (int r = api.GetUniqueId(&id)) return nccl_fail(nullptr, r, "ncclGetUniqueId");
     std::memcpy(out128, &id, sizeof(id));
     return PMF_OK;
 }
@@ -278,11 +298,15 @@ extern "C" int pmf_create_sharded(const pmf_config* cfg, const double* A, const 
     };
     if (!virt) {
         NcclApi& api = NcclApi::get();
-        if (!api.ok) fail(PMF_E_CUDA, api.why);
+        if (!api.ok) fail(PMF_E_NCCL, api.why);
         else {
             NcclApi::UniqueId id;
             std::memcpy(&id, unique_id, sizeof(id));
-            if (api.CommInitRank(&S->comm, world, id, rank)) fail(PMF_E_CUDA, "ncclCommInitRank failed");
+            if (int r = api.CommInitRank(&S->comm, world, id, rank)) {
+                const std::string m = std::string("ncclCommInitRank failed") +
+                                      (api.GetErrorString ? std::string(": ") + api.GetErrorString(r) : "");
+                fail(PMF_E_NCCL, m);
+            }
         }
     }
     const int nshards = virt ? world : 1;

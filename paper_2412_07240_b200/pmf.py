@@ -19,7 +19,7 @@ LIB_PATH = os.path.join(_HERE, "libpmf.so")
 PMF_OK = 0
 ERRORS = {-1: "PMF_E_ARG", -2: "PMF_E_ODD_N", -3: "PMF_E_RADIX", -4: "PMF_E_Q_NOT_PSD",
           -5: "PMF_E_SINGULAR_GRID", -6: "PMF_E_NO_SUPPORT", -7: "PMF_E_DT", -8: "PMF_E_STATE",
-          -9: "PMF_E_CUDA", -10: "PMF_E_NOMEM"}
+          -9: "PMF_E_CUDA", -10: "PMF_E_NOMEM", -11: "PMF_E_NCCL"}
 F64, F32 = 0, 1
 DIFF_FULL, DIFF_AXIS_LITERAL, DIFF_FDM = 0, 1, 2
 STEP_EULER, STEP_CN = 0, 1
@@ -122,6 +122,33 @@ def _dptr(a: np.ndarray):
     return a.ctypes.data_as(C.POINTER(C.c_double))
 
 
+def _arg_error(msg: str) -> PMFError:
+    return PMFError(-1, msg)
+
+
+def _check_device_tensor(t, device: int, dtype, min_numel: int, what: str):
+    """A torch tensor handed to the library as a raw device pointer: it must live on the
+    context's CUDA device, have the expected dtype, be contiguous and hold at least
+    min_numel elements -- anything else would be read or written out of bounds."""
+    if not getattr(t, "is_cuda", False):
+        raise _arg_error(f"{what}: expected a CUDA tensor on cuda:{device}, got device {getattr(t, 'device', '?')}")
+    if t.device.index != device:
+        raise _arg_error(f"{what}: tensor is on cuda:{t.device.index}, the filter on cuda:{device}")
+    if t.dtype != dtype:
+        raise _arg_error(f"{what}: dtype {t.dtype}, expected {dtype}")
+    if not t.is_contiguous():
+        raise _arg_error(f"{what}: tensor must be contiguous")
+    if t.numel() < min_numel:
+        raise _arg_error(f"{what}: {t.numel()} elements, need {min_numel}")
+
+
+def _check_host_array(a, shape, what: str):
+    """A numpy array the library writes into: float64, C-contiguous, exactly `shape`."""
+    if not isinstance(a, np.ndarray) or a.dtype != np.float64 or not a.flags.c_contiguous or \
+            tuple(a.shape) != tuple(shape):
+        raise _arg_error(f"{what}: need a C-contiguous float64 array of shape {tuple(shape)}")
+
+
 def make_likelihood(kind: int, nx: int, H=None, R=None, sigma: float = 0.0, gm=None) -> pmf_likelihood:
     """gm (TERRAIN_GM): sequence of (weight, mean, variance) noise components."""
     lk = pmf_likelihood()
@@ -159,6 +186,7 @@ class Filter:
         process is `rank` over NCCL; without it all slabs are "virtual ranks" here."""
         self.lib = load_library()
         self.nx, self.n, self.batch = nx, tuple(int(v) for v in n), batch
+        self.device = int(device)
         self.dtype = dtype
         self.np_dtype = np.float64 if dtype == "f64" else np.float32
         cfg = pmf_config()
@@ -223,6 +251,7 @@ class Filter:
         center = np.ascontiguousarray(np.asarray(center, dtype=np.float64).reshape(self.batch, self.nx))
         B = np.ascontiguousarray(np.asarray(B, dtype=np.float64).reshape(self.batch, self.nx, self.nx))
         if hasattr(weights, "data_ptr"):      # torch tensor on the device
+            _check_device_tensor(weights, self.device, self._torch_dtype(), self.batch * self.ntot, "set_state weights")
             self._check(self.lib.pmf_set_state(self.h, _dptr(center), _dptr(B), C.c_void_p(weights.data_ptr()), 1))
         else:
             w = np.ascontiguousarray(np.asarray(weights, dtype=self.np_dtype).reshape(-1))
@@ -231,14 +260,25 @@ class Filter:
     def predict(self, dt: float, steps: int):
         self._check(self.lib.pmf_predict(self.h, float(dt), int(steps)))
 
-    def _z(self, z):
+    def _torch_dtype(self):
+        import torch
+        return torch.float64 if self.dtype == "f64" else torch.float32
+
+    def _z(self, z, lik: pmf_likelihood):
+        need = self.batch * int(lik.nz)
         if hasattr(z, "data_ptr"):
-            return C.c_void_p(z.data_ptr()), 1, z
+            if getattr(z, "is_cuda", False):
+                import torch
+                _check_device_tensor(z, self.device, torch.float64, need, "z")
+                return C.c_void_p(z.data_ptr()), 1, z
+            z = z.numpy()                     # a CPU tensor: passed as host memory
         zz = np.ascontiguousarray(np.asarray(z, dtype=np.float64).reshape(-1))
+        if zz.size < need:
+            raise _arg_error(f"z: {zz.size} values, need batch x nz = {need}")
         return zz.ctypes.data_as(C.c_void_p), 0, zz
 
     def update(self, z, lik: pmf_likelihood):
-        p, dev, keep = self._z(z)
+        p, dev, keep = self._z(z, lik)
         self._check(self.lib.pmf_update(self.h, p, dev, C.byref(lik)))
         del keep
 
@@ -246,7 +286,7 @@ class Filter:
         self._check(self.lib.pmf_regrid(self.h, float(k_sigma)))
 
     def step(self, dt: float, steps: int, z, lik: pmf_likelihood, k_sigma: float):
-        p, dev, keep = self._z(z)
+        p, dev, keep = self._z(z, lik)
         self._check(self.lib.pmf_step(self.h, float(dt), int(steps), p, dev, C.byref(lik), float(k_sigma)))
         del keep
 
@@ -258,6 +298,9 @@ class Filter:
         return mean, cov, logc
 
     def moments_into(self, mean: np.ndarray, cov: np.ndarray, logc: np.ndarray):
+        _check_host_array(mean, (self.batch, self.nx), "mean")
+        _check_host_array(cov, (self.batch, self.nx, self.nx), "cov")
+        _check_host_array(logc, (self.batch,), "logc")
         self._check(self.lib.pmf_moments(self.h, _dptr(mean), _dptr(cov), _dptr(logc)))
 
     def weights(self) -> np.ndarray:
@@ -268,6 +311,7 @@ class Filter:
 
     def weights_to(self, tensor):
         """Write the normalised densities into a device tensor (torch)."""
+        _check_device_tensor(tensor, self.device, self._torch_dtype(), self.batch * self.ntot, "weights_to")
         self._check(self.lib.pmf_get_weights(self.h, C.c_void_p(tensor.data_ptr()), 1))
 
     def grid(self):
@@ -310,7 +354,18 @@ class Filter:
         """Enqueue the last update's moments into ``dst`` (pinned host memory, a torch tensor
         or numpy array of moments_bytes bytes): records of (nx + nx^2 + 2) doubles per
         filter -- mean, cov, log normaliser, failure flag. Read after sync()."""
-        ptr = dst.data_ptr() if hasattr(dst, "data_ptr") else dst.ctypes.data
+        need = self.moments_bytes
+        if hasattr(dst, "data_ptr"):
+            import torch
+            if dst.is_cuda or dst.dtype != torch.float64 or not dst.is_contiguous() or \
+                    dst.numel() * 8 < need:
+                raise _arg_error(f"moments_async: need a contiguous float64 host tensor of >= {need} bytes")
+            ptr = dst.data_ptr()
+        else:
+            if not isinstance(dst, np.ndarray) or dst.dtype != np.float64 or not dst.flags.c_contiguous or \
+                    dst.nbytes < need:
+                raise _arg_error(f"moments_async: need a C-contiguous float64 array of >= {need} bytes")
+            ptr = dst.ctypes.data
         self._check(self.lib.pmf_moments_async(self.h, C.c_void_p(ptr)))
 
     @property

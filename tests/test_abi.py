@@ -84,7 +84,22 @@ def test_binding_constants_match_header():
     paths = _header_defines("PMF_PATH_")
     assert (paths["PMF_PATH_AUTO"], paths["PMF_PATH_PENCIL"], paths["PMF_PATH_RESIDENT"],
             paths["PMF_PATH_PLANE"]) == (pmf.PATH_AUTO, pmf.PATH_PENCIL, pmf.PATH_RESIDENT, pmf.PATH_PLANE)
+    errs = _header_defines("PMF_E_")
+    assert {v: k for k, v in errs.items()} == pmf.ERRORS
     grids = _header_defines("PMF_GRID_")
     assert (grids["PMF_GRID_AXIS"], grids["PMF_GRID_EIGEN"]) == (pmf.GRID_AXIS, pmf.GRID_EIGEN)
     lib = pmf.load_library()
     assert lib.pmf_epoch_kernel(None) == -1 and lib.pmf_path(None) == -1
+
+
+def test_binding_validates_buffers():
+    """Raw pointers are only taken from buffers of the right device, dtype, layout and size
+    (ADVICE r1): a CPU tensor never reaches the library as a device pointer, and host
+    output arrays must be float64, C-contiguous and of the exact shape."""
+    import torch
+    with pytest.raises(pmf.PMFError):
+        pmf._check_device_tensor(torch.zeros(8, dtype=torch.float64), 0, torch.float64, 8, "x")
+    pmf._check_host_array(np.zeros((3, 2)), (3, 2), "mean")
+    for bad in (np.zeros((3, 2), dtype=np.float32), np.zeros((2, 3)).T, np.zeros((3, 3)), [[0.0] * 2] * 3):
+        with pytest.raises(pmf.PMFError):
+            pmf._check_host_array(bad, (3, 2), "mean")

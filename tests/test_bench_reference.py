@@ -19,7 +19,8 @@ def test_reference_arm_json_line():
     assert d["impl"] == "reference"
     assert d["metric"] == "grid-point FPE updates/sec (fp64)" and d["unit"] == "grid-point updates/s"
     assert d["value"] > 0 and d["higher_is_better"] is True and d["steps"] == 2 and d["warmup"] == 1
-    assert d["config"]["workload"].startswith("C1: 1 x 64 1-D filters per GPU, l=10")
+    assert d["config"]["workload"].startswith("C1: 1 x 64 1-D filters, l=10")
+    assert 0 < d["ms_per_step"] < 60e3   # the measured time of one step's sampled oracle work
     cb = d["cpu_baseline"]
     assert cb["kind"] == "oracle" and cb["cores"] >= 1 and cb["value"] == d["value"] and cb["sample"]
     assert d["e2e"] == {"value": d["value"], "unit": d["unit"], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}

@@ -252,6 +252,33 @@ def test_graph_replay_bitwise_equal(cid, over):
     assert a[4] == b[4]
 
 
+@pytest.mark.parametrize("cid,over", [("C5", {"batch": 3}), ("C4", {"n": (32, 32, 16, 16)}), ("C3", {"n": (16, 12, 24)})])
+def test_graph_replay_varying_substeps(cid, over):
+    """Graphs captured at l = 10 are not replayed after a predict with more substeps
+    reallocated the substep table and coefficient buffers: l = 10 -> 100 -> 10
+    with graphs on equals graphs off, bit for bit."""
+    import torch
+    cfg = make_config(cid, **over)
+    T = 3
+    zs = simulate(cfg, T=T)["z"]
+    lik = lik_of(cfg)
+    outs = []
+    for graphs in (True, False):
+        s = torch.cuda.Stream()
+        f = pmf.Filter(cfg.nx, cfg.n, cfg.A, cfg.Q, batch=cfg.batch, stream=s.cuda_stream)
+        f.use_graphs(graphs)
+        f.set_gaussian(cfg.prior_mean, np.broadcast_to(cfg.prior_cov, (cfg.batch, cfg.nx, cfg.nx)), cfg.k_sigma)
+        f.update(zs[0], lik)
+        f.regrid(cfg.k_sigma)
+        for k, l in zip(range(1, T + 1), (10, 100, 10)):
+            f.step(cfg.tau / l, l, zs[k], lik, cfg.k_sigma)
+        mean, cov, logc = f.moments()
+        outs.append((f.weights(), mean, cov, logc))
+        f.close()
+    a, b = outs
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1]) and np.array_equal(a[3], b[3])
+
+
 @pytest.mark.parametrize("name", ["C1", "C2s", "C3s", "C4s", "C5s", "C3_plane_32", "C4_plane_32", "C5_resident",
                                   "C5_resident_step"])
 def test_crank_nicolson_parity(name):
