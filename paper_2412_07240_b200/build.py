@@ -23,7 +23,7 @@ HEADERS = ["plane_common.cuh", "pmf_internal.h", "pmf_ctx_impl.h", "device_commo
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "--expt-relaxed-constexpr",
-         "-Xptxas", "-warn-spills"]
+         "-Xptxas", "-warn-spills"] + os.environ.get("PMF_NVCC_EXTRA", "").split()
 
 
 def _stale(obj: str, deps: list[str]) -> bool:
@@ -37,6 +37,13 @@ def build(force: bool = False, verbose: bool = False) -> str:
     hdrs = [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(ROOT, "include", "pmf.h")]
     objdir = os.path.join(HERE, "build_obj")
     os.makedirs(objdir, exist_ok=True)
+    # a change of the compiler flags (e.g. PMF_NVCC_EXTRA) rebuilds everything
+    stamp = os.path.join(objdir, "flags.txt")
+    flags = " ".join([NVCC, *ARCH, *FLAGS])
+    if not os.path.exists(stamp) or open(stamp).read() != flags:
+        force = True
+        with open(stamp, "w") as fh:
+            fh.write(flags)
     objs, cmds = [], []
     for src in SOURCES:
         sp = os.path.join(CSRC, src)

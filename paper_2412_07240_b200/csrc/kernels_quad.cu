@@ -43,6 +43,20 @@ namespace pln {
 
 using V = double2;
 
+// Phase cycle counters (debug builds with -DPMF_QPROF only): thread 0 of every CTA adds the
+// clock64() deltas of its phases; read with pmf_debug_counters (tools/qprof.py).
+__device__ unsigned long long g_qprof[16];
+#ifdef PMF_QPROF
+#define QPROF_T(v) \
+    __syncthreads();  \
+    const long long v = clock64()
+#define QPROF_ADD(i, a, b) \
+    if (threadIdx.x == 0) atomicAdd(&g_qprof[i], (unsigned long long)((b) - (a)))
+#else
+#define QPROF_T(v)
+#define QPROF_ADD(i, a, b)
+#endif
+
 struct QArgs {
     const double* Wsrc;      // weights read by K1 (old grid when regridding)
     const double* W2src;     // pre-regridded weights (general regrid map, flag 2)
@@ -67,7 +81,7 @@ struct QArgs {
 // mbarrier. At N = 96: 2 x 76.8 KB + 75.3 KB + 1.5 KB = 230.5 KB.
 template <int N> struct F1 {
     static constexpr int SP2 = N + 2;
-    static constexpr size_t XB = sizeof(V) * Cfg<N>::H * Cfg<N>::PITCH;
+    static constexpr size_t XB = (sizeof(V) * Cfg<N>::H * Cfg<N>::PITCH + 127) / 128 * 128;   // TMA: 128-B aligned
     static constexpr size_t SB = sizeof(double) * N * SP2 + 16;
     static constexpr size_t SMEM = 2 * XB + SB + sizeof(V) * N + 16;
     static constexpr int MINB = SMEM <= 113 * 1024 ? 2 : 1;
@@ -140,10 +154,10 @@ template <int N, bool RG>
 __global__ void __launch_bounds__(Cfg<N>::NT, F1<N>::MINB) k_q_fwd(QArgs a) {
     using C = Cfg<N>;
     constexpr int R1 = C::R1, H = C::H, PITCH = C::PITCH, NT = C::NT, SP2 = F1<N>::SP2;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
+    extern __shared__ __align__(128) unsigned char smem_raw[];
     V* XA = reinterpret_cast<V*>(smem_raw);
-    V* XB = XA + H * PITCH;
-    double* stg = reinterpret_cast<double*>(XB + H * PITCH) + 2;   // after the zero guard
+    V* XB = reinterpret_cast<V*>(smem_raw + F1<N>::XB);
+    double* stg = reinterpret_cast<double*>(smem_raw + 2 * F1<N>::XB) + 2;   // after the zero guard
     V* tw = reinterpret_cast<V*>(stg + N * SP2);
     unsigned long long* bar = reinterpret_cast<unsigned long long*>(tw + N);
     const int tid = threadIdx.x, m = tid >> 3, t = tid & 7;
@@ -186,7 +200,10 @@ __global__ void __launch_bounds__(Cfg<N>::NT, F1<N>::MINB) k_q_fwd(QArgs a) {
         const bool skip = P[PL_SKIP] != 0.0;
 #pragma unroll 1
         for (int h = 0; h < 2; ++h, ++k) {
+            QPROF_T(p0);
             tma::mbar_wait(bar, (unsigned)(k & 1));
+            QPROF_T(p1);
+            QPROF_ADD(6, p0, p1);
             V z[R1];
             if (RG && flag == 4) {
                 // in-plane part of the split regrid map (R12): bilinear from the staged old
@@ -227,6 +244,8 @@ __global__ void __launch_bounds__(Cfg<N>::NT, F1<N>::MINB) k_q_fwd(QArgs a) {
                 for (int r = 0; r < R1; ++r) z[r] = *reinterpret_cast<const V*>(stg + (t + 8 * r) * SP2 + 2 * m);
             }
             __syncthreads();                                  // staged plane consumed
+            QPROF_T(p2);
+            QPROF_ADD(7, p1, p2);
             if (h == 0) issue(f, j3 * n2 + j2 + 1);
             else if (u + (int)gridDim.x < units) {
                 int f2, j32, j22;
@@ -235,9 +254,14 @@ __global__ void __launch_bounds__(Cfg<N>::NT, F1<N>::MINB) k_q_fwd(QArgs a) {
             }
             if (skip) continue;                               // uniform
             fwd_plane<N>(h ? XB : XA, z, tw, m, t);
+            QPROF_T(p3);
+            QPROF_ADD(8, p2, p3);
         }
+        QPROF_T(p4);
         if (skip) continue;
         // both planes' coefficients (k1, k0) as one 32-byte store each: Y[f][k1][k0][j3][j2, j2+1]
+        // (measured: a tensor-map TMA store per plane -- 16-byte elements -- is bound by the TMA
+        // unit at ~8 B/clk per SM and slower than these 32-byte stores)
         if (tid == 0) {
             a.dcpart[(long long)f * ppf + j3 * n2 + j2] = XA[0].x;      // sums of the input planes
             a.dcpart[(long long)f * ppf + j3 * n2 + j2 + 1] = XB[0].x;
@@ -252,6 +276,9 @@ __global__ void __launch_bounds__(Cfg<N>::NT, F1<N>::MINB) k_q_fwd(QArgs a) {
                          : "memory");
         }
         __syncthreads();                                      // X_A, X_B free
+        QPROF_T(p5);
+        QPROF_ADD(9, p4, p5);
+        QPROF_ADD(10, 0, 1);
     }
 }
 
@@ -270,9 +297,86 @@ __global__ void __launch_bounds__(Cfg<N>::NT, F1<N>::MINB) k_q_fwd(QArgs a) {
 template <int NQ> struct Q2 {
     static constexpr int PSP = NQ + 1;                       // Psi table pitch (doubles)
     static constexpr int R3 = (NQ + 31) / 32;                // k3 values per lane in the table phase
+    static constexpr int QTW = 6;                            // doubles per substep in the item's table
     static constexpr size_t SMEM = sizeof(V) * NQ * QCfg<NQ>::P + sizeof(double) * NQ * PSP +
-                                   (sizeof(double) + sizeof(int)) * NQ + sizeof(V) * NQ + 16;
+                                   2 * (sizeof(double) + sizeof(int)) * NQ + sizeof(V) * NQ + 16 +
+                                   sizeof(double) * QTW * (LCAP + 1) + sizeof(double) * PL_EU;
 };
+
+// The item's Euler-factor table (Alg. 3 with R3's D_n): for substep n the factor at
+// (k0, k1, k2, k3) is f_n = gb_n + c2_n kap2^2 + d_n kx2 + (e_n + c9_n kx2) kx3 + a_n kap3^2,
+// where gb_n = 1 + c0 kap0^2 + c1 kap1^2 + c4 kx0 kx1, d_n = c5 kx0 + c7 kx1, e_n = c6 kx0 + c8 kx1
+// collect the (k0, k1) terms once per item (cf = the coefficients of substep_coefs, packed
+// order diag 0..3, (0,1) (0,2) (0,3) (1,2) (1,3) (2,3)); row n = {gb, d, e, c2, c9, a}.
+__device__ __forceinline__ void q_item_table(const double* cf, int nsets, const double* kap, const double* kx,
+                                             double* qt) {
+    for (int n = threadIdx.x; n < nsets; n += blockDim.x) {
+        const double* c = cf + 10 * n;
+        double* o = qt + 6 * n;
+        o[0] = fma(c[4], kx[0] * kx[1], fma(c[1], kap[1] * kap[1], fma(c[0], kap[0] * kap[0], 1.0)));
+        o[1] = fma(c[7], kx[1], c[5] * kx[0]);
+        o[2] = fma(c[8], kx[1], c[6] * kx[0]);
+        o[3] = c[2];
+        o[4] = c[9];
+        o[5] = c[3];
+    }
+}
+
+// pair j of list `list` as a quartic in kap3 (psi_pair's output layout) from the item table
+__device__ __forceinline__ void q_pair(const double* qt, int l, int cn, int list, int j, double kap2sq, double kx2,
+                                       double2* q) {
+    const int base = (list == 0 && cn) ? 1 : 0;        // CN den: f_1 .. f_l
+    auto gba = [&](int n, double& g, double& b, double& a) {
+        const double* r = qt + 6 * n;
+        g = fma(r[3], kap2sq, fma(r[1], kx2, r[0]));
+        b = fma(r[4], kx2, r[2]);
+        a = r[5];
+    };
+    double g0, b0, a0, g1 = 1.0, b1 = 0.0, a1 = 0.0;
+    gba(base + 2 * j, g0, b0, a0);
+    const bool two = 2 * j + 1 < l;
+    if (two) gba(base + 2 * j + 1, g1, b1, a1);
+    if (list == 1) {                                   // 2 - f = (2 - g) - b k - a k^2
+        g0 = 2.0 - g0;
+        b0 = -b0;
+        a0 = -a0;
+        if (two) {
+            g1 = 2.0 - g1;
+            b1 = -b1;
+            a1 = -a1;
+        }
+    }
+    constexpr double kn2 = PMF_PI * PMF_PI;
+    q[0] = double2{g0 * g1, fma(g0, b1, b0 * g1)};
+    q[1] = double2{fma(g0, a1, fma(b0, b1, a0 * g1)), fma(b0, a1, a0 * b1)};
+    q[2] = double2{a0 * a1, fma(a0, kn2, g0) * fma(a1, kn2, g1)};
+}
+
+// acc[r] *= product of list `list`'s pair quartics at kap3 = kp[r]; every thread forms the
+// quartics itself from the item table (no shuffles: the 12 Horner chains per pair overlap
+// the next pair's coefficients)
+template <int NQ>
+__device__ __forceinline__ void q_psi_prod(double (&acc)[NQ / 8], const double (&kp)[NQ / 8], const double* qt, int l,
+                                           int cn, int list, double kap2sq, double kx2, int t) {
+    constexpr int R = NQ / 8;
+    const int nq = (l + 1) >> 1;
+    double nyq = 1.0;
+    // (measured: software-pipelining pair j + 1's quartic under pair j's Horner chains, or
+    // computing Psi inside the F3 loop instead of this table, both run K2 7-9 % slower)
+#pragma unroll 1
+    for (int j = 0; j < nq; ++j) {
+        double2 c[3];
+        q_pair(qt, l, cn, list, j, kap2sq, kx2, c);
+        nyq *= c[2].y;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const double x1 = kp[r];
+            acc[r] *= fma(fma(fma(fma(c[2].x, x1, c[1].y), x1, c[1].x), x1, c[0].y), x1, c[0].x);
+        }
+    }
+    if (t == ((NQ / 2) & 7)) acc[(NQ / 2) >> 3] = nyq;
+}
+
 template <int NQ>
 static size_t qmid_smem() { return Q2<NQ>::SMEM; }
 
@@ -282,13 +386,16 @@ __global__ void __launch_bounds__(QCfg<NQ, TM>::NT, 1) k_q_mid(QArgs a, int I, i
     constexpr int R = C::R, TEAMS = C::TEAMS, P = C::P;
     constexpr int PSP = Q2<NQ>::PSP;
     constexpr unsigned PLANE = NQ * NQ * sizeof(V);
-    extern __shared__ __align__(16) unsigned char smem_raw[];
+    extern __shared__ __align__(128) unsigned char smem_raw[];
     V* X = reinterpret_cast<V*>(smem_raw);                    // [NQ][P]: row j3
     double* psi = reinterpret_cast<double*>(X + NQ * P);      // [k2][PSP]
-    double* w3t = psi + NQ * PSP;                             // [u3'] axis-3 weight (split regrid)
-    int* j3t = reinterpret_cast<int*>(w3t + NQ);              // [u3'] first old row
-    V* tw = reinterpret_cast<V*>(j3t + NQ);
+    double* w3t = psi + NQ * PSP;                             // [u3'][2] axis-3 tap weights (split regrid)
+    int* j3t = reinterpret_cast<int*>(w3t + 2 * NQ);          // [u3'][2] axis-3 tap rows (clamped)
+    V* tw = reinterpret_cast<V*>(j3t + 2 * NQ);
     unsigned long long* bar = reinterpret_cast<unsigned long long*>(tw + NQ);
+    double* qt = reinterpret_cast<double*>(bar + 2);          // [nsets][6] the item's factor table
+    double* hd = qt + Q2<NQ>::QTW * (LCAP + 1);               // the filter's coefficient head (PL_*)
+    int curf = -1;
     const int tid = threadIdx.x, q = tid >> 3, t = tid & 7;
     init_tw<NQ>(tw);
     if (tid == 0) tma::mbar_init(bar, 1);
@@ -306,9 +413,16 @@ __global__ void __launch_bounds__(QCfg<NQ, TM>::NT, 1) k_q_mid(QArgs a, int I, i
     }
     int k = 0;
     for (int item = blockIdx.x; item < items; item += gridDim.x, ++k) {
+        QPROF_T(q0);
         const int nxt = item + gridDim.x;
         const unsigned f = (unsigned)item / (unsigned)I, i = (unsigned)item - f * (unsigned)I;
-        const double* Pc = a.coef + (long long)f * a.cs;
+        if ((int)f != curf) {                                 // uniform: cache the filter's head
+            if (tid < PL_EU) hd[tid] = a.coef[(long long)f * a.cs + tid];
+            curf = (int)f;
+            __syncthreads();
+        }
+        const double* Pg = a.coef + (long long)f * a.cs;      // (the substep coefficients stay global)
+        const double* Pc = hd;
         const bool skip = Pc[PL_SKIP] != 0.0;
         const int flag = (int)Pc[PL_FLAG];
         if (!skip) {
@@ -317,8 +431,8 @@ __global__ void __launch_bounds__(QCfg<NQ, TM>::NT, 1) k_q_mid(QArgs a, int I, i
             // f_n = gam_n + bet_n kx3 + alp_n kap3^2 multiplied in pairs as quartics in kap3;
             // warp w owns columns k2 = w + NW j, lane owns k3 = lane + 32 r; pair j's quartic is
             // computed by lane j % 32 and broadcast
-            const double* cf = Pc + PL_EU;
-            const int cn = a.step, l = a.l, nq = (l + 1) >> 1;
+            const double* cf = Pg + PL_EU;
+            const int cn = a.step, l = a.l;
             const unsigned k1 = i / (unsigned)N0;
             const int k0 = (int)(i - k1 * (unsigned)N0);
             const int N1 = 2 * (H1 - 1);
@@ -328,27 +442,35 @@ __global__ void __launch_bounds__(QCfg<NQ, TM>::NT, 1) k_q_mid(QArgs a, int I, i
             kap[1] = (2.0 * PMF_PI / N1) * (int)k1;
             kx[1] = (2 * (int)k1 == N1) ? 0.0 : kap[1];
             const double mult = Pc[PL_SN];
+            q_item_table(cf, l + cn, kap, kx, qt);
+            __syncthreads();
             double kp[R];
 #pragma unroll
             for (int r = 0; r < R; ++r) {
                 const int kk = t + 8 * r;
                 kp[r] = (2.0 * PMF_PI / NQ) * (kk < NQ / 2 ? kk : kk - NQ);
             }
-            // team q: columns k2 = q + TEAMS j; thread t: k3 = t + 8 r (pair quartics by
-            // width-8 shuffles, quad_psi_prod)
+            // team q: columns k2 = q + TEAMS j; thread t: k3 = t + 8 r
 #pragma unroll 1
             for (int k2 = q; k2 < NQ; k2 += TEAMS) {
-                kap[2] = (2.0 * PMF_PI / NQ) * (k2 < NQ / 2 ? k2 : k2 - NQ);
-                kx[2] = (2 * k2 == NQ) ? 0.0 : kap[2];
+                const double kap2 = (2.0 * PMF_PI / NQ) * (k2 < NQ / 2 ? k2 : k2 - NQ);
+                const double kx2 = (2 * k2 == NQ) ? 0.0 : kap2;
                 double den[R], ps[R];
 #pragma unroll
                 for (int r = 0; r < R; ++r) den[r] = 1.0;
-                quad_psi_prod<NQ>(den, kp, cf, l, cn, 0, kap, kx, t);
+#if !defined(QDBG) || (QDBG != 1 && QDBG != 3)
+                q_psi_prod<NQ>(den, kp, qt, l, cn, 0, kap2 * kap2, kx2, t);
+#endif
+#if !defined(QDBG) || QDBG < 2
                 psi_div<R>(den, mult, ps);
+#else
+#pragma unroll
+                for (int r = 0; r < R; ++r) ps[r] = den[r] * mult;
+#endif
                 if (cn) {                                     // Crank-Nicolson numerators (R27)
 #pragma unroll
                     for (int r = 0; r < R; ++r) den[r] = 1.0;
-                    quad_psi_prod<NQ>(den, kp, cf, l, cn, 1, kap, kx, t);
+                    q_psi_prod<NQ>(den, kp, qt, l, cn, 1, kap2 * kap2, kx2, t);
 #pragma unroll
                     for (int r = 0; r < R; ++r) ps[r] *= den[r];
                 }
@@ -356,40 +478,47 @@ __global__ void __launch_bounds__(QCfg<NQ, TM>::NT, 1) k_q_mid(QArgs a, int I, i
                 for (int r = 0; r < R; ++r) psi[k2 * PSP + t + 8 * r] = ps[r];
             }
             if (flag == 4 && tid < NQ) {
-                // axis-3 part of the split regrid (R12): output row u3' reads old rows ja, ja + 1
+                // axis-3 part of the split regrid (R12): output row u3' = (1 - w3) old row ja +
+                // w3 old row ja + 1, zero ghosts: taps outside the grid get weight 0 (row clamped)
                 const double v3 = fma(Pc[PL_M + 15], (double)tid - 0.5 * (NQ - 1), Pc[PL_O + 3]), f3 = floor(v3);
                 const int fi3 = __double2int_rz(f3);
                 const int ja = min(max(fi3, -2), NQ);
-                j3t[tid] = ja;
-                w3t[tid] = (ja == fi3) ? v3 - f3 : 0.0;
+                const double w3 = (ja == fi3) ? v3 - f3 : 0.0;
+                const bool va = ja >= 0 && ja < NQ, vb = ja + 1 >= 0 && ja + 1 < NQ;
+                j3t[2 * tid] = va ? ja : 0;
+                j3t[2 * tid + 1] = vb ? ja + 1 : 0;
+                w3t[2 * tid] = va ? 1.0 - w3 : 0.0;
+                w3t[2 * tid + 1] = vb ? w3 : 0.0;
             }
         }
+        QPROF_T(q1);
         tma::mbar_wait(bar, (unsigned)(k & 1));               // the plane is in shared memory
         __syncthreads();                                      // (and the tables are written)
+        QPROF_T(q2);
+        QPROF_ADD(0, q0, q1);
+        QPROF_ADD(1, q1, q2);
         if (!skip) {
             // ------------------------------------------------------------ [split regrid] + F2
             const bool rg = flag == 4;
             if (rg) {
+                int ia[R], ib[R];
+                double wa[R], wb[R];
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    const int u3 = t + 8 * r;
+                    ia[r] = j3t[2 * u3] * P;
+                    ib[r] = j3t[2 * u3 + 1] * P;
+                    wa[r] = w3t[2 * u3];
+                    wb[r] = w3t[2 * u3 + 1];
+                }
 #pragma unroll 1
                 for (int j2 = q; j2 < NQ; j2 += TEAMS) {
                     V* col = X + j2;
                     V z[R];
 #pragma unroll
                     for (int r = 0; r < R; ++r) {
-                        const int u3 = t + 8 * r, ja = j3t[u3];
-                        const double w3 = w3t[u3];
-                        double zx = 0.0, zy = 0.0;
-                        if (ja >= 0 && ja < NQ) {
-                            const V v = col[ja * P];
-                            zx = (1.0 - w3) * v.x;
-                            zy = (1.0 - w3) * v.y;
-                        }
-                        if (ja + 1 >= 0 && ja + 1 < NQ) {
-                            const V v = col[(ja + 1) * P];
-                            zx = fma(w3, v.x, zx);
-                            zy = fma(w3, v.y, zy);
-                        }
-                        z[r] = V{zx, zy};
+                        const V va = col[ia[r]], vb = col[ib[r]];
+                        z[r] = V{fma(wb[r], vb.x, wa[r] * va.x), fma(wb[r], vb.y, wa[r] * va.y)};
                     }
                     __syncwarp();
 #pragma unroll
@@ -412,6 +541,8 @@ __global__ void __launch_bounds__(QCfg<NQ, TM>::NT, 1) k_q_mid(QArgs a, int I, i
                 }
             }
             __syncthreads();
+            QPROF_T(q3);
+            QPROF_ADD(2, q2, q3);
             // ------------------------------------------------------------ F3: axis 3, x table, inverse
 #pragma unroll 1
             for (int k2 = q; k2 < NQ; k2 += TEAMS) {
@@ -442,6 +573,8 @@ __global__ void __launch_bounds__(QCfg<NQ, TM>::NT, 1) k_q_mid(QArgs a, int I, i
         }
         if (tid == 0 && nxt < items) tma::mbar_expect_tx(bar, PLANE);   // the next phase's bytes
         __syncthreads();
+        QPROF_T(q4);
+        QPROF_ADD(3, q2, q4);
         // ---------------------------------------------------------------- I2: inverse axis 2, store, refill
         V* dst = a.Y + (long long)item * (NQ * NQ);
 #pragma unroll 1
@@ -467,6 +600,9 @@ __global__ void __launch_bounds__(QCfg<NQ, TM>::NT, 1) k_q_mid(QArgs a, int I, i
                 if (t == 0) load_row(nxt, j3);
             }
         }
+        QPROF_T(q5);
+        QPROF_ADD(4, q4, q5);
+        QPROF_ADD(5, 0, 1);
     }
 }
 
@@ -546,8 +682,11 @@ __global__ void __launch_bounds__(Cfg<N>::NT, 1) k_q_inv(QArgs a, const __grid_c
     int k = 0;
     for (int p = blockIdx.x; p < nplanes; p += gridDim.x, ++k) {
         const int buf = k & 1;
+        QPROF_T(r0);
         issue(p + gridDim.x, buf ^ 1);
         tma::mbar_wait(&bar[buf], (unsigned)((k >> 1) & 1));
+        QPROF_T(r1);
+        QPROF_ADD(11, r0, r1);
         V* X = X0 + buf * XSV;
         const int filt = p / ppf, pl = p - filt * ppf;
         if (filt != curf) {                                   // uniform
@@ -587,6 +726,8 @@ __global__ void __launch_bounds__(Cfg<N>::NT, 1) k_q_inv(QArgs a, const __grid_c
             }
         }
         __syncthreads();
+        QPROF_T(r2);
+        QPROF_ADD(12, r1, r2);
         // ------------------------------------------------------------ inverse axis 1 of the column pair
         V x[R1];
         {
@@ -610,6 +751,8 @@ __global__ void __launch_bounds__(Cfg<N>::NT, 1) k_q_inv(QArgs a, const __grid_c
             }
             team_dft_dif<R1, true>(pa, pb, x, X, tw, t, [&](int s, int tt) { return cslot<N>(s, tt, m); });
         }
+        QPROF_T(r3);
+        QPROF_ADD(13, r2, r3);
         int j2, j3;
         plane_j(pl, n2, j2, j3);
         double* Wp = a.W + filt * ntot + (long long)pl * N * N;
@@ -727,6 +870,9 @@ __global__ void __launch_bounds__(Cfg<N>::NT, 1) k_q_inv(QArgs a, const __grid_c
                 }
         }
         __syncthreads();                  // X is consumed
+        QPROF_T(r4);
+        QPROF_ADD(14, r3, r4);
+        QPROF_ADD(15, 0, 1);
     }
     if (UP) flush();
     (void)lane;
@@ -736,6 +882,18 @@ __global__ void __launch_bounds__(Cfg<N>::NT, 1) k_q_inv(QArgs a, const __grid_c
 }  // namespace pln
 
 using namespace pln;
+
+// debug: read (and optionally reset) the phase counters of -DPMF_QPROF builds
+int quad_debug_counters(double* out, int n, int reset) {
+    unsigned long long h[16];
+    if (cudaMemcpyFromSymbol(h, g_qprof, sizeof(h)) != cudaSuccess) return -1;
+    for (int i = 0; i < n && i < 16; ++i) out[i] = (double)h[i];
+    if (reset) {
+        std::fill(h, h + 16, 0ull);
+        cudaMemcpyToSymbol(g_qprof, h, sizeof(h));
+    }
+    return 0;
+}
 
 bool quad_supported(const Dims& d, int dtype) {
     if (dtype != 0 || d.nx != 4 || d.n[0] != d.n[1] || d.n[2] != d.n[3]) return false;
@@ -808,6 +966,8 @@ static cudaError_t quad_n(const Dims& d, PencilBufs& b, QArgs qa, bool rg, bool 
                           int* ginv) {
     using Cf = Cfg<N>;
     cudaError_t e;
+    CUtensorMap ymap;
+    if ((e = y_map(qa, N, Cf::H, &ymap)) != cudaSuccess) return e;
     {
         const size_t smem = F1<N>::SMEM;
         int grid = 1;
@@ -838,8 +998,6 @@ static cudaError_t quad_n(const Dims& d, PencilBufs& b, QArgs qa, bool rg, bool 
     }
     if (b.ev1) cudaEventRecordWithFlags(b.ev1, s, cudaEventRecordExternal);
     {
-        CUtensorMap ymap;
-        if ((e = y_map(qa, N, Cf::H, &ymap)) != cudaSuccess) return e;
         const size_t smem = qinv_smem<N>();
         const long long nplanes = (long long)d.batch * d.n[2] * d.n[3];
         if (up) {

@@ -1072,3 +1072,7 @@ int pmf_path(const pmf_ctx* c) { return c ? c->path : -1; }
 int pmf_epoch_kernel(const pmf_ctx* c) { return c ? c->epoch_kernel : -1; }
 
 }  // extern "C"
+
+// Debug only (not in pmf.h): per-phase cycle counters of the nx = 4 three-pass kernels in
+// builds compiled with -DPMF_QPROF (tools/qprof.py); zeros otherwise.
+extern "C" int pmf_debug_counters(double* out, int n, int reset) { return quad_debug_counters(out, n, reset); }

@@ -208,6 +208,7 @@ cudaError_t launch_plane(const Dims& d, int dtype, PencilBufs& b, const ModelPar
 // nx = 4 fp64 three-pass route (kernels_quad.cu): spectrum in the transposed layout
 // [filter][k1][k0][j3][j2]; called by launch_plane between its prep and finaliser
 bool quad_supported(const Dims& d, int dtype);
+int quad_debug_counters(double* out, int n, int reset);
 cudaError_t launch_quad(const Dims& d, PencilBufs& b, const ModelParams& mp, int range, bool rg, bool up,
                         double* dcpart, double* dc3, double* part, cudaStream_t s, int64_t* launches, int* ginv);
 
