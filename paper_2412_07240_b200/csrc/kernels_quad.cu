@@ -622,7 +622,8 @@ template <int N>
 static size_t qinv_smem() { return Q3<N>::SMEM; }
 
 template <int N, bool UP>
-__global__ void __launch_bounds__(Cfg<N>::NT, 1) k_q_inv(QArgs a, const __grid_constant__ CUtensorMap ymap) {
+__global__ void __launch_bounds__(Cfg<N>::NT, 1) k_q_inv(QArgs a, const __grid_constant__ CUtensorMap ymap,
+                                                       const __grid_constant__ CUtensorMap wmap) {
     using C = Cfg<N>;
     constexpr int R1 = C::R1, H = C::H, PITCH = C::PITCH, NT = C::NT, NW = NT / 32, NX = 4;
     constexpr int XSV = (int)(Q3<N>::XS / sizeof(V));
@@ -638,6 +639,7 @@ __global__ void __launch_bounds__(Cfg<N>::NT, 1) k_q_inv(QArgs a, const __grid_c
         tma::mbar_init(&bar[0], 1);
         tma::mbar_init(&bar[1], 1);
         asm volatile("prefetch.tensormap [%0];" ::"l"(&ymap) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&wmap) : "memory");
     }
     const int n2 = a.n2, n3 = a.n3, ppf = n2 * n3;
     const long long ntot = (long long)N * N * ppf, nq = (long long)n2 * n3;
@@ -683,7 +685,6 @@ __global__ void __launch_bounds__(Cfg<N>::NT, 1) k_q_inv(QArgs a, const __grid_c
     for (int p = blockIdx.x; p < nplanes; p += gridDim.x, ++k) {
         const int buf = k & 1;
         QPROF_T(r0);
-        issue(p + gridDim.x, buf ^ 1);
         tma::mbar_wait(&bar[buf], (unsigned)((k >> 1) & 1));
         QPROF_T(r1);
         QPROF_ADD(11, r0, r1);
@@ -696,7 +697,9 @@ __global__ void __launch_bounds__(Cfg<N>::NT, 1) k_q_inv(QArgs a, const __grid_c
             __syncthreads();
         }
         const double* P = cfs;
-        if (P[PL_SKIP] != 0.0) {
+        if (P[PL_SKIP] != 0.0) {                              // uniform: failed filter, left untouched
+            if (tid == 0) tma::bulk_wait_read<0>();
+            issue(p + gridDim.x, buf ^ 1);
             __syncthreads();
             continue;
         }
@@ -726,6 +729,9 @@ __global__ void __launch_bounds__(Cfg<N>::NT, 1) k_q_inv(QArgs a, const __grid_c
             }
         }
         __syncthreads();
+        // the next plane into the other buffer, once that buffer's weight store has read it
+        if (tid == 0) tma::bulk_wait_read<0>();
+        issue(p + gridDim.x, buf ^ 1);
         QPROF_T(r2);
         QPROF_ADD(12, r1, r2);
         // ------------------------------------------------------------ inverse axis 1 of the column pair
@@ -755,11 +761,24 @@ __global__ void __launch_bounds__(Cfg<N>::NT, 1) k_q_inv(QArgs a, const __grid_c
         QPROF_ADD(13, r2, r3);
         int j2, j3;
         plane_j(pl, n2, j2, j3);
-        double* Wp = a.W + filt * ntot + (long long)pl * N * N;
+        // the plane's weights are staged in X (rows of pitch N + 2 doubles: conflict-free) and
+        // leave by one TMA tensor store (768-byte rows) instead of per-thread strided stores
+        __syncthreads();                                      // X is consumed by the transforms
+        double* Ws = reinterpret_cast<double*>(X);
+        auto store_plane = [&]() {
+            __syncthreads();                                  // the staged rows are complete
+            if (tid == 0) {
+                tma::fence_proxy_async();
+                asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];"
+                             ::"l"(&wmap), "r"(0), "r"(0), "r"(p), "r"(tma::smem_u32(Ws))
+                             : "memory");
+                tma::bulk_commit();
+            }
+        };
         if (!UP) {
 #pragma unroll
-            for (int r = 0; r < R1; ++r) *reinterpret_cast<V*>(Wp + (long long)(t + 8 * r) * N + 2 * m) = x[r];
-            __syncthreads();
+            for (int r = 0; r < R1; ++r) *reinterpret_cast<V*>(Ws + (t + 8 * r) * (N + 2) + 2 * m) = x[r];
+            store_plane();
             continue;
         }
         const double u2 = j2 - 0.5 * (n2 - 1), u3 = j3 - 0.5 * (n3 - 1);
@@ -807,7 +826,7 @@ __global__ void __launch_bounds__(Cfg<N>::NT, 1) k_q_inv(QArgs a, const __grid_c
                 Rr[0] *= Gr[0];
                 Lr[1] *= Rr[1];
                 Rr[1] *= Gr[1];
-                *reinterpret_cast<V*>(Wp + (long long)(t + 8 * r) * N + 2 * m) = V{o0, o1};
+                *reinterpret_cast<V*>(Ws + (t + 8 * r) * (N + 2) + 2 * m) = V{o0, o1};
             }
         } else {
             const double* q = P + PL_LQ;
@@ -844,7 +863,7 @@ __global__ void __launch_bounds__(Cfg<N>::NT, 1) k_q_inv(QArgs a, const __grid_c
                     const double w = e == 0 ? x[r].x : x[r].y;
                     o[e] = emit(r, e, w * exp_fast(ll));
                 }
-                *reinterpret_cast<V*>(Wp + (long long)(t + 8 * r) * N + 2 * m) = V{o[0], o[1]};
+                *reinterpret_cast<V*>(Ws + (t + 8 * r) * (N + 2) + 2 * m) = V{o[0], o[1]};
             }
         }
         {
@@ -869,12 +888,13 @@ __global__ void __launch_bounds__(Cfg<N>::NT, 1) k_q_inv(QArgs a, const __grid_c
                     mom[(kk++) * NT] += v;
                 }
         }
-        __syncthreads();                  // X is consumed
+        store_plane();                    // (its barrier: the moment sums are also complete)
         QPROF_T(r4);
         QPROF_ADD(14, r3, r4);
         QPROF_ADD(15, 0, 1);
     }
     if (UP) flush();
+    if (tid == 0) tma::bulk_wait_all();
     (void)lane;
     (void)warp;
 }
@@ -942,6 +962,29 @@ static cudaError_t y_map(const QArgs& qa, int N, int H, CUtensorMap* m) {
     return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
+// Tensor map of the weights for K3's plane stores: doubles, dims j0 N, j1 N, planes
+// batch * n2 * n3; box (N + 2) x N x 1 -- the staged rows' two padding doubles fall beyond
+// j0 = N - 1 and are not written.
+static cudaError_t w_map(const QArgs& qa, int N, CUtensorMap* m) {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    if (!encode) {
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&encode, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess || !encode) {
+            encode = nullptr;
+            return cudaErrorNotSupported;
+        }
+    }
+    cuuint64_t dims[3] = {(cuuint64_t)N, (cuuint64_t)N, (cuuint64_t)qa.batch * qa.n2 * qa.n3};
+    cuuint64_t str[2] = {8 * (cuuint64_t)N, 8 * (cuuint64_t)N * N};
+    cuuint32_t box[3] = {(cuuint32_t)(N + 2), (cuuint32_t)N, 1};
+    cuuint32_t es[3] = {1, 1, 1};
+    CUresult r = encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void*)qa.W, dims, str, box, es,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
 template <int NQ, int TM>
 static cudaError_t qmid_tm(const QArgs& qa, int I, int N0, int H1, cudaStream_t s) {
     using Cq = QCfg<NQ, TM>;
@@ -966,8 +1009,9 @@ static cudaError_t quad_n(const Dims& d, PencilBufs& b, QArgs qa, bool rg, bool 
                           int* ginv) {
     using Cf = Cfg<N>;
     cudaError_t e;
-    CUtensorMap ymap;
+    CUtensorMap ymap, wmap;
     if ((e = y_map(qa, N, Cf::H, &ymap)) != cudaSuccess) return e;
+    if ((e = w_map(qa, N, &wmap)) != cudaSuccess) return e;
     {
         const size_t smem = F1<N>::SMEM;
         int grid = 1;
@@ -1004,10 +1048,10 @@ static cudaError_t quad_n(const Dims& d, PencilBufs& b, QArgs qa, bool rg, bool 
             e = q_grid(k_q_inv<N, true>, Cf::NT, smem, nplanes, ginv);
             if (e == cudaSuccess && d.batch > 1)
                 e = cudaMemsetAsync(qa.part, 0, sizeof(double) * NMOM * (*ginv) * (size_t)d.batch, s);
-            if (e == cudaSuccess) k_q_inv<N, true><<<*ginv, Cf::NT, smem, s>>>(qa, ymap);
+            if (e == cudaSuccess) k_q_inv<N, true><<<*ginv, Cf::NT, smem, s>>>(qa, ymap, wmap);
         } else {
             e = q_grid(k_q_inv<N, false>, Cf::NT, smem, nplanes, ginv);
-            if (e == cudaSuccess) k_q_inv<N, false><<<*ginv, Cf::NT, smem, s>>>(qa, ymap);
+            if (e == cudaSuccess) k_q_inv<N, false><<<*ginv, Cf::NT, smem, s>>>(qa, ymap, wmap);
         }
         if (e != cudaSuccess) return e;
         ++*launches;
