@@ -1226,18 +1226,8 @@ static cudaError_t plane_t(const Dims& d, PencilBufs& b, const ModelParams& mp, 
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
     // nx = 4, fp64: the three-pass transposed-spectrum route (kernels_quad.cu)
-    if constexpr (NX == 4 && std::is_same<T, double>::value && N <= 96) {
-        if (quad_supported(d, 0)) {
-            int ginv = 1;
-            e = launch_quad(d, b, mp, pa.range, rg, lp != nullptr, pa.dcpart, pa.dc3, pa.part, s, launches, &ginv);
-            if (e != cudaSuccess) return e;
-            k_plane_fin<NX><<<d.batch, 256, 0, s>>>(b.st, b.coef, cs, pa.dcpart, pa.dc3, pa.part, ppf, n3, ginv,
-                                                    lp ? 1 : 0);
-            ++*launches;
-            return cudaGetLastError();
-        }
-    }
-    // forward plane pass
+    const bool quad = NX == 4 && std::is_same<T, double>::value && N <= 96 && quad_supported(d, 0);
+    // forward plane pass (K1 of both routes: the per-plane half spectrum S[f][j3][j2][k1][k0])
     {
         const size_t smem = fwd_smem<T, N>();
         int grid = 1;
@@ -1251,6 +1241,17 @@ static cudaError_t plane_t(const Dims& d, PencilBufs& b, const ModelParams& mp, 
         if (e != cudaSuccess) return e;
         ++*launches;
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    }
+    if (quad) {
+        // nx = 4, fp64: K2 (gathers (j3, j2)-planes from S, writes S2 in the transposed layout)
+        // and K3 (kernels_quad.cu) replace the three strided passes and the inverse plane pass
+        int ginv = 1;
+        e = launch_quad(d, b, mp, pa.range, lp != nullptr, pa.dcpart, pa.dc3, pa.part, s, launches, &ginv);
+        if (e != cudaSuccess) return e;
+        k_plane_fin<NX><<<d.batch, 256, 0, s>>>(b.st, b.coef, cs, pa.dcpart, pa.dc3, pa.part, ppf, n3, ginv,
+                                                lp ? 1 : 0);
+        ++*launches;
+        return cudaGetLastError();
     }
     // strided axes: forward 2..nx-2 (the first out of place, + the split regrid's (2,3) part),
     // the last axis with Psi, inverse nx-2..2

@@ -1,31 +1,24 @@
 // kernels_quad.cu -- the three-pass ("transposed spectrum") time update for nx = 4
 // grids (BASELINE configs[3], C4: 96^4 fp64).
 //
-// The 4-D half spectrum is kept in HBM in the layout
+//   K1 k_plane_fwd (kernels_plane.cu)  per (j0, j1)-plane: [split regrid, in-plane part,
+//                R12] -> forward DFT along axes 1 and 0 (Alg. 1, eq:fourtrsf P:221) -> the
+//                plane's half spectrum S[filter][j3][j2][k1][k0] (contiguous rows)
+//   K2 k_q_mid   per (filter, k1, k0): its (j3, j2)-plane gathered from S by tensor-map TMA
+//                loads (16-byte elements, the row pitch padded by an out-of-range column)
+//                -> [split regrid, axes-2/3 part] -> forward DFT along axes 2, 3 -> s Psi /
+//                N_tot (Alg. 3-4) -> inverse DFT along axes 3, 2 (Alg. 5) -> contiguous rows
+//                of S2[filter][k1][k0][j3][j2] (the transposed layout)
+//   K3 k_q_inv   per (j0, j1)-plane: its coefficients gathered from S2 by one TMA load ->
+//                inverse DFT along axes 0, 1 -> likelihood at the moved points (eq:filt
+//                P:46, R13) -> weights staged in shared memory, one TMA store; index-space
+//                moment partials
 //
-//     Y[filter][k1 (0..N/2)][k0 (0..N-1)][j3][j2]          (complex fp64)
-//
-// so that, for every axis-0/1 wavenumber pair (k0, k1), the (j2, j3)-plane that the
-// axis-2/3 transforms need is ONE contiguous n3 x n2 block (147 KB at 96^2). One
-// prediction interval + measurement update is then three passes over HBM:
-//
-//   K1 k_q_fwd   per PAIR of (j0, j1)-planes (j2, j2 + 1; same j3): [split regrid,
-//                in-plane part, R12] -> forward DFT along axes 1 and 0 (Alg. 1,
-//                eq:fourtrsf P:221) of both planes in shared memory -> the two
-//                planes' coefficients (k1, k0) leave as one 32-byte store each
-//                (both j2 of the pair are adjacent in Y)
-//   K2 k_q_mid   per (filter, k1, k0): the contiguous (j3, j2)-plane by bulk copies
-//                -> [split regrid, axes-2/3 part] -> forward DFT along axes 2, 3 ->
-//                s Psi / N_tot (Alg. 3-4, Euler factors paired into quartics) ->
-//                inverse DFT along axes 3, 2 (Alg. 5) -> back in place
-//   K3 k_q_inv   per (j0, j1)-plane: gather of its coefficients (16-byte cp.async,
-//                neighbouring planes on neighbouring CTAs share the 32-byte sectors
-//                in L2) -> inverse DFT along axes 0, 1 -> likelihood at the moved
-//                points (eq:filt P:46, R13), store, index-space moment partials
-//
-// against five passes on the per-plane layout of kernels_plane.cu. Prep, the general
-// regrid pre-pass and the finaliser are shared with that path. fp64 only (the pair
-// store is one 32-byte sector); N_0 = N_1 in {32, 64, 96}, n2 = n3 in {16, .., 96}.
+// Three passes over HBM (K1 reads the weights and writes S, K2 reads S and writes S2, K3
+// reads S2 and writes the weights) against five on the per-plane layout of
+// kernels_plane.cu: the transposition rides on the TMA gathers, whose 16-byte element
+// rate is hidden behind each kernel's arithmetic. fp64 only; N_0 = N_1 in {32, 64, 96},
+// n2 = n3 in {16, .., 96}.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -58,13 +51,11 @@ __device__ unsigned long long g_qprof[16];
 #endif
 
 struct QArgs {
-    const double* Wsrc;      // weights read by K1 (old grid when regridding)
-    const double* W2src;     // pre-regridded weights (general regrid map, flag 2)
     double* W;               // weights written by K3
-    V* Y;                    // spectrum, layout [filter][k1][k0][j3][j2]
+    const V* Yin;            // K1's spectrum S[filter][j3][j2][k1][k0] (K2's input)
+    V* Y;                    // S2[filter][k1][k0][j3][j2] (K2's output, K3's input)
     const double* coef;
     int cs;
-    double* dcpart;          // [plane] sums of K1's input planes
     double* dc3;             // [filter][n3] the regridded sums (split maps; K2)
     double* part;            // [filter][K3 CTAs][NMOM]
     int batch;
@@ -72,215 +63,6 @@ struct QArgs {
     int l, step;
     int range;               // likelihood kind 1 (range), else linear Gauss
 };
-
-// ============================================================================ K1: forward plane pairs
-// shared memory: X_A, X_B [H][PITCH] complex, a 16-byte zero guard, the staged real plane
-// [N][SP2] (pitch N + 2: 16-byte rows, the 8 rows a team reads in distinct bank groups;
-// the two padding columns stay zero and are the zero ghost nodes of R12 -- column N of
-// row r and column -1 of row r + 1, the guard being column -1 of row 0), twiddles, one
-// mbarrier. At N = 96: 2 x 76.8 KB + 75.3 KB + 1.5 KB = 230.5 KB.
-template <int N> struct F1 {
-    static constexpr int SP2 = N + 2;
-    static constexpr size_t XB = (sizeof(V) * Cfg<N>::H * Cfg<N>::PITCH + 127) / 128 * 128;   // TMA: 128-B aligned
-    static constexpr size_t SB = sizeof(double) * N * SP2 + 16;
-    static constexpr size_t SMEM = 2 * XB + SB + sizeof(V) * N + 16;
-    static constexpr int MINB = SMEM <= 113 * 1024 ? 2 : 1;
-};
-
-// forward DFT along axis 1 (column pairs, packed complex) and axis 0 (rows) of one
-// real plane whose column pair (2m, 2m+1) is in z[r] = (w(2m, t+8r), w(2m+1, t+8r));
-// result: X[k1][k0] natural order, k1 = 0..N/2 (as k_plane_fwd)
-template <int N>
-__device__ __forceinline__ void fwd_plane(V* X, V (&z)[N / 8], const V* tw, int m, int t) {
-    constexpr int R1 = N / 8, PITCH = Cfg<N>::PITCH;
-    {
-        V pa[8], pb[8];
-        team_dft<R1, false>(z, pa, pb, X, tw, t, [&](int s2, int tt) { return cslot<N>(s2, tt, m); });
-        if (s_on<R1>(t)) {
-            const int sa = s_a<R1>(t), sb = s_b<R1>(t);
-            auto store_pair = [&](int k1, V zk, V zp) {
-                X[k1 * PITCH + xcol(k1, 2 * m)] = V{0.5 * (zk.x + zp.x), 0.5 * (zk.y - zp.y)};
-                X[k1 * PITCH + xcol(k1, 2 * m + 1)] = V{0.5 * (zk.y + zp.y), 0.5 * (zp.x - zk.x)};
-            };
-            const bool t0 = t == 0;
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const V ma = t0 ? pa[(8 - q) & 7] : pb[7 - q];
-                const V mb = t0 ? pb[7 - q] : pa[7 - q];
-                store_pair(sa + R1 * q, pa[q], ma);
-                store_pair(sb + R1 * q, pb[q], mb);
-            }
-            if (t0) store_pair(R1 * 4, pa[4], pa[4]);
-        }
-    }
-    __syncthreads();
-    {
-        V x[R1], pa[8], pb[8];
-        V* row = X + m * PITCH;
-        const bool m0 = m == 0;
-#pragma unroll
-        for (int r = 0; r < R1; ++r) {
-            const V A = row[xcol(m, t + 8 * r)];
-            const double B = m0 ? X[(N / 2) * PITCH + t + 8 * r].x : 0.0;
-            x[r] = m0 ? V{A.x, B} : A;
-        }
-        team_dft<R1, false>(x, pa, pb, row, tw, t, [](int s2, int tt) { return rslot(s2, tt); });
-        if (s_on<R1>(t)) {
-            const int sa = s_a<R1>(t), sb = s_b<R1>(t);
-            if (m == 0) {
-                auto unpack = [&](int kk, V rk, V rm) {
-                    X[kk] = V{0.5 * (rk.x + rm.x), 0.5 * (rk.y - rm.y)};
-                    X[(N / 2) * PITCH + kk] = V{0.5 * (rk.y + rm.y), 0.5 * (rm.x - rk.x)};
-                };
-                const bool t0 = t == 0;
-#pragma unroll
-                for (int q = 0; q < 8; ++q) {
-                    unpack(sa + R1 * q, pa[q], t0 ? pa[(8 - q) & 7] : pb[7 - q]);
-                    unpack(sb + R1 * q, pb[q], t0 ? pb[7 - q] : pa[7 - q]);
-                }
-            } else {
-#pragma unroll
-                for (int q = 0; q < 8; ++q) {
-                    row[sa + R1 * q] = pa[q];
-                    row[sb + R1 * q] = pb[q];
-                }
-            }
-        }
-    }
-    __syncthreads();
-}
-
-template <int N, bool RG>
-__global__ void __launch_bounds__(Cfg<N>::NT, F1<N>::MINB) k_q_fwd(QArgs a) {
-    using C = Cfg<N>;
-    constexpr int R1 = C::R1, H = C::H, PITCH = C::PITCH, NT = C::NT, SP2 = F1<N>::SP2;
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    V* XA = reinterpret_cast<V*>(smem_raw);
-    V* XB = reinterpret_cast<V*>(smem_raw + F1<N>::XB);
-    double* stg = reinterpret_cast<double*>(smem_raw + 2 * F1<N>::XB) + 2;   // after the zero guard
-    V* tw = reinterpret_cast<V*>(stg + N * SP2);
-    unsigned long long* bar = reinterpret_cast<unsigned long long*>(tw + N);
-    const int tid = threadIdx.x, m = tid >> 3, t = tid & 7;
-    init_tw<N>(tw);
-    if (tid == 0) tma::mbar_init(bar, 1);
-    for (int i = tid; i < 2 * N + 2; i += NT) {               // ghost columns and guard: zero
-        if (i < 2) stg[i - 2] = 0.0;
-        else stg[((i - 2) >> 1) * SP2 + N + ((i - 2) & 1)] = 0.0;
-    }
-    const int n2 = a.n2, n3 = a.n3, ppf = n2 * n3, hp = n2 / 2;
-    const long long ntot = (long long)N * N * ppf, nq = (long long)n2 * n3;
-    const int units = a.batch * n3 * hp;
-    __syncthreads();
-    // stage plane pl of filter f (rows issued by the first N threads)
-    auto issue = [&](int f, int pl) {
-        if (tid >= N) return;
-        const double* P = a.coef + (long long)f * a.cs;
-        const double* src = ((RG && (int)P[PL_FLAG] == 2) ? a.W2src : a.Wsrc) + f * ntot + (long long)pl * N * N;
-        tma::fence_proxy_async();
-        if (tid == 0) tma::mbar_expect_tx(bar, (unsigned)(N * N * sizeof(double)));
-        tma::bulk_g2s(stg + tid * SP2, src + (long long)tid * N, (unsigned)(N * sizeof(double)), bar);
-    };
-    auto decode = [&](int u, int& f, int& j3, int& j2) {
-        f = u / (n3 * hp);
-        const int r = u - f * n3 * hp;
-        j3 = r / hp;
-        j2 = 2 * (r - j3 * hp);
-    };
-    if ((int)blockIdx.x < units) {
-        int f, j3, j2;
-        decode(blockIdx.x, f, j3, j2);
-        issue(f, j3 * n2 + j2);
-    }
-    int k = 0;
-    for (int u = blockIdx.x; u < units; u += gridDim.x) {
-        int f, j3, j2;
-        decode(u, f, j3, j2);
-        const double* P = a.coef + (long long)f * a.cs;
-        const int flag = RG ? (int)P[PL_FLAG] : 0;
-        const bool skip = P[PL_SKIP] != 0.0;
-#pragma unroll 1
-        for (int h = 0; h < 2; ++h, ++k) {
-            QPROF_T(p0);
-            tma::mbar_wait(bar, (unsigned)(k & 1));
-            QPROF_T(p1);
-            QPROF_ADD(6, p0, p1);
-            V z[R1];
-            if (RG && flag == 4) {
-                // in-plane part of the split regrid map (R12): bilinear from the staged old
-                // plane, v1 = o1 + M11 u1', v0 = o0 + M00 u0' + M01 u1'; zero ghost nodes
-                const double M00 = P[PL_M], M01 = P[PL_M + 1], M11 = P[PL_M + 5], o0 = P[PL_O], o1 = P[PL_O + 1];
-                auto split = [&](double v, int& i, double& fr) {
-                    const double fl = floor(v);
-                    const int fi = __double2int_rz(fl);
-                    i = min(max(fi, -1), N);
-                    fr = (fi == i) ? v - fl : 0.0;
-                };
-#pragma unroll
-                for (int r = 0; r < R1; ++r) {
-                    const double u1 = (t + 8 * r) - 0.5 * (N - 1);
-                    int i1;
-                    double a1;
-                    split(fma(M11, u1, o1), i1, a1);
-                    // ghost rows -1 and N: selected to zero (the ghost columns are in the buffer)
-                    const bool va = (unsigned)i1 < (unsigned)N, vb = (unsigned)(i1 + 1) < (unsigned)N;
-                    const double* ra = stg + (va ? i1 : 0) * SP2;              // in-bounds addresses
-                    const double* rb = stg + (vb ? i1 + 1 : 0) * SP2;
-                    const double vbase = fma(M01, u1, o0);
-                    double val[2];
-#pragma unroll
-                    for (int e = 0; e < 2; ++e) {
-                        int i0;
-                        double a0;
-                        split(fma(M00, (2 * m + e) - 0.5 * (N - 1), vbase), i0, a0);
-                        const double w00 = va ? ra[i0] : 0.0, w01 = va ? ra[i0 + 1] : 0.0;
-                        const double w10 = vb ? rb[i0] : 0.0, w11 = vb ? rb[i0 + 1] : 0.0;
-                        const double lo = fma(a0, w01 - w00, w00), hi = fma(a0, w11 - w10, w10);
-                        val[e] = fma(a1, hi - lo, lo);
-                    }
-                    z[r] = V{val[0], val[1]};
-                }
-            } else {
-#pragma unroll
-                for (int r = 0; r < R1; ++r) z[r] = *reinterpret_cast<const V*>(stg + (t + 8 * r) * SP2 + 2 * m);
-            }
-            __syncthreads();                                  // staged plane consumed
-            QPROF_T(p2);
-            QPROF_ADD(7, p1, p2);
-            if (h == 0) issue(f, j3 * n2 + j2 + 1);
-            else if (u + (int)gridDim.x < units) {
-                int f2, j32, j22;
-                decode(u + gridDim.x, f2, j32, j22);
-                issue(f2, j32 * n2 + j22);
-            }
-            if (skip) continue;                               // uniform
-            fwd_plane<N>(h ? XB : XA, z, tw, m, t);
-            QPROF_T(p3);
-            QPROF_ADD(8, p2, p3);
-        }
-        QPROF_T(p4);
-        if (skip) continue;
-        // both planes' coefficients (k1, k0) as one 32-byte store each: Y[f][k1][k0][j3][j2, j2+1]
-        // (measured: a tensor-map TMA store per plane -- 16-byte elements -- is bound by the TMA
-        // unit at ~8 B/clk per SM and slower than these 32-byte stores)
-        if (tid == 0) {
-            a.dcpart[(long long)f * ppf + j3 * n2 + j2] = XA[0].x;      // sums of the input planes
-            a.dcpart[(long long)f * ppf + j3 * n2 + j2 + 1] = XB[0].x;
-        }
-        double* yb = reinterpret_cast<double*>(a.Y + (long long)f * H * N * nq + (long long)j3 * n2 + j2);
-        for (int e = tid; e < H * N; e += NT) {
-            const int k1 = e / N, k0 = e - k1 * N;
-            const V va = XA[k1 * PITCH + k0], vb = XB[k1 * PITCH + k0];
-            double* g = yb + 2 * (long long)e * nq;
-            asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(g), "d"(va.x), "d"(va.y), "d"(vb.x),
-                         "d"(vb.y)
-                         : "memory");
-        }
-        __syncthreads();                                      // X_A, X_B free
-        QPROF_T(p5);
-        QPROF_ADD(9, p4, p5);
-        QPROF_ADD(10, 0, 1);
-    }
-}
 
 // ============================================================================ K2: contiguous (j3, j2)-planes
 // Work item = (filter, k1, k0); its plane Y[f][k1][k0][.][.] (NQ rows of NQ complex) is
@@ -298,6 +80,7 @@ template <int NQ> struct Q2 {
     static constexpr int PSP = NQ + 1;                       // Psi table pitch (doubles)
     static constexpr int R3 = (NQ + 31) / 32;                // k3 values per lane in the table phase
     static constexpr int QTW = 6;                            // doubles per substep in the item's table
+    static constexpr int RP = NQ < 32 ? NQ : 32;             // rows per TMA part of the gathered plane
     static constexpr size_t SMEM = sizeof(V) * NQ * QCfg<NQ>::P + sizeof(double) * NQ * PSP +
                                    2 * (sizeof(double) + sizeof(int)) * NQ + sizeof(V) * NQ + 16 +
                                    sizeof(double) * QTW * (LCAP + 1) + sizeof(double) * PL_EU;
@@ -381,11 +164,13 @@ template <int NQ>
 static size_t qmid_smem() { return Q2<NQ>::SMEM; }
 
 template <int NQ, int TM>
-__global__ void __launch_bounds__(QCfg<NQ, TM>::NT, 1) k_q_mid(QArgs a, int I, int N0, int H1) {
+__global__ void __launch_bounds__(QCfg<NQ, TM>::NT, 1) k_q_mid(QArgs a, int I, int N0, int H1,
+                                                                const __grid_constant__ CUtensorMap smap) {
     using C = QCfg<NQ, TM>;
     constexpr int R = C::R, TEAMS = C::TEAMS, P = C::P;
     constexpr int PSP = Q2<NQ>::PSP;
-    constexpr unsigned PLANE = NQ * NQ * sizeof(V);
+    constexpr int RP = Q2<NQ>::RP, NPART = NQ / RP;          // rows per TMA part, parts per item
+    constexpr unsigned PLANE = NQ * P * sizeof(V);            // incl. the zero-filled padding column
     extern __shared__ __align__(128) unsigned char smem_raw[];
     V* X = reinterpret_cast<V*>(smem_raw);                    // [NQ][P]: row j3
     double* psi = reinterpret_cast<double*>(X + NQ * P);      // [k2][PSP]
@@ -403,13 +188,22 @@ __global__ void __launch_bounds__(QCfg<NQ, TM>::NT, 1) k_q_mid(QArgs a, int I, i
     __syncthreads();
     auto rs = [](int s2, int tt) { return rslot(s2, tt); };
     auto cs = [](int s2, int tt) { return rslot(s2, tt) * P; };
-    auto load_row = [&](int it, int j3) {
-        tma::bulk_g2s(X + j3 * P, a.Y + (long long)it * (NQ * NQ) + j3 * NQ, NQ * sizeof(V), bar);
+    // rows [c RP, (c + 1) RP) of item `it`'s (j3, j2)-plane: one TMA load (thread 0; the caller
+    // has ordered the rows' earlier reads before it); 128-byte aligned (P RP = 0 mod 8)
+    auto load_part = [&](int it, int c) {
+        const unsigned fi = (unsigned)it / (unsigned)I, ii = (unsigned)it - fi * (unsigned)I;
+        const unsigned k1 = ii / (unsigned)N0, k0 = ii - k1 * (unsigned)N0;
+        asm volatile(
+            "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, "
+            "%6}], [%7];" ::"r"(tma::smem_u32(X + c * RP * P)),
+            "l"(&smap), "r"(0), "r"((int)k0), "r"((int)k1), "r"(0), "r"((int)(fi * NQ + c * RP)),
+            "r"(tma::smem_u32(bar))
+            : "memory");
     };
-    if ((int)blockIdx.x < items) {
-        if (tid == 0) tma::mbar_expect_tx(bar, PLANE);
-        __syncthreads();
-        if (tid < NQ) load_row(blockIdx.x, tid);
+    if (tid == 0) asm volatile("prefetch.tensormap [%0];" ::"l"(&smap) : "memory");
+    if ((int)blockIdx.x < items && tid == 0) {
+        tma::mbar_expect_tx(bar, PLANE);
+        for (int c = 0; c < NPART; ++c) load_part(blockIdx.x, c);
     }
     int k = 0;
     for (int item = blockIdx.x; item < items; item += gridDim.x, ++k) {
@@ -576,28 +370,34 @@ __global__ void __launch_bounds__(QCfg<NQ, TM>::NT, 1) k_q_mid(QArgs a, int I, i
         QPROF_T(q4);
         QPROF_ADD(3, q2, q4);
         // ---------------------------------------------------------------- I2: inverse axis 2, store, refill
+        // by parts of RP rows: once every team has finished a part, its rows take the next
+        // item's part (one TMA load), which then overlaps the rest of this item and the next
+        // item's tables
         V* dst = a.Y + (long long)item * (NQ * NQ);
 #pragma unroll 1
-        for (int j3 = q; j3 < NQ; j3 += TEAMS) {
-            V* row = X + j3 * P;
-            if (!skip) {
-                V x[R], pa[8], pb[8];
-                if (s_on<R>(t)) {
-                    const int sa = s_a<R>(t), sb = s_b<R>(t);
+        for (int c = 0; c < NPART; ++c) {
+#pragma unroll 1
+            for (int j3 = c * RP + q; j3 < (c + 1) * RP; j3 += TEAMS) {
+                V* row = X + j3 * P;
+                if (!skip) {
+                    V x[R], pa[8], pb[8];
+                    if (s_on<R>(t)) {
+                        const int sa = s_a<R>(t), sb = s_b<R>(t);
 #pragma unroll
-                    for (int qq = 0; qq < 8; ++qq) {
-                        pa[qq] = row[sa + R * qq];
-                        pb[qq] = row[sb + R * qq];
+                        for (int qq = 0; qq < 8; ++qq) {
+                            pa[qq] = row[sa + R * qq];
+                            pb[qq] = row[sb + R * qq];
+                        }
                     }
-                }
-                team_dft_dif<R, true>(pa, pb, x, row, tw, t, rs);   // x[r] = element j2 = t + 8r
+                    team_dft_dif<R, true>(pa, pb, x, row, tw, t, rs);   // x[r] = element j2 = t + 8r
 #pragma unroll
-                for (int r = 0; r < R; ++r) __stcg(dst + j3 * NQ + t + 8 * r, x[r]);
+                    for (int r = 0; r < R; ++r) __stcg(dst + j3 * NQ + t + 8 * r, x[r]);
+                }
             }
             if (nxt < items) {
-                tma::fence_proxy_async();                     // this lane's reads of the row precede the copy
-                __syncwarp();
-                if (t == 0) load_row(nxt, j3);
+                tma::fence_proxy_async();                     // this thread's reads of the part's rows
+                __syncthreads();                              // ... and everyone's precede the load
+                if (tid == 0) load_part(nxt, c);
             }
         }
         QPROF_T(q5);
@@ -985,56 +785,67 @@ static cudaError_t w_map(const QArgs& qa, int N, CUtensorMap* m) {
     return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
+// Tensor map of K1's spectrum S for K2's plane gathers: doubles, dims (innermost first) re/im 2,
+// k0 N, k1 H, j2 n2, (filter, j3) batch*n3; box 2 x 1 x 1 x (n2 + 1) x RP -- the j2 beyond n2 - 1 is
+// out of range (zero-filled) and pads each shared-memory row to n2 + 1 (conflict-free columns)
+static cudaError_t s_map(const QArgs& qa, int N, int H, CUtensorMap* m) {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    if (!encode) {
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&encode, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess || !encode) {
+            encode = nullptr;
+            return cudaErrorNotSupported;
+        }
+    }
+    const cuuint64_t n2 = qa.n2, n3 = qa.n3;
+    const cuuint32_t rp = qa.n2 < 32 ? (cuuint32_t)qa.n2 : 32;
+    cuuint64_t dims[5] = {2, (cuuint64_t)N, (cuuint64_t)H, n2, (cuuint64_t)qa.batch * n3};
+    cuuint64_t str[4] = {16, 16 * (cuuint64_t)N, 16 * (cuuint64_t)N * H, 16 * (cuuint64_t)N * H * n2};
+    cuuint32_t box[5] = {2, 1, 1, (cuuint32_t)(qa.n2 + 1), rp};
+    cuuint32_t es[5] = {1, 1, 1, 1, 1};
+    CUresult r = encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, (void*)qa.Yin, dims, str, box, es,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
 template <int NQ, int TM>
-static cudaError_t qmid_tm(const QArgs& qa, int I, int N0, int H1, cudaStream_t s) {
+static cudaError_t qmid_tm(const QArgs& qa, int I, int N0, int H1, const CUtensorMap& smap, cudaStream_t s) {
     using Cq = QCfg<NQ, TM>;
     const size_t smem = qmid_smem<NQ>();
     int grid = 1;
     cudaError_t e = q_grid(k_q_mid<NQ, TM>, Cq::NT, smem, (long long)qa.batch * I, &grid);
     if (e != cudaSuccess) return e;
-    k_q_mid<NQ, TM><<<grid, Cq::NT, smem, s>>>(qa, I, N0, H1);
+    k_q_mid<NQ, TM><<<grid, Cq::NT, smem, s>>>(qa, I, N0, H1, smap);
     return cudaGetLastError();
 }
 
 // (48 teams at NQ = 96 -- 12 warps, 168 registers -- measured 7 % slower than 32 teams)
 template <int NQ>
-static cudaError_t qmid_launch(const QArgs& qa, int I, int N0, int H1, cudaStream_t s) {
-    return qmid_tm<NQ, QCfg<NQ>::TEAMS>(qa, I, N0, H1, s);
+static cudaError_t qmid_launch(const QArgs& qa, int I, int N0, int H1, const CUtensorMap& smap, cudaStream_t s) {
+    return qmid_tm<NQ, QCfg<NQ>::TEAMS>(qa, I, N0, H1, smap, s);
 }
 
 // K1 -> K2 -> K3 (prep, the general-map pre-pass and the finaliser are the plane path's;
 // launch_plane calls this between them). Returns the K3 grid (its partials per filter).
 template <int N>
-static cudaError_t quad_n(const Dims& d, PencilBufs& b, QArgs qa, bool rg, bool up, cudaStream_t s, int64_t* launches,
+static cudaError_t quad_n(const Dims& d, PencilBufs& b, QArgs qa, bool up, cudaStream_t s, int64_t* launches,
                           int* ginv) {
     using Cf = Cfg<N>;
     cudaError_t e;
-    CUtensorMap ymap, wmap;
+    CUtensorMap smap, ymap, wmap;
+    if ((e = s_map(qa, N, Cf::H, &smap)) != cudaSuccess) return e;
     if ((e = y_map(qa, N, Cf::H, &ymap)) != cudaSuccess) return e;
     if ((e = w_map(qa, N, &wmap)) != cudaSuccess) return e;
-    {
-        const size_t smem = F1<N>::SMEM;
-        int grid = 1;
-        const long long units = (long long)d.batch * d.n[3] * (d.n[2] / 2);
-        if (rg) {
-            e = q_grid(k_q_fwd<N, true>, Cf::NT, smem, units, &grid);
-            if (e == cudaSuccess) k_q_fwd<N, true><<<grid, Cf::NT, smem, s>>>(qa);
-        } else {
-            e = q_grid(k_q_fwd<N, false>, Cf::NT, smem, units, &grid);
-            if (e == cudaSuccess) k_q_fwd<N, false><<<grid, Cf::NT, smem, s>>>(qa);
-        }
-        if (e != cudaSuccess) return e;
-        ++*launches;
-        if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    }
     if (b.ev0) cudaEventRecordWithFlags(b.ev0, s, cudaEventRecordExternal);
     {
         const int I = Cf::H * N;
         switch (d.n[2]) {
-            case 16: e = qmid_launch<16>(qa, I, N, Cf::H, s); break;
-            case 32: e = qmid_launch<32>(qa, I, N, Cf::H, s); break;
-            case 64: e = qmid_launch<64>(qa, I, N, Cf::H, s); break;
-            case 96: e = qmid_launch<96>(qa, I, N, Cf::H, s); break;
+            case 16: e = qmid_launch<16>(qa, I, N, Cf::H, smap, s); break;
+            case 32: e = qmid_launch<32>(qa, I, N, Cf::H, smap, s); break;
+            case 64: e = qmid_launch<64>(qa, I, N, Cf::H, smap, s); break;
+            case 96: e = qmid_launch<96>(qa, I, N, Cf::H, smap, s); break;
             default: e = cudaErrorInvalidValue;
         }
         if (e != cudaSuccess) return e;
@@ -1059,16 +870,15 @@ static cudaError_t quad_n(const Dims& d, PencilBufs& b, QArgs qa, bool rg, bool 
     return cudaGetLastError();
 }
 
-cudaError_t launch_quad(const Dims& d, PencilBufs& b, const ModelParams& mp, int range, bool rg, bool up,
-                        double* dcpart, double* dc3, double* part, cudaStream_t s, int64_t* launches, int* ginv) {
+cudaError_t launch_quad(const Dims& d, PencilBufs& b, const ModelParams& mp, int range, bool up, double* dcpart,
+                        double* dc3, double* part, cudaStream_t s, int64_t* launches, int* ginv) {
+    (void)dcpart;
     QArgs qa;
-    qa.Wsrc = (const double*)b.W;
-    qa.W2src = (const double*)b.W2;
     qa.W = (double*)b.W;
-    qa.Y = (V*)b.S;
+    qa.Yin = (const V*)b.S;
+    qa.Y = (V*)b.S2;
     qa.coef = b.coef;
     qa.cs = coef_stride(mp.l);
-    qa.dcpart = dcpart;
     qa.dc3 = dc3;
     qa.part = part;
     qa.batch = d.batch;
@@ -1078,9 +888,9 @@ cudaError_t launch_quad(const Dims& d, PencilBufs& b, const ModelParams& mp, int
     qa.step = mp.step;
     qa.range = range;
     switch (d.n[0]) {
-        case 32: return quad_n<32>(d, b, qa, rg, up, s, launches, ginv);
-        case 64: return quad_n<64>(d, b, qa, rg, up, s, launches, ginv);
-        case 96: return quad_n<96>(d, b, qa, rg, up, s, launches, ginv);
+        case 32: return quad_n<32>(d, b, qa, up, s, launches, ginv);
+        case 64: return quad_n<64>(d, b, qa, up, s, launches, ginv);
+        case 96: return quad_n<96>(d, b, qa, up, s, launches, ginv);
         default: return cudaErrorInvalidValue;
     }
 }

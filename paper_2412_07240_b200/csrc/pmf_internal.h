@@ -205,12 +205,13 @@ size_t plane_partials_doubles(const Dims& d);
 cudaError_t launch_plane(const Dims& d, int dtype, PencilBufs& b, const ModelParams& mp, const LikParams* lp,
                          double k_sigma /* < 0 = no regrid */, cudaStream_t s, int64_t* launches);
 
-// nx = 4 fp64 three-pass route (kernels_quad.cu): spectrum in the transposed layout
-// [filter][k1][k0][j3][j2]; called by launch_plane between its prep and finaliser
+// nx = 4 fp64 three-pass route (kernels_quad.cu): after the forward plane pass (spectrum
+// S[filter][j3][j2][k1][k0]), K2 writes S2 in the transposed layout [filter][k1][k0][j3][j2]
+// and K3 reads it; called by launch_plane between its forward pass and finaliser
 bool quad_supported(const Dims& d, int dtype);
 int quad_debug_counters(double* out, int n, int reset);
-cudaError_t launch_quad(const Dims& d, PencilBufs& b, const ModelParams& mp, int range, bool rg, bool up,
-                        double* dcpart, double* dc3, double* part, cudaStream_t s, int64_t* launches, int* ginv);
+cudaError_t launch_quad(const Dims& d, PencilBufs& b, const ModelParams& mp, int range, bool up, double* dcpart,
+                        double* dc3, double* part, cudaStream_t s, int64_t* launches, int* ginv);
 
 // FDM baseline predictor (eq:FST; kernels_fdm.cu): prep + DST-I passes on FP64 tensor
 // cores; the caller normalises (explicit sum) and runs the update

@@ -24,12 +24,9 @@ v = list(buf)
 for title, idx, cnt, names in (
         ("K2 k_q_mid, per item", 0, 5, ["tables (Psi + regrid taps)", "wait for the plane", "split regrid + F2",
                                         "F2..F3 end", "I2 + refill"]),
-        ("K1 k_q_fwd, per plane (store: per pair)", 6, 10, ["wait staged plane", "load z (+ in-plane regrid)",
-                                                           "P1 + P2 FFTs", "pair store"]),
         ("K3 k_q_inv, per plane", 11, 15, ["wait TMA plane", "inverse axis 0", "inverse axis 1",
                                           "likelihood + store + moments"])):
     n_ = v[cnt] or 1
     print(f"{title}: {n_:.0f} units; cycles per unit (thread 0 of each CTA):")
     for i, nm in enumerate(names):
-        div = n_ if not (idx == 6 and i < 3) else 2 * n_
-        print(f"  {nm:30s} {v[idx + i] / div:10.0f}")
+        print(f"  {nm:30s} {v[idx + i] / n_:10.0f}")
