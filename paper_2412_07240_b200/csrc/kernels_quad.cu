@@ -295,24 +295,19 @@ __global__ void __launch_bounds__(QCfg<NQ, TM>::NT, 1) k_q_mid(QArgs a, int I, i
             // ------------------------------------------------------------ [split regrid] + F2
             const bool rg = flag == 4;
             if (rg) {
-                int ia[R], ib[R];
-                double wa[R], wb[R];
-#pragma unroll
-                for (int r = 0; r < R; ++r) {
-                    const int u3 = t + 8 * r;
-                    ia[r] = j3t[2 * u3] * P;
-                    ib[r] = j3t[2 * u3 + 1] * P;
-                    wa[r] = w3t[2 * u3];
-                    wb[r] = w3t[2 * u3 + 1];
-                }
 #pragma unroll 1
                 for (int j2 = q; j2 < NQ; j2 += TEAMS) {
                     V* col = X + j2;
+                    int tt = t;
+                    asm volatile("" : "+r"(tt));              // taps re-read per column (broadcast), not hoisted
                     V z[R];
 #pragma unroll
                     for (int r = 0; r < R; ++r) {
-                        const V va = col[ia[r]], vb = col[ib[r]];
-                        z[r] = V{fma(wb[r], vb.x, wa[r] * va.x), fma(wb[r], vb.y, wa[r] * va.y)};
+                        const int u3 = tt + 8 * r;
+                        const int2 ij = reinterpret_cast<const int2*>(j3t)[u3];
+                        const double2 w = reinterpret_cast<const double2*>(w3t)[u3];
+                        const V va = col[ij.x * P], vb = col[ij.y * P];
+                        z[r] = V{fma(w.y, vb.x, w.x * va.x), fma(w.y, vb.y, w.x * va.y)};
                     }
                     __syncwarp();
 #pragma unroll
