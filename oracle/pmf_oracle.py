@@ -258,30 +258,16 @@ def psi_factor(D: np.ndarray, dt: float, n: tuple) -> np.ndarray:
     """One Euler factor psi_n over the full wavenumber grid (Alg. 3 P:333-336,
     Euler display P:313-318 read as R2):
 
-        psi = 1 / (1 + dt/2 [ sum_m D_mm kappa_m^2 + 2 sum_{m<m'} D_mm' kx_m kx_m' ])
+        psi = 1 / (1 + dt/2 q),   q = quad_form(D, n)
+            = 1 / (1 + dt/2 [ sum_m D_mm kappa_m^2 + 2 sum_{m<m'} D_mm' kx_m kx_m' ])
 
     kappa_m = 2 pi k_m / N_m (index coordinates, so -c''_m Q_mm = D_mm kappa_m^2
     on a diagonal grid); kx is kappa with the Nyquist wavenumber zeroed (R7: the
     first-derivative symbol drops Nyquist), the squared terms keep it
     (P:238). Pinned by test_spectral (S:440 golden, 0 < psi <= 1, psi(0) = 1)
-    and the dense brute-force solve (P4)."""
-    nx = len(n)
-    kap = []
-    kapx = []
-    for m, N in enumerate(n):
-        k = 2.0 * math.pi * wavenumbers(N) / N
-        kx = k.copy()
-        kx[N // 2] = 0.0
-        shape = [1] * nx
-        shape[m] = N
-        kap.append(k.reshape(shape))
-        kapx.append(kx.reshape(shape))
-    q = np.zeros(n)
-    for a in range(nx):
-        q = q + D[a, a] * kap[a] ** 2
-        for b in range(a + 1, nx):
-            q = q + 2.0 * D[a, b] * kapx[a] * kapx[b]
-    return 1.0 / (1.0 + 0.5 * dt * q)
+    and the dense brute-force solve (P4); the symbol itself is quad_form's (one copy,
+    shared with the Crank-Nicolson factors)."""
+    return 1.0 / (1.0 + 0.5 * dt * quad_form(D, n))
 
 
 def trace_factor(A, dt: float, l: int, sign: int = TRACE_SIGN_PHYSICAL) -> float:

@@ -18,6 +18,9 @@
 //       normalise by the DC coefficient (Alg. 6: sum w' = s sum w), likelihood
 //       (eq:filt P:46), store, moments -> normaliser C, mean and cov.
 // HBM traffic: read + write each weight once (16 B/point fp64).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
@@ -26,6 +29,24 @@
 #include "fft_reg.cuh"
 
 namespace pmf {
+
+// Phase cycle counters of the resident kernel (debug builds with -DPMF_QPROF only; thread 0
+// of every CTA adds its clock64() deltas; read with pmf_debug_counters index 16..).
+__device__ unsigned long long g_rprof[12];
+#ifdef PMF_QPROF
+#define RPROF_T(v) \
+    __syncthreads();  \
+    const long long v = clock64()
+#define RPROF_ADD(i, a, b) \
+    if (threadIdx.x == 0) atomicAdd(&g_rprof[i], (unsigned long long)((b) - (a)))
+#define RPROF_SET(v) \
+    __syncthreads();   \
+    v = clock64()
+#else
+#define RPROF_SET(v)
+#define RPROF_T(v)
+#define RPROF_ADD(i, a, b)
+#endif
 
 namespace res {
 
@@ -366,8 +387,16 @@ __device__ __forceinline__ double warp_sum8(const double* v, int lane) {
 }
 
 // ============================================================================ the fused epoch kernel
+// weight staging rows for the TMA store: 128 values + padding (16-byte rows; the padding lies
+// beyond j0 = 127 of the box and is not written)
+template <typename T> struct WsPitch;
+template <> struct WsPitch<double> { static constexpr int P = 130; };
+template <> struct WsPitch<float> { static constexpr int P = 132; };
+template <typename T> __host__ __device__ constexpr size_t ws_bytes() { return (size_t)64 * WsPitch<T>::P * sizeof(T); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+
 template <typename T, bool REGRID, bool UPDATE, bool CN>
-__global__ void __launch_bounds__(NT, 1) k_resident_epoch(ResArgs<T> a) {
+__global__ void __launch_bounds__(NT, 1) k_resident_epoch(ResArgs<T> a, const __grid_constant__ CUtensorMap wmap) {
     using V = typename C2<T>::type;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     V* X = reinterpret_cast<V*>(smem_raw);                          // [H][PITCH]; also the dense staging area
@@ -379,6 +408,9 @@ __global__ void __launch_bounds__(NT, 1) k_resident_epoch(ResArgs<T> a) {
     double* dcs = red + 16 * 6;                                     // DC of the current filter
     unsigned long long* bar = reinterpret_cast<unsigned long long*>(dcs + 2);
     double* pb0 = reinterpret_cast<double*>(bar + 2);               // 2 x pstride parameter buffers
+    T* Ws = reinterpret_cast<T*>(smem_raw + ((XBYTES + sizeof(V) * 128 + 16 * 6 * sizeof(double) + 2 * sizeof(double) +
+                                             2 * sizeof(unsigned long long) + 2 * sizeof(double) * a.pstride + 127) /
+                                            128 * 128));            // 64 x WsPitch staged weight rows
 
     const int tid = threadIdx.x;
     const int m = tid >> 3, t = tid & 7;
@@ -404,7 +436,13 @@ __global__ void __launch_bounds__(NT, 1) k_resident_epoch(ResArgs<T> a) {
         const double* P = pb0 + (it & 1) * a.pstride;
         double* Pn = pb0 + ((it + 1) & 1) * a.pstride;
         const int nxt = filt + gridDim.x;
+        RPROF_T(c0);
         mbar_wait(bar, it & 1);                 // weights + constants of this filter are in shared memory
+        RPROF_T(c1);
+        RPROF_ADD(0, c0, c1);
+#ifdef PMF_QPROF
+        long long c2 = 0;
+#endif
 
         if (warp == 0 && lane < 8 && nxt < a.batch) {
             // pull the next filter's weights into L2 now; its TMA staging (issued late in P3,
@@ -481,6 +519,8 @@ __global__ void __launch_bounds__(NT, 1) k_resident_epoch(ResArgs<T> a) {
                 }
             }
             __syncthreads();                      // the staged weights are consumed: X is free
+            RPROF_SET(c2);
+            RPROF_ADD(1, c1, c2);
             dft16<false>(z);                      // over r: Y_t(s)
 #pragma unroll
             for (int s = 1; s < 16; ++s) z[s] = cmul(z[s], tw[s * 8 + t]);
@@ -516,6 +556,8 @@ __global__ void __launch_bounds__(NT, 1) k_resident_epoch(ResArgs<T> a) {
         }
         __syncthreads();
 
+        RPROF_T(c3);
+        RPROF_ADD(2, c2, c3);
         // ---------------------------------------------------------------- P2: rows, FFT axis 0, s Psi / N^2, inverse
         {
             V x[16];
@@ -710,6 +752,8 @@ __global__ void __launch_bounds__(NT, 1) k_resident_epoch(ResArgs<T> a) {
         }
         __syncthreads();
 
+        RPROF_T(c4);
+        RPROF_ADD(3, c3, c4);
         // ---------------------------------------------------------------- P3: inverse axis 1, normalise, update
         {
             V pa[8], pb[8];
@@ -754,6 +798,8 @@ __global__ void __launch_bounds__(NT, 1) k_resident_epoch(ResArgs<T> a) {
                 qe[e] = fma(2.0 * P[P_QG + 1], u0, P[P_QB + 1]);
             }
             __syncthreads();                      // X is consumed
+            RPROF_T(c5);
+            RPROF_ADD(4, c4, c5);
             zero_ring<T>(smem_raw, tid);          // visible to the gather after the end-of-filter barrier
             if (nxt < a.batch) stage(a, nxt, smem_raw, Pn, bar, tid);   // overlaps the rest of P3
 #pragma unroll
@@ -763,6 +809,8 @@ __global__ void __launch_bounds__(NT, 1) k_resident_epoch(ResArgs<T> a) {
                 x[s] = cmul(x[s], w);
             }
             dft16<true>(x);                       // x[r] = w(2m, t+8r) + i w(2m+1, t+8r) (unnormalised)
+            RPROF_T(d1);
+            RPROF_ADD(7, c5, d1);
             // Likelihood (linear Gauss): along this thread's column e the exponent is a quadratic
             // in r (u1 = u1_0 + 8 r): E(r) = E0 + E1 r + E2 r^2, so L(r+1) = L(r) R(r) and
             // R(r+1) = R(r) exp(2 E2) -- two multiplies per point. Used when every partial
@@ -798,10 +846,13 @@ __global__ void __launch_bounds__(NT, 1) k_resident_epoch(ResArgs<T> a) {
                 }
                 return wt;
             };
+            // the filter's new weights leave through shared memory (rows of pitch WSP, two halves of
+            // 64 rows) and a tensor-map TMA store each -- 1 KB rows instead of per-thread 64-byte
+            // row pieces (measured: the strided stores cost ~15 % of the kernel) -- whenever every
+            // thread has its outputs in registers (CTA-uniform); the generic likelihood path stores
+            // directly
+            const bool staged = __syncthreads_and(!UPDATE || rec);
             if (!UPDATE) {
-#pragma unroll
-                for (int r = 0; r < 16; ++r)
-                    *reinterpret_cast<V*>(Wf + (t + 8 * r) * N + 2 * m) = V{(T)(double)x[r].x, (T)(double)x[r].y};
             } else if (rec) {
 #pragma unroll
                 for (int r = 0; r < 16; ++r) {
@@ -811,7 +862,8 @@ __global__ void __launch_bounds__(NT, 1) k_resident_epoch(ResArgs<T> a) {
                     Rr[0] *= Gr[0];
                     Lr[1] *= Rr[1];
                     Rr[1] *= Gr[1];
-                    *reinterpret_cast<V*>(Wf + (t + 8 * r) * N + 2 * m) = V{o0, o1};
+                    if (staged) x[r] = V{o0, o1};
+                    else *reinterpret_cast<V*>(Wf + (t + 8 * r) * N + 2 * m) = V{o0, o1};
                 }
             } else {
 #pragma unroll 1
@@ -851,6 +903,28 @@ __global__ void __launch_bounds__(NT, 1) k_resident_epoch(ResArgs<T> a) {
                     }
                 }
             }
+            RPROF_T(d2);
+            RPROF_ADD(8, d1, d2);
+            if (staged) {
+                constexpr int WSP = WsPitch<T>::P;
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    if (tid == 0) bulk_wait_read0();                 // the previous half's store has read Ws
+                    __syncthreads();
+#pragma unroll
+                    for (int r = 8 * h; r < 8 * h + 8; ++r)
+                        *reinterpret_cast<V*>(Ws + (t + 8 * (r - 8 * h)) * WSP + 2 * m) = x[r];
+                    __syncthreads();
+                    if (tid == 0) {
+                        fence_proxy_async();
+                        asm volatile(
+                            "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(&wmap),
+                            "r"(0), "r"(64 * h), "r"(filt), "r"(smem_u32(Ws))
+                            : "memory");
+                        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                    }
+                }
+            }
             double acc[6];
             {
                 const double ua = (2 * m) - 0.5 * (N - 1), ub = ua + 1.0;
@@ -877,8 +951,23 @@ __global__ void __launch_bounds__(NT, 1) k_resident_epoch(ResArgs<T> a) {
                 if (lane == 6) v = *dcs;
                 if (lane < 7) a.out[(long long)filt * 8 + lane] = v;
             }
+            RPROF_T(c6);
+            RPROF_ADD(5, c5, c6);
+            RPROF_ADD(6, 0, 1);
         }
     }
+    if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+int resident_debug_counters(double* out, int n, int reset) {
+    unsigned long long h[12];
+    if (cudaMemcpyFromSymbol(h, g_rprof, sizeof(h)) != cudaSuccess) return -1;
+    for (int i = 0; i < n && i < 12; ++i) out[i] = (double)h[i];
+    if (reset) {
+        std::fill(h, h + 12, 0ull);
+        cudaMemcpyToSymbol(g_rprof, h, sizeof(h));
+    }
+    return 0;
 }
 
 bool resident_supported(const Dims& d, int dtype) {
@@ -888,14 +977,41 @@ bool resident_supported(const Dims& d, int dtype) {
 
 size_t resident_param_bytes(int l, int batch) { return sizeof(double) * (size_t)prm_stride(l) * batch; }
 
+// Tensor map of the weights [batch][128][128] for the kernel's row stores: box
+// WsPitch x 64 x 1 -- the staged rows' padding lies beyond j0 = 127 and is not written
+template <typename T>
+static cudaError_t w_map(T* W, int batch, CUtensorMap* m) {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    if (!encode) {
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&encode, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess || !encode) {
+            encode = nullptr;
+            return cudaErrorNotSupported;
+        }
+    }
+    cuuint64_t dims[3] = {(cuuint64_t)N, (cuuint64_t)N, (cuuint64_t)batch};
+    cuuint64_t str[2] = {sizeof(T) * (cuuint64_t)N, sizeof(T) * (cuuint64_t)N * N};
+    cuuint32_t box[3] = {(cuuint32_t)WsPitch<T>::P, 64, 1};
+    cuuint32_t es[3] = {1, 1, 1};
+    CUresult r = encode(m, sizeof(T) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void*)W,
+                        dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
 template <typename T, bool RG, bool UP, bool CN>
 static cudaError_t launch_t(ResArgs<T> a, cudaStream_t s, int64_t* launches, cudaEvent_t ev0, cudaEvent_t ev1) {
     using V = typename C2<T>::type;
     const size_t xbytes = std::max<size_t>(sizeof(V) * H * PITCH, stage_bytes<T>());
-    const size_t smem = xbytes + sizeof(V) * 128 + 16 * 6 * sizeof(double) + 2 * sizeof(double) +
+    const size_t base = xbytes + sizeof(V) * 128 + 16 * 6 * sizeof(double) + 2 * sizeof(double) +
                         2 * sizeof(unsigned long long) + 2 * sizeof(double) * (size_t)a.pstride;
+    const size_t smem = (base + 127) / 128 * 128 + ws_bytes<T>();
+    CUtensorMap wmap;
+    cudaError_t e = w_map<T>(a.W, a.batch, &wmap);
+    if (e != cudaSuccess) return e;
     auto kern = k_resident_epoch<T, RG, UP, CN>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int dev = 0, nsm = 148, occ = 1;
     cudaGetDevice(&dev);
@@ -905,7 +1021,7 @@ static cudaError_t launch_t(ResArgs<T> a, cudaStream_t s, int64_t* launches, cud
     if (occ < 1) return cudaErrorInvalidConfiguration;
     const int grid = std::min(a.batch, nsm * occ);
     if (ev0) cudaEventRecordWithFlags(ev0, s, cudaEventRecordExternal);
-    kern<<<grid, NT, smem, s>>>(a);
+    kern<<<grid, NT, smem, s>>>(a, wmap);
     if (ev1) cudaEventRecordWithFlags(ev1, s, cudaEventRecordExternal);
     ++*launches;
     return cudaGetLastError();

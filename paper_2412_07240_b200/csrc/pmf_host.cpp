@@ -1075,4 +1075,8 @@ int pmf_epoch_kernel(const pmf_ctx* c) { return c ? c->epoch_kernel : -1; }
 
 // Debug only (not in pmf.h): per-phase cycle counters of the nx = 4 three-pass kernels in
 // builds compiled with -DPMF_QPROF (tools/qprof.py); zeros otherwise.
-extern "C" int pmf_debug_counters(double* out, int n, int reset) { return quad_debug_counters(out, n, reset); }
+extern "C" int pmf_debug_counters(double* out, int n, int reset) {
+    int r = quad_debug_counters(out, n < 16 ? n : 16, reset);
+    if (r == 0 && n > 16) r = resident_debug_counters(out + 16, n - 16, reset);
+    return r;
+}

@@ -210,6 +210,7 @@ cudaError_t launch_plane(const Dims& d, int dtype, PencilBufs& b, const ModelPar
 // and K3 reads it; called by launch_plane between its forward pass and finaliser
 bool quad_supported(const Dims& d, int dtype);
 int quad_debug_counters(double* out, int n, int reset);
+int resident_debug_counters(double* out, int n, int reset);
 cudaError_t launch_quad(const Dims& d, PencilBufs& b, const ModelParams& mp, int range, bool up, double* dcpart,
                         double* dc3, double* part, cudaStream_t s, int64_t* launches, int* ginv);
 

@@ -3,9 +3,10 @@ launch configuration bench.py times where it applies:
 
 * C2 (one 256^2 filter, all 100 epochs) and C3 (one 128^3 filter, 2 epochs): the oracle
   runs them whole; every epoch's weights, moments, normaliser and grid are compared.
-* C5 (4096 filters x 128^2, the bench workload): the whole batch runs on the GPU with
-  the fused pmf_step API (as bench.py), the oracle runs a sample of filters one by one;
-  per-epoch moments/normaliser and the final weights and grid of the sampled filters.
+* C5 (4096 filters x 128^2, all 50 epochs): the whole batch runs on the GPU with the fused
+  pmf_step API (as bench.py), the oracle runs a sample of filters one by one (first, middle
+  and last -- partial -- CTA rounds); per-epoch moments/normaliser and the final weights and
+  grid of the sampled filters.
 * C4 (96^4 = 85M points): too large for the oracle's O(N^2) DFTs, so a property that
   holds at any size pins it: the predicted mean and covariance equal the scheme's
   closed form e^{At}m and the Riemann-sum Kalman-Bucy covariance (P6) of the sampled
@@ -51,15 +52,20 @@ def test_c5_all_epochs_resident_vs_oracle():
 
 
 def test_full_size_c5_batch_sampled_vs_oracle():
+    """The whole 4096-filter batch for all 50 epochs through bench.py's pmf_step call;
+    sampled filters from every CTA round of the persistent kernel (148 CTAs walk filters
+    b = blockIdx + 148 j): the first round, a middle one and the last, partial round
+    (filters 3996..4095 run on CTAs 0..99), against the oracle every epoch."""
     cfg = make_config("C5")
     assert cfg.batch == 4096
-    T = 3
+    T = cfg.T
+    assert T == 50
     zs = simulate(cfg, T=T)["z"]
     f = make_filter(cfg)
     assert f.path == pmf.PATH_RESIDENT
     lik = lik_of(cfg)
     dt = cfg.tau / cfg.l
-    sample = [0, 1, 1023, 2048, 3071, 4095]
+    sample = [0, 1, 147, 148, 1023, 2048, 3995, 3996, 4050, 4095]
     rec = []
     for k in range(T + 1):
         if k == 0:
@@ -131,3 +137,53 @@ def test_full_size_c4_predict_moments_closed_form():
                                    for s in range(l))
     assert np.max(np.abs(mean - F @ m0)) < 1e-11 * math.sqrt(np.max(np.diag(covx)))
     assert rel_linf(cov, covx) < 1e-10
+
+
+def _golden(name):
+    import os
+    p = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", name)
+    if not os.path.exists(p):
+        pytest.skip(f"{name} missing (tools/make_golden.py)")
+    return np.load(p)
+
+
+@pytest.mark.parametrize("cid, T", [("C3", 50), ("C4", 1)])
+def test_full_size_run_vs_oracle_fixture(cid, T):
+    """BASELINE C3 (128^3, all 50 epochs) and C4 (96^4 = 85 M points, epochs 0-1) at full
+    size, in bench.py's launch configuration (the plane path; C4 on the three-pass route),
+    against the oracle's run of the same seeded inputs: tests/golden/<cfg>_full_T<T>.npz,
+    written by tools/make_golden.py (oracle/ only). Every epoch: moments, normaliser and
+    grid, and the posterior weights element by element at 8192 (C4) / 2048 (C3) seeded
+    positions plus the peak, relative to the oracle's peak |w|; then the final regridded
+    weights."""
+    G = _golden(f"{cid.lower()}_full_T{T}.npz")
+    cfg = make_config(cid)
+    zs = simulate(cfg, T=T)["z"]
+    f = make_filter(cfg)
+    assert f.path == pmf.PATH_PLANE
+    lik = lik_of(cfg)
+    dt = cfg.tau / cfg.l
+    for k in range(T + 1):
+        if k > 0:
+            f.predict(dt, cfg.l)
+        f.update(zs[k], lik)
+        mean, cov, logc = f.moments()
+        c, B = f.grid()
+        sd = math.sqrt(np.max(np.linalg.eigvalsh(G[f"cov_{k}"])))
+        assert np.max(np.abs(mean[0] - G[f"mean_{k}"])) / sd < 1e-10, k
+        assert rel_linf(cov[0], G[f"cov_{k}"]) < 1e-10, k
+        assert abs(logc[0] - float(G[f"logC_{k}"])) < 1e-10, k
+        assert rel_linf(B[0], G[f"B_{k}"]) < 1e-10, k
+        assert np.max(np.abs(c[0] - G[f"c_{k}"])) < 1e-10 * np.max(np.abs(G[f"B_{k}"])), k
+        if k == T or cid == "C4" or k % 10 == 0:
+            w = f.weights()[0].reshape(-1)
+            ii = G[f"idx_{k}"]
+            peak = float(G[f"peak_{k}"])
+            assert abs(float(np.max(np.abs(w))) - peak) <= 1e-10 * peak, k
+            assert float(np.max(np.abs(w[ii] - G[f"w_{k}"]))) <= 1e-10 * peak, k
+            del w
+        f.regrid(cfg.k_sigma)
+    w = f.weights()[0].reshape(-1)                           # flushes the last regrid
+    c, B = f.grid()
+    assert float(np.max(np.abs(w[G["idx"]] - G["w_final"]))) <= 1e-10 * float(G["peak_final"])
+    assert rel_linf(B[0], G["B_final"]) < 1e-12
