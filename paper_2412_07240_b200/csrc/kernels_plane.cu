@@ -375,8 +375,16 @@ __global__ void __launch_bounds__(Cfg<N>::NT, Cfg<N>::MINB) k_plane_fwd(PlaneArg
         if (tid == 0) a.dcpart[p] = (double)X[0].x;           // sum of the plane's input weights
         if (tid < H) {                                        // one bulk store per spectrum row
             tma::fence_proxy_async();
-            tma::bulk_s2g(a.S + (long long)p * (H * N) + (long long)tid * N, X + tid * PITCH,
-                          (unsigned)(N * sizeof(V)));
+            if (a.chunks == 1) {
+                tma::bulk_s2g(a.S + (long long)p * (H * N) + (long long)tid * N, X + tid * PITCH,
+                              (unsigned)(N * sizeof(V)));
+            } else {
+                // sharded: k0 range q of the row to destination rank q's block
+                const int Nc = N / a.chunks;
+                for (int q = 0; q < a.chunks; ++q)
+                    tma::bulk_s2g(a.S + q * a.chunk_stride + ((long long)p * H + tid) * Nc, X + tid * PITCH + q * Nc,
+                                  (unsigned)(Nc * sizeof(V)));
+            }
             tma::bulk_commit();
         }
         if (!SEP) {
@@ -1322,6 +1330,66 @@ static cudaError_t plane_n(const Dims& d, PencilBufs& b, const ModelParams& mp, 
         case 128: return plane_t<T, 128, NX>(d, b, mp, lp, ks, s, launches);
         default: return cudaErrorInvalidValue;
     }
+}
+
+// sharded nx = 4 fp64 route (pmf_sharded.cpp): the plane prep without a regrid, and the forward
+// plane pass over the shard's planes writing each spectrum row in `chunks` k0 pieces, piece q
+// to S + q chunk_stride (the all-to-all send blocks)
+cudaError_t launch_plane_prep(const Dims& d, PencilBufs& b, const ModelParams& mp, const LikParams* lp, cudaStream_t s,
+                              int64_t* launches) {
+    LikParams lpv = lp ? *lp : LikParams{};
+    k_plane_prep<4><<<d.batch, 32, 0, s>>>(b.st, b.coef, coef_stride(mp.l), mp, b.sub, lpv, b.z, -1.0, lp ? 1 : 0, d);
+    ++*launches;
+    return cudaGetLastError();
+}
+
+template <int N>
+static cudaError_t fwd_chunks_n(const Dims& d, PencilBufs& b, const ModelParams& mp, int chunks,
+                                long long chunk_stride, double* dcpart, cudaStream_t s, int64_t* launches) {
+    using Cf = Cfg<N>;
+    PlaneArgs<double> pa{};
+    pa.Wsrc = (const double*)b.W;
+    pa.W2src = (const double*)b.W;
+    pa.W = (double*)b.W;
+    pa.S = (double2*)b.S;
+    pa.Sinv = (double2*)b.S;
+    pa.coef = b.coef;
+    pa.cs = coef_stride(mp.l);
+    pa.ppf = d.n[2] * d.n[3];
+    pa.nplanes = pa.ppf * d.batch;
+    pa.dcpart = dcpart;
+    pa.n2 = d.n[2];
+    pa.n3 = d.n[3];
+    pa.l = mp.l;
+    pa.chunks = chunks;
+    pa.chunk_stride = chunk_stride;
+    const size_t smem = fwd_smem<double, N>();
+    int grid = 1;
+    cudaError_t e = occ_grid(k_plane_fwd<double, N, 4, false>, Cf::NT, smem, pa.nplanes, &grid);
+    if (e != cudaSuccess) return e;
+    k_plane_fwd<double, N, 4, false><<<grid, Cf::NT, smem, s>>>(pa);
+    ++*launches;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_plane_fwd_chunks(const Dims& d, PencilBufs& b, const ModelParams& mp, int chunks,
+                                    long long chunk_stride, double* dcpart, cudaStream_t s, int64_t* launches) {
+    switch (d.n[0]) {
+        case 32: return fwd_chunks_n<32>(d, b, mp, chunks, chunk_stride, dcpart, s, launches);
+        case 64: return fwd_chunks_n<64>(d, b, mp, chunks, chunk_stride, dcpart, s, launches);
+        case 96: return fwd_chunks_n<96>(d, b, mp, chunks, chunk_stride, dcpart, s, launches);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+// the plane finaliser from per-filter totals tot[16] = {15 index-space moment sums, DC}
+// (ppf = n3 = ginv = 1: k_plane_fin then reads exactly these)
+cudaError_t launch_plane_fin_tot(const Dims& d, PencilBufs& b, const ModelParams& mp, double* tot, int update,
+                                 cudaStream_t s, int64_t* launches) {
+    k_plane_fin<4><<<d.batch, 256, 0, s>>>(b.st, b.coef, coef_stride(mp.l), tot + NMOM, tot + NMOM, tot, 1, 1, 1,
+                                           update);
+    ++*launches;
+    return cudaGetLastError();
 }
 
 cudaError_t launch_plane(const Dims& d, int dtype, PencilBufs& b, const ModelParams& mp, const LikParams* lp,

@@ -53,15 +53,23 @@ __device__ unsigned long long g_qprof[16];
 struct QArgs {
     double* W;               // weights written by K3
     const V* Yin;            // K1's spectrum S[filter][j3][j2][k1][k0] (K2's input)
-    V* Y;                    // S2[filter][k1][k0][j3][j2] (K2's output, K3's input)
+    V* Y;                    // S2[filter][k0][k1][j3][j2] (K2's output, K3's input)
     const double* coef;
     int cs;
     double* dc3;             // [filter][n3] the regridded sums (split maps; K2)
     double* part;            // [filter][K3 CTAs][NMOM]
     int batch;
-    int n2, n3;              // plane sizes (n2 == n3 == NQ)
+    int n2, n3;              // plane sizes (n2 == n3 == NQ) of this block (K3: its j3 slab)
     int l, step;
     int range;               // likelihood kind 1 (range), else linear Gauss
+    // slab sharding over G ranks (unsharded: G = 1, koff = 0, j3off = 0, slab = n3g = n3):
+    // K2 runs the k0 range [koff, koff + N0/G) and writes output row j3 to rank j3 / slab's
+    // block; K3 runs the planes j3 in [j3off, j3off + slab) of n3g
+    int N0f;                 // N_0 (wavenumbers)
+    int koff;
+    int G, slab, j3off, n3g;
+    // S2 layout: G == 1 -> [filter][k1][k0][j3][j2]; G > 1 -> per destination block
+    // [k0][k1][j3 % slab][j2] (k0 outermost, so the back exchange stacks the blocks into k0)
 };
 
 // ============================================================================ K2: contiguous (j3, j2)-planes
@@ -228,11 +236,11 @@ __global__ void __launch_bounds__(QCfg<NQ, TM>::NT, 1) k_q_mid(QArgs a, int I, i
             const double* cf = Pg + PL_EU;
             const int cn = a.step, l = a.l;
             const unsigned k1 = i / (unsigned)N0;
-            const int k0 = (int)(i - k1 * (unsigned)N0);
+            const int N0f = a.N0f, k0 = a.koff + (int)(i - k1 * (unsigned)N0);   // global k0
             const int N1 = 2 * (H1 - 1);
             double kap[3], kx[3];
-            kap[0] = (2.0 * PMF_PI / N0) * (k0 < N0 / 2 ? k0 : k0 - N0);
-            kx[0] = (2 * k0 == N0) ? 0.0 : kap[0];
+            kap[0] = (2.0 * PMF_PI / N0f) * (k0 < N0f / 2 ? k0 : k0 - N0f);
+            kx[0] = (2 * k0 == N0f) ? 0.0 : kap[0];
             kap[1] = (2.0 * PMF_PI / N1) * (int)k1;
             kx[1] = (2 * (int)k1 == N1) ? 0.0 : kap[1];
             const double mult = Pc[PL_SN];
@@ -341,7 +349,7 @@ __global__ void __launch_bounds__(QCfg<NQ, TM>::NT, 1) k_q_mid(QArgs a, int I, i
 #pragma unroll
                 for (int r = 0; r < R; ++r) x[r] = col[(t + 8 * r) * P];
                 team_dft<R, false>(x, pa, pb, col, tw, t, cs);
-                if (flag == 4 && i == 0 && k2 == 0 && t == 0) {
+                if (flag == 4 && i == 0 && a.koff == 0 && k2 == 0 && t == 0) {
                     // (k0, k1, k2, k3) = 0: the sum of the regridded weights
                     a.dc3[(long long)f * a.n3] = pa[0].x;
                     for (int j = 1; j < a.n3; ++j) a.dc3[(long long)f * a.n3 + j] = 0.0;
@@ -368,7 +376,13 @@ __global__ void __launch_bounds__(QCfg<NQ, TM>::NT, 1) k_q_mid(QArgs a, int I, i
         // by parts of RP rows: once every team has finished a part, its rows take the next
         // item's part (one TMA load), which then overlaps the rest of this item and the next
         // item's tables
-        V* dst = a.Y + (long long)item * (NQ * NQ);
+        // output row j3 of this item: G == 1: S2[f][k1][k0][j3][j2]; G > 1: S2 (rank j3 / slab's
+        // block)[k0][k1][j3 % slab][j2]. (Measured: the k0-major order for G == 1 doubles K3's
+        // DRAM reads of S2 -- the same sectors, gathered in a different order, miss L2.)
+        const unsigned ok1 = i / (unsigned)N0, ok0 = i - ok1 * (unsigned)N0;
+        V* dst = a.Y + (long long)f * ((long long)a.G * N0 * H1 * a.slab * NQ) +
+                 (a.G == 1 ? (long long)i : ((long long)ok0 * H1 + ok1)) * ((long long)a.slab * NQ);
+        const long long rstride = (long long)N0 * H1 * a.slab * NQ;      // between destination blocks
 #pragma unroll 1
         for (int c = 0; c < NPART; ++c) {
 #pragma unroll 1
@@ -385,8 +399,12 @@ __global__ void __launch_bounds__(QCfg<NQ, TM>::NT, 1) k_q_mid(QArgs a, int I, i
                         }
                     }
                     team_dft_dif<R, true>(pa, pb, x, row, tw, t, rs);   // x[r] = element j2 = t + 8r
+                    {
+                        const int rk = j3 / a.slab, j3l = j3 - rk * a.slab;
+                        V* o = dst + rk * rstride + j3l * NQ + t;
 #pragma unroll
-                    for (int r = 0; r < R; ++r) __stcg(dst + j3 * NQ + t + 8 * r, x[r]);
+                        for (int r = 0; r < R; ++r) __stcg(o + 8 * r, x[r]);
+                    }
                 }
             }
             if (nxt < items) {
@@ -472,7 +490,8 @@ __global__ void __launch_bounds__(Cfg<N>::NT, 1) k_q_inv(QArgs a, const __grid_c
         asm volatile(
             "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, "
             "%6}], [%7];" ::"r"(tma::smem_u32(X0 + buf * XSV)),
-            "l"(&ymap), "r"(0), "r"(j2), "r"(j3), "r"(0), "r"(f * H), "r"(tma::smem_u32(&bar[buf]))
+            "l"(&ymap), "r"(0), "r"(a.G == 1 ? 0 : f * N), "r"(a.G == 1 ? f * H : 0), "r"(j2), "r"(j3),
+            "r"(tma::smem_u32(&bar[buf]))
             : "memory");
     };
     issue(blockIdx.x, 0);
@@ -576,7 +595,7 @@ __global__ void __launch_bounds__(Cfg<N>::NT, 1) k_q_inv(QArgs a, const __grid_c
             store_plane();
             continue;
         }
-        const double u2 = j2 - 0.5 * (n2 - 1), u3 = j3 - 0.5 * (n3 - 1);
+        const double u2 = j2 - 0.5 * (n2 - 1), u3 = (a.j3off + j3) - 0.5 * (a.n3g - 1);   // global j3
         const double u10 = t - 0.5 * (N - 1);
         const double lgn = P[PL_LGN];
         double S[2] = {0, 0}, Tm[2] = {0, 0}, U[2] = {0, 0};
@@ -698,6 +717,31 @@ __global__ void __launch_bounds__(Cfg<N>::NT, 1) k_q_inv(QArgs a, const __grid_c
 
 using namespace pln;
 
+// sharded route: one shard's totals tot[16] = {K3's 15 index-space moment sums over its CTAs,
+// the DC (sum of K1's per-plane input sums)} in a fixed order (block tree), all-reduced next
+__global__ void k_shard_sum(const double* __restrict__ dcpart, int nplanes, const double* __restrict__ part, int ginv,
+                            int update, double* tot) {
+    __shared__ double red[32 * 16];
+    double acc[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) acc[i] = 0.0;
+    for (int p = threadIdx.x; p < nplanes; p += blockDim.x) acc[15] += dcpart[p];
+    if (update)
+        for (int c = threadIdx.x; c < ginv; c += blockDim.x)
+#pragma unroll
+            for (int i = 0; i < NMOM; ++i) acc[i] += part[(long long)c * NMOM + i];
+    block_sum<16>(acc, red);
+    if (threadIdx.x == 0)
+        for (int i = 0; i < 16; ++i) tot[i] = acc[i];
+}
+
+cudaError_t launch_shard_sum(const double* dcpart, int nplanes, const double* part, int ginv, int update, double* tot,
+                             cudaStream_t s, int64_t* launches) {
+    k_shard_sum<<<1, 256, 0, s>>>(dcpart, nplanes, part, ginv, update, tot);
+    ++*launches;
+    return cudaGetLastError();
+}
+
 // debug: read (and optionally reset) the phase counters of -DPMF_QPROF builds
 int quad_debug_counters(double* out, int n, int reset) {
     unsigned long long h[16];
@@ -746,10 +790,21 @@ static cudaError_t y_map(const QArgs& qa, int N, int H, CUtensorMap* m) {
             return cudaErrorNotSupported;
         }
     }
-    const cuuint64_t n2 = qa.n2, n3 = qa.n3;
-    cuuint64_t dims[5] = {2, n2, n3, (cuuint64_t)N, (cuuint64_t)qa.batch * H};
-    cuuint64_t str[4] = {16, 16 * n2, 16 * n2 * n3, 16 * n2 * n3 * (cuuint64_t)N};
-    cuuint32_t box[5] = {2, 1, 1, (cuuint32_t)(N + 2), (cuuint32_t)H};
+    // S2 = [filter, k0][k1][j3 (this block's slab)][j2] (filter and k0 merged: adjacent); the dims
+    // are listed innermost-first as re/im, (filter, k0), k1, j2, j3 -- the box (2, N + 2, H, 1, 1)
+    // lands as [k1][k0 + 2 padding] (the padding reads beyond k0 = N - 1: out of range for the
+    // last filter, the next filter's first k0 otherwise -- never used)
+    const cuuint64_t n2 = qa.n2, sl = qa.n3;
+    cuuint64_t dims[5] = {2, (cuuint64_t)qa.batch * N, (cuuint64_t)H, n2, sl};
+    cuuint64_t str[4] = {16 * (cuuint64_t)H * sl * n2, 16 * sl * n2, 16, 16 * n2};
+    if (qa.G == 1) {
+        // S2 = [filter][k1][k0][j3][j2]: dims re/im, k0, (filter, k1) merged, j2, j3
+        dims[1] = (cuuint64_t)N;
+        dims[2] = (cuuint64_t)qa.batch * H;
+        str[0] = 16 * sl * n2;
+        str[1] = 16 * sl * n2 * (cuuint64_t)N;
+    }
+    cuuint32_t box[5] = {2, (cuuint32_t)(N + 2), (cuuint32_t)H, 1, 1};
     cuuint32_t es[5] = {1, 1, 1, 1, 1};
     CUresult r = encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, (void*)qa.Y, dims, str, box, es,
                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -825,49 +880,44 @@ static cudaError_t qmid_launch(const QArgs& qa, int I, int N0, int H1, const CUt
 // K1 -> K2 -> K3 (prep, the general-map pre-pass and the finaliser are the plane path's;
 // launch_plane calls this between them). Returns the K3 grid (its partials per filter).
 template <int N>
-static cudaError_t quad_n(const Dims& d, PencilBufs& b, QArgs qa, bool up, cudaStream_t s, int64_t* launches,
-                          int* ginv) {
+static cudaError_t quad_mid_n(const Dims& d, QArgs qa, int N0c, cudaStream_t s) {
     using Cf = Cfg<N>;
+    CUtensorMap smap;
+    cudaError_t e = s_map(qa, N0c, Cf::H, &smap);
+    if (e != cudaSuccess) return e;
+    const int I = Cf::H * N0c;
+    switch (d.n[2]) {
+        case 16: return qmid_launch<16>(qa, I, N0c, Cf::H, smap, s);
+        case 32: return qmid_launch<32>(qa, I, N0c, Cf::H, smap, s);
+        case 64: return qmid_launch<64>(qa, I, N0c, Cf::H, smap, s);
+        case 96: return qmid_launch<96>(qa, I, N0c, Cf::H, smap, s);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+template <int N>
+static cudaError_t quad_inv_n(QArgs qa, bool up, cudaStream_t s, int* ginv) {
+    using Cf = Cfg<N>;
+    CUtensorMap ymap, wmap;
     cudaError_t e;
-    CUtensorMap smap, ymap, wmap;
-    if ((e = s_map(qa, N, Cf::H, &smap)) != cudaSuccess) return e;
     if ((e = y_map(qa, N, Cf::H, &ymap)) != cudaSuccess) return e;
     if ((e = w_map(qa, N, &wmap)) != cudaSuccess) return e;
-    if (b.ev0) cudaEventRecordWithFlags(b.ev0, s, cudaEventRecordExternal);
-    {
-        const int I = Cf::H * N;
-        switch (d.n[2]) {
-            case 16: e = qmid_launch<16>(qa, I, N, Cf::H, smap, s); break;
-            case 32: e = qmid_launch<32>(qa, I, N, Cf::H, smap, s); break;
-            case 64: e = qmid_launch<64>(qa, I, N, Cf::H, smap, s); break;
-            case 96: e = qmid_launch<96>(qa, I, N, Cf::H, smap, s); break;
-            default: e = cudaErrorInvalidValue;
-        }
-        if (e != cudaSuccess) return e;
-        ++*launches;
+    const size_t smem = qinv_smem<N>();
+    const long long nplanes = (long long)qa.batch * qa.n2 * qa.n3;
+    if (up) {
+        e = q_grid(k_q_inv<N, true>, Cf::NT, smem, nplanes, ginv);
+        if (e == cudaSuccess && qa.batch > 1)
+            e = cudaMemsetAsync(qa.part, 0, sizeof(double) * NMOM * (*ginv) * (size_t)qa.batch, s);
+        if (e == cudaSuccess) k_q_inv<N, true><<<*ginv, Cf::NT, smem, s>>>(qa, ymap, wmap);
+    } else {
+        e = q_grid(k_q_inv<N, false>, Cf::NT, smem, nplanes, ginv);
+        if (e == cudaSuccess) k_q_inv<N, false><<<*ginv, Cf::NT, smem, s>>>(qa, ymap, wmap);
     }
-    if (b.ev1) cudaEventRecordWithFlags(b.ev1, s, cudaEventRecordExternal);
-    {
-        const size_t smem = qinv_smem<N>();
-        const long long nplanes = (long long)d.batch * d.n[2] * d.n[3];
-        if (up) {
-            e = q_grid(k_q_inv<N, true>, Cf::NT, smem, nplanes, ginv);
-            if (e == cudaSuccess && d.batch > 1)
-                e = cudaMemsetAsync(qa.part, 0, sizeof(double) * NMOM * (*ginv) * (size_t)d.batch, s);
-            if (e == cudaSuccess) k_q_inv<N, true><<<*ginv, Cf::NT, smem, s>>>(qa, ymap, wmap);
-        } else {
-            e = q_grid(k_q_inv<N, false>, Cf::NT, smem, nplanes, ginv);
-            if (e == cudaSuccess) k_q_inv<N, false><<<*ginv, Cf::NT, smem, s>>>(qa, ymap, wmap);
-        }
-        if (e != cudaSuccess) return e;
-        ++*launches;
-    }
+    if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
 
-cudaError_t launch_quad(const Dims& d, PencilBufs& b, const ModelParams& mp, int range, bool up, double* dcpart,
-                        double* dc3, double* part, cudaStream_t s, int64_t* launches, int* ginv) {
-    (void)dcpart;
+static QArgs make_qargs(const Dims& d, PencilBufs& b, const ModelParams& mp, int range, double* dc3, double* part) {
     QArgs qa;
     qa.W = (double*)b.W;
     qa.Yin = (const V*)b.S;
@@ -882,12 +932,85 @@ cudaError_t launch_quad(const Dims& d, PencilBufs& b, const ModelParams& mp, int
     qa.l = mp.l;
     qa.step = mp.step;
     qa.range = range;
+    qa.N0f = d.ng[0];
+    qa.koff = 0;
+    qa.G = 1;
+    qa.slab = d.n[3];
+    qa.j3off = 0;
+    qa.n3g = d.n[3];
+    return qa;
+}
+
+cudaError_t launch_quad(const Dims& d, PencilBufs& b, const ModelParams& mp, int range, bool up, double* dcpart,
+                        double* dc3, double* part, cudaStream_t s, int64_t* launches, int* ginv) {
+    (void)dcpart;
+    QArgs qa = make_qargs(d, b, mp, range, dc3, part);
+    cudaError_t e;
+    if (b.ev0) cudaEventRecordWithFlags(b.ev0, s, cudaEventRecordExternal);
     switch (d.n[0]) {
-        case 32: return quad_n<32>(d, b, qa, up, s, launches, ginv);
-        case 64: return quad_n<64>(d, b, qa, up, s, launches, ginv);
-        case 96: return quad_n<96>(d, b, qa, up, s, launches, ginv);
-        default: return cudaErrorInvalidValue;
+        case 32: e = quad_mid_n<32>(d, qa, 32, s); break;
+        case 64: e = quad_mid_n<64>(d, qa, 64, s); break;
+        case 96: e = quad_mid_n<96>(d, qa, 96, s); break;
+        default: e = cudaErrorInvalidValue;
     }
+    if (e != cudaSuccess) return e;
+    ++*launches;
+    if (b.ev1) cudaEventRecordWithFlags(b.ev1, s, cudaEventRecordExternal);
+    switch (d.n[0]) {
+        case 32: e = quad_inv_n<32>(qa, up, s, ginv); break;
+        case 64: e = quad_inv_n<64>(qa, up, s, ginv); break;
+        case 96: e = quad_inv_n<96>(qa, up, s, ginv); break;
+        default: e = cudaErrorInvalidValue;
+    }
+    if (e != cudaSuccess) return e;
+    ++*launches;
+    return cudaSuccess;
+}
+
+// Sharded (slab over j3, G ranks; pmf_sharded.cpp): K2 of rank q over the k0 range
+// [q N0/G, (q+1) N0/G) reading the all-to-all receive buffer `in` = [j3][j2][k1][k0 - q N0/G]
+// (K1's blocks of every rank, stacked in rank order) and writing `out` = [dest rank][k0][k1]
+// [j3 % slab][j2]; K3 of rank r over its slab's planes reading `in` = [k0][k1][j3 % slab][j2]
+// (the back exchange, source blocks stacked in rank order) and writing the shard's weights.
+cudaError_t launch_quad_mid_shard(const Dims& d, PencilBufs& b, const ModelParams& mp, int rank, int world,
+                                  const void* in, void* out, cudaStream_t s, int64_t* launches) {
+    QArgs qa = make_qargs(d, b, mp, 0, nullptr, nullptr);
+    qa.Yin = (const V*)in;
+    qa.Y = (V*)out;
+    qa.n3 = d.ng[3];                        // K2 sees whole (j3, j2)-planes
+    qa.G = world;
+    qa.slab = d.n[3];
+    qa.koff = rank * (d.ng[0] / world);
+    qa.n3g = d.ng[3];
+    const int N0c = d.ng[0] / world;
+    cudaError_t e;
+    switch (d.n[0]) {
+        case 32: e = quad_mid_n<32>(d, qa, N0c, s); break;
+        case 64: e = quad_mid_n<64>(d, qa, N0c, s); break;
+        case 96: e = quad_mid_n<96>(d, qa, N0c, s); break;
+        default: e = cudaErrorInvalidValue;
+    }
+    if (e == cudaSuccess) ++*launches;
+    return e;
+}
+
+cudaError_t launch_quad_inv_shard(const Dims& d, PencilBufs& b, const ModelParams& mp, const LikParams* lp, int rank,
+                                  int world, const void* in, double* part, cudaStream_t s, int64_t* launches,
+                                  int* ginv) {
+    QArgs qa = make_qargs(d, b, mp, lp ? (lp->kind == 1) : 0, nullptr, part);
+    qa.Y = (V*)in;
+    qa.G = world;
+    qa.j3off = rank * d.n[3];
+    qa.n3g = d.ng[3];
+    cudaError_t e;
+    switch (d.n[0]) {
+        case 32: e = quad_inv_n<32>(qa, lp != nullptr, s, ginv); break;
+        case 64: e = quad_inv_n<64>(qa, lp != nullptr, s, ginv); break;
+        case 96: e = quad_inv_n<96>(qa, lp != nullptr, s, ginv); break;
+        default: e = cudaErrorInvalidValue;
+    }
+    if (e == cudaSuccess) ++*launches;
+    return e;
 }
 
 }  // namespace pmf

@@ -152,6 +152,8 @@ struct PlaneArgs {
     int n2, n3;             // sizes of axes 2, 3 (1 if absent)
     int l;
     int range;              // likelihood kind 1
+    int chunks = 1;         // forward pass: each spectrum row leaves as `chunks` pieces of N / chunks
+    long long chunk_stride = 0;   // ... piece q to S + q chunk_stride + (plane H + k1) N / chunks (sharded)
 };
 
 // plane p of its filter -> (j2, j3)

@@ -210,6 +210,21 @@ cudaError_t launch_plane(const Dims& d, int dtype, PencilBufs& b, const ModelPar
 // and K3 reads it; called by launch_plane between its forward pass and finaliser
 bool quad_supported(const Dims& d, int dtype);
 int quad_debug_counters(double* out, int n, int reset);
+// the sharded nx = 4 route (slab over j3; pmf_sharded.cpp): plane prep without regrid, forward
+// plane pass writing per-destination k0 blocks, K2 / K3 on the exchanged blocks, per-shard totals
+cudaError_t launch_plane_prep(const Dims& d, PencilBufs& b, const ModelParams& mp, const LikParams* lp, cudaStream_t s,
+                              int64_t* launches);
+cudaError_t launch_plane_fwd_chunks(const Dims& d, PencilBufs& b, const ModelParams& mp, int chunks,
+                                    long long chunk_stride, double* dcpart, cudaStream_t s, int64_t* launches);
+cudaError_t launch_plane_fin_tot(const Dims& d, PencilBufs& b, const ModelParams& mp, double* tot, int update,
+                                 cudaStream_t s, int64_t* launches);
+cudaError_t launch_quad_mid_shard(const Dims& d, PencilBufs& b, const ModelParams& mp, int rank, int world,
+                                  const void* in, void* out, cudaStream_t s, int64_t* launches);
+cudaError_t launch_quad_inv_shard(const Dims& d, PencilBufs& b, const ModelParams& mp, const LikParams* lp, int rank,
+                                  int world, const void* in, double* part, cudaStream_t s, int64_t* launches,
+                                  int* ginv);
+cudaError_t launch_shard_sum(const double* dcpart, int nplanes, const double* part, int ginv, int update, double* tot,
+                             cudaStream_t s, int64_t* launches);
 int resident_debug_counters(double* out, int n, int reset);
 cudaError_t launch_quad(const Dims& d, PencilBufs& b, const ModelParams& mp, int range, bool up, double* dcpart,
                         double* dc3, double* part, cudaStream_t s, int64_t* launches, int* ginv);

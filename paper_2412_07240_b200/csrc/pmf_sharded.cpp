@@ -21,6 +21,7 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <memory>
@@ -172,25 +173,26 @@ static int exchange(pmf_ctx* c, const std::vector<Xfer>& xs, void* (*sbuf)(Shard
     return nccl_poll(c);
 }
 
-// sum of the shards' tot[0..NMOM) over ranks, written back to every shard
-static int allreduce_tot(pmf_ctx* c) {
+// sum of the shards' tot[0..n) over ranks (n <= NTOT), written back to every shard
+constexpr int NTOT = NMOM + 1;          // 15 moment sums + the DC of the three-pass route
+static int allreduce_tot(pmf_ctx* c, int n = NMOM) {
     ShardSet& S = *c->sh;
     if (!S.virt) {
         NcclApi& api = NcclApi::get();
-        if (int r = api.AllReduce(S.sh[0].tot, S.sh[0].tot, NMOM, NCCL_FLOAT64, NCCL_SUM, S.comm, c->stream))
+        if (int r = api.AllReduce(S.sh[0].tot, S.sh[0].tot, n, NCCL_FLOAT64, NCCL_SUM, S.comm, c->stream))
             return nccl_fail(c, r, "ncclAllReduce");
         return nccl_poll(c);
     }
     // virtual: host-free reduction in rank order -- gather, sum on device, scatter
     for (int r = 0; r < S.world; ++r) {
-        cudaError_t e = cudaMemcpyAsync(S.sum_scratch + r * NMOM, S.sh[r].tot, NMOM * sizeof(double),
+        cudaError_t e = cudaMemcpyAsync(S.sum_scratch + r * n, S.sh[r].tot, n * sizeof(double),
                                         cudaMemcpyDeviceToDevice, c->stream);
         if (e != cudaSuccess) return pmf_cuda_fail(c, e, "virtual allreduce gather");
     }
-    cudaError_t e = launch_sum_ranks(S.sum_scratch, S.sh[0].tot, S.world, NMOM, c->stream, &c->launches);
+    cudaError_t e = launch_sum_ranks(S.sum_scratch, S.sh[0].tot, S.world, n, c->stream, &c->launches);
     if (e != cudaSuccess) return pmf_cuda_fail(c, e, "virtual allreduce sum");
     for (int r = 1; r < S.world; ++r) {
-        e = cudaMemcpyAsync(S.sh[r].tot, S.sh[0].tot, NMOM * sizeof(double), cudaMemcpyDeviceToDevice, c->stream);
+        e = cudaMemcpyAsync(S.sh[r].tot, S.sh[0].tot, n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream);
         if (e != cudaSuccess) return pmf_cuda_fail(c, e, "virtual allreduce scatter");
     }
     return PMF_OK;
@@ -332,14 +334,14 @@ extern "C" int pmf_create_sharded(const pmf_config* cfg, const double* A, const 
         if (!err && pmf_dalloc(c, &sd.recv, cs * spec)) err = PMF_E_NOMEM;
         if (!err && pmf_dalloc(c, (void**)&sd.st, sizeof(FilterState))) err = PMF_E_NOMEM;
         if (!err && pmf_dalloc(c, (void**)&sd.partials, sizeof(double) * NMOM * 2048)) err = PMF_E_NOMEM;
-        if (!err && pmf_dalloc(c, (void**)&sd.tot, sizeof(double) * NMOM)) err = PMF_E_NOMEM;
+        if (!err && pmf_dalloc(c, (void**)&sd.tot, sizeof(double) * NTOT)) err = PMF_E_NOMEM;
         if (!err && pmf_dalloc(c, (void**)&sd.gauss, sizeof(double) * 21)) err = PMF_E_NOMEM;
         S->sh.push_back(sd);
     }
     if (!err && pmf_dalloc(c, (void**)&S->d_off, sizeof(long long) * (world + 1))) err = PMF_E_NOMEM;
     if (!err && cudaMemcpy(S->d_off, S->off.data(), sizeof(long long) * (world + 1), cudaMemcpyHostToDevice))
         fail(PMF_E_CUDA, "upload offsets");
-    if (!err && pmf_dalloc(c, (void**)&S->sum_scratch, sizeof(double) * NMOM * world)) err = PMF_E_NOMEM;
+    if (!err && pmf_dalloc(c, (void**)&S->sum_scratch, sizeof(double) * NTOT * world)) err = PMF_E_NOMEM;
     // context-level buffers shared by the shards (same device): z, model table, moments, twiddles
     if (!err && pmf_dalloc(c, (void**)&c->z, sizeof(double) * PMF_MAX_NZ)) err = PMF_E_NOMEM;
     if (!err && pmf_dalloc(c, (void**)&c->mom_dev, sizeof(double) * (nx + nx * nx + 2))) err = PMF_E_NOMEM;
@@ -534,6 +536,78 @@ static int sh_regrid_all(pmf_ctx* c, double ks) {
 }
 
 // ============================================================================ predict / update
+// ============================================================================ three-pass route
+// nx = 4, fp64, N_0 = N_1 in {32, 64, 96}, n2 = n3 in {16, .., 96}, N_0 divisible by world
+// (kernels_quad.cu): rank r owns the j3 slab [r slab, (r+1) slab):
+//   K1  forward plane pass over its planes; each spectrum row leaves in world k0 blocks,
+//       block q = [j3 % slab][j2][k1][k0 in q's range] (contiguous per destination)
+//   ALL-TO-ALL  block q of rank r -> rank q, stacked in rank order: [j3][j2][k1][k0 - q N0/G]
+//   K2  rank q: the (j3, j2)-planes of its (k1, k0) items (whole planes: the axis-2/3 DFTs,
+//       s Psi, inverses); output row j3 to block j3 / slab = [k0][k1][j3 % slab][j2]
+//   ALL-TO-ALL back  block r of rank q -> rank r, stacked in rank order: [k0][k1][j3 % slab][j2]
+//   K3  rank r: inverse DFT along axes 0, 1 of its planes, likelihood, weights, moment sums
+//   ALL-REDUCE of {15 moment sums, DC} -> normaliser, closed-form scale, moments
+// Both exchanges move every spectrum element once: 2 (G-1)/G x 16 B x H N^3 per rank and predict.
+static bool sh_quad_ok(pmf_ctx* c) {
+    const Dims& g = c->d;
+    const ShardSet& S = *c->sh;
+    if (c->dtype != PMF_F64 || g.nx != 4 || g.n[0] != g.n[1] || g.n[2] != g.n[3]) return false;
+    const int N = g.n[0], NQ = g.n[2];
+    if ((N != 32 && N != 64 && N != 96) || (NQ != 16 && NQ != 32 && NQ != 64 && NQ != 96)) return false;
+    if (N % S.world || (N / S.world) < 1 || c->mp.l + 1 > 64 || c->cfg.diff_mode != PMF_DIFF_FULL) return false;
+    const char* e = std::getenv("PMF_NO_QUAD");
+    return !(e && e[0] == '1');
+}
+
+static int sh_predict_quad(pmf_ctx* c, const LikParams* lp) {
+    ShardSet& S = *c->sh;
+    const Dims& g = c->d;
+    const int G = S.world, N = g.n[0], H = N / 2 + 1, NQ = g.n[2], slab = S.n_loc, N0c = N / G;
+    const size_t blk = (size_t)slab * NQ * H * N0c;            // complex elements per (source, destination)
+    const size_t cb = c->esize * 2;
+    const int nplanes = slab * NQ;
+    cudaError_t e;
+    for (Shard& sd : S.sh) {
+        PencilBufs b = shard_bufs(c, sd);
+        e = launch_plane_prep(sd.d, b, c->mp, lp, c->stream, &c->launches);
+        if (e == cudaSuccess)
+            e = launch_plane_fwd_chunks(sd.d, b, c->mp, G, (long long)blk, sd.partials, c->stream, &c->launches);
+        if (e != cudaSuccess) return pmf_cuda_fail(c, e, "sharded forward plane pass");
+    }
+    std::vector<Xfer> x1, x2;
+    for (int r = 0; r < G; ++r)
+        for (int q = 0; q < G; ++q) {
+            x1.push_back({r, q, cb * q * blk, cb * r * blk, cb * blk});   // K1 block q of r -> q's slot r
+            x2.push_back({q, r, cb * r * blk, cb * q * blk, cb * blk});   // K2 block r of q -> r's slot q
+        }
+    int rc = exchange(c, x1, [](Shard& s) -> void* { return s.S; }, [](Shard& s) -> void* { return s.recv; });
+    if (rc) return rc;
+    for (Shard& sd : S.sh) {
+        PencilBufs b = shard_bufs(c, sd);
+        e = launch_quad_mid_shard(sd.d, b, c->mp, sd.rank, G, sd.recv, sd.send, c->stream, &c->launches);
+        if (e != cudaSuccess) return pmf_cuda_fail(c, e, "sharded axis-2/3 pass");
+    }
+    rc = exchange(c, x2, [](Shard& s) -> void* { return s.send; }, [](Shard& s) -> void* { return s.S; });
+    if (rc) return rc;
+    for (Shard& sd : S.sh) {
+        PencilBufs b = shard_bufs(c, sd);
+        int ginv = 1;
+        double* part = sd.partials + nplanes;
+        e = launch_quad_inv_shard(sd.d, b, c->mp, lp, sd.rank, G, sd.S, part, c->stream, &c->launches, &ginv);
+        if (e == cudaSuccess)
+            e = launch_shard_sum(sd.partials, nplanes, part, ginv, lp ? 1 : 0, sd.tot, c->stream, &c->launches);
+        if (e != cudaSuccess) return pmf_cuda_fail(c, e, "sharded inverse plane pass");
+    }
+    rc = allreduce_tot(c, NTOT);
+    if (rc) return rc;
+    for (Shard& sd : S.sh) {
+        PencilBufs b = shard_bufs(c, sd);
+        e = launch_plane_fin_tot(sd.d, b, c->mp, sd.tot, lp ? 1 : 0, c->stream, &c->launches);
+        if (e != cudaSuccess) return pmf_cuda_fail(c, e, "sharded finalise");
+    }
+    return PMF_OK;
+}
+
 static int sh_predict_all(pmf_ctx* c, const LikParams* lp) {
     ShardSet& S = *c->sh;
     const size_t cs = c->esize * 2;
@@ -546,6 +620,7 @@ static int sh_predict_all(pmf_ctx* c, const LikParams* lp) {
             sd.coef_bytes = need;
         }
     }
+    if (sh_quad_ok(c)) return sh_predict_quad(c, lp);
     cudaError_t e;
     for (Shard& sd : S.sh) {
         PencilBufs b = shard_bufs(c, sd);

@@ -15,6 +15,10 @@ pytestmark = pytest.mark.gpu
 
 CASES = {
     "C4s": ("C4", {"n": (8, 6, 12, 8)}, 3, (2, 4)),
+    # the three-pass route (kernels_quad.cu) sharded: K1 blocks -> all-to-all -> K2 on whole
+    # (j3, j2)-planes of a k0 range -> all-to-all back -> K3 on the slab
+    "C4q": ("C4", {"n": (32, 32, 32, 32)}, 2, (2, 4, 8)),
+    "C4q96": ("C4", {"n": (96, 96, 16, 16)}, 2, (2, 4, 8)),
     "C2s": ("C2", {"n": (32, 48)}, 4, (2, 3)),
     "C3s": ("C3", {"n": (16, 12, 24)}, 3, (2, 4)),
 }
@@ -95,3 +99,19 @@ def test_sharded_crank_nicolson():
     g = run_gpu(cfg, zs, T, path=pmf.PATH_PENCIL, world=2, step=pmf.STEP_CN)
     e = compare_runs(cfg, g, orc, T, TOL["f64"])
     assert e["w"] <= 1e-10 and e["mean"] <= 1e-10 and e["cov"] <= 1e-10 and e["logC"] <= 1e-10, e
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_sharded_three_pass_route_is_taken(world):
+    """The sharded nx = 4 fp64 context runs the three-pass route (K1 blocks, two all-to-all,
+    K2, K3: 5 kernels + prep/sum/finaliser per shard), not the pencil passes."""
+    cfg = make_config("C4", n=(32, 32, 32, 32))
+    zs = simulate(cfg, T=1)["z"]
+    f = pmf.Filter(cfg.nx, cfg.n, cfg.A, cfg.Q, world=world, sharded=True)
+    f.set_gaussian(cfg.prior_mean, cfg.prior_cov[None], cfg.k_sigma)
+    f.update(zs[0], lik_of(cfg))
+    l0 = f.launches
+    f.predict(cfg.tau / cfg.l, cfg.l)
+    f.sync()
+    # per shard: prep, K1, K2, K3, sum, finaliser (+ the virtual all-reduce's sum kernel)
+    assert f.launches - l0 == 6 * world + 1, f.launches - l0
