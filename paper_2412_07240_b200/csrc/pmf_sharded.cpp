@@ -548,6 +548,16 @@ static int sh_regrid_all(pmf_ctx* c, double ks) {
 //   K3  rank r: inverse DFT along axes 0, 1 of its planes, likelihood, weights, moment sums
 //   ALL-REDUCE of {15 moment sums, DC} -> normaliser, closed-form scale, moments
 // Both exchanges move every spectrum element once: 2 (G-1)/G x 16 B x H N^3 per rank and predict.
+// the two all-to-all plans of the three-pass route: blocks of `blk` elements of `cb` bytes;
+// x1: K1's block q on rank r -> rank q, slot r; x2: K2's block r on rank q -> rank r, slot q
+static void quad_xfers(int G, size_t blk, size_t cb, std::vector<Xfer>& x1, std::vector<Xfer>& x2) {
+    for (int r = 0; r < G; ++r)
+        for (int q = 0; q < G; ++q) {
+            x1.push_back({r, q, cb * q * blk, cb * r * blk, cb * blk});
+            x2.push_back({q, r, cb * r * blk, cb * q * blk, cb * blk});
+        }
+}
+
 static bool sh_quad_ok(pmf_ctx* c) {
     const Dims& g = c->d;
     const ShardSet& S = *c->sh;
@@ -575,11 +585,7 @@ static int sh_predict_quad(pmf_ctx* c, const LikParams* lp) {
         if (e != cudaSuccess) return pmf_cuda_fail(c, e, "sharded forward plane pass");
     }
     std::vector<Xfer> x1, x2;
-    for (int r = 0; r < G; ++r)
-        for (int q = 0; q < G; ++q) {
-            x1.push_back({r, q, cb * q * blk, cb * r * blk, cb * blk});   // K1 block q of r -> q's slot r
-            x2.push_back({q, r, cb * r * blk, cb * q * blk, cb * blk});   // K2 block r of q -> r's slot q
-        }
+    quad_xfers(G, blk, cb, x1, x2);
     int rc = exchange(c, x1, [](Shard& s) -> void* { return s.S; }, [](Shard& s) -> void* { return s.recv; });
     if (rc) return rc;
     for (Shard& sd : S.sh) {
@@ -709,3 +715,22 @@ int sh_get_weights(pmf_ctx* c, void* dst, int on_device) {
 }
 
 extern "C" int pmf_world(const pmf_ctx* c) { return (c && c->sh) ? c->sh->world : 1; }
+
+// Test hook (not in pmf.h; host only, no device): the three-pass route's exchange plans for
+// `world` ranks and blocks of `blk` complex fp64 elements: 2 world^2 rows of (source rank,
+// destination rank, source byte offset, destination byte offset, bytes), x1 then x2.
+extern "C" int pmf_debug_quad_plan(int world, long long blk, long long* out) {
+    if (world < 1 || blk < 1 || !out) return PMF_E_ARG;
+    std::vector<Xfer> x1, x2;
+    quad_xfers(world, (size_t)blk, 16, x1, x2);
+    long long* o = out;
+    for (const auto* v : {&x1, &x2})
+        for (const Xfer& x : *v) {
+            *o++ = x.src;
+            *o++ = x.dst;
+            *o++ = (long long)x.so;
+            *o++ = (long long)x.dof;
+            *o++ = (long long)x.bytes;
+        }
+    return PMF_OK;
+}
