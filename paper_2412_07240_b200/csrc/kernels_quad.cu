@@ -88,7 +88,8 @@ template <int NQ> struct Q2 {
     static constexpr int PSP = NQ + 1;                       // Psi table pitch (doubles)
     static constexpr int R3 = (NQ + 31) / 32;                // k3 values per lane in the table phase
     static constexpr int QTW = 6;                            // doubles per substep in the item's table
-    static constexpr int RP = NQ < 32 ? NQ : 32;             // rows per TMA part of the gathered plane
+    static constexpr int TEAMS = NQ == 96 ? 48 : (NQ >= 64 ? 32 : NQ / 2);   // K2's teams (8 threads)
+    static constexpr int RP = TEAMS;                         // rows per TMA part of the gathered plane
     static constexpr size_t SMEM = sizeof(V) * NQ * QCfg<NQ>::P + sizeof(double) * NQ * PSP +
                                    2 * (sizeof(double) + sizeof(int)) * NQ + sizeof(V) * NQ + 16 +
                                    sizeof(double) * QTW * (LCAP + 1) + sizeof(double) * PL_EU;
@@ -334,7 +335,13 @@ __global__ void __launch_bounds__(QCfg<NQ, TM>::NT, 1) k_q_mid(QArgs a, int I, i
 #pragma unroll
                         for (int r = 0; r < R; ++r) x[r] = X[j3 * P + t + 8 * r];
                     }
-                    quad_f2_row<NQ>(x, X + j3 * P, tw, t);
+                    // forward DFT along axis 2; the row's spectrum stays in exchange-slot order
+                    // (X(k2) at slot(k2 % R, k2 / R))
+                    V* row = X + j3 * P;
+                    __syncwarp();
+                    tdft_s1<R, false>(x, row, tw, t, rs);
+                    __syncwarp();
+                    tdft_s2<R>(row, t, rs, [](int, V* p) { reg::dft8<false>(p); });
                 }
             }
             __syncthreads();
@@ -343,27 +350,32 @@ __global__ void __launch_bounds__(QCfg<NQ, TM>::NT, 1) k_q_mid(QArgs a, int I, i
             // ------------------------------------------------------------ F3: axis 3, x table, inverse
 #pragma unroll 1
             for (int k2 = q; k2 < NQ; k2 += TEAMS) {
-                V* col = X + k2;
+                V* col = X + rslot(k2 % R, k2 / R);           // logical column k2 (slot order)
                 const double* pr = psi + k2 * PSP;
-                V x[R], pa[8], pb[8];
+                V x[R];
 #pragma unroll
                 for (int r = 0; r < R; ++r) x[r] = col[(t + 8 * r) * P];
-                team_dft<R, false>(x, pa, pb, col, tw, t, cs);
-                if (flag == 4 && i == 0 && a.koff == 0 && k2 == 0 && t == 0) {
-                    // (k0, k1, k2, k3) = 0: the sum of the regridded weights
-                    a.dc3[(long long)f * a.n3] = pa[0].x;
-                    for (int j = 1; j < a.n3; ++j) a.dc3[(long long)f * a.n3 + j] = 0.0;
-                }
-                if (s_on<R>(t)) {
-                    const int sa = s_a<R>(t), sb = s_b<R>(t);
+                __syncwarp();
+                tdft_s1<R, false>(x, col, tw, t, cs);
+                __syncwarp();
+                const bool dc = flag == 4 && i == 0 && a.koff == 0 && k2 == 0;
+                tdft_s2<R>(col, t, cs, [&](int s3, V* p) {
+                    reg::dft8<false>(p);                      // X(k2, k3 = s3 + R qq)
+                    if (dc && s3 == 0) {
+                        // (k0, k1, k2, k3) = 0: the sum of the regridded weights
+                        a.dc3[(long long)f * a.n3] = p[0].x;
+                        for (int j = 1; j < a.n3; ++j) a.dc3[(long long)f * a.n3 + j] = 0.0;
+                    }
 #pragma unroll
                     for (int qq = 0; qq < 8; ++qq) {
-                        const double fa = pr[sa + R * qq], fb = pr[sb + R * qq];
-                        pa[qq] = V{pa[qq].x * fa, pa[qq].y * fa};
-                        pb[qq] = V{pb[qq].x * fb, pb[qq].y * fb};
+                        const double fq = pr[s3 + R * qq];
+                        p[qq] = V{p[qq].x * fq, p[qq].y * fq};
                     }
-                }
-                team_dft_dif<R, true>(pa, pb, x, col, tw, t, cs);
+                    reg::dft8<true>(p);
+                });
+                __syncwarp();
+                tdft_s1_dif<R, true>(x, col, tw, t, cs);
+                __syncwarp();
 #pragma unroll
                 for (int r = 0; r < R; ++r) col[(t + 8 * r) * P] = x[r];
             }
@@ -389,16 +401,11 @@ __global__ void __launch_bounds__(QCfg<NQ, TM>::NT, 1) k_q_mid(QArgs a, int I, i
             for (int j3 = c * RP + q; j3 < (c + 1) * RP; j3 += TEAMS) {
                 V* row = X + j3 * P;
                 if (!skip) {
-                    V x[R], pa[8], pb[8];
-                    if (s_on<R>(t)) {
-                        const int sa = s_a<R>(t), sb = s_b<R>(t);
-#pragma unroll
-                        for (int qq = 0; qq < 8; ++qq) {
-                            pa[qq] = row[sa + R * qq];
-                            pb[qq] = row[sb + R * qq];
-                        }
-                    }
-                    team_dft_dif<R, true>(pa, pb, x, row, tw, t, rs);   // x[r] = element j2 = t + 8r
+                    V x[R];
+                    // inverse DFT along axis 2 from the slot-order spectrum: x[r] = element j2 = t + 8r
+                    tdft_s2<R>(row, t, rs, [](int, V* p) { reg::dft8<true>(p); });
+                    __syncwarp();
+                    tdft_s1_dif<R, true>(x, row, tw, t, rs);
                     {
                         const int rk = j3 / a.slab, j3l = j3 - rk * a.slab;
                         V* o = dst + rk * rstride + j3l * NQ + t;
@@ -849,7 +856,7 @@ static cudaError_t s_map(const QArgs& qa, int N, int H, CUtensorMap* m) {
         }
     }
     const cuuint64_t n2 = qa.n2, n3 = qa.n3;
-    const cuuint32_t rp = qa.n2 < 32 ? (cuuint32_t)qa.n2 : 32;
+    const cuuint32_t rp = qa.n2 == 96 ? 48 : (qa.n2 >= 64 ? 32 : (cuuint32_t)qa.n2 / 2);   // Q2<NQ>::RP
     cuuint64_t dims[5] = {2, (cuuint64_t)N, (cuuint64_t)H, n2, (cuuint64_t)qa.batch * n3};
     cuuint64_t str[4] = {16, 16 * (cuuint64_t)N, 16 * (cuuint64_t)N * H, 16 * (cuuint64_t)N * H * n2};
     cuuint32_t box[5] = {2, 1, 1, (cuuint32_t)(qa.n2 + 1), rp};
@@ -871,10 +878,10 @@ static cudaError_t qmid_tm(const QArgs& qa, int I, int N0, int H1, const CUtenso
     return cudaGetLastError();
 }
 
-// (48 teams at NQ = 96 -- 12 warps, 168 registers -- measured 7 % slower than 32 teams)
+// (48 teams at NQ = 96: 12 warps, no spills with the split team DFT)
 template <int NQ>
 static cudaError_t qmid_launch(const QArgs& qa, int I, int N0, int H1, const CUtensorMap& smap, cudaStream_t s) {
-    return qmid_tm<NQ, QCfg<NQ>::TEAMS>(qa, I, N0, H1, smap, s);
+    return qmid_tm<NQ, Q2<NQ>::TEAMS>(qa, I, N0, H1, smap, s);
 }
 
 // K1 -> K2 -> K3 (prep, the general-map pre-pass and the finaliser are the plane path's;

@@ -135,6 +135,48 @@ __device__ __forceinline__ void team_dft_dif(V* pa, V* pb, V* x, V* ex, const V*
     __syncwarp();
 }
 
+// ---------------------------------------------------------------------------- split team DFT
+// The team DFT in two halves with an exchange area that doubles as the spectrum's home:
+//   tdft_s1      DIT stage 1: x[r] (element t + 8r) -> ex[slot(s, t)] = DFT_R1(x)_s W_N^{ts}
+//   tdft_s2      stage 2 over the thread's own s values (sa, then sb), one 8-point group at a
+//                time: ex[slot(s, tt)] (tt < 8) -> f(s, p) -> back into the same slots, i.e.
+//                X[s + R1 q] stays at slot(s, q)
+//   tdft_s1_dif  the inverse's last stage: ex[slot(s, t)] -> twiddle -> DFT_R1 -> x[r]
+// A thread only rewrites the slots it read, so stage 2 needs no second warp sync, keeps
+// 8 values live instead of 16, and a spectrum left "in slot order" between passes costs no
+// permutation (callers address column k as slot(k % R1, k / R1)).
+template <int R1, bool INV, typename V, typename SLOT>
+__device__ __forceinline__ void tdft_s1(V* x, V* ex, const V* tw, int t, SLOT slot) {
+    dftR<R1, INV>(x);
+#pragma unroll
+    for (int s = 1; s < R1; ++s) x[s] = twid<INV>(x[s], tw[s * 8 + t]);
+#pragma unroll
+    for (int s = 0; s < R1; ++s) ex[slot(s, t)] = x[s];
+}
+template <int R1, typename V, typename SLOT, typename F>
+__device__ __forceinline__ void tdft_s2(V* ex, int t, SLOT slot, F f) {
+    if (s_on<R1>(t)) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int s = h ? s_b<R1>(t) : s_a<R1>(t);
+            V p[8];
+#pragma unroll
+            for (int tt = 0; tt < 8; ++tt) p[tt] = ex[slot(s, tt)];
+            f(s, p);
+#pragma unroll
+            for (int tt = 0; tt < 8; ++tt) ex[slot(s, tt)] = p[tt];
+        }
+    }
+}
+template <int R1, bool INV, typename V, typename SLOT>
+__device__ __forceinline__ void tdft_s1_dif(V* x, const V* ex, const V* tw, int t, SLOT slot) {
+#pragma unroll
+    for (int s = 0; s < R1; ++s) x[s] = ex[slot(s, t)];
+#pragma unroll
+    for (int s = 1; s < R1; ++s) x[s] = twid<INV>(x[s], tw[s * 8 + t]);
+    dftR<R1, INV>(x);
+}
+
 template <typename T>
 struct PlaneArgs {
     const T* Wsrc;          // weights read by the forward pass (old grid when regridding)

@@ -194,6 +194,137 @@ static void run(const char* name, int items, bool last = false) {
            us_item * 4704.0 / 148.0, cudaGetErrorString(cudaGetLastError()), last ? "" : ",");
 }
 
+
+// V3: stage 2 one s-value at a time (8 complex live), the spectral row kept in exchange-slot
+// order between the passes (X(s + R q) at slot(s, q)): every thread writes back only the
+// slots it read, so no second warp sync and no pa/pb pair in registers
+template <bool INV, typename SLOT>
+__device__ __forceinline__ void st1(V* x, V* ex, const V* tw, int t, SLOT slot) {
+    // DIT stage 1: x[r] (element t + 8r) -> ex[slot(s, t)] = Y_t(s) W^{ts}
+    reg::dft12<INV>(x);
+#pragma unroll
+    for (int s = 1; s < R; ++s) x[s] = twid<INV>(x[s], tw[s * 8 + t]);
+#pragma unroll
+    for (int s = 0; s < R; ++s) ex[slot(s, t)] = x[s];
+}
+template <bool INV, typename SLOT>
+__device__ __forceinline__ void st1_dif(V* x, V* ex, const V* tw, int t, SLOT slot) {
+    // DIF stage 1 (inverse of st1's layout): ex[slot(s, t)] -> x[r] = element t + 8r
+#pragma unroll
+    for (int s = 0; s < R; ++s) x[s] = ex[slot(s, t)];
+#pragma unroll
+    for (int s = 1; s < R; ++s) x[s] = twid<INV>(x[s], tw[s * 8 + t]);
+    reg::dft12<INV>(x);
+}
+// stage 2 on this thread's own s values: f(s, p) transforms the 8 values in place
+template <typename SLOT, typename F>
+__device__ __forceinline__ void st2(V* ex, int t, SLOT slot, F f) {
+    if (s_on<R>(t)) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int s = h ? s_b<R>(t) : s_a<R>(t);
+            V p[8];
+#pragma unroll
+            for (int tt = 0; tt < 8; ++tt) p[tt] = ex[slot(s, tt)];
+            f(s, p);
+#pragma unroll
+            for (int tt = 0; tt < 8; ++tt) ex[slot(s, tt)] = p[tt];
+        }
+    }
+}
+
+template <int TEAMS>
+__global__ void __launch_bounds__(8 * TEAMS, 1) k_fft3(double* out, int items) {
+    constexpr int NT = 8 * TEAMS;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    V* X = reinterpret_cast<V*>(smem_raw);
+    V* tw = X + NQ * P;
+    const int tid = threadIdx.x, q = tid >> 3, t = tid & 7;
+    init_tw<NQ>(tw);
+    for (int i = tid; i < NQ * P; i += NT) X[i] = V{1e-3 * (i % 97), 1e-3 * (i % 89)};
+    __syncthreads();
+    auto rs = [](int s2, int tt) { return rslot(s2, tt); };
+    auto cs = [](int s2, int tt) { return rslot(s2, tt) * P; };
+    for (int it = 0; it < items; ++it) {
+#pragma unroll 1
+        for (int j3 = q; j3 < NQ; j3 += TEAMS) {           // F2 -> row in slot order
+            V* row = X + j3 * P;
+            V x[R];
+#pragma unroll
+            for (int r = 0; r < R; ++r) x[r] = row[t + 8 * r];
+            __syncwarp();
+            st1<false>(x, row, tw, t, rs);
+            __syncwarp();
+            st2(row, t, rs, [](int, V* p) { reg::dft8<false>(p); });
+            __syncwarp();
+        }
+        __syncthreads();
+#pragma unroll 1
+        for (int k2 = q; k2 < NQ; k2 += TEAMS) {           // F3 on column pos(k2)
+            V* col = X + rslot(k2 % R, k2 / R);
+            V x[R];
+#pragma unroll
+            for (int r = 0; r < R; ++r) x[r] = col[(t + 8 * r) * P];
+            __syncwarp();
+            st1<false>(x, col, tw, t, cs);
+            __syncwarp();
+            st2(col, t, cs, [](int, V* p) {
+                reg::dft8<false>(p);
+#pragma unroll
+                for (int qq = 0; qq < 8; ++qq) p[qq] = V{p[qq].x * (1.0 / 96), p[qq].y * (1.0 / 96)};
+                reg::dft8<true>(p);
+            });
+            __syncwarp();
+            st1_dif<true>(x, col, tw, t, cs);
+            __syncwarp();
+#pragma unroll
+            for (int r = 0; r < R; ++r) col[(t + 8 * r) * P] = x[r];
+        }
+        __syncthreads();
+#pragma unroll 1
+        for (int j3 = q; j3 < NQ; j3 += TEAMS) {           // I2 from slot order
+            V* row = X + j3 * P;
+            st2(row, t, rs, [](int, V* p) { reg::dft8<true>(p); });
+            __syncwarp();
+            V x[R];
+            st1_dif<true>(x, row, tw, t, rs);
+            __syncwarp();
+#pragma unroll
+            for (int r = 0; r < R; ++r) row[t + 8 * r] = V{x[r].x * (1.0 / 96), x[r].y * (1.0 / 96)};
+        }
+        __syncthreads();
+    }
+    if (tid == 0) out[blockIdx.x] = X[5].x + X[P + 7].y;
+}
+
+template <int TEAMS>
+static void run3(const char* name, int items, bool last = false) {
+    constexpr int NT = 8 * TEAMS;
+    const size_t smem = sizeof(V) * (NQ * P + NQ);
+    cudaFuncSetAttribute(k_fft3<TEAMS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    double* out;
+    cudaMalloc(&out, 148 * 8);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    k_fft3<TEAMS><<<148, NT, smem>>>(out, 2);
+    cudaDeviceSynchronize();
+    std::vector<float> ts;
+    for (int r = 0; r < 5; ++r) {
+        cudaEventRecord(e0);
+        k_fft3<TEAMS><<<148, NT, smem>>>(out, items);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms;
+        cudaEventElapsedTime(&ms, e0, e1);
+        ts.push_back(ms);
+    }
+    std::sort(ts.begin(), ts.end());
+    const double us_item = 1e3 * ts[2] / items;
+    printf("  \"%s\": {\"us_per_item_per_sm\": %.3f, \"c4_k2_fft_only_us\": %.1f, \"err\": \"%s\"}%s\n", name, us_item,
+           us_item * 4704.0 / 148.0, cudaGetErrorString(cudaGetLastError()), last ? "" : ",");
+}
+
 int main() {
     printf("{\n");
     run<0, 32>("v0_table_twiddles_8w", 64);
@@ -201,7 +332,9 @@ int main() {
     run<0, 48>("v0_table_twiddles_12w", 64);
     run<1, 48>("v1_tree_twiddles_12w", 64);
     run<2, 32>("v2_opaque_t_8w", 64);
-    run<2, 48>("v2_opaque_t_12w", 64, true);
+    run<2, 48>("v2_opaque_t_12w", 64);
+    run3<32>("v3_half_stage2_slot_order_8w", 64);
+    run3<48>("v3_half_stage2_slot_order_12w", 64, true);
     printf("}\n");
     return 0;
 }
