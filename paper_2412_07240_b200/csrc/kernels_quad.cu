@@ -525,29 +525,32 @@ __global__ void __launch_bounds__(Cfg<N>::NT, 1) k_q_inv(QArgs a, const __grid_c
             continue;
         }
         // ------------------------------------------------------------ inverse axis 0 of row k1 = m
+        // split team DFT: the row's spectrum is left in (swizzled) slot order, read as such below
         {
-            V x[R1], pa[8], pb[8];
+            V x[R1];
             V* row = X + m * PITCH;
             const bool m0 = m == 0;
+            const int sw = (m >> 2) & 1;
+            auto slot = [sw](int s, int tt) { return rslot(s, tt) ^ sw; };
 #pragma unroll
             for (int r = 0; r < R1; ++r) {
                 const V A = row[t + 8 * r];
                 const V B = m0 ? X[(N / 2) * PITCH + t + 8 * r] : V{0.0, 0.0};
                 x[r] = V{A.x - B.y, A.y + B.x};
             }
-            team_dft<R1, true>(x, pa, pb, row, tw, t, [](int s, int tt) { return rslot(s, tt); });
-            if (s_on<R1>(t)) {
-                const int sa = s_a<R1>(t), sb = s_b<R1>(t);
+            __syncwarp();
+            tdft_s1<R1, true>(x, row, tw, t, slot);
+            __syncwarp();
+            tdft_s2<R1>(row, t, slot, [&](int s, V* p) {
+                reg::dft8<true>(p);
+                if (m0) {                                     // rows 0 and N/2 were packed as one
 #pragma unroll
-                for (int q = 0; q < 8; ++q) {
-                    row[xcol(m, sa + R1 * q)] = m0 ? V{pa[q].x, 0.0} : pa[q];
-                    row[xcol(m, sb + R1 * q)] = m0 ? V{pb[q].x, 0.0} : pb[q];
-                    if (m0) {
-                        X[(N / 2) * PITCH + sa + R1 * q] = V{pa[q].y, 0.0};
-                        X[(N / 2) * PITCH + sb + R1 * q] = V{pb[q].y, 0.0};
+                    for (int q = 0; q < 8; ++q) {
+                        X[(N / 2) * PITCH + rslot(s, q)] = V{p[q].y, 0.0};
+                        p[q] = V{p[q].x, 0.0};
                     }
                 }
-            }
+            });
         }
         __syncthreads();
         // the next plane into the other buffer, once that buffer's weight store has read it
@@ -559,7 +562,8 @@ __global__ void __launch_bounds__(Cfg<N>::NT, 1) k_q_inv(QArgs a, const __grid_c
         V x[R1];
         {
             V pa[8], pb[8];
-            auto ld = [&](int k1, int col) -> V { return X[k1 * PITCH + xcol(k1, 2 * m + col)]; };
+            const int oc0 = rslot((2 * m) % R1, (2 * m) / R1), oc1 = rslot((2 * m + 1) % R1, (2 * m + 1) / R1);
+            auto ld = [&](int k1, int col) -> V { return X[k1 * PITCH + ((col ? oc1 : oc0) ^ ((k1 >> 2) & 1))]; };
             auto zdir = [&](int k1) -> V {
                 const V wa = ld(k1, 0), wb = ld(k1, 1);
                 return V{wa.x - wb.y, wa.y + wb.x};
@@ -576,7 +580,11 @@ __global__ void __launch_bounds__(Cfg<N>::NT, 1) k_q_inv(QArgs a, const __grid_c
                     pb[q] = (q < 4) ? zdir(sb + R1 * q) : zmir(mb + R1 * (7 - q));
                 }
             }
-            team_dft_dif<R1, true>(pa, pb, x, X, tw, t, [&](int s, int tt) { return cslot<N>(s, tt, m); });
+            // exchange inside this team's own two column homes (the other teams' are still being read)
+            team_dft_dif<R1, true>(pa, pb, x, X, tw, t, [&](int s, int tt) {
+                const int r = 4 * s + ((tt >> 1) ^ (s & 3)), cb = (tt & 1) ^ ((s >> 2) & 1);
+                return r * PITCH + ((cb ? oc1 : oc0) ^ (s & 1));
+            });
         }
         QPROF_T(r3);
         QPROF_ADD(13, r2, r3);
