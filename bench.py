@@ -184,7 +184,7 @@ def oracle_sample_cfg(cfg):
     per-point rate at 96^4 is about a third of the sub-grid's (stated with the number)."""
     if cfg.batch == 1 and cfg.points > 4_000_000:
         sub = cfg.replace(n=(32,) * cfg.nx)
-        return sub, f"one epoch of the {cfg.name} model on a 32^{cfg.nx} sub-grid (at 96^{cfg.nx} the oracle needs " \
+        return sub, f"{{nf}} successive epochs of the {cfg.name} model on a 32^{cfg.nx} sub-grid (at 96^{cfg.nx} the oracle needs " \
                     f"{cfg.points / 32 ** cfg.nx:.0f}x the points at ~3x the per-point work: minutes per epoch)"
     return cfg, None
 
@@ -197,19 +197,26 @@ def oracle_sample(cfg, zs, budget_s: float, max_filters: int, threads=None):
     from oracle import pmf_oracle as O
     n = tuple(cfg.n)
     done, t_tot = 0, 0.0
+    nb = min(cfg.batch, max_filters)
     with threadpool_limits(threads):
-        for b in range(min(cfg.batch, max_filters)):
-            w, c, B = O.initial_density(cfg.prior_mean[b], cfg.prior_cov, n, cfg.k_sigma)
+        # batched: filters 0, 1, .. one epoch each; one filter (batch 1): its successive
+        # epochs, until the budget is used
+        b, w = 0, None
+        while True:
+            if w is None or nb > 1:
+                w, c, B = O.initial_density(cfg.prior_mean[b], cfg.prior_cov, n, cfg.k_sigma)
             t0 = time.perf_counter()
             w, c, B = O.predict(w, c, B, cfg.A, cfg.Q, cfg.tau, cfg.l)
             w, _ = O.update(w, c, B, O.make_likelihood(cfg, O.grid_points(c, B, n), zs[1, b]))
             mean, cov = O.moments(w, c, B)
             c2, B2 = O.regrid_target(mean, cov, n, cfg.k_sigma)
             w = O.regrid(w, c, B, c2, B2)
+            c, B = c2, B2
             t_tot += time.perf_counter() - t0
             done += 1
-            if t_tot >= budget_s:
+            if t_tot >= budget_s or (nb > 1 and done >= nb):
                 break
+            b = (b + 1) % nb
     return done * cfg.points / t_tot, done, t_tot
 
 
@@ -262,7 +269,8 @@ def run_reference(args):
     timed = per_step[args.warmup:]
     val = statistics.median(v for v, _, _ in timed)
     nf = timed[0][1]
-    sample = (note or f"{nf} of {cfg.batch} filters x 1 epoch") + " per step (the oracle is an O(N^2) naive DFT)"
+    sample = (note.format(nf=nf) if note else f"{nf} of {cfg.batch} filters x 1 epoch") + \
+        " per step (the oracle is an O(N^2) naive DFT)"
     nproc, model = cpu_info()
     line = {"impl": "reference", "metric": metric_name(cfg.dtype), "value": val,
             "unit": "grid-point updates/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -564,7 +572,8 @@ def dominant_kernel(cfg, f, pmf, wl, epoch_kernel, esize, points_step):
                 "per": f"{2 * esize} B per grid point"}
     if f.path == pmf.PATH_PLANE and cfg.nx == 4 and cfg.dtype == "f64" and cfg.n[2] == cfg.n[3]:
         # K2: reads and writes the half spectrum once
-        return {"name": f"k_q_mid<{cfg.n[2]}, 32>", "bytes": 2 * 2 * esize * nspec,
+        tm = 48 if cfg.n[2] == 96 else (32 if cfg.n[2] >= 64 else cfg.n[2] // 2)   # Q2<NQ>::TEAMS
+        return {"name": f"k_q_mid<{cfg.n[2]}, {tm}>", "bytes": 2 * 2 * esize * nspec,
                 "per": f"{4 * esize} B per half-spectrum point (read + write of the spectrum)"}
     if f.path == pmf.PATH_PLANE:
         return {"name": f"k_plane_mid<{tname}, {cfg.n[-1]}, 2, {cfg.nx}, {1 if cfg.n[-1] == 96 else 3}>",

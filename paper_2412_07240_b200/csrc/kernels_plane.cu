@@ -289,9 +289,14 @@ __global__ void __launch_bounds__(Cfg<N>::NT, Cfg<N>::MINB) k_plane_fwd(PlaneArg
                 double a1;
                 split(fma(M11, u1, o1), i1, a1);
                 const double vb = fma(M01, u1, o0);
+                // odd teams take column 2m + 1 first: in each load instruction half the warp
+                // reads even and half odd source columns (all 16 eight-byte bank slots),
+                // instead of every lane the same parity (rows start 16-byte aligned)
+                const int ep = m & 1;
                 T val[2];
 #pragma unroll
-                for (int e = 0; e < 2; ++e) {
+                for (int k = 0; k < 2; ++k) {
+                    const int e = k ^ ep;
                     int i0;
                     double a0;
                     split(fma(M00, (2 * m + e) - 0.5 * (N - 1), vb), i0, a0);
@@ -299,9 +304,9 @@ __global__ void __launch_bounds__(Cfg<N>::NT, Cfg<N>::MINB) k_plane_fwd(PlaneArg
                     const double w00 = (double)r0[0], w01 = (double)r0[1];
                     const double w10 = (double)r0[SP], w11 = (double)r0[SP + 1];
                     const double lo = fma(a0, w01 - w00, w00), hi = fma(a0, w11 - w10, w10);
-                    val[e] = (T)fma(a1, hi - lo, lo);
+                    val[k] = (T)fma(a1, hi - lo, lo);
                 }
-                z[r] = V{val[0], val[1]};
+                z[r] = ep ? V{val[1], val[0]} : V{val[0], val[1]};
             }
         } else {
 #pragma unroll

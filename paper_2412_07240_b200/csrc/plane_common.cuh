@@ -86,14 +86,39 @@ __device__ __forceinline__ V twid(V a, V w) {
     return cmul(a, w);
 }
 
+// x[s] *= W_N^{ts} (conjugated for INV), s = 1 .. R1-1. With s = a + 4b (a < 4) the twiddle is
+// W^{ta} W^{4tb}: R1/4 + 2 table loads and one complex product each for the rest, instead of
+// R1 - 1 loads (16-byte shared loads cost 4 wavefronts per warp: the twiddles were 10 % of
+// the plane kernels' shared-memory traffic).
+template <int R1, bool INV, typename V>
+__device__ __forceinline__ void apply_tw(V* x, const V* tw, int t) {
+    if constexpr (R1 <= 4) {
+#pragma unroll
+        for (int s = 1; s < R1; ++s) x[s] = twid<INV>(x[s], tw[s * 8 + t]);
+    } else {
+        V wa[4];
+#pragma unroll
+        for (int a = 1; a < 4; ++a) {
+            wa[a] = tw[a * 8 + t];
+            x[a] = twid<INV>(x[a], wa[a]);
+        }
+#pragma unroll
+        for (int b = 1; b < R1 / 4; ++b) {
+            const V wb = tw[4 * b * 8 + t];
+            x[4 * b] = twid<INV>(x[4 * b], wb);
+#pragma unroll
+            for (int a = 1; a < 4; ++a) x[a + 4 * b] = twid<INV>(x[a + 4 * b], cmul(wa[a], wb));
+        }
+    }
+}
+
 // Team DFT, DIT order: in x[r] = element t + 8r (registers), out pa[q] = X[sa + R1 q],
 // pb[q] = X[sb + R1 q] on the threads with s_on(t). `ex` is the team's exchange area,
 // `slot(s, t)` its conflict-free layout.
 template <int R1, bool INV, typename V, typename SLOT>
 __device__ __forceinline__ void team_dft(V* x, V* pa, V* pb, V* ex, const V* tw, int t, SLOT slot) {
     dftR<R1, INV>(x);
-#pragma unroll
-    for (int s = 1; s < R1; ++s) x[s] = twid<INV>(x[s], tw[s * 8 + t]);
+    apply_tw<R1, INV>(x, tw, t);
     __syncwarp();
 #pragma unroll
     for (int s = 0; s < R1; ++s) ex[slot(s, t)] = x[s];
@@ -129,8 +154,7 @@ __device__ __forceinline__ void team_dft_dif(V* pa, V* pb, V* x, V* ex, const V*
     __syncwarp();
 #pragma unroll
     for (int s = 0; s < R1; ++s) x[s] = ex[slot(s, t)];
-#pragma unroll
-    for (int s = 1; s < R1; ++s) x[s] = twid<INV>(x[s], tw[s * 8 + t]);
+    apply_tw<R1, INV>(x, tw, t);
     dftR<R1, INV>(x);
     __syncwarp();
 }
@@ -148,8 +172,7 @@ __device__ __forceinline__ void team_dft_dif(V* pa, V* pb, V* x, V* ex, const V*
 template <int R1, bool INV, typename V, typename SLOT>
 __device__ __forceinline__ void tdft_s1(V* x, V* ex, const V* tw, int t, SLOT slot) {
     dftR<R1, INV>(x);
-#pragma unroll
-    for (int s = 1; s < R1; ++s) x[s] = twid<INV>(x[s], tw[s * 8 + t]);
+    apply_tw<R1, INV>(x, tw, t);
 #pragma unroll
     for (int s = 0; s < R1; ++s) ex[slot(s, t)] = x[s];
 }
@@ -172,8 +195,7 @@ template <int R1, bool INV, typename V, typename SLOT>
 __device__ __forceinline__ void tdft_s1_dif(V* x, const V* ex, const V* tw, int t, SLOT slot) {
 #pragma unroll
     for (int s = 0; s < R1; ++s) x[s] = ex[slot(s, t)];
-#pragma unroll
-    for (int s = 1; s < R1; ++s) x[s] = twid<INV>(x[s], tw[s * 8 + t]);
+    apply_tw<R1, INV>(x, tw, t);
     dftR<R1, INV>(x);
 }
 

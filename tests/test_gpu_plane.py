@@ -31,6 +31,7 @@ CASES = {
     "C4_32x32x64x64": ("C4", {"n": (32, 32, 64, 64)}, 1),
     "C4_32x32x96x96": ("C4", {"n": (32, 32, 96, 96)}, 1),
     "C4_64x64x16x16": ("C4", {"n": (64, 64, 16, 16)}, 2),
+    "C4_64x64x32x32": ("C4", {"n": (64, 64, 32, 32)}, 1),
     "C4_96x96x16x16": ("C4", {"n": (96, 96, 16, 16)}, 2),
     "C4_b3_96x96x32x32": ("C4", {"n": (96, 96, 32, 32), "batch": 3}, 1),
 }
