@@ -57,6 +57,27 @@ constexpr int NT = 512;           // threads: 64 teams x 8
 
 using namespace reg;
 
+// x[s] *= W_128^{ts} (conjugated for INV), s = 1..15, as W^{ta} W^{4tb} (s = a + 4b, a < 4):
+// six 16-byte table loads and nine complex products instead of fifteen loads
+template <bool INV, typename V>
+__device__ __forceinline__ void tw16(V* x, const V* tw, int t) {
+    V wa[4];
+#pragma unroll
+    for (int a = 1; a < 4; ++a) {
+        wa[a] = tw[a * 8 + t];
+        if (INV) wa[a].y = -wa[a].y;
+        x[a] = cmul(x[a], wa[a]);
+    }
+#pragma unroll
+    for (int b = 1; b < 4; ++b) {
+        V wb = tw[4 * b * 8 + t];
+        if (INV) wb.y = -wb.y;
+        x[4 * b] = cmul(x[4 * b], wb);
+#pragma unroll
+        for (int a = 1; a < 4; ++a) x[a + 4 * b] = cmul(x[a + 4 * b], cmul(wa[a], wb));
+    }
+}
+
 // Spectrum element (k1, j0) lives at X[k1 * PITCH + xcol(k1, j0)]: the two columns of a
 // pair swap places in rows with (k1 & 4), so the 8 threads of a team touching rows
 // t + 16 q of one column hit 8 distinct 16-byte bank groups (PITCH = 2 mod 8).
@@ -522,8 +543,7 @@ __global__ void __launch_bounds__(NT, 1) k_resident_epoch(ResArgs<T> a, const __
             RPROF_SET(c2);
             RPROF_ADD(1, c1, c2);
             dft16<false>(z);                      // over r: Y_t(s)
-#pragma unroll
-            for (int s = 1; s < 16; ++s) z[s] = cmul(z[s], tw[s * 8 + t]);
+            tw16<false>(z, tw, t);
 #pragma unroll
             for (int s = 0; s < 16; ++s) X[cslot(s, t, m)] = z[s];
             __syncwarp();
@@ -573,8 +593,7 @@ __global__ void __launch_bounds__(NT, 1) k_resident_epoch(ResArgs<T> a, const __
                 for (int r = 0; r < 16; ++r) x[r] = row[xcol(m, t + 8 * r)];
             }
             dft16<false>(x);
-#pragma unroll
-            for (int s = 1; s < 16; ++s) x[s] = cmul(x[s], tw[s * 8 + t]);
+            tw16<false>(x, tw, t);
             __syncwarp();
 #pragma unroll
             for (int s = 0; s < 16; ++s) row[rslot(s, t)] = x[s];
@@ -730,12 +749,7 @@ __global__ void __launch_bounds__(NT, 1) k_resident_epoch(ResArgs<T> a, const __
             __syncwarp();
 #pragma unroll
             for (int s = 0; s < 16; ++s) x[s] = row[rslot(s, t)];
-#pragma unroll
-            for (int s = 1; s < 16; ++s) {
-                V w = tw[s * 8 + t];
-                w.y = -w.y;
-                x[s] = cmul(x[s], w);
-            }
+            tw16<true>(x, tw, t);
             dft16<true>(x);
             __syncwarp();
             if (m == 0) {
@@ -802,12 +816,7 @@ __global__ void __launch_bounds__(NT, 1) k_resident_epoch(ResArgs<T> a, const __
             RPROF_ADD(4, c4, c5);
             zero_ring<T>(smem_raw, tid);          // visible to the gather after the end-of-filter barrier
             if (nxt < a.batch) stage(a, nxt, smem_raw, Pn, bar, tid);   // overlaps the rest of P3
-#pragma unroll
-            for (int s = 1; s < 16; ++s) {
-                V w = tw[s * 8 + t];
-                w.y = -w.y;
-                x[s] = cmul(x[s], w);
-            }
+            tw16<true>(x, tw, t);
             dft16<true>(x);                       // x[r] = w(2m, t+8r) + i w(2m+1, t+8r) (unnormalised)
             RPROF_T(d1);
             RPROF_ADD(7, c5, d1);
