@@ -87,7 +87,10 @@ def test_full_size_c5_batch_sampled_vs_oracle():
             assert abs(rec[k][2][i] - o["logC"][k]) < 1e-10
         wo, co, Bo = o["final"]
         assert rel_linf(w[b], O.to_lib(wo)) < 1e-10
-        assert rel_linf(B[b], Bo) < 1e-12 and np.max(np.abs(c[b] - co)) < 1e-12 * np.max(np.abs(Bo))
+        # the centre is the re-centred mean (R12) after 50 epochs: fp64 rounding relative to
+        # |c|, not to the grid spacing (|c| ~ 50 spacings here)
+        assert rel_linf(B[b], Bo) < 1e-12
+        assert np.max(np.abs(c[b] - co)) < 1e-12 * max(np.max(np.abs(co)), np.max(np.abs(Bo)))
 
 
 def _index_moments(w, n):
