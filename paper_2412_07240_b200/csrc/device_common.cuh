@@ -29,48 +29,74 @@ template <bool INV, typename V> __device__ __forceinline__ V mul_mi(V a) {
 }
 
 // ---------------------------------------------------------------- small linear algebra (stride 4)
+// Every loop runs to 4 under an `nx` guard and is fully unrolled, so the 4x4 arrays stay in
+// registers (no local-memory stack) whether nx is a compile-time constant or not; the
+// arithmetic and its order are those of the plain nx-bounded loops.
 __device__ __forceinline__ void mat_mul4(int nx, const double* A, const double* B, double* C) {
-    for (int i = 0; i < nx; ++i)
-        for (int j = 0; j < nx; ++j) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            if (i >= nx || j >= nx) continue;
             double s = 0.0;
-            for (int k = 0; k < nx; ++k) s = fma(A[i * 4 + k], B[k * 4 + j], s);
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                if (k < nx) s = fma(A[i * 4 + k], B[k * 4 + j], s);
             C[i * 4 + j] = s;
         }
 }
 
-// Gauss-Jordan inverse with partial pivoting; returns determinant (0 if singular).
-__device__ inline double mat_inv4(int nx, const double* A, double* Ai) {
+// Gauss-Jordan inverse with partial pivoting; returns determinant (0 if singular). The pivot
+// row swap is a chain of predicated exchanges over compile-time row indices.
+__device__ __forceinline__ double mat_inv4(int nx, const double* A, double* Ai) {
     double M[16], I[16];
+#pragma unroll
     for (int i = 0; i < 16; ++i) { M[i] = A[i]; I[i] = 0.0; }
-    for (int i = 0; i < nx; ++i) I[i * 4 + i] = 1.0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+        if (i < nx) I[i * 4 + i] = 1.0;
     double det = 1.0;
-    for (int col = 0; col < nx; ++col) {
+#pragma unroll
+    for (int col = 0; col < 4; ++col) {
+        if (col >= nx) break;
         int piv = col;
         double best = fabs(M[col * 4 + col]);
-        for (int r = col + 1; r < nx; ++r)
-            if (fabs(M[r * 4 + col]) > best) { best = fabs(M[r * 4 + col]); piv = r; }
+#pragma unroll
+        for (int r = col + 1; r < 4; ++r)
+            if (r < nx && fabs(M[r * 4 + col]) > best) { best = fabs(M[r * 4 + col]); piv = r; }
         if (best == 0.0) return 0.0;
-        if (piv != col) {
+#pragma unroll
+        for (int r = col + 1; r < 4; ++r) {
+            const bool sw = piv == r;
+#pragma unroll
             for (int k = 0; k < 4; ++k) {
-                double t = M[col * 4 + k]; M[col * 4 + k] = M[piv * 4 + k]; M[piv * 4 + k] = t;
-                t = I[col * 4 + k]; I[col * 4 + k] = I[piv * 4 + k]; I[piv * 4 + k] = t;
+                const double mc = M[col * 4 + k], mr = M[r * 4 + k];
+                const double ic = I[col * 4 + k], ir = I[r * 4 + k];
+                M[col * 4 + k] = sw ? mr : mc;
+                M[r * 4 + k] = sw ? mc : mr;
+                I[col * 4 + k] = sw ? ir : ic;
+                I[r * 4 + k] = sw ? ic : ir;
             }
-            det = -det;
         }
+        if (piv != col) det = -det;
         double p = M[col * 4 + col];
         det *= p;
         double ip = 1.0 / p;
+#pragma unroll
         for (int k = 0; k < 4; ++k) { M[col * 4 + k] *= ip; I[col * 4 + k] *= ip; }
-        for (int r = 0; r < nx; ++r) {
-            if (r == col) continue;
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            if (r == col || r >= nx) continue;
             double f = M[r * 4 + col];
             if (f == 0.0) continue;
+#pragma unroll
             for (int k = 0; k < 4; ++k) {
                 M[r * 4 + k] = fma(-f, M[col * 4 + k], M[r * 4 + k]);
                 I[r * 4 + k] = fma(-f, I[col * 4 + k], I[r * 4 + k]);
             }
         }
     }
+#pragma unroll
     for (int i = 0; i < 16; ++i) Ai[i] = I[i];
     return det;
 }
@@ -96,34 +122,63 @@ __device__ __forceinline__ int pair_index(int nx, int a, int b) {
 // cross term folded in), D_n = B^-1 E_n B^-T (FULL) or diag(Q_mm/||B_n[:,m]||^2)
 // (AXIS_LITERAL). Writes 10 doubles per substep (packed as pair_index).
 // One substep n (Bi = B^-1 precomputed by the caller; 10 doubles to `o`).
-__device__ inline void substep_coefs(int nx, const double* B, const double* Bi, const ModelParams& mp,
-                                     const SubstepEntry& e, double* o) {
+__device__ __forceinline__ void substep_coefs(int nx, const double* B, const double* Bi, const ModelParams& mp,
+                                              const SubstepEntry& e, double* o) {
     double D[16];
     if (mp.diff_mode == 0) {
-        double T1[16], BiT[16];
+        double T1[16], BiT[16], E[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) E[i] = e.E[i];
+#pragma unroll
         for (int i = 0; i < 4; ++i)
+#pragma unroll
             for (int j = 0; j < 4; ++j) BiT[i * 4 + j] = Bi[j * 4 + i];
-        mat_mul4(nx, Bi, e.E, T1);
+        mat_mul4(nx, Bi, E, T1);
         mat_mul4(nx, T1, BiT, D);
     } else {
-        double Bn[16];
-        mat_mul4(nx, e.P, B, Bn);
+        double Bn[16], Pn[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) Pn[i] = e.P[i];
+        mat_mul4(nx, Pn, B, Bn);
+#pragma unroll
         for (int i = 0; i < 16; ++i) D[i] = 0.0;
-        for (int m = 0; m < nx; ++m) {
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+            if (m >= nx) continue;
             double len2 = 0.0;
-            for (int r = 0; r < nx; ++r) len2 = fma(Bn[r * 4 + m], Bn[r * 4 + m], len2);
+#pragma unroll
+            for (int r = 0; r < 4; ++r)
+                if (r < nx) len2 = fma(Bn[r * 4 + m], Bn[r * 4 + m], len2);
             D[m * 4 + m] = mp.Q[m * 4 + m] / len2;
         }
     }
-    for (int k = 0; k < 10; ++k) o[k] = 0.0;
+    double out[10];
+#pragma unroll
+    for (int k = 0; k < 10; ++k) out[k] = 0.0;
     // f_n = 1 + h kappa^T D_n kappa: h = dt/2 (Euler factor 1/f_n), dt/4 (Crank-Nicolson:
     // (2 - f_n) / f_{n+1})
     const double h = mp.step ? 0.25 * mp.dt : 0.5 * mp.dt;
-    int idx = nx;
-    for (int a = 0; a < nx; ++a) {
-        o[a] = h * D[a * 4 + a];
-        for (int b = a + 1; b < nx; ++b) o[idx++] = h * (D[a * 4 + b] + D[b * 4 + a]);
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+        if (a >= nx) continue;
+        out[a] = h * D[a * 4 + a];
+#pragma unroll
+        for (int b = a + 1; b < 4; ++b) {
+            if (b >= nx) continue;
+            // packed index of (a, b): nx + the pairs before it (pair_index order)
+            int idx = nx;
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = i + 1; j < 4; ++j)
+                    if (j < nx && (i < a || (i == a && j < b))) ++idx;
+            // (idx < 10 always; selects keep `out` in registers)
+#pragma unroll
+            for (int k = 0; k < 10; ++k)
+                if (k == idx) out[k] = h * (D[a * 4 + b] + D[b * 4 + a]);
+        }
     }
+    for (int k = 0; k < 10; ++k) o[k] = out[k];
 }
 
 __device__ inline void epoch_coefs(const double* B, const ModelParams& mp,
@@ -298,15 +353,100 @@ __device__ inline void finish_moments(int nx, const double* acc, const double* c
 
 // New grid of the re-centring policy (R12): c' = mean, B' = diag(2 ks sqrt(cov_mm)/N_m).
 // Returns false when some variance is non-finite or <= 0.
-__device__ inline bool regrid_target(int nx, const int* n, const FilterState& st, double ks,
-                                     double* cn, double* Bn, int grid = 0) {
-    if (grid == 1) {                          // R28: eigen-aligned
-        for (int a = 0; a < nx; ++a) cn[a] = st.mean[a];
-        return eigen_grid(nx, n, st.cov, ks, Bn);
+// Linear-Gaussian likelihood exponent as a quadratic form in the moved grid's index
+// coordinates u (R13): r(u) = (z - H c) - (H B) u, e = r^T R^-1 r = q[0] + sum_a q[1+a] u_a +
+// sum_{a<=b} q[5+tri(a,b)] u_a u_b. Loops unrolled to 4 under nx / nz guards (registers only).
+__device__ __forceinline__ void lik_quadform(int nx, const LikParams& lp, const double* c, const double* B,
+                                             const double* zf, double* q) {
+    const int nz = lp.nz;
+    double r0[4], G[16], w[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        r0[i] = 0.0;
+        w[i] = 0.0;
+#pragma unroll
+        for (int a = 0; a < 4; ++a) G[i * 4 + a] = 0.0;
+        if (i >= nz) continue;
+        double hc = 0.0;
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+            if (a < nx) hc = fma(lp.H[i * 4 + a], c[a], hc);
+        r0[i] = zf[i] - hc;
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+            if (a >= nx) continue;
+            double g = 0.0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                if (k < nx) g = fma(lp.H[i * 4 + k], B[k * 4 + a], g);
+            G[i * 4 + a] = g;
+        }
     }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {     // R^-1 r0
+        if (i >= nz) continue;
+        double s = 0.0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            if (j < nz) s = fma(lp.Rinv[i * 4 + j], r0[j], s);
+        w[i] = s;
+    }
+    double qa = 0.0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+        if (i < nz) qa = fma(r0[i], w[i], qa);
+    q[0] = qa;
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+        if (a >= nx) continue;
+        double s = 0.0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+            if (i < nz) s = fma(G[i * 4 + a], w[i], s);
+        q[1 + a] = -2.0 * s;
+    }
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int c2 = a; c2 < 4; ++c2) {
+            if (c2 >= nx) continue;
+            double s = 0.0;
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    if (i < nz && j < nz) s = fma(G[i * 4 + a] * lp.Rinv[i * 4 + j], G[j * 4 + c2], s);
+            q[5 + tri(a, c2)] = (a == c2) ? s : 2.0 * s;
+        }
+}
+
+// (the Jacobi rotations index their arrays dynamically: kept out of line so that the
+// caller's arrays stay in registers; only this branch's copy goes through local memory)
+static __device__ __noinline__ bool eigen_grid_dev(int nx, const int* n, const double* cov, double ks, double* B) {
+    return eigen_grid(nx, n, cov, ks, B);
+}
+
+__device__ __forceinline__ bool regrid_target(int nx, const int* n, const FilterState& st, double ks,
+                                              double* cn, double* Bn, int grid = 0) {
+    if (grid == 1) {                          // R28: eigen-aligned
+        double Be[16];
+        int ng[4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a) ng[a] = a < nx ? n[a] : 1;
+        const bool ok = eigen_grid_dev(nx, ng, st.cov, ks, Be);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) Bn[i] = Be[i];
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+            if (a < nx) cn[a] = st.mean[a];
+        return ok;
+    }
+#pragma unroll
     for (int i = 0; i < 16; ++i) Bn[i] = 0.0;
     bool ok = true;
-    for (int a = 0; a < nx; ++a) {
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+        if (a >= nx) continue;
         double v = st.cov[a * 4 + a];
         if (!(v > 0.0) || !isfinite(v)) ok = false;
         cn[a] = st.mean[a];

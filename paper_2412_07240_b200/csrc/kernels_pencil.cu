@@ -159,9 +159,12 @@ __global__ void k_predict_prep(FilterState* st, double* coef, int cstride, Model
     double Bn[16], cn[4];
     for (int i = 0; i < 16; ++i) Bn[i] = 0.0;
     mat_mul4(nx, mp.Mtau, f.B, Bn);
-    for (int a = 0; a < nx; ++a) {
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
         double s = 0.0;
-        for (int k = 0; k < nx; ++k) s = fma(mp.Mtau[a * 4 + k], f.c[k], s);
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            if (k < nx) s = fma(mp.Mtau[a * 4 + k], f.c[k], s);
         cn[a] = s;
     }
     double voll = fabs(det4(nx, Bn));
@@ -170,41 +173,7 @@ __global__ void k_predict_prep(FilterState* st, double* coef, int cstride, Model
     f.scale = vol0 / (voll * mp.s);
     double* q = cf + lq_off(mp.l);
     for (int i = 0; i < 16; ++i) q[i] = 0.0;
-    if (update && lp.kind == 0) {
-        const double* zf = z + (long long)b * lp.nz;
-        double r0[4], G[16];
-        for (int i = 0; i < lp.nz; ++i) {
-            double hc = 0.0;
-            for (int a = 0; a < nx; ++a) hc = fma(lp.H[i * 4 + a], cn[a], hc);
-            r0[i] = zf[i] - hc;
-            for (int a = 0; a < nx; ++a) {
-                double g = 0.0;
-                for (int k = 0; k < nx; ++k) g = fma(lp.H[i * 4 + k], Bn[k * 4 + a], g);
-                G[i * 4 + a] = g;
-            }
-        }
-        double w[4];     // R^-1 r0
-        for (int i = 0; i < lp.nz; ++i) {
-            double s = 0.0;
-            for (int j = 0; j < lp.nz; ++j) s = fma(lp.Rinv[i * 4 + j], r0[j], s);
-            w[i] = s;
-        }
-        double qa = 0.0;
-        for (int i = 0; i < lp.nz; ++i) qa = fma(r0[i], w[i], qa);
-        q[0] = qa;
-        for (int a = 0; a < nx; ++a) {
-            double s = 0.0;
-            for (int i = 0; i < lp.nz; ++i) s = fma(G[i * 4 + a], w[i], s);
-            q[1 + a] = -2.0 * s;
-        }
-        for (int a = 0; a < nx; ++a)
-            for (int c = a; c < nx; ++c) {
-                double s = 0.0;
-                for (int i = 0; i < lp.nz; ++i)
-                    for (int j = 0; j < lp.nz; ++j) s = fma(G[i * 4 + a] * lp.Rinv[i * 4 + j], G[j * 4 + c], s);
-                q[5 + tri(a, c)] = (a == c) ? s : 2.0 * s;
-            }
-    }
+    if (update && lp.kind == 0) lik_quadform(nx, lp, cn, Bn, z + (long long)b * lp.nz, q);
 }
 
 // ============================================================================ spectral multiplier helpers

@@ -110,38 +110,7 @@ __global__ void k_plane_prep(FilterState* st, double* coef, int cs, ModelParams 
     double* q = P + PL_LQ;
     for (int i = 0; i < 16; ++i) q[i] = 0.0;
     if (update && lp.kind == 0) {
-        const double* zf = z + (long long)b * lp.nz;
-        double r0[4], G[16], w[4];
-        for (int i = 0; i < lp.nz; ++i) {
-            double hc = 0.0;
-            for (int a = 0; a < NX; ++a) hc = fma(lp.H[i * 4 + a], cl[a], hc);
-            r0[i] = zf[i] - hc;
-            for (int a = 0; a < NX; ++a) {
-                double g = 0.0;
-                for (int k = 0; k < NX; ++k) g = fma(lp.H[i * 4 + k], Bl[k * 4 + a], g);
-                G[i * 4 + a] = g;
-            }
-        }
-        for (int i = 0; i < lp.nz; ++i) {
-            double s = 0.0;
-            for (int j = 0; j < lp.nz; ++j) s = fma(lp.Rinv[i * 4 + j], r0[j], s);
-            w[i] = s;
-        }
-        double qa = 0.0;
-        for (int i = 0; i < lp.nz; ++i) qa = fma(r0[i], w[i], qa);
-        q[0] = qa;
-        for (int a = 0; a < NX; ++a) {
-            double s = 0.0;
-            for (int i = 0; i < lp.nz; ++i) s = fma(G[i * 4 + a], w[i], s);
-            q[1 + a] = -2.0 * s;
-        }
-        for (int a = 0; a < NX; ++a)
-            for (int c = a; c < NX; ++c) {
-                double s = 0.0;
-                for (int i = 0; i < lp.nz; ++i)
-                    for (int j = 0; j < lp.nz; ++j) s = fma(G[i * 4 + a] * lp.Rinv[i * 4 + j], G[j * 4 + c], s);
-                q[5 + tri(a, c)] = (a == c) ? s : 2.0 * s;
-            }
+        lik_quadform(NX, lp, cl, Bl, z + (long long)b * lp.nz, q);
     } else if (update) {
         P[PL_ZR] = z[b];
     }
@@ -163,13 +132,16 @@ __global__ void __launch_bounds__(256) k_plane_pre(const T* __restrict__ W, T* _
     const T* Wf = W + filt * ntot;
     T* Wn = W2 + filt * ntot;
     const int nsz[4] = {d.n[0], d.n[1], d.n[2], NX == 4 ? d.n[3] : 1};
-    for (long long pt = (long long)qb * blockDim.x + threadIdx.x; pt < ntot; pt += (long long)bpf * blockDim.x) {
+    // 32-bit index arithmetic (ntot < 2^31 per filter): 64-bit divisions by runtime sizes
+    // dominated this pass
+    const unsigned nt = (unsigned)ntot;
+    for (unsigned pt = (unsigned)qb * blockDim.x + threadIdx.x; pt < nt; pt += (unsigned)bpf * blockDim.x) {
         double u[4];
-        long long r = pt;
+        unsigned r = pt;
 #pragma unroll
         for (int a2 = 0; a2 < NX; ++a2) {
-            const long long q = r / nsz[a2];
-            u[a2] = (double)(r - q * nsz[a2]) - 0.5 * (nsz[a2] - 1);
+            const unsigned q = r / (unsigned)nsz[a2];
+            u[a2] = (double)(int)(r - q * (unsigned)nsz[a2]) - 0.5 * (nsz[a2] - 1);
             r = q;
         }
         double v[4];

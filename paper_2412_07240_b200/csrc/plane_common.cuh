@@ -233,7 +233,7 @@ __device__ __forceinline__ double gather_point(const T* __restrict__ Wf, const i
     int i[4];
     double fr[4];
     bool lo[4], hi[4];
-    long long base = 0, stride[4];
+    int base = 0, stride[4];              // 32-bit: a filter's grid has < 2^31 points (pmf_create)
     stride[0] = 1;
 #pragma unroll
     for (int a = 1; a < NX; ++a) stride[a] = stride[a - 1] * n[a - 1];
@@ -244,13 +244,13 @@ __device__ __forceinline__ double gather_point(const T* __restrict__ Wf, const i
         fr[a] = v[a] - fl;
         lo[a] = i[a] >= 0 && i[a] <= n[a] - 1;
         hi[a] = i[a] >= -1 && i[a] <= n[a] - 2;
-        base += (long long)i[a] * stride[a];
+        base += i[a] * stride[a];
     }
     double val = 0.0;
 #pragma unroll
     for (int c = 0; c < (1 << NX); ++c) {
         double wt = 1.0;
-        long long off = base;
+        int off = base;
         bool ok = true;
 #pragma unroll
         for (int a = 0; a < NX; ++a) {
