@@ -228,9 +228,9 @@ __global__ void __launch_bounds__(Cfg<N>::NT, Cfg<N>::MINB) k_plane_fwd(PlaneArg
         if (tid == 0) tma::mbar_expect_tx(bar, (unsigned)(N * N * sizeof(T)));
         tma::bulk_g2s(stg + (tid + 1) * SP + OFF, src + (long long)tid * N, (unsigned)(N * sizeof(T)), bar);
     };
-    if (SEP) issue(blockIdx.x);
+    if (SEP) issue(a.pbeg + blockIdx.x);
     int k = 0;
-    for (int p = blockIdx.x; p < a.nplanes; p += gridDim.x, ++k) {
+    for (int p = a.pbeg + blockIdx.x; p < a.nplanes; p += gridDim.x, ++k) {
         if (!SEP) {
             if (k > 0) {
                 zero_ring<T, N>(stg, tid, NT);
@@ -1205,7 +1205,8 @@ static cudaError_t plane_t(const Dims& d, PencilBufs& b, const ModelParams& mp, 
     pa.range = lpv.kind == 1;
     // general regrid maps: gather pre-pass into W2 (exits at once for the other filters)
     if (rg) {
-        const int bpf = (int)std::max(1LL, std::min(1024LL, (d.ntot + 2047) / 2048));
+        // one point per thread: the 2^nx-tap gathers are latency-bound, a thread's points serial
+        const int bpf = (int)std::max(1LL, std::min(1LL << 22, (d.ntot + 255) / 256));
         k_plane_pre<T, NX><<<(unsigned)(bpf * d.batch), 256, 0, s>>>((const T*)b.W, (T*)b.W2, b.coef, cs, d, bpf);
         ++*launches;
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
@@ -1322,7 +1323,8 @@ cudaError_t launch_plane_prep(const Dims& d, PencilBufs& b, const ModelParams& m
 
 template <int N>
 static cudaError_t fwd_chunks_n(const Dims& d, PencilBufs& b, const ModelParams& mp, int chunks,
-                                long long chunk_stride, double* dcpart, cudaStream_t s, int64_t* launches) {
+                                long long chunk_stride, double* dcpart, int pbeg, int pend, cudaStream_t s,
+                                int64_t* launches) {
     using Cf = Cfg<N>;
     PlaneArgs<double> pa{};
     pa.Wsrc = (const double*)b.W;
@@ -1340,9 +1342,14 @@ static cudaError_t fwd_chunks_n(const Dims& d, PencilBufs& b, const ModelParams&
     pa.l = mp.l;
     pa.chunks = chunks;
     pa.chunk_stride = chunk_stride;
+    if (pend >= 0) {                       // a sub-range of the planes (pipelined exchange)
+        pa.pbeg = pbeg;
+        pa.nplanes = pend;
+    }
+    if (pa.nplanes <= pa.pbeg) return cudaSuccess;
     const size_t smem = fwd_smem<double, N>();
     int grid = 1;
-    cudaError_t e = occ_grid(k_plane_fwd<double, N, 4, false>, Cf::NT, smem, pa.nplanes, &grid);
+    cudaError_t e = occ_grid(k_plane_fwd<double, N, 4, false>, Cf::NT, smem, pa.nplanes - pa.pbeg, &grid);
     if (e != cudaSuccess) return e;
     k_plane_fwd<double, N, 4, false><<<grid, Cf::NT, smem, s>>>(pa);
     ++*launches;
@@ -1350,11 +1357,12 @@ static cudaError_t fwd_chunks_n(const Dims& d, PencilBufs& b, const ModelParams&
 }
 
 cudaError_t launch_plane_fwd_chunks(const Dims& d, PencilBufs& b, const ModelParams& mp, int chunks,
-                                    long long chunk_stride, double* dcpart, cudaStream_t s, int64_t* launches) {
+                                    long long chunk_stride, double* dcpart, int pbeg, int pend, cudaStream_t s,
+                                    int64_t* launches) {
     switch (d.n[0]) {
-        case 32: return fwd_chunks_n<32>(d, b, mp, chunks, chunk_stride, dcpart, s, launches);
-        case 64: return fwd_chunks_n<64>(d, b, mp, chunks, chunk_stride, dcpart, s, launches);
-        case 96: return fwd_chunks_n<96>(d, b, mp, chunks, chunk_stride, dcpart, s, launches);
+        case 32: return fwd_chunks_n<32>(d, b, mp, chunks, chunk_stride, dcpart, pbeg, pend, s, launches);
+        case 64: return fwd_chunks_n<64>(d, b, mp, chunks, chunk_stride, dcpart, pbeg, pend, s, launches);
+        case 96: return fwd_chunks_n<96>(d, b, mp, chunks, chunk_stride, dcpart, pbeg, pend, s, launches);
         default: return cudaErrorInvalidValue;
     }
 }

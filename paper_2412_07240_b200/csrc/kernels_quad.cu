@@ -68,6 +68,9 @@ struct QArgs {
     int N0f;                 // N_0 (wavenumbers)
     int koff;
     int G, slab, j3off, n3g;
+    // K2 over a k0 sub-range (pipelined back exchange): items (k1, k0 in [kbeg, kbeg + N0)) of the
+    // input's N0blk k0 columns; the output blocks keep their full k0 extent N0blk
+    int kbeg = 0, N0blk = 0;
     // S2 layout: G == 1 -> [filter][k1][k0][j3][j2]; G > 1 -> per destination block
     // [k0][k1][j3 % slab][j2] (k0 outermost, so the back exchange stacks the blocks into k0)
 };
@@ -201,7 +204,7 @@ __global__ void __launch_bounds__(QCfg<NQ, TM>::NT, 1) k_q_mid(QArgs a, int I, i
     // has ordered the rows' earlier reads before it); 128-byte aligned (P RP = 0 mod 8)
     auto load_part = [&](int it, int c) {
         const unsigned fi = (unsigned)it / (unsigned)I, ii = (unsigned)it - fi * (unsigned)I;
-        const unsigned k1 = ii / (unsigned)N0, k0 = ii - k1 * (unsigned)N0;
+        const unsigned k1 = ii / (unsigned)N0, k0 = ii - k1 * (unsigned)N0 + (unsigned)a.kbeg;
         asm volatile(
             "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, "
             "%6}], [%7];" ::"r"(tma::smem_u32(X + c * RP * P)),
@@ -237,7 +240,7 @@ __global__ void __launch_bounds__(QCfg<NQ, TM>::NT, 1) k_q_mid(QArgs a, int I, i
             const double* cf = Pg + PL_EU;
             const int cn = a.step, l = a.l;
             const unsigned k1 = i / (unsigned)N0;
-            const int N0f = a.N0f, k0 = a.koff + (int)(i - k1 * (unsigned)N0);   // global k0
+            const int N0f = a.N0f, k0 = a.koff + a.kbeg + (int)(i - k1 * (unsigned)N0);   // global k0
             const int N1 = 2 * (H1 - 1);
             double kap[3], kx[3];
             kap[0] = (2.0 * PMF_PI / N0f) * (k0 < N0f / 2 ? k0 : k0 - N0f);
@@ -358,7 +361,7 @@ __global__ void __launch_bounds__(QCfg<NQ, TM>::NT, 1) k_q_mid(QArgs a, int I, i
                 __syncwarp();
                 tdft_s1<R, false>(x, col, tw, t, cs);
                 __syncwarp();
-                const bool dc = flag == 4 && i == 0 && a.koff == 0 && k2 == 0;
+                const bool dc = flag == 4 && i == 0 && a.koff + a.kbeg == 0 && k2 == 0;
                 tdft_s2<R>(col, t, cs, [&](int s3, V* p) {
                     reg::dft8<false>(p);                      // X(k2, k3 = s3 + R qq)
                     if (dc && s3 == 0) {
@@ -391,10 +394,11 @@ __global__ void __launch_bounds__(QCfg<NQ, TM>::NT, 1) k_q_mid(QArgs a, int I, i
         // output row j3 of this item: G == 1: S2[f][k1][k0][j3][j2]; G > 1: S2 (rank j3 / slab's
         // block)[k0][k1][j3 % slab][j2]. (Measured: the k0-major order for G == 1 doubles K3's
         // DRAM reads of S2 -- the same sectors, gathered in a different order, miss L2.)
-        const unsigned ok1 = i / (unsigned)N0, ok0 = i - ok1 * (unsigned)N0;
-        V* dst = a.Y + (long long)f * ((long long)a.G * N0 * H1 * a.slab * NQ) +
+        const unsigned ok1 = i / (unsigned)N0, ok0 = i - ok1 * (unsigned)N0 + (unsigned)a.kbeg;
+        const int NB = a.N0blk ? a.N0blk : N0;                            // k0 extent of an output block
+        V* dst = a.Y + (long long)f * ((long long)a.G * NB * H1 * a.slab * NQ) +
                  (a.G == 1 ? (long long)i : ((long long)ok0 * H1 + ok1)) * ((long long)a.slab * NQ);
-        const long long rstride = (long long)N0 * H1 * a.slab * NQ;      // between destination blocks
+        const long long rstride = (long long)NB * H1 * a.slab * NQ;      // between destination blocks
 #pragma unroll 1
         for (int c = 0; c < NPART; ++c) {
 #pragma unroll 1
@@ -895,17 +899,18 @@ static cudaError_t qmid_launch(const QArgs& qa, int I, int N0, int H1, const CUt
 // K1 -> K2 -> K3 (prep, the general-map pre-pass and the finaliser are the plane path's;
 // launch_plane calls this between them). Returns the K3 grid (its partials per filter).
 template <int N>
-static cudaError_t quad_mid_n(const Dims& d, QArgs qa, int N0c, cudaStream_t s) {
+static cudaError_t quad_mid_n(const Dims& d, QArgs qa, int N0c, cudaStream_t s, int nk = -1) {
     using Cf = Cfg<N>;
     CUtensorMap smap;
     cudaError_t e = s_map(qa, N0c, Cf::H, &smap);
     if (e != cudaSuccess) return e;
-    const int I = Cf::H * N0c;
+    if (nk < 0) nk = N0c;                   // k0 columns [kbeg, kbeg + nk) of the N0c in the input
+    const int I = Cf::H * nk;
     switch (d.n[2]) {
-        case 16: return qmid_launch<16>(qa, I, N0c, Cf::H, smap, s);
-        case 32: return qmid_launch<32>(qa, I, N0c, Cf::H, smap, s);
-        case 64: return qmid_launch<64>(qa, I, N0c, Cf::H, smap, s);
-        case 96: return qmid_launch<96>(qa, I, N0c, Cf::H, smap, s);
+        case 16: return qmid_launch<16>(qa, I, nk, Cf::H, smap, s);
+        case 32: return qmid_launch<32>(qa, I, nk, Cf::H, smap, s);
+        case 64: return qmid_launch<64>(qa, I, nk, Cf::H, smap, s);
+        case 96: return qmid_launch<96>(qa, I, nk, Cf::H, smap, s);
         default: return cudaErrorInvalidValue;
     }
 }
@@ -988,7 +993,7 @@ cudaError_t launch_quad(const Dims& d, PencilBufs& b, const ModelParams& mp, int
 // [j3 % slab][j2]; K3 of rank r over its slab's planes reading `in` = [k0][k1][j3 % slab][j2]
 // (the back exchange, source blocks stacked in rank order) and writing the shard's weights.
 cudaError_t launch_quad_mid_shard(const Dims& d, PencilBufs& b, const ModelParams& mp, int rank, int world,
-                                  const void* in, void* out, cudaStream_t s, int64_t* launches) {
+                                  const void* in, void* out, int kbeg, int kend, cudaStream_t s, int64_t* launches) {
     QArgs qa = make_qargs(d, b, mp, 0, nullptr, nullptr);
     qa.Yin = (const V*)in;
     qa.Y = (V*)out;
@@ -998,11 +1003,18 @@ cudaError_t launch_quad_mid_shard(const Dims& d, PencilBufs& b, const ModelParam
     qa.koff = rank * (d.ng[0] / world);
     qa.n3g = d.ng[3];
     const int N0c = d.ng[0] / world;
+    if (kend < 0) {
+        kbeg = 0;
+        kend = N0c;
+    }
+    if (kend <= kbeg) return cudaSuccess;
+    qa.kbeg = kbeg;
+    qa.N0blk = N0c;
     cudaError_t e;
     switch (d.n[0]) {
-        case 32: e = quad_mid_n<32>(d, qa, N0c, s); break;
-        case 64: e = quad_mid_n<64>(d, qa, N0c, s); break;
-        case 96: e = quad_mid_n<96>(d, qa, N0c, s); break;
+        case 32: e = quad_mid_n<32>(d, qa, N0c, s, kend - kbeg); break;
+        case 64: e = quad_mid_n<64>(d, qa, N0c, s, kend - kbeg); break;
+        case 96: e = quad_mid_n<96>(d, qa, N0c, s, kend - kbeg); break;
         default: e = cudaErrorInvalidValue;
     }
     if (e == cudaSuccess) ++*launches;

@@ -218,6 +218,7 @@ struct PlaneArgs {
     int range;              // likelihood kind 1
     int chunks = 1;         // forward pass: each spectrum row leaves as `chunks` pieces of N / chunks
     long long chunk_stride = 0;   // ... piece q to S + q chunk_stride + (plane H + k1) N / chunks (sharded)
+    int pbeg = 0;           // forward pass: planes [pbeg, nplanes) (sharded: one chunk of the slab's planes)
 };
 
 // plane p of its filter -> (j2, j3)

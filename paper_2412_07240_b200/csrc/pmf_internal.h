@@ -215,11 +215,12 @@ int quad_debug_counters(double* out, int n, int reset);
 cudaError_t launch_plane_prep(const Dims& d, PencilBufs& b, const ModelParams& mp, const LikParams* lp, cudaStream_t s,
                               int64_t* launches);
 cudaError_t launch_plane_fwd_chunks(const Dims& d, PencilBufs& b, const ModelParams& mp, int chunks,
-                                    long long chunk_stride, double* dcpart, cudaStream_t s, int64_t* launches);
+                                    long long chunk_stride, double* dcpart, int pbeg, int pend, cudaStream_t s,
+                                    int64_t* launches);
 cudaError_t launch_plane_fin_tot(const Dims& d, PencilBufs& b, const ModelParams& mp, double* tot, int update,
                                  cudaStream_t s, int64_t* launches);
 cudaError_t launch_quad_mid_shard(const Dims& d, PencilBufs& b, const ModelParams& mp, int rank, int world,
-                                  const void* in, void* out, cudaStream_t s, int64_t* launches);
+                                  const void* in, void* out, int kbeg, int kend, cudaStream_t s, int64_t* launches);
 cudaError_t launch_quad_inv_shard(const Dims& d, PencilBufs& b, const ModelParams& mp, const LikParams* lp, int rank,
                                   int world, const void* in, double* part, cudaStream_t s, int64_t* launches,
                                   int* ginv);

@@ -124,6 +124,10 @@ struct ShardSet {
     std::vector<Shard> sh;              // virtual: world shards; real: 1
     NcclApi::Comm comm = nullptr;
     double* sum_scratch = nullptr;      // virtual all-reduce staging [world][NMOM]
+    // pipelined all-to-alls of the three-pass route: the exchanges run on `xs` (a second
+    // stream), ordered against the compute stream by events (created on first use)
+    cudaStream_t xs = nullptr;
+    std::vector<cudaEvent_t> ev;
 };
 
 }  // namespace pmf
@@ -139,14 +143,16 @@ static int nccl_poll(pmf_ctx* c) {
     return PMF_OK;
 }
 
-static int exchange(pmf_ctx* c, const std::vector<Xfer>& xs, void* (*sbuf)(Shard&), void* (*rbuf)(Shard&)) {
+static int exchange(pmf_ctx* c, const std::vector<Xfer>& xs, void* (*sbuf)(Shard&), void* (*rbuf)(Shard&),
+                    cudaStream_t st = nullptr) {
     ShardSet& S = *c->sh;
+    if (!st) st = c->stream;
     if (S.virt) {
         for (const Xfer& x : xs) {
             char* src = (char*)sbuf(S.sh[x.src]) + x.so;
             char* dst = (char*)rbuf(S.sh[x.dst]) + x.dof;
             if (x.bytes) {
-                cudaError_t e = cudaMemcpyAsync(dst, src, x.bytes, cudaMemcpyDeviceToDevice, c->stream);
+                cudaError_t e = cudaMemcpyAsync(dst, src, x.bytes, cudaMemcpyDeviceToDevice, st);
                 if (e != cudaSuccess) return pmf_cuda_fail(c, e, "virtual exchange");
             }
         }
@@ -159,13 +165,13 @@ static int exchange(pmf_ctx* c, const std::vector<Xfer>& xs, void* (*sbuf)(Shard
         if (!x.bytes) continue;
         if (x.src == S.rank && x.dst == S.rank) {
             cudaError_t e = cudaMemcpyAsync((char*)rbuf(me) + x.dof, (char*)sbuf(me) + x.so, x.bytes,
-                                            cudaMemcpyDeviceToDevice, c->stream);
+                                            cudaMemcpyDeviceToDevice, st);
             if (e != cudaSuccess) { api.GroupEnd(); return pmf_cuda_fail(c, e, "local exchange"); }
         } else if (x.src == S.rank) {
-            int r = api.Send((char*)sbuf(me) + x.so, x.bytes, NCCL_INT8, x.dst, S.comm, c->stream);
+            int r = api.Send((char*)sbuf(me) + x.so, x.bytes, NCCL_INT8, x.dst, S.comm, st);
             if (r) { api.GroupEnd(); return nccl_fail(c, r, "ncclSend"); }
         } else if (x.dst == S.rank) {
-            int r = api.Recv((char*)rbuf(me) + x.dof, x.bytes, NCCL_INT8, x.src, S.comm, c->stream);
+            int r = api.Recv((char*)rbuf(me) + x.dof, x.bytes, NCCL_INT8, x.src, S.comm, st);
             if (r) { api.GroupEnd(); return nccl_fail(c, r, "ncclRecv"); }
         }
     }
@@ -387,6 +393,9 @@ void sh_destroy(pmf_ctx* c) {
     }
     if (S->d_off) cudaFree(S->d_off);
     if (S->sum_scratch) cudaFree(S->sum_scratch);
+    if (S->xs) cudaStreamSynchronize(S->xs);
+    for (cudaEvent_t e : S->ev) cudaEventDestroy(e);
+    if (S->xs) cudaStreamDestroy(S->xs);
     if (S->comm) NcclApi::get().CommDestroy(S->comm);
     c->st = nullptr;                    // aliased shard 0's state
     delete S;
@@ -569,6 +578,23 @@ static bool sh_quad_ok(pmf_ctx* c) {
     return !(e && e[0] == '1');
 }
 
+// Chunks of the pipelined exchanges (PMF_XCHUNKS, default 4; 1 = one exchange after each pass)
+static int xchunks() {
+    const char* e = std::getenv("PMF_XCHUNKS");
+    const int v = e ? std::atoi(e) : 4;
+    return v < 1 ? 1 : (v > 16 ? 16 : v);
+}
+
+// the pieces of chunk [lo, hi) of every block in a plan: each (source, destination) block of
+// `blk` elements is split along its outermost index (j3 % slab for K1's blocks, k0 for K2's),
+// `inner` elements per index value
+static void chunk_xfers(const std::vector<Xfer>& full, size_t cb, size_t inner, int lo, int hi,
+                        std::vector<Xfer>& out) {
+    out.clear();
+    for (const Xfer& x : full)
+        out.push_back({x.src, x.dst, x.so + cb * inner * lo, x.dof + cb * inner * lo, cb * inner * (hi - lo)});
+}
+
 static int sh_predict_quad(pmf_ctx* c, const LikParams* lp) {
     ShardSet& S = *c->sh;
     const Dims& g = c->d;
@@ -577,31 +603,73 @@ static int sh_predict_quad(pmf_ctx* c, const LikParams* lp) {
     const size_t cb = c->esize * 2;
     const int nplanes = slab * NQ;
     cudaError_t e;
+    // the two all-to-alls overlap the passes next to them. K1 runs in C1 chunks
+    // of its slab (j3 ranges; each chunk's rows are contiguous in every destination block) and
+    // chunk i's pieces leave while K1 works on chunk i + 1; K2 runs in C2 chunks of its k0
+    // range and chunk i returns while K2 works on chunk i + 1. Exchanges on the stream S.xs,
+    // ordered by events; K2 (K3) starts when the last piece of the first (second) exchange is in.
+    const int C1 = std::min(xchunks(), slab), C2 = std::min(xchunks(), N0c);
+    if (!S.xs && cudaStreamCreateWithFlags(&S.xs, cudaStreamNonBlocking) != cudaSuccess)
+        return pmf_cuda_fail(c, cudaGetLastError(), "exchange stream");
+    while ((int)S.ev.size() < 2 * 16 + 2) {
+        cudaEvent_t ev;
+        if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess)
+            return pmf_cuda_fail(c, cudaGetLastError(), "exchange event");
+        S.ev.push_back(ev);
+    }
+    cudaEvent_t* ev = S.ev.data();                              // [0, 16) K1 chunks, [16, 32) K2 chunks
+    cudaEvent_t ev_x1 = S.ev[32], ev_x2 = S.ev[33];             // exchange 1 / 2 complete
+    std::vector<Xfer> x1, x2, part;
+    quad_xfers(G, blk, cb, x1, x2);
     for (Shard& sd : S.sh) {
         PencilBufs b = shard_bufs(c, sd);
         e = launch_plane_prep(sd.d, b, c->mp, lp, c->stream, &c->launches);
-        if (e == cudaSuccess)
-            e = launch_plane_fwd_chunks(sd.d, b, c->mp, G, (long long)blk, sd.partials, c->stream, &c->launches);
-        if (e != cudaSuccess) return pmf_cuda_fail(c, e, "sharded forward plane pass");
+        if (e != cudaSuccess) return pmf_cuda_fail(c, e, "sharded prep");
     }
-    std::vector<Xfer> x1, x2;
-    quad_xfers(G, blk, cb, x1, x2);
-    int rc = exchange(c, x1, [](Shard& s) -> void* { return s.S; }, [](Shard& s) -> void* { return s.recv; });
-    if (rc) return rc;
-    for (Shard& sd : S.sh) {
-        PencilBufs b = shard_bufs(c, sd);
-        e = launch_quad_mid_shard(sd.d, b, c->mp, sd.rank, G, sd.recv, sd.send, c->stream, &c->launches);
-        if (e != cudaSuccess) return pmf_cuda_fail(c, e, "sharded axis-2/3 pass");
+    // the exchange stream may still be reading last predict's buffers: order it after this
+    // predict's start (and everything before it on the compute stream)
+    for (int i = 0; i < C1; ++i) {
+        const int jb = (int)((long long)slab * i / C1), je = (int)((long long)slab * (i + 1) / C1);
+        for (Shard& sd : S.sh) {
+            PencilBufs b = shard_bufs(c, sd);
+            e = launch_plane_fwd_chunks(sd.d, b, c->mp, G, (long long)blk, sd.partials, jb * NQ, je * NQ, c->stream,
+                                        &c->launches);
+            if (e != cudaSuccess) return pmf_cuda_fail(c, e, "sharded forward plane pass");
+        }
+        if ((e = cudaEventRecord(ev[i], c->stream)) != cudaSuccess || (e = cudaStreamWaitEvent(S.xs, ev[i], 0)))
+            return pmf_cuda_fail(c, e, "exchange order");
+        chunk_xfers(x1, cb, (size_t)NQ * H * N0c, jb, je, part);
+        int rc = exchange(c, part, [](Shard& s) -> void* { return s.S; }, [](Shard& s) -> void* { return s.recv; },
+                          S.xs);
+        if (rc) return rc;
     }
-    rc = exchange(c, x2, [](Shard& s) -> void* { return s.send; }, [](Shard& s) -> void* { return s.S; });
-    if (rc) return rc;
+    if ((e = cudaEventRecord(ev_x1, S.xs)) != cudaSuccess || (e = cudaStreamWaitEvent(c->stream, ev_x1, 0)))
+        return pmf_cuda_fail(c, e, "exchange order");
+    for (int i = 0; i < C2; ++i) {
+        const int kb = (int)((long long)N0c * i / C2), ke = (int)((long long)N0c * (i + 1) / C2);
+        for (Shard& sd : S.sh) {
+            PencilBufs b = shard_bufs(c, sd);
+            e = launch_quad_mid_shard(sd.d, b, c->mp, sd.rank, G, sd.recv, sd.send, kb, ke, c->stream, &c->launches);
+            if (e != cudaSuccess) return pmf_cuda_fail(c, e, "sharded axis-2/3 pass");
+        }
+        if ((e = cudaEventRecord(ev[16 + i], c->stream)) != cudaSuccess ||
+            (e = cudaStreamWaitEvent(S.xs, ev[16 + i], 0)))
+            return pmf_cuda_fail(c, e, "exchange order");
+        chunk_xfers(x2, cb, (size_t)H * slab * NQ, kb, ke, part);
+        int rc = exchange(c, part, [](Shard& s) -> void* { return s.send; }, [](Shard& s) -> void* { return s.S; },
+                          S.xs);
+        if (rc) return rc;
+    }
+    if ((e = cudaEventRecord(ev_x2, S.xs)) != cudaSuccess || (e = cudaStreamWaitEvent(c->stream, ev_x2, 0)))
+        return pmf_cuda_fail(c, e, "exchange order");
+    int rc;
     for (Shard& sd : S.sh) {
         PencilBufs b = shard_bufs(c, sd);
         int ginv = 1;
-        double* part = sd.partials + nplanes;
-        e = launch_quad_inv_shard(sd.d, b, c->mp, lp, sd.rank, G, sd.S, part, c->stream, &c->launches, &ginv);
+        double* part_ = sd.partials + nplanes;
+        e = launch_quad_inv_shard(sd.d, b, c->mp, lp, sd.rank, G, sd.S, part_, c->stream, &c->launches, &ginv);
         if (e == cudaSuccess)
-            e = launch_shard_sum(sd.partials, nplanes, part, ginv, lp ? 1 : 0, sd.tot, c->stream, &c->launches);
+            e = launch_shard_sum(sd.partials, nplanes, part_, ginv, lp ? 1 : 0, sd.tot, c->stream, &c->launches);
         if (e != cudaSuccess) return pmf_cuda_fail(c, e, "sharded inverse plane pass");
     }
     rc = allreduce_tot(c, NTOT);
@@ -719,6 +787,25 @@ extern "C" int pmf_world(const pmf_ctx* c) { return (c && c->sh) ? c->sh->world 
 // Test hook (not in pmf.h; host only, no device): the three-pass route's exchange plans for
 // `world` ranks and blocks of `blk` complex fp64 elements: 2 world^2 rows of (source rank,
 // destination rank, source byte offset, destination byte offset, bytes), x1 then x2.
+// chunk [lo, hi) of plan `which` (0: K1 -> K2, 1: K2 -> K3) with `inner` elements per value of
+// the blocks' outermost index: the pieces sh_predict_quad's pipelined exchange issues
+extern "C" int pmf_debug_quad_chunk(int world, long long blk, int which, long long inner, int lo, int hi,
+                                    long long* out) {
+    if (world < 1 || blk < 1 || inner < 1 || lo < 0 || hi < lo || !out || (which != 0 && which != 1)) return PMF_E_ARG;
+    std::vector<Xfer> x1, x2, part;
+    quad_xfers(world, (size_t)blk, 16, x1, x2);
+    chunk_xfers(which ? x2 : x1, 16, (size_t)inner, lo, hi, part);
+    long long* o = out;
+    for (const Xfer& x : part) {
+        *o++ = x.src;
+        *o++ = x.dst;
+        *o++ = (long long)x.so;
+        *o++ = (long long)x.dof;
+        *o++ = (long long)x.bytes;
+    }
+    return PMF_OK;
+}
+
 extern "C" int pmf_debug_quad_plan(int world, long long blk, long long* out) {
     if (world < 1 || blk < 1 || !out) return PMF_E_ARG;
     std::vector<Xfer> x1, x2;
