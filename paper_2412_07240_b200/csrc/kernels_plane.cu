@@ -1205,8 +1205,7 @@ static cudaError_t plane_t(const Dims& d, PencilBufs& b, const ModelParams& mp, 
     pa.range = lpv.kind == 1;
     // general regrid maps: gather pre-pass into W2 (exits at once for the other filters)
     if (rg) {
-        // one point per thread: the 2^nx-tap gathers are latency-bound, a thread's points serial
-        const int bpf = (int)std::max(1LL, std::min(1LL << 22, (d.ntot + 255) / 256));
+        const int bpf = (int)std::max(1LL, std::min(1024LL, (d.ntot + 2047) / 2048));
         k_plane_pre<T, NX><<<(unsigned)(bpf * d.batch), 256, 0, s>>>((const T*)b.W, (T*)b.W2, b.coef, cs, d, bpf);
         ++*launches;
         if ((e = cudaGetLastError()) != cudaSuccess) return e;

@@ -150,10 +150,10 @@ __device__ __forceinline__ void q_pair(const double* qt, int l, int cn, int list
 // acc[r] *= product of list `list`'s pair quartics at kap3 = kp[r]; every thread forms the
 // quartics itself from the item table (no shuffles: the 12 Horner chains per pair overlap
 // the next pair's coefficients)
-template <int NQ>
-__device__ __forceinline__ void q_psi_prod(double (&acc)[NQ / 8], const double (&kp)[NQ / 8], const double* qt, int l,
+template <int NQ, int R = NQ / 8>
+__device__ __forceinline__ void q_psi_prod(double (&acc)[R], const double* kp, const double* qt, int l,
                                            int cn, int list, double kap2sq, double kx2, int t) {
-    constexpr int R = NQ / 8;
+    static_assert((NQ / 2) >> 3 < R, "the Nyquist value k3 = NQ/2 must be among the thread's values");
     const int nq = (l + 1) >> 1;
     double nyq = 1.0;
     // (measured: software-pipelining pair j + 1's quartic under pair j's Horner chains, or
@@ -256,6 +256,42 @@ __global__ void __launch_bounds__(QCfg<NQ, TM>::NT, 1) k_q_mid(QArgs a, int I, i
                 const int kk = t + 8 * r;
                 kp[r] = (2.0 * PMF_PI / NQ) * (kk < NQ / 2 ? kk : kk - NQ);
             }
+            // Point symmetry: when no Euler factor couples (k0, k1) with (k2, k3) (d_n = e_n = 0 in
+            // the item table -- the two independent CV blocks of C4), f_n(k2, k3) = f_n(-k2, -k3)
+            // (R7: kx = 0 and kap^2 = pi^2 at the Nyquist index either way), so each thread
+            // evaluates its values with k3 = t + 8r <= NQ/2 + 7 only and writes every value twice,
+            // at (k2, k3) and (-k2, -k3): 7 of the 12 Horner sweeps at NQ = 96. The mirrored
+            // entries are covered by the owner of column -k2 (bitwise-equal values where two
+            // threads write the same entry: k3 = 0, NQ/2).
+            bool sym = true;
+            for (int n = 0; n < l + cn; ++n) sym = sym && qt[6 * n + 1] == 0.0 && qt[6 * n + 2] == 0.0;
+            constexpr int RH = NQ % 16 == 0 ? NQ / 16 + 1 : R;
+            if (sym && RH < R) {
+#pragma unroll 1
+                for (int k2 = q; k2 < NQ; k2 += TEAMS) {
+                    const double kap2 = (2.0 * PMF_PI / NQ) * (k2 < NQ / 2 ? k2 : k2 - NQ);
+                    const double kx2 = (2 * k2 == NQ) ? 0.0 : kap2;
+                    double den[RH], ps[RH];
+#pragma unroll
+                    for (int r = 0; r < RH; ++r) den[r] = 1.0;
+                    q_psi_prod<NQ, RH>(den, kp, qt, l, cn, 0, kap2 * kap2, kx2, t);
+                    psi_div<RH>(den, mult, ps);
+                    if (cn) {                                 // Crank-Nicolson numerators (R27)
+#pragma unroll
+                        for (int r = 0; r < RH; ++r) den[r] = 1.0;
+                        q_psi_prod<NQ, RH>(den, kp, qt, l, cn, 1, kap2 * kap2, kx2, t);
+#pragma unroll
+                        for (int r = 0; r < RH; ++r) ps[r] *= den[r];
+                    }
+                    const int m2 = k2 ? NQ - k2 : 0;
+#pragma unroll
+                    for (int r = 0; r < RH; ++r) {
+                        const int k3 = t + 8 * r;
+                        psi[k2 * PSP + k3] = ps[r];
+                        psi[m2 * PSP + (k3 ? NQ - k3 : 0)] = ps[r];
+                    }
+                }
+            } else
             // team q: columns k2 = q + TEAMS j; thread t: k3 = t + 8 r
 #pragma unroll 1
             for (int k2 = q; k2 < NQ; k2 += TEAMS) {
