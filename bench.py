@@ -568,7 +568,8 @@ def dominant_kernel(cfg, f, pmf, wl, epoch_kernel, esize, points_step):
         return {"name": f"k_dst<{cfg.n[-1]}, {'true' if cfg.nx == 1 else 'false'}, 2>",
                 "bytes": 2 * esize * points_step, "per": f"{2 * esize} B per grid point"}
     if f.path == pmf.PATH_RESIDENT:
-        return {"name": f"k_resident_epoch<{tname}, 1, 1>", "bytes": 2 * esize * points_step,
+        cn = 1 if wl.get("step", 0) else 0                # template <T, RG, UPDATE, CN>
+        return {"name": f"k_resident_epoch<{tname}, 1, 1, {cn}>", "bytes": 2 * esize * points_step,
                 "per": f"{2 * esize} B per grid point"}
     if f.path == pmf.PATH_PLANE and cfg.nx == 4 and cfg.dtype == "f64" and cfg.n[2] == cfg.n[3]:
         # K2: reads and writes the half spectrum once
