@@ -499,6 +499,8 @@ def run_workload(args, workload, rank, world, local, secondary=False):
                 "achieved_GBps": dom["bytes"] / (kern_ms * 1e-3) / 1e9 if kern_ms > 0 else None,
                 "dram_bytes_ncu": km.get("dram_bytes"), "fp64_pipe_frac_ncu":
                     (km["fp64_pipe_pct"] / 100.0) if "fp64_pipe_pct" in km else None,
+                # the co-bottleneck of the FFT passes: shared-memory wavefronts (% of peak, ncu)
+                "smem_wavefronts_frac_ncu": (km["smem_wavefronts_pct"] / 100.0) if "smem_wavefronts_pct" in km else None,
                 "ncu_source": km.get("source")}]
     ls = launch_shares(workload)
     roof = {"bound": "hbm", "achieved": achieved, "peak": hbm_gbs, "unit": "GB/s", "frac": achieved / hbm_gbs,

@@ -14,7 +14,7 @@ from typing import Optional
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libpmf.so")
+LIB_PATH = os.environ.get("PMF_LIB") or os.path.join(_HERE, "libpmf.so")   # PMF_LIB: A/B builds (tools/ab.sh)
 
 PMF_OK = 0
 ERRORS = {-1: "PMF_E_ARG", -2: "PMF_E_ODD_N", -3: "PMF_E_RADIX", -4: "PMF_E_Q_NOT_PSD",

@@ -34,6 +34,7 @@ m = {"dram_bytes": num("dram__bytes_read.sum") + num("dram__bytes_write.sum"),
      "dram_read": num("dram__bytes_read.sum"), "dram_write": num("dram__bytes_write.sum"),
      "duration_s": num("gpu__time_duration.sum"),
      "fp64_pipe_pct": float(d["sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"]),
+     "smem_wavefronts_pct": float(d["l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed"]),
      "sm_clock_hz": num("sm__cycles_elapsed.avg.per_second") * (1e9 if unit.get("sm__cycles_elapsed.avg.per_second") == "Ghz" else 1),
      "source": a.source or a.rep}
 path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", "kernel_metrics.json")
