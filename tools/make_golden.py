@@ -2,7 +2,7 @@
 """Write the full-size oracle fixtures the GPU parity tests compare against (test
 infrastructure: calls only oracle/ and workloads/, never the CUDA path):
 
-    python tools/make_golden.py C4 1 8192      # 96^4, epochs 0..1, 8192 sampled weights per epoch
+    python tools/make_golden.py C4 2 8192      # 96^4, epochs 0..2, 8192 sampled weights per epoch
     python tools/make_golden.py C3 50 2048     # 128^3, all 50 epochs
 
 tests/golden/<cfg>_full_T<T>.npz holds, per epoch k: the moments, log normaliser and grid
