@@ -36,6 +36,10 @@ namespace pln {
 
 using V = double2;
 
+#ifndef PMF_K2_TEAMS96
+#define PMF_K2_TEAMS96 48    // K2's 8-thread teams at NQ = 96 (a divisor of 96; 48 measured best)
+#endif
+
 // Phase cycle counters (debug builds with -DPMF_QPROF only): thread 0 of every CTA adds the
 // clock64() deltas of its phases; read with pmf_debug_counters (tools/qprof.py).
 __device__ unsigned long long g_qprof[16];
@@ -79,8 +83,9 @@ struct QArgs {
 // Work item = (filter, k1, k0); its plane Y[f][k1][k0][.][.] (NQ rows of NQ complex) is
 // staged row by row (bulk copies completing on one mbarrier) into rows of pitch NQ + 1
 // (conflict-free along rows and columns). Team q owns rows / columns q + TEAMS j.
-//   [split regrid, axes 3 then 2 (R12), in place]
-//   F2  forward DFT along axis 2 of every row
+//   F2  [split regrid (R12): each output row u3' bilinear from old rows ja, ja + 1 (per-item
+//       tap table) at v2 = o2 + M22 u2' + M23 u3', into registers; CTA barrier] forward DFT
+//       along axis 2 of every row
 //   F3  per column k2: forward DFT along axis 3, x s Psi / N_tot (Alg. 3-4), inverse
 //   I2  inverse DFT along axis 2 of every row, stored back in place from registers;
 //       each freed row is refilled at once with the next item's row (its bulk copy
@@ -91,7 +96,7 @@ template <int NQ> struct Q2 {
     static constexpr int PSP = NQ + 1;                       // Psi table pitch (doubles)
     static constexpr int R3 = (NQ + 31) / 32;                // k3 values per lane in the table phase
     static constexpr int QTW = 6;                            // doubles per substep in the item's table
-    static constexpr int TEAMS = NQ == 96 ? 48 : (NQ >= 64 ? 32 : NQ / 2);   // K2's teams (8 threads)
+    static constexpr int TEAMS = NQ == 96 ? PMF_K2_TEAMS96 : (NQ >= 64 ? 32 : NQ / 2);   // K2's teams (8 threads)
     static constexpr int RP = TEAMS;                         // rows per TMA part of the gathered plane
     static constexpr size_t SMEM = sizeof(V) * NQ * QCfg<NQ>::P + sizeof(double) * NQ * PSP +
                                    2 * (sizeof(double) + sizeof(int)) * NQ + sizeof(V) * NQ + 16 +
@@ -342,38 +347,55 @@ __global__ void __launch_bounds__(QCfg<NQ, TM>::NT, 1) k_q_mid(QArgs a, int I, i
         if (!skip) {
             // ------------------------------------------------------------ [split regrid] + F2
             const bool rg = flag == 4;
+            static_assert(NQ == 2 * TEAMS, "two rows per team");
             if (rg) {
-#pragma unroll 1
-                for (int j2 = q; j2 < NQ; j2 += TEAMS) {
-                    V* col = X + j2;
-                    int tt = t;
-                    asm volatile("" : "+r"(tt));              // taps re-read per column (broadcast), not hoisted
-                    V z[R];
+                // both of the team's output rows u3' (q, q + TEAMS): the bilinear value (axis 3 by the
+                // per-row taps, then axis 2 at v2 = o2 + M22 u2' + M23 u3', zero ghosts) straight
+                // into registers; every read precedes every write (CTA barrier), then the forward
+                // DFT along axis 2 continues from registers (one pass over the plane, not two)
+                const double M22 = Pc[PL_M + 10], M23 = Pc[PL_M + 11], o2 = Pc[PL_O + 2];
+                V xr[2][R];
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int u3 = q + h * TEAMS;
+                    const int2 ij = reinterpret_cast<const int2*>(j3t)[u3];
+                    const double2 w = reinterpret_cast<const double2*>(w3t)[u3];
+                    const V* ra = X + ij.x * P;
+                    const V* rb = X + ij.y * P;
+                    const double vb2 = fma(M23, (double)u3 - 0.5 * (NQ - 1), o2);
 #pragma unroll
                     for (int r = 0; r < R; ++r) {
-                        const int u3 = tt + 8 * r;
-                        const int2 ij = reinterpret_cast<const int2*>(j3t)[u3];
-                        const double2 w = reinterpret_cast<const double2*>(w3t)[u3];
-                        const V va = col[ij.x * P], vb = col[ij.y * P];
-                        z[r] = V{fma(w.y, vb.x, w.x * va.x), fma(w.y, vb.y, w.x * va.y)};
+                        const double v2 = fma(M22, (t + 8 * r) - 0.5 * (NQ - 1), vb2), fl = floor(v2);
+                        const int fi = min(max(__double2int_rz(fl), -2), NQ);
+                        const double fr = v2 - fl;
+                        const bool vl = fi >= 0 && fi < NQ, vh = fi + 1 >= 0 && fi + 1 < NQ;
+                        const V la = vl ? ra[fi] : V{0.0, 0.0}, ha = vh ? ra[fi + 1] : V{0.0, 0.0};
+                        const V lb = vl ? rb[fi] : V{0.0, 0.0}, hb = vh ? rb[fi + 1] : V{0.0, 0.0};
+                        const double ax = fma(fr, ha.x - la.x, la.x), ay = fma(fr, ha.y - la.y, la.y);
+                        const double bx = fma(fr, hb.x - lb.x, lb.x), by = fma(fr, hb.y - lb.y, lb.y);
+                        xr[h][r] = V{fma(w.y, bx, w.x * ax), fma(w.y, by, w.x * ay)};
                     }
-                    __syncwarp();
-#pragma unroll
-                    for (int r = 0; r < R; ++r) col[(t + 8 * r) * P] = z[r];
+                    dftR<R, false>(xr[h]);
+                    apply_tw<R, false>(xr[h], tw, t);
                 }
                 __syncthreads();
-            }
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    V* row = X + (q + h * TEAMS) * P;
+#pragma unroll
+                    for (int s2 = 0; s2 < R; ++s2) row[rs(s2, t)] = xr[h][s2];
+                }
+                __syncwarp();
+#pragma unroll 1
+                for (int h = 0; h < 2; ++h)
+                    tdft_s2<R>(X + (q + h * TEAMS) * P, t, rs, [](int, V* p) { reg::dft8<false>(p); });
+            } else
             {
-                const double M22 = Pc[PL_M + 10], M23 = Pc[PL_M + 11], o2 = Pc[PL_O + 2];
 #pragma unroll 1
                 for (int j3 = q; j3 < NQ; j3 += TEAMS) {
                     V x[R];
-                    if (rg) {
-                        quad_regrid_row<double, NQ>(x, X + j3 * P, j3, t, M22, M23, o2);
-                    } else {
 #pragma unroll
-                        for (int r = 0; r < R; ++r) x[r] = X[j3 * P + t + 8 * r];
-                    }
+                    for (int r = 0; r < R; ++r) x[r] = X[j3 * P + t + 8 * r];
                     // forward DFT along axis 2; the row's spectrum stays in exchange-slot order
                     // (X(k2) at slot(k2 % R, k2 / R))
                     V* row = X + j3 * P;
@@ -904,7 +926,7 @@ static cudaError_t s_map(const QArgs& qa, int N, int H, CUtensorMap* m) {
         }
     }
     const cuuint64_t n2 = qa.n2, n3 = qa.n3;
-    const cuuint32_t rp = qa.n2 == 96 ? 48 : (qa.n2 >= 64 ? 32 : (cuuint32_t)qa.n2 / 2);   // Q2<NQ>::RP
+    const cuuint32_t rp = qa.n2 == 96 ? PMF_K2_TEAMS96 : (qa.n2 >= 64 ? 32 : (cuuint32_t)qa.n2 / 2);   // Q2<NQ>::RP
     cuuint64_t dims[5] = {2, (cuuint64_t)N, (cuuint64_t)H, n2, (cuuint64_t)qa.batch * n3};
     cuuint64_t str[4] = {16, 16 * (cuuint64_t)N, 16 * (cuuint64_t)N * H, 16 * (cuuint64_t)N * H * n2};
     cuuint32_t box[5] = {2, 1, 1, (cuuint32_t)(qa.n2 + 1), rp};

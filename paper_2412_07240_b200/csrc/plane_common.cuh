@@ -356,55 +356,6 @@ __device__ __forceinline__ void quad_f2_row(V (&x)[NQ / 8], V* row, const V* tw,
     }
 }
 
-// Split regrid (R12) of the staged plane, in place, in two steps that each read only
-// the team's own column / row. Step A, column j2: Z(u3') = (1 - w3) S(ja) + w3 S(ja + 1),
-// v3 = o3 + M33 u3' (zero ghosts); all reads precede the writes (warp sync).
-template <typename T, int NQ, typename V>
-__device__ __forceinline__ void quad_regrid_col(V* col, int t, double M33, double o3) {
-    constexpr int R = NQ / 8, P = QCfg<NQ>::P;
-    V z[R];
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-        const double v3 = fma(M33, (double)(t + 8 * r) - 0.5 * (NQ - 1), o3), f3 = floor(v3);
-        const int fi3 = __double2int_rz(f3);
-        const int ja = min(max(fi3, -2), NQ);
-        const double w3 = (ja == fi3) ? v3 - f3 : 0.0;
-        double zx = 0.0, zy = 0.0;
-        if (ja >= 0 && ja < NQ) {
-            const V v = col[ja * P];
-            zx = (1.0 - w3) * (double)v.x;
-            zy = (1.0 - w3) * (double)v.y;
-        }
-        if (ja + 1 >= 0 && ja + 1 < NQ) {
-            const V v = col[(ja + 1) * P];
-            zx = fma(w3, (double)v.x, zx);
-            zy = fma(w3, (double)v.y, zy);
-        }
-        z[r] = V{(T)zx, (T)zy};
-    }
-    __syncwarp();
-#pragma unroll
-    for (int r = 0; r < R; ++r) col[(t + 8 * r) * P] = z[r];
-}
-
-// Step B, row u3': x[r] = linear interpolation of Z along j2 at v2 = o2 + M22 u2' + M23 u3'
-// (u2' = t + 8r, zero ghosts), read from the team's own row
-template <typename T, int NQ, typename V>
-__device__ __forceinline__ void quad_regrid_row(V (&x)[NQ / 8], const V* row, int u3, int t, double M22, double M23,
-                                                double o2) {
-    const double vb2 = fma(M23, (double)u3 - 0.5 * (NQ - 1), o2);
-#pragma unroll
-    for (int r = 0; r < NQ / 8; ++r) {
-        const double v2 = fma(M22, (t + 8 * r) - 0.5 * (NQ - 1), vb2), fl = floor(v2);
-        const int fi = min(max(__double2int_rz(fl), -2), NQ);
-        const double fr = v2 - fl;
-        const V lo = (fi >= 0 && fi < NQ) ? row[fi] : V{T(0), T(0)};
-        const V hi = (fi + 1 >= 0 && fi + 1 < NQ) ? row[fi + 1] : V{T(0), T(0)};
-        x[r] = V{(T)fma(fr, (double)hi.x - (double)lo.x, (double)lo.x),
-                 (T)fma(fr, (double)hi.y - (double)lo.y, (double)lo.y)};
-    }
-}
-
 // acc[r] *= product of list `list`'s Euler-factor pairs at kap_3 = kp[r]; pair j's quartic is
 // computed by thread j % 8 of the team and broadcast by shuffles (full warp, width 8)
 template <int NQ>
