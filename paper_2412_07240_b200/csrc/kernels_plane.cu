@@ -254,6 +254,29 @@ __global__ void __launch_bounds__(Cfg<N>::NT, Cfg<N>::MINB) k_plane_fwd(PlaneArg
                 i = min(max(fi, -1), N);
                 fr = (fi == i) ? v - f : 0.0;
             };
+            if (M00 >= 0.0 && M00 < 1.0) {
+                // 0 <= M00 < 1 (the new spacing below the old one: the usual case after an update):
+                // the two columns' taps lie in one 3-wide window of the staged rows i1, i1 + 1,
+                // so 6 loads serve both (the second column's pair starts 0 or 1 further)
+#pragma unroll
+                for (int r = 0; r < R1; ++r) {
+                    const double u1 = (t + 8 * r) - 0.5 * (N - 1);
+                    int i1, i0a, i0b;
+                    double a1, a0a, a0b;
+                    split(fma(M11, u1, o1), i1, a1);
+                    const double vb = fma(M01, u1, o0);
+                    split(fma(M00, (2 * m) - 0.5 * (N - 1), vb), i0a, a0a);
+                    split(fma(M00, (2 * m + 1) - 0.5 * (N - 1), vb), i0b, a0b);
+                    const T* r0 = stg + (i1 + 1) * SP + i0a + OFF;
+                    const double w0 = (double)r0[0], w1 = (double)r0[1], w2 = (double)r0[2];
+                    const double v0 = (double)r0[SP], v1 = (double)r0[SP + 1], v2 = (double)r0[SP + 2];
+                    const bool d = i0b != i0a;
+                    const double x0 = d ? w1 : w0, x1 = d ? w2 : w1, y0 = d ? v1 : v0, y1 = d ? v2 : v1;
+                    const double loa = fma(a0a, w1 - w0, w0), hia = fma(a0a, v1 - v0, v0);
+                    const double lob = fma(a0b, x1 - x0, x0), hib = fma(a0b, y1 - y0, y0);
+                    z[r] = V{(T)fma(a1, hia - loa, loa), (T)fma(a1, hib - lob, lob)};
+                }
+            } else
 #pragma unroll
             for (int r = 0; r < R1; ++r) {
                 const double u1 = (t + 8 * r) - 0.5 * (N - 1);

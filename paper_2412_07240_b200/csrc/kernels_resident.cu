@@ -516,6 +516,27 @@ __global__ void __launch_bounds__(NT, 1) k_resident_epoch(ResArgs<T> a, const __
                 const bool sw = m & 1;
                 const double b0a = sw ? b0[1] : b0[0], b0b = sw ? b0[0] : b0[1];
                 const double b1a = sw ? b1[1] : b1[0], b1b = sw ? b1[0] : b1[1];
+                if (tri && M0 >= 0.0 && M0 < 1.0) {
+                    // one row split serves both columns and 0 <= M0 < 1: their taps lie in one
+                    // 3-wide window of the staged rows i1, i1 + 1 (6 loads instead of 8)
+#pragma unroll
+                    for (int r = 0; r < 16; ++r) {
+                        int i1, i0a, i0b;
+                        double a1, a0a, a0b;
+                        split(fma((double)r, s1, b1[0]), i1, a1);
+                        split(fma((double)r, s0, b0[0]), i0a, a0a);
+                        split(fma((double)r, s0, b0[1]), i0b, a0b);
+                        const T* row0 = reinterpret_cast<const T*>(Xs + i1 * (int)StagePitch<T>::B) + i0a;
+                        const T* row1 = reinterpret_cast<const T*>(reinterpret_cast<const char*>(row0) + StagePitch<T>::B);
+                        const double w0 = (double)row0[0], w1 = (double)row0[1], w2 = (double)row0[2];
+                        const double v0 = (double)row1[0], v1 = (double)row1[1], v2 = (double)row1[2];
+                        const bool d = i0b != i0a;
+                        const double x0 = d ? w1 : w0, x1 = d ? w2 : w1, y0 = d ? v1 : v0, y1 = d ? v2 : v1;
+                        const double loa = fma(a0a, w1 - w0, w0), hia = fma(a0a, v1 - v0, v0);
+                        const double lob = fma(a0b, x1 - x0, x0), hib = fma(a0b, y1 - y0, y0);
+                        z[r] = V{(T)fma(a1, hia - loa, loa), (T)fma(a1, hib - lob, lob)};
+                    }
+                } else
 #pragma unroll
                 for (int r = 0; r < 16; ++r) {
                     T val[2];
