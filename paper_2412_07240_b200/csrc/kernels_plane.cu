@@ -121,7 +121,62 @@ __global__ void k_plane_prep(FilterState* st, double* coef, int cs, ModelParams 
 // ============================================================================ general regrid pre-pass
 // Filters whose regrid map is neither absent nor split (flag 2): multilinear
 // interpolation (R12, zero ghosts) of the old weights at every new point into W2,
-// which the forward pass then reads plainly.
+// which the forward pass then reads plainly. One warp per axis-0 row (N0 is a multiple
+// of 32 on the plane path): the row's (j1, j2, j3) split once per warp, v = v_row +
+// M[:,0] u0 per point, the 2^nx taps loaded together (zero outside the old grid) and
+// combined by nested linear interpolation, axis 0 first (2^nx - 1 lerps).
+template <typename T, int NX>
+__device__ __forceinline__ double gather_lerp(const T* __restrict__ Wf, const int* n, const int* st, const double* v) {
+    int base = 0;
+    double fr[NX];
+    bool lo[NX], hi[NX];
+#pragma unroll
+    for (int a = 0; a < NX; ++a) {
+        const double fl = floor(v[a]);
+        const int i = __double2int_rz(fl);
+        fr[a] = v[a] - fl;
+        lo[a] = i >= 0 && i <= n[a] - 1;
+        hi[a] = i >= -1 && i <= n[a] - 2;
+        base += i * st[a];
+    }
+    double w[1 << NX];
+    bool inner = true;
+#pragma unroll
+    for (int a = 0; a < NX; ++a) inner = inner && lo[a] && hi[a];
+    if (inner) {
+        // every tap inside the old grid (all but the points near its edge): one base
+        // pointer, no per-tap predicates
+        const T* pb = Wf + base;
+#pragma unroll
+        for (int c = 0; c < (1 << NX); c += 2) {
+            int off = 0;
+#pragma unroll
+            for (int a = 1; a < NX; ++a)
+                if ((c >> a) & 1) off += st[a];
+            w[c] = (double)__ldg(pb + off);
+            w[c + 1] = (double)__ldg(pb + off + 1);
+        }
+    } else {
+#pragma unroll
+        for (int c = 0; c < (1 << NX); ++c) {
+            int off = base;
+            bool ok = true;
+#pragma unroll
+            for (int a = 0; a < NX; ++a) {
+                const bool bit = (c >> a) & 1;
+                ok = ok && (bit ? hi[a] : lo[a]);
+                if (bit) off += st[a];
+            }
+            w[c] = ok ? (double)__ldg(Wf + off) : 0.0;
+        }
+    }
+#pragma unroll
+    for (int a = 0; a < NX; ++a)
+#pragma unroll
+        for (int c = 0; c < (1 << (NX - 1 - a)); ++c) w[c] = fma(fr[a], w[2 * c + 1] - w[2 * c], w[2 * c]);
+    return w[0];
+}
+
 template <typename T, int NX>
 __global__ void __launch_bounds__(256) k_plane_pre(const T* __restrict__ W, T* __restrict__ W2,
                                                    const double* __restrict__ coef, int cs, Dims d, int bpf) {
@@ -132,27 +187,36 @@ __global__ void __launch_bounds__(256) k_plane_pre(const T* __restrict__ W, T* _
     const T* Wf = W + filt * ntot;
     T* Wn = W2 + filt * ntot;
     const int nsz[4] = {d.n[0], d.n[1], d.n[2], NX == 4 ? d.n[3] : 1};
-    // 32-bit index arithmetic (ntot < 2^31 per filter): 64-bit divisions by runtime sizes
-    // dominated this pass
-    const unsigned nt = (unsigned)ntot;
-    for (unsigned pt = (unsigned)qb * blockDim.x + threadIdx.x; pt < nt; pt += (unsigned)bpf * blockDim.x) {
-        double u[4];
-        unsigned r = pt;
+    const int st[4] = {1, nsz[0], nsz[0] * nsz[1], nsz[0] * nsz[1] * nsz[2]};
+    double M0[NX], o[NX];
 #pragma unroll
-        for (int a2 = 0; a2 < NX; ++a2) {
-            const unsigned q = r / (unsigned)nsz[a2];
-            u[a2] = (double)(int)(r - q * (unsigned)nsz[a2]) - 0.5 * (nsz[a2] - 1);
-            r = q;
+    for (int a = 0; a < NX; ++a) {
+        M0[a] = P[PL_M + a * 4];
+        o[a] = P[PL_O + a];
+    }
+    const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    const int nrows = nsz[1] * nsz[2] * nsz[3], n0 = nsz[0];
+    for (int row = qb * nw + (threadIdx.x >> 5); row < nrows; row += bpf * nw) {
+        const int q1 = row / nsz[1], j1 = row - q1 * nsz[1];          // warp-uniform
+        const int j3 = q1 / nsz[2], j2 = q1 - j3 * nsz[2];
+        const double u[4] = {0.0, j1 - 0.5 * (nsz[1] - 1), j2 - 0.5 * (nsz[2] - 1), j3 - 0.5 * (nsz[3] - 1)};
+        double vr[NX];
+#pragma unroll
+        for (int a = 0; a < NX; ++a) {
+            double x = o[a];
+#pragma unroll
+            for (int b = 1; b < NX; ++b) x = fma(P[PL_M + a * 4 + b], u[b], x);
+            vr[a] = x;
         }
-        double v[4];
+        T* out = Wn + (long long)row * n0;
+#pragma unroll 4
+        for (int j0 = lane; j0 < n0; j0 += 32) {
+            const double u0 = j0 - 0.5 * (n0 - 1);
+            double v[NX];
 #pragma unroll
-        for (int a2 = 0; a2 < NX; ++a2) {
-            double x = P[PL_O + a2];
-#pragma unroll
-            for (int b2 = 0; b2 < NX; ++b2) x = fma(P[PL_M + a2 * 4 + b2], u[b2], x);
-            v[a2] = x;
+            for (int a = 0; a < NX; ++a) v[a] = fma(M0[a], u0, vr[a]);
+            out[j0] = (T)gather_lerp<T, NX>(Wf, nsz, st, v);
         }
-        Wn[pt] = (T)gather_point<T, NX>(Wf, nsz, v);
     }
 }
 
@@ -974,6 +1038,39 @@ __global__ void __launch_bounds__(Cfg<N>::NT, Cfg<N>::MINB) k_plane_inv(PlaneArg
                 Rr[1] *= Gr[1];
                 *reinterpret_cast<V*>(Wp + (long long)(t + 8 * r) * N + 2 * m) = V{o0, o1};
             }
+        } else if (a.range) {
+            // range likelihood: along the column the moved point is linear in r,
+            // y(r) = y0 + r (8 B[:,1]); coefficients held in registers (the stores to W may
+            // alias P, so per-point reads of P would be reloaded)
+            const double zr = P[PL_ZR], isg = P[PL_ISG];
+            double y0[2][NX], dy[NX];
+#pragma unroll
+            for (int a2 = 0; a2 < NX; ++a2) {
+                const double b0 = P[PL_BL + a2 * 4], b1 = P[PL_BL + a2 * 4 + 1], b2 = P[PL_BL + a2 * 4 + 2];
+                double yc = fma(b1, u10, P[PL_CL + a2]);
+                yc = fma(b2, u2, yc);
+                if (NX == 4) yc = fma(P[PL_BL + a2 * 4 + 3], u3, yc);
+                dy[a2] = 8.0 * b1;
+#pragma unroll
+                for (int e = 0; e < 2; ++e) y0[e][a2] = fma(b0, (2 * m + e) - 0.5 * (N - 1), yc);
+            }
+#pragma unroll
+            for (int r = 0; r < R1; ++r) {
+                T o[2];
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    double r2 = 0.0;
+#pragma unroll
+                    for (int a2 = 0; a2 < NX; ++a2) {
+                        const double y = fma((double)r, dy[a2], y0[e][a2]);
+                        r2 = fma(y, y, r2);
+                    }
+                    const double dd = (zr - sqrt(r2)) * isg;
+                    const double w = (double)(e == 0 ? x[r].x : x[r].y);
+                    o[e] = emit(r, e, w * exp_fast(fma(-0.5 * dd, dd, lgn)));
+                }
+                *reinterpret_cast<V*>(Wp + (long long)(t + 8 * r) * N + 2 * m) = V{o[0], o[1]};
+            }
         } else {
             const double* q = P + PL_LQ;
 #pragma unroll
@@ -1228,7 +1325,8 @@ static cudaError_t plane_t(const Dims& d, PencilBufs& b, const ModelParams& mp, 
     pa.range = lpv.kind == 1;
     // general regrid maps: gather pre-pass into W2 (exits at once for the other filters)
     if (rg) {
-        const int bpf = (int)std::max(1LL, std::min(1024LL, (d.ntot + 2047) / 2048));
+        const long long rows = d.ntot / d.n[0];                   // one warp per axis-0 row
+        const int bpf = (int)std::max(1LL, std::min(2048LL, (rows + 7) / 8));
         k_plane_pre<T, NX><<<(unsigned)(bpf * d.batch), 256, 0, s>>>((const T*)b.W, (T*)b.W2, b.coef, cs, d, bpf);
         ++*launches;
         if ((e = cudaGetLastError()) != cudaSuccess) return e;

@@ -227,44 +227,6 @@ __device__ __forceinline__ void plane_j(int pl, int n2, int& j2, int& j3) {
     j2 = pl - j3 * n2;
 }
 
-// multilinear interpolation (R12) of the old weights Wf (grid sizes n) at old index
-// coordinates v, zero ghost nodes
-template <typename T, int NX>
-__device__ __forceinline__ double gather_point(const T* __restrict__ Wf, const int* n, const double* v) {
-    int i[4];
-    double fr[4];
-    bool lo[4], hi[4];
-    int base = 0, stride[4];              // 32-bit: a filter's grid has < 2^31 points (pmf_create)
-    stride[0] = 1;
-#pragma unroll
-    for (int a = 1; a < NX; ++a) stride[a] = stride[a - 1] * n[a - 1];
-#pragma unroll
-    for (int a = 0; a < NX; ++a) {
-        const double fl = floor(v[a]);
-        i[a] = __double2int_rz(fl);
-        fr[a] = v[a] - fl;
-        lo[a] = i[a] >= 0 && i[a] <= n[a] - 1;
-        hi[a] = i[a] >= -1 && i[a] <= n[a] - 2;
-        base += i[a] * stride[a];
-    }
-    double val = 0.0;
-#pragma unroll
-    for (int c = 0; c < (1 << NX); ++c) {
-        double wt = 1.0;
-        int off = base;
-        bool ok = true;
-#pragma unroll
-        for (int a = 0; a < NX; ++a) {
-            const bool bit = (c >> a) & 1;
-            wt *= bit ? fr[a] : 1.0 - fr[a];
-            ok = ok && (bit ? hi[a] : lo[a]);
-            if (bit) off += stride[a];
-        }
-        if (ok) val = fma(wt, (double)__ldg(Wf + off), val);
-    }
-    return val;
-}
-
 // ps[r] = mult / den[r] with ONE division for all R values (prefix products, kept in ps
 // itself), every den >= 1; when the product of the R values leaves the range, one
 // division per value
