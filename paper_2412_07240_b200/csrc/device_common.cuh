@@ -299,9 +299,12 @@ __device__ __forceinline__ void block_sum(double* v, double* scratch) {
     }
     __syncthreads();
     if (lane == 0)
+#pragma unroll
         for (int i = 0; i < NV; ++i) scratch[wid * NV + i] = v[i];
     __syncthreads();
     if (threadIdx.x == 0) {
+        // unrolled: v[] stays in registers (a runtime index put it in local memory)
+#pragma unroll
         for (int i = 0; i < NV; ++i) {
             double s = 0.0;
             for (int w = 0; w < nw; ++w) s += scratch[w * NV + i];
@@ -313,7 +316,7 @@ __device__ __forceinline__ void block_sum(double* v, double* scratch) {
 
 // Finalise moments from accumulators (index coordinates u) into physical mean/cov:
 // ubar = S1/S0, S = S2/S0 - ubar ubar^T, mean = c + B ubar, cov = B S B^T (R14).
-__device__ inline void finish_moments(int nx, const double* acc, const double* c, const double* B,
+__device__ __forceinline__ void finish_moments(int nx, const double* acc, const double* c, const double* B,
                                       double* mean, double* cov) {
     double S0 = acc[0];
     double ub[4] = {0, 0, 0, 0}, Su[16];
