@@ -242,12 +242,23 @@ __device__ __forceinline__ double terrain_height(const LikParams& lp, double px,
 }
 
 // p(z | x) for z = h(x) + v, v ~ sum_g w_g N(mu_g, var_g) (eq:ex1_PDF P:413-418)
+// Loops unrolled to their maxima with runtime guards (same operations in the same order):
+// a runtime index into x[] or r[] would put the caller's arrays in local memory.
 __device__ __forceinline__ double lik_terrain_gm(const LikParams& lp, const double* x, const double* z) {
-    const double d = z[0] - terrain_height(lp, x[lp.ix], x[lp.iy]);
+    double px = x[0], py = x[0];
+#pragma unroll
+    for (int a = 1; a < 4; ++a) {
+        px = lp.ix == a ? x[a] : px;
+        py = lp.iy == a ? x[a] : py;
+    }
+    const double d = z[0] - terrain_height(lp, px, py);
     double s = 0.0;
-    for (int g = 0; g < lp.ncomp; ++g) {
-        const double e = d - lp.gm_mu[g];
-        s += exp_fast(fma(-0.5 * e * lp.gm_ivar[g], e, lp.gm_logc[g]));
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {
+        if (g < lp.ncomp) {
+            const double e = d - lp.gm_mu[g];
+            s += exp_fast(fma(-0.5 * e * lp.gm_ivar[g], e, lp.gm_logc[g]));
+        }
     }
     return s;
 }
@@ -255,21 +266,33 @@ __device__ __forceinline__ double lik_terrain_gm(const LikParams& lp, const doub
 __device__ __forceinline__ double log_lik(const LikParams& lp, const double* x, const double* z) {
     if (lp.kind == 1) {
         double r2 = 0.0;
-        for (int a = 0; a < lp.nx; ++a) r2 = fma(x[a], x[a], r2);
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+            if (a < lp.nx) r2 = fma(x[a], x[a], r2);
         double d = (z[0] - sqrt(r2)) * lp.inv_sigma;
         return fma(-0.5 * d, d, lp.lognorm);
     }
-    double r[4];
-    for (int i = 0; i < lp.nz; ++i) {
-        double hx = 0.0;
-        for (int a = 0; a < lp.nx; ++a) hx = fma(lp.H[i * 4 + a], x[a], hx);
-        r[i] = z[i] - hx;
+    double r[4] = {0, 0, 0, 0};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        if (i < lp.nz) {
+            double hx = 0.0;
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+                if (a < lp.nx) hx = fma(lp.H[i * 4 + a], x[a], hx);
+            r[i] = z[i] - hx;
+        }
     }
     double e = 0.0;
-    for (int i = 0; i < lp.nz; ++i) {
-        double t = 0.0;
-        for (int j = 0; j < lp.nz; ++j) t = fma(lp.Rinv[i * 4 + j], r[j], t);
-        e = fma(r[i], t, e);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        if (i < lp.nz) {
+            double t = 0.0;
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                if (j < lp.nz) t = fma(lp.Rinv[i * 4 + j], r[j], t);
+            e = fma(r[i], t, e);
+        }
     }
     return fma(-0.5, e, lp.lognorm);
 }

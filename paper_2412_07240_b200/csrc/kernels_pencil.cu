@@ -561,6 +561,18 @@ static int blocks_per_filter(long long ntot) {
     return (int)std::max(1LL, std::min(nb, 1024LL));
 }
 
+// blocks per filter for the grid-stride point passes: at most one wave of the device
+// (a partial second or third wave made the tail; C6: 653 blocks on 296 slots)
+template <typename K>
+static int wave_bpf(K kern, int threads, size_t smem, long long ntot, int batch) {
+    int occ = 0, dev = 0, sms = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+        sms = 148;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem) != cudaSuccess || occ < 1) occ = 1;
+    const long long per = std::max(1LL, (long long)occ * sms / std::max(1, batch));
+    return (int)std::max(1LL, std::min((long long)blocks_per_filter(ntot), per));
+}
+
 template <typename T, int MODE, int NX>   // 0: standalone update, 1: init gaussian, 2: plain sum
 __global__ void __launch_bounds__(kThreads, 2) k_points(T* __restrict__ W, const FilterState* __restrict__ st, Dims d,
                                                       DivSet dv, int nbpf, LikParams lp,
@@ -627,8 +639,11 @@ __device__ inline void block_sum_partials(const double* __restrict__ partials, l
 // MODE 0: update -> normaliser C = vol * sum, log C, scale = 1/C, moments.
 // MODE 1: renormalise (init/set_state): scale = 1/(vol * sum).
 // MODE 2: commit a regrid: new grid (R12), scale = 1/(vol' * sum).
-__device__ inline void finalize_from(FilterState& f, const double* acc, const Dims& d, int mode, double ks) {
-    const int nx = d.nx;
+// NX a compile-time constant: the small matrix loops unroll into registers (with a
+// runtime nx they ran from a 700-byte stack frame in one thread: C6's finaliser 16.8 us)
+template <int NX>
+__device__ __forceinline__ void finalize_from_t(FilterState& f, const double* acc, const Dims& d, int mode, double ks) {
+    constexpr int nx = NX;
     if (mode == 2) {
         double cn[4], Bn[16];
         bool ok = regrid_target(nx, d.ng, f, ks, cn, Bn, d.grid);
@@ -656,6 +671,15 @@ __device__ inline void finalize_from(FilterState& f, const double* acc, const Di
     } else {
         if (!(C > 0.0) || !isfinite(C)) { f.status = -6; return; }
         f.scale = 1.0 / C;
+    }
+}
+
+__device__ __forceinline__ void finalize_from(FilterState& f, const double* acc, const Dims& d, int mode, double ks) {
+    switch (d.nx) {
+        case 1: finalize_from_t<1>(f, acc, d, mode, ks); break;
+        case 2: finalize_from_t<2>(f, acc, d, mode, ks); break;
+        case 3: finalize_from_t<3>(f, acc, d, mode, ks); break;
+        default: finalize_from_t<4>(f, acc, d, mode, ks); break;
     }
 }
 
@@ -1401,7 +1425,7 @@ cudaError_t launch_predict_pencil(const Dims& d, int dtype, PencilBufs& b, const
 template <typename T, int MODE, int NX>
 static cudaError_t points_nd(const Dims& d, PencilBufs& b, const LikParams& lp, cudaStream_t s, int64_t* launches,
                              int fin_mode) {
-    int nbpf = blocks_per_filter(d.ntot);
+    const int nbpf = wave_bpf(k_points<T, MODE, NX>, kThreads, 0, d.ntot, d.batch);
     k_points<T, MODE, NX><<<(unsigned)((long long)nbpf * d.batch), kThreads, 0, s>>>(
         (T*)b.W, b.st, d, make_divs(d), nbpf, lp, b.z, b.gauss, b.partials);
     ++*launches;
@@ -1447,6 +1471,7 @@ static cudaError_t regrid_nd(const Dims& d, PencilBufs& b, double ks, cudaStream
         // row-separable path (falls back to the per-point gather inside when M is not)
         const size_t sm = sizeof(double) * 8 * (size_t)d.n[0];
         PMF_TRY(smem_attr(k_regrid_rows<T, NX>, sm));
+        nbpf = wave_bpf(k_regrid_rows<T, NX>, 128, sm, d.ntot, d.batch);
         k_regrid_rows<T, NX><<<(unsigned)((long long)nbpf * d.batch), 128, sm, s>>>(
             (const T*)b.W, (T*)b.W2, b.st, d, make_divs(d), nbpf, ks, b.partials);
     } else {
