@@ -312,7 +312,14 @@ def run_workload(args, workload, rank, world, local, secondary=False):
     # One large filter (batch 1) with N > 1 GPUs (or --virtual-ranks): its grid is split into
     # slabs along the last axis (strong scaling, all-to-all transposes). Batched filters (C5):
     # filter index sharded, 4096/N per rank (strong scaling, no data-path collective).
-    sharded = cfg.batch == 1 and cfg.nx >= 2 and (world > 1 or args.virtual_ranks > 1)
+    real_nccl = world > 1 or args.nccl_self          # --nccl-self: a 1-rank NCCL communicator at N = 1
+    sharded = cfg.batch == 1 and cfg.nx >= 2 and (real_nccl or args.virtual_ranks > 1)
+
+    def nccl_kw():
+        obj = [pmf.nccl_unique_id() if rank == 0 else None]
+        if world > 1:
+            dist.broadcast_object_list(obj, src=0)
+        return dict(world=world, rank=rank, unique_id=obj[0], sharded=True)
     T = args.warmup + 2 * args.steps + 3
     glob_batch = cfg.batch
     zs = simulate(cfg, T=T)["z"]                        # (T+1, batch, nz)
@@ -322,10 +329,8 @@ def run_workload(args, workload, rank, world, local, secondary=False):
         zs = np.ascontiguousarray(zs[:, lo:hi])
     stream = torch.cuda.Stream()
     fkw = {}
-    if sharded and world > 1:
-        obj = [pmf.nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        fkw = dict(world=world, rank=rank, unique_id=obj[0])
+    if sharded and real_nccl:
+        fkw = nccl_kw()
     elif sharded:
         fkw = dict(world=args.virtual_ranks, sharded=True)
     f, lik = make_filter(pmf, cfg, wl, args, local, stream, fkw)
@@ -436,10 +441,8 @@ def run_workload(args, workload, rank, world, local, secondary=False):
         Te = min(args.steps, 10)
         zs_e = zs[:Te + 3]
         z_pin = torch.tensor(zs_e, dtype=torch.float64).pin_memory()
-        if sharded and world > 1:
-            obj = [pmf.nccl_unique_id() if rank == 0 else None]
-            dist.broadcast_object_list(obj, src=0)
-            fkw = dict(world=world, rank=rank, unique_id=obj[0])
+        if sharded and real_nccl:
+            fkw = nccl_kw()
         fe, _ = make_filter(pmf, cfg, wl, args, local, stream, fkw)
         mean = np.empty((cfg.batch, cfg.nx))
         cov = np.empty((cfg.batch, cfg.nx, cfg.nx))
@@ -461,7 +464,7 @@ def run_workload(args, workload, rank, world, local, secondary=False):
         # them), and the step's result (moments of every filter) read back into pinned host memory
         # asynchronously on the library's stream (pmf_moments_async): no host stall between steps;
         # all reads complete inside the timed region (e1 follows them)
-        async_ok = not (sharded and world > 1) and args.virtual_ranks == 1
+        async_ok = not (sharded and real_nccl) and args.virtual_ranks == 1
         mom_pin = torch.empty(fe.moments_bytes // 8, dtype=torch.float64).pin_memory()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
@@ -543,7 +546,8 @@ def run_workload(args, workload, rank, world, local, secondary=False):
                        "grid": "eigenvector-aligned (R28)" if wl.get("grid", 0) else "axis-aligned (R12)",
                        "l2": l2txt,
                        "path": ("fdm: DST-I GEMMs on FP64 tensor cores" if wl.get("diff_mode", 0) == 2 else epoch_kernel),
-                       "parallelism": (f"slab-sharded x{world if world > 1 else args.virtual_ranks} along the last "
+                       "parallelism": (f"slab-sharded x{world if real_nccl else args.virtual_ranks}"
+                                       f"{' (NCCL)' if real_nccl else ' (virtual ranks)'} along the last "
                                        "axis (2 all-to-all per predict, all-reduce per update)" if sharded
                                        else f"filter-sharded x{world}: {cfg.batch} of {glob_batch} filters on this "
                                             "rank (no data-path collective)" if glob_batch > 1
@@ -604,6 +608,9 @@ def main():
     ap.add_argument("--no-time-update", action="store_true")
     ap.add_argument("--virtual-ranks", type=int, default=1,
                     help="split one filter into this many slabs on one GPU (exercises the sharded path)")
+    ap.add_argument("--nccl-self", action="store_true",
+                    help="N = 1 only: run the one-filter workload on the real NCCL sharded path with a "
+                         "1-rank communicator (send/recv to itself): checks the multi-process code path on one GPU")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=16.0)
     ap.add_argument("--ref-budget", type=float, default=4.0)
@@ -630,7 +637,7 @@ def main():
         also = {}
         for w in also_list.split(","):
             sub = argparse.Namespace(**{**vars(args), "steps": 20, "warmup": 3, "no_e2e": w != "C5",
-                                        "no_cpu": w != "C5", "path": 0, "virtual_ranks": 1, "cpu_budget": 8.0})
+                                        "no_cpu": w != "C5", "path": 0, "virtual_ranks": 1, "nccl_self": False, "cpu_budget": 8.0})
             r = run_workload(sub, w, rank, world, local, secondary=True)
             also[w] = {k: r[k] for k in ("value", "unit", "ms_per_step", "dtype", "steps_timing", "steps_unflushed",
                                          "roofline", "time_update", "gpu_launches", "clocks", "e2e", "cpu_baseline")}

@@ -120,3 +120,23 @@ def test_sharded_three_pass_route_is_taken(world):
     ch = max(1, min(16, int(os.environ.get("PMF_XCHUNKS", "4"))))
     c1, c2 = min(ch, cfg.n[3] // world), min(ch, cfg.n[0] // world)
     assert f.launches - l0 == (4 + c1 + c2) * world + 1, f.launches - l0
+
+
+@pytest.mark.parametrize("name", ["C4q", "C3s", "C2s"])
+def test_real_nccl_single_rank(name):
+    """The multi-process code path proper on one GPU: a real NCCL communicator of world size 1
+    (pmf_nccl_unique_id + pmf_create_sharded with unique_id != NULL). libnccl is loaded, the
+    communicator initialised, every all-to-all runs as grouped ncclSend/ncclRecv (to itself),
+    the moment sums go through ncclAllReduce and ncclCommGetAsyncError is polled after every
+    exchange -- none of which the virtual-rank contexts execute. Parity vs the oracle."""
+    cid, over, T, _ = CASES[name]
+    cfg = make_config(cid, **over)
+    zs = simulate(cfg, T=T)["z"]
+    orc = run_oracle(cfg, zs, T)
+    uid = pmf.nccl_unique_id()
+    assert len(uid) == 128 and any(uid)
+    g = run_gpu(cfg, zs, T, path=pmf.PATH_PENCIL, world=1, rank=0, unique_id=uid, sharded=True)
+    assert g["filter"].world == 1 and g["filter"].epoch_kernel == "sharded"
+    e = compare_runs(cfg, g, orc, T, TOL["f64"])
+    assert e["w"] <= 1e-10 and e["mean"] <= 1e-10 and e["cov"] <= 1e-10 and e["logC"] <= 1e-10, e
+    assert e["grid"] <= 1e-10, e
