@@ -621,6 +621,11 @@ def main():
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
+    # stdout carries exactly ONE line, the JSON: anything a library prints there during the run
+    # (NCCL's "NCCL version ..." banner goes to stdout) is sent to stderr instead
+    sys.stdout.flush()
+    json_fd = os.dup(1)
+    os.dup2(2, 1)
 
     import torch
     import torch.distributed as dist
@@ -644,7 +649,8 @@ def main():
             also[w].update(workload=r["config"]["workload"], path=r["config"]["path"], l2=r["config"]["l2"])
         line["also"] = also
     if rank == 0:
-        print(json.dumps(line), flush=True)
+        sys.stdout.flush()
+        os.write(json_fd, (json.dumps(line) + "\n").encode())
         if args.json_out:
             with open(args.json_out, "w") as fh:
                 json.dump(line, fh, indent=1)

@@ -608,7 +608,10 @@ static int sh_predict_quad(pmf_ctx* c, const LikParams* lp) {
     // chunk i's pieces leave while K1 works on chunk i + 1; K2 runs in C2 chunks of its k0
     // range and chunk i returns while K2 works on chunk i + 1. Exchanges on the stream S.xs,
     // ordered by events; K2 (K3) starts when the last piece of the first (second) exchange is in.
-    const int C1 = std::min(xchunks(), slab), C2 = std::min(xchunks(), N0c);
+    // A single rank (G = 1: a 1-rank communicator or one virtual slab) keeps K2's output in the
+    // unsharded route's k1-major order [k1][k0][j3][j2] (what K3 then reads), in which a k0
+    // sub-range is neither contiguous nor addressed per chunk: K2 runs whole, one piece back.
+    const int C1 = std::min(xchunks(), slab), C2 = G == 1 ? 1 : std::min(xchunks(), N0c);
     if (!S.xs && cudaStreamCreateWithFlags(&S.xs, cudaStreamNonBlocking) != cudaSuccess)
         return pmf_cuda_fail(c, cudaGetLastError(), "exchange stream");
     while ((int)S.ev.size() < 2 * 16 + 2) {

@@ -122,20 +122,28 @@ def test_sharded_three_pass_route_is_taken(world):
     assert f.launches - l0 == (4 + c1 + c2) * world + 1, f.launches - l0
 
 
-@pytest.mark.parametrize("name", ["C4q", "C3s", "C2s"])
-def test_real_nccl_single_rank(name):
-    """The multi-process code path proper on one GPU: a real NCCL communicator of world size 1
-    (pmf_nccl_unique_id + pmf_create_sharded with unique_id != NULL). libnccl is loaded, the
-    communicator initialised, every all-to-all runs as grouped ncclSend/ncclRecv (to itself),
-    the moment sums go through ncclAllReduce and ncclCommGetAsyncError is polled after every
-    exchange -- none of which the virtual-rank contexts execute. Parity vs the oracle."""
+@pytest.mark.parametrize("name,real", [("C4q", True), ("C4q96", True), ("C3s", True), ("C2s", True),
+                                       ("C4q", False), ("C3s", False)])
+def test_single_rank_sharded_context(name, real):
+    """real: the multi-process code path proper on one GPU -- a real NCCL communicator of world
+    size 1 (pmf_nccl_unique_id + pmf_create_sharded with unique_id != NULL). libnccl is loaded,
+    the communicator initialised, the all-to-all plans run (a rank's own piece is a device copy
+    inside the NCCL group), the moment sums go through ncclAllReduce and
+    ncclCommGetAsyncError is polled after every exchange -- none of which the virtual-rank
+    contexts execute. not real: one virtual slab. G = 1 is also the degenerate case of the
+    three-pass route: K2 keeps the unsharded k1-major output order, so it is not split into k0
+    chunks (found by this test: the chunked K2 wrote its pieces at chunk-relative offsets).
+    Parity vs the oracle."""
     cid, over, T, _ = CASES[name]
     cfg = make_config(cid, **over)
     zs = simulate(cfg, T=T)["z"]
     orc = run_oracle(cfg, zs, T)
-    uid = pmf.nccl_unique_id()
-    assert len(uid) == 128 and any(uid)
-    g = run_gpu(cfg, zs, T, path=pmf.PATH_PENCIL, world=1, rank=0, unique_id=uid, sharded=True)
+    kw = {}
+    if real:
+        uid = pmf.nccl_unique_id()
+        assert len(uid) == 128 and any(uid)
+        kw = dict(rank=0, unique_id=uid)
+    g = run_gpu(cfg, zs, T, path=pmf.PATH_PENCIL, world=1, sharded=True, **kw)
     assert g["filter"].world == 1 and g["filter"].epoch_kernel == "sharded"
     e = compare_runs(cfg, g, orc, T, TOL["f64"])
     assert e["w"] <= 1e-10 and e["mean"] <= 1e-10 and e["cov"] <= 1e-10 and e["logC"] <= 1e-10, e
