@@ -1033,12 +1033,16 @@ __global__ void __launch_bounds__(128, 4) k_regrid_rows(const T* __restrict__ Wo
 #pragma unroll
     for (int a2 = 1; a2 < NX; ++a2) stride[a2] = stride[a2 - 1] * d.n[a2 - 1];
     if (sep_sh) {
+        // chunks of CH rows interleaved over the filter's blocks: the blocks running together
+        // sweep one contiguous region of rows, so the old rows a chunk shares with its
+        // neighbours along axes 1.. (the +1 corners: N_1 and N_1 N_2 rows ahead) are still in
+        // L2 when those chunks come up. (A contiguous range per block put the concurrent
+        // blocks ~rows/blocks apart: at 96^4 every corner row came from DRAM again, 2.66 GB
+        // read for 0.68 GB of weights.)
         const long long rpf = d.ntot / N0;
-        const long long per = (rpf + nbpf - 1) / nbpf;
-        const long long rb = (long long)qb * per, re = rb + per < rpf ? rb + per : rpf;
         const float invN0 = 1.0f / N0;
-        for (long long c0 = rb; c0 < re; c0 += CH) {
-            const int nr = (int)((re - c0) < CH ? (re - c0) : CH);
+        for (long long c0 = (long long)qb * CH; c0 < rpf; c0 += (long long)nbpf * CH) {
+            const int nr = (int)((rpf - c0) < CH ? (rpf - c0) : CH);
             // per-row constants: old-row corners and weights, v0 offset
             if (threadIdx.x < nr) {
                 const int rl = threadIdx.x;
