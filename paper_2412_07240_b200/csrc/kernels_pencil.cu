@@ -988,12 +988,11 @@ __global__ void __launch_bounds__(kThreads, 2) k_regrid_gather(const T* __restri
 // linearly along axis 0 (zero ghosts at both ends). Identical to the 2^nx-tap
 // multilinear formula of R12 up to rounding order. Otherwise the kernel falls back
 // to the per-point gather (k_regrid_gather's arithmetic).
-template <typename T, int NX>
+template <typename T, int NX, int CH = 8>               // CH: new rows per chunk (shared memory CH x N0 doubles)
 __global__ void __launch_bounds__(128, 4) k_regrid_rows(const T* __restrict__ Wold, T* __restrict__ Wnew,
                                                        const FilterState* __restrict__ st, Dims d, DivSet dv,
                                                        int nbpf, double ks, double* __restrict__ partials) {
     constexpr int NC = 1 << (NX - 1);                  // old rows blended per new row
-    constexpr int CH = 8;                              // new rows per chunk
     __shared__ double red[32 * NMOM];
     __shared__ double Msh[16], osh[4];
     __shared__ int sep_sh;
@@ -1584,22 +1583,26 @@ template <typename T>
 static cudaError_t sh_regrid_t(const Dims& d, const void* src, void* dst, PencilBufs& b, double ks, double* tot,
                                cudaStream_t s, int64_t* launches) {
     int nbpf = blocks_per_filter(d.ntot);
-    const size_t sm = sizeof(double) * 8 * (size_t)d.n[0];
     const unsigned g = (unsigned)((long long)nbpf * d.batch);
-    switch (d.nx) {
-        case 2:
-            PMF_TRY(smem_attr(k_regrid_rows<T, 2>, sm));
-            k_regrid_rows<T, 2><<<g, 128, sm, s>>>((const T*)src, (T*)dst, b.st, d, make_divs(d), nbpf, ks, b.partials);
-            break;
-        case 3:
-            PMF_TRY(smem_attr(k_regrid_rows<T, 3>, sm));
-            k_regrid_rows<T, 3><<<g, 128, sm, s>>>((const T*)src, (T*)dst, b.st, d, make_divs(d), nbpf, ks, b.partials);
-            break;
-        default:
-            PMF_TRY(smem_attr(k_regrid_rows<T, 4>, sm));
-            k_regrid_rows<T, 4><<<g, 128, sm, s>>>((const T*)src, (T*)dst, b.st, d, make_divs(d), nbpf, ks, b.partials);
-            break;
+    // large slabs (many chunks per block): 32-row chunks -- the per-row setup runs on a full
+    // warp and the two barriers per chunk are amortised over 4x the points
+    const bool big = d.ntot / d.n[0] / nbpf >= 128 && d.n[0] <= 128;
+    const size_t sm = sizeof(double) * (big ? 32 : 8) * (size_t)d.n[0];
+#define PMF_RG_ROWS(NX_)                                                                                              \
+    if (big) {                                                                                                         \
+        PMF_TRY(smem_attr(k_regrid_rows<T, NX_, 32>, sm));                                                             \
+        k_regrid_rows<T, NX_, 32><<<g, 128, sm, s>>>((const T*)src, (T*)dst, b.st, d, make_divs(d), nbpf, ks,          \
+                                                     b.partials);                                                      \
+    } else {                                                                                                           \
+        PMF_TRY(smem_attr(k_regrid_rows<T, NX_>, sm));                                                                 \
+        k_regrid_rows<T, NX_><<<g, 128, sm, s>>>((const T*)src, (T*)dst, b.st, d, make_divs(d), nbpf, ks, b.partials); \
     }
+    switch (d.nx) {
+        case 2: PMF_RG_ROWS(2) break;
+        case 3: PMF_RG_ROWS(3) break;
+        default: PMF_RG_ROWS(4) break;
+    }
+#undef PMF_RG_ROWS
     ++*launches;
     PMF_TRY(cudaGetLastError());
     k_reduce_partials<<<d.batch, kThreads, 0, s>>>(b.partials, nbpf, tot);

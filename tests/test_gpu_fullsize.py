@@ -150,12 +150,16 @@ def _golden(name):
     return np.load(p)
 
 
-@pytest.mark.parametrize("cid, T", [("C3", 50), ("C4", 2)])
-def test_full_size_run_vs_oracle_fixture(cid, T):
+@pytest.mark.parametrize("cid, T, kw", [("C3", 50, {}), ("C4", 2, {}),
+                                        ("C4", 2, {"path": pmf.PATH_PENCIL, "world": 4, "sharded": True})],
+                         ids=["C3", "C4", "C4_sharded_x4"])
+def test_full_size_run_vs_oracle_fixture(cid, T, kw):
     """BASELINE C3 (128^3, all 50 epochs) and C4 (96^4 = 85 M points, epochs 0-2: epoch 2's
     predict carries the regrid off the sheared grid of epoch 1, i.e. the split map with
     M23 != 0 through K1 and K2) at full
     size, in bench.py's launch configuration (the plane path; C4 on the three-pass route),
+    (and C4 slab-sharded over 4 virtual ranks: the sharded three-pass route with its
+    pipelined exchanges and the standalone window regrid in its large-slab configuration)
     against the oracle's run of the same seeded inputs: tests/golden/<cfg>_full_T<T>.npz,
     written by tools/make_golden.py (oracle/ only). Every epoch: moments, normaliser and
     grid, and the posterior weights element by element at 8192 (C4) / 2048 (C3) seeded
@@ -164,8 +168,8 @@ def test_full_size_run_vs_oracle_fixture(cid, T):
     G = _golden(f"{cid.lower()}_full_T{T}.npz")
     cfg = make_config(cid)
     zs = simulate(cfg, T=T)["z"]
-    f = make_filter(cfg)
-    assert f.path == pmf.PATH_PLANE
+    f = make_filter(cfg, **kw)
+    assert f.world == 4 if kw else f.path == pmf.PATH_PLANE
     lik = lik_of(cfg)
     dt = cfg.tau / cfg.l
     for k in range(T + 1):
