@@ -21,6 +21,8 @@ CASES = {
     # (j3, j2)-planes of a k0 range -> all-to-all back -> K3 on the slab
     "C4q": ("C4", {"n": (32, 32, 32, 32)}, 2, (2, 4, 8)),
     "C4q96": ("C4", {"n": (96, 96, 16, 16)}, 2, (2, 4, 8)),
+    # the thinnest shards: slabs of 2 and 1 planes, k0 ranges of 2 and 1 columns (one chunk each)
+    "C4q_thin": ("C4", {"n": (32, 32, 32, 32)}, 1, (16, 32)),
     "C2s": ("C2", {"n": (32, 48)}, 4, (2, 3)),
     "C3s": ("C3", {"n": (16, 12, 24)}, 3, (2, 4)),
 }
