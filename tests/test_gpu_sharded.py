@@ -150,3 +150,21 @@ def test_single_rank_sharded_context(name, real):
     e = compare_runs(cfg, g, orc, T, TOL["f64"])
     assert e["w"] <= 1e-10 and e["mean"] <= 1e-10 and e["cov"] <= 1e-10 and e["logC"] <= 1e-10, e
     assert e["grid"] <= 1e-10, e
+
+
+@pytest.mark.parametrize("name", ["C4q", "C4s", "C3s", "C2s"])
+def test_sharded_step_api(name):
+    """pmf_step (regrid + predict + update in one call: the call bench.py times) on sharded
+    contexts -- two virtual ranks and a real 1-rank NCCL communicator -- against the unsharded
+    unfused sequence: moments and normaliser of every epoch to 1e-12."""
+    cid, over, T, _ = CASES[name]
+    cfg = make_config(cid, **over)
+    zs = simulate(cfg, T=T)["z"]
+    ref = run_gpu(cfg, zs, T, path=pmf.PATH_PENCIL)
+    for kw in ({"world": 2}, {"world": 1, "rank": 0, "unique_id": pmf.nccl_unique_id()}):
+        g = run_gpu(cfg, zs, T, path=pmf.PATH_PENCIL, use_step=True, sharded=True, **kw)
+        assert g["filter"].epoch_kernel == "sharded"
+        for k in range(T + 1):
+            assert np.max(np.abs(g["mean"][k] - ref["mean"][k])) <= 1e-12, (kw["world"], k)
+            assert rel_linf(g["cov"][k], ref["cov"][k]) <= 1e-12, (kw["world"], k)
+            assert np.max(np.abs(g["logC"][k] - ref["logC"][k])) <= 1e-12, (kw["world"], k)
