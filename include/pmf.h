@@ -218,7 +218,12 @@ int pmf_moments_async(pmf_ctx* ctx, double* dst);
  * north_star "re-centre the grid"): c' = mean, B' = diag(2 k_sigma sqrt(cov_mm)/N_m)
  * (PMF_GRID_EIGEN: the eigenvector-aligned B' of R28, see pmf_config.grid),
  * multilinear interpolation of the old weights at the new points with zero
- * ghost nodes, renormalised. Lazy. PMF_E_STATE before the first update. */
+ * ghost nodes, renormalised. Lazy. PMF_E_STATE before the first update.
+ * The mean and covariance are those of the last pmf_update (predictions do not
+ * recompute them): call it right after an update, as pmf_step does. After
+ * predictions with no update in between it re-centres on the stale posterior
+ * and can cut off mass that has drifted away (the next update may then fail
+ * with PMF_E_NO_SUPPORT). */
 int pmf_regrid(pmf_ctx* ctx, double k_sigma);
 
 /* One filter epoch = pmf_predict(dt, steps); pmf_update(z, lik); pmf_regrid(k_sigma)
